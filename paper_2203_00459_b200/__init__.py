@@ -1,0 +1,466 @@
+"""B200-native decoupled Fourier pose search (f-MbyM, arXiv 2203.00459).
+
+Python host side of the drop-in for the reference hot path
+``fscan::scan_match`` (proj/src/matcher.cpp:189-216) and its pybind11 binding
+``fscan.scan_match(f, g, delta, config)`` (proj/python/module.cpp:117-136).
+Everything computes in the sm_100a kernels of ``libfscan_b200.so`` through the
+C ABI declared in ``include/fscan_cuda.h``; this module only marshals
+pointers. There is no CPU fallback: without the library or a B200 every
+compute call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+import subprocess
+from dataclasses import dataclass, field
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+LIB_PATH = os.path.join(HERE, "libfscan_b200.so")
+
+OK, ERR_INVALID_ARGUMENT, ERR_NONFINITE, ERR_MASK_RANGE, ERR_UNSUPPORTED, ERR_CUDA, ERR_NO_DEVICE = range(7)
+_STATUS = {0: "OK", 1: "INVALID_ARGUMENT", 2: "NONFINITE", 3: "MASK_RANGE", 4: "UNSUPPORTED",
+           5: "CUDA", 6: "NO_DEVICE"}
+
+
+class FscanError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"[{_STATUS.get(status, status)}] {msg}")
+        self.status = status
+
+
+class FscanInvalidArgument(FscanError, ValueError):
+    """std::invalid_argument of the reference (bad config, NaN/Inf, mask range)."""
+
+
+def _raise(status: int, msg: str):
+    if status in (ERR_INVALID_ARGUMENT, ERR_NONFINITE, ERR_MASK_RANGE):
+        raise FscanInvalidArgument(status, msg)
+    raise FscanError(status, msg)
+
+
+class CConfig(C.Structure):
+    _fields_ = [
+        ("n_theta", C.c_int32), ("delta_theta", C.c_double), ("t_theta", C.c_double),
+        ("n_xy", C.c_int32), ("delta_xy", C.c_double), ("t_xy", C.c_double),
+        ("band_lo", C.c_double), ("band_hi", C.c_double),
+        ("n_radius", C.c_int32), ("pad_angle", C.c_int32),
+        ("softargmax_window", C.c_int32), ("normalize_scores", C.c_int32),
+    ]
+
+
+class CPairResult(C.Structure):
+    _fields_ = [
+        ("theta", C.c_double), ("tx", C.c_double), ("ty", C.c_double),
+        ("theta_hard", C.c_double), ("theta_peak", C.c_double),
+        ("xy_hard_x", C.c_double), ("xy_hard_y", C.c_double), ("xy_peak", C.c_double),
+        ("theta_bin", C.c_int32), ("xy_row", C.c_int32), ("xy_col", C.c_int32), ("status", C.c_int32),
+    ]
+
+
+RESULT_DTYPE = np.dtype([
+    ("theta", "f8"), ("tx", "f8"), ("ty", "f8"), ("theta_hard", "f8"), ("theta_peak", "f8"),
+    ("xy_hard_x", "f8"), ("xy_hard_y", "f8"), ("xy_peak", "f8"),
+    ("theta_bin", "i4"), ("xy_row", "i4"), ("xy_col", "i4"), ("status", "i4")])
+assert RESULT_DTYPE.itemsize == C.sizeof(CPairResult)
+
+
+class CSynthSpec(C.Structure):
+    _fields_ = [
+        ("polar", C.c_int), ("n", C.c_int), ("delta", C.c_double),
+        ("n_reflectors", C.c_int), ("n_segments", C.c_int),
+        ("sigma_lo_px", C.c_double), ("sigma_hi_px", C.c_double), ("seg_sigma_px", C.c_double),
+        ("extent_frac", C.c_double), ("theta_max", C.c_double), ("t_max", C.c_double),
+        ("speckle", C.c_double), ("masks", C.c_int), ("mask_sigma", C.c_double),
+        ("n_az", C.c_int), ("n_range", C.c_int), ("range_res", C.c_double), ("att_r0", C.c_double),
+        ("seed", C.c_uint64),
+    ]
+
+
+def build(force: bool = False) -> str:
+    """Compile libfscan_b200.so for sm_100a (nvcc cross-compiles without a GPU)."""
+    cmd = ["make", "-s", "-C", os.path.join(HERE, "csrc")]
+    if force:
+        subprocess.run(cmd + ["clean"], check=True)
+    subprocess.run(cmd + ["-j8"], check=True)
+    return LIB_PATH
+
+
+_lib: C.CDLL | None = None
+
+_P = C.c_void_p
+SYMBOLS = {
+    # name: (restype, argtypes)
+    "fscan_config_defaults": (None, [C.POINTER(CConfig)]),
+    "fscan_config_finalize": (None, [C.POINTER(CConfig)]),
+    "fscan_config_validate": (C.c_int, [C.POINTER(CConfig), C.c_char_p, C.c_size_t]),
+    "fscan_ctx_create": (C.c_int, [C.c_int, C.POINTER(CConfig), C.c_int, C.POINTER(_P)]),
+    "fscan_ctx_destroy": (None, [_P]),
+    "fscan_ctx_last_error": (C.c_char_p, [_P]),
+    "fscan_ctx_n": (C.c_int, [_P]),
+    "fscan_ctx_set_chunk": (C.c_int, [_P, C.c_int]),
+    "fscan_match_batch": (C.c_int, [_P, _P, _P, _P, _P, C.c_int, C.c_double, _P, _P, _P, _P]),
+    "fscan_match_batch_host": (C.c_int, [_P, _P, _P, _P, _P, C.c_int, C.c_double, _P, _P, _P]),
+    "fscan_estimate_rotation_batch": (C.c_int, [_P, _P, _P, C.c_int, _P, _P, _P]),
+    "fscan_estimate_translation_batch": (C.c_int, [_P, _P, _P, C.c_int, C.c_double, _P, _P, _P, _P]),
+    "fscan_band_magnitude_batch": (C.c_int, [_P, _P, C.c_int, _P, _P]),
+    "fscan_polar_to_cart_batch": (C.c_int, [_P, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int,
+                                            C.c_double, _P, _P]),
+    "fscan_check_results": (C.c_int, [_P, C.c_int, _P, C.POINTER(C.c_int)]),
+    "fscan_ctx_launches_last": (C.c_int, [_P]),
+    "fscan_synth_preset": (C.c_int, [C.c_int, C.POINTER(CSynthSpec)]),
+    "fscan_synth_pairs_host": (C.c_int, [C.POINTER(CSynthSpec), C.c_int, C.c_int, _P, _P, _P, _P, _P,
+                                         C.c_int]),
+    "fscan_synth_polar_host": (C.c_int, [C.POINTER(CSynthSpec), C.c_int, C.c_int, _P, _P, _P, C.c_int]),
+    "fscan_synth_pairs_device": (C.c_int, [C.POINTER(CSynthSpec), C.c_int, C.c_int, _P, _P, _P, _P, _P,
+                                           _P]),
+    "fscan_synth_polar_device": (C.c_int, [C.POINTER(CSynthSpec), C.c_int, C.c_int, _P, _P, _P, _P]),
+}
+
+
+def lib() -> C.CDLL:
+    """Load (building if needed) the native library. Raises if it cannot."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        build()
+    L = C.CDLL(LIB_PATH)
+    for name, (res, args) in SYMBOLS.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = L
+    return L
+
+
+# ---------------------------------------------------------------- config
+
+@dataclass
+class MatchConfig:
+    """fscan::MatchConfig (matcher.hpp:13-26) with the reference defaults."""
+    n_theta: int = 733
+    delta_theta: float = math.pi / 733.0
+    t_theta: float = 2.0
+    n_xy: int = 255
+    delta_xy: float = 0.4
+    t_xy: float = 1.0
+    band_lo: float = 0.03
+    band_hi: float = 0.75
+    n_radius: int = 128
+    pad_angle: int = 92
+    softargmax_window: int = 16
+    normalize_scores: bool = True
+
+    def to_c(self) -> CConfig:
+        return CConfig(int(self.n_theta), float(self.delta_theta), float(self.t_theta), int(self.n_xy),
+                       float(self.delta_xy), float(self.t_xy), float(self.band_lo), float(self.band_hi),
+                       int(self.n_radius), int(self.pad_angle), int(self.softargmax_window),
+                       int(bool(self.normalize_scores)))
+
+    def finalize(self) -> "MatchConfig":
+        """matcher.cpp:11-15, in place; returns self."""
+        c = self.to_c()
+        lib().fscan_config_finalize(C.byref(c))
+        self.n_radius, self.pad_angle = c.n_radius, c.pad_angle
+        return self
+
+    def validate(self) -> None:
+        """matcher.cpp:17-37 (odd-n rule excepted)."""
+        c = self.to_c()
+        buf = C.create_string_buffer(256)
+        st = lib().fscan_config_validate(C.byref(c), buf, 256)
+        if st:
+            _raise(st, buf.value.decode())
+
+    @staticmethod
+    def for_grid(n: int, delta: float, n_theta: int, **kw) -> "MatchConfig":
+        """BASELINE-style config: delta_theta = pi/n_theta, sentinels resolved."""
+        cfg = MatchConfig(n_theta=n_theta, delta_theta=math.pi / n_theta, n_xy=n, delta_xy=delta,
+                          n_radius=0, pad_angle=-1, **kw)
+        return cfg.finalize()
+
+
+# BASELINE.json configs 1..5
+def baseline_config(cid: int) -> tuple[MatchConfig, float, int]:
+    """(config, grid delta in metres, batch) for BASELINE config 1..5."""
+    if cid in (1, 2):
+        t = 1.0 if cid == 2 else None
+        cfg = MatchConfig.for_grid(256, 0.5, 360)
+        if t is not None:
+            cfg.t_theta = cfg.t_xy = t
+        return cfg, 0.5, (1 if cid == 1 else 64)
+    if cid in (3, 4):
+        cfg = MatchConfig.for_grid(512, 0.25, 720, t_theta=1.0, t_xy=1.0)
+        return cfg, 0.25, (64 if cid == 3 else 4096)
+    if cid == 5:
+        cfg = MatchConfig.for_grid(1024, 0.125, 1440, t_theta=0.5, t_xy=0.5)
+        return cfg, 0.125, 1024
+    raise ValueError(cid)
+
+
+# ---------------------------------------------------------------- matcher
+
+def _ptr(t) -> int | None:
+    """Device pointer of a CUDA torch tensor (or None)."""
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("expected a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError("expected a contiguous tensor")
+    return t.data_ptr()
+
+
+def _stream_ptr(stream) -> int | None:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+class Matcher:
+    """One device context: a finalized config, tables, workspace and streams."""
+
+    def __init__(self, cfg: MatchConfig, max_batch: int, device: int = 0, chunk: int = 0):
+        self.cfg = cfg
+        self.device = device
+        self.max_batch = max_batch
+        h = C.c_void_p()
+        c = cfg.to_c()
+        st = lib().fscan_ctx_create(device, C.byref(c), max_batch, C.byref(h))
+        self._h = h
+        if st != OK:
+            msg = lib().fscan_ctx_last_error(h).decode() if h.value else ""
+            self.close()
+            _raise(st, f"fscan_ctx_create: {msg}")
+        self.n = lib().fscan_ctx_n(h)
+        if chunk:
+            self.set_chunk(chunk)
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib().fscan_ctx_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, st: int, what: str):
+        if st != OK:
+            _raise(st, f"{what}: {lib().fscan_ctx_last_error(self._h).decode()}")
+
+    def set_chunk(self, pairs: int):
+        self._check(lib().fscan_ctx_set_chunk(self._h, int(pairs)), "set_chunk")
+
+    @property
+    def launches_last(self) -> int:
+        return lib().fscan_ctx_launches_last(self._h)
+
+    def match_device(self, f, g, mf=None, mg=None, *, delta: float, out=None, theta_surface=None,
+                     xy_surface=None, stream=None):
+        """Asynchronous batched scan_match on CUDA tensors [B, N, N] float32.
+
+        ``out`` is a uint8 CUDA tensor of B * sizeof(result) bytes (allocated if
+        None) and is returned; decode with :func:`decode_results` after sync.
+        """
+        import torch
+        b = int(f.shape[0])
+        if out is None:
+            out = torch.empty(b * RESULT_DTYPE.itemsize, dtype=torch.uint8, device=f.device)
+        st = lib().fscan_match_batch(self._h, _ptr(f), _ptr(g), _ptr(mf), _ptr(mg), b, float(delta),
+                                     _ptr(out), _ptr(theta_surface), _ptr(xy_surface), _stream_ptr(stream))
+        self._check(st, "fscan_match_batch")
+        return out
+
+    def match_host(self, f: np.ndarray, g: np.ndarray, mf=None, mg=None, *, delta: float,
+                   surfaces: bool = False):
+        """Synchronous batched scan_match on host float32 arrays [B, N, N]."""
+        f = np.ascontiguousarray(f, dtype=np.float32)
+        g = np.ascontiguousarray(g, dtype=np.float32)
+        if f.ndim == 2:
+            f, g = f[None], g[None]
+            mf = None if mf is None else np.ascontiguousarray(mf, dtype=np.float32)[None]
+            mg = None if mg is None else np.ascontiguousarray(mg, dtype=np.float32)[None]
+        mf = None if mf is None else np.ascontiguousarray(mf, dtype=np.float32)
+        mg = None if mg is None else np.ascontiguousarray(mg, dtype=np.float32)
+        b, n = f.shape[0], f.shape[1]
+        res = np.zeros(b, dtype=RESULT_DTYPE)
+        ts = np.zeros((b, max(1, self.cfg.n_theta)), dtype=np.float64) if surfaces else None
+        xs = np.zeros((b, n, n), dtype=np.float32) if surfaces else None
+        p = lambda a: None if a is None else a.ctypes.data  # noqa: E731
+        st = lib().fscan_match_batch_host(self._h, p(f), p(g), p(mf), p(mg), b, float(delta), p(res), p(ts),
+                                          p(xs))
+        self._check(st, "fscan_match_batch_host")
+        return (res, ts, xs) if surfaces else res
+
+    def estimate_rotation(self, f, g, *, theta=None, theta_surface=None, stream=None):
+        import torch
+        b = int(f.shape[0])
+        if theta is None:
+            theta = torch.empty(b, dtype=torch.float64, device=f.device)
+        st = lib().fscan_estimate_rotation_batch(self._h, _ptr(f), _ptr(g), b, _ptr(theta), _ptr(theta_surface),
+                                                 _stream_ptr(stream))
+        self._check(st, "fscan_estimate_rotation_batch")
+        return theta
+
+    def estimate_translation(self, f, g, theta, *, delta: float, xy_surface=None, stream=None):
+        import torch
+        b = int(f.shape[0])
+        txy = torch.empty((b, 2), dtype=torch.float64, device=f.device)
+        st = lib().fscan_estimate_translation_batch(self._h, _ptr(f), _ptr(g), b, float(delta), _ptr(theta),
+                                                    _ptr(txy), _ptr(xy_surface), _stream_ptr(stream))
+        self._check(st, "fscan_estimate_translation_batch")
+        return txy
+
+    def band_magnitude(self, img, *, stream=None):
+        import torch
+        b, n = int(img.shape[0]), int(img.shape[1])
+        out = torch.empty((b, n, n // 2), dtype=torch.float32, device=img.device)
+        st = lib().fscan_band_magnitude_batch(self._h, _ptr(img), b, _ptr(out), _stream_ptr(stream))
+        self._check(st, "fscan_band_magnitude_batch")
+        return out
+
+
+def decode_results(buf) -> np.ndarray:
+    """uint8 tensor/array of results -> numpy structured array (RESULT_DTYPE)."""
+    a = buf.cpu().numpy() if hasattr(buf, "cpu") else np.asarray(buf)
+    return np.frombuffer(a.tobytes(), dtype=RESULT_DTYPE).copy()
+
+
+def polar_to_cart(polar, *, range_res: float, n: int, delta: float, stream=None):
+    """K0 on CUDA tensors: [B, n_az, n_range] -> [B, n, n] float32."""
+    import torch
+    b, n_az, n_range = (int(x) for x in polar.shape)
+    out = torch.empty((b, n, n), dtype=torch.float32, device=polar.device)
+    st = lib().fscan_polar_to_cart_batch(_ptr(polar), b, n_az, n_range, float(range_res), int(n), float(delta),
+                                         _ptr(out), _stream_ptr(stream))
+    if st != OK:
+        _raise(st, "fscan_polar_to_cart_batch")
+    return out
+
+
+# ---------------------------------------------------------------- reference-style single-pair API
+
+@dataclass
+class Pose2D:
+    theta: float = 0.0
+    tx: float = 0.0
+    ty: float = 0.0
+
+
+@dataclass
+class MatchResult:
+    """Mirror of the pybind11 MatchResult (module.cpp:98-115)."""
+    pose: Pose2D
+    theta_scores: np.ndarray = field(repr=False)
+    theta_coords: np.ndarray = field(repr=False)
+    xy_scores: np.ndarray = field(repr=False)
+    raw: np.void = field(repr=False, default=None)
+
+
+_ctx_cache: dict = {}
+
+
+def scan_match(f, g, delta: float, config: MatchConfig | None = None, mask_f=None, mask_g=None) -> MatchResult:
+    """fscan.scan_match(f, g, delta, config) of proj/python/module.cpp:117-136.
+
+    f, g: N x N arrays (any float dtype; converted to float32 for the GPU).
+    Without a config, the stock config with the grid geometry swapped in.
+    """
+    f = np.asarray(f)
+    n = int(f.shape[0])
+    if config is None:
+        config = MatchConfig(n_xy=n, delta_xy=delta, n_radius=0)
+    cfg = MatchConfig(**config.__dict__).finalize()
+    cfg.validate()
+    if n != cfg.n_xy:
+        _raise(ERR_INVALID_ARGUMENT, "estimate_rotation: grid size != config n_xy")
+    key = (tuple(cfg.__dict__.items()),)
+    m = _ctx_cache.get(key)
+    if m is None:
+        m = _ctx_cache[key] = Matcher(cfg, max_batch=1)
+    res, ts, xs = m.match_host(f, g, mask_f, mask_g, delta=delta, surfaces=True)
+    r = res[0]
+    coords = np.array([(k - cfg.n_theta // 2) * cfg.delta_theta for k in range(cfg.n_theta)]) \
+        if cfg.n_theta > 1 else np.zeros(1)
+    return MatchResult(Pose2D(float(r["theta"]), float(r["tx"]), float(r["ty"])), ts[0][:, None], coords,
+                       xs[0].astype(np.float64), r)
+
+
+# ---------------------------------------------------------------- synthetic inputs
+
+def synth_spec(config_id: int, **overrides) -> CSynthSpec:
+    s = CSynthSpec()
+    if lib().fscan_synth_preset(int(config_id), C.byref(s)) != 0:
+        raise ValueError(f"unknown config {config_id}")
+    for k, v in overrides.items():
+        setattr(s, k, v)
+    return s
+
+
+def synth_pairs_host(spec: CSynthSpec, first: int, count: int, threads: int = 0):
+    """(f, g, mf, mg, truth) float32 [count, N, N] (+ float64 [count, 3]) on the host."""
+    n = spec.n
+    f = np.empty((count, n, n), np.float32)
+    g = np.empty_like(f)
+    mf = np.empty_like(f)
+    mg = np.empty_like(f)
+    truth = np.empty((count, 3), np.float64)
+    st = lib().fscan_synth_pairs_host(C.byref(spec), first, count, f.ctypes.data, g.ctypes.data, mf.ctypes.data,
+                                      mg.ctypes.data, truth.ctypes.data, threads)
+    if st:
+        raise RuntimeError(f"fscan_synth_pairs_host failed ({st})")
+    return f, g, mf, mg, truth
+
+
+def synth_polar_host(spec: CSynthSpec, first: int, count: int, threads: int = 0):
+    pf = np.empty((count, spec.n_az, spec.n_range), np.float32)
+    pg = np.empty_like(pf)
+    truth = np.empty((count, 3), np.float64)
+    st = lib().fscan_synth_polar_host(C.byref(spec), first, count, pf.ctypes.data, pg.ctypes.data,
+                                      truth.ctypes.data, threads)
+    if st:
+        raise RuntimeError(f"fscan_synth_polar_host failed ({st})")
+    return pf, pg, truth
+
+
+def synth_pairs_device(spec: CSynthSpec, first: int, count: int, device: int = 0):
+    """Device-rendered pairs as CUDA tensors (f, g, mf, mg) and host truth."""
+    import torch
+    n = spec.n
+    dev = torch.device("cuda", device)
+    f = torch.empty((count, n, n), dtype=torch.float32, device=dev)
+    g = torch.empty_like(f)
+    mf = torch.empty_like(f)
+    mg = torch.empty_like(f)
+    truth = np.empty((count, 3), np.float64)
+    torch.cuda.synchronize(dev)
+    st = lib().fscan_synth_pairs_device(C.byref(spec), first, count, f.data_ptr(), g.data_ptr(), mf.data_ptr(),
+                                        mg.data_ptr(), truth.ctypes.data, torch.cuda.current_stream(dev).cuda_stream)
+    if st:
+        raise RuntimeError(f"fscan_synth_pairs_device failed ({st})")
+    torch.cuda.synchronize(dev)
+    return f, g, mf, mg, truth
+
+
+def synth_polar_device(spec: CSynthSpec, first: int, count: int, device: int = 0):
+    import torch
+    dev = torch.device("cuda", device)
+    pf = torch.empty((count, spec.n_az, spec.n_range), dtype=torch.float32, device=dev)
+    pg = torch.empty_like(pf)
+    truth = np.empty((count, 3), np.float64)
+    torch.cuda.synchronize(dev)
+    st = lib().fscan_synth_polar_device(C.byref(spec), first, count, pf.data_ptr(), pg.data_ptr(),
+                                        truth.ctypes.data, torch.cuda.current_stream(dev).cuda_stream)
+    if st:
+        raise RuntimeError(f"fscan_synth_polar_device failed ({st})")
+    torch.cuda.synchronize(dev)
+    return pf, pg, truth

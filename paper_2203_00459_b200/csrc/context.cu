@@ -1,0 +1,660 @@
+// context.cu — runtime behind include/fscan_cuda.h: config handling, per-config
+// tables (twiddles, Hann window, band intervals, cart2pol taps), workspace
+// arena, streams, and the chunked batch pipeline K1a..K6 (kernels.cu).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "fscan_cuda.h"
+#include "pipeline.h"
+
+using namespace fscan_detail;
+
+namespace {
+
+constexpr double kPi = 3.141592653589793;  // std::numbers::pi (geometry.hpp:11)
+constexpr int kLanes = 2;                  // concurrent chunk pipelines
+
+struct Lane {
+    cudaStream_t stream = nullptr;
+    cudaEvent_t done = nullptr;
+    // workspace for `chunk` pairs
+    float* ft = nullptr;
+    float* gt = nullptr;
+    float2* zbuf = nullptr;
+    float* mag = nullptr;
+    float4* fgt = nullptr;
+    Partial* part = nullptr;
+    RotState* rot = nullptr;
+    int* flags = nullptr;
+    // host-API staging
+    float* in = nullptr;  // 4 grids x chunk
+    fscan_pair_result* res = nullptr;
+    double* tsurf = nullptr;
+    float* xsurf = nullptr;
+};
+
+}  // namespace
+
+struct fscan_ctx {
+    int device = 0;
+    fscan_config cfg{};
+    int n = 0;
+    int max_batch = 0;
+    int chunk = 0;       // pairs per pipeline chunk
+    int alloc_chunk = 0; // workspace capacity (pairs)
+    int n_live = 0;
+    int launches_last = 0;
+    std::string err;
+    std::mutex mu;
+    // tables
+    float2* tw_n = nullptr;
+    float2* tw_2n = nullptr;
+    float* hann = nullptr;
+    int2* band = nullptr;
+    PolarTap* taps = nullptr;
+    Lane lanes[kLanes];
+    cudaEvent_t start_ev = nullptr;
+};
+
+namespace {
+
+fscan_status fail(fscan_ctx* ctx, fscan_status st, const std::string& msg) {
+    if (ctx) ctx->err = msg;
+    return st;
+}
+
+fscan_status cuda_fail(fscan_ctx* ctx, cudaError_t e, const char* where) {
+    return fail(ctx, FSCAN_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(call)                                               \
+    do {                                                       \
+        cudaError_t e_ = (call);                               \
+        if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #call); \
+    } while (0)
+
+bool is_pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
+
+// bandpass_mask (imageops.cpp:44-59) restricted to the u >= 0 half plane:
+// per centred row, the interval of u in [0, n/2) inside the band.
+bool build_band(int n, double lo, double hi, std::vector<int2>& out, std::vector<unsigned char>& inband) {
+    const int c = n / 2;
+    const double nyq = n / 2.0;
+    out.assign(n, make_int2(1, 0));
+    inband.assign((size_t)n * (n / 2), 0);
+    for (int i = 0; i < n; ++i) {
+        int first = -1, last = -2;
+        for (int u = 0; u < n / 2; ++u) {
+            const int j = c + u;
+            const double rho = std::hypot(double(i - c), double(j - c)) / nyq;
+            const bool in = (rho >= lo && rho <= hi);
+            inband[(size_t)i * (n / 2) + u] = in;
+            if (in) {
+                if (first < 0) first = u;
+                else if (last != u - 1) return false;  // not an interval
+                last = u;
+            }
+        }
+        if (first >= 0) out[i] = make_int2(first, last);
+    }
+    return true;
+}
+
+// cart2pol taps (imageops.cpp:81-99 through sample_bilinear 10-26), exact
+// fp64 coordinates; entries whose four taps all sit outside the band (or the
+// array) contribute exactly 0 and are dropped by trimming the radius range.
+bool build_taps(int n, const fscan_config& cfg, const std::vector<unsigned char>& inband,
+                std::vector<PolarTap>& taps, int* n_live, std::string* why) {
+    const int nt = cfg.n_theta, nr = cfg.n_radius;
+    const double span = nt * cfg.delta_theta;
+    const int c = n / 2;
+    const double r_max = n / 2.0;
+    const int W = n / 2;
+    std::vector<PolarTap> all((size_t)nt * nr);
+    int jlo = nr, jhi = -1;
+    for (int i = 0; i < nt; ++i) {
+        const double phi = -span / 2.0 + span * i / nt;
+        const double cp = std::cos(phi), sp = std::sin(phi);
+        for (int j = 0; j < nr; ++j) {
+            const double r = r_max * (j + 1) / nr;
+            const double row = c - r * sp, col = c + r * cp;
+            const double r0f = std::floor(row), c0f = std::floor(col);
+            const long r0 = (long)r0f, c0 = (long)c0f;
+            const long u0 = c0 - c;
+            int flags = 0, live = 0;
+            for (int tp = 0; tp < 4; ++tp) {
+                const long rr = r0 + (tp >> 1), uu = u0 + (tp & 1);
+                const long cc = c + uu;
+                const bool in_ref = rr >= 0 && rr < n && cc >= 0 && cc < n;  // reference array bounds
+                if (!in_ref) continue;
+                if (uu < 0) {
+                    // tap on the u < 0 half plane; never happens for spans <= pi
+                    if (uu >= -W) {
+                        *why = "cart2pol tap on the u<0 half plane (span > pi?)";
+                        return false;
+                    }
+                    continue;
+                }
+                if (uu >= W) continue;  // column n: outside the reference array
+                const int bit = (tp == 0) ? 1 : (tp == 1) ? 2 : (tp == 2) ? 4 : 8;
+                flags |= bit;
+                if (inband[(size_t)rr * W + uu]) live = 1;
+            }
+            PolarTap& e = all[(size_t)i * nr + j];
+            e.packed = (int)(r0 & 0xFFF) | (int)((u0 & 0xFFF) << 12) | (flags << 24);
+            e.fr = (float)(row - r0f);
+            e.fc = (float)(col - c0f);
+            e.pad_ = 0.f;
+            if (r0 < 0 || r0 > n || u0 < 0 || u0 > W) {
+                if (flags) {
+                    *why = "cart2pol tap out of table range";
+                    return false;
+                }
+            }
+            if (live) {
+                jlo = std::min(jlo, j);
+                jhi = std::max(jhi, j);
+            }
+        }
+    }
+    if (jhi < jlo) {  // nothing in band: keep one (all-zero) column
+        jlo = 0;
+        jhi = 0;
+    }
+    *n_live = jhi - jlo + 1;
+    taps.resize((size_t)nt * (*n_live));
+    for (int i = 0; i < nt; ++i)
+        for (int j = jlo; j <= jhi; ++j) taps[(size_t)i * (*n_live) + (j - jlo)] = all[(size_t)i * nr + j];
+    return true;
+}
+
+void free_lane(Lane& l) {
+    cudaFree(l.ft);
+    cudaFree(l.gt);
+    cudaFree(l.zbuf);
+    cudaFree(l.mag);
+    cudaFree(l.fgt);
+    cudaFree(l.part);
+    cudaFree(l.rot);
+    cudaFree(l.flags);
+    cudaFree(l.in);
+    cudaFree(l.res);
+    cudaFree(l.tsurf);
+    cudaFree(l.xsurf);
+    l = Lane{l.stream, l.done};
+}
+
+fscan_status alloc_lane(fscan_ctx* ctx, Lane& l, int chunk) {
+    const size_t n = (size_t)ctx->n, nn = n * n;
+    const int nparts = ctx->n / rows_per_block_out(ctx->n);
+    CK(cudaMalloc(&l.ft, nn * sizeof(float) * chunk));
+    CK(cudaMalloc(&l.gt, nn * sizeof(float) * chunk));
+    CK(cudaMalloc(&l.zbuf, n * (n + 1) * sizeof(float2) * chunk));
+    CK(cudaMalloc(&l.mag, nn * sizeof(float) * chunk));
+    CK(cudaMalloc(&l.fgt, (n + 1) * n * sizeof(float4) * chunk));
+    CK(cudaMalloc(&l.part, sizeof(Partial) * nparts * chunk));
+    CK(cudaMalloc(&l.rot, sizeof(RotState) * chunk));
+    CK(cudaMalloc(&l.flags, sizeof(int) * chunk));
+    return FSCAN_OK;
+}
+
+fscan_status alloc_host_staging(fscan_ctx* ctx, Lane& l, int chunk) {
+    if (l.in) return FSCAN_OK;
+    const size_t nn = (size_t)ctx->n * ctx->n;
+    CK(cudaMalloc(&l.in, 4 * nn * sizeof(float) * chunk));
+    CK(cudaMalloc(&l.res, sizeof(fscan_pair_result) * chunk));
+    CK(cudaMalloc(&l.tsurf, sizeof(double) * std::max(1, ctx->cfg.n_theta) * chunk));
+    CK(cudaMalloc(&l.xsurf, nn * sizeof(float) * chunk));
+    return FSCAN_OK;
+}
+
+Params base_params(fscan_ctx* ctx, Lane& l, int batch, double delta) {
+    Params p{};
+    p.n = ctx->n;
+    p.batch = batch;
+    p.ft = l.ft;
+    p.gt = l.gt;
+    p.zbuf = l.zbuf;
+    p.mag = l.mag;
+    p.fgt = l.fgt;
+    p.surf = l.mag;  // the magnitude planes are dead once K2 has run
+    p.part = l.part;
+    p.rot = l.rot;
+    p.flags = l.flags;
+    p.tw_n = ctx->tw_n;
+    p.tw_2n = ctx->tw_2n;
+    p.hann = ctx->hann;
+    p.band = ctx->band;
+    p.taps = ctx->taps;
+    p.n_live = ctx->n_live;
+    p.n_theta = ctx->cfg.n_theta;
+    p.pad = ctx->cfg.pad_angle;
+    p.L = ctx->cfg.n_theta + 2 * ctx->cfg.pad_angle;
+    p.C = ctx->cfg.n_radius + 2 * ctx->cfg.pad_angle;
+    p.delta_theta = ctx->cfg.delta_theta;
+    p.t_theta = ctx->cfg.t_theta;
+    p.t_xy = ctx->cfg.t_xy;
+    p.delta = delta;
+    p.window = ctx->cfg.softargmax_window;
+    p.normalize = ctx->cfg.normalize_scores != 0;
+    return p;
+}
+
+enum class Stages { Full, Rotation, Translation, Magnitude };
+
+// Launch the pipeline for one chunk on lane l. Inputs are device pointers.
+fscan_status run_chunk(fscan_ctx* ctx, Lane& l, Params p, Stages what, int* launches) {
+    cudaStream_t s = l.stream;
+    CK(cudaMemsetAsync(l.flags, 0, sizeof(int) * p.batch, s));
+    int k = 0;
+    CK(launch_rot_rows(p, s));
+    ++k;
+    if (what == Stages::Magnitude) {
+        CK(launch_rot_cols(p, s));
+        CK(launch_mag_unpack(p, s));
+        *launches += k + 2;
+        return FSCAN_OK;
+    }
+    if (what != Stages::Translation) {
+        if (ctx->cfg.n_theta > 1) {
+            CK(launch_rot_cols(p, s));
+            ++k;
+        }
+        CK(launch_rot_polar(p, s));
+        ++k;
+    } else {
+        CK(launch_theta_in(p, s));
+        ++k;
+    }
+    if (what != Stages::Rotation) {
+        CK(launch_xlat_rows(p, s));
+        CK(launch_xlat_cols(p, s));
+        CK(launch_xlat_out(p, s));
+        CK(launch_finalize(p, s));
+        k += 4;
+    }
+    *launches += k;
+    return FSCAN_OK;
+}
+
+fscan_status check_ctx(fscan_ctx* ctx, int batch) {
+    if (!ctx) return FSCAN_ERR_INVALID_ARGUMENT;
+    if (batch < 0 || batch > ctx->max_batch)
+        return fail(ctx, FSCAN_ERR_INVALID_ARGUMENT, "batch exceeds the context's max_batch");
+    cudaError_t e = cudaSetDevice(ctx->device);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
+    return FSCAN_OK;
+}
+
+// Generic device-side driver: split `batch` into chunks over the lanes,
+// ordered after `user` and with `user` waiting for all lanes.
+template <typename F>
+fscan_status drive(fscan_ctx* ctx, int batch, cudaStream_t user, F&& per_chunk) {
+    CK(cudaEventRecord(ctx->start_ev, user));
+    for (auto& l : ctx->lanes) CK(cudaStreamWaitEvent(l.stream, ctx->start_ev, 0));
+    ctx->launches_last = 0;
+    int li = 0;
+    for (int off = 0; off < batch; off += ctx->chunk, li = (li + 1) % kLanes) {
+        const int cnt = std::min(ctx->chunk, batch - off);
+        fscan_status st = per_chunk(ctx->lanes[li], off, cnt);
+        if (st != FSCAN_OK) return st;
+    }
+    for (auto& l : ctx->lanes) {
+        CK(cudaEventRecord(l.done, l.stream));
+        CK(cudaStreamWaitEvent(user, l.done, 0));
+    }
+    return FSCAN_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+void fscan_config_defaults(fscan_config* c) {
+    // MatchConfig defaults (matcher.hpp:13-26)
+    c->n_theta = 733;
+    c->delta_theta = kPi / 733.0;
+    c->t_theta = 2.0;
+    c->n_xy = 255;
+    c->delta_xy = 0.4;
+    c->t_xy = 1.0;
+    c->band_lo = 0.03;
+    c->band_hi = 0.75;
+    c->n_radius = 128;
+    c->pad_angle = 92;
+    c->softargmax_window = 16;
+    c->normalize_scores = 1;
+}
+
+void fscan_config_finalize(fscan_config* c) {  // matcher.cpp:11-15
+    if (c->n_radius <= 0) c->n_radius = (c->n_xy + 1) / 2;
+    if (c->pad_angle < 0) c->pad_angle = std::min((c->n_theta + 7) / 8, c->n_theta - 1);
+}
+
+fscan_status fscan_config_validate(const fscan_config* c, char* msg, size_t len) {
+    auto bad = [&](const char* m) {
+        if (msg && len) std::snprintf(msg, len, "%s", m);
+        return FSCAN_ERR_INVALID_ARGUMENT;
+    };
+    // matcher.cpp:17-37 (the odd-n rule is the D1 exception)
+    if (c->n_theta < 1) return bad("config: n_theta must be >= 1");
+    if (!(c->delta_theta > 0.0)) return bad("config: delta_theta must be positive");
+    if (c->n_theta * c->delta_theta > kPi + 1e-9) return bad("config: n_theta * delta_theta must not exceed pi");
+    if (!(c->t_theta > 0.0) || !(c->t_xy > 0.0)) return bad("config: softmax gains must be positive");
+    if (c->n_xy < 3) return bad("config: n_xy must be >= 3");
+    if (!(c->delta_xy > 0.0)) return bad("config: delta_xy must be positive");
+    if (!(c->band_lo >= 0.0 && c->band_lo < c->band_hi && c->band_hi <= 1.0))
+        return bad("config: band must satisfy 0 <= lo < hi <= 1");
+    if (c->n_theta > 1 && c->n_radius < 2) return bad("config: n_radius must be >= 2");
+    if (c->pad_angle < 0 || c->pad_angle >= c->n_theta) return bad("config: need 0 <= pad_angle < n_theta");
+    if (c->softargmax_window < 1) return bad("config: softargmax_window must be >= 1");
+    if (msg && len) msg[0] = 0;
+    return FSCAN_OK;
+}
+
+fscan_status fscan_ctx_create(int device, const fscan_config* cfg_in, int max_batch, fscan_ctx** out) {
+    if (!out || !cfg_in || max_batch < 1) return FSCAN_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    fscan_config cfg = *cfg_in;
+    fscan_config_finalize(&cfg);
+    char msg[256];
+    fscan_status st = fscan_config_validate(&cfg, msg, sizeof msg);
+    fscan_ctx* ctx = new fscan_ctx();
+    ctx->cfg = cfg;
+    ctx->device = device;
+    ctx->n = cfg.n_xy;
+    ctx->max_batch = max_batch;
+    if (st != FSCAN_OK) {
+        ctx->err = msg;
+        *out = ctx;
+        return st;
+    }
+    *out = ctx;
+    if (!is_pow2(ctx->n) || ctx->n < 64 || ctx->n > 1024)
+        return fail(ctx, FSCAN_ERR_UNSUPPORTED, "n_xy must be a power of two in [64, 1024] on the GPU path");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
+        return fail(ctx, FSCAN_ERR_NO_DEVICE, "no CUDA device " + std::to_string(device));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10) return fail(ctx, FSCAN_ERR_NO_DEVICE, "needs an sm_100 (B200) device");
+    CK(cudaSetDevice(device));
+
+    const int n = ctx->n;
+    // tables
+    std::vector<float2> tw(n), tw2(2 * n);
+    for (int i = 0; i < n; ++i) {
+        const double a = -2.0 * kPi * i / n;
+        tw[i] = make_float2((float)std::cos(a), (float)std::sin(a));
+    }
+    for (int i = 0; i < 2 * n; ++i) {
+        const double a = -2.0 * kPi * i / (2 * n);
+        tw2[i] = make_float2((float)std::cos(a), (float)std::sin(a));
+    }
+    std::vector<float> hann(n, 1.0f);  // imageops.cpp:30-42
+    if (n > 1)
+        for (int i = 0; i < n; ++i) hann[i] = (float)(0.5 * (1.0 - std::cos(2.0 * kPi * i / (n - 1))));
+    std::vector<int2> band;
+    std::vector<unsigned char> inband;
+    if (!build_band(n, cfg.band_lo, cfg.band_hi, band, inband))
+        return fail(ctx, FSCAN_ERR_UNSUPPORTED, "band is not an interval per row");
+    std::vector<PolarTap> taps;
+    if (cfg.n_theta > 1) {
+        std::string why;
+        if (!build_taps(n, cfg, inband, taps, &ctx->n_live, &why)) return fail(ctx, FSCAN_ERR_UNSUPPORTED, why);
+    } else {
+        taps.resize(1);
+        ctx->n_live = 1;
+    }
+    CK(cudaMalloc(&ctx->tw_n, sizeof(float2) * n));
+    CK(cudaMalloc(&ctx->tw_2n, sizeof(float2) * 2 * n));
+    CK(cudaMalloc(&ctx->hann, sizeof(float) * n));
+    CK(cudaMalloc(&ctx->band, sizeof(int2) * n));
+    CK(cudaMalloc(&ctx->taps, sizeof(PolarTap) * taps.size()));
+    CK(cudaMemcpy(ctx->tw_n, tw.data(), sizeof(float2) * n, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->tw_2n, tw2.data(), sizeof(float2) * 2 * n, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->hann, hann.data(), sizeof(float) * n, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->band, band.data(), sizeof(int2) * n, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->taps, taps.data(), sizeof(PolarTap) * taps.size(), cudaMemcpyHostToDevice));
+
+    // default chunk: about 1 GiB of workspace per lane
+    const double per_pair = (double)n * n * (8 + 4) + (double)n * (n + 1) * (8 + 16);
+    int chunk = (int)std::max(1.0, std::floor((1024.0 * 1024 * 1024) / per_pair));
+    chunk = std::min(chunk, max_batch);
+    ctx->chunk = chunk;
+    ctx->alloc_chunk = chunk;
+    CK(cudaEventCreateWithFlags(&ctx->start_ev, cudaEventDisableTiming));
+    for (auto& l : ctx->lanes) {
+        CK(cudaStreamCreateWithFlags(&l.stream, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&l.done, cudaEventDisableTiming));
+        fscan_status a = alloc_lane(ctx, l, chunk);
+        if (a != FSCAN_OK) return a;
+    }
+    return FSCAN_OK;
+}
+
+void fscan_ctx_destroy(fscan_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    for (auto& l : ctx->lanes) {
+        if (l.stream) cudaStreamSynchronize(l.stream);
+        free_lane(l);
+        if (l.stream) cudaStreamDestroy(l.stream);
+        if (l.done) cudaEventDestroy(l.done);
+    }
+    if (ctx->start_ev) cudaEventDestroy(ctx->start_ev);
+    cudaFree(ctx->tw_n);
+    cudaFree(ctx->tw_2n);
+    cudaFree(ctx->hann);
+    cudaFree(ctx->band);
+    cudaFree(ctx->taps);
+    delete ctx;
+}
+
+const char* fscan_ctx_last_error(const fscan_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int fscan_ctx_n(const fscan_ctx* ctx) { return ctx ? ctx->n : 0; }
+
+int fscan_ctx_launches_last(const fscan_ctx* ctx) { return ctx ? ctx->launches_last : 0; }
+
+fscan_status fscan_ctx_set_chunk(fscan_ctx* ctx, int pairs) {
+    if (!ctx || pairs < 0) return FSCAN_ERR_INVALID_ARGUMENT;
+    std::lock_guard<std::mutex> g(ctx->mu);
+    if (pairs == 0) pairs = ctx->alloc_chunk;
+    if (pairs > ctx->alloc_chunk) {
+        cudaSetDevice(ctx->device);
+        for (auto& l : ctx->lanes) {
+            cudaStreamSynchronize(l.stream);
+            const bool had_host = l.in != nullptr;
+            free_lane(l);
+            fscan_status a = alloc_lane(ctx, l, pairs);
+            if (a != FSCAN_OK) return a;
+            if (had_host) {
+                a = alloc_host_staging(ctx, l, pairs);
+                if (a != FSCAN_OK) return a;
+            }
+        }
+        ctx->alloc_chunk = pairs;
+    }
+    ctx->chunk = pairs;
+    return FSCAN_OK;
+}
+
+fscan_status fscan_match_batch(fscan_ctx* ctx, const float* d_f, const float* d_g, const float* d_mf,
+                               const float* d_mg, int batch, double delta, fscan_pair_result* d_out,
+                               double* d_tsurf, float* d_xsurf, void* stream) {
+    fscan_status st = check_ctx(ctx, batch);
+    if (st != FSCAN_OK) return st;
+    std::lock_guard<std::mutex> g(ctx->mu);
+    if (!ctx->tw_n) return fail(ctx, FSCAN_ERR_INVALID_ARGUMENT, "context was not created successfully");
+    if (!d_f || !d_g || !d_out || ((d_mf == nullptr) != (d_mg == nullptr)) || !(delta > 0.0))
+        return fail(ctx, FSCAN_ERR_INVALID_ARGUMENT, "fscan_match_batch: bad pointers or delta");
+    if (batch == 0) return FSCAN_OK;
+    const size_t nn = (size_t)ctx->n * ctx->n;
+    const int nt = ctx->cfg.n_theta;
+    return drive(ctx, batch, (cudaStream_t)stream, [&](Lane& l, int off, int cnt) {
+        Params p = base_params(ctx, l, cnt, delta);
+        p.f = d_f + off * nn;
+        p.g = d_g + off * nn;
+        p.mf = d_mf ? d_mf + off * nn : nullptr;
+        p.mg = d_mg ? d_mg + off * nn : nullptr;
+        p.out = d_out + off;
+        p.theta_surf = d_tsurf ? d_tsurf + (size_t)off * nt : nullptr;
+        p.xy_surf = d_xsurf ? d_xsurf + off * nn : nullptr;
+        return run_chunk(ctx, l, p, Stages::Full, &ctx->launches_last);
+    });
+}
+
+fscan_status fscan_estimate_rotation_batch(fscan_ctx* ctx, const float* d_f, const float* d_g, int batch,
+                                           double* d_theta, double* d_tsurf, void* stream) {
+    fscan_status st = check_ctx(ctx, batch);
+    if (st != FSCAN_OK) return st;
+    std::lock_guard<std::mutex> g(ctx->mu);
+    if (!d_f || !d_g || !d_theta) return fail(ctx, FSCAN_ERR_INVALID_ARGUMENT, "bad pointers");
+    if (batch == 0) return FSCAN_OK;
+    const size_t nn = (size_t)ctx->n * ctx->n;
+    return drive(ctx, batch, (cudaStream_t)stream, [&](Lane& l, int off, int cnt) {
+        Params p = base_params(ctx, l, cnt, 1.0);
+        p.f = d_f + off * nn;
+        p.g = d_g + off * nn;
+        p.theta_only = d_theta + off;
+        p.theta_surf = d_tsurf ? d_tsurf + (size_t)off * ctx->cfg.n_theta : nullptr;
+        return run_chunk(ctx, l, p, Stages::Rotation, &ctx->launches_last);
+    });
+}
+
+fscan_status fscan_estimate_translation_batch(fscan_ctx* ctx, const float* d_f, const float* d_g, int batch,
+                                              double delta, const double* d_theta, double* d_txy,
+                                              float* d_xsurf, void* stream) {
+    fscan_status st = check_ctx(ctx, batch);
+    if (st != FSCAN_OK) return st;
+    std::lock_guard<std::mutex> g(ctx->mu);
+    if (!d_f || !d_g || !d_theta || !d_txy || !(delta > 0.0))
+        return fail(ctx, FSCAN_ERR_INVALID_ARGUMENT, "bad pointers or delta");
+    if (batch == 0) return FSCAN_OK;
+    const size_t nn = (size_t)ctx->n * ctx->n;
+    return drive(ctx, batch, (cudaStream_t)stream, [&](Lane& l, int off, int cnt) {
+        Params p = base_params(ctx, l, cnt, delta);
+        p.f = d_f + off * nn;
+        p.g = d_g + off * nn;
+        p.theta_in = d_theta + off;
+        p.txy_only = d_txy + 2 * off;
+        p.xy_surf = d_xsurf ? d_xsurf + off * nn : nullptr;
+        return run_chunk(ctx, l, p, Stages::Translation, &ctx->launches_last);
+    });
+}
+
+fscan_status fscan_band_magnitude_batch(fscan_ctx* ctx, const float* d_img, int batch, float* d_out,
+                                        void* stream) {
+    fscan_status st = check_ctx(ctx, batch);
+    if (st != FSCAN_OK) return st;
+    std::lock_guard<std::mutex> g(ctx->mu);
+    if (!d_img || !d_out) return fail(ctx, FSCAN_ERR_INVALID_ARGUMENT, "bad pointers");
+    if (batch == 0) return FSCAN_OK;
+    const size_t nn = (size_t)ctx->n * ctx->n;
+    return drive(ctx, batch, (cudaStream_t)stream, [&](Lane& l, int off, int cnt) {
+        Params p = base_params(ctx, l, cnt, 1.0);
+        p.f = d_img + off * nn;
+        p.g = d_img + off * nn;
+        p.mag_out = d_out + off * (nn / 2);
+        return run_chunk(ctx, l, p, Stages::Magnitude, &ctx->launches_last);
+    });
+}
+
+fscan_status fscan_match_batch_host(fscan_ctx* ctx, const float* f, const float* g, const float* mf,
+                                    const float* mg, int batch, double delta, fscan_pair_result* out,
+                                    double* tsurf, float* xsurf) {
+    fscan_status st = check_ctx(ctx, batch);
+    if (st != FSCAN_OK) return st;
+    std::lock_guard<std::mutex> guard(ctx->mu);
+    if (!ctx->tw_n) return fail(ctx, FSCAN_ERR_INVALID_ARGUMENT, "context was not created successfully");
+    if (!f || !g || !out || ((mf == nullptr) != (mg == nullptr)) || !(delta > 0.0))
+        return fail(ctx, FSCAN_ERR_INVALID_ARGUMENT, "fscan_match_batch_host: bad pointers or delta");
+    if (batch == 0) return FSCAN_OK;
+    const size_t nn = (size_t)ctx->n * ctx->n;
+    const int nt = ctx->cfg.n_theta;
+    for (auto& l : ctx->lanes) {
+        fscan_status a = alloc_host_staging(ctx, l, ctx->alloc_chunk);
+        if (a != FSCAN_OK) return a;
+    }
+    ctx->launches_last = 0;
+    int li = 0;
+    // lane-alternating chunks: H2D(i+1) overlaps compute(i) on the other lane
+    for (int off = 0; off < batch; off += ctx->chunk, li = (li + 1) % kLanes) {
+        Lane& l = ctx->lanes[li];
+        const int cnt = std::min(ctx->chunk, batch - off);
+        cudaStream_t s = l.stream;
+        float* df = l.in;
+        float* dg = l.in + nn * cnt;
+        float* dmf = mf ? l.in + 2 * nn * cnt : nullptr;
+        float* dmg = mf ? l.in + 3 * nn * cnt : nullptr;
+        CK(cudaMemcpyAsync(df, f + off * nn, nn * cnt * sizeof(float), cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(dg, g + off * nn, nn * cnt * sizeof(float), cudaMemcpyHostToDevice, s));
+        if (mf) {
+            CK(cudaMemcpyAsync(dmf, mf + off * nn, nn * cnt * sizeof(float), cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(dmg, mg + off * nn, nn * cnt * sizeof(float), cudaMemcpyHostToDevice, s));
+        }
+        Params p = base_params(ctx, l, cnt, delta);
+        p.f = df;
+        p.g = dg;
+        p.mf = dmf;
+        p.mg = dmg;
+        p.out = l.res;
+        p.theta_surf = tsurf ? l.tsurf : nullptr;
+        p.xy_surf = xsurf ? l.xsurf : nullptr;
+        fscan_status r = run_chunk(ctx, l, p, Stages::Full, &ctx->launches_last);
+        if (r != FSCAN_OK) return r;
+        CK(cudaMemcpyAsync(out + off, l.res, sizeof(fscan_pair_result) * cnt, cudaMemcpyDeviceToHost, s));
+        if (tsurf)
+            CK(cudaMemcpyAsync(tsurf + (size_t)off * nt, l.tsurf, sizeof(double) * nt * cnt,
+                               cudaMemcpyDeviceToHost, s));
+        if (xsurf)
+            CK(cudaMemcpyAsync(xsurf + off * nn, l.xsurf, sizeof(float) * nn * cnt, cudaMemcpyDeviceToHost, s));
+        // the staging buffers of this lane are reused two chunks later: the
+        // stream order already serialises that reuse.
+    }
+    for (auto& l : ctx->lanes) CK(cudaStreamSynchronize(l.stream));
+    for (int i = 0; i < batch; ++i)
+        if (out[i].status != FSCAN_OK) {
+            const fscan_status bad = (fscan_status)out[i].status;
+            return fail(ctx, bad,
+                        bad == FSCAN_ERR_MASK_RANGE ? "MaskGrid: values must lie in [0, 1]"
+                                                    : "scan_match: input grids contain non-finite values");
+        }
+    return FSCAN_OK;
+}
+
+fscan_status fscan_polar_to_cart_batch(const float* d_polar, int batch, int n_az, int n_range,
+                                       double range_res, int n, double delta, float* d_out, void* stream) {
+    if (!d_polar || !d_out || batch < 0 || n_az < 1 || n_range < 1 || n < 1 || !(range_res > 0) || !(delta > 0))
+        return FSCAN_ERR_INVALID_ARGUMENT;
+    if (batch == 0) return FSCAN_OK;
+    cudaError_t e = launch_polar_to_cart(d_polar, batch, n_az, n_range, range_res, n, delta, d_out,
+                                         (cudaStream_t)stream);
+    return e == cudaSuccess ? FSCAN_OK : FSCAN_ERR_CUDA;
+}
+
+fscan_status fscan_check_results(const fscan_pair_result* d_out, int batch, void* stream, int* first_bad) {
+    if (first_bad) *first_bad = -1;
+    if (batch <= 0) return FSCAN_OK;
+    std::vector<fscan_pair_result> h(batch);
+    if (cudaMemcpyAsync(h.data(), d_out, sizeof(fscan_pair_result) * batch, cudaMemcpyDeviceToHost,
+                        (cudaStream_t)stream) != cudaSuccess)
+        return FSCAN_ERR_CUDA;
+    if (cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) return FSCAN_ERR_CUDA;
+    for (int i = 0; i < batch; ++i)
+        if (h[i].status != FSCAN_OK) {
+            if (first_bad) *first_bad = i;
+            return (fscan_status)h[i].status;
+        }
+    return FSCAN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,212 @@
+// fft.cuh — register/shared-memory radix-16 Stockham FFT engine (sm_100a).
+//
+// Replaces the FFTW c2c transforms the reference calls through
+// proj/src/spectral.cpp:73-153 (dft2 / idft2 / xcorr) on the GPU path.
+//
+// One length-N transform (N = 2^k, 64 <= N <= 2048) is owned by T = N/16
+// threads; thread t of a transform holds the 16 complex values
+//     v[m] = x[t + m*T],  m = 0..15
+// before and after the call (natural order in, natural order out). Stages are
+// radix 16 while at least 16*16 points remain, then one radix-R stage
+// (R = N / 16^s in {2,4,8,16}) done as 16/R butterflies per thread:
+//     N=64: 16.4   128: 16.8   256: 16.16   512: 16.16.2   1024: 16.16.4   2048: 16.16.8
+// Stage (radix R, span Ns) butterfly b reads x[b + r*N/R] (= registers
+// j + r*(16/R) of thread t, b = t + j*T), multiplies by W_{Ns*R}^{r*(b mod Ns)},
+// does an R-point DFT and writes y[(b/Ns)*Ns*R + (b mod Ns) + r*Ns]. The last
+// stage lands back in the input register slots, so only S-1 shared-memory
+// exchanges are needed (one for N <= 256, two for 512..2048). The exchange
+// buffer is split real/imag (4-byte banks) with one pad float every 32.
+//
+// Twiddles come from a fp32 table tw[i] = exp(-2*pi*i*i/N) (rounded from fp64
+// on the host); SIGN = +1 uses the conjugate. Transforms are unnormalised,
+// matching FFTW_FORWARD / FFTW_BACKWARD.
+//
+// Every thread of the CTA must call fft_regs the same number of times (it
+// contains __syncthreads()).
+#pragma once
+
+#include <cuda_runtime.h>
+
+namespace fscan_fft {
+
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+    return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
+// a * (-i) for SIGN=-1, a * (+i) for SIGN=+1
+template <int SIGN>
+__device__ __forceinline__ float2 mul_mi(float2 a) {
+    return SIGN < 0 ? make_float2(a.y, -a.x) : make_float2(-a.y, a.x);
+}
+
+template <int SIGN>
+__device__ __forceinline__ void dft2(float2& a, float2& b) {
+    const float2 t = a;
+    a = cadd(t, b);
+    b = csub(t, b);
+}
+
+// 4-point DFT in place, natural order out.
+template <int SIGN>
+__device__ __forceinline__ void dft4(float2& x0, float2& x1, float2& x2, float2& x3) {
+    const float2 a = cadd(x0, x2), b = csub(x0, x2);
+    const float2 c = cadd(x1, x3), d = mul_mi<SIGN>(csub(x1, x3));
+    x0 = cadd(a, c);
+    x2 = csub(a, c);
+    x1 = cadd(b, d);
+    x3 = csub(b, d);
+}
+
+// 8-point DFT: x[k1 + 2*k2]... done as radix-2 x radix-4 (DIT over n = 2*n1 + n2).
+template <int SIGN>
+__device__ __forceinline__ void dft8(float2* x) {
+    constexpr float r = 0.70710678118654752f;
+    // 4-point DFTs over even and odd samples
+    float2 e0 = x[0], e1 = x[2], e2 = x[4], e3 = x[6];
+    float2 o0 = x[1], o1 = x[3], o2 = x[5], o3 = x[7];
+    dft4<SIGN>(e0, e1, e2, e3);
+    dft4<SIGN>(o0, o1, o2, o3);
+    // twiddles W8^k on odd part
+    o1 = SIGN < 0 ? make_float2(r * (o1.x + o1.y), r * (o1.y - o1.x)) : make_float2(r * (o1.x - o1.y), r * (o1.y + o1.x));
+    o2 = mul_mi<SIGN>(o2);
+    o3 = SIGN < 0 ? make_float2(r * (o3.y - o3.x), -r * (o3.x + o3.y)) : make_float2(-r * (o3.x + o3.y), r * (o3.x - o3.y));
+    x[0] = cadd(e0, o0);
+    x[4] = csub(e0, o0);
+    x[1] = cadd(e1, o1);
+    x[5] = csub(e1, o1);
+    x[2] = cadd(e2, o2);
+    x[6] = csub(e2, o2);
+    x[3] = cadd(e3, o3);
+    x[7] = csub(e3, o3);
+}
+
+// 16-point DFT as 4x4: X[k1 + 4*k2] = sum_n2 W4^(n2 k2) W16^(n2 k1) sum_n1 x[4 n1 + n2] W4^(n1 k1)
+template <int SIGN>
+__device__ __forceinline__ void dft16(float2* x) {
+    constexpr float c1 = 0.92387953251128674f;  // cos(pi/8)
+    constexpr float s1 = 0.38268343236508977f;  // sin(pi/8)
+    constexpr float r = 0.70710678118654752f;
+#pragma unroll
+    for (int n2 = 0; n2 < 4; ++n2) dft4<SIGN>(x[n2], x[4 + n2], x[8 + n2], x[12 + n2]);
+    // now x[4*k1 + n2] holds a[n2][k1]; apply W16^(n2*k1)
+    const float sg = (float)SIGN;  // W16^m = cos(2 pi m/16) + i*SIGN*sin(2 pi m/16)
+    const float2 w1 = make_float2(c1, sg * s1), w2 = make_float2(r, sg * r), w3 = make_float2(s1, sg * c1);
+    const float2 w6 = make_float2(-r, sg * r), w9 = make_float2(-c1, -sg * s1);
+    x[4 * 1 + 1] = cmul(x[4 * 1 + 1], w1);
+    x[4 * 2 + 1] = cmul(x[4 * 2 + 1], w2);
+    x[4 * 3 + 1] = cmul(x[4 * 3 + 1], w3);
+    x[4 * 1 + 2] = cmul(x[4 * 1 + 2], w2);
+    x[4 * 2 + 2] = mul_mi<SIGN>(x[4 * 2 + 2]);
+    x[4 * 3 + 2] = cmul(x[4 * 3 + 2], w6);
+    x[4 * 1 + 3] = cmul(x[4 * 1 + 3], w3);
+    x[4 * 2 + 3] = cmul(x[4 * 2 + 3], w6);
+    x[4 * 3 + 3] = cmul(x[4 * 3 + 3], w9);
+    // 4-point DFTs over n2 for each k1: inputs x[4 k1 + n2], outputs X[k1 + 4 k2]
+    float2 y[16];
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) {
+        float2 a0 = x[4 * k1], a1 = x[4 * k1 + 1], a2 = x[4 * k1 + 2], a3 = x[4 * k1 + 3];
+        dft4<SIGN>(a0, a1, a2, a3);
+        y[k1] = a0;
+        y[k1 + 4] = a1;
+        y[k1 + 8] = a2;
+        y[k1 + 12] = a3;
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) x[i] = y[i];
+}
+
+template <int R, int SIGN>
+__device__ __forceinline__ void dft_r(float2* x) {
+    if constexpr (R == 2) {
+        dft2<SIGN>(x[0], x[1]);
+    } else if constexpr (R == 4) {
+        dft4<SIGN>(x[0], x[1], x[2], x[3]);
+    } else if constexpr (R == 8) {
+        dft8<SIGN>(x);
+    } else {
+        dft16<SIGN>(x);
+    }
+}
+
+__device__ __forceinline__ int spad(int i) { return i + (i >> 5); }
+
+// floats of exchange buffer per transform (re + im halves)
+template <int N>
+struct Cfg {
+    static constexpr int T = N / 16;
+    static constexpr int kHalf = N + N / 32;  // padded real (or imag) part
+    static constexpr int kFloats = 2 * kHalf;
+    static constexpr int kStages = (N <= 256) ? 2 : 3;
+    static constexpr int kLastR = (N <= 256) ? (N / 16) : (N / 256);
+};
+
+template <int SIGN>
+__device__ __forceinline__ float2 twiddle(const float2* __restrict__ tw, int idx) {
+    const float2 w = __ldg(tw + idx);
+    return SIGN < 0 ? w : make_float2(w.x, -w.y);
+}
+
+// One Stockham stage. Ns = span before this stage, R = radix.
+template <int N, int R, int Ns, bool LAST, int SIGN>
+__device__ __forceinline__ void stage(float2 (&v)[16], int t, float* sre, float* sim,
+                                      const float2* __restrict__ tw) {
+    constexpr int T = N / 16;
+    constexpr int NB = 16 / R;
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+        float2 u[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) u[r] = v[j + r * NB];
+        const int b = t + j * T;
+        const int k = b & (Ns - 1);
+        if constexpr (Ns > 1) {
+            constexpr int q = N / (Ns * R);  // W_{Ns R}^x = tw[x * q]
+#pragma unroll
+            for (int r = 1; r < R; ++r) u[r] = cmul(u[r], twiddle<SIGN>(tw, r * k * q));
+        }
+        dft_r<R, SIGN>(u);
+        if constexpr (LAST) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) v[j + r * NB] = u[r];
+        } else {
+            const int base = (b / Ns) * Ns * R + k;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int p = spad(base + r * Ns);
+                sre[p] = u[r].x;
+                sim[p] = u[r].y;
+            }
+        }
+    }
+    if constexpr (!LAST) {
+        __syncthreads();
+#pragma unroll
+        for (int m = 0; m < 16; ++m) {
+            const int p = spad(t + m * T);
+            v[m] = make_float2(sre[p], sim[p]);
+        }
+        __syncthreads();
+    }
+}
+
+// In-register FFT of one length-N transform (see header comment).
+// sbuf: Cfg<N>::kFloats floats of shared memory owned by this transform.
+template <int N, int SIGN>
+__device__ __forceinline__ void fft_regs(float2 (&v)[16], int t, float* sbuf,
+                                         const float2* __restrict__ tw) {
+    float* sre = sbuf;
+    float* sim = sbuf + Cfg<N>::kHalf;
+    if constexpr (N <= 256) {
+        stage<N, 16, 1, false, SIGN>(v, t, sre, sim, tw);
+        stage<N, N / 16, 16, true, SIGN>(v, t, sre, sim, tw);
+    } else {
+        stage<N, 16, 1, false, SIGN>(v, t, sre, sim, tw);
+        stage<N, 16, 16, false, SIGN>(v, t, sre, sim, tw);
+        stage<N, N / 256, 256, true, SIGN>(v, t, sre, sim, tw);
+    }
+}
+
+}  // namespace fscan_fft

@@ -1,0 +1,90 @@
+// pipeline.h — device-side parameter block and kernel launchers of the
+// sm_100a scan_match pipeline (kernels.cu), used by the runtime (context.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "fscan_cuda.h"
+
+namespace fscan_detail {
+
+// One precomputed bilinear tap set of cart2pol (imageops.cpp:81-99 via
+// sample_bilinear 10-26): packed = r0 | u0 << 12 | valid-tap bits << 24,
+// with (r0, u0) the top-left tap in (centred row, u >= 0 column) coordinates.
+struct PolarTap {
+    int packed;
+    float fr, fc;
+    float pad_;
+};
+
+// Per-pair state handed from the angular stage to the translation stage.
+struct RotState {
+    double theta;      // soft-argmax theta (radians, not wrapped)
+    double st, ct;     // sin(-theta), cos(-theta) for rotate_bilinear(g, -theta)
+    double peak;       // theta surface at the hard argmax
+    double hard;       // coordinate of the hard argmax
+    int bin;           // hard argmax row
+    int identity;      // -theta == 0.0: rotate_bilinear returns g unchanged
+};
+
+struct Partial {
+    float val;
+    int idx;
+};
+
+struct Params {
+    int n;        // grid side N (power of two)
+    int batch;    // pairs in this launch
+    // inputs (device)
+    const float* f;
+    const float* g;
+    const float* mf;  // nullable
+    const float* mg;
+    // workspace
+    float* ft;     // masked f  [batch][N][N]
+    float* gt;     // masked g
+    float2* zbuf;  // K1a->K1b spectra [batch][N][N]; reused as K4->K5 rows [batch][N][N+1]
+    float* mag;    // |F|,|G| band-passed half planes, tiled [batch][2][N/16][N][8]; reused as surface
+    float4* fgt;   // row spectra of f, g_rot, transposed [batch][N+1][N] (F.re, F.im, G.re, G.im)
+    float* surf;   // translation surface [batch][N][N]
+    Partial* part; // K5 per-block argmax [batch][N / rows_per_block]
+    RotState* rot; // [batch]
+    int* flags;    // [batch] bit0 non-finite, bit1 mask out of [0,1]
+    // tables
+    const float2* tw_n;   // exp(-2 pi i k / N), k < N
+    const float2* tw_2n;  // exp(-2 pi i k / 2N), k < 2N
+    const float* hann;    // N
+    const int2* band;     // per centred row: [u_lo, u_hi] in band (empty: lo > hi)
+    const PolarTap* taps; // [n_theta][n_live]
+    int n_live;
+    // config
+    int n_theta, pad, L, C;
+    double delta_theta, t_theta, t_xy, delta;
+    int window, normalize;
+    // outputs
+    fscan_pair_result* out;   // nullable for stage calls
+    double* theta_surf;       // nullable
+    float* xy_surf;           // nullable (else surf is workspace)
+    double* theta_only;       // stage API: theta per pair (nullable)
+    double* txy_only;         // stage API: (tx, ty) per pair (nullable)
+    const double* theta_in;   // stage API: theta per pair for translation-only runs
+    float* mag_out;           // stage API: band magnitude, [batch][N][N/2] (nullable)
+};
+
+// Launch the stages; each returns cudaGetLastError() of its launch.
+cudaError_t launch_rot_rows(const Params& p, cudaStream_t s);        // K1a
+cudaError_t launch_rot_cols(const Params& p, cudaStream_t s);        // K1b
+cudaError_t launch_rot_polar(const Params& p, cudaStream_t s);       // K2
+cudaError_t launch_theta_in(const Params& p, cudaStream_t s);        // stage API: theta from caller
+cudaError_t launch_xlat_rows(const Params& p, cudaStream_t s);       // K3
+cudaError_t launch_xlat_cols(const Params& p, cudaStream_t s);       // K4
+cudaError_t launch_xlat_out(const Params& p, cudaStream_t s);        // K5
+cudaError_t launch_finalize(const Params& p, cudaStream_t s);        // K6
+cudaError_t launch_mag_unpack(const Params& p, cudaStream_t s);      // stage API helper
+cudaError_t launch_polar_to_cart(const float* d_polar, int batch, int n_az, int n_range,
+                                 double range_res, int n, double delta, float* d_out,
+                                 cudaStream_t stream);                  // K0
+int rows_per_block_out(int n);  // K5 rows per CTA (partials per pair = n / this)
+
+}  // namespace fscan_detail
