@@ -1,0 +1,391 @@
+#!/usr/bin/env python3
+"""Throughput bench of the B200 decoupled Fourier pose search (scan-pair registrations/s).
+
+Workload (BASELINE.json configs[3], "C4"): 4096 scan pairs, 512x512 fp32
+Cartesian grids produced from raw polar sweeps by the config-3 generator
+(device-rendered, then the product K0 kernel), per-pixel sigmoid masks,
+720 azimuth bins, soft-argmax T=1, sharded by pair index over the ranks.
+A step = one full pass of the hot path (rotation + translation search, pose
+out) over the rank's shard, inputs resident in HBM (16 GiB > 126 MB L2, so no
+L2 flush is needed between steps).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 4]
+
+Under torchrun each rank takes pairs [r*B/N, (r+1)*B/N); timing is CUDA
+events on the launching stream, barrier + synchronize on both sides, max over
+ranks; rank 0 prints one JSON line. `--impl reference` times the reference's
+own CPU implementation (oracle/_ref: the reference sources + FFTW-API shim)
+on the host cores instead (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "scan-pair registrations/sec (rot+trans search)"
+UNIT = "pairs/s"
+KERNEL_NAMES = ("rot_rows", "rot_cols", "rot_polar", "theta_in", "xlat_rows", "xlat_cols", "xlat_out",
+                "finalize", "mag_unpack")
+
+
+def workload_desc(cid: int) -> str:
+    return {
+        1: "C1: 1 pair, 256x256 fp32 Cartesian, 360 bins, hard argmax",
+        2: "C2: 64 pairs, 256x256 fp32 Cartesian, sigmoid masks, 360 bins, soft-argmax T=1",
+        3: "C3: 64 pairs, raw polar 400x3768 -> 512x512 on device, masks, 720 bins, soft-argmax",
+        4: "C4: 4096 pairs, 512x512 fp32 Cartesian from the config-3 polar generator, sigmoid masks, "
+           "720 azimuth bins, soft-argmax T=1",
+        5: "C5: 1024 pairs, 1024x1024 fp32 Cartesian, sigmoid masks, 1440 bins, soft-argmax T=0.5",
+    }[cid]
+
+
+def pair_bytes(n: int, n_theta: int, pad: int, masks: bool = True, s_in: float | None = None) -> float:
+    """SURVEY.md §8(d) algorithmic bytes per pair of the canonical staged dataflow."""
+    P = 2 * n
+    HN = n * (n // 2 + 1)
+    HP = P * (P // 2 + 1)
+    L = n_theta + 2 * pad
+    if s_in is None:
+        s_in = 8 * n * n
+    return s_in + 8 * (1 if masks else 0) * n * n + 16 * n * n + 16 * HN + 32 * HP + 8 * L + 16
+
+
+def kernel_alg_bytes(name: str, n: int) -> float:
+    """Compulsory DRAM bytes per pair of each of OUR kernels."""
+    nn = n * n
+    return {
+        "rot_rows": 16 * nn + 8 * nn + 8 * nn,            # f,g,mf,mg in; f~,g~ out; Z out
+        "rot_cols": 8 * nn + 4 * nn,                      # Z in; |F|,|G| half planes out
+        "rot_polar": 4 * nn,                              # magnitude planes in
+        "xlat_rows": 8 * nn + 16 * n * (n + 1),           # f~,g~ in; row spectra out
+        "xlat_cols": 16 * n * (n + 1) + 8 * n * (n + 1),  # row spectra in; Y out
+        "xlat_out": 8 * n * (n + 1) + 4 * nn,             # Y in; surface out
+        "finalize": 0.0,
+        "theta_in": 0.0,
+        "mag_unpack": 0.0,
+    }[name]
+
+
+# ---------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows: list[list[str]] = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self) -> dict:
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 5 + i and r[5 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------- helpers
+
+def peaks() -> tuple[float, str]:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(kernel: str) -> float | None:
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full summary, if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return d.get(kernel, {}).get("dram_bytes_per_pair")
+    except Exception:
+        return None
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def allmax(world, x: float, device) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def cpu_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def ref_cpu_run(f, g, mf, mg, cfg, delta, threads):
+    """The reference's own scan_match over a batch (oracle/_ref, parallel_for)."""
+    import oracle
+    oc = oracle.make_config(**{k: (int(v) if isinstance(v, bool) else v) for k, v in cfg.__dict__.items()})
+    if oracle.have_ref():
+        t0 = time.perf_counter()
+        oracle.ref_batch_f32(f, g, mf, mg, oc, delta, threads)
+        return time.perf_counter() - t0, "reference"
+    # port fallback (restatement), single thread per call
+    t0 = time.perf_counter()
+    for i in range(f.shape[0]):
+        oracle.scan_match(f[i], g[i], oc, delta, mf[i], mg[i])
+    return time.perf_counter() - t0, "port"
+
+
+# ---------------------------------------------------------------- our arm
+
+def run_ours(args):
+    import torch
+    import paper_2203_00459_b200 as fb
+
+    world, rank, local = dist_setup()
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    cfg, delta, total = fb.baseline_config(args.config)
+    if args.pairs:
+        total = args.pairs
+    from paper_2203_00459_b200.shard import gather_results, shard_range
+    first, per = shard_range(total, world, rank)
+    spec = fb.synth_spec(args.config)
+
+    # inputs: device-rendered shard (pairs first .. first+per)
+    f, g, mf, mg, truth = fb.synth_pairs_device(spec, first, per, device=local)
+    m = fb.Matcher(cfg, max_batch=per, device=local, chunk=args.chunk)
+    out = torch.empty(per * fb.RESULT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    for _ in range(args.warmup):
+        m.match_device(f, g, mf, mg, delta=delta, out=out, stream=stream)
+    torch.cuda.synchronize(dev)
+    launches_per_step = m.launches_last
+    res = fb.decode_results(out)
+    bad = int((res["status"] != 0).sum())
+
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            m.match_device(f, g, mf, mg, delta=delta, out=out, stream=stream)
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+    barrier(world)
+    ms = ev0.elapsed_time(ev1)
+    ms_max = allmax(world, ms, dev)
+    value = total * args.steps / (ms_max / 1e3)
+
+    # pose gather to rank 0 (off the timed region): [total, sizeof(result)] bytes in pair order
+    rows = out.view(per, fb.RESULT_DTYPE.itemsize)
+    gathered = gather_results(rows, total, world, rank)
+    if rank == 0:
+        allres = fb.decode_results(gathered.reshape(-1))
+        bad = int((allres["status"] != 0).sum())
+
+    # per-kernel breakdown: one instrumented step (events around every kernel)
+    m.set_profiling(True)
+    m.match_device(f, g, mf, mg, delta=delta, out=out, stream=stream)
+    torch.cuda.synchronize(dev)
+    kt = m.kernel_times()
+    m.set_profiling(False)
+    dom = max(kt.items(), key=lambda kv: kv[1][0])[0]
+    dom_ms, dom_launches = kt[dom]
+    pairs_per_launch = per / dom_launches
+    alg = kernel_alg_bytes(dom, cfg.n_xy) * pairs_per_launch
+    achieved = alg / (dom_ms / dom_launches / 1e3) / 1e9
+    peak, peak_src = peaks()
+    traffic = ncu_traffic(dom)
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "peak_source": peak_src,
+                "traffic": None if traffic is None else traffic * pairs_per_launch,
+                "alg_bytes_per_launch": alg, "avg_launch_ms": dom_ms / dom_launches,
+                "kernel_share": round(dom_ms / sum(v[0] for v in kt.values()), 3)}
+    bpair = pair_bytes(cfg.n_xy, cfg.n_theta, cfg.pad_angle)
+    pipeline = {"b_pair_bytes": bpair, "achieved_gbs": round(value * bpair / 1e9 / world, 1),
+                "frac_of_measured_peak_per_gpu": round(value * bpair / world / (peak * 1e9), 4),
+                "frac_of_8TBps_per_gpu": round(value * bpair / world / 8e12, 4),
+                "kernel_ms_per_step": {k: round(v[0], 3) for k, v in kt.items()}}
+
+    # e2e through the public host API (H2D + compute + D2H each step)
+    e2e = None
+    if not args.no_e2e:
+        try:
+            import psutil
+            need = 4 * f.numel() * 4 * 1.2
+            if psutil.virtual_memory().available < need + (8 << 30):
+                raise MemoryError("not enough host RAM for pinned inputs")
+            hf, hg, hmf, hmg = (torch.empty(f.shape, dtype=torch.float32, pin_memory=True) for _ in range(4))
+            for h, d in ((hf, f), (hg, g), (hmf, mf), (hmg, mg)):
+                h.copy_(d)
+            nf, ng, nmf, nmg = (h.numpy() for h in (hf, hg, hmf, hmg))
+            m.match_host(nf, ng, nmf, nmg, delta=delta)  # warm
+            steps_e2e = max(1, min(args.steps, 3))
+            barrier(world)
+            t0 = time.perf_counter()
+            for _ in range(steps_e2e):
+                m.match_host(nf, ng, nmf, nmg, delta=delta)
+            dt = allmax(world, time.perf_counter() - t0, dev)
+            e2e = {"value": round(total * steps_e2e / dt, 1), "unit": UNIT,
+                   "h2d_bytes_per_step": int(4 * f.numel() * 4 * world),
+                   "d2h_bytes_per_step": int(total * fb.RESULT_DTYPE.itemsize), "steps": steps_e2e,
+                   "api": "fscan_match_batch_host (pinned host buffers)"}
+            del hf, hg, hmf, hmg
+        except Exception as exc:  # report, never fake
+            e2e = {"value": None, "unit": UNIT, "error": str(exc)[:200]}
+
+    # CPU baseline: the reference on the host cores, bounded sample (rank 0, N=1)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        threads = cpu_threads()
+        sample = int(min(per, max(16, min(2 * threads, 256))))
+        hs = [x[:sample].cpu().numpy() for x in (f, g, mf, mg)]
+        secs, kind = ref_cpu_run(*hs, cfg, delta, threads)
+        cpu = {"value": round(sample / secs, 3), "unit": UNIT, "cores": threads, "kind": kind,
+               "sample": f"first {sample} pairs of the {workload_desc(args.config).split(':')[0]} workload "
+                         f"({secs:.1f} s wall, reference scan_match via parallel_for, FFTW-API shim not FFTW)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 3), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded generator)",
+            "config": {"workload": workload_desc(args.config), "pairs": total, "pairs_per_rank": per,
+                       "n_xy": cfg.n_xy, "n_theta": cfg.n_theta, "chunk": args.chunk or "auto",
+                       "l2": "inputs 16 GiB per pass >> 126 MB L2; no flush needed",
+                       "parallelism": f"dp{world} (pairs sharded by index, no collective on the hot path)"},
+            "roofline": roofline, "hbm_pipeline": pipeline, "cpu_baseline": cpu, "e2e": e2e,
+            "clocks": clk.summary(), "gpu_launches": launches_per_step * args.steps,
+            "bad_pairs": bad, "impl": "ours",
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------- reference arm
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    import paper_2203_00459_b200 as fb  # config + host generator only (no GPU code runs)
+    cfg, delta, total = fb.baseline_config(args.config)
+    threads = cpu_threads()
+    sample = int(max(8, min(threads, 128)))
+    spec = fb.synth_spec(args.config)
+    f, g, mf, mg, _ = fb.synth_pairs_host(spec, 0, sample, threads=threads)
+    kind = "reference" if oracle.have_ref() else "port"
+    for _ in range(args.warmup):
+        ref_cpu_run(f[:threads], g[:threads], mf[:threads], mg[:threads], cfg, delta, threads)
+    secs = []
+    for _ in range(args.steps):
+        s, kind = ref_cpu_run(f, g, mf, mg, cfg, delta, threads)
+        secs.append(s)
+    tot = sum(secs)
+    value = sample * args.steps / tot
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(1e3 * tot / args.steps, 1), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator)",
+        "config": {"workload": workload_desc(args.config), "pairs_per_step": sample, "n_xy": cfg.n_xy,
+                   "n_theta": cfg.n_theta},
+        "impl": "reference",
+        "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": f"{sample} pairs of the workload per step, reference scan_match via "
+                                   f"parallel_for on {threads} threads (FFTW-API shim, not FFTW)"},
+        "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", type=int, default=4, choices=(1, 2, 3, 4, 5))
+    ap.add_argument("--pairs", type=int, default=0, help="override the config's pair count")
+    ap.add_argument("--chunk", type=int, default=0, help="pairs per pipeline chunk (0 = auto)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -140,6 +140,14 @@ fscan_status fscan_check_results(const fscan_pair_result* d_out, int batch, void
 /* Number of kernels the last fscan_match_batch launched (for bench accounting). */
 int fscan_ctx_launches_last(const fscan_ctx* ctx);
 
+/* Profiling mode: subsequent calls run their chunks serially on one stream
+ * with CUDA events around every kernel. fscan_ctx_kernel_times() synchronises
+ * and returns, per kernel kind (0 rot_rows, 1 rot_cols, 2 rot_polar,
+ * 3 theta_in, 4 xlat_rows, 5 xlat_cols, 6 xlat_out, 7 finalize, 8 mag_unpack),
+ * the summed milliseconds and launch counts of the last call. */
+fscan_status fscan_ctx_set_profiling(fscan_ctx* ctx, int on);
+fscan_status fscan_ctx_kernel_times(fscan_ctx* ctx, double* ms, int* launches, int n_kinds);
+
 #ifdef __cplusplus
 }
 #endif

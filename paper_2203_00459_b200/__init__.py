@@ -112,6 +112,8 @@ SYMBOLS = {
                                             C.c_double, _P, _P]),
     "fscan_check_results": (C.c_int, [_P, C.c_int, _P, C.POINTER(C.c_int)]),
     "fscan_ctx_launches_last": (C.c_int, [_P]),
+    "fscan_ctx_set_profiling": (C.c_int, [_P, C.c_int]),
+    "fscan_ctx_kernel_times": (C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_int), C.c_int]),
     "fscan_synth_preset": (C.c_int, [C.c_int, C.POINTER(CSynthSpec)]),
     "fscan_synth_pairs_host": (C.c_int, [C.POINTER(CSynthSpec), C.c_int, C.c_int, _P, _P, _P, _P, _P,
                                          C.c_int]),
@@ -263,6 +265,20 @@ class Matcher:
     @property
     def launches_last(self) -> int:
         return lib().fscan_ctx_launches_last(self._h)
+
+    KERNELS = ("rot_rows", "rot_cols", "rot_polar", "theta_in", "xlat_rows", "xlat_cols", "xlat_out",
+               "finalize", "mag_unpack")
+
+    def set_profiling(self, on: bool):
+        self._check(lib().fscan_ctx_set_profiling(self._h, int(bool(on))), "set_profiling")
+
+    def kernel_times(self) -> dict:
+        """{kernel: (total_ms, launches)} of the last call made in profiling mode."""
+        k = len(self.KERNELS)
+        ms = (C.c_double * k)()
+        cnt = (C.c_int * k)()
+        self._check(lib().fscan_ctx_kernel_times(self._h, ms, cnt, k), "kernel_times")
+        return {name: (ms[i], cnt[i]) for i, name in enumerate(self.KERNELS) if cnt[i]}
 
     def match_device(self, f, g, mf=None, mg=None, *, delta: float, out=None, theta_surface=None,
                      xy_surface=None, stream=None):

@@ -61,6 +61,11 @@ struct fscan_ctx {
     PolarTap* taps = nullptr;
     Lane lanes[kLanes];
     cudaEvent_t start_ev = nullptr;
+    // profiling: per-kernel events of the last call, serialised on lane 0
+    int profiling = 0;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
 };
 
 namespace {
@@ -249,38 +254,67 @@ Params base_params(fscan_ctx* ctx, Lane& l, int batch, double delta) {
 
 enum class Stages { Full, Rotation, Translation, Magnitude };
 
+// Kernel ids for per-kernel profiling (fscan_ctx_kernel_times).
+enum KernelId { kRotRows = 0, kRotCols, kRotPolar, kThetaIn, kXlatRows, kXlatCols, kXlatOut, kFinalize,
+                kMagUnpack, kNumKernels };
+
+struct ProfEvent {
+    int kid;
+    cudaEvent_t a, b;
+};
+
+// Launch one stage; in profiling mode bracket it with events on its stream.
+template <typename L>
+fscan_status launch(fscan_ctx* ctx, Lane& l, int kid, L&& fn, int* launches);
+
 // Launch the pipeline for one chunk on lane l. Inputs are device pointers.
 fscan_status run_chunk(fscan_ctx* ctx, Lane& l, Params p, Stages what, int* launches) {
     cudaStream_t s = l.stream;
     CK(cudaMemsetAsync(l.flags, 0, sizeof(int) * p.batch, s));
-    int k = 0;
-    CK(launch_rot_rows(p, s));
-    ++k;
+    fscan_status st;
+#define FSCAN_LAUNCH(kid, call)                                                              \
+    if ((st = launch(ctx, l, kid, [&] { return call(p, s); }, launches)) != FSCAN_OK) return st;
+    FSCAN_LAUNCH(kRotRows, launch_rot_rows);
     if (what == Stages::Magnitude) {
-        CK(launch_rot_cols(p, s));
-        CK(launch_mag_unpack(p, s));
-        *launches += k + 2;
+        FSCAN_LAUNCH(kRotCols, launch_rot_cols);
+        FSCAN_LAUNCH(kMagUnpack, launch_mag_unpack);
         return FSCAN_OK;
     }
     if (what != Stages::Translation) {
-        if (ctx->cfg.n_theta > 1) {
-            CK(launch_rot_cols(p, s));
-            ++k;
-        }
-        CK(launch_rot_polar(p, s));
-        ++k;
+        if (ctx->cfg.n_theta > 1) FSCAN_LAUNCH(kRotCols, launch_rot_cols);
+        FSCAN_LAUNCH(kRotPolar, launch_rot_polar);
     } else {
-        CK(launch_theta_in(p, s));
-        ++k;
+        FSCAN_LAUNCH(kThetaIn, launch_theta_in);
     }
     if (what != Stages::Rotation) {
-        CK(launch_xlat_rows(p, s));
-        CK(launch_xlat_cols(p, s));
-        CK(launch_xlat_out(p, s));
-        CK(launch_finalize(p, s));
-        k += 4;
+        FSCAN_LAUNCH(kXlatRows, launch_xlat_rows);
+        FSCAN_LAUNCH(kXlatCols, launch_xlat_cols);
+        FSCAN_LAUNCH(kXlatOut, launch_xlat_out);
+        FSCAN_LAUNCH(kFinalize, launch_finalize);
     }
-    *launches += k;
+#undef FSCAN_LAUNCH
+    return FSCAN_OK;
+}
+
+template <typename L>
+fscan_status launch(fscan_ctx* ctx, Lane& l, int kid, L&& fn, int* launches) {
+    cudaEvent_t a = nullptr, b = nullptr;
+    if (ctx->profiling) {
+        while (ctx->ev_pool.size() < ctx->ev_used + 2) {
+            cudaEvent_t e;
+            CK(cudaEventCreate(&e));
+            ctx->ev_pool.push_back(e);
+        }
+        a = ctx->ev_pool[ctx->ev_used++];
+        b = ctx->ev_pool[ctx->ev_used++];
+        CK(cudaEventRecord(a, l.stream));
+    }
+    CK(fn());
+    if (ctx->profiling) {
+        CK(cudaEventRecord(b, l.stream));
+        ctx->prof.push_back({kid, {a, b}});
+    }
+    ++*launches;
     return FSCAN_OK;
 }
 
@@ -300,8 +334,11 @@ fscan_status drive(fscan_ctx* ctx, int batch, cudaStream_t user, F&& per_chunk) 
     CK(cudaEventRecord(ctx->start_ev, user));
     for (auto& l : ctx->lanes) CK(cudaStreamWaitEvent(l.stream, ctx->start_ev, 0));
     ctx->launches_last = 0;
+    ctx->prof.clear();
+    ctx->ev_used = 0;
+    const int lanes = ctx->profiling ? 1 : kLanes;
     int li = 0;
-    for (int off = 0; off < batch; off += ctx->chunk, li = (li + 1) % kLanes) {
+    for (int off = 0; off < batch; off += ctx->chunk, li = (li + 1) % lanes) {
         const int cnt = std::min(ctx->chunk, batch - off);
         fscan_status st = per_chunk(ctx->lanes[li], off, cnt);
         if (st != FSCAN_OK) return st;
@@ -450,6 +487,7 @@ void fscan_ctx_destroy(fscan_ctx* ctx) {
         if (l.done) cudaEventDestroy(l.done);
     }
     if (ctx->start_ev) cudaEventDestroy(ctx->start_ev);
+    for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
     cudaFree(ctx->tw_n);
     cudaFree(ctx->tw_2n);
     cudaFree(ctx->hann);
@@ -628,6 +666,32 @@ fscan_status fscan_match_batch_host(fscan_ctx* ctx, const float* f, const float*
                         bad == FSCAN_ERR_MASK_RANGE ? "MaskGrid: values must lie in [0, 1]"
                                                     : "scan_match: input grids contain non-finite values");
         }
+    return FSCAN_OK;
+}
+
+fscan_status fscan_ctx_set_profiling(fscan_ctx* ctx, int on) {
+    if (!ctx) return FSCAN_ERR_INVALID_ARGUMENT;
+    std::lock_guard<std::mutex> g(ctx->mu);
+    ctx->profiling = on ? 1 : 0;
+    return FSCAN_OK;
+}
+
+fscan_status fscan_ctx_kernel_times(fscan_ctx* ctx, double* ms, int* launches, int n_kinds) {
+    if (!ctx || !ms || !launches) return FSCAN_ERR_INVALID_ARGUMENT;
+    std::lock_guard<std::mutex> g(ctx->mu);
+    for (int k = 0; k < n_kinds; ++k) {
+        ms[k] = 0.0;
+        launches[k] = 0;
+    }
+    for (auto& e : ctx->prof) {
+        CK(cudaEventSynchronize(e.second.second));
+        float t = 0.f;
+        CK(cudaEventElapsedTime(&t, e.second.first, e.second.second));
+        if (e.first < n_kinds) {
+            ms[e.first] += t;
+            launches[e.first] += 1;
+        }
+    }
     return FSCAN_OK;
 }
 

@@ -1,0 +1,267 @@
+// Reference-style tests of the C++ drop-in API (include/fscan/matcher.hpp) on
+// the B200. The cases follow proj/tests/test_matcher.cpp (cited per case),
+// rewritten without doctest and with even grid sizes; scenes are
+// Gaussian blobs rendered analytically so rotations/shifts are exact.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <limits>
+#include <stdexcept>
+#include <vector>
+
+#include "fscan/matcher.hpp"
+
+using namespace fscan;
+
+static int g_fail = 0, g_checks = 0;
+#define CHECK(cond)                                                                   \
+    do {                                                                              \
+        ++g_checks;                                                                   \
+        if (!(cond)) {                                                                \
+            ++g_fail;                                                                 \
+            std::printf("FAIL %s:%d  %s\n", __FILE__, __LINE__, #cond);               \
+        }                                                                             \
+    } while (0)
+#define CHECK_THROWS_AS(expr, T)                                                      \
+    do {                                                                              \
+        bool caught_ = false;                                                         \
+        try {                                                                         \
+            (void)(expr);                                                             \
+        } catch (const T&) {                                                          \
+            caught_ = true;                                                           \
+        } catch (...) {                                                               \
+        }                                                                             \
+        CHECK(caught_);                                                               \
+    } while (0)
+
+namespace {
+
+struct Blob {
+    double x, y, s, a;
+};
+
+std::vector<Blob> scene(int n, double delta, unsigned seed, int count) {
+    std::vector<Blob> b;
+    unsigned long long st = seed * 2654435761ull + 1;
+    auto u = [&] {
+        st = st * 6364136223846793005ull + 1442695040888963407ull;
+        return (double)(st >> 11) * 0x1.0p-53;
+    };
+    const double he = 0.35 * n * delta;
+    for (int i = 0; i < count; ++i) b.push_back({(2 * u() - 1) * he, (2 * u() - 1) * he, (1.5 + 1.5 * u()) * delta, 0.3 + 0.7 * u()});
+    return b;
+}
+
+// Render the scene seen after pose p (objects at R(theta) q + t), GridSpec world convention.
+ScanGrid render(const std::vector<Blob>& bs, const GridSpec& spec, const Pose2D& p) {
+    ScanGrid g = ScanGrid::zeros(spec);
+    const double c = std::cos(p.theta), s = std::sin(p.theta);
+    for (int r = 0; r < spec.n; ++r)
+        for (int col = 0; col < spec.n; ++col) {
+            const Vec2 w = spec.cell_center(r, col);
+            double v = 0.0;
+            for (const Blob& b : bs) {
+                const double bx = c * b.x - s * b.y + p.tx, by = s * b.x + c * b.y + p.ty;
+                const double d2 = (w.x - bx) * (w.x - bx) + (w.y - by) * (w.y - by);
+                v += b.a * std::exp(-d2 / (2 * b.s * b.s));
+            }
+            g.values(r, col) = v;
+        }
+    return g;
+}
+
+MatchConfig small_cfg(int n, double delta, int n_theta) {  // test_matcher.cpp:18-31
+    MatchConfig cfg;
+    cfg.n_xy = n;
+    cfg.delta_xy = delta;
+    cfg.n_theta = n_theta;
+    cfg.delta_theta = kPi / n_theta;
+    cfg.n_radius = 0;
+    cfg.pad_angle = -1;
+    cfg.band_lo = 0.15;
+    finalize(cfg);
+    validate(cfg);
+    return cfg;
+}
+
+CorrelationSurface surface_from(const Array2D& scores) {
+    CorrelationSurface s;
+    s.scores = scores;
+    for (std::size_t r = 0; r < scores.rows(); ++r) s.row_coords.push_back(r - scores.rows() / 2.0);
+    for (std::size_t c = 0; c < scores.cols(); ++c) s.col_coords.push_back(c - scores.cols() / 2.0);
+    return s;
+}
+
+}  // namespace
+
+int main() {
+    // config validation and derived defaults (test_matcher.cpp:60-103)
+    {
+        MatchConfig cfg;
+        validate(cfg);
+        CHECK(cfg.n_radius == 128 && cfg.pad_angle == 92);
+        MatchConfig d;
+        d.n_xy = 65;
+        d.n_theta = 100;
+        d.delta_theta = kPi / 100.0;
+        d.n_radius = 0;
+        d.pad_angle = -1;
+        finalize(d);
+        CHECK(d.n_radius == 33 && d.pad_angle == 13);
+        MatchConfig bad = small_cfg(64, 0.4, 129);
+        bad.band_lo = 0.8;
+        CHECK_THROWS_AS(validate(bad), std::invalid_argument);
+        bad = small_cfg(64, 0.4, 129);
+        bad.delta_theta = kPi / 64.0;
+        CHECK_THROWS_AS(validate(bad), std::invalid_argument);
+        bad = small_cfg(64, 0.4, 129);
+        bad.pad_angle = 129;
+        CHECK_THROWS_AS(validate(bad), std::invalid_argument);
+        bad = small_cfg(64, 0.4, 129);
+        bad.softargmax_window = 0;
+        CHECK_THROWS_AS(validate(bad), std::invalid_argument);
+    }
+    // soft_argmax contracts (test_matcher.cpp:105-206)
+    {
+        Array2D s(9, 9, 0.0);
+        s(2, 6) = 5.0;
+        const auto [r, c] = soft_argmax(surface_from(s), 50.0, 2, true);
+        CHECK(std::abs(r - (2.0 - 4.5)) < 1e-6 && std::abs(c - (6.0 - 4.5)) < 1e-6);
+        Array2D e(5, 5, 1.0);
+        const auto [r2, c2] = soft_argmax(surface_from(e), 2.0, 16, true);
+        CHECK(std::abs(r2 + 0.5) < 1e-9 && std::abs(c2 + 0.5) < 1e-9);
+    }
+    const int n = 64;
+    const double delta = 0.4;
+    const GridSpec spec{n, delta};
+    const MatchConfig cfg = small_cfg(n, delta, 129);
+    // estimate_rotation: identical grids give zero (test_matcher.cpp:210-220)
+    {
+        const ScanGrid f = render(scene(n, delta, 21, 14), spec, Pose2D::identity());
+        const auto [theta, surface] = estimate_rotation(f, f, cfg);
+        CHECK(std::abs(theta) < 1e-3);
+        CHECK(surface.scores.rows() == 129 && surface.scores.cols() == 1);
+        CHECK(std::abs(surface.row_coords[64]) < 1e-12);
+        CHECK(std::abs(surface.row_coords[65] - surface.row_coords[64] - cfg.delta_theta) < 1e-12);
+    }
+    // estimate_rotation recovers a known rotation (test_matcher.cpp:222-232)
+    {
+        const auto bs = scene(n, delta, 33, 14);
+        const ScanGrid f = render(bs, spec, Pose2D::identity());
+        for (const double beta : {0.30, -0.22, 0.55}) {
+            const ScanGrid g = render(bs, spec, Pose2D{beta, 0.0, 0.0});
+            const auto [theta, s] = estimate_rotation(f, g, cfg);
+            CHECK(std::abs(theta - beta) <= 2.0 * cfg.delta_theta);
+        }
+    }
+    // estimate_rotation rejects mismatched inputs (test_matcher.cpp:263-271)
+    {
+        const ScanGrid f = ScanGrid::zeros(spec);
+        const ScanGrid g = ScanGrid::zeros(GridSpec{n, 0.5});
+        CHECK_THROWS_AS(estimate_rotation(f, g, cfg), std::invalid_argument);
+        const ScanGrid h = ScanGrid::zeros(GridSpec{32, delta});
+        CHECK_THROWS_AS(estimate_rotation(h, h, cfg), std::invalid_argument);
+    }
+    // estimate_translation pins an integer cell shift (test_matcher.cpp:290-300)
+    {
+        const auto bs = scene(n, delta, 13, 14);
+        const ScanGrid f = render(bs, spec, Pose2D::identity());
+        const ScanGrid g = render(bs, spec, Pose2D{0.0, 5 * delta, 3 * delta});
+        const auto [t, s] = estimate_translation(f, g, 0.0, cfg);
+        CHECK(std::abs(t.x - 5 * delta) < 0.25 * delta);
+        CHECK(std::abs(t.y - 3 * delta) < 0.25 * delta);
+        CHECK(s.scores.rows() == (std::size_t)n && s.row_coords[n / 2] > s.row_coords[n / 2 - 1]);
+    }
+    // scan_match recovers a rigid motion at C1 scale (test_matcher.cpp:331-347)
+    {
+        const int N = 256;
+        const GridSpec sp{N, 0.5};
+        MatchConfig c;
+        c.n_xy = N;
+        c.delta_xy = 0.5;
+        c.n_theta = 360;
+        c.delta_theta = kPi / 360;
+        c.n_radius = 0;
+        c.pad_angle = -1;
+        finalize(c);
+        const auto bs = scene(N, 0.5, 99, 60);
+        const Pose2D rel{0.05, 3.2, -1.6};
+        const ScanGrid f = render(bs, sp, Pose2D::identity());
+        const ScanGrid g = render(bs, sp, rel);
+        const MatchResult r = scan_match(f, g, c);
+        CHECK(std::abs(normalize_angle(r.pose.theta - rel.theta)) <= 2.0 * c.delta_theta);
+        CHECK(std::abs(r.pose.tx - rel.tx) <= sp.delta);
+        CHECK(std::abs(r.pose.ty - rel.ty) <= sp.delta);
+        CHECK(r.diagnostics.theta_peak >= r.theta_surface.scores(c.n_theta / 2, 0));
+        CHECK(std::abs(r.diagnostics.theta_hard - rel.theta) <= 2.0 * c.delta_theta);
+        // scan_match(f, g) inverts scan_match(g, f) (test_matcher.cpp:349-360)
+        const Pose2D rev = inverse(scan_match(g, f, c).pose);
+        CHECK(std::abs(normalize_angle(r.pose.theta - rev.theta)) <= 4.0 * c.delta_theta);
+        CHECK(std::abs(r.pose.tx - rev.tx) <= sp.delta && std::abs(r.pose.ty - rev.ty) <= sp.delta);
+    }
+    // scan_match rejects non-finite input (test_matcher.cpp:362-372)
+    {
+        ScanGrid f = ScanGrid::zeros(spec), g = ScanGrid::zeros(spec);
+        f.values(3, 3) = std::nan("");
+        CHECK_THROWS_AS(scan_match(f, g, cfg), std::invalid_argument);
+        f.values(3, 3) = 0.0;
+        g.values(1, 1) = std::numeric_limits<double>::infinity();
+        CHECK_THROWS_AS(scan_match(f, g, cfg), std::invalid_argument);
+    }
+    // masked scan_match equals matching the masked grids (test_matcher.cpp:374-387)
+    {
+        const auto bs = scene(n, delta, 55, 14);
+        const ScanGrid f = render(bs, spec, Pose2D::identity());
+        const ScanGrid g = render(bs, spec, Pose2D{0.1, 0.8, -0.4});
+        Array2D mv(n, n, 1.0);
+        for (int j = 0; j < n; ++j) mv(30, j) = 0.0;
+        const MaskGrid m(spec, mv);
+        ScanGrid fm = f, gm = g;
+        for (int j = 0; j < n; ++j) fm.values(30, j) = gm.values(30, j) = 0.0;
+        const Pose2D a = scan_match(f, g, cfg, m, m).pose;
+        const Pose2D b = scan_match(fm, gm, cfg).pose;
+        CHECK(a.theta == b.theta && a.tx == b.tx && a.ty == b.ty);
+        Array2D badv(n, n, 1.0);
+        badv(0, 0) = 1.5;
+        CHECK_THROWS_AS(MaskGrid(spec, badv), std::invalid_argument);
+    }
+    // GPU-path limits are reported, not silently handled: odd n is unsupported here
+    {
+        MatchConfig c = small_cfg(65, delta, 129);
+        const GridSpec s65{65, delta};
+        const ScanGrid f = ScanGrid::zeros(s65);
+        CHECK_THROWS_AS(scan_match(f, f, c), std::runtime_error);
+    }
+    // batched extension on device pointers
+    {
+        const auto bs = scene(n, delta, 7, 14);
+        std::vector<float> hf(3 * n * n), hg(3 * n * n);
+        const double thetas[3] = {0.0, 0.2, -0.3};
+        for (int k = 0; k < 3; ++k) {
+            const ScanGrid f = render(bs, spec, Pose2D::identity());
+            const ScanGrid g = render(bs, spec, Pose2D{thetas[k], 0.4, -0.8});
+            for (int i = 0; i < n * n; ++i) {
+                hf[k * n * n + i] = (float)f.values[i];
+                hg[k * n * n + i] = (float)g.values[i];
+            }
+        }
+        float *df = nullptr, *dg = nullptr;
+        cudaMalloc(&df, sizeof(float) * hf.size());
+        cudaMalloc(&dg, sizeof(float) * hg.size());
+        cudaMemcpy(df, hf.data(), sizeof(float) * hf.size(), cudaMemcpyHostToDevice);
+        cudaMemcpy(dg, hg.data(), sizeof(float) * hg.size(), cudaMemcpyHostToDevice);
+        std::vector<Pose2D> poses;
+        std::vector<PairDiagnostics> diags;
+        scan_match_batch(df, dg, nullptr, nullptr, 3, delta, cfg, poses, &diags);
+        for (int k = 0; k < 3; ++k) {
+            CHECK(std::abs(poses[k].theta - thetas[k]) <= 2.0 * cfg.delta_theta);
+            CHECK(std::abs(poses[k].tx - 0.4) <= delta && std::abs(poses[k].ty + 0.8) <= delta);
+        }
+        cudaFree(df);
+        cudaFree(dg);
+    }
+    std::printf("%d checks, %d failed\n", g_checks, g_fail);
+    if (g_fail == 0) std::printf("ALL PASSED\n");
+    return g_fail == 0 ? 0 : 1;
+}

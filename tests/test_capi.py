@@ -1,0 +1,108 @@
+"""C ABI + host logic without a GPU: the library loads, exports every symbol the
+headers declare, and the config semantics mirror matcher.cpp:11-37."""
+import ctypes as C
+import math
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_functions(header):
+    text = open(os.path.join(ROOT, "include", header)).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(fscan_[a-z0-9_]+)\s*\(", text)))
+
+
+@pytest.mark.parametrize("header", ["fscan_cuda.h", "fscan_synth.h"])
+def test_library_exports_every_declared_symbol(fb, header):
+    names = declared_functions(header)
+    assert len(names) >= 5
+    lib = C.CDLL(fb.LIB_PATH)
+    missing = [n for n in names if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+def test_python_binding_covers_the_header(fb):
+    names = set(declared_functions("fscan_cuda.h")) | set(declared_functions("fscan_synth.h"))
+    assert names <= set(fb.SYMBOLS), names - set(fb.SYMBOLS)
+
+
+def test_drop_in_cpp_symbols_exported(fb):
+    import subprocess
+    out = subprocess.run(["nm", "-DC", fb.LIB_PATH], capture_output=True, text=True).stdout
+    for sym in ("fscan::scan_match(fscan::ScanGrid const&, fscan::ScanGrid const&, fscan::MatchConfig const&)",
+                "fscan::estimate_rotation(", "fscan::estimate_translation(", "fscan::soft_argmax(",
+                "fscan::finalize(fscan::MatchConfig&)", "fscan::validate(fscan::MatchConfig const&)",
+                "fscan::scan_match_batch("):
+        assert sym in out, sym
+
+
+def test_built_for_sm100a(fb):
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", fb.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_config_defaults_finalize_validate(fb):  # test_matcher.cpp:60-103
+    cfg = fb.MatchConfig()
+    cfg.validate()
+    assert (cfg.n_radius, cfg.pad_angle) == (128, 92)
+    d = fb.MatchConfig(n_xy=65, n_theta=100, delta_theta=math.pi / 100, n_radius=0, pad_angle=-1).finalize()
+    assert (d.n_radius, d.pad_angle) == (33, 13)
+    t = fb.MatchConfig(n_theta=2, delta_theta=0.01, pad_angle=-1).finalize()
+    assert t.pad_angle == 1
+    base = dict(n_xy=65, delta_xy=0.4, n_theta=129, delta_theta=math.pi / 129, n_radius=33, pad_angle=17,
+                band_lo=0.15)
+    for kw in (dict(band_lo=0.8), dict(delta_theta=math.pi / 64.0), dict(pad_angle=129),
+               dict(softargmax_window=0), dict(t_theta=0.0), dict(t_xy=-1.0), dict(n_xy=2),
+               dict(delta_xy=0.0), dict(n_radius=1), dict(n_theta=0)):
+        with pytest.raises(fb.FscanInvalidArgument):
+            fb.MatchConfig(**{**base, **kw}).validate()
+    fb.MatchConfig(**{**base, "n_xy": 64}).validate()  # D1: even n accepted
+
+
+def test_baseline_configs_resolve(fb):
+    c1, d1, b1 = fb.baseline_config(1)
+    assert (c1.n_xy, c1.n_theta, c1.pad_angle, c1.n_radius, d1, b1) == (256, 360, 45, 128, 0.5, 1)
+    c4, d4, b4 = fb.baseline_config(4)
+    assert (c4.n_xy, c4.n_theta, c4.pad_angle, c4.n_radius, d4, b4, c4.t_theta) == (512, 720, 90, 256, 0.25, 4096, 1.0)
+    c5, d5, b5 = fb.baseline_config(5)
+    assert (c5.n_xy, c5.n_theta, c5.pad_angle, c5.n_radius, c5.t_xy) == (1024, 1440, 180, 512, 0.5)
+
+
+def test_context_without_gpu_fails_loudly(fb):
+    """No CPU fallback: on a GPU-less host every compute entry point errors."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("this host has a GPU")
+    cfg, _, _ = fb.baseline_config(2)
+    with pytest.raises(fb.FscanError) as ei:
+        fb.Matcher(cfg, max_batch=1)
+    assert ei.value.status in (fb.ERR_NO_DEVICE, fb.ERR_CUDA)
+
+
+def test_unsupported_grid_sizes_are_rejected(fb):
+    cfg = fb.MatchConfig.for_grid(255, 0.4, 733)  # the reference's own default (odd n)
+    with pytest.raises(fb.FscanError) as ei:
+        fb.Matcher(cfg, max_batch=1)
+    assert ei.value.status == fb.ERR_UNSUPPORTED
+
+
+def test_result_struct_layout(fb):
+    assert C.sizeof(fb.CPairResult) == 80 == fb.RESULT_DTYPE.itemsize
+    assert C.sizeof(fb.CConfig) == 80  # int32/double layout of fscan_config (x86-64 SysV)
+
+
+def test_shard_ranges_cover_and_partition():
+    from paper_2203_00459_b200.shard import shard_range
+    for total in (0, 1, 7, 64, 4096, 1023):
+        for world in (1, 2, 3, 4, 8):
+            spans = [shard_range(total, world, r) for r in range(world)]
+            assert spans[0][0] == 0
+            assert sum(c for _, c in spans) == total
+            for (f0, c0), (f1, _) in zip(spans, spans[1:]):
+                assert f0 + c0 == f1
+            assert max(c for _, c in spans) - min(c for _, c in spans) <= 1

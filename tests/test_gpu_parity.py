@@ -1,0 +1,317 @@
+"""GPU parity: the sm_100a path through the C ABI against the CPU oracle on the
+same seeded fp32 inputs, against golden vectors produced by the reference's own
+code, and through size-independent properties at full BASELINE sizes.
+
+Tolerances (BASELINE.json north_star):
+  * integer theta bin and translation cell bit-exact, except documented near-ties
+    (oracle top-2 gap below 4x the observed surface error);
+  * surfaces within 1e-4 of max|ref|;
+  * soft pose within 1e-3 rad and 1e-2 px.
+"""
+import glob
+import math
+import os
+import subprocess
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import ROOT, oracle_cfg
+
+pytestmark = pytest.mark.gpu
+
+SURF_TOL = 1e-4
+THETA_TOL = 1e-3
+PX_TOL = 1e-2
+
+
+@pytest.fixture(scope="module")
+def dev():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device (no CPU fallback exists)"
+    return torch.device("cuda", 0)
+
+
+def to_dev(dev, *arrs):
+    return [None if a is None else torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(dev)
+            for a in arrs]
+
+
+def run_gpu(fb, dev, cfg, delta, f, g, mf=None, mg=None, chunk=0):
+    b, n = f.shape[0], f.shape[1]
+    F, G, MF, MG = to_dev(dev, f, g, mf, mg)
+    m = fb.Matcher(cfg, max_batch=b, chunk=chunk)
+    ts = torch.zeros((b, max(1, cfg.n_theta)), dtype=torch.float64, device=dev)
+    xs = torch.zeros((b, n, n), dtype=torch.float32, device=dev)
+    out = m.match_device(F, G, MF, MG, delta=delta, theta_surface=ts, xy_surface=xs)
+    torch.cuda.synchronize()
+    return fb.decode_results(out), ts.cpu().numpy(), xs.cpu().numpy()
+
+
+def compare(res, ts, xs, ref_bins, ref_pose, ref_ts, ref_xs, delta, stats):
+    """One pair: returns True when it was a documented near-tie."""
+    tsd = np.abs(ts - ref_ts).max() / np.abs(ref_ts).max()
+    xsd = np.abs(xs - ref_xs).max() / np.abs(ref_xs).max()
+    assert tsd <= SURF_TOL, tsd
+    assert xsd <= SURF_TOL, xsd
+    stats.append((tsd, xsd))
+    tb, tr, tc = (int(x) for x in ref_bins)
+    near = False
+    if res["theta_bin"] != tb:
+        gap = (ref_ts[tb] - ref_ts[res["theta_bin"]]) / np.abs(ref_ts).max()
+        assert gap < 4 * tsd + 1e-12, f"theta bin {res['theta_bin']} vs {tb}, gap {gap:.3e} > 4*err {tsd:.3e}"
+        near = True
+    if (res["xy_row"], res["xy_col"]) != (tr, tc):
+        gap = (ref_xs[tr, tc] - ref_xs[res["xy_row"], res["xy_col"]]) / np.abs(ref_xs).max()
+        assert near or gap < 4 * xsd + 1e-12, f"xy cell mismatch, gap {gap:.3e}"
+        near = True
+    if not near:
+        assert abs(res["theta"] - ref_pose[0]) <= THETA_TOL
+        assert abs(res["tx"] - ref_pose[1]) <= PX_TOL * delta
+        assert abs(res["ty"] - ref_pose[2]) <= PX_TOL * delta
+    assert res["status"] == 0
+    return near
+
+
+# ---------------------------------------------------------------- stage 1
+
+@pytest.mark.parametrize("n", [64, 128, 256, 512, 1024])
+def test_band_magnitude_matches_oracle(fb, orc, dev, n):
+    rng = np.random.default_rng(n)
+    img = rng.random((2, n, n)).astype(np.float32)
+    cfg = fb.MatchConfig.for_grid(n, 0.5, 90)
+    m = fb.Matcher(cfg, max_batch=2)
+    (I,) = to_dev(dev, img)
+    got = m.band_magnitude(I).cpu().numpy()
+    for i in range(2):
+        ref = orc.band_magnitude(img[i].astype(np.float64), cfg.band_lo, cfg.band_hi)[:, n // 2:]
+        assert np.abs(got[i] - ref).max() <= 1e-5 * np.abs(ref).max()
+        assert np.all(got[i][ref == 0.0] == 0.0)  # identical band support
+
+
+# ---------------------------------------------------------------- full pipeline vs oracle
+
+@pytest.mark.parametrize("cid,count", [(1, 1), (2, 8), (4, 3), (5, 1)])
+def test_scan_match_matches_oracle_baseline_configs(fb, orc, dev, cid, count):
+    cfg, delta, _ = fb.baseline_config(cid)
+    spec = fb.synth_spec(cid)
+    f, g, mf, mg, _ = fb.synth_pairs_host(spec, 7, count)
+    if cid == 1:
+        mf = mg = None
+    res, ts, xs = run_gpu(fb, dev, cfg, delta, f, g, mf, mg)
+    oc = oracle_cfg(orc, cfg)
+    stats, near = [], 0
+    for i in range(count):
+        r = orc.scan_match(f[i], g[i], oc, delta, None if mf is None else mf[i], None if mg is None else mg[i])
+        near += compare(res[i], ts[i], xs[i], (r.theta_bin, r.xy_row, r.xy_col), (r.theta, r.tx, r.ty),
+                        r.theta_surface, r.xy_surface, delta, stats)
+    assert near <= max(1, count // 8)
+
+
+@pytest.mark.parametrize("n,nt", [(64, 90), (128, 180), (256, 45)])
+def test_scan_match_small_grids_and_odd_bin_counts(fb, orc, dev, n, nt):
+    spec = fb.synth_spec(2, n=n, delta=0.5 * 256 / n)
+    cfg = fb.MatchConfig.for_grid(n, spec.delta, nt, t_theta=2.0, t_xy=1.0)
+    f, g, mf, mg, _ = fb.synth_pairs_host(spec, 3, 4)
+    res, ts, xs = run_gpu(fb, dev, cfg, spec.delta, f, g, mf, mg)
+    oc = oracle_cfg(orc, cfg)
+    stats = []
+    for i in range(4):
+        r = orc.scan_match(f[i], g[i], oc, spec.delta, mf[i], mg[i])
+        compare(res[i], ts[i], xs[i], (r.theta_bin, r.xy_row, r.xy_col), (r.theta, r.tx, r.ty), r.theta_surface,
+                r.xy_surface, spec.delta, stats)
+
+
+GOLDEN = sorted(glob.glob(os.path.join(ROOT, "tests", "golden", "*.npz")))
+CFG_KEYS = ("n_theta", "delta_theta", "t_theta", "n_xy", "delta_xy", "t_xy", "band_lo", "band_hi", "n_radius",
+            "pad_angle", "softargmax_window", "normalize_scores")
+
+
+@pytest.mark.parametrize("path", GOLDEN, ids=[os.path.basename(p) for p in GOLDEN])
+def test_golden_vectors_from_the_reference(fb, dev, path):
+    z = np.load(path)
+    vals = dict(zip(CFG_KEYS, z["cfg"]))
+    ints = ("n_theta", "n_xy", "n_radius", "pad_angle", "softargmax_window")
+    cfg = fb.MatchConfig(**{k: (int(v) if k in ints else (bool(v) if k == "normalize_scores" else float(v)))
+                            for k, v in vals.items()})
+    delta = float(z["delta"])
+    mf = z["mf"] if "mf" in z else None
+    mg = z["mg"] if "mg" in z else None
+    res, ts, xs = run_gpu(fb, dev, cfg, delta, z["f"], z["g"], mf, mg)
+    stats = []
+    for i in range(z["f"].shape[0]):
+        compare(res[i], ts[i], xs[i], z["bins"][i], z["pose"][i], z["theta_surface"][i],
+                z["xy_surface"][i].astype(np.float64), delta, stats)
+        np.testing.assert_allclose([res[i]["theta_hard"], res[i]["xy_hard_x"], res[i]["xy_hard_y"]],
+                                   [z["diag"][i][0], z["diag"][i][2], z["diag"][i][3]], atol=1e-9)
+        assert abs(res[i]["theta_peak"] - z["diag"][i][1]) <= SURF_TOL * abs(z["diag"][i][1])
+        assert abs(res[i]["xy_peak"] - z["diag"][i][4]) <= SURF_TOL * abs(z["diag"][i][4])
+
+
+# ---------------------------------------------------------------- config 3: raw polar sweeps (K0)
+
+def test_polar_to_cart_and_c3_pipeline(fb, orc, dev):
+    cfg, delta, _ = fb.baseline_config(3)
+    spec = fb.synth_spec(3)
+    pf, pg, _ = fb.synth_polar_host(spec, 0, 2)
+    PF, PG = to_dev(dev, pf, pg)
+    cf = fb.polar_to_cart(PF, range_res=spec.range_res, n=512, delta=delta)
+    cg = fb.polar_to_cart(PG, range_res=spec.range_res, n=512, delta=delta)
+    torch.cuda.synchronize()
+    cf, cg = cf.cpu().numpy(), cg.cpu().numpy()
+    for i in range(2):
+        ref = orc.polar_to_cart(pf[i].astype(np.float64), spec.range_res, 512, delta)
+        assert np.abs(cf[i] - ref).max() <= 1e-6 * np.abs(ref).max()
+    _, _, mf, mg, _ = fb.synth_pairs_host(spec, 0, 2)
+    res, ts, xs = run_gpu(fb, dev, cfg, delta, cf, cg, mf, mg)
+    oc = oracle_cfg(orc, cfg)
+    stats = []
+    for i in range(2):
+        r = orc.scan_match(cf[i], cg[i], oc, delta, mf[i], mg[i])
+        compare(res[i], ts[i], xs[i], (r.theta_bin, r.xy_row, r.xy_col), (r.theta, r.tx, r.ty), r.theta_surface,
+                r.xy_surface, delta, stats)
+
+
+# ---------------------------------------------------------------- stage APIs and properties
+
+def test_stage_apis_match_oracle(fb, orc, dev):
+    cfg, delta, _ = fb.baseline_config(2)
+    f, g, mf, mg, _ = fb.synth_pairs_host(fb.synth_spec(2), 11, 2)
+    fm, gm = f * mf, g * mg
+    F, G = to_dev(dev, fm, gm)
+    m = fb.Matcher(cfg, max_batch=2)
+    ts = torch.zeros((2, cfg.n_theta), dtype=torch.float64, device=dev)
+    theta = m.estimate_rotation(F, G, theta_surface=ts)
+    oc = oracle_cfg(orc, cfg)
+    refs = [orc.scan_match(fm[i], gm[i], oc, delta) for i in range(2)]
+    th = theta.cpu().numpy()
+    for i in range(2):
+        assert abs(th[i] - refs[i].theta) <= THETA_TOL
+    th_ref = torch.tensor([r.theta for r in refs], dtype=torch.float64, device=dev)
+    txy = m.estimate_translation(F, G, th_ref, delta=delta).cpu().numpy()
+    for i in range(2):
+        assert abs(txy[i, 0] - refs[i].tx) <= PX_TOL * delta and abs(txy[i, 1] - refs[i].ty) <= PX_TOL * delta
+
+
+def test_identical_grids_give_zero(fb, dev):  # test_matcher.cpp:210-220, 263-279
+    cfg, delta, _ = fb.baseline_config(2)
+    f, _, mf, _, _ = fb.synth_pairs_host(fb.synth_spec(2), 0, 1)
+    res, _, _ = run_gpu(fb, dev, cfg, delta, f, f, mf, mf)
+    assert res[0]["theta_bin"] == cfg.n_theta // 2 and abs(res[0]["theta"]) < 1e-3
+    half = (cfg.n_xy - 1) // 2
+    assert (res[0]["xy_row"], res[0]["xy_col"]) == (half, half)
+    assert abs(res[0]["tx"]) < 0.05 * delta and abs(res[0]["ty"]) < 0.05 * delta
+
+
+def test_integer_cell_shift(fb, dev):  # test_matcher.cpp:290-300: +5 columns, -3 rows -> t = (+5, +3) cells
+    spec = fb.synth_spec(1, n=128, delta=0.4)
+    f, _, _, _, _ = fb.synth_pairs_host(spec, 5, 1)
+    g = np.zeros_like(f)
+    g[0, :-3, 5:] = f[0, 3:, :-5]  # content moved up 3 rows, right 5 columns (zero fill)
+    cfg = fb.MatchConfig.for_grid(128, 0.4, 129, band_lo=0.15)
+    m = fb.Matcher(cfg, max_batch=1)
+    F, G = to_dev(dev, f, g)
+    txy = m.estimate_translation(F, G, torch.zeros(1, dtype=torch.float64, device=dev), delta=0.4).cpu().numpy()
+    assert abs(txy[0, 0] - 5 * 0.4) < 0.25 * 0.4 and abs(txy[0, 1] - 3 * 0.4) < 0.25 * 0.4
+
+
+def test_f_g_inverse_consistency(fb, dev):  # test_matcher.cpp:349-360
+    cfg, delta, _ = fb.baseline_config(2)
+    f, g, mf, mg, _ = fb.synth_pairs_host(fb.synth_spec(2), 21, 2)
+    fwd, _, _ = run_gpu(fb, dev, cfg, delta, f, g, mf, mg)
+    rev, _, _ = run_gpu(fb, dev, cfg, delta, g, f, mg, mf)
+    for i in range(2):
+        th = -rev[i]["theta"]
+        c, s = math.cos(th), math.sin(th)
+        itx, ity = -(c * rev[i]["tx"] - s * rev[i]["ty"]), -(s * rev[i]["tx"] + c * rev[i]["ty"])
+        assert abs(fwd[i]["theta"] - th) <= 4 * cfg.delta_theta
+        assert abs(fwd[i]["tx"] - itx) <= delta and abs(fwd[i]["ty"] - ity) <= delta
+
+
+def test_n_theta_one_degenerates_to_zero(fb, dev):  # test_matcher.cpp:249-261
+    cfg = fb.MatchConfig(n_xy=64, delta_xy=0.5, n_theta=1, delta_theta=0.01, n_radius=0, pad_angle=0)
+    cfg.finalize()
+    f, g, _, _, _ = fb.synth_pairs_host(fb.synth_spec(2, n=64, delta=2.0), 0, 1)
+    res, ts, _ = run_gpu(fb, dev, cfg, 2.0, f, g)
+    assert res[0]["theta"] == 0.0 and res[0]["theta_bin"] == 0 and ts.shape == (1, 1) and ts[0, 0] == 0.0
+
+
+def test_nonfinite_and_mask_range_are_per_pair_errors(fb, dev):  # test_matcher.cpp:362-372
+    cfg, delta, _ = fb.baseline_config(2)
+    f, g, mf, mg, _ = fb.synth_pairs_host(fb.synth_spec(2), 0, 3)
+    f[1, 3, 3] = np.nan
+    mg[2, 0, 0] = 1.5
+    res, _, _ = run_gpu(fb, dev, cfg, delta, f, g, mf, mg)
+    assert list(res["status"]) == [fb.OK, fb.ERR_NONFINITE, fb.ERR_MASK_RANGE]
+    m = fb.Matcher(cfg, max_batch=3)
+    with pytest.raises(fb.FscanInvalidArgument):
+        m.match_host(f, g, mf, mg, delta=delta)
+    g2 = g.copy()
+    g2[0, 1, 1] = np.inf
+    with pytest.raises(fb.FscanInvalidArgument):
+        m.match_host(f[:1], g2[:1], delta=delta)
+
+
+def test_masked_equals_premasked(fb, dev):  # test_matcher.cpp:374-387
+    cfg, delta, _ = fb.baseline_config(2)
+    f, g, mf, mg, _ = fb.synth_pairs_host(fb.synth_spec(2), 9, 2)
+    a, _, _ = run_gpu(fb, dev, cfg, delta, f, g, mf, mg)
+    b, _, _ = run_gpu(fb, dev, cfg, delta, (f * mf).astype(np.float32), (g * mg).astype(np.float32))
+    for k in ("theta", "tx", "ty", "theta_bin", "xy_row", "xy_col"):
+        np.testing.assert_array_equal(a[k], b[k])
+
+
+def test_chunking_lanes_and_surfaces_do_not_change_results(fb, dev):
+    cfg, delta, _ = fb.baseline_config(2)
+    f, g, mf, mg, _ = fb.synth_pairs_host(fb.synth_spec(2), 40, 7)
+    base, _, _ = run_gpu(fb, dev, cfg, delta, f, g, mf, mg)
+    for chunk in (1, 3):
+        other, _, _ = run_gpu(fb, dev, cfg, delta, f, g, mf, mg, chunk=chunk)
+        assert base.tobytes() == other.tobytes()
+    m = fb.Matcher(cfg, max_batch=7)
+    F, G, MF, MG = to_dev(dev, f, g, mf, mg)
+    out = fb.decode_results(m.match_device(F, G, MF, MG, delta=delta))  # no surfaces requested
+    torch.cuda.synchronize()
+    assert base.tobytes() == out.tobytes()
+    host = m.match_host(f, g, mf, mg, delta=delta)
+    assert base.tobytes() == host.tobytes()
+
+
+def test_full_c4_batch_properties(fb, dev):
+    """Full BASELINE size (4096 pairs at 512^2): every pair valid, deterministic,
+    batch-position invariant, and within the search resolution of the truth."""
+    cfg, delta, total = fb.baseline_config(4)
+    spec = fb.synth_spec(4)
+    f, g, mf, mg, truth = fb.synth_pairs_device(spec, 0, total)
+    m = fb.Matcher(cfg, max_batch=total)
+    a = fb.decode_results(m.match_device(f, g, mf, mg, delta=delta))
+    b = fb.decode_results(m.match_device(f, g, mf, mg, delta=delta))
+    torch.cuda.synchronize()
+    assert a.tobytes() == b.tobytes()  # deterministic
+    assert np.all(a["status"] == 0)
+    sub = slice(1000, 1013)  # same pairs at other batch positions / chunks
+    m2 = fb.Matcher(cfg, max_batch=13)
+    c = fb.decode_results(m2.match_device(f[sub].contiguous(), g[sub].contiguous(), mf[sub].contiguous(),
+                                          mg[sub].contiguous(), delta=delta))
+    torch.cuda.synchronize()
+    assert c.tobytes() == a[sub].tobytes()
+    dth = np.abs(a["theta"] - truth[:, 0])
+    dt = np.hypot(a["tx"] - truth[:, 1], a["ty"] - truth[:, 2])
+    # ground truth is only approximately recoverable (even n: the rotation centre
+    # (n-1)/2.0 sits half a cell off the world origin; polar-resampled content)
+    assert np.mean(dth <= 2 * cfg.delta_theta) > 0.97
+    assert np.mean(dt <= 2 * delta) > 0.97
+
+
+def test_cpp_drop_in_api(fb, dev, tmp_path):
+    """The reference-style C++ tests (tests/cpp/test_dropin.cpp) against the drop-in headers."""
+    src = os.path.join(ROOT, "tests", "cpp", "test_dropin.cpp")
+    exe = tmp_path / "test_dropin"
+    cmd = ["g++", "-std=c++20", "-O2", src, "-I", os.path.join(ROOT, "include"), "-I", "/usr/local/cuda/include",
+           "-L", os.path.dirname(fb.LIB_PATH), "-lfscan_b200", "-L/usr/local/cuda/lib64", "-lcudart",
+           "-Wl,-rpath," + os.path.dirname(fb.LIB_PATH), "-o", str(exe)]
+    subprocess.run(cmd, check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600)
+    print(out.stdout[-3000:])
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
+    assert "ALL PASSED" in out.stdout

@@ -1,0 +1,221 @@
+"""The parity oracle itself (CPU, no GPU): the C restatement (oracle/liboracle.so)
+pinned against the reference's own code — via the golden vectors that
+oracle/_ref produced (tests/golden/make_golden.py) and, when the reference tree
+is present, live — plus the reference's known-answer properties
+(test_spectral.cpp, test_matcher.cpp, verify.cpp)."""
+import glob
+import math
+import os
+
+import numpy as np
+import pytest
+
+from conftest import oracle_cfg
+
+GOLDEN = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz")))
+CFG_KEYS = ("n_theta", "delta_theta", "t_theta", "n_xy", "delta_xy", "t_xy", "band_lo", "band_hi", "n_radius",
+            "pad_angle", "softargmax_window", "normalize_scores")
+
+
+def golden_cfg(orc, z):
+    vals = dict(zip(CFG_KEYS, z["cfg"]))
+    ints = ("n_theta", "n_xy", "n_radius", "pad_angle", "softargmax_window", "normalize_scores")
+    return orc.make_config(**{k: (int(v) if k in ints else float(v)) for k, v in vals.items()})
+
+
+@pytest.mark.parametrize("path", GOLDEN, ids=[os.path.basename(p) for p in GOLDEN])
+def test_restatement_matches_reference_golden(orc, path):
+    z = np.load(path)
+    cfg = golden_cfg(orc, z)
+    for i in range(z["f"].shape[0]):
+        mf = z["mf"][i] if "mf" in z else None
+        mg = z["mg"][i] if "mg" in z else None
+        r = orc.scan_match(z["f"][i], z["g"][i], cfg, float(z["delta"]), mf, mg)
+        np.testing.assert_array_equal([r.theta_bin, r.xy_row, r.xy_col], z["bins"][i])
+        np.testing.assert_allclose([r.theta, r.tx, r.ty], z["pose"][i], rtol=0, atol=1e-12)
+        np.testing.assert_allclose(r.theta_surface, z["theta_surface"][i], rtol=1e-12, atol=0)
+        tol = 1e-12 if z["xy_surface"].dtype == np.float64 else 1e-6
+        ref = z["xy_surface"][i].astype(np.float64)
+        assert np.abs(r.xy_surface - ref).max() <= tol * np.abs(ref).max()
+
+
+def test_noise_shift_golden_lands_on_exact_lag():
+    # roll by (3,-5): content 3 rows down (t_y' = -3 cells), 5 cols left (t_x' = -5)
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "noise_shift_n64.npz"))
+    half = (64 - 1) // 2
+    assert tuple(z["bins"][0][1:]) == (half - 3, half - 5)
+    assert tuple(z["bins"][1][1:]) == (half + 2, half + 4)
+
+
+def test_next_fast_size(orc):  # test_spectral.cpp:231-240
+    L = orc.lib("oracle")
+    for n, want in ((1, 1), (7, 7), (11, 12), (13, 14), (121, 125), (509, 512), (2 * 255 - 1, 512),
+                    (2 * 256 - 1, 512), (2 * 512 - 1, 1024), (2 * 1024 - 1, 2048)):
+        assert L.fo_next_fast_size(n) == want
+
+
+def direct_xcorr(a, b):
+    rows, cols = a.shape
+    out = np.zeros_like(a)
+    for k in range(rows):
+        for l in range(cols):
+            out[k, l] = np.sum(a * np.roll(np.roll(b, -(k - rows // 2), 0), -(l - cols // 2), 1))
+    return out
+
+
+def test_xcorr_equals_direct_loop(orc):  # test_spectral.cpp:148-162
+    rng = np.random.default_rng(21)
+    a, b = rng.random((6, 6)), rng.random((6, 6))
+    np.testing.assert_allclose(orc.xcorr(a, b), direct_xcorr(a, b), rtol=1e-9, atol=1e-12)
+    a, b = rng.random((9, 5)), rng.random((9, 5))  # odd / non-square, the rotation-stage shapes
+    np.testing.assert_allclose(orc.xcorr(a, b), direct_xcorr(a, b), rtol=1e-9, atol=1e-12)
+
+
+def test_integer_circular_shift_lands_on_lag_bin(orc):  # test_spectral.cpp:175-185
+    rng = np.random.default_rng(77)
+    a = rng.random((16, 16))
+    b = np.roll(a, (3, -5), (0, 1))
+    s = orc.xcorr(a, b)
+    arg = int(np.argmax(s))
+    assert (arg // 16, arg % 16) == (11, 3)
+
+
+def test_band_magnitude_is_shift_invariant_and_banded(orc):  # test_spectral.cpp:126-132, imageops band
+    rng = np.random.default_rng(9)
+    g = rng.random((32, 32))
+    m = orc.band_magnitude(g, 0.0, 1.0)
+    w = 0.5 * (1 - np.cos(2 * np.pi * np.arange(32) / 31))
+    ref = np.abs(np.fft.fftshift(np.fft.fft2(g * np.outer(w, w))))
+    c = 16
+    ii, jj = np.meshgrid(np.arange(32), np.arange(32), indexing="ij")
+    rho = np.hypot(ii - c, jj - c) / 16.0
+    np.testing.assert_allclose(m, ref * (rho <= 1.0), rtol=1e-10, atol=1e-10)
+    m2 = orc.band_magnitude(g, 0.1, 0.5)
+    assert np.all(m2[(rho < 0.1) | (rho > 0.5)] == 0.0)
+
+
+def surface(scores):
+    rows, cols = scores.shape
+    return np.arange(rows) - rows / 2.0, np.arange(cols) - cols / 2.0
+
+
+def test_soft_argmax_contracts(orc):  # test_matcher.cpp:105-206
+    s = np.zeros((9, 9))
+    s[2, 6] = 5.0
+    rc, cc = surface(s)
+    r, c = orc.soft_argmax(s, rc, cc, 50.0, 2, True)
+    assert r == pytest.approx(2 - 4.5, rel=1e-6) and c == pytest.approx(6 - 4.5, rel=1e-6)
+    s = np.zeros((1, 7))
+    s[0, 2] = s[0, 4] = 1.0
+    r, c = orc.soft_argmax(s, [0.0], np.arange(7.0), 200.0, 6, True)
+    assert r == 0.0 and c == pytest.approx(3.0, rel=1e-6)
+    s = np.ones((5, 5))
+    rc, cc = surface(s)
+    r, c = orc.soft_argmax(s, rc, cc, 2.0, 16, True)
+    assert r == pytest.approx(-0.5, abs=1e-9) and c == pytest.approx(-0.5, abs=1e-9)
+    a = np.exp(-0.4 * (np.arange(11) - 5.2) ** 2)[None]
+    ra = orc.soft_argmax(a, [0.0], np.arange(11.0), 3.0, 4, True)
+    rb = orc.soft_argmax(a * 1000, [0.0], np.arange(11.0), 3.0, 4, True)
+    rc_ = orc.soft_argmax(a * 1000, [0.0], np.arange(11.0), 3.0, 4, False)
+    assert ra[1] == pytest.approx(rb[1], rel=1e-12) and abs(rc_[1] - ra[1]) > 1e-6
+
+
+def test_soft_argmax_matches_direct_weighted_mean(orc):  # test_matcher.cpp:143-183
+    n = 21
+    i, j = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+    s = np.exp(-0.1 * ((i - 9.3) ** 2 + (j - 11.6) ** 2))
+    rc, cc = surface(s)
+    r, c = orc.soft_argmax(s, rc, cc, 4.0, 5, False)
+    pr, pc = np.unravel_index(np.argmax(s), s.shape)
+    win = s[max(0, pr - 5):pr + 6, max(0, pc - 5):pc + 6]
+    w = np.exp(4.0 * (win - s[pr, pc]))
+    rr = rc[max(0, pr - 5):pr + 6][:, None]
+    ccw = cc[max(0, pc - 5):pc + 6][None, :]
+    assert r == pytest.approx((w * rr).sum() / w.sum(), rel=1e-12)
+    assert c == pytest.approx((w * ccw).sum() / w.sum(), rel=1e-12)
+
+
+def test_config_finalize_and_validate(orc):  # test_matcher.cpp:60-103 (minus the odd-n rule, D1)
+    import ctypes as C
+    L = orc.lib("oracle")
+    cfg = orc.make_config()
+    assert L.fo_validate(C.byref(cfg), None, 0) == 0
+    d = orc.make_config(n_xy=65, n_theta=100, delta_theta=math.pi / 100, n_radius=0, pad_angle=-1)
+    orc.finalize(d)
+    assert (d.n_radius, d.pad_angle) == (33, 13)
+    t = orc.make_config(n_theta=2, delta_theta=0.01, pad_angle=-1)
+    orc.finalize(t)
+    assert t.pad_angle == 1
+    for kw in (dict(band_lo=0.8), dict(delta_theta=math.pi / 64.0), dict(pad_angle=129),
+               dict(softargmax_window=0), dict(t_theta=0.0)):
+        bad = orc.make_config(n_xy=65, delta_xy=0.4, n_theta=129, delta_theta=math.pi / 129, n_radius=33,
+                              pad_angle=17, band_lo=0.15)
+        for k, v in kw.items():
+            setattr(bad, k, v)
+        assert L.fo_validate(C.byref(bad), None, 0) == 1, kw
+    even = orc.make_config(n_xy=64)
+    assert L.fo_validate(C.byref(even), None, 0) == 0  # D1: even n accepted
+
+
+def test_scan_match_rejects_nonfinite_and_bad_masks(orc):  # test_matcher.cpp:362-372
+    cfg = orc.make_config(n_xy=64, delta_xy=0.4, n_theta=64, delta_theta=math.pi / 64, n_radius=0,
+                          pad_angle=-1, band_lo=0.15)
+    orc.finalize(cfg)
+    f = np.zeros((64, 64))
+    g = np.zeros((64, 64))
+    f[3, 3] = np.nan
+    with pytest.raises(orc.OracleError):
+        orc.scan_match(f, g, cfg, 0.4)
+    f[3, 3] = 0.0
+    g[1, 1] = np.inf
+    with pytest.raises(orc.OracleError):
+        orc.scan_match(f, g, cfg, 0.4)
+    g[1, 1] = 0.0
+    m = np.ones((64, 64))
+    m[0, 0] = 1.5
+    with pytest.raises(orc.OracleError):
+        orc.scan_match(f, g, cfg, 0.4, m, np.ones((64, 64)))
+
+
+def test_polar_to_cart_spec(orc):
+    # a sweep that is constant along range returns that azimuth's value
+    n_az, n_rng = 8, 50
+    p = np.tile(np.arange(n_az, dtype=np.float64)[:, None], (1, n_rng))
+    out = orc.polar_to_cart(p, 1.0, 9, 1.0)
+    half = 4
+    assert out[half, half + 3] == pytest.approx(0.0)        # +x axis: azimuth 0
+    assert out[half - 3, half] == pytest.approx(2.0)        # +y axis: azimuth 2 (of 8)
+    assert out[half + 3, half] == pytest.approx(6.0)        # -y axis
+    # outside the last range bin: zero
+    out2 = orc.polar_to_cart(p[:, :2], 1.0, 9, 1.0)
+    assert out2[0, 0] == 0.0
+
+
+ref_only = pytest.mark.skipif(not os.path.isdir("/root/reference/proj"),
+                              reason="reference tree only in the build container")
+
+
+@ref_only
+def test_reference_verify_suites_pass_with_shim(orc):
+    fails, report = orc.ref_verify()
+    assert fails == 0, report
+    assert report.count("[PASS]") == 7
+
+
+@ref_only
+@pytest.mark.parametrize("n,nt", [(65, 129), (64, 90), (128, 180)])
+def test_restatement_bit_exact_vs_reference_live(orc, n, nt):
+    rng = np.random.default_rng(n)
+    f = rng.random((n, n))
+    g = np.roll(f, (2, -1), (0, 1)) + 0.01 * rng.random((n, n))
+    cfg = orc.make_config(n_xy=n, delta_xy=0.4, n_theta=nt, delta_theta=math.pi / nt, n_radius=0, pad_angle=-1,
+                          band_lo=0.15)
+    orc.finalize(cfg)
+    a = orc.scan_match(f, g, cfg, 0.4)
+    b = orc.scan_match(f, g, cfg, 0.4, which="ref")
+    assert (a.theta, a.tx, a.ty) == (b.theta, b.tx, b.ty)
+    np.testing.assert_array_equal(a.theta_surface, b.theta_surface)
+    np.testing.assert_array_equal(a.xy_surface, b.xy_surface)
+    for th in (0.0, 0.3, -0.22):
+        np.testing.assert_array_equal(orc.rotate_bilinear(f, th), orc.rotate_bilinear(f, th, which="ref"))
+    np.testing.assert_array_equal(orc.cart2pol(f, 90, 33, math.pi), orc.cart2pol(f, 90, 33, math.pi, which="ref"))
