@@ -1,0 +1,7 @@
+python tests/gpu_probe.py 2>&1 | tail -24
+python -m pytest tests -m gpu -x -q 2>&1 | tail -4
+python bench.py --steps 10 --warmup 3 --no-e2e --no-cpu > gpurun_out/bench5.json 2> gpurun_out/bench5.err; python -c "import json;d=json.load(open('gpurun_out/bench5.json'));print(d['value'], d['hbm_pipeline']['kernel_ms_per_step'])"
+CMD="python bench.py --pairs 256 --steps 2 --warmup 3 --no-e2e --no-cpu"
+$CMD > gpurun_out/small.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:"xlat_rows|xlat_out|xlat_cols" -s 6 -c 3 -o gpurun_out/prof5 $CMD > gpurun_out/ncu5.log 2>&1
+echo ncu rc=$?

@@ -55,7 +55,9 @@ struct fscan_ctx {
     std::mutex mu;
     // tables
     float2* tw_n = nullptr;
-    float2* tw_2n = nullptr;
+    float2* tw_k = nullptr;
+    float2* tw_k2 = nullptr;
+    float2* tw_m = nullptr;
     float* hann = nullptr;
     int2* band = nullptr;
     PolarTap* taps = nullptr;
@@ -201,9 +203,9 @@ fscan_status alloc_lane(fscan_ctx* ctx, Lane& l, int chunk) {
     const int nparts = ctx->n / rows_per_block_out(ctx->n);
     CK(cudaMalloc(&l.ft, nn * sizeof(float) * chunk));
     CK(cudaMalloc(&l.gt, nn * sizeof(float) * chunk));
-    CK(cudaMalloc(&l.zbuf, n * (n + 1) * sizeof(float2) * chunk));
+    CK(cudaMalloc(&l.zbuf, n * n * sizeof(float2) * chunk));
     CK(cudaMalloc(&l.mag, nn * sizeof(float) * chunk));
-    CK(cudaMalloc(&l.fgt, (n + 1) * n * sizeof(float4) * chunk));
+    CK(cudaMalloc(&l.fgt, (3 * n / 4 + 1) * n * sizeof(float4) * chunk));
     CK(cudaMalloc(&l.part, sizeof(Partial) * nparts * chunk));
     CK(cudaMalloc(&l.rot, sizeof(RotState) * chunk));
     CK(cudaMalloc(&l.flags, sizeof(int) * chunk));
@@ -234,7 +236,9 @@ Params base_params(fscan_ctx* ctx, Lane& l, int batch, double delta) {
     p.rot = l.rot;
     p.flags = l.flags;
     p.tw_n = ctx->tw_n;
-    p.tw_2n = ctx->tw_2n;
+    p.tw_k = ctx->tw_k;
+    p.tw_k2 = ctx->tw_k2;
+    p.tw_m = ctx->tw_m;
     p.hann = ctx->hann;
     p.band = ctx->band;
     p.taps = ctx->taps;
@@ -426,15 +430,17 @@ fscan_status fscan_ctx_create(int device, const fscan_config* cfg_in, int max_ba
 
     const int n = ctx->n;
     // tables
-    std::vector<float2> tw(n), tw2(2 * n);
-    for (int i = 0; i < n; ++i) {
-        const double a = -2.0 * kPi * i / n;
-        tw[i] = make_float2((float)std::cos(a), (float)std::sin(a));
-    }
-    for (int i = 0; i < 2 * n; ++i) {
-        const double a = -2.0 * kPi * i / (2 * n);
-        tw2[i] = make_float2((float)std::cos(a), (float)std::sin(a));
-    }
+    // twiddle tables exp(-2 pi i k / L), fp64-accurate then rounded to fp32:
+    // L = N (rotation stage), K = N/2 and K/2 (translation FFTs), M = 3N/2
+    auto table = [](int len) {
+        std::vector<float2> t(len);
+        for (int i = 0; i < len; ++i) {
+            const double a = -2.0 * kPi * i / len;
+            t[i] = make_float2((float)std::cos(a), (float)std::sin(a));
+        }
+        return t;
+    };
+    const std::vector<float2> tw = table(n), twk = table(n / 2), twk2 = table(n / 4), twm = table(3 * n / 2);
     std::vector<float> hann(n, 1.0f);  // imageops.cpp:30-42
     if (n > 1)
         for (int i = 0; i < n; ++i) hann[i] = (float)(0.5 * (1.0 - std::cos(2.0 * kPi * i / (n - 1))));
@@ -451,12 +457,16 @@ fscan_status fscan_ctx_create(int device, const fscan_config* cfg_in, int max_ba
         ctx->n_live = 1;
     }
     CK(cudaMalloc(&ctx->tw_n, sizeof(float2) * n));
-    CK(cudaMalloc(&ctx->tw_2n, sizeof(float2) * 2 * n));
+    CK(cudaMalloc(&ctx->tw_k, sizeof(float2) * twk.size()));
+    CK(cudaMalloc(&ctx->tw_k2, sizeof(float2) * twk2.size()));
+    CK(cudaMalloc(&ctx->tw_m, sizeof(float2) * twm.size()));
+    CK(cudaMemcpy(ctx->tw_k, twk.data(), sizeof(float2) * twk.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->tw_k2, twk2.data(), sizeof(float2) * twk2.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->tw_m, twm.data(), sizeof(float2) * twm.size(), cudaMemcpyHostToDevice));
     CK(cudaMalloc(&ctx->hann, sizeof(float) * n));
     CK(cudaMalloc(&ctx->band, sizeof(int2) * n));
     CK(cudaMalloc(&ctx->taps, sizeof(PolarTap) * taps.size()));
     CK(cudaMemcpy(ctx->tw_n, tw.data(), sizeof(float2) * n, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(ctx->tw_2n, tw2.data(), sizeof(float2) * 2 * n, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(ctx->hann, hann.data(), sizeof(float) * n, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(ctx->band, band.data(), sizeof(int2) * n, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(ctx->taps, taps.data(), sizeof(PolarTap) * taps.size(), cudaMemcpyHostToDevice));
@@ -489,7 +499,9 @@ void fscan_ctx_destroy(fscan_ctx* ctx) {
     if (ctx->start_ev) cudaEventDestroy(ctx->start_ev);
     for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
     cudaFree(ctx->tw_n);
-    cudaFree(ctx->tw_2n);
+    cudaFree(ctx->tw_k);
+    cudaFree(ctx->tw_k2);
+    cudaFree(ctx->tw_m);
     cudaFree(ctx->hann);
     cudaFree(ctx->band);
     cudaFree(ctx->taps);

@@ -3,26 +3,33 @@
 // Replaces the FFTW c2c transforms the reference calls through
 // proj/src/spectral.cpp:73-153 (dft2 / idft2 / xcorr) on the GPU path.
 //
-// One length-N transform (N = 2^k, 64 <= N <= 2048) is owned by T = N/16
+// One length-N transform (N = 2^k, 16 <= N <= 2048) is owned by T = N/16
 // threads; thread t of a transform holds the 16 complex values
 //     v[m] = x[t + m*T],  m = 0..15
 // before and after the call (natural order in, natural order out). Stages are
 // radix 16 while at least 16*16 points remain, then one radix-R stage
 // (R = N / 16^s in {2,4,8,16}) done as 16/R butterflies per thread:
-//     N=64: 16.4   128: 16.8   256: 16.16   512: 16.16.2   1024: 16.16.4   2048: 16.16.8
+//     N=16: 16   32: 16.2   64: 16.4   128: 16.8   256: 16.16   512: 16.16.2
+//     1024: 16.16.4   2048: 16.16.8
 // Stage (radix R, span Ns) butterfly b reads x[b + r*N/R] (= registers
 // j + r*(16/R) of thread t, b = t + j*T), multiplies by W_{Ns*R}^{r*(b mod Ns)},
 // does an R-point DFT and writes y[(b/Ns)*Ns*R + (b mod Ns) + r*Ns]. The last
 // stage lands back in the input register slots, so only S-1 shared-memory
-// exchanges are needed (one for N <= 256, two for 512..2048). The exchange
-// buffer is split real/imag (4-byte banks) with one pad float every 32.
+// exchanges are needed (one for N <= 256, two for 512..2048).
+//
+// Exchange buffers are split real/imag (4-byte banks). Two bank-conflict-free
+// layouts (verified for every exchange by an access-pattern model, see
+// DESIGN.md §5):
+//   Lay<1>  one transform per warp group (T >= 32): XOR swizzle of the 5-bit
+//           offset inside each 32-float line by m(line) = (line & 15) | bit3(line) << 4
+//   Lay<W>  W transforms interleaved element-wise, transform index fastest in
+//           the warp (T < 32, or column kernels with W = 16):
+//           addr = W * (i + i/16) + sub
 //
 // Twiddles come from a fp32 table tw[i] = exp(-2*pi*i*i/N) (rounded from fp64
 // on the host); SIGN = +1 uses the conjugate. Transforms are unnormalised,
-// matching FFTW_FORWARD / FFTW_BACKWARD.
-//
-// Every thread of the CTA must call fft_regs the same number of times (it
-// contains __syncthreads()).
+// matching FFTW_FORWARD / FFTW_BACKWARD. Every thread of the CTA must call
+// fft_regs the same number of times (it contains __syncthreads()).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -59,16 +66,14 @@ __device__ __forceinline__ void dft4(float2& x0, float2& x1, float2& x2, float2&
     x3 = csub(b, d);
 }
 
-// 8-point DFT: x[k1 + 2*k2]... done as radix-2 x radix-4 (DIT over n = 2*n1 + n2).
+// 8-point DFT as radix-2 x radix-4 (DIT over n = 2*n1 + n2).
 template <int SIGN>
 __device__ __forceinline__ void dft8(float2* x) {
     constexpr float r = 0.70710678118654752f;
-    // 4-point DFTs over even and odd samples
     float2 e0 = x[0], e1 = x[2], e2 = x[4], e3 = x[6];
     float2 o0 = x[1], o1 = x[3], o2 = x[5], o3 = x[7];
     dft4<SIGN>(e0, e1, e2, e3);
     dft4<SIGN>(o0, o1, o2, o3);
-    // twiddles W8^k on odd part
     o1 = SIGN < 0 ? make_float2(r * (o1.x + o1.y), r * (o1.y - o1.x)) : make_float2(r * (o1.x - o1.y), r * (o1.y + o1.x));
     o2 = mul_mi<SIGN>(o2);
     o3 = SIGN < 0 ? make_float2(r * (o3.y - o3.x), -r * (o3.x + o3.y)) : make_float2(-r * (o3.x + o3.y), r * (o3.x - o3.y));
@@ -90,8 +95,8 @@ __device__ __forceinline__ void dft16(float2* x) {
     constexpr float r = 0.70710678118654752f;
 #pragma unroll
     for (int n2 = 0; n2 < 4; ++n2) dft4<SIGN>(x[n2], x[4 + n2], x[8 + n2], x[12 + n2]);
-    // now x[4*k1 + n2] holds a[n2][k1]; apply W16^(n2*k1)
-    const float sg = (float)SIGN;  // W16^m = cos(2 pi m/16) + i*SIGN*sin(2 pi m/16)
+    // x[4*k1 + n2] holds a[n2][k1]; apply W16^(n2*k1) = cos + i*SIGN*sin
+    const float sg = (float)SIGN;
     const float2 w1 = make_float2(c1, sg * s1), w2 = make_float2(r, sg * r), w3 = make_float2(s1, sg * c1);
     const float2 w6 = make_float2(-r, sg * r), w9 = make_float2(-c1, -sg * s1);
     x[4 * 1 + 1] = cmul(x[4 * 1 + 1], w1);
@@ -103,7 +108,6 @@ __device__ __forceinline__ void dft16(float2* x) {
     x[4 * 1 + 3] = cmul(x[4 * 1 + 3], w3);
     x[4 * 2 + 3] = cmul(x[4 * 2 + 3], w6);
     x[4 * 3 + 3] = cmul(x[4 * 3 + 3], w9);
-    // 4-point DFTs over n2 for each k1: inputs x[4 k1 + n2], outputs X[k1 + 4 k2]
     float2 y[16];
 #pragma unroll
     for (int k1 = 0; k1 < 4; ++k1) {
@@ -131,16 +135,75 @@ __device__ __forceinline__ void dft_r(float2* x) {
     }
 }
 
-__device__ __forceinline__ int spad(int i) { return i + (i >> 5); }
+// Exchange-buffer layout of one transform (see header comment).
+template <int W>
+struct Lay {
+    float* re;
+    float* im;
+    int sub;  // transform index inside an interleaved group (W > 1)
+    __device__ __forceinline__ int at(int i) const {
+        if constexpr (W == 1) {
+            const int j = i >> 5;
+            return (i & ~31) | ((i & 31) ^ ((j & 15) | (((j >> 3) & 1) << 4)));
+        } else {
+            return W * (i + (i >> 4)) + sub;
+        }
+    }
+    __device__ __forceinline__ void put(int i, float2 v) const {
+        const int a = at(i);
+        re[a] = v.x;
+        im[a] = v.y;
+    }
+    __device__ __forceinline__ float2 get(int i) const {
+        const int a = at(i);
+        return make_float2(re[a], im[a]);
+    }
+};
 
-// floats of exchange buffer per transform (re + im halves)
-template <int N>
-struct Cfg {
+// Floats of one real (or imaginary) part for a group of W transforms of length N.
+template <int N, int W>
+__host__ __device__ constexpr int part_floats() {
+    return W == 1 ? N + 2 : W * (N + N / 16);
+}
+
+// Thread/transform geometry of kernels whose transforms are "rows": T = N/16
+// threads per transform; transforms of a warp interleaved (W per warp) when T < 32.
+template <int N, int THREADS>
+struct Geom {
     static constexpr int T = N / 16;
-    static constexpr int kHalf = N + N / 32;  // padded real (or imag) part
-    static constexpr int kFloats = 2 * kHalf;
-    static constexpr int kStages = (N <= 256) ? 2 : 3;
-    static constexpr int kLastR = (N <= 256) ? (N / 16) : (N / 256);
+    static constexpr int W = T >= 32 ? 1 : 32 / T;  // transforms per warp
+    static constexpr int PER_CTA = THREADS / T;      // transforms per CTA
+    static constexpr int GROUPS = PER_CTA / W;
+    static constexpr int PART = part_floats<N, W>();
+    static constexpr int FLOATS = GROUPS * 2 * PART;  // one exchange buffer per transform
+    static_assert(GROUPS >= 1 && PER_CTA % W == 0, "a CTA must hold whole warps of transforms");
+    __device__ __forceinline__ static void map(int tid, int& tr, int& t) {
+        if constexpr (W == 1) {
+            tr = tid / T;
+            t = tid % T;
+        } else {
+            const int w = tid >> 5, lane = tid & 31;
+            tr = w * W + lane % W;
+            t = lane / W;
+        }
+    }
+    // layout of transform tr inside buffer `base` (FLOATS floats)
+    __device__ __forceinline__ static Lay<W> lay(float* base, int tr) {
+        float* g = base + (tr / W) * 2 * PART;
+        return Lay<W>{g, g + PART, tr % W};
+    }
+    // layout of transform tr for a buffer holding length-LEN data per transform
+    // (same interleave; used to stash inputs that are longer than the transform)
+    template <int LEN>
+    __device__ __forceinline__ static Lay<W> lay_len(float* base, int tr) {
+        constexpr int P = part_floats<LEN, W>();
+        float* g = base + (tr / W) * 2 * P;
+        return Lay<W>{g, g + P, tr % W};
+    }
+    template <int LEN>
+    __host__ __device__ static constexpr int floats_len() {
+        return GROUPS * 2 * part_floats<LEN, W>();
+    }
 };
 
 template <int SIGN>
@@ -150,9 +213,8 @@ __device__ __forceinline__ float2 twiddle(const float2* __restrict__ tw, int idx
 }
 
 // One Stockham stage. Ns = span before this stage, R = radix.
-template <int N, int R, int Ns, bool LAST, int SIGN>
-__device__ __forceinline__ void stage(float2 (&v)[16], int t, float* sre, float* sim,
-                                      const float2* __restrict__ tw) {
+template <int N, int R, int Ns, bool LAST, int SIGN, typename L>
+__device__ __forceinline__ void stage(float2 (&v)[16], int t, const L& lay, const float2* __restrict__ tw) {
     constexpr int T = N / 16;
     constexpr int NB = 16 / R;
 #pragma unroll
@@ -174,38 +236,30 @@ __device__ __forceinline__ void stage(float2 (&v)[16], int t, float* sre, float*
         } else {
             const int base = (b / Ns) * Ns * R + k;
 #pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const int p = spad(base + r * Ns);
-                sre[p] = u[r].x;
-                sim[p] = u[r].y;
-            }
+            for (int r = 0; r < R; ++r) lay.put(base + r * Ns, u[r]);
         }
     }
     if constexpr (!LAST) {
         __syncthreads();
 #pragma unroll
-        for (int m = 0; m < 16; ++m) {
-            const int p = spad(t + m * T);
-            v[m] = make_float2(sre[p], sim[p]);
-        }
+        for (int m = 0; m < 16; ++m) v[m] = lay.get(t + m * T);
         __syncthreads();
     }
 }
 
 // In-register FFT of one length-N transform (see header comment).
-// sbuf: Cfg<N>::kFloats floats of shared memory owned by this transform.
-template <int N, int SIGN>
-__device__ __forceinline__ void fft_regs(float2 (&v)[16], int t, float* sbuf,
-                                         const float2* __restrict__ tw) {
-    float* sre = sbuf;
-    float* sim = sbuf + Cfg<N>::kHalf;
-    if constexpr (N <= 256) {
-        stage<N, 16, 1, false, SIGN>(v, t, sre, sim, tw);
-        stage<N, N / 16, 16, true, SIGN>(v, t, sre, sim, tw);
+template <int N, int SIGN, typename L>
+__device__ __forceinline__ void fft_regs(float2 (&v)[16], int t, const L& lay, const float2* __restrict__ tw) {
+    static_assert(N >= 16 && (N & (N - 1)) == 0, "power-of-two length >= 16");
+    if constexpr (N == 16) {
+        stage<N, 16, 1, true, SIGN>(v, t, lay, tw);
+    } else if constexpr (N <= 256) {
+        stage<N, 16, 1, false, SIGN>(v, t, lay, tw);
+        stage<N, N / 16, 16, true, SIGN>(v, t, lay, tw);
     } else {
-        stage<N, 16, 1, false, SIGN>(v, t, sre, sim, tw);
-        stage<N, 16, 16, false, SIGN>(v, t, sre, sim, tw);
-        stage<N, N / 256, 256, true, SIGN>(v, t, sre, sim, tw);
+        stage<N, 16, 1, false, SIGN>(v, t, lay, tw);
+        stage<N, 16, 16, false, SIGN>(v, t, lay, tw);
+        stage<N, N / 256, 256, true, SIGN>(v, t, lay, tw);
     }
 }
 

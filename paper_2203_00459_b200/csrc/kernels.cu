@@ -25,21 +25,25 @@
 
 namespace fscan_detail {
 
-using fscan_fft::Cfg;
 using fscan_fft::cadd;
 using fscan_fft::cconj;
 using fscan_fft::cmul;
 using fscan_fft::csub;
 using fscan_fft::fft_regs;
-using fscan_fft::spad;
+using fscan_fft::Geom;
+using fscan_fft::Lay;
+using fscan_fft::part_floats;
 
 namespace {
 
 constexpr int kRowThreads = 256;
 
 template <int N>
+using RowG = Geom<N, kRowThreads>;
+
+template <int N>
 __host__ __device__ constexpr int rows_per_block() {
-    return kRowThreads / (N / 16) < 1 ? 1 : kRowThreads / (N / 16);
+    return RowG<N>::PER_CTA;
 }
 
 __device__ __forceinline__ float bilerp(float fr, float fc, float a00, float a01, float a10, float a11) {
@@ -53,13 +57,14 @@ __device__ __forceinline__ float bilerp(float fr, float fc, float a00, float a01
 // z = f~w + i g~w.
 template <int N>
 __global__ void __launch_bounds__(kRowThreads) k_rot_rows(Params p) {
-    constexpr int T = N / 16;
-    constexpr int RPB = rows_per_block<N>();
+    using G = RowG<N>;
+    constexpr int T = G::T;
     extern __shared__ float smem[];
     const int pair = blockIdx.y;
-    const int tr = threadIdx.x / T, t = threadIdx.x % T;
-    const int y = blockIdx.x * RPB + tr;
-    float* sb = smem + tr * Cfg<N>::kFloats;
+    int tr, t;
+    G::map(threadIdx.x, tr, t);
+    const int y = blockIdx.x * G::PER_CTA + tr;
+    const auto lay = G::lay(smem, tr);
     const size_t base = ((size_t)pair * N + y) * N;
     const float hy = p.hann[y];
     int bad = 0;
@@ -81,38 +86,34 @@ __global__ void __launch_bounds__(kRowThreads) k_rot_rows(Params p) {
         const float w = hy * __ldg(p.hann + x);
         v[m] = make_float2(fv * w, gv * w);
     }
-    fft_regs<N, -1>(v, t, sb, p.tw_n);
+    fft_regs<N, -1>(v, t, lay, p.tw_n);
 #pragma unroll
     for (int m = 0; m < 16; ++m) p.zbuf[base + t + m * T] = v[m];
     if (bad) atomicOr(p.flags + pair, bad);
 }
 
 // ---------------------------------------------------------------- K1b
-// 8 output columns u in [u0, u0+8) plus their mirrors (N-u) mod N; column
-// FFTs; F = (Z[v,u] + conj Z[-v,-u]) / 2, G = (Z[v,u] - conj Z[-v,-u]) / 2i;
+// 8 output columns u in [u0, u0+8) plus their mirrors (N-u) mod N, 16
+// interleaved column FFTs (column index fastest in the warp, Lay<16>);
+// F = (Z[v,u] + conj Z[-v,-u]) / 2, G = (Z[v,u] - conj Z[-v,-u]) / 2i;
 // |F|, |G| times the annular band, written as an [N centred rows][8] tile.
 template <int N>
 __global__ void __launch_bounds__(N) k_rot_cols(Params p) {
     constexpr int T = N / 16;
+    constexpr int PART = part_floats<N, 16>();
     extern __shared__ float smem[];
     const int pair = blockIdx.y;
     const int u0 = blockIdx.x * 8;
     const int c = threadIdx.x % 16, t = threadIdx.x / 16;
     const int col = c < 8 ? (u0 + c) : ((N - (u0 + c - 8)) & (N - 1));
-    float* sb = smem + c * Cfg<N>::kFloats;
+    const Lay<16> lay{smem, smem + PART, c};
     const float2* z = p.zbuf + (size_t)pair * N * N;
     float2 v[16];
 #pragma unroll
     for (int m = 0; m < 16; ++m) v[m] = z[(size_t)(t + m * T) * N + col];
-    fft_regs<N, -1>(v, t, sb, p.tw_n);
-    float* sre = sb;
-    float* sim = sb + Cfg<N>::kHalf;
+    fft_regs<N, -1>(v, t, lay, p.tw_n);
 #pragma unroll
-    for (int m = 0; m < 16; ++m) {
-        const int q = spad(t + m * T);
-        sre[q] = v[m].x;
-        sim[q] = v[m].y;
-    }
+    for (int m = 0; m < 16; ++m) lay.put(t + m * T, v[m]);
     __syncthreads();
     float* outf = p.mag + (((size_t)pair * 2 + 0) * (N / 16) + blockIdx.x) * (size_t)(N * 8);
     float* outg = p.mag + (((size_t)pair * 2 + 1) * (N / 16) + blockIdx.x) * (size_t)(N * 8);
@@ -122,10 +123,8 @@ __global__ void __launch_bounds__(N) k_rot_cols(Params p) {
         const int cc = o & 7, vc = o >> 3;
         const int vn = (vc + N / 2) & (N - 1);  // natural row of centred row vc
         const int vm = (N - vn) & (N - 1);      // row of -v
-        const float* a = smem + cc * Cfg<N>::kFloats;
-        const float* b = smem + (8 + cc) * Cfg<N>::kFloats;
-        const float2 z1 = make_float2(a[spad(vn)], a[Cfg<N>::kHalf + spad(vn)]);
-        const float2 z2 = make_float2(b[spad(vm)], b[Cfg<N>::kHalf + spad(vm)]);
+        const float2 z1 = Lay<16>{smem, smem + PART, cc}.get(vn);
+        const float2 z2 = Lay<16>{smem, smem + PART, 8 + cc}.get(vm);
         const float fr = z1.x + z2.x, fi = z1.y - z2.y;  // Z1 + conj(Z2)
         const float gr = z1.x - z2.x, gi = z1.y + z2.y;  // Z1 - conj(Z2)
         const int2 bd = __ldg(p.band + vc);
@@ -177,16 +176,31 @@ __global__ void __launch_bounds__(kPolarThreads) k_rot_polar(Params p) {
     for (int i = warp; i < nt; i += nwarps) {
         double af = 0.0, ag = 0.0;
         const PolarTap* row = p.taps + (size_t)i * p.n_live;
-        for (int jj = lane; jj < p.n_live; jj += 32) {
-            const PolarTap e = row[jj];
-            const int r0 = e.packed & 0xFFF, u = (e.packed >> 12) & 0xFFF, fl = e.packed >> 24;
-            float f00 = 0.f, f01 = 0.f, f10 = 0.f, f11 = 0.f, g00 = 0.f, g01 = 0.f, g10 = 0.f, g11 = 0.f;
-            if (fl & 1) { f00 = tile_at(mf, n, r0, u); g00 = tile_at(mg, n, r0, u); }
-            if (fl & 2) { f01 = tile_at(mf, n, r0, u + 1); g01 = tile_at(mg, n, r0, u + 1); }
-            if (fl & 4) { f10 = tile_at(mf, n, r0 + 1, u); g10 = tile_at(mg, n, r0 + 1, u); }
-            if (fl & 8) { f11 = tile_at(mf, n, r0 + 1, u + 1); g11 = tile_at(mg, n, r0 + 1, u + 1); }
-            af += (double)bilerp(e.fr, e.fc, f00, f01, f10, f11);
-            ag += (double)bilerp(e.fr, e.fc, g00, g01, g10, g11);
+        constexpr int U = 4;  // independent entries in flight per lane (memory-level parallelism)
+        for (int j0 = 0; j0 < p.n_live; j0 += 32 * U) {
+            PolarTap e[U];
+#pragma unroll
+            for (int q = 0; q < U; ++q) {
+                const int jj = j0 + q * 32 + lane;
+                e[q] = jj < p.n_live ? row[jj] : PolarTap{0, 0.f, 0.f, 0.f};  // flags 0: contributes 0
+            }
+            float fv[U][4], gv[U][4];
+#pragma unroll
+            for (int q = 0; q < U; ++q) {
+                const int r0 = e[q].packed & 0xFFF, u = (e[q].packed >> 12) & 0xFFF, fl = e[q].packed >> 24;
+#pragma unroll
+                for (int tp = 0; tp < 4; ++tp) {
+                    const bool on = (fl >> tp) & 1;
+                    const int rr = r0 + (tp >> 1), uu = u + (tp & 1);
+                    fv[q][tp] = on ? tile_at(mf, n, rr, uu) : 0.f;
+                    gv[q][tp] = on ? tile_at(mg, n, rr, uu) : 0.f;
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < U; ++q) {
+                af += (double)bilerp(e[q].fr, e[q].fc, fv[q][0], fv[q][1], fv[q][2], fv[q][3]);
+                ag += (double)bilerp(e[q].fr, e[q].fc, gv[q][0], gv[q][1], gv[q][2], gv[q][3]);
+            }
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -298,39 +312,74 @@ __global__ void k_theta_in(Params p) {
     rs->bin = 0;
 }
 
+// ---------------------------------------------------------------- translation stage
+// The reference correlates the scans zero-padded to P = next_fast_size(2N-1)
+// (matcher.cpp:165-167) and keeps the lags ky in [-N/2, N/2), kx in
+// [-(N/2-1), N/2] (crop, matcher.cpp:171-182). The linear correlation has
+// support |k| <= N-1, so a CIRCULAR correlation of length M = 3N/2 already
+// equals it on those lags (aliases land at |k| >= N). With K = N/2, M = 3K,
+// and the data at offset 0 (a shift common to both scans cancels in conj(F)G),
+// every length-M transform of an N-sample signal is three K-point FFTs:
+//   X[3k+q] = FFT_K( W_M^{nq} (x[n] + W_3^q x[n+K]) )[k],  q = 0, 1, 2.
+// This is 1.8x fewer FFT flops than the power-of-two P = 2N route.
+constexpr float kS3 = 0.86602540378443865f;  // sqrt(3)/2
+
+__device__ __forceinline__ float2 w3(int q) {  // W_3^q = exp(-2 pi i q / 3)
+    q %= 3;
+    return q == 0 ? make_float2(1.f, 0.f) : (q == 1 ? make_float2(-0.5f, -kS3) : make_float2(-0.5f, kS3));
+}
+
+// W_M^e for 0 <= e < M (every caller passes a reduced exponent)
+__device__ __forceinline__ float2 wm(const float2* __restrict__ tw_m, int e) { return __ldg(tw_m + e); }
+
+// Rows/columns of the translation stage each own THREE K-point transforms
+// (q = 0, 1, 2), run concurrently by three thread groups: transform index
+// tr = 3 * unit + q in the Geom mapping.
+
 // ---------------------------------------------------------------- K3
-// Row y of the translation stage: f~ row and the de-rotated g~ row
-// (rotate_bilinear(g~, -theta), imageops.cpp:61-79, exact fp64 index map),
-// packed z = f~ + i g~r; the 2N-point row transform of the zero-padded row
-// is E = FFT_N(z) (even bins) and O = FFT_N(z W_2N^x) (odd bins); then the
-// real spectra F = (Z[k] + conj Z[2N-k]) / 2, G = (Z[k] - conj Z[2N-k]) / 2i,
-// k in [0, N], written transposed as fgt[k][y].
+// Row y: z = f~ + i g~r (g~r = rotate_bilinear(g~, -theta), imageops.cpp:61-79,
+// exact fp64 index map) gathered once into a shared stash; group q forms
+// W_M^{nq}(z[n] + W_3^q z[n+K]) and FFTs it (E_q); then the real spectra
+// F = (Z[k'] + conj Z[M-k'])/2, G = (Z[k'] - conj Z[M-k'])/2i, Z[3k+q] = E_q[k],
+// for k' in [0, M/2] are written transposed as fgt[k'][y].
+constexpr int kXThreads = 384;
+
 template <int N>
-__global__ void __launch_bounds__(kRowThreads) k_xlat_rows(Params p) {
-    constexpr int T = N / 16;
-    constexpr int RPB = rows_per_block<N>();
-    constexpr int KF = Cfg<N>::kFloats, KH = Cfg<N>::kHalf;
+struct XRowGeom {
+    using G = Geom<N / 2, kXThreads>;
+    static constexpr int ROWS = G::PER_CTA / 3;
+    static constexpr int SP0 = N + N / 32;
+    static constexpr int SP = (SP0 % 32 == 0) ? SP0 + 16 : SP0;  // stash row stride (floats)
+    static constexpr size_t SMEM = ((size_t)2 * ROWS * SP + G::FLOATS) * sizeof(float);
+    static_assert(G::PER_CTA % 3 == 0, "three transforms per row");
+};
+
+template <int N>
+__global__ void __launch_bounds__(kXThreads) k_xlat_rows(Params p) {
+    constexpr int K = N / 2, M = 3 * K, H = M / 2;
+    using X = XRowGeom<N>;
+    using G = typename X::G;
+    constexpr int T = G::T, ROWS = X::ROWS, SP = X::SP;
     extern __shared__ float smem[];
+    float* st_re = smem;
+    float* st_im = smem + ROWS * SP;
+    float* xbase = smem + 2 * ROWS * SP;
     const int pair = blockIdx.y;
-    const int tr = threadIdx.x / T, t = threadIdx.x % T;
-    const int y = blockIdx.x * RPB + tr;
-    float* sa = smem + (2 * tr) * KF;
-    float* sbb = smem + (2 * tr + 1) * KF;
+    const int y0 = blockIdx.x * ROWS;
     const RotState rs = p.rot[pair];
     const float* ft = p.ft + (size_t)pair * N * N;
     const float* gt = p.gt + (size_t)pair * N * N;
     const double c0 = (N - 1) / 2.0;
-    const double vv = y - c0;
-    float2 v[16], w[16];
-#pragma unroll
-    for (int m = 0; m < 16; ++m) {
-        const int x = t + m * T;
+    // gather: ROWS rows x N cells over all threads, consecutive threads on consecutive x
+    for (int e = threadIdx.x; e < ROWS * N; e += kXThreads) {
+        const int yl = e / N, x = e % N;
+        const int y = y0 + yl;
         const float fv = ft[(size_t)y * N + x];
         float gv;
         if (rs.identity) {
             gv = gt[(size_t)y * N + x];
         } else {
-            const double u = x - c0;
+            const double u = x - c0, vv = y - c0;
             // (c + st*u) + ct*v and (c + ct*u) - st*v, no contraction
             const double sr = __dadd_rn(__dadd_rn(c0, __dmul_rn(rs.st, u)), __dmul_rn(rs.ct, vv));
             const double sc = __dsub_rn(__dadd_rn(c0, __dmul_rn(rs.ct, u)), __dmul_rn(rs.st, vv));
@@ -345,174 +394,234 @@ __global__ void __launch_bounds__(kRowThreads) k_xlat_rows(Params p) {
             const float a11 = (rin1 && cin1) ? gt[(size_t)(r0 + 1) * N + cc0 + 1] : 0.0f;
             gv = bilerp(fr, fc, a00, a01, a10, a11);
         }
-        v[m] = make_float2(fv, gv);
-        w[m] = cmul(v[m], __ldg(p.tw_2n + x));
-    }
-    fft_regs<N, -1>(v, t, sa, p.tw_n);
-    fft_regs<N, -1>(w, t, sbb, p.tw_n);
-#pragma unroll
-    for (int m = 0; m < 16; ++m) {
-        const int q = spad(t + m * T);
-        sa[q] = v[m].x;
-        sa[KH + q] = v[m].y;
-        sbb[q] = w[m].x;
-        sbb[KH + q] = w[m].y;
+        const int a = yl * SP + x + (x >> 5);
+        st_re[a] = fv;
+        st_im[a] = gv;
     }
     __syncthreads();
-    // write fgt[k][y0 .. y0+RPB) with consecutive threads on consecutive y
-    constexpr int KSTEP = kRowThreads / RPB;
-    const int yl = threadIdx.x % RPB, kk = threadIdx.x / RPB;
-    const int yy = blockIdx.x * RPB + yl;
-    const float* ea = smem + (2 * yl) * KF;      // E of row yy
-    const float* ob = smem + (2 * yl + 1) * KF;  // O of row yy
-    float4* dst = p.fgt + (size_t)pair * (N + 1) * N;
-    for (int k = kk; k <= N; k += KSTEP) {
-        // Z[k]: even k -> E[k/2], odd k -> O[(k-1)/2]; partner Z[2N-k]
-        const int kp = (2 * N - k) & (2 * N - 1);
-        float2 z1, z2;
-        if (k & 1) {
-            const int q = spad(k >> 1);
-            z1 = make_float2(ob[q], ob[KH + q]);
-        } else {
-            const int q = spad(k >> 1);
-            z1 = make_float2(ea[q], ea[KH + q]);
+    int tr, t;
+    G::map(threadIdx.x, tr, t);
+    const int yl = tr / 3, q = tr % 3;
+    {
+        const float2 w3q = w3(q);
+        float2 v[16];
+#pragma unroll
+        for (int m = 0; m < 16; ++m) {
+            const int n0 = t + m * T, n1 = n0 + K;
+            const int a0 = yl * SP + n0 + (n0 >> 5), a1 = yl * SP + n1 + (n1 >> 5);
+            const float2 s = cadd(make_float2(st_re[a0], st_im[a0]), cmul(w3q, make_float2(st_re[a1], st_im[a1])));
+            v[m] = q ? cmul(wm(p.tw_m, n0 * q), s) : s;
         }
-        if (kp & 1) {
-            const int q = spad(kp >> 1);
-            z2 = make_float2(ob[q], ob[KH + q]);
-        } else {
-            const int q = spad(kp >> 1);
-            z2 = make_float2(ea[q], ea[KH + q]);
-        }
-        // F = (z1 + conj z2)/2 ; G = (z1 - conj z2)/(2i) = (im, -re)/2 of (z1 - conj z2)
+        const auto b = G::lay(xbase, tr);
+        fft_regs<K, -1>(v, t, b, p.tw_k);
+#pragma unroll
+        for (int m = 0; m < 16; ++m) b.put(t + m * T, v[m]);
+    }
+    __syncthreads();
+    // separation + transposed write: consecutive threads on consecutive rows y
+    constexpr int KSTEP = kXThreads / ROWS;
+    const int ol = threadIdx.x % ROWS, kk = threadIdx.x / ROWS;
+    const auto e0 = G::lay(xbase, 3 * ol), e1 = G::lay(xbase, 3 * ol + 1), e2 = G::lay(xbase, 3 * ol + 2);
+    auto Z = [&](int kp) {  // Z[k'] = E_{k' mod 3}[k' / 3]
+        const int qq = kp % 3, k = kp / 3;
+        return qq == 0 ? e0.get(k) : (qq == 1 ? e1.get(k) : e2.get(k));
+    };
+    float4* dst = p.fgt + (size_t)pair * (H + 1) * N;
+    for (int kp = kk; kp <= H; kp += KSTEP) {
+        const float2 z1 = Z(kp), z2 = Z(kp == 0 ? 0 : M - kp);
+        // F = (z1 + conj z2)/2 ; G = (z1 - conj z2)/(2i)
         const float Fr = 0.5f * (z1.x + z2.x), Fi = 0.5f * (z1.y - z2.y);
         const float dr = z1.x - z2.x, di = z1.y + z2.y;
-        const float Gr = 0.5f * di, Gi = -0.5f * dr;
-        dst[(size_t)k * N + yy] = make_float4(Fr, Fi, Gr, Gi);
+        dst[(size_t)kp * N + y0 + ol] = make_float4(Fr, Fi, 0.5f * di, -0.5f * dr);
     }
 }
 
 // ---------------------------------------------------------------- K4
-// Column k of the row spectra: 2N-point transforms of the half-zero columns
-// F[:,k], G[:,k] (each as even/odd N-point FFTs), X = conj(F) G, inverse with
-// output pruning to the N lags ky in [-N/2, N/2):
-//   Y[ky] = e[j] + W_2N^{-j} o[j] (j < N/2, ky = j), e[j] - W_2N^{-j} o[j] (ky = j - N)
-// with e = IFFT_N(X_even), o = IFFT_N(X_odd). Rows are stored by surface row
-// i = half - ky (the world-flipped crop of matcher.cpp:171-182).
+// Column k' of the row spectra. Group q: F_q = FFT_K(W_M^{nq}(F[n] + W_3^q F[n+K]))
+// (transformed in buffer A and parked there), G_q likewise in buffer B,
+// X_q = conj(F_q) G_q, e_q = IFFT_K(X_q) (left in buffer B). Then the needed
+// lags ky in [-K, K) of IFFT_M(X) by a radix-3 combine:
+//   ky = n in [0, K):     sum_q W_M^{-nq} e_q[n]
+//   ky = n - K in [-K,0): sum_q W_M^{-nq} W_3^{q} e_q[n]
+// stored by surface row i = half - ky (the flip of matcher.cpp:171-182).
 template <int N>
-__global__ void __launch_bounds__(N / 2) k_xlat_cols(Params p) {
-    constexpr int T = N / 16;
-    constexpr int KF = Cfg<N>::kFloats;
+struct XColGeom {
+    static constexpr int T = N / 32;
+    // columns per CTA: 3 * COLS * T threads must fill whole warps
+    static constexpr int COLS = (T >= 32) ? 4 : ((T >= 4) ? 8 : 16);
+    static constexpr int PITCH = COLS + 1;
+    static constexpr int THREADS = 3 * COLS * T;
+    using G = Geom<N / 2, THREADS>;
+    static constexpr size_t FFT_FLOATS = (size_t)2 * G::FLOATS;
+    static constexpr size_t TILE_FLOATS = (size_t)2 * N * PITCH;
+    static constexpr size_t SMEM = (FFT_FLOATS > TILE_FLOATS ? FFT_FLOATS : TILE_FLOATS) * sizeof(float);
+};
+
+template <int N>
+__global__ void __launch_bounds__(XColGeom<N>::THREADS) k_xlat_cols(Params p) {
+    constexpr int K = N / 2, M = 3 * K, H = M / 2;
+    using X = XColGeom<N>;
+    using G = typename X::G;
+    constexpr int T = G::T, COLS = X::COLS, PITCH = X::PITCH;
+    constexpr int half = N / 2 - 1;
     extern __shared__ float smem[];
     const int pair = blockIdx.y;
-    const int c = threadIdx.x / T, t = threadIdx.x % T;
-    const int k = blockIdx.x * 8 + c;
-    const bool live = k <= N;  // last block holds only column N
-    const int kk = live ? k : N;
-    float* sb = smem + c * KF;
-    const float4* src = p.fgt + ((size_t)pair * (N + 1) + kk) * N;
-    // the [row][8 columns] output tile lives after the 8 FFT buffers
-    float2* tile = reinterpret_cast<float2*>(smem + 8 * KF);
-    constexpr int half = N / 2 - 1;
-    float2 a[16], b[16];
-    // odd bins first: tile <- +-W_2N^{-j} o[j]
+    int tr, t;
+    G::map(threadIdx.x, tr, t);
+    const int c = tr / 3, q = tr % 3;
+    const int kp = blockIdx.x * COLS + c;
+    const int kq = kp <= H ? kp : H;  // the last block may hold fewer columns
+    const auto bufA = G::lay(smem, tr);
+    const auto bufB = G::lay(smem + G::FLOATS, tr);
+    const float4* src = p.fgt + ((size_t)pair * (H + 1) + kq) * N;
+    const float2 w3q = w3(q);
+    float2 a[16];
 #pragma unroll
     for (int m = 0; m < 16; ++m) {
-        const float4 q = src[t + m * T];
-        const float2 tw = __ldg(p.tw_2n + t + m * T);
-        a[m] = cmul(make_float2(q.x, q.y), tw);
-        b[m] = cmul(make_float2(q.z, q.w), tw);
+        const int n0 = t + m * T;
+        const float4 u0 = src[n0], u1 = src[n0 + K];
+        const float2 s = cadd(make_float2(u0.x, u0.y), cmul(w3q, make_float2(u1.x, u1.y)));
+        a[m] = q ? cmul(wm(p.tw_m, n0 * q), s) : s;
     }
-    fft_regs<N, -1>(a, t, sb, p.tw_n);
-    fft_regs<N, -1>(b, t, sb, p.tw_n);
+    fft_regs<K, -1>(a, t, bufA, p.tw_k);
 #pragma unroll
-    for (int m = 0; m < 16; ++m) a[m] = cmul(cconj(a[m]), b[m]);
-    fft_regs<N, +1>(a, t, sb, p.tw_n);
+    for (int m = 0; m < 16; ++m) bufA.put(t + m * T, a[m]);  // park F_q (own slots)
 #pragma unroll
     for (int m = 0; m < 16; ++m) {
-        const int j = t + m * T;
-        const float2 wo = cmul(cconj(__ldg(p.tw_2n + j)), a[m]);  // W_2N^{-j} o[j]
-        const int ky = j < N / 2 ? j : j - N;
-        tile[(half - ky) * 8 + c] = j < N / 2 ? wo : make_float2(-wo.x, -wo.y);
+        const int n0 = t + m * T;
+        const float4 u0 = src[n0], u1 = src[n0 + K];
+        const float2 s = cadd(make_float2(u0.z, u0.w), cmul(w3q, make_float2(u1.z, u1.w)));
+        a[m] = q ? cmul(wm(p.tw_m, n0 * q), s) : s;
     }
-    // even bins: tile += e[j] (same thread, same slot: no barrier needed)
+    fft_regs<K, -1>(a, t, bufB, p.tw_k);
 #pragma unroll
-    for (int m = 0; m < 16; ++m) {
-        const float4 q = src[t + m * T];
-        a[m] = make_float2(q.x, q.y);
-        b[m] = make_float2(q.z, q.w);
+    for (int m = 0; m < 16; ++m) a[m] = cmul(cconj(bufA.get(t + m * T)), a[m]);  // conj(F) G
+    fft_regs<K, +1>(a, t, bufB, p.tw_k);
+#pragma unroll
+    for (int m = 0; m < 16; ++m) bufB.put(t + m * T, a[m]);
+    __syncthreads();
+    // radix-3 combine: group q handles the slots m = q, q+3, ... of its column
+    const auto e0 = G::lay(smem + G::FLOATS, 3 * c), e1 = G::lay(smem + G::FLOATS, 3 * c + 1),
+               e2 = G::lay(smem + G::FLOATS, 3 * c + 2);
+    const float2 w31 = w3(1), w32 = w3(2);
+    float2 accp[6], accn[6];
+#pragma unroll
+    for (int j = 0; j < 6; ++j) {
+        const int m = q + 3 * j;
+        if (m < 16) {
+            const int n0 = t + m * T;
+            const float2 x0 = e0.get(n0);
+            const float2 x1 = cmul(cconj(wm(p.tw_m, n0)), e1.get(n0));
+            const float2 x2 = cmul(cconj(wm(p.tw_m, 2 * n0)), e2.get(n0));
+            accp[j] = cadd(x0, cadd(x1, x2));
+            accn[j] = cadd(x0, cadd(cmul(w31, x1), cmul(w32, x2)));
+        }
     }
-    fft_regs<N, -1>(a, t, sb, p.tw_n);
-    fft_regs<N, -1>(b, t, sb, p.tw_n);
+    __syncthreads();  // the buffers become the output tile
+    float2* tile = reinterpret_cast<float2*>(smem);  // [N rows][PITCH]
 #pragma unroll
-    for (int m = 0; m < 16; ++m) a[m] = cmul(cconj(a[m]), b[m]);
-    fft_regs<N, +1>(a, t, sb, p.tw_n);
-#pragma unroll
-    for (int m = 0; m < 16; ++m) {
-        const int j = t + m * T;
-        const int ky = j < N / 2 ? j : j - N;
-        float2* slot = tile + (half - ky) * 8 + c;
-        *slot = cadd(*slot, a[m]);
+    for (int j = 0; j < 6; ++j) {
+        const int m = q + 3 * j;
+        if (m < 16) {
+            const int n0 = t + m * T;
+            tile[(half - n0) * PITCH + c] = accp[j];
+            tile[(half - (n0 - K)) * PITCH + c] = accn[j];
+        }
     }
     __syncthreads();
-    float2* dst = p.zbuf + (size_t)pair * N * (N + 1);
-    const int ncols = min(8, N + 1 - blockIdx.x * 8);
-    for (int o = threadIdx.x; o < N * 8; o += N / 2) {
-        const int i = o >> 3, cc = o & 7;
-        if (cc < ncols) dst[(size_t)i * (N + 1) + blockIdx.x * 8 + cc] = tile[o];
+    float2* dst = p.zbuf + (size_t)pair * N * (H + 1);
+    const int ncols = min(COLS, H + 1 - (int)blockIdx.x * COLS);
+    for (int o = threadIdx.x; o < N * COLS; o += blockDim.x) {
+        const int i = o / COLS, cc = o % COLS;
+        if (cc < ncols) dst[(size_t)i * (H + 1) + blockIdx.x * COLS + cc] = tile[i * PITCH + cc];
     }
 }
 
 // ---------------------------------------------------------------- K5
-// Surface row i: the length-2N real inverse along x of the Hermitian half
-// Y[0..N] as one N-point complex inverse FFT:
-//   A[k] = Y[k] + conj Y[N-k], B[k] = (Y[k] - conj Y[N-k]) W_2N^{-k},
-//   z = IFFT_N(A + iB), x[2n] = Re z[n], x[2n+1] = Im z[n];
-// scaled by 1/P^2 (spectral.cpp:145), cropped to lags [-(N/2-1), N/2]
-// (surface col j = lag + half), plus this block's hard argmax.
+// Surface row i: real inverse of length M along x from the Hermitian half
+// Y[0..M/2] as one complex inverse of length M/2 = 3 K2 (K2 = K/2):
+//   A[k] = Y[k] + conj Y[M/2-k], B[k] = (Y[k] - conj Y[M/2-k]) W_M^{-k},
+//   z = IFFT_{M/2}(A + iB) = sum_q W_M^{-2nq} W_3^{-sq} IFFT_K2(Z_q)[n0], n = n0 + s K2,
+//   x[2n] = Re z[n], x[2n+1] = Im z[n];
+// group q inverts Z_q; scaled by 1/M^2, cropped to lags kx in [-(N/2-1), N/2]
+// (surface col j = kx + half), plus this block's hard argmax (lowest index on ties).
 template <int N>
-__global__ void __launch_bounds__(kRowThreads) k_xlat_out(Params p) {
-    constexpr int T = N / 16;
-    constexpr int RPB = rows_per_block<N>();
-    extern __shared__ float smem[];
-    __shared__ float red_v[kRowThreads / 32];
-    __shared__ int red_i[kRowThreads / 32];
-    const int pair = blockIdx.y;
-    const int tr = threadIdx.x / T, t = threadIdx.x % T;
-    const int i = blockIdx.x * RPB + tr;
-    float* sb = smem + tr * Cfg<N>::kFloats;
-    const float2* yrow = p.zbuf + ((size_t)pair * N + i) * (N + 1);
-    float2 v[16];
-#pragma unroll
-    for (int m = 0; m < 16; ++m) {
-        const int k = t + m * T;
-        const float2 a = yrow[k], b = cconj(yrow[N - k]);
-        const float2 A = cadd(a, b);
-        const float2 B = cmul(csub(a, b), cconj(__ldg(p.tw_2n + k)));
-        v[m] = make_float2(A.x - B.y, A.y + B.x);  // A + iB
-    }
-    fft_regs<N, +1>(v, t, sb, p.tw_n);
-    const float scale = 1.0f / ((float)(2 * N) * (float)(2 * N));
+struct XOutGeom {
+    static constexpr int K2 = N / 4;
+    static constexpr int T = K2 / 16;
+    static constexpr int ROWS0 = 128 / T;                 // 384 threads at 3 transforms per row
+    static constexpr int ROWS = ROWS0 < N ? ROWS0 : N;
+    static constexpr int THREADS = 3 * ROWS * T;
+    using G = Geom<K2, THREADS>;
+    static constexpr size_t SMEM = (size_t)G::FLOATS * sizeof(float);
+};
+
+template <int N>
+__global__ void __launch_bounds__(XOutGeom<N>::THREADS) k_xlat_out(Params p) {
+    constexpr int K = N / 2, M = 3 * K, H = M / 2;
+    using X = XOutGeom<N>;
+    using G = typename X::G;
+    constexpr int THREADS = X::THREADS, ROWS = X::ROWS;
+    constexpr int NW = THREADS / 32;
+    constexpr int T = G::T;
     constexpr int half = N / 2 - 1;
+    extern __shared__ float smem[];
+    __shared__ float red_v[NW];
+    __shared__ int red_i[NW];
+    const int pair = blockIdx.y;
+    int tr, t;
+    G::map(threadIdx.x, tr, t);
+    const int rl = tr / 3, q = tr % 3;
+    const int i = blockIdx.x * ROWS + rl;
+    const float2* yrow = p.zbuf + ((size_t)pair * N + i) * (H + 1);
+    const auto buf = G::lay(smem, tr);
+    {
+        float2 v[16];
+#pragma unroll
+        for (int m = 0; m < 16; ++m) {
+            const int k = 3 * (t + m * T) + q;
+            const float2 a = yrow[k], b = cconj(yrow[H - k]);
+            const float2 A = cadd(a, b);
+            const float2 B = cmul(csub(a, b), cconj(wm(p.tw_m, k)));
+            v[m] = make_float2(A.x - B.y, A.y + B.x);  // A + iB
+        }
+        fft_regs<X::K2, +1>(v, t, buf, p.tw_k2);
+#pragma unroll
+        for (int m = 0; m < 16; ++m) buf.put(t + m * T, v[m]);
+    }
+    __syncthreads();
+    const float scale = 1.0f / ((float)M * (float)M);
     float* srow = (p.xy_surf ? p.xy_surf : p.surf) + ((size_t)pair * N + i) * N;
     float best_v = -INFINITY;
     int best_i = 0x7fffffff;
+    auto emit = [&](int kx, float val) {
+        const int j = kx + half;
+        srow[j] = val;
+        const int li = i * N + j;
+        if (val > best_v || (val == best_v && li < best_i)) {
+            best_v = val;
+            best_i = li;
+        }
+    };
+    const auto e0 = G::lay(smem, 3 * rl), e1 = G::lay(smem, 3 * rl + 1), e2 = G::lay(smem, 3 * rl + 2);
+    const float2 w31 = w3(1), w32 = w3(2);
 #pragma unroll
-    for (int m = 0; m < 16; ++m) {
-        const int nn = t + m * T;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int pos = 2 * nn + h;                       // position in [0, 2N)
-            const int lag = pos <= N / 2 ? pos : pos - 2 * N;  // valid when in [-(N/2-1), N/2]
-            if (lag >= -half && lag <= N / 2) {
-                const float val = (h ? v[m].y : v[m].x) * scale;
-                const int j = lag + half;
-                srow[j] = val;
-                const int li = i * N + j;
-                if (val > best_v || (val == best_v && li < best_i)) {
-                    best_v = val;
-                    best_i = li;
-                }
+    for (int j = 0; j < 6; ++j) {
+        const int m = q + 3 * j;
+        if (m < 16) {
+            const int n0 = t + m * T;
+            const float2 x0 = e0.get(n0);
+            const float2 x1 = cmul(cconj(wm(p.tw_m, 2 * n0)), e1.get(n0));
+            const float2 x2 = cmul(cconj(wm(p.tw_m, 4 * n0)), e2.get(n0));
+            const float2 z0 = cadd(x0, cadd(x1, x2));                        // s = 0
+            const float2 z2 = cadd(x0, cadd(cmul(w31, x1), cmul(w32, x2)));  // s = 2: W_3^{-2q} = W_3^{q}
+            emit(2 * n0, z0.x * scale);                   // pos 2n0, 2n0+1 -> kx = pos
+            emit(2 * n0 + 1, z0.y * scale);
+            if (n0 >= 1) emit(2 * n0 - K, z2.x * scale);  // pos 2n0+2K -> kx = 2n0-K
+            emit(2 * n0 + 1 - K, z2.y * scale);
+            if (n0 == 0) {  // s = 1, n0 = 0: pos K -> kx = N/2
+                const float2 z1 = cadd(x0, cadd(cmul(cconj(w31), x1), cmul(cconj(w32), x2)));  // W_3^{-q}
+                emit(K, z1.x * scale);
             }
         }
     }
@@ -532,7 +641,7 @@ __global__ void __launch_bounds__(kRowThreads) k_xlat_out(Params p) {
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        for (int w = 1; w < kRowThreads / 32; ++w)
+        for (int w = 1; w < NW; ++w)
             if (red_v[w] > best_v || (red_v[w] == best_v && red_i[w] < best_i)) {
                 best_v = red_v[w];
                 best_i = red_i[w];
@@ -688,17 +797,16 @@ cudaError_t set_smem(K kernel, size_t bytes) {
 
 template <int N>
 cudaError_t rot_rows(const Params& p, cudaStream_t s) {
-    constexpr int RPB = rows_per_block<N>();
-    const size_t sm = (size_t)RPB * Cfg<N>::kFloats * sizeof(float);
+    const size_t sm = (size_t)RowG<N>::FLOATS * sizeof(float);
     cudaError_t e = set_smem(k_rot_rows<N>, sm);
     if (e != cudaSuccess) return e;
-    k_rot_rows<N><<<dim3(N / RPB, p.batch), kRowThreads, sm, s>>>(p);
+    k_rot_rows<N><<<dim3(N / RowG<N>::PER_CTA, p.batch), kRowThreads, sm, s>>>(p);
     return cudaGetLastError();
 }
 
 template <int N>
 cudaError_t rot_cols(const Params& p, cudaStream_t s) {
-    const size_t sm = (size_t)16 * Cfg<N>::kFloats * sizeof(float);
+    const size_t sm = (size_t)2 * part_floats<N, 16>() * sizeof(float);
     cudaError_t e = set_smem(k_rot_cols<N>, sm);
     if (e != cudaSuccess) return e;
     k_rot_cols<N><<<dim3(N / 16, p.batch), N, sm, s>>>(p);
@@ -707,30 +815,29 @@ cudaError_t rot_cols(const Params& p, cudaStream_t s) {
 
 template <int N>
 cudaError_t xlat_rows(const Params& p, cudaStream_t s) {
-    constexpr int RPB = rows_per_block<N>();
-    const size_t sm = (size_t)2 * RPB * Cfg<N>::kFloats * sizeof(float);
-    cudaError_t e = set_smem(k_xlat_rows<N>, sm);
+    using X = XRowGeom<N>;
+    cudaError_t e = set_smem(k_xlat_rows<N>, X::SMEM);
     if (e != cudaSuccess) return e;
-    k_xlat_rows<N><<<dim3(N / RPB, p.batch), kRowThreads, sm, s>>>(p);
+    k_xlat_rows<N><<<dim3(N / X::ROWS, p.batch), kXThreads, X::SMEM, s>>>(p);
     return cudaGetLastError();
 }
 
 template <int N>
 cudaError_t xlat_cols(const Params& p, cudaStream_t s) {
-    const size_t sm = (size_t)8 * Cfg<N>::kFloats * sizeof(float) + (size_t)8 * N * sizeof(float2);
-    cudaError_t e = set_smem(k_xlat_cols<N>, sm);
+    using X = XColGeom<N>;
+    constexpr int H = 3 * N / 4;
+    cudaError_t e = set_smem(k_xlat_cols<N>, X::SMEM);
     if (e != cudaSuccess) return e;
-    k_xlat_cols<N><<<dim3((N + 1 + 7) / 8, p.batch), N / 2, sm, s>>>(p);
+    k_xlat_cols<N><<<dim3((H + 1 + X::COLS - 1) / X::COLS, p.batch), X::THREADS, X::SMEM, s>>>(p);
     return cudaGetLastError();
 }
 
 template <int N>
 cudaError_t xlat_out(const Params& p, cudaStream_t s) {
-    constexpr int RPB = rows_per_block<N>();
-    const size_t sm = (size_t)RPB * Cfg<N>::kFloats * sizeof(float);
-    cudaError_t e = set_smem(k_xlat_out<N>, sm);
+    using X = XOutGeom<N>;
+    cudaError_t e = set_smem(k_xlat_out<N>, X::SMEM);
     if (e != cudaSuccess) return e;
-    k_xlat_out<N><<<dim3(N / RPB, p.batch), kRowThreads, sm, s>>>(p);
+    k_xlat_out<N><<<dim3(N / X::ROWS, p.batch), X::THREADS, X::SMEM, s>>>(p);
     return cudaGetLastError();
 }
 
@@ -738,11 +845,11 @@ cudaError_t xlat_out(const Params& p, cudaStream_t s) {
 
 int rows_per_block_out(int n) {
     switch (n) {
-        case 64: return rows_per_block<64>();
-        case 128: return rows_per_block<128>();
-        case 256: return rows_per_block<256>();
-        case 512: return rows_per_block<512>();
-        case 1024: return rows_per_block<1024>();
+        case 64: return XOutGeom<64>::ROWS;
+        case 128: return XOutGeom<128>::ROWS;
+        case 256: return XOutGeom<256>::ROWS;
+        case 512: return XOutGeom<512>::ROWS;
+        case 1024: return XOutGeom<1024>::ROWS;
         default: return 1;
     }
 }

@@ -44,16 +44,18 @@ struct Params {
     // workspace
     float* ft;     // masked f  [batch][N][N]
     float* gt;     // masked g
-    float2* zbuf;  // K1a->K1b spectra [batch][N][N]; reused as K4->K5 rows [batch][N][N+1]
+    float2* zbuf;  // K1a->K1b spectra [batch][N][N]; reused as K4->K5 rows [batch][N][3N/4+1]
     float* mag;    // |F|,|G| band-passed half planes, tiled [batch][2][N/16][N][8]; reused as surface
-    float4* fgt;   // row spectra of f, g_rot, transposed [batch][N+1][N] (F.re, F.im, G.re, G.im)
+    float4* fgt;   // row spectra of f, g_rot (length 3N/2), transposed [batch][3N/4+1][N] (F, G)
     float* surf;   // translation surface [batch][N][N]
     Partial* part; // K5 per-block argmax [batch][N / rows_per_block]
     RotState* rot; // [batch]
     int* flags;    // [batch] bit0 non-finite, bit1 mask out of [0,1]
     // tables
     const float2* tw_n;   // exp(-2 pi i k / N), k < N
-    const float2* tw_2n;  // exp(-2 pi i k / 2N), k < 2N
+    const float2* tw_k;   // exp(-2 pi i k / K), K = N/2
+    const float2* tw_k2;  // exp(-2 pi i k / (K/2))
+    const float2* tw_m;   // exp(-2 pi i k / M), M = 3N/2
     const float* hann;    // N
     const int2* band;     // per centred row: [u_lo, u_hi] in band (empty: lo > hi)
     const PolarTap* taps; // [n_theta][n_live]
