@@ -370,33 +370,56 @@ __global__ void __launch_bounds__(kXThreads) k_xlat_rows(Params p) {
     const float* ft = p.ft + (size_t)pair * N * N;
     const float* gt = p.gt + (size_t)pair * N * N;
     const double c0 = (N - 1) / 2.0;
-    // gather: ROWS rows x N cells over all threads, consecutive threads on consecutive x
-    for (int e = threadIdx.x; e < ROWS * N; e += kXThreads) {
-        const int yl = e / N, x = e % N;
-        const int y = y0 + yl;
-        const float fv = ft[(size_t)y * N + x];
-        float gv;
-        if (rs.identity) {
-            gv = gt[(size_t)y * N + x];
-        } else {
-            const double u = x - c0, vv = y - c0;
-            // (c + st*u) + ct*v and (c + ct*u) - st*v, no contraction
-            const double sr = __dadd_rn(__dadd_rn(c0, __dmul_rn(rs.st, u)), __dmul_rn(rs.ct, vv));
-            const double sc = __dsub_rn(__dadd_rn(c0, __dmul_rn(rs.ct, u)), __dmul_rn(rs.st, vv));
-            const double r0f = floor(sr), c0f = floor(sc);
-            const int r0 = (int)r0f, cc0 = (int)c0f;
-            const float fr = (float)(sr - r0f), fc = (float)(sc - c0f);
-            const bool rin0 = (unsigned)r0 < (unsigned)N, rin1 = (unsigned)(r0 + 1) < (unsigned)N;
-            const bool cin0 = (unsigned)cc0 < (unsigned)N, cin1 = (unsigned)(cc0 + 1) < (unsigned)N;
-            const float a00 = (rin0 && cin0) ? gt[(size_t)r0 * N + cc0] : 0.0f;
-            const float a01 = (rin0 && cin1) ? gt[(size_t)r0 * N + cc0 + 1] : 0.0f;
-            const float a10 = (rin1 && cin0) ? gt[(size_t)(r0 + 1) * N + cc0] : 0.0f;
-            const float a11 = (rin1 && cin1) ? gt[(size_t)(r0 + 1) * N + cc0 + 1] : 0.0f;
-            gv = bilerp(fr, fc, a00, a01, a10, a11);
+    // gather: ROWS rows x N cells over all threads, consecutive threads on
+    // consecutive x; U cells per thread per round with every load issued
+    // before any use (memory-level parallelism for the L2/DRAM latency)
+    constexpr int CELLS = ROWS * N;
+    constexpr int U = 6;
+#pragma unroll 1
+    for (int e0 = threadIdx.x; e0 < CELLS; e0 += U * kXThreads) {
+        float fv[U], tap[U][4], frs[U], fcs[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int e = e0 + u * kXThreads;
+            const bool live = e < CELLS;
+            const int yl = live ? e / N : 0, x = live ? e % N : 0;
+            const int y = y0 + yl;
+            int r0 = y, cc0 = x;
+            float fr = 0.f, fc = 0.f;
+            bool rin0 = live, rin1 = false, cin0 = true, cin1 = false;
+            if (!rs.identity) {  // rotate_bilinear(g~, -theta): -theta == 0.0 returns g~ itself
+                const double uu = x - c0, vv = y - c0;
+                // (c + st*u) + ct*v and (c + ct*u) - st*v, no contraction
+                const double sr = __dadd_rn(__dadd_rn(c0, __dmul_rn(rs.st, uu)), __dmul_rn(rs.ct, vv));
+                const double sc = __dsub_rn(__dadd_rn(c0, __dmul_rn(rs.ct, uu)), __dmul_rn(rs.st, vv));
+                const double r0f = floor(sr), c0f = floor(sc);
+                r0 = (int)r0f;
+                cc0 = (int)c0f;
+                fr = (float)(sr - r0f);
+                fc = (float)(sc - c0f);
+                rin0 = live && (unsigned)r0 < (unsigned)N;
+                rin1 = live && (unsigned)(r0 + 1) < (unsigned)N;
+                cin0 = (unsigned)cc0 < (unsigned)N;
+                cin1 = (unsigned)(cc0 + 1) < (unsigned)N;
+            }
+            frs[u] = fr;
+            fcs[u] = fc;
+            fv[u] = live ? ft[(size_t)y * N + x] : 0.f;
+            tap[u][0] = (rin0 && cin0) ? gt[(size_t)r0 * N + cc0] : 0.0f;
+            tap[u][1] = (rin0 && cin1) ? gt[(size_t)r0 * N + cc0 + 1] : 0.0f;
+            tap[u][2] = (rin1 && cin0) ? gt[(size_t)(r0 + 1) * N + cc0] : 0.0f;
+            tap[u][3] = (rin1 && cin1) ? gt[(size_t)(r0 + 1) * N + cc0 + 1] : 0.0f;
         }
-        const int a = yl * SP + x + (x >> 5);
-        st_re[a] = fv;
-        st_im[a] = gv;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int e = e0 + u * kXThreads;
+            if (e < CELLS) {
+                const int yl = e / N, x = e % N;
+                const int a = yl * SP + x + (x >> 5);
+                st_re[a] = fv[u];
+                st_im[a] = bilerp(frs[u], fcs[u], tap[u][0], tap[u][1], tap[u][2], tap[u][3]);
+            }
+        }
     }
     __syncthreads();
     int tr, t;
