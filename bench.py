@@ -37,7 +37,7 @@ sys.path.insert(0, ROOT)
 METRIC = "scan-pair registrations/sec (rot+trans search)"
 UNIT = "pairs/s"
 KERNEL_NAMES = ("rot_rows", "rot_cols", "rot_polar", "theta_in", "xlat_rows", "xlat_cols", "xlat_out",
-                "finalize", "mag_unpack")
+                "finalize", "rot_gather", "polar_to_cart", "mag_unpack")
 
 
 def workload_desc(cid: int) -> str:
@@ -63,18 +63,21 @@ def pair_bytes(n: int, n_theta: int, pad: int, masks: bool = True, s_in: float |
 
 
 def kernel_alg_bytes(name: str, n: int) -> float:
-    """Compulsory DRAM bytes per pair of each of OUR kernels (DESIGN.md §3)."""
+    """Compulsory DRAM bytes per pair of each of OUR kernels (DESIGN.md §3.4)."""
     nn = n * n
+    h1 = 3 * n // 4 + 1  # M/2 + 1 spectral bins of the length M = 3N/2 translation transforms
     return {
         "rot_rows": 16 * nn + 8 * nn + 8 * nn,            # f,g,mf,mg in; f~,g~ out; Z out
         "rot_cols": 8 * nn + 4 * nn,                      # Z in; |F|,|G| half planes out
-        "rot_polar": 4 * nn,                              # magnitude planes in
-        "xlat_rows": 8 * nn + 16 * n * (n + 1),           # f~,g~ in; row spectra out
-        "xlat_cols": 16 * n * (n + 1) + 8 * n * (n + 1),  # row spectra in; Y out
-        "xlat_out": 8 * n * (n + 1) + 4 * nn,             # Y in; surface out
+        "rot_gather": 4 * nn,                             # magnitude planes in (polar gather)
+        "rot_polar": 0.0,                                 # profiles only (fp64 correlation)
+        "xlat_rows": 8 * nn + 16 * n * h1,                # f~,g~ in; row spectra (F,G; M/2+1 bins) out
+        "xlat_cols": 16 * n * h1 + 8 * n * h1,            # row spectra in; Y (N lags x M/2+1) out
+        "xlat_out": 8 * n * h1 + 4 * nn,                  # Y in; surface out
         "finalize": 0.0,
         "theta_in": 0.0,
         "mag_unpack": 0.0,
+        "polar_to_cart": 4 * 400 * 3768 + 4 * nn,         # one raw sweep in, one grid out (per launch: f or g)
     }[name]
 
 
@@ -219,9 +222,17 @@ def run_ours(args):
     m = fb.Matcher(cfg, max_batch=per, device=local, chunk=args.chunk)
     out = torch.empty(per * fb.RESULT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
+    polar = args.config == 3
+    if polar:  # C3: the raw sweeps are the input; K0 runs inside every step
+        pf, pg, _ = fb.synth_polar_device(spec, first, per, device=local)
+
+    def step():
+        if polar:
+            return m.match_polar(pf, pg, mf, mg, range_res=spec.range_res, delta=delta, out=out, stream=stream)
+        return m.match_device(f, g, mf, mg, delta=delta, out=out, stream=stream)
 
     for _ in range(args.warmup):
-        m.match_device(f, g, mf, mg, delta=delta, out=out, stream=stream)
+        step()
     torch.cuda.synchronize(dev)
     launches_per_step = m.launches_last
     res = fb.decode_results(out)
@@ -233,7 +244,7 @@ def run_ours(args):
     with ClockSampler(local) as clk:
         ev0.record(stream)
         for _ in range(args.steps):
-            m.match_device(f, g, mf, mg, delta=delta, out=out, stream=stream)
+            step()
         ev1.record(stream)
         torch.cuda.synchronize(dev)
     barrier(world)
@@ -250,7 +261,7 @@ def run_ours(args):
 
     # per-kernel breakdown: one instrumented step (events around every kernel)
     m.set_profiling(True)
-    m.match_device(f, g, mf, mg, delta=delta, out=out, stream=stream)
+    step()
     torch.cuda.synchronize(dev)
     kt = m.kernel_times()
     m.set_profiling(False)
@@ -266,7 +277,8 @@ def run_ours(args):
                 "traffic": None if traffic is None else traffic * pairs_per_launch,
                 "alg_bytes_per_launch": alg, "avg_launch_ms": dom_ms / dom_launches,
                 "kernel_share": round(dom_ms / sum(v[0] for v in kt.values()), 3)}
-    bpair = pair_bytes(cfg.n_xy, cfg.n_theta, cfg.pad_angle)
+    bpair = pair_bytes(cfg.n_xy, cfg.n_theta, cfg.pad_angle,
+                       s_in=(8.0 * spec.n_az * spec.n_range) if polar else None)
     pipeline = {"b_pair_bytes": bpair, "achieved_gbs": round(value * bpair / 1e9 / world, 1),
                 "frac_of_measured_peak_per_gpu": round(value * bpair / world / (peak * 1e9), 4),
                 "frac_of_8TBps_per_gpu": round(value * bpair / world / 8e12, 4),

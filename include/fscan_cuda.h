@@ -101,6 +101,16 @@ fscan_status fscan_match_batch(fscan_ctx* ctx, const float* d_f, const float* d_
                                double delta, fscan_pair_result* d_out, double* d_theta_surface,
                                float* d_xy_surface, void* stream);
 
+/* Config-3 hot path: raw polar sweeps (batch x n_az x n_range floats, device)
+ * are resampled on the device to N x N Cartesian grids at `delta` metres per
+ * cell (K0, see fscan_polar_to_cart_batch) and matched like fscan_match_batch.
+ * Masks (optional) are Cartesian N x N. */
+fscan_status fscan_match_batch_polar(fscan_ctx* ctx, const float* d_polar_f, const float* d_polar_g,
+                                     int n_az, int n_range, double range_res, const float* d_mask_f,
+                                     const float* d_mask_g, int batch, double delta,
+                                     fscan_pair_result* d_out, double* d_theta_surface,
+                                     float* d_xy_surface, void* stream);
+
 /* Same on HOST pointers (pageable or pinned): host->device copies, compute and
  * device->host copy of the results, overlapped chunk by chunk; synchronous.
  * Returns the first failing pair's status (FSCAN_ERR_NONFINITE, ...). */
@@ -143,7 +153,8 @@ int fscan_ctx_launches_last(const fscan_ctx* ctx);
 /* Profiling mode: subsequent calls run their chunks serially on one stream
  * with CUDA events around every kernel. fscan_ctx_kernel_times() synchronises
  * and returns, per kernel kind (0 rot_rows, 1 rot_cols, 2 rot_polar,
- * 3 theta_in, 4 xlat_rows, 5 xlat_cols, 6 xlat_out, 7 finalize, 8 mag_unpack),
+ * 3 theta_in, 4 xlat_rows, 5 xlat_cols, 6 xlat_out, 7 finalize, 8 rot_gather,
+ * 9 polar_to_cart, 10 mag_unpack),
  * the summed milliseconds and launch counts of the last call. */
 fscan_status fscan_ctx_set_profiling(fscan_ctx* ctx, int on);
 fscan_status fscan_ctx_kernel_times(fscan_ctx* ctx, double* ms, int* launches, int n_kinds);

@@ -105,6 +105,8 @@ SYMBOLS = {
     "fscan_ctx_set_chunk": (C.c_int, [_P, C.c_int]),
     "fscan_match_batch": (C.c_int, [_P, _P, _P, _P, _P, C.c_int, C.c_double, _P, _P, _P, _P]),
     "fscan_match_batch_host": (C.c_int, [_P, _P, _P, _P, _P, C.c_int, C.c_double, _P, _P, _P]),
+    "fscan_match_batch_polar": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, C.c_double, _P, _P, C.c_int, C.c_double,
+                                          _P, _P, _P, _P]),
     "fscan_estimate_rotation_batch": (C.c_int, [_P, _P, _P, C.c_int, _P, _P, _P]),
     "fscan_estimate_translation_batch": (C.c_int, [_P, _P, _P, C.c_int, C.c_double, _P, _P, _P, _P]),
     "fscan_band_magnitude_batch": (C.c_int, [_P, _P, C.c_int, _P, _P]),
@@ -267,7 +269,7 @@ class Matcher:
         return lib().fscan_ctx_launches_last(self._h)
 
     KERNELS = ("rot_rows", "rot_cols", "rot_polar", "theta_in", "xlat_rows", "xlat_cols", "xlat_out",
-               "finalize", "mag_unpack")
+               "finalize", "rot_gather", "polar_to_cart", "mag_unpack")
 
     def set_profiling(self, on: bool):
         self._check(lib().fscan_ctx_set_profiling(self._h, int(bool(on))), "set_profiling")
@@ -294,6 +296,19 @@ class Matcher:
         st = lib().fscan_match_batch(self._h, _ptr(f), _ptr(g), _ptr(mf), _ptr(mg), b, float(delta),
                                      _ptr(out), _ptr(theta_surface), _ptr(xy_surface), _stream_ptr(stream))
         self._check(st, "fscan_match_batch")
+        return out
+
+    def match_polar(self, pf, pg, mf=None, mg=None, *, range_res: float, delta: float, out=None,
+                    theta_surface=None, xy_surface=None, stream=None):
+        """Config-3 path: raw polar sweeps [B, n_az, n_range] (CUDA tensors) -> K0 -> match."""
+        import torch
+        b, n_az, n_range = (int(x) for x in pf.shape)
+        if out is None:
+            out = torch.empty(b * RESULT_DTYPE.itemsize, dtype=torch.uint8, device=pf.device)
+        st = lib().fscan_match_batch_polar(self._h, _ptr(pf), _ptr(pg), n_az, n_range, float(range_res), _ptr(mf),
+                                           _ptr(mg), b, float(delta), _ptr(out), _ptr(theta_surface),
+                                           _ptr(xy_surface), _stream_ptr(stream))
+        self._check(st, "fscan_match_batch_polar")
         return out
 
     def match_host(self, f: np.ndarray, g: np.ndarray, mf=None, mg=None, *, delta: float,

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -19,7 +20,7 @@ using namespace fscan_detail;
 namespace {
 
 constexpr double kPi = 3.141592653589793;  // std::numbers::pi (geometry.hpp:11)
-constexpr int kLanes = 2;                  // concurrent chunk pipelines
+constexpr int kMaxLanes = 8;               // concurrent chunk pipelines (FSCAN_LANES, default 2)
 
 struct Lane {
     cudaStream_t stream = nullptr;
@@ -32,9 +33,11 @@ struct Lane {
     float4* fgt = nullptr;
     Partial* part = nullptr;
     RotState* rot = nullptr;
+    double* prof = nullptr;
     int* flags = nullptr;
     // host-API staging
     float* in = nullptr;  // 4 grids x chunk
+    float* cart = nullptr;  // K0 output (polar API): 2 grids x chunk
     fscan_pair_result* res = nullptr;
     double* tsurf = nullptr;
     float* xsurf = nullptr;
@@ -61,7 +64,10 @@ struct fscan_ctx {
     float* hann = nullptr;
     int2* band = nullptr;
     PolarTap* taps = nullptr;
-    Lane lanes[kLanes];
+    Lane lanes_[kMaxLanes];
+    int nlanes = 2;
+    Lane* lbegin() { return lanes_; }
+    Lane* lend() { return lanes_ + nlanes; }
     cudaEvent_t start_ev = nullptr;
     // profiling: per-kernel events of the last call, serialised on lane 0
     int profiling = 0;
@@ -71,6 +77,12 @@ struct fscan_ctx {
 };
 
 namespace {
+
+struct LaneRange {
+    fscan_ctx* c;
+    Lane* begin() const { return c->lbegin(); }
+    Lane* end() const { return c->lend(); }
+};
 
 fscan_status fail(fscan_ctx* ctx, fscan_status st, const std::string& msg) {
     if (ctx) ctx->err = msg;
@@ -190,8 +202,10 @@ void free_lane(Lane& l) {
     cudaFree(l.fgt);
     cudaFree(l.part);
     cudaFree(l.rot);
+    cudaFree(l.prof);
     cudaFree(l.flags);
     cudaFree(l.in);
+    cudaFree(l.cart);
     cudaFree(l.res);
     cudaFree(l.tsurf);
     cudaFree(l.xsurf);
@@ -208,6 +222,7 @@ fscan_status alloc_lane(fscan_ctx* ctx, Lane& l, int chunk) {
     CK(cudaMalloc(&l.fgt, (3 * n / 4 + 1) * n * sizeof(float4) * chunk));
     CK(cudaMalloc(&l.part, sizeof(Partial) * nparts * chunk));
     CK(cudaMalloc(&l.rot, sizeof(RotState) * chunk));
+    CK(cudaMalloc(&l.prof, sizeof(double) * 2 * std::max(1, ctx->cfg.n_theta) * chunk));
     CK(cudaMalloc(&l.flags, sizeof(int) * chunk));
     return FSCAN_OK;
 }
@@ -234,6 +249,7 @@ Params base_params(fscan_ctx* ctx, Lane& l, int batch, double delta) {
     p.surf = l.mag;  // the magnitude planes are dead once K2 has run
     p.part = l.part;
     p.rot = l.rot;
+    p.prof = l.prof;
     p.flags = l.flags;
     p.tw_n = ctx->tw_n;
     p.tw_k = ctx->tw_k;
@@ -260,6 +276,7 @@ enum class Stages { Full, Rotation, Translation, Magnitude };
 
 // Kernel ids for per-kernel profiling (fscan_ctx_kernel_times).
 enum KernelId { kRotRows = 0, kRotCols, kRotPolar, kThetaIn, kXlatRows, kXlatCols, kXlatOut, kFinalize,
+                kRotGather, kPolarToCart,
                 kMagUnpack, kNumKernels };
 
 struct ProfEvent {
@@ -286,6 +303,7 @@ fscan_status run_chunk(fscan_ctx* ctx, Lane& l, Params p, Stages what, int* laun
     }
     if (what != Stages::Translation) {
         if (ctx->cfg.n_theta > 1) FSCAN_LAUNCH(kRotCols, launch_rot_cols);
+        if (ctx->cfg.n_theta > 1) FSCAN_LAUNCH(kRotGather, launch_rot_gather);
         FSCAN_LAUNCH(kRotPolar, launch_rot_polar);
     } else {
         FSCAN_LAUNCH(kThetaIn, launch_theta_in);
@@ -336,18 +354,18 @@ fscan_status check_ctx(fscan_ctx* ctx, int batch) {
 template <typename F>
 fscan_status drive(fscan_ctx* ctx, int batch, cudaStream_t user, F&& per_chunk) {
     CK(cudaEventRecord(ctx->start_ev, user));
-    for (auto& l : ctx->lanes) CK(cudaStreamWaitEvent(l.stream, ctx->start_ev, 0));
+    for (Lane& l : LaneRange{ctx}) CK(cudaStreamWaitEvent(l.stream, ctx->start_ev, 0));
     ctx->launches_last = 0;
     ctx->prof.clear();
     ctx->ev_used = 0;
-    const int lanes = ctx->profiling ? 1 : kLanes;
+    const int lanes = ctx->profiling ? 1 : ctx->nlanes;
     int li = 0;
     for (int off = 0; off < batch; off += ctx->chunk, li = (li + 1) % lanes) {
         const int cnt = std::min(ctx->chunk, batch - off);
-        fscan_status st = per_chunk(ctx->lanes[li], off, cnt);
+        fscan_status st = per_chunk(ctx->lanes_[li], off, cnt);
         if (st != FSCAN_OK) return st;
     }
-    for (auto& l : ctx->lanes) {
+    for (Lane& l : LaneRange{ctx}) {
         CK(cudaEventRecord(l.done, l.stream));
         CK(cudaStreamWaitEvent(user, l.done, 0));
     }
@@ -471,14 +489,17 @@ fscan_status fscan_ctx_create(int device, const fscan_config* cfg_in, int max_ba
     CK(cudaMemcpy(ctx->band, band.data(), sizeof(int2) * n, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(ctx->taps, taps.data(), sizeof(PolarTap) * taps.size(), cudaMemcpyHostToDevice));
 
-    // default chunk: about 1 GiB of workspace per lane
-    const double per_pair = (double)n * n * (8 + 4) + (double)n * (n + 1) * (8 + 16);
+    // lanes (concurrent chunk pipelines) and chunk size: FSCAN_LANES / FSCAN_CHUNK
+    // override the defaults (2 lanes, ~1 GiB of workspace per lane)
+    if (const char* e = std::getenv("FSCAN_LANES")) ctx->nlanes = std::clamp(std::atoi(e), 1, kMaxLanes);
+    const double per_pair = (double)n * n * (8 + 4 + 8) + (double)n * (3 * n / 4 + 1) * 16;
     int chunk = (int)std::max(1.0, std::floor((1024.0 * 1024 * 1024) / per_pair));
+    if (const char* e = std::getenv("FSCAN_CHUNK")) chunk = std::max(1, std::atoi(e));
     chunk = std::min(chunk, max_batch);
     ctx->chunk = chunk;
     ctx->alloc_chunk = chunk;
     CK(cudaEventCreateWithFlags(&ctx->start_ev, cudaEventDisableTiming));
-    for (auto& l : ctx->lanes) {
+    for (Lane& l : LaneRange{ctx}) {
         CK(cudaStreamCreateWithFlags(&l.stream, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&l.done, cudaEventDisableTiming));
         fscan_status a = alloc_lane(ctx, l, chunk);
@@ -490,7 +511,7 @@ fscan_status fscan_ctx_create(int device, const fscan_config* cfg_in, int max_ba
 void fscan_ctx_destroy(fscan_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
-    for (auto& l : ctx->lanes) {
+    for (Lane& l : LaneRange{ctx}) {
         if (l.stream) cudaStreamSynchronize(l.stream);
         free_lane(l);
         if (l.stream) cudaStreamDestroy(l.stream);
@@ -520,7 +541,7 @@ fscan_status fscan_ctx_set_chunk(fscan_ctx* ctx, int pairs) {
     if (pairs == 0) pairs = ctx->alloc_chunk;
     if (pairs > ctx->alloc_chunk) {
         cudaSetDevice(ctx->device);
-        for (auto& l : ctx->lanes) {
+        for (Lane& l : LaneRange{ctx}) {
             cudaStreamSynchronize(l.stream);
             const bool had_host = l.in != nullptr;
             free_lane(l);
@@ -553,6 +574,47 @@ fscan_status fscan_match_batch(fscan_ctx* ctx, const float* d_f, const float* d_
         Params p = base_params(ctx, l, cnt, delta);
         p.f = d_f + off * nn;
         p.g = d_g + off * nn;
+        p.mf = d_mf ? d_mf + off * nn : nullptr;
+        p.mg = d_mg ? d_mg + off * nn : nullptr;
+        p.out = d_out + off;
+        p.theta_surf = d_tsurf ? d_tsurf + (size_t)off * nt : nullptr;
+        p.xy_surf = d_xsurf ? d_xsurf + off * nn : nullptr;
+        return run_chunk(ctx, l, p, Stages::Full, &ctx->launches_last);
+    });
+}
+
+fscan_status fscan_match_batch_polar(fscan_ctx* ctx, const float* d_pf, const float* d_pg, int n_az,
+                                     int n_range, double range_res, const float* d_mf, const float* d_mg,
+                                     int batch, double delta, fscan_pair_result* d_out, double* d_tsurf,
+                                     float* d_xsurf, void* stream) {
+    fscan_status st = check_ctx(ctx, batch);
+    if (st != FSCAN_OK) return st;
+    std::lock_guard<std::mutex> g(ctx->mu);
+    if (!ctx->tw_n) return fail(ctx, FSCAN_ERR_INVALID_ARGUMENT, "context was not created successfully");
+    if (!d_pf || !d_pg || !d_out || ((d_mf == nullptr) != (d_mg == nullptr)) || !(delta > 0.0) || n_az < 1 ||
+        n_range < 1 || !(range_res > 0.0))
+        return fail(ctx, FSCAN_ERR_INVALID_ARGUMENT, "fscan_match_batch_polar: bad pointers or geometry");
+    if (batch == 0) return FSCAN_OK;
+    const size_t nn = (size_t)ctx->n * ctx->n, np = (size_t)n_az * n_range;
+    const int nt = ctx->cfg.n_theta;
+    for (Lane& l : LaneRange{ctx})
+        if (!l.cart) CK(cudaMalloc(&l.cart, 2 * nn * sizeof(float) * ctx->alloc_chunk));
+    return drive(ctx, batch, (cudaStream_t)stream, [&](Lane& l, int off, int cnt) {
+        // K0: both sweeps of the chunk -> Cartesian grids in the lane's staging buffer
+        fscan_status s2;
+        if ((s2 = launch(ctx, l, kPolarToCart, [&] {
+                 return launch_polar_to_cart(d_pf + off * np, cnt, n_az, n_range, range_res, ctx->n, delta,
+                                             l.cart, l.stream);
+             }, &ctx->launches_last)) != FSCAN_OK)
+            return s2;
+        if ((s2 = launch(ctx, l, kPolarToCart, [&] {
+                 return launch_polar_to_cart(d_pg + off * np, cnt, n_az, n_range, range_res, ctx->n, delta,
+                                             l.cart + nn * cnt, l.stream);
+             }, &ctx->launches_last)) != FSCAN_OK)
+            return s2;
+        Params p = base_params(ctx, l, cnt, delta);
+        p.f = l.cart;
+        p.g = l.cart + nn * cnt;
         p.mf = d_mf ? d_mf + off * nn : nullptr;
         p.mg = d_mg ? d_mg + off * nn : nullptr;
         p.out = d_out + off;
@@ -630,15 +692,15 @@ fscan_status fscan_match_batch_host(fscan_ctx* ctx, const float* f, const float*
     if (batch == 0) return FSCAN_OK;
     const size_t nn = (size_t)ctx->n * ctx->n;
     const int nt = ctx->cfg.n_theta;
-    for (auto& l : ctx->lanes) {
+    for (Lane& l : LaneRange{ctx}) {
         fscan_status a = alloc_host_staging(ctx, l, ctx->alloc_chunk);
         if (a != FSCAN_OK) return a;
     }
     ctx->launches_last = 0;
     int li = 0;
     // lane-alternating chunks: H2D(i+1) overlaps compute(i) on the other lane
-    for (int off = 0; off < batch; off += ctx->chunk, li = (li + 1) % kLanes) {
-        Lane& l = ctx->lanes[li];
+    for (int off = 0; off < batch; off += ctx->chunk, li = (li + 1) % ctx->nlanes) {
+        Lane& l = ctx->lanes_[li];
         const int cnt = std::min(ctx->chunk, batch - off);
         cudaStream_t s = l.stream;
         float* df = l.in;
@@ -670,7 +732,7 @@ fscan_status fscan_match_batch_host(fscan_ctx* ctx, const float* f, const float*
         // the staging buffers of this lane are reused two chunks later: the
         // stream order already serialises that reuse.
     }
-    for (auto& l : ctx->lanes) CK(cudaStreamSynchronize(l.stream));
+    for (Lane& l : LaneRange{ctx}) CK(cudaStreamSynchronize(l.stream));
     for (int i = 0; i < batch; ++i)
         if (out[i].status != FSCAN_OK) {
             const fscan_status bad = (fscan_status)out[i].status;

@@ -161,9 +161,12 @@ struct Lay {
 };
 
 // Floats of one real (or imaginary) part for a group of W transforms of length N.
+// The +2 makes consecutive groups start 4 banks apart (2 parts per group), so
+// loops that read several transforms' buffers at the same index (separation,
+// radix-3 combines, output staging) spread over the banks.
 template <int N, int W>
 __host__ __device__ constexpr int part_floats() {
-    return W == 1 ? N + 2 : W * (N + N / 16);
+    return W == 1 ? N + 2 : W * (N + N / 16) + 2;
 }
 
 // Thread/transform geometry of kernels whose transforms are "rows": T = N/16

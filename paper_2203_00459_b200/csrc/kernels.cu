@@ -142,38 +142,20 @@ __device__ __forceinline__ float tile_at(const float* m, int n, int r, int u) {
     return __ldg(m + ((size_t)(u >> 3) * n + r) * 8 + (u & 7));
 }
 
-__global__ void __launch_bounds__(kPolarThreads) k_rot_polar(Params p) {
-    extern __shared__ double dsm[];
-    const int pair = blockIdx.x;
-    const int nt = p.n_theta, L = p.L, pad = p.pad, n = p.n;
-    double* A = dsm;           // wrap-extended radial-sum profiles, length L
-    double* B = dsm + L;
-    double* s = dsm + 2 * L;   // theta surface, n_theta
-    double* red_v = s + nt;    // block reduction scratch (32 entries each)
-    int* red_i = (int*)(red_v + 32);
+// K2a: radial sums of the bilinear polar resample (cart2pol) of |F| and |G|,
+// one warp per azimuth row, kGatherCtas CTAs per pair; fp64 sums written to
+// p.prof[pair][2][n_theta].
+constexpr int kGatherCtas = 8;
+
+__global__ void __launch_bounds__(kPolarThreads) k_rot_gather(Params p) {
+    const int pair = blockIdx.y;
+    const int nt = p.n_theta, n = p.n;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nwarps = kPolarThreads / 32;
-    RotState* rs = p.rot + pair;
-
-    if (nt == 1) {  // matcher.cpp:103-110
-        if (threadIdx.x == 0) {
-            rs->theta = 0.0;
-            rs->st = 0.0;
-            rs->ct = 1.0;
-            rs->peak = 0.0;
-            rs->hard = 0.0;
-            rs->bin = 0;
-            rs->identity = 1;
-            if (p.theta_surf) p.theta_surf[pair] = 0.0;
-            if (p.theta_only) p.theta_only[pair] = 0.0;
-        }
-        return;
-    }
-
     const float* mf = p.mag + (size_t)pair * 2 * n * (n / 2);
     const float* mg = mf + (size_t)n * (n / 2);
-    // radial sums of the bilinear polar resample (cart2pol) of |F| and |G|
-    for (int i = warp; i < nt; i += nwarps) {
+    double* prof = p.prof + (size_t)pair * 2 * nt;
+    for (int i = blockIdx.x * nwarps + warp; i < nt; i += gridDim.x * nwarps) {
         double af = 0.0, ag = 0.0;
         const PolarTap* row = p.taps + (size_t)i * p.n_live;
         constexpr int U = 4;  // independent entries in flight per lane (memory-level parallelism)
@@ -208,16 +190,48 @@ __global__ void __launch_bounds__(kPolarThreads) k_rot_polar(Params p) {
             ag += __shfl_xor_sync(0xffffffffu, ag, o);
         }
         if (lane == 0) {
-            // wrap_pad (imageops.cpp:101-113): padded row q holds profile row (q - pad) mod nt
-            for (int q = i + pad; q < L; q += nt) {
-                A[q] = af;
-                B[q] = ag;
-            }
-            for (int q = i + pad - nt; q >= 0; q -= nt) {
-                A[q] = af;
-                B[q] = ag;
-            }
+            prof[i] = af;
+            prof[nt + i] = ag;
         }
+    }
+}
+
+// K2b: angular correlation of the profiles, hard + soft argmax over theta.
+__global__ void __launch_bounds__(kPolarThreads) k_rot_polar(Params p) {
+    extern __shared__ double dsm[];
+    const int pair = blockIdx.x;
+    const int nt = p.n_theta, L = p.L, pad = p.pad, n = p.n;
+    double* A = dsm;           // wrap-extended radial-sum profiles, length L
+    double* B = dsm + L;
+    double* s = dsm + 2 * L;   // theta surface, n_theta
+    double* red_v = s + nt;    // block reduction scratch (32 entries each)
+    int* red_i = (int*)(red_v + 32);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nwarps = kPolarThreads / 32;
+    RotState* rs = p.rot + pair;
+
+    if (nt == 1) {  // matcher.cpp:103-110
+        if (threadIdx.x == 0) {
+            rs->theta = 0.0;
+            rs->st = 0.0;
+            rs->ct = 1.0;
+            rs->peak = 0.0;
+            rs->hard = 0.0;
+            rs->bin = 0;
+            rs->identity = 1;
+            if (p.theta_surf) p.theta_surf[pair] = 0.0;
+            if (p.theta_only) p.theta_only[pair] = 0.0;
+        }
+        return;
+    }
+
+    // wrap_pad (imageops.cpp:101-113): padded row q holds profile row (q - pad) mod nt
+    const double* prof = p.prof + (size_t)pair * 2 * nt;
+    for (int q = threadIdx.x; q < L; q += kPolarThreads) {
+        int i = (q - pad) % nt;
+        if (i < 0) i += nt;
+        A[q] = prof[i];
+        B[q] = prof[nt + i];
     }
     __syncthreads();
     // s[k] = (1/C) sum_q A[q] B[(q + lag) mod L], lag = k - nt/2
@@ -882,6 +896,12 @@ cudaError_t launch_rot_cols(const Params& p, cudaStream_t s) { FSCAN_DISPATCH_N(
 cudaError_t launch_xlat_rows(const Params& p, cudaStream_t s) { FSCAN_DISPATCH_N(p.n, xlat_rows) }
 cudaError_t launch_xlat_cols(const Params& p, cudaStream_t s) { FSCAN_DISPATCH_N(p.n, xlat_cols) }
 cudaError_t launch_xlat_out(const Params& p, cudaStream_t s) { FSCAN_DISPATCH_N(p.n, xlat_out) }
+
+cudaError_t launch_rot_gather(const Params& p, cudaStream_t s) {
+    if (p.n_theta == 1) return cudaSuccess;
+    k_rot_gather<<<dim3(kGatherCtas, p.batch), kPolarThreads, 0, s>>>(p);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_rot_polar(const Params& p, cudaStream_t s) {
     const size_t sm = (size_t)(2 * p.L + p.n_theta + 32) * sizeof(double) + 32 * sizeof(int);

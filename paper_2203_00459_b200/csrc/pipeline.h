@@ -50,6 +50,7 @@ struct Params {
     float* surf;   // translation surface [batch][N][N]
     Partial* part; // K5 per-block argmax [batch][N / rows_per_block]
     RotState* rot; // [batch]
+    double* prof;  // K2a radial-sum profiles [batch][2][n_theta]
     int* flags;    // [batch] bit0 non-finite, bit1 mask out of [0,1]
     // tables
     const float2* tw_n;   // exp(-2 pi i k / N), k < N
@@ -77,7 +78,8 @@ struct Params {
 // Launch the stages; each returns cudaGetLastError() of its launch.
 cudaError_t launch_rot_rows(const Params& p, cudaStream_t s);        // K1a
 cudaError_t launch_rot_cols(const Params& p, cudaStream_t s);        // K1b
-cudaError_t launch_rot_polar(const Params& p, cudaStream_t s);       // K2
+cudaError_t launch_rot_gather(const Params& p, cudaStream_t s);      // K2a
+cudaError_t launch_rot_polar(const Params& p, cudaStream_t s);       // K2b
 cudaError_t launch_theta_in(const Params& p, cudaStream_t s);        // stage API: theta from caller
 cudaError_t launch_xlat_rows(const Params& p, cudaStream_t s);       // K3
 cudaError_t launch_xlat_cols(const Params& p, cudaStream_t s);       // K4

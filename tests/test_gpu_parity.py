@@ -318,3 +318,25 @@ def test_cpp_drop_in_api(fb, dev, tmp_path):
     print(out.stdout[-3000:])
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
     assert "ALL PASSED" in out.stdout
+
+
+def test_match_polar_equals_k0_then_match(fb, orc, dev):
+    """Config-3 API: raw sweeps in, K0 inside the call; identical to K0 + match."""
+    cfg, delta, _ = fb.baseline_config(3)
+    spec = fb.synth_spec(3)
+    pf, pg, _ = fb.synth_polar_host(spec, 2, 3)
+    _, _, mf, mg, _ = fb.synth_pairs_host(spec, 2, 3)
+    PF, PG, MF, MG = to_dev(dev, pf, pg, mf, mg)
+    m = fb.Matcher(cfg, max_batch=3)
+    a = fb.decode_results(m.match_polar(PF, PG, MF, MG, range_res=spec.range_res, delta=delta))
+    cf = fb.polar_to_cart(PF, range_res=spec.range_res, n=512, delta=delta)
+    cg = fb.polar_to_cart(PG, range_res=spec.range_res, n=512, delta=delta)
+    b = fb.decode_results(m.match_device(cf, cg, MF, MG, delta=delta))
+    torch.cuda.synchronize()
+    assert a.tobytes() == b.tobytes()
+    oc = oracle_cfg(orc, cfg)
+    cfn, cgn = cf.cpu().numpy(), cg.cpu().numpy()
+    for i in range(3):
+        r = orc.scan_match(cfn[i], cgn[i], oc, delta, mf[i], mg[i])
+        assert (a[i]["theta_bin"], a[i]["xy_row"], a[i]["xy_col"]) == (r.theta_bin, r.xy_row, r.xy_col)
+        assert abs(a[i]["theta"] - r.theta) <= THETA_TOL
