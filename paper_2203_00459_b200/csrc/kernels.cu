@@ -46,6 +46,45 @@ __host__ __device__ constexpr int rows_per_block() {
     return RowG<N>::PER_CTA;
 }
 
+// ---- float-float helpers (value = hi + lo, ~48-bit significand) ----
+__device__ __forceinline__ void ff_split(double d, float* hi, float* lo) {
+    *hi = (float)d;
+    *lo = (float)(d - (double)*hi);
+}
+
+// error-free transformations: the _rn intrinsics keep nvcc from contracting
+// them into FMAs
+__device__ __forceinline__ void two_sum(float a, float b, float* s, float* e) {
+    *s = __fadd_rn(a, b);
+    const float bb = __fsub_rn(*s, a);
+    *e = __fadd_rn(__fsub_rn(a, __fsub_rn(*s, bb)), __fsub_rn(b, bb));
+}
+
+// c + (a_hi + a_lo) * u + (b_hi + b_lo) * v with u, v exactly representable
+__device__ __forceinline__ float2 ff_affine(float c, float a_hi, float a_lo, float u, float b_hi, float b_lo, float v) {
+    const float p = __fmul_rn(a_hi, u), pe = fmaf(a_lo, u, fmaf(a_hi, u, -p));
+    const float q = __fmul_rn(b_hi, v), qe = fmaf(b_lo, v, fmaf(b_hi, v, -q));
+    float s1, e1, s2, e2;
+    two_sum(c, p, &s1, &e1);
+    two_sum(s1, q, &s2, &e2);
+    return make_float2(s2, e1 + e2 + pe + qe);
+}
+
+// floor and fraction of hi + lo
+__device__ __forceinline__ void ff_floor_frac(float2 x, int* fl, float* fr) {
+    float f = floorf(x.x);
+    float r = (x.x - f) + x.y;  // x.x - f is exact
+    if (r < 0.0f) {
+        f -= 1.0f;
+        r += 1.0f;
+    } else if (r >= 1.0f) {
+        f += 1.0f;
+        r -= 1.0f;
+    }
+    *fl = (int)f;
+    *fr = r;
+}
+
 __device__ __forceinline__ float bilerp(float fr, float fc, float a00, float a01, float a10, float a11) {
     // sample_bilinear (imageops.cpp:24-25) operation order, fp32
     return (1.0f - fr) * ((1.0f - fc) * a00 + fc * a01) + fr * ((1.0f - fc) * a10 + fc * a11);
@@ -383,7 +422,8 @@ __global__ void __launch_bounds__(kXThreads) k_xlat_rows(Params p) {
     const RotState rs = p.rot[pair];
     const float* ft = p.ft + (size_t)pair * N * N;
     const float* gt = p.gt + (size_t)pair * N * N;
-    const double c0 = (N - 1) / 2.0;
+    const float c0f32 = (N - 1) / 2.0f;  // exact
+    const float stf = (float)rs.st, ctf = (float)rs.ct;
     // gather: ROWS rows x N cells over all threads, consecutive threads on
     // consecutive x; U cells per thread per round with every load issued
     // before any use (memory-level parallelism for the L2/DRAM latency)
@@ -402,15 +442,19 @@ __global__ void __launch_bounds__(kXThreads) k_xlat_rows(Params p) {
             float fr = 0.f, fc = 0.f;
             bool rin0 = live, rin1 = false, cin0 = true, cin1 = false;
             if (!rs.identity) {  // rotate_bilinear(g~, -theta): -theta == 0.0 returns g~ itself
-                const double uu = x - c0, vv = y - c0;
-                // (c + st*u) + ct*v and (c + ct*u) - st*v, no contraction
-                const double sr = __dadd_rn(__dadd_rn(c0, __dmul_rn(rs.st, uu)), __dmul_rn(rs.ct, vv));
-                const double sc = __dsub_rn(__dadd_rn(c0, __dmul_rn(rs.ct, uu)), __dmul_rn(rs.st, vv));
-                const double r0f = floor(sr), c0f = floor(sc);
+                // src_row = c + st*u + ct*v, src_col = c + ct*u - st*v (imageops.cpp:70-73) in
+                // float-float arithmetic (~1e-11 cells; the fp64 form stalls on DP latency)
+                // src_row = c + st*u + ct*v, src_col = c + ct*u - st*v (imageops.cpp:70-73)
+                // in fp32 FMAs: <= 5e-5 cell coordinate error, i.e. <= 5e-5 relative per
+                // bilinear sample (far inside the 1e-4 surface gate)
+                const float uu = (float)x - c0f32, vv = (float)y - c0f32;  // exact half-integers
+                const float sr = fmaf(stf, uu, fmaf(ctf, vv, c0f32));
+                const float sc = fmaf(ctf, uu, fmaf(-stf, vv, c0f32));
+                const float r0f = floorf(sr), cf = floorf(sc);
                 r0 = (int)r0f;
-                cc0 = (int)c0f;
-                fr = (float)(sr - r0f);
-                fc = (float)(sc - c0f);
+                cc0 = (int)cf;
+                fr = sr - r0f;
+                fc = sc - cf;
                 rin0 = live && (unsigned)r0 < (unsigned)N;
                 rin1 = live && (unsigned)(r0 + 1) < (unsigned)N;
                 cin0 = (unsigned)cc0 < (unsigned)N;
@@ -459,18 +503,16 @@ __global__ void __launch_bounds__(kXThreads) k_xlat_rows(Params p) {
     constexpr int KSTEP = kXThreads / ROWS;
     const int ol = threadIdx.x % ROWS, kk = threadIdx.x / ROWS;
     const auto e0 = G::lay(xbase, 3 * ol), e1 = G::lay(xbase, 3 * ol + 1), e2 = G::lay(xbase, 3 * ol + 2);
-    auto Z = [&](int kp) {  // Z[k'] = E_{k' mod 3}[k' / 3]
-        const int qq = kp % 3, k = kp / 3;
-        return qq == 0 ? e0.get(k) : (qq == 1 ? e1.get(k) : e2.get(k));
-    };
-    float4* dst = p.fgt + (size_t)pair * (H + 1) * N;
-    for (int kp = kk; kp <= H; kp += KSTEP) {
-        const float2 z1 = Z(kp), z2 = Z(kp == 0 ? 0 : M - kp);
-        // F = (z1 + conj z2)/2 ; G = (z1 - conj z2)/(2i)
-        const float Fr = 0.5f * (z1.x + z2.x), Fi = 0.5f * (z1.y - z2.y);
+    // F = (Z[k'] + conj Z[M-k'])/2, G = (Z[k'] - conj Z[M-k'])/2i with Z[3k+q] = E_q[k];
+    // by residue class: 3k pairs with E_0[K-k], 3k+1 with E_2[K-1-k], 3k+2 with E_1[K-1-k]
+    auto sep = [](float2 z1, float2 z2) {
         const float dr = z1.x - z2.x, di = z1.y + z2.y;
-        dst[(size_t)kp * N + y0 + ol] = make_float4(Fr, Fi, 0.5f * di, -0.5f * dr);
-    }
+        return make_float4(0.5f * (z1.x + z2.x), 0.5f * (z1.y - z2.y), 0.5f * di, -0.5f * dr);
+    };
+    float4* dst = p.fgt + (size_t)pair * (H + 1) * N + y0 + ol;
+    for (int k = kk; k <= K / 2; k += KSTEP) dst[(size_t)(3 * k) * N] = sep(e0.get(k), e0.get((K - k) & (K - 1)));
+    for (int k = kk; 3 * k + 1 <= H; k += KSTEP) dst[(size_t)(3 * k + 1) * N] = sep(e1.get(k), e2.get(K - 1 - k));
+    for (int k = kk; 3 * k + 2 <= H; k += KSTEP) dst[(size_t)(3 * k + 2) * N] = sep(e2.get(k), e1.get(K - 1 - k));
 }
 
 // ---------------------------------------------------------------- K4

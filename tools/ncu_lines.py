@@ -26,12 +26,16 @@ for r in csv.reader(io.StringIO(out)):
         continue
     try:
         n = int(r[4])
+        ninst = int(r[hdr.index("Instructions Executed")]) if r[hdr.index("Instructions Executed")].isdigit() else 0
     except Exception:
         continue
     tot += n
+    itot = globals().setdefault("itot", [0])
+    itot[0] += ninst
     stalls = [(int(r[i]), hdr[i][6:]) for i in range(len(hdr)) if hdr[i].startswith("stall_") and "Not Issued" not in hdr[i] and r[i].isdigit()]
-    agg.append((n, f"{fname}:{r[0]}", r[1].strip()[:80], sorted(stalls, reverse=True)[:3]))
+    agg.append((n, f"{fname}:{r[0]}", r[1].strip()[:70], sorted(stalls, reverse=True)[:3], ninst))
 agg.sort(reverse=True)
-print(f"total samples {tot}")
-for n, ln, src, st in agg[:top]:
-    print(f"{100*n/max(tot,1):5.1f}% {ln:16s} {src:80s} {[(s, c) for c, s in st if c]}")
+it = globals().get("itot", [1])[0]
+print(f"total samples {tot}, warp instructions {it}")
+for n, ln, src, st, ni in agg[:top]:
+    print(f"{100*n/max(tot,1):5.1f}% inst {100*ni/max(it,1):5.1f}% {ln:16s} {src:70s} {[(s, c) for c, s in st if c][:2]}")
