@@ -177,6 +177,13 @@ __global__ void __launch_bounds__(N) k_rot_cols(Params p) {
 // ---------------------------------------------------------------- K2
 constexpr int kPolarThreads = 512;
 
+// q-range split of the angular correlation so that (lag quads) x parts fills the CTA
+__host__ __device__ inline int polar_parts(int nt) {
+    const int quads = (nt + 3) / 4;
+    const int np = kPolarThreads / (quads > 0 ? quads : 1);
+    return np < 1 ? 1 : (np > 8 ? 8 : np);
+}
+
 __device__ __forceinline__ float tile_at(const float* m, int n, int r, int u) {
     return __ldg(m + ((size_t)(u >> 3) * n + r) * 8 + (u & 7));
 }
@@ -240,11 +247,11 @@ __global__ void __launch_bounds__(kPolarThreads) k_rot_polar(Params p) {
     extern __shared__ double dsm[];
     const int pair = blockIdx.x;
     const int nt = p.n_theta, L = p.L, pad = p.pad, n = p.n;
-    double* A = dsm;           // wrap-extended radial-sum profiles, length L
-    double* B = dsm + L;
-    double* s = dsm + 2 * L;   // theta surface, n_theta
-    double* red_v = s + nt;    // block reduction scratch (32 entries each)
-    int* red_i = (int*)(red_v + 32);
+    double* A = dsm;                 // wrap-extended radial-sum profiles, length L
+    double* B = dsm + L;             // length L + nt + 4 (see below)
+    double* s = B + L + nt + 4;      // theta surface, n_theta
+    double* red_v;                   // block reduction scratch (32 entries each), after the partials
+    int* red_i;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nwarps = kPolarThreads / 32;
     RotState* rs = p.rot + pair;
@@ -264,29 +271,62 @@ __global__ void __launch_bounds__(kPolarThreads) k_rot_polar(Params p) {
         return;
     }
 
-    // wrap_pad (imageops.cpp:101-113): padded row q holds profile row (q - pad) mod nt
+    // wrap_pad (imageops.cpp:101-113): padded row q holds profile row (q - pad) mod nt.
+    // B is stored circularly extended, Bx[j] = B[(j - nt/2) mod L], so the score
+    // s[k] = (1/C) sum_q A[q] B[(q + k - nt/2) mod L] is
+    // sum_q A[q] Bx[q + k] without modular indexing.
     const double* prof = p.prof + (size_t)pair * 2 * nt;
+    const int np = polar_parts(nt);
+    double* Bx = B;                        // L + nt + 4 (tail padding for the last lag quad)
+    double* part = s + nt;                 // np x nt partial sums
+    red_v = part + (size_t)np * nt;
+    red_i = (int*)(red_v + 32);
     for (int q = threadIdx.x; q < L; q += kPolarThreads) {
         int i = (q - pad) % nt;
         if (i < 0) i += nt;
         A[q] = prof[i];
-        B[q] = prof[nt + i];
+    }
+    for (int j = threadIdx.x; j < L + nt + 4; j += kPolarThreads) {
+        int qq = (j - nt / 2) % L;
+        if (qq < 0) qq += L;
+        int i = (qq - pad) % nt;
+        if (i < 0) i += nt;
+        Bx[j] = prof[nt + i];
     }
     __syncthreads();
-    // s[k] = (1/C) sum_q A[q] B[(q + lag) mod L], lag = k - nt/2
+    // register-blocked: each item owns 4 consecutive lags over one of np q-ranges
+    {
+        const int quads = (nt + 3) / 4;
+        const int item = threadIdx.x;
+        if (item < quads * np) {
+            const int k0 = 4 * (item % quads), pi = item / quads;
+            const int q0 = (int)((long)L * pi / np), q1 = (int)((long)L * (pi + 1) / np);
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+            double b0 = Bx[q0 + k0], b1 = Bx[q0 + k0 + 1], b2 = Bx[q0 + k0 + 2];
+            for (int q = q0; q < q1; ++q) {
+                const double a = A[q], b3 = Bx[q + k0 + 3];
+                a0 = fma(a, b0, a0);
+                a1 = fma(a, b1, a1);
+                a2 = fma(a, b2, a2);
+                a3 = fma(a, b3, a3);
+                b0 = b1;
+                b1 = b2;
+                b2 = b3;
+            }
+            double* pr = part + (size_t)pi * nt + k0;
+            if (k0 < nt) pr[0] = a0;
+            if (k0 + 1 < nt) pr[1] = a1;
+            if (k0 + 2 < nt) pr[2] = a2;
+            if (k0 + 3 < nt) pr[3] = a3;
+        }
+    }
+    __syncthreads();
     const double invC = 1.0 / (double)p.C;
     double best_v = -INFINITY;
     int best_i = 0x7fffffff;
     for (int k = threadIdx.x; k < nt; k += kPolarThreads) {
-        const int lag = k - nt / 2;
         double acc = 0.0;
-        if (lag >= 0) {
-            for (int q = 0; q < L - lag; ++q) acc = fma(A[q], B[q + lag], acc);
-            for (int q = L - lag; q < L; ++q) acc = fma(A[q], B[q + lag - L], acc);
-        } else {
-            for (int q = 0; q < -lag; ++q) acc = fma(A[q], B[q + lag + L], acc);
-            for (int q = -lag; q < L; ++q) acc = fma(A[q], B[q + lag], acc);
-        }
+        for (int pi = 0; pi < np; ++pi) acc += part[(size_t)pi * nt + k];  // fixed order: deterministic
         const double sv = acc * invC;
         s[k] = sv;
         if (sv > best_v) {  // k increases per thread: strict > keeps the lowest index
@@ -946,7 +986,8 @@ cudaError_t launch_rot_gather(const Params& p, cudaStream_t s) {
 }
 
 cudaError_t launch_rot_polar(const Params& p, cudaStream_t s) {
-    const size_t sm = (size_t)(2 * p.L + p.n_theta + 32) * sizeof(double) + 32 * sizeof(int);
+    const size_t sm = (size_t)(2 * p.L + 4 + p.n_theta * (2 + polar_parts(p.n_theta)) + 32) * sizeof(double) +
+                      32 * sizeof(int);
     cudaError_t e = set_smem(k_rot_polar, sm);
     if (e != cudaSuccess) return e;
     k_rot_polar<<<p.batch, kPolarThreads, sm, s>>>(p);
