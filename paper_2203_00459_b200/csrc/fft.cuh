@@ -17,14 +17,12 @@
 // stage lands back in the input register slots, so only S-1 shared-memory
 // exchanges are needed (one for N <= 256, two for 512..2048).
 //
-// Exchange buffers are split real/imag (4-byte banks). Two bank-conflict-free
-// layouts (verified for every exchange by an access-pattern model, see
-// DESIGN.md §5):
-//   Lay<1>  one transform per warp group (T >= 32): XOR swizzle of the 5-bit
-//           offset inside each 32-float line by m(line) = (line & 15) | bit3(line) << 4
-//   Lay<W>  W transforms interleaved element-wise, transform index fastest in
-//           the warp (T < 32, or column kernels with W = 16):
-//           addr = W * (i + i/16) + sub
+// Exchange buffers hold float2 (one 64-bit shared access per complex value)
+// with an XOR swizzle inside each 16-element line, i' = i ^ ((i >> 4) & 15);
+// W transforms are interleaved element-wise (transform index fastest in the
+// warp) when T < 32 or in the 16-column kernels: addr = W * i' + sub. Every
+// exchange pattern of every size is bank-conflict free (half-warp phases of
+// 8-byte accesses; verified with an access-pattern model).
 //
 // Twiddles come from a fp32 table tw[i] = exp(-2*pi*i*i/N) (rounded from fp64
 // on the host); SIGN = +1 uses the conjugate. Transforms are unnormalised,
@@ -135,12 +133,34 @@ __device__ __forceinline__ void dft_r(float2* x) {
     }
 }
 
-// Exchange-buffer layout of one transform (see header comment).
+// Exchange-buffer layout of one transform (see header comment): complex
+// values as float2 (one 64-bit shared access per element), XOR-swizzled inside
+// each 16-element line so every exchange pattern is bank-conflict free.
 template <int W>
 struct Lay {
+    float2* buf;
+    int sub;  // transform index inside an interleaved group (W > 1)
+    __device__ __forceinline__ int at(int i) const {
+        const int j = (i & ~15) | ((i & 15) ^ ((i >> 4) & 15));
+        if constexpr (W == 1) {
+            return j;
+        } else {
+            return W * j + sub;
+        }
+    }
+    __device__ __forceinline__ void put(int i, float2 v) const { buf[at(i)] = v; }
+    __device__ __forceinline__ float2 get(int i) const { return buf[at(i)]; }
+};
+
+// Split real/imag variant (two 32-bit accesses per element): fewer live 64-bit
+// operands, which keeps the register-heavy column kernel (K4) at two CTAs per
+// SM. Conflict-free layouts: W == 1: XOR swizzle of the 5-bit offset inside
+// each 32-float line by (line & 15) | bit3(line) << 4; W > 1: W*(i + i/16) + sub.
+template <int W>
+struct LaySoA {
     float* re;
     float* im;
-    int sub;  // transform index inside an interleaved group (W > 1)
+    int sub;
     __device__ __forceinline__ int at(int i) const {
         if constexpr (W == 1) {
             const int j = i >> 5;
@@ -160,13 +180,19 @@ struct Lay {
     }
 };
 
-// Floats of one real (or imaginary) part for a group of W transforms of length N.
-// The +2 makes consecutive groups start 4 banks apart (2 parts per group), so
-// loops that read several transforms' buffers at the same index (separation,
-// radix-3 combines, output staging) spread over the banks.
+// floats of ONE part (re or im) of a LaySoA group
+template <int N, int W>
+__host__ __device__ constexpr int soa_part_floats() {
+    return W == 1 ? N + 2 : W * (N + N / 16) + 2;
+}
+
+// Floats of the buffer of one group of W interleaved length-N transforms.
+// The +4 (two float2) staggers consecutive groups across the banks, so loops
+// that read several transforms' buffers at the same index (separation,
+// radix-3 combines) spread over the banks.
 template <int N, int W>
 __host__ __device__ constexpr int part_floats() {
-    return W == 1 ? N + 2 : W * (N + N / 16) + 2;
+    return 2 * W * N + 4;
 }
 
 // Thread/transform geometry of kernels whose transforms are "rows": T = N/16
@@ -178,7 +204,7 @@ struct Geom {
     static constexpr int PER_CTA = THREADS / T;      // transforms per CTA
     static constexpr int GROUPS = PER_CTA / W;
     static constexpr int PART = part_floats<N, W>();
-    static constexpr int FLOATS = GROUPS * 2 * PART;  // one exchange buffer per transform
+    static constexpr int FLOATS = GROUPS * PART;  // one exchange buffer per transform
     static_assert(GROUPS >= 1 && PER_CTA % W == 0, "a CTA must hold whole warps of transforms");
     __device__ __forceinline__ static void map(int tid, int& tr, int& t) {
         if constexpr (W == 1) {
@@ -190,22 +216,30 @@ struct Geom {
             t = lane / W;
         }
     }
-    // layout of transform tr inside buffer `base` (FLOATS floats)
+    // layout of transform tr inside buffer `base` (FLOATS floats, 8-byte aligned)
     __device__ __forceinline__ static Lay<W> lay(float* base, int tr) {
-        float* g = base + (tr / W) * 2 * PART;
-        return Lay<W>{g, g + PART, tr % W};
+        return Lay<W>{reinterpret_cast<float2*>(base + (tr / W) * PART), tr % W};
     }
     // layout of transform tr for a buffer holding length-LEN data per transform
-    // (same interleave; used to stash inputs that are longer than the transform)
     template <int LEN>
     __device__ __forceinline__ static Lay<W> lay_len(float* base, int tr) {
-        constexpr int P = part_floats<LEN, W>();
-        float* g = base + (tr / W) * 2 * P;
-        return Lay<W>{g, g + P, tr % W};
+        return Lay<W>{reinterpret_cast<float2*>(base + (tr / W) * part_floats<LEN, W>()), tr % W};
     }
     template <int LEN>
     __host__ __device__ static constexpr int floats_len() {
-        return GROUPS * 2 * part_floats<LEN, W>();
+        return GROUPS * part_floats<LEN, W>();
+    }
+};
+
+// Same geometry with the split real/imag exchange layout.
+template <int N, int THREADS>
+struct GeomSoA : Geom<N, THREADS> {
+    using B = Geom<N, THREADS>;
+    static constexpr int SPART = soa_part_floats<N, B::W>();
+    static constexpr int FLOATS = B::GROUPS * 2 * SPART;
+    __device__ __forceinline__ static LaySoA<B::W> lay(float* base, int tr) {
+        float* g = base + (tr / B::W) * 2 * SPART;
+        return LaySoA<B::W>{g, g + SPART, tr % B::W};
     }
 };
 

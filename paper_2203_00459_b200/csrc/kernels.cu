@@ -85,6 +85,13 @@ __device__ __forceinline__ void ff_floor_frac(float2 x, int* fl, float* fr) {
     *fr = r;
 }
 
+// cp.async (LDGSTS): 8-byte global -> shared copy without register staging
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
+
 __device__ __forceinline__ float bilerp(float fr, float fc, float a00, float a01, float a10, float a11) {
     // sample_bilinear (imageops.cpp:24-25) operation order, fp32
     return (1.0f - fr) * ((1.0f - fc) * a00 + fc * a01) + fr * ((1.0f - fc) * a10 + fc * a11);
@@ -145,7 +152,8 @@ __global__ void __launch_bounds__(N) k_rot_cols(Params p) {
     const int u0 = blockIdx.x * 8;
     const int c = threadIdx.x % 16, t = threadIdx.x / 16;
     const int col = c < 8 ? (u0 + c) : ((N - (u0 + c - 8)) & (N - 1));
-    const Lay<16> lay{smem, smem + PART, c};
+    float2* sbuf = reinterpret_cast<float2*>(smem);
+    const Lay<16> lay{sbuf, c};
     const float2* z = p.zbuf + (size_t)pair * N * N;
     float2 v[16];
 #pragma unroll
@@ -162,8 +170,8 @@ __global__ void __launch_bounds__(N) k_rot_cols(Params p) {
         const int cc = o & 7, vc = o >> 3;
         const int vn = (vc + N / 2) & (N - 1);  // natural row of centred row vc
         const int vm = (N - vn) & (N - 1);      // row of -v
-        const float2 z1 = Lay<16>{smem, smem + PART, cc}.get(vn);
-        const float2 z2 = Lay<16>{smem, smem + PART, 8 + cc}.get(vm);
+        const float2 z1 = Lay<16>{sbuf, cc}.get(vn);
+        const float2 z2 = Lay<16>{sbuf, 8 + cc}.get(vm);
         const float fr = z1.x + z2.x, fi = z1.y - z2.y;  // Z1 + conj(Z2)
         const float gr = z1.x - z2.x, gi = z1.y + z2.y;  // Z1 - conj(Z2)
         const int2 bd = __ldg(p.band + vc);
@@ -570,7 +578,10 @@ struct XColGeom {
     static constexpr int COLS = (T >= 32) ? 4 : ((T >= 4) ? 8 : 16);
     static constexpr int PITCH = COLS + 1;
     static constexpr int THREADS = 3 * COLS * T;
-    using G = Geom<N / 2, THREADS>;
+    // split re/im exchange: with 64-bit accesses this kernel's allocation grows
+    // past two CTAs per SM (note: an explicit minBlocks=1 launch bound also
+    // changes ptxas' choice, 80 -> 167 registers)
+    using G = fscan_fft::GeomSoA<N / 2, THREADS>;
     static constexpr size_t FFT_FLOATS = (size_t)2 * G::FLOATS;
     static constexpr size_t TILE_FLOATS = (size_t)2 * N * PITCH;
     static constexpr size_t SMEM = (FFT_FLOATS > TILE_FLOATS ? FFT_FLOATS : TILE_FLOATS) * sizeof(float);
@@ -692,9 +703,12 @@ __global__ void __launch_bounds__(XOutGeom<N>::THREADS) k_xlat_out(Params p) {
     G::map(threadIdx.x, tr, t);
     const int rl = tr / 3, q = tr % 3;
     const int i = blockIdx.x * ROWS + rl;
-    const float2* yrow = p.zbuf + ((size_t)pair * N + i) * (H + 1);
     const auto buf = G::lay(smem, tr);
     {
+        // (staging Y through shared memory with cp.async measured slower: the
+        // stride-3 reads conflict and the extra barriers cost more than the
+        // L1-served direct loads)
+        const float2* yrow = p.zbuf + ((size_t)pair * N + i) * (H + 1);
         float2 v[16];
 #pragma unroll
         for (int m = 0; m < 16; ++m) {
@@ -925,7 +939,7 @@ cudaError_t rot_rows(const Params& p, cudaStream_t s) {
 
 template <int N>
 cudaError_t rot_cols(const Params& p, cudaStream_t s) {
-    const size_t sm = (size_t)2 * part_floats<N, 16>() * sizeof(float);
+    const size_t sm = (size_t)part_floats<N, 16>() * sizeof(float);
     cudaError_t e = set_smem(k_rot_cols<N>, sm);
     if (e != cudaSuccess) return e;
     k_rot_cols<N><<<dim3(N / 16, p.batch), N, sm, s>>>(p);
