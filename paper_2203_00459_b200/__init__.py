@@ -20,7 +20,8 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-LIB_PATH = os.path.join(HERE, "libfscan_b200.so")
+# FSCAN_LIB: load an alternative build of the same library (A/B kernel timing)
+LIB_PATH = os.environ.get("FSCAN_LIB") or os.path.join(HERE, "libfscan_b200.so")
 
 OK, ERR_INVALID_ARGUMENT, ERR_NONFINITE, ERR_MASK_RANGE, ERR_UNSUPPORTED, ERR_CUDA, ERR_NO_DEVICE = range(7)
 _STATUS = {0: "OK", 1: "INVALID_ARGUMENT", 2: "NONFINITE", 3: "MASK_RANGE", 4: "UNSUPPORTED",

@@ -19,10 +19,10 @@
 //
 // Exchange buffers hold float2 (one 64-bit shared access per complex value)
 // with an XOR swizzle inside each 16-element line, i' = i ^ ((i >> 4) & 15);
-// W transforms are interleaved element-wise (transform index fastest in the
-// warp) when T < 32 or in the 16-column kernels: addr = W * i' + sub. Every
-// exchange pattern of every size is bank-conflict free (half-warp phases of
-// 8-byte accesses; verified with an access-pattern model).
+// row kernels give every transform its own buffer (staggered, see Geom), the
+// 16-column kernel interleaves W transforms element-wise: addr = W * i' + sub.
+// Every exchange pattern of every size is bank-conflict free (half-warp phases
+// of 8-byte accesses; verified with an access-pattern model).
 //
 // Twiddles come from a fp32 table tw[i] = exp(-2*pi*i*i/N) (rounded from fp64
 // on the host); SIGN = +1 uses the conjugate. Transforms are unnormalised,
@@ -152,10 +152,62 @@ struct Lay {
     __device__ __forceinline__ float2 get(int i) const { return buf[at(i)]; }
 };
 
-// Split real/imag variant (two 32-bit accesses per element): fewer live 64-bit
-// operands, which keeps the register-heavy column kernel (K4) at two CTAs per
-// SM. Conflict-free layouts: W == 1: XOR swizzle of the 5-bit offset inside
-// each 32-float line by (line & 15) | bit3(line) << 4; W > 1: W*(i + i/16) + sub.
+// Floats of the buffer of one group of W interleaved length-N transforms
+// (the 16-column kernel); the +4 staggers consecutive buffers across banks.
+template <int N, int W>
+__host__ __device__ constexpr int part_floats() {
+    return 2 * W * N + 4;
+}
+
+// Thread/transform geometry of kernels whose transforms are "rows": T = N/16
+// threads per transform, the T lanes of a transform contiguous in the warp
+// (W = 32/T transforms per warp when T < 32). Every transform has its own
+// exchange buffer; consecutive buffers are staggered by T elements (T < 16)
+// so that the W transforms sharing a warp, and loops that read several
+// transforms' buffers at the same index (separation, radix-3 combines), hit
+// disjoint banks (T >= 16: any stride is conflict-free for the FFT; 2 and 12
+// are chosen for the row-separation loop of K3, see XRowGeom). Verified
+// conflict-free for all exchange and combine patterns with an access-pattern
+// model.
+template <int N, int THREADS>
+struct Geom {
+    static constexpr int T = N / 16;
+    static constexpr int W = T >= 32 ? 1 : 32 / T;  // transforms per warp
+    static constexpr int PER_CTA = THREADS / T;      // transforms per CTA
+    static constexpr int GROUPS = PER_CTA / W;
+    static_assert(GROUPS >= 1 && PER_CTA % W == 0, "a CTA must hold whole warps of transforms");
+    // float2 elements per transform buffer holding length-LEN data
+    template <int LEN>
+    __host__ __device__ static constexpr int stride_len() {
+        return LEN + (T < 16 ? T : (T == 16 ? 2 : 12));
+    }
+    static constexpr int FLOATS = PER_CTA * 2 * stride_len<N>();  // one exchange buffer per transform
+    __device__ __forceinline__ static void map(int tid, int& tr, int& t) {
+        tr = tid / T;
+        t = tid % T;
+    }
+    // layout of transform tr inside buffer `base` (FLOATS floats, 8-byte aligned)
+    __device__ __forceinline__ static Lay<1> lay(float* base, int tr) {
+        return Lay<1>{reinterpret_cast<float2*>(base) + tr * stride_len<N>(), 0};
+    }
+    // layout of transform tr for a buffer holding length-LEN data per transform
+    template <int LEN>
+    __device__ __forceinline__ static Lay<1> lay_len(float* base, int tr) {
+        return Lay<1>{reinterpret_cast<float2*>(base) + tr * stride_len<LEN>(), 0};
+    }
+    template <int LEN>
+    __host__ __device__ static constexpr int floats_len() {
+        return PER_CTA * 2 * stride_len<LEN>();
+    }
+};
+
+// Split real/imag exchange layout of the column kernel K4 (two 32-bit
+// accesses per element: fewer live 64-bit operands keep K4 at 80 registers and
+// two CTAs per SM). W transforms interleaved element-wise (transform index =
+// lane % W fastest in the warp): addr = W*(i + i/16) + sub; W == 1: XOR of the
+// 5-bit offset inside each 32-float line by (line & 15) | bit3(line) << 4.
+// (A per-transform layout with the lane/T mapping of Geom removes the last
+// radix-3-combine conflicts but measured 4% slower in K4.)
 template <int W>
 struct LaySoA {
     float* re;
@@ -180,32 +232,14 @@ struct LaySoA {
     }
 };
 
-// floats of ONE part (re or im) of a LaySoA group
-template <int N, int W>
-__host__ __device__ constexpr int soa_part_floats() {
-    return W == 1 ? N + 2 : W * (N + N / 16) + 2;
-}
-
-// Floats of the buffer of one group of W interleaved length-N transforms.
-// The +4 (two float2) staggers consecutive groups across the banks, so loops
-// that read several transforms' buffers at the same index (separation,
-// radix-3 combines) spread over the banks.
-template <int N, int W>
-__host__ __device__ constexpr int part_floats() {
-    return 2 * W * N + 4;
-}
-
-// Thread/transform geometry of kernels whose transforms are "rows": T = N/16
-// threads per transform; transforms of a warp interleaved (W per warp) when T < 32.
 template <int N, int THREADS>
-struct Geom {
+struct GeomSoA {
     static constexpr int T = N / 16;
-    static constexpr int W = T >= 32 ? 1 : 32 / T;  // transforms per warp
-    static constexpr int PER_CTA = THREADS / T;      // transforms per CTA
+    static constexpr int W = T >= 32 ? 1 : 32 / T;
+    static constexpr int PER_CTA = THREADS / T;
     static constexpr int GROUPS = PER_CTA / W;
-    static constexpr int PART = part_floats<N, W>();
-    static constexpr int FLOATS = GROUPS * PART;  // one exchange buffer per transform
-    static_assert(GROUPS >= 1 && PER_CTA % W == 0, "a CTA must hold whole warps of transforms");
+    static constexpr int SPART = W == 1 ? N + 2 : W * (N + N / 16) + 2;
+    static constexpr int FLOATS = GROUPS * 2 * SPART;
     __device__ __forceinline__ static void map(int tid, int& tr, int& t) {
         if constexpr (W == 1) {
             tr = tid / T;
@@ -216,30 +250,9 @@ struct Geom {
             t = lane / W;
         }
     }
-    // layout of transform tr inside buffer `base` (FLOATS floats, 8-byte aligned)
-    __device__ __forceinline__ static Lay<W> lay(float* base, int tr) {
-        return Lay<W>{reinterpret_cast<float2*>(base + (tr / W) * PART), tr % W};
-    }
-    // layout of transform tr for a buffer holding length-LEN data per transform
-    template <int LEN>
-    __device__ __forceinline__ static Lay<W> lay_len(float* base, int tr) {
-        return Lay<W>{reinterpret_cast<float2*>(base + (tr / W) * part_floats<LEN, W>()), tr % W};
-    }
-    template <int LEN>
-    __host__ __device__ static constexpr int floats_len() {
-        return GROUPS * part_floats<LEN, W>();
-    }
-};
-
-// Same geometry with the split real/imag exchange layout.
-template <int N, int THREADS>
-struct GeomSoA : Geom<N, THREADS> {
-    using B = Geom<N, THREADS>;
-    static constexpr int SPART = soa_part_floats<N, B::W>();
-    static constexpr int FLOATS = B::GROUPS * 2 * SPART;
-    __device__ __forceinline__ static LaySoA<B::W> lay(float* base, int tr) {
-        float* g = base + (tr / B::W) * 2 * SPART;
-        return LaySoA<B::W>{g, g + SPART, tr % B::W};
+    __device__ __forceinline__ static LaySoA<W> lay(float* base, int tr) {
+        float* g = base + (tr / W) * 2 * SPART;
+        return LaySoA<W>{g, g + SPART, tr % W};
     }
 };
 

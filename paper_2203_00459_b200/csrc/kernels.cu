@@ -46,52 +46,6 @@ __host__ __device__ constexpr int rows_per_block() {
     return RowG<N>::PER_CTA;
 }
 
-// ---- float-float helpers (value = hi + lo, ~48-bit significand) ----
-__device__ __forceinline__ void ff_split(double d, float* hi, float* lo) {
-    *hi = (float)d;
-    *lo = (float)(d - (double)*hi);
-}
-
-// error-free transformations: the _rn intrinsics keep nvcc from contracting
-// them into FMAs
-__device__ __forceinline__ void two_sum(float a, float b, float* s, float* e) {
-    *s = __fadd_rn(a, b);
-    const float bb = __fsub_rn(*s, a);
-    *e = __fadd_rn(__fsub_rn(a, __fsub_rn(*s, bb)), __fsub_rn(b, bb));
-}
-
-// c + (a_hi + a_lo) * u + (b_hi + b_lo) * v with u, v exactly representable
-__device__ __forceinline__ float2 ff_affine(float c, float a_hi, float a_lo, float u, float b_hi, float b_lo, float v) {
-    const float p = __fmul_rn(a_hi, u), pe = fmaf(a_lo, u, fmaf(a_hi, u, -p));
-    const float q = __fmul_rn(b_hi, v), qe = fmaf(b_lo, v, fmaf(b_hi, v, -q));
-    float s1, e1, s2, e2;
-    two_sum(c, p, &s1, &e1);
-    two_sum(s1, q, &s2, &e2);
-    return make_float2(s2, e1 + e2 + pe + qe);
-}
-
-// floor and fraction of hi + lo
-__device__ __forceinline__ void ff_floor_frac(float2 x, int* fl, float* fr) {
-    float f = floorf(x.x);
-    float r = (x.x - f) + x.y;  // x.x - f is exact
-    if (r < 0.0f) {
-        f -= 1.0f;
-        r += 1.0f;
-    } else if (r >= 1.0f) {
-        f += 1.0f;
-        r -= 1.0f;
-    }
-    *fl = (int)f;
-    *fr = r;
-}
-
-// cp.async (LDGSTS): 8-byte global -> shared copy without register staging
-__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gsrc));
-}
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
-
 __device__ __forceinline__ float bilerp(float fr, float fc, float a00, float a01, float a10, float a11) {
     // sample_bilinear (imageops.cpp:24-25) operation order, fp32
     return (1.0f - fr) * ((1.0f - fc) * a00 + fc * a01) + fr * ((1.0f - fc) * a10 + fc * a11);
@@ -254,7 +208,7 @@ __global__ void __launch_bounds__(kPolarThreads) k_rot_gather(Params p) {
 __global__ void __launch_bounds__(kPolarThreads) k_rot_polar(Params p) {
     extern __shared__ double dsm[];
     const int pair = blockIdx.x;
-    const int nt = p.n_theta, L = p.L, pad = p.pad, n = p.n;
+    const int nt = p.n_theta, L = p.L, pad = p.pad;
     double* A = dsm;                 // wrap-extended radial-sum profiles, length L
     double* B = dsm + L;             // length L + nt + 4 (see below)
     double* s = B + L + nt + 4;      // theta surface, n_theta
@@ -453,6 +407,20 @@ struct XRowGeom {
     static constexpr int SP = (SP0 % 32 == 0) ? SP0 + 16 : SP0;  // stash row stride (floats)
     static constexpr size_t SMEM = ((size_t)2 * ROWS * SP + G::FLOATS) * sizeof(float);
     static_assert(G::PER_CTA % 3 == 0, "three transforms per row");
+    // separation loop: a half-warp reads R rows x KB consecutive k. Row ol's
+    // buffers start at 3 * ol * stride, i.e. bank offset o * ol (mod 16); R =
+    // 16 / gcd(o, 16) rows then cover distinct offsets and the aligned KB-blocks
+    // of k fill the gaps, so the reads are conflict free.
+    static constexpr int O = (3 * G::template stride_len<N / 2>()) % 16;
+    static constexpr int KB = O == 0 ? 16 : ((O & -O) < 16 ? (O & -O) : 16);
+    static constexpr int R = 16 / KB;
+    static_assert(ROWS % R == 0 && kXThreads % 16 == 0, "separation mapping");
+    __device__ __forceinline__ static void sep_map(int tid, int& ol, int& kk) {
+        constexpr int RG = ROWS / R;  // half-warps per k-block
+        const int g = tid >> 4, hl = tid & 15;
+        ol = (g % RG) * R + hl / KB;
+        kk = (g / RG) * KB + hl % KB;
+    }
 };
 
 template <int N>
@@ -490,8 +458,6 @@ __global__ void __launch_bounds__(kXThreads) k_xlat_rows(Params p) {
             float fr = 0.f, fc = 0.f;
             bool rin0 = live, rin1 = false, cin0 = true, cin1 = false;
             if (!rs.identity) {  // rotate_bilinear(g~, -theta): -theta == 0.0 returns g~ itself
-                // src_row = c + st*u + ct*v, src_col = c + ct*u - st*v (imageops.cpp:70-73) in
-                // float-float arithmetic (~1e-11 cells; the fp64 form stalls on DP latency)
                 // src_row = c + st*u + ct*v, src_col = c + ct*u - st*v (imageops.cpp:70-73)
                 // in fp32 FMAs: <= 5e-5 cell coordinate error, i.e. <= 5e-5 relative per
                 // bilinear sample (far inside the 1e-4 surface gate)
@@ -547,9 +513,10 @@ __global__ void __launch_bounds__(kXThreads) k_xlat_rows(Params p) {
         for (int m = 0; m < 16; ++m) b.put(t + m * T, v[m]);
     }
     __syncthreads();
-    // separation + transposed write: consecutive threads on consecutive rows y
+    // separation + transposed write (k = kk, kk + KSTEP, ...; see sep_map)
     constexpr int KSTEP = kXThreads / ROWS;
-    const int ol = threadIdx.x % ROWS, kk = threadIdx.x / ROWS;
+    int ol, kk;
+    X::sep_map(threadIdx.x, ol, kk);
     const auto e0 = G::lay(xbase, 3 * ol), e1 = G::lay(xbase, 3 * ol + 1), e2 = G::lay(xbase, 3 * ol + 2);
     // F = (Z[k'] + conj Z[M-k'])/2, G = (Z[k'] - conj Z[M-k'])/2i with Z[3k+q] = E_q[k];
     // by residue class: 3k pairs with E_0[K-k], 3k+1 with E_2[K-1-k], 3k+2 with E_1[K-1-k]
@@ -570,13 +537,15 @@ __global__ void __launch_bounds__(kXThreads) k_xlat_rows(Params p) {
 // lags ky in [-K, K) of IFFT_M(X) by a radix-3 combine:
 //   ky = n in [0, K):     sum_q W_M^{-nq} e_q[n]
 //   ky = n - K in [-K,0): sum_q W_M^{-nq} W_3^{q} e_q[n]
-// stored by surface row i = half - ky (the flip of matcher.cpp:171-182).
+// stored by surface row i = half - ky (the flip of matcher.cpp:171-182)
+// through a shared-memory tile (a k'-major output written straight from the
+// registers measured slower: K4 grows to 120 registers and K5's loads scatter).
 template <int N>
 struct XColGeom {
     static constexpr int T = N / 32;
     // columns per CTA: 3 * COLS * T threads must fill whole warps
     static constexpr int COLS = (T >= 32) ? 4 : ((T >= 4) ? 8 : 16);
-    static constexpr int PITCH = COLS + 1;
+    static constexpr int PITCH = COLS + 1;  // output tile [N rows][PITCH] float2
     static constexpr int THREADS = 3 * COLS * T;
     // split re/im exchange: with 64-bit accesses this kernel's allocation grows
     // past two CTAs per SM (note: an explicit minBlocks=1 launch bound also
@@ -592,7 +561,7 @@ __global__ void __launch_bounds__(XColGeom<N>::THREADS) k_xlat_cols(Params p) {
     constexpr int K = N / 2, M = 3 * K, H = M / 2;
     using X = XColGeom<N>;
     using G = typename X::G;
-    constexpr int T = G::T, COLS = X::COLS, PITCH = X::PITCH;
+    constexpr int T = G::T, COLS = X::COLS;
     constexpr int half = N / 2 - 1;
     extern __shared__ float smem[];
     const int pair = blockIdx.y;
@@ -654,8 +623,8 @@ __global__ void __launch_bounds__(XColGeom<N>::THREADS) k_xlat_cols(Params p) {
         const int m = q + 3 * j;
         if (m < 16) {
             const int n0 = t + m * T;
-            tile[(half - n0) * PITCH + c] = accp[j];
-            tile[(half - (n0 - K)) * PITCH + c] = accn[j];
+            tile[(half - n0) * X::PITCH + c] = accp[j];
+            tile[(half - (n0 - K)) * X::PITCH + c] = accn[j];
         }
     }
     __syncthreads();
@@ -663,7 +632,7 @@ __global__ void __launch_bounds__(XColGeom<N>::THREADS) k_xlat_cols(Params p) {
     const int ncols = min(COLS, H + 1 - (int)blockIdx.x * COLS);
     for (int o = threadIdx.x; o < N * COLS; o += blockDim.x) {
         const int i = o / COLS, cc = o % COLS;
-        if (cc < ncols) dst[(size_t)i * (H + 1) + blockIdx.x * COLS + cc] = tile[i * PITCH + cc];
+        if (cc < ncols) dst[(size_t)i * (H + 1) + blockIdx.x * COLS + cc] = tile[i * X::PITCH + cc];
     }
 }
 
@@ -705,9 +674,9 @@ __global__ void __launch_bounds__(XOutGeom<N>::THREADS) k_xlat_out(Params p) {
     const int i = blockIdx.x * ROWS + rl;
     const auto buf = G::lay(smem, tr);
     {
-        // (staging Y through shared memory with cp.async measured slower: the
-        // stride-3 reads conflict and the extra barriers cost more than the
-        // L1-served direct loads)
+        // (staging Y through shared memory with cp.async, or a k'-major Y
+        // written straight from K4's registers, both measured slower: the
+        // stride-3 row reads are served by L1 across the three q groups)
         const float2* yrow = p.zbuf + ((size_t)pair * N + i) * (H + 1);
         float2 v[16];
 #pragma unroll
