@@ -53,6 +53,7 @@ struct fscan_ctx {
     int chunk = 0;       // pairs per pipeline chunk
     int alloc_chunk = 0; // workspace capacity (pairs)
     int n_live = 0;
+    int rot_col_blocks = 0;  // K1b column blocks (8 columns each) the polar taps read
     int launches_last = 0;
     std::string err;
     std::mutex mu;
@@ -129,8 +130,11 @@ bool build_band(int n, double lo, double hi, std::vector<int2>& out, std::vector
 // cart2pol taps (imageops.cpp:81-99 through sample_bilinear 10-26), exact
 // fp64 coordinates; entries whose four taps all sit outside the band (or the
 // array) contribute exactly 0 and are dropped by trimming the radius range.
+// Taps on band-zeroed cells are not read either (flag bit clear: the value is
+// exactly 0 in the reference too), so K1b only computes the column blocks up
+// to *u_hi, the largest in-band column any tap reads.
 bool build_taps(int n, const fscan_config& cfg, const std::vector<unsigned char>& inband,
-                std::vector<PolarTap>& taps, int* n_live, std::string* why) {
+                std::vector<PolarTap>& taps, int* n_live, int* u_hi, std::string* why) {
     const int nt = cfg.n_theta, nr = cfg.n_radius;
     const double span = nt * cfg.delta_theta;
     const int c = n / 2;
@@ -138,6 +142,7 @@ bool build_taps(int n, const fscan_config& cfg, const std::vector<unsigned char>
     const int W = n / 2;
     std::vector<PolarTap> all((size_t)nt * nr);
     int jlo = nr, jhi = -1;
+    *u_hi = 0;
     for (int i = 0; i < nt; ++i) {
         const double phi = -span / 2.0 + span * i / nt;
         const double cp = std::cos(phi), sp = std::sin(phi);
@@ -162,9 +167,10 @@ bool build_taps(int n, const fscan_config& cfg, const std::vector<unsigned char>
                     continue;
                 }
                 if (uu >= W) continue;  // column n: outside the reference array
-                const int bit = (tp == 0) ? 1 : (tp == 1) ? 2 : (tp == 2) ? 4 : 8;
-                flags |= bit;
-                if (inband[(size_t)rr * W + uu]) live = 1;
+                if (!inband[(size_t)rr * W + uu]) continue;
+                flags |= 1 << tp;
+                live = 1;
+                *u_hi = std::max(*u_hi, (int)uu);
             }
             PolarTap& e = all[(size_t)i * nr + j];
             e.packed = (int)(r0 & 0xFFF) | (int)((u0 & 0xFFF) << 12) | (flags << 24);
@@ -259,6 +265,7 @@ Params base_params(fscan_ctx* ctx, Lane& l, int batch, double delta) {
     p.band = ctx->band;
     p.taps = ctx->taps;
     p.n_live = ctx->n_live;
+    p.zcols = 8 * ctx->rot_col_blocks;
     p.n_theta = ctx->cfg.n_theta;
     p.pad = ctx->cfg.pad_angle;
     p.L = ctx->cfg.n_theta + 2 * ctx->cfg.pad_angle;
@@ -469,10 +476,13 @@ fscan_status fscan_ctx_create(int device, const fscan_config* cfg_in, int max_ba
     std::vector<PolarTap> taps;
     if (cfg.n_theta > 1) {
         std::string why;
-        if (!build_taps(n, cfg, inband, taps, &ctx->n_live, &why)) return fail(ctx, FSCAN_ERR_UNSUPPORTED, why);
+        int u_hi = 0;
+        if (!build_taps(n, cfg, inband, taps, &ctx->n_live, &u_hi, &why)) return fail(ctx, FSCAN_ERR_UNSUPPORTED, why);
+        ctx->rot_col_blocks = std::min(n / 16, u_hi / 8 + 1);
     } else {
         taps.resize(1);
         ctx->n_live = 1;
+        ctx->rot_col_blocks = n / 16;
     }
     CK(cudaMalloc(&ctx->tw_n, sizeof(float2) * n));
     CK(cudaMalloc(&ctx->tw_k, sizeof(float2) * twk.size()));
@@ -676,6 +686,7 @@ fscan_status fscan_band_magnitude_batch(fscan_ctx* ctx, const float* d_img, int 
         p.f = d_img + off * nn;
         p.g = d_img + off * nn;
         p.mag_out = d_out + off * (nn / 2);
+        p.zcols = ctx->n / 2;  // the whole half plane
         return run_chunk(ctx, l, p, Stages::Magnitude, &ctx->launches_last);
     });
 }

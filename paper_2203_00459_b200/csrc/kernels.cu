@@ -88,7 +88,10 @@ __global__ void __launch_bounds__(kRowThreads) k_rot_rows(Params p) {
     }
     fft_regs<N, -1>(v, t, lay, p.tw_n);
 #pragma unroll
-    for (int m = 0; m < 16; ++m) p.zbuf[base + t + m * T] = v[m];
+    for (int m = 0; m < 16; ++m) {
+        const int x = t + m * T;
+        if (x < p.zcols || x > N - p.zcols) p.zbuf[base + x] = v[m];  // columns K1b reads
+    }
     if (bad) atomicOr(p.flags + pair, bad);
 }
 
@@ -911,7 +914,7 @@ cudaError_t rot_cols(const Params& p, cudaStream_t s) {
     const size_t sm = (size_t)part_floats<N, 16>() * sizeof(float);
     cudaError_t e = set_smem(k_rot_cols<N>, sm);
     if (e != cudaSuccess) return e;
-    k_rot_cols<N><<<dim3(N / 16, p.batch), N, sm, s>>>(p);
+    k_rot_cols<N><<<dim3(p.zcols / 8, p.batch), N, sm, s>>>(p);
     return cudaGetLastError();
 }
 

@@ -61,6 +61,7 @@ struct Params {
     const int2* band;     // per centred row: [u_lo, u_hi] in band (empty: lo > hi)
     const PolarTap* taps; // [n_theta][n_live]
     int n_live;
+    int zcols;            // K1b computes columns u < zcols (multiple of 8); K1a stores only those and their mirrors
     // config
     int n_theta, pad, L, C;
     double delta_theta, t_theta, t_xy, delta;
