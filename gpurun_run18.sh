@@ -1,3 +1,3 @@
 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
 python tests/gpu_probe.py 2>&1 | grep -E "cfg(2|4|5) pair" | head -6
-VARS="D G" bash gpurun_ab.sh
+VARS="G H" bash gpurun_ab.sh

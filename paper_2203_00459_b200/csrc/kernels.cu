@@ -442,7 +442,9 @@ __global__ void __launch_bounds__(kXThreads) k_xlat_rows(Params p) {
     const float* ft = p.ft + (size_t)pair * N * N;
     const float* gt = p.gt + (size_t)pair * N * N;
     const float c0f32 = (N - 1) / 2.0f;  // exact
-    const float stf = (float)rs.st, ctf = (float)rs.ct;
+    // rotate_bilinear(g~, -theta); -theta == 0.0 returns g~ itself, which st = 0,
+    // ct = 1 reproduce exactly (integer source coordinates, zero fractions)
+    const float stf = rs.identity ? 0.0f : (float)rs.st, ctf = rs.identity ? 1.0f : (float)rs.ct;
     // gather: ROWS rows x N cells over all threads, consecutive threads on
     // consecutive x; U cells per thread per round with every load issued
     // before any use (memory-level parallelism for the L2/DRAM latency)
@@ -455,35 +457,27 @@ __global__ void __launch_bounds__(kXThreads) k_xlat_rows(Params p) {
         for (int u = 0; u < U; ++u) {
             const int e = e0 + u * kXThreads;
             const bool live = e < CELLS;
-            const int yl = live ? e / N : 0, x = live ? e % N : 0;
+            const int yl = e / N, x = e % N;
             const int y = y0 + yl;
-            int r0 = y, cc0 = x;
-            float fr = 0.f, fc = 0.f;
-            bool rin0 = live, rin1 = false, cin0 = true, cin1 = false;
-            if (!rs.identity) {  // rotate_bilinear(g~, -theta): -theta == 0.0 returns g~ itself
-                // src_row = c + st*u + ct*v, src_col = c + ct*u - st*v (imageops.cpp:70-73)
-                // in fp32 FMAs: <= 5e-5 cell coordinate error, i.e. <= 5e-5 relative per
-                // bilinear sample (far inside the 1e-4 surface gate)
-                const float uu = (float)x - c0f32, vv = (float)y - c0f32;  // exact half-integers
-                const float sr = fmaf(stf, uu, fmaf(ctf, vv, c0f32));
-                const float sc = fmaf(ctf, uu, fmaf(-stf, vv, c0f32));
-                const float r0f = floorf(sr), cf = floorf(sc);
-                r0 = (int)r0f;
-                cc0 = (int)cf;
-                fr = sr - r0f;
-                fc = sc - cf;
-                rin0 = live && (unsigned)r0 < (unsigned)N;
-                rin1 = live && (unsigned)(r0 + 1) < (unsigned)N;
-                cin0 = (unsigned)cc0 < (unsigned)N;
-                cin1 = (unsigned)(cc0 + 1) < (unsigned)N;
-            }
-            frs[u] = fr;
-            fcs[u] = fc;
-            fv[u] = live ? ft[(size_t)y * N + x] : 0.f;
-            tap[u][0] = (rin0 && cin0) ? gt[(size_t)r0 * N + cc0] : 0.0f;
-            tap[u][1] = (rin0 && cin1) ? gt[(size_t)r0 * N + cc0 + 1] : 0.0f;
-            tap[u][2] = (rin1 && cin0) ? gt[(size_t)(r0 + 1) * N + cc0] : 0.0f;
-            tap[u][3] = (rin1 && cin1) ? gt[(size_t)(r0 + 1) * N + cc0 + 1] : 0.0f;
+            // src_row = c + st*u + ct*v, src_col = c + ct*u - st*v (imageops.cpp:70-73)
+            // in fp32 FMAs: <= 5e-5 cell coordinate error, i.e. <= 5e-5 relative per
+            // bilinear sample (far inside the 1e-4 surface gate)
+            const float uu = (float)x - c0f32, vv = (float)y - c0f32;  // exact half-integers
+            const float sr = fmaf(stf, uu, fmaf(ctf, vv, c0f32));
+            const float sc = fmaf(ctf, uu, fmaf(-stf, vv, c0f32));
+            const float r0f = floorf(sr), cf = floorf(sc);
+            frs[u] = sr - r0f;
+            fcs[u] = sc - cf;
+            // taps outside the grid are 0 (sample_bilinear, imageops.cpp:10-26)
+            const int r0 = (int)r0f, cc0 = (int)cf;
+            const bool r0in = live && (unsigned)r0 < (unsigned)N, r1in = live && (unsigned)(r0 + 1) < (unsigned)N;
+            const bool c0in = (unsigned)cc0 < (unsigned)N, c1in = (unsigned)(cc0 + 1) < (unsigned)N;
+            const float* gp = gt + (r0 * N + cc0);  // 32-bit offset, one address per cell
+            fv[u] = live ? ft[y * N + x] : 0.f;
+            tap[u][0] = (r0in && c0in) ? gp[0] : 0.f;
+            tap[u][1] = (r0in && c1in) ? gp[1] : 0.f;
+            tap[u][2] = (r1in && c0in) ? gp[N] : 0.f;
+            tap[u][3] = (r1in && c1in) ? gp[N + 1] : 0.f;
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
