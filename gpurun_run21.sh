@@ -1,1 +1,1 @@
-VARS="G M" bash gpurun_ab.sh
+VARS="M O" bash gpurun_ab.sh

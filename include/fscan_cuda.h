@@ -143,6 +143,27 @@ fscan_status fscan_polar_to_cart_batch(const float* d_polar, int batch, int n_az
                                        double range_res, int n, double delta, float* d_out,
                                        void* stream);
 
+/* Brute-force correlative search (the reference's oracle, proj/src/oracle.cpp:21-67,
+ * proj/include/fscan/oracle.hpp:10-23): for every candidate theta (in list
+ * order) g is de-rotated by -theta and the zero-padded translation correlation
+ * with f is scored; the result is the global hard argmax over (theta, row,
+ * col) with ties to the earlier theta, then the lower linear index. f and g
+ * are used as given (no masks, no window), like brute_force_match. */
+typedef struct fscan_bf_result {
+    double theta, tx, ty;   /* pose (theta normalised to (-pi, pi], t in metres) */
+    double score;           /* correlation at the winning cell (OracleResult::score) */
+    int32_t theta_index;    /* winning candidate */
+    int32_t xy_row, xy_col; /* winning cell of the N x N lag window */
+    int32_t status;         /* FSCAN_ERR_NONFINITE if the winning score is not finite */
+} fscan_bf_result;
+
+/* batch pairs (device, N x N each), n_thetas candidates from a HOST array,
+ * results to device d_out[batch]. Asynchronous on `stream`. Cost: one
+ * translation stage per (pair, candidate). */
+fscan_status fscan_brute_force_batch(fscan_ctx* ctx, const float* d_f, const float* d_g, int batch,
+                                     const double* thetas, int n_thetas, double delta,
+                                     fscan_bf_result* d_out, void* stream);
+
 /* Synchronises `stream` and scans d_out for the first non-OK status. */
 fscan_status fscan_check_results(const fscan_pair_result* d_out, int batch, void* stream,
                                  int* first_bad_pair);
@@ -154,7 +175,7 @@ int fscan_ctx_launches_last(const fscan_ctx* ctx);
  * with CUDA events around every kernel. fscan_ctx_kernel_times() synchronises
  * and returns, per kernel kind (0 rot_rows, 1 rot_cols, 2 rot_polar,
  * 3 theta_in, 4 xlat_rows, 5 xlat_cols, 6 xlat_out, 7 finalize, 8 rot_gather,
- * 9 polar_to_cart, 10 mag_unpack),
+ * 9 polar_to_cart, 10 mag_unpack, 11 bf_items, 12 bf_final),
  * the summed milliseconds and launch counts of the last call. */
 fscan_status fscan_ctx_set_profiling(fscan_ctx* ctx, int on);
 fscan_status fscan_ctx_kernel_times(fscan_ctx* ctx, double* ms, int* launches, int n_kinds);

@@ -39,6 +39,13 @@ class FoResult(C.Structure):
     ]
 
 
+class FoBfResult(C.Structure):
+    _fields_ = [
+        ("theta", C.c_double), ("tx", C.c_double), ("ty", C.c_double), ("score", C.c_double),
+        ("theta_index", C.c_int), ("xy_row", C.c_int), ("xy_col", C.c_int), ("pad_", C.c_int),
+    ]
+
+
 def build(ref: bool = True) -> None:
     """Build liboracle.so (and _ref when the reference tree is present)."""
     target = "all" if (ref and os.path.isdir(REF_SRC)) else "oracle"
@@ -89,7 +96,14 @@ def lib(which: str = "oracle") -> C.CDLL:
         L.fo_polar_to_cart.argtypes = [C.POINTER(C.c_double), C.c_int, C.c_int, C.c_double,
                                        C.c_int, C.c_double, C.POINTER(C.c_double)]
         L.fo_polar_to_cart.restype = C.c_int
+        L.fo_brute_force.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int, C.c_double,
+                                     C.POINTER(C.c_double), C.c_int, C.POINTER(FoBfResult)]
+        L.fo_brute_force.restype = C.c_int
     else:
+        L.ref_brute_force.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int, C.c_double,
+                                      C.POINTER(C.c_double), C.c_int, C.POINTER(FoBfResult), C.c_char_p,
+                                      C.c_int]
+        L.ref_brute_force.restype = C.c_int
         L.ref_verify.argtypes = [C.c_char_p, C.c_int]
         L.ref_verify.restype = C.c_int
         L.ref_scan_match_batch_f32.argtypes = [
@@ -176,6 +190,26 @@ def scan_match(f, g, cfg: FoConfig, delta: float, mf=None, mg=None, which: str =
     return MatchOut(res.theta, res.tx, res.ty, res.theta_hard, res.theta_peak,
                     (res.xy_hard_x, res.xy_hard_y), res.xy_peak, res.theta_bin,
                     res.xy_row, res.xy_col, ts, xs)
+
+
+def brute_force(f, g, thetas, delta: float, which: str = "oracle") -> FoBfResult:
+    """brute_force_match (oracle.cpp:40-67) on float64 copies of the inputs."""
+    L = lib(which)
+    n = int(f.shape[0])
+    f = np.ascontiguousarray(f, dtype=np.float64)
+    g = np.ascontiguousarray(g, dtype=np.float64)
+    th = np.ascontiguousarray(thetas, dtype=np.float64)
+    res = FoBfResult()
+    if which == "oracle":
+        rc = L.fo_brute_force(_p(f), _p(g), n, delta, _p(th), int(th.size), C.byref(res))
+        if rc != 0:
+            raise OracleError("brute_force_match: empty theta candidate list")
+    else:
+        err = C.create_string_buffer(512)
+        rc = L.ref_brute_force(_p(f), _p(g), n, delta, _p(th), int(th.size), C.byref(res), err, 512)
+        if rc != 0:
+            raise OracleError(err.value.decode())
+    return res
 
 
 def band_magnitude(img, band_lo, band_hi, which="oracle"):

@@ -357,6 +357,61 @@ static double normalize_angle(double theta) {
     return theta;
 }
 
+/* oracle.cpp:21-38 (score_theta) and 40-67 (brute_force_match): per candidate
+ * the hard argmax of the cropped, flipped zero-padded correlation (row-major
+ * scan from cell (0, 0), strict >), then the first candidate with the largest
+ * score; t = rotate_vec(theta, ((col - half) delta, (row - half) delta)). */
+int fo_brute_force(const double* f, const double* g, int n, double delta, const double* thetas,
+                   int nth, fo_bf_result* out) {
+    if (nth < 1 || n < 1) return 1;
+    const size_t nn = (size_t)n * n;
+    const int big = fo_next_fast_size(2 * n - 1);
+    const int h = big / 2, half = (n - 1) / 2;
+    double* gr = (double*)malloc(sizeof(double) * nn);
+    double* raw = (double*)malloc(sizeof(double) * (size_t)big * big);
+    double* fp = zero_pad(f, n, big);
+    double best_score = 0.0;
+    int best_k = 0, best_i = 0, best_j = 0;
+    for (int k = 0; k < nth; ++k) {
+        fo_rotate_bilinear(g, n, -thetas[k], gr);
+        double* gp = zero_pad(gr, n, big);
+        fo_xcorr(fp, gp, big, big, raw);
+        free(gp);
+        double b = raw[(size_t)(h + half) * big + (h - half)];
+        int bi = 0, bj = 0;
+        for (int i = 0; i < n; ++i)
+            for (int j = 0; j < n; ++j) {
+                const double v = raw[(size_t)(h - (i - half)) * big + h + (j - half)];
+                if (v > b) {
+                    b = v;
+                    bi = i;
+                    bj = j;
+                }
+            }
+        if (k == 0 || b > best_score) {
+            best_score = b;
+            best_k = k;
+            best_i = bi;
+            best_j = bj;
+        }
+    }
+    free(gr);
+    free(raw);
+    free(fp);
+    const double theta = thetas[best_k];
+    const double dx = (best_j - half) * delta, dy = (best_i - half) * delta;
+    const double c = cos(theta), sn = sin(theta);
+    out->theta = normalize_angle(theta);
+    out->tx = c * dx - sn * dy;
+    out->ty = sn * dx + c * dy;
+    out->score = best_score;
+    out->theta_index = best_k;
+    out->xy_row = best_i;
+    out->xy_col = best_j;
+    out->pad_ = 0;
+    return 0;
+}
+
 int fo_band_magnitude(const double* img, int n, double lo, double hi, double* out) {
     const size_t nn = (size_t)n * n;
     double* w = (double*)malloc(sizeof(double) * n);

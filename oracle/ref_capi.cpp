@@ -11,6 +11,8 @@
 //   soft_argmax           proj/src/matcher.cpp:57-93
 //   verify suites         proj/src/verify.cpp:73,115
 //   parallel_for          proj/src/parallel.cpp:24-45
+//   brute_force_match     proj/src/oracle.cpp:40-67
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <exception>
@@ -21,6 +23,7 @@
 #include "fscan/grid.hpp"
 #include "fscan/imageops.hpp"
 #include "fscan/matcher.hpp"
+#include "fscan/oracle.hpp"
 #include "fscan/parallel.hpp"
 #include "fscan/spectral.hpp"
 #include "fscan/verify.hpp"
@@ -165,6 +168,35 @@ int ref_scan_match(const double* f, const double* g, const double* mf, const dou
         fill_result(r, out);
         if (theta_surface) to_ptr(r.theta_surface.scores, theta_surface);
         if (xy_surface) to_ptr(r.xy_surface.scores, xy_surface);
+    });
+}
+
+int ref_brute_force(const double* f, const double* g, int n, double delta, const double* thetas,
+                    int n_thetas, fo_bf_result* out, char* err, int errlen) {
+    return guard(err, errlen, [&] {
+        const GridSpec spec{n, delta};
+        const ScanGrid fs(spec, from_ptr(f, n, n));
+        const ScanGrid gs(spec, from_ptr(g, n, n));
+        const std::vector<double> th(thetas, thetas + (n_thetas > 0 ? n_thetas : 0));
+        MatchConfig cfg;  // unused by the search (oracle.cpp:48)
+        const OracleResult r = brute_force_match(fs, gs, th, cfg);
+        out->theta = r.pose.theta;
+        out->tx = r.pose.tx;
+        out->ty = r.pose.ty;
+        out->score = r.score;
+        // first candidate whose normalised angle is the returned one
+        out->theta_index = 0;
+        for (int k = 0; k < n_thetas; ++k)
+            if (normalize_angle(thetas[k]) == r.pose.theta) {
+                out->theta_index = k;
+                break;
+            }
+        // cell from the back-rotated translation (exact up to rounding)
+        const Vec2 d = rotate_vec(-thetas[out->theta_index], Vec2{r.pose.tx, r.pose.ty});
+        const int half = (n - 1) / 2;
+        out->xy_col = static_cast<int>(std::lround(d.x / delta)) + half;
+        out->xy_row = static_cast<int>(std::lround(d.y / delta)) + half;
+        out->pad_ = 0;
     });
 }
 

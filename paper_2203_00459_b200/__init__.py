@@ -70,6 +70,18 @@ RESULT_DTYPE = np.dtype([
 assert RESULT_DTYPE.itemsize == C.sizeof(CPairResult)
 
 
+class CBfResult(C.Structure):
+    _fields_ = [
+        ("theta", C.c_double), ("tx", C.c_double), ("ty", C.c_double), ("score", C.c_double),
+        ("theta_index", C.c_int32), ("xy_row", C.c_int32), ("xy_col", C.c_int32), ("status", C.c_int32),
+    ]
+
+
+BF_DTYPE = np.dtype([("theta", "f8"), ("tx", "f8"), ("ty", "f8"), ("score", "f8"),
+                     ("theta_index", "i4"), ("xy_row", "i4"), ("xy_col", "i4"), ("status", "i4")])
+assert BF_DTYPE.itemsize == C.sizeof(CBfResult)
+
+
 class CSynthSpec(C.Structure):
     _fields_ = [
         ("polar", C.c_int), ("n", C.c_int), ("delta", C.c_double),
@@ -111,6 +123,7 @@ SYMBOLS = {
     "fscan_estimate_rotation_batch": (C.c_int, [_P, _P, _P, C.c_int, _P, _P, _P]),
     "fscan_estimate_translation_batch": (C.c_int, [_P, _P, _P, C.c_int, C.c_double, _P, _P, _P, _P]),
     "fscan_band_magnitude_batch": (C.c_int, [_P, _P, C.c_int, _P, _P]),
+    "fscan_brute_force_batch": (C.c_int, [_P, _P, _P, C.c_int, _P, C.c_int, C.c_double, _P, _P]),
     "fscan_polar_to_cart_batch": (C.c_int, [_P, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int,
                                             C.c_double, _P, _P]),
     "fscan_check_results": (C.c_int, [_P, C.c_int, _P, C.POINTER(C.c_int)]),
@@ -270,7 +283,7 @@ class Matcher:
         return lib().fscan_ctx_launches_last(self._h)
 
     KERNELS = ("rot_rows", "rot_cols", "rot_polar", "theta_in", "xlat_rows", "xlat_cols", "xlat_out",
-               "finalize", "rot_gather", "polar_to_cart", "mag_unpack")
+               "finalize", "rot_gather", "polar_to_cart", "mag_unpack", "bf_items", "bf_final")
 
     def set_profiling(self, on: bool):
         self._check(lib().fscan_ctx_set_profiling(self._h, int(bool(on))), "set_profiling")
@@ -352,6 +365,20 @@ class Matcher:
         self._check(st, "fscan_estimate_translation_batch")
         return txy
 
+    def brute_force(self, f, g, thetas, *, delta: float, out=None, stream=None):
+        """Exhaustive search over the theta candidates (oracle.cpp:40-67) for a batch
+        of CUDA pairs [B, N, N]; returns a uint8 device buffer of BF_DTYPE records
+        (decode with decode_bf_results)."""
+        import torch
+        b = int(f.shape[0])
+        th = np.ascontiguousarray(np.asarray(thetas, dtype=np.float64).ravel())
+        if out is None:
+            out = torch.empty(b * BF_DTYPE.itemsize, dtype=torch.uint8, device=f.device)
+        st = lib().fscan_brute_force_batch(self._h, _ptr(f), _ptr(g), b, th.ctypes.data, int(th.size),
+                                           float(delta), _ptr(out), _stream_ptr(stream))
+        self._check(st, "fscan_brute_force_batch")
+        return out
+
     def band_magnitude(self, img, *, stream=None):
         import torch
         b, n = int(img.shape[0]), int(img.shape[1])
@@ -365,6 +392,12 @@ def decode_results(buf) -> np.ndarray:
     """uint8 tensor/array of results -> numpy structured array (RESULT_DTYPE)."""
     a = buf.cpu().numpy() if hasattr(buf, "cpu") else np.asarray(buf)
     return np.frombuffer(a.tobytes(), dtype=RESULT_DTYPE).copy()
+
+
+def decode_bf_results(buf) -> np.ndarray:
+    """uint8 tensor/array of brute-force results -> numpy structured array (BF_DTYPE)."""
+    a = buf.cpu().numpy() if hasattr(buf, "cpu") else np.asarray(buf)
+    return np.frombuffer(a.tobytes(), dtype=BF_DTYPE).copy()
 
 
 def polar_to_cart(polar, *, range_res: float, n: int, delta: float, stream=None):
@@ -425,6 +458,37 @@ def scan_match(f, g, delta: float, config: MatchConfig | None = None, mask_f=Non
         if cfg.n_theta > 1 else np.zeros(1)
     return MatchResult(Pose2D(float(r["theta"]), float(r["tx"]), float(r["ty"])), ts[0][:, None], coords,
                        xs[0].astype(np.float64), r)
+
+
+@dataclass
+class OracleResult:
+    """Mirror of fscan::OracleResult (oracle.hpp:10-13)."""
+    pose: Pose2D
+    score: float
+    raw: np.void = field(repr=False, default=None)
+
+
+def brute_force_match(f, g, thetas, delta: float, config: MatchConfig | None = None) -> OracleResult:
+    """fscan::brute_force_match (oracle.hpp:20-23) for one pair of N x N arrays on the GPU."""
+    import torch
+    f = np.asarray(f)
+    n = int(f.shape[0])
+    if np.asarray(g).shape != f.shape:
+        _raise(ERR_INVALID_ARGUMENT, "brute_force_match: grid specs differ")
+    if len(np.atleast_1d(thetas)) == 0:
+        _raise(ERR_INVALID_ARGUMENT, "brute_force_match: empty theta candidate list")
+    cfg = MatchConfig(**(config or MatchConfig(n_xy=n, delta_xy=delta, n_radius=0)).__dict__)
+    cfg.n_xy = n
+    cfg = cfg.finalize()
+    key = ("bf", tuple(cfg.__dict__.items()))
+    m = _ctx_cache.get(key)
+    if m is None:
+        m = _ctx_cache[key] = Matcher(cfg, max_batch=1)
+    dev = torch.device("cuda", m.device)
+    ft = torch.as_tensor(np.ascontiguousarray(f, dtype=np.float32)).to(dev)[None]
+    gt = torch.as_tensor(np.ascontiguousarray(g, dtype=np.float32)).to(dev)[None]
+    r = decode_bf_results(m.brute_force(ft, gt, thetas, delta=delta))[0]
+    return OracleResult(Pose2D(float(r["theta"]), float(r["tx"]), float(r["ty"])), float(r["score"]), r)
 
 
 # ---------------------------------------------------------------- synthetic inputs

@@ -54,6 +54,11 @@ struct fscan_ctx {
     int alloc_chunk = 0; // workspace capacity (pairs)
     int n_live = 0;
     int rot_col_blocks = 0;  // K1b column blocks (8 columns each) the polar taps read
+    // brute-force search scratch (grown on demand)
+    double* bf_thetas = nullptr;
+    int bf_theta_cap = 0;
+    Partial* bf_items = nullptr;
+    int bf_item_cap = 0;
     int launches_last = 0;
     std::string err;
     std::mutex mu;
@@ -266,6 +271,7 @@ Params base_params(fscan_ctx* ctx, Lane& l, int batch, double delta) {
     p.taps = ctx->taps;
     p.n_live = ctx->n_live;
     p.zcols = 8 * ctx->rot_col_blocks;
+    p.src_div = 1;
     p.n_theta = ctx->cfg.n_theta;
     p.pad = ctx->cfg.pad_angle;
     p.L = ctx->cfg.n_theta + 2 * ctx->cfg.pad_angle;
@@ -284,7 +290,7 @@ enum class Stages { Full, Rotation, Translation, Magnitude };
 // Kernel ids for per-kernel profiling (fscan_ctx_kernel_times).
 enum KernelId { kRotRows = 0, kRotCols, kRotPolar, kThetaIn, kXlatRows, kXlatCols, kXlatOut, kFinalize,
                 kRotGather, kPolarToCart,
-                kMagUnpack, kNumKernels };
+                kMagUnpack, kBfItems, kBfFinal, kNumKernels };
 
 struct ProfEvent {
     int kid;
@@ -536,6 +542,8 @@ void fscan_ctx_destroy(fscan_ctx* ctx) {
     cudaFree(ctx->hann);
     cudaFree(ctx->band);
     cudaFree(ctx->taps);
+    cudaFree(ctx->bf_thetas);
+    cudaFree(ctx->bf_items);
     delete ctx;
 }
 
@@ -671,6 +679,67 @@ fscan_status fscan_estimate_translation_batch(fscan_ctx* ctx, const float* d_f, 
         p.xy_surf = d_xsurf ? d_xsurf + off * nn : nullptr;
         return run_chunk(ctx, l, p, Stages::Translation, &ctx->launches_last);
     });
+}
+
+fscan_status fscan_brute_force_batch(fscan_ctx* ctx, const float* d_f, const float* d_g, int batch,
+                                     const double* thetas, int nth, double delta, fscan_bf_result* d_out,
+                                     void* stream) {
+    fscan_status st = check_ctx(ctx, batch);
+    if (st != FSCAN_OK) return st;
+    std::lock_guard<std::mutex> g(ctx->mu);
+    if (!ctx->tw_n) return fail(ctx, FSCAN_ERR_INVALID_ARGUMENT, "context was not created successfully");
+    if (!d_f || !d_g || !d_out || !(delta > 0.0))
+        return fail(ctx, FSCAN_ERR_INVALID_ARGUMENT, "fscan_brute_force_batch: bad pointers or delta");
+    if (!thetas || nth < 1)  // oracle.cpp:46-47
+        return fail(ctx, FSCAN_ERR_INVALID_ARGUMENT, "brute_force_match: empty theta candidate list");
+    if ((long long)batch * nth > (1LL << 30))
+        return fail(ctx, FSCAN_ERR_INVALID_ARGUMENT, "fscan_brute_force_batch: too many (pair, theta) items");
+    if (batch == 0) return FSCAN_OK;
+    cudaStream_t user = (cudaStream_t)stream;
+    const int items = batch * nth;
+    if (ctx->bf_theta_cap < nth) {
+        cudaFree(ctx->bf_thetas);
+        ctx->bf_thetas = nullptr;
+        CK(cudaMalloc(&ctx->bf_thetas, sizeof(double) * nth));
+        ctx->bf_theta_cap = nth;
+    }
+    if (ctx->bf_item_cap < items) {
+        cudaFree(ctx->bf_items);
+        ctx->bf_items = nullptr;
+        CK(cudaMalloc(&ctx->bf_items, sizeof(Partial) * items));
+        ctx->bf_item_cap = items;
+    }
+    // the candidate list is small: a synchronous copy keeps the host array's lifetime simple
+    CK(cudaStreamSynchronize(user));
+    CK(cudaMemcpy(ctx->bf_thetas, thetas, sizeof(double) * nth, cudaMemcpyHostToDevice));
+    st = drive(ctx, items, user, [&](Lane& l, int off, int cnt) {
+        Params p = base_params(ctx, l, cnt, delta);
+        // brute_force_match scores the scans as given; only K3 reads ft / gt here
+        p.ft = const_cast<float*>(d_f);
+        p.gt = const_cast<float*>(d_g);
+        p.item_base = off;
+        p.src_div = nth;
+        p.theta_in = ctx->bf_thetas;
+        p.theta_mod = nth;
+        p.skip_surface = 1;
+        p.bf_items = ctx->bf_items;
+        cudaStream_t s = l.stream;
+        fscan_status r;
+#define FSCAN_LAUNCH(kid, call)                                                              \
+    if ((r = launch(ctx, l, kid, [&] { return call(p, s); }, &ctx->launches_last)) != FSCAN_OK) return r;
+        FSCAN_LAUNCH(kThetaIn, launch_theta_in);
+        FSCAN_LAUNCH(kXlatRows, launch_xlat_rows);
+        FSCAN_LAUNCH(kXlatCols, launch_xlat_cols);
+        FSCAN_LAUNCH(kXlatOut, launch_xlat_out);
+        FSCAN_LAUNCH(kBfItems, launch_bf_items);
+#undef FSCAN_LAUNCH
+        return FSCAN_OK;
+    });
+    if (st != FSCAN_OK) return st;
+    // all lanes are joined into `user`: the per-pair winner over the candidates
+    CK(launch_bf_final(ctx->bf_items, ctx->bf_thetas, nth, batch, ctx->n, delta, d_out, user));
+    ++ctx->launches_last;
+    return FSCAN_OK;
 }
 
 fscan_status fscan_band_magnitude_batch(fscan_ctx* ctx, const float* d_img, int batch, float* d_out,

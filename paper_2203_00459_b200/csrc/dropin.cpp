@@ -5,12 +5,14 @@
 //   finalize / validate              matcher.cpp:11-37 (validate without the odd-n rule, D1)
 //   soft_argmax                      matcher.cpp:57-93 (host utility on a given surface)
 //   geometry helpers                 proj/src/geometry.cpp:9-70
+//   brute_force_match / timing_comparison   proj/src/oracle.cpp:40-101
 // Single-pair calls convert the fp64 grids to fp32, run the batch pipeline on
 // device 0 with a cached per-config context, and return surfaces as doubles.
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <charconv>
+#include <chrono>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -21,6 +23,7 @@
 #include <vector>
 
 #include "fscan/matcher.hpp"
+#include "fscan/oracle.hpp"
 #include "fscan_cuda.h"
 
 namespace fscan {
@@ -363,6 +366,53 @@ void scan_match_batch(const float* d_f, const float* d_g, const float* d_mf, con
             d.xy_col = h[i].xy_col;
         }
     }
+}
+
+// ---- exhaustive search (oracle.cpp:40-101) ----
+
+OracleResult brute_force_match(const ScanGrid& f, const ScanGrid& g, const std::vector<double>& thetas,
+                               const MatchConfig& cfg) {
+    if (!(f.spec == g.spec)) throw std::invalid_argument("brute_force_match: grid specs differ");
+    if (thetas.empty()) throw std::invalid_argument("brute_force_match: empty theta candidate list");
+    MatchConfig c = cfg;  // the context is sized from the grid; the search ignores the rest
+    c.n_xy = f.spec.n;
+    c.delta_xy = f.spec.delta;
+    finalize(c);
+    fscan_ctx* ctx = context_for(c, 0, 1);
+    const int n = f.spec.n;
+    DevBuf<float> df((std::size_t)n * n), dg((std::size_t)n * n);
+    DevBuf<fscan_bf_result> res(1);
+    upload(f.values, df.p);
+    upload(g.values, dg.p);
+    check(fscan_brute_force_batch(ctx, df.p, dg.p, 1, thetas.data(), (int)thetas.size(), f.spec.delta, res.p,
+                                  nullptr),
+          ctx, "brute_force_match");
+    fscan_bf_result h;
+    ck(cudaMemcpy(&h, res.p, sizeof h, cudaMemcpyDeviceToHost), "D2H");
+    return OracleResult{Pose2D{h.theta, h.tx, h.ty}, h.score};
+}
+
+TimingComparison timing_comparison(const ScanGrid& f, const ScanGrid& g, const MatchConfig& cfg, int repeats) {
+    if (repeats < 10) throw std::invalid_argument("timing_comparison: repeats must be >= 10");
+    std::vector<double> thetas(cfg.n_theta);
+    for (int k = 0; k < cfg.n_theta; ++k) thetas[k] = (k - cfg.n_theta / 2) * cfg.delta_theta;
+    auto median_of = [&](auto&& fn) {
+        for (int i = 0; i < 3; ++i) fn();  // burn-in
+        std::vector<double> ms(repeats);
+        for (int i = 0; i < repeats; ++i) {
+            const auto t0 = std::chrono::steady_clock::now();
+            fn();
+            ms[i] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        }
+        std::sort(ms.begin(), ms.end());
+        return ms[ms.size() / 2];
+    };
+    TimingComparison out;
+    out.repeats = repeats;
+    out.matcher_median_ms = median_of([&] { (void)scan_match(f, g, cfg); });
+    out.oracle_median_ms = median_of([&] { (void)brute_force_match(f, g, thetas, cfg); });
+    out.ratio = out.oracle_median_ms / out.matcher_median_ms;
+    return out;
 }
 
 }  // namespace fscan

@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(kPolarThreads) k_rot_polar(Params p) {
 __global__ void k_theta_in(Params p) {
     const int pair = blockIdx.x * blockDim.x + threadIdx.x;
     if (pair >= p.batch) return;
-    const double theta = p.theta_in[pair];
+    const double theta = p.theta_mod > 0 ? p.theta_in[(p.item_base + pair) % p.theta_mod] : p.theta_in[pair];
     RotState* rs = p.rot + pair;
     rs->theta = theta;
     double sn, cs;
@@ -439,8 +439,9 @@ __global__ void __launch_bounds__(kXThreads) k_xlat_rows(Params p) {
     const int pair = blockIdx.y;
     const int y0 = blockIdx.x * ROWS;
     const RotState rs = p.rot[pair];
-    const float* ft = p.ft + (size_t)pair * N * N;
-    const float* gt = p.gt + (size_t)pair * N * N;
+    const int src = (p.item_base + pair) / p.src_div;  // pair whose scans this item reads
+    const float* ft = p.ft + (size_t)src * N * N;
+    const float* gt = p.gt + (size_t)src * N * N;
     const float c0f32 = (N - 1) / 2.0f;  // exact
     // rotate_bilinear(g~, -theta); -theta == 0.0 returns g~ itself, which st = 0,
     // ct = 1 reproduce exactly (integer source coordinates, zero fractions)
@@ -695,7 +696,7 @@ __global__ void __launch_bounds__(XOutGeom<N>::THREADS) k_xlat_out(Params p) {
     int best_i = 0x7fffffff;
     auto emit = [&](int kx, float val) {
         const int j = kx + half;
-        srow[j] = val;
+        if (!p.skip_surface) srow[j] = val;
         const int li = i * N + j;
         if (val > best_v || (val == best_v && li < best_i)) {
             best_v = val;
@@ -877,6 +878,51 @@ __global__ void k_polar_to_cart(const float* polar, int n_az, int n_range, doubl
         polar + (size_t)pair * n_az * n_range, n_az, n_range, res, n, delta, r, c);
 }
 
+// Brute-force correlative search (oracle.cpp:21-67): per (pair, candidate)
+// item the hard argmax of its translation surface from K5's block partials
+// (strict >, lowest linear index on ties, like score_theta's row-major scan).
+__global__ void k_bf_items(Params p, int nparts) {
+    const int item = blockIdx.x * blockDim.x + threadIdx.x;
+    if (item >= p.batch) return;
+    const Partial* pp = p.part + (size_t)item * nparts;
+    Partial b = pp[0];
+    for (int k = 1; k < nparts; ++k)
+        if (pp[k].val > b.val || (pp[k].val == b.val && pp[k].idx < b.idx)) b = pp[k];
+    p.bf_items[p.item_base + item] = b;
+}
+
+// Winner over the candidates of each pair (strict >: the earlier theta wins
+// ties, oracle.cpp:56-58) and its pose: t = R(theta) (col - half, row - half) delta.
+__global__ void k_bf_final(const Partial* items, const double* thetas, int nth, int batch, int n,
+                           double delta, fscan_bf_result* out) {
+    const int pair = blockIdx.x * blockDim.x + threadIdx.x;
+    if (pair >= batch) return;
+    const Partial* it = items + (size_t)pair * nth;
+    int w = 0;
+    for (int k = 1; k < nth; ++k)
+        if (it[k].val > it[w].val) w = k;
+    const int half = (n - 1) / 2;
+    const int row = it[w].idx / n, col = it[w].idx % n;
+    const double theta = thetas[w];
+    const double dx = (col - half) * delta, dy = (row - half) * delta;
+    double sn, cs;
+    sincos(theta, &sn, &cs);  // rotate_vec (geometry.cpp:31-35)
+    const double two_pi = 6.283185307179586, pi = 3.141592653589793;
+    double th = fmod(theta, two_pi);  // normalize_angle (geometry.cpp:9-14)
+    if (th <= -pi) th += two_pi;
+    if (th > pi) th -= two_pi;
+    fscan_bf_result o;
+    o.theta = th;
+    o.tx = cs * dx - sn * dy;
+    o.ty = sn * dx + cs * dy;
+    o.score = (double)it[w].val;
+    o.theta_index = w;
+    o.xy_row = row;
+    o.xy_col = col;
+    o.status = isfinite(it[w].val) ? FSCAN_OK : FSCAN_ERR_NONFINITE;
+    out[pair] = o;
+}
+
 template <typename K>
 cudaError_t set_smem(K kernel, size_t bytes) {
     if (bytes > 48 * 1024)
@@ -987,6 +1033,17 @@ cudaError_t launch_finalize(const Params& p, cudaStream_t s) {
 cudaError_t launch_mag_unpack(const Params& p, cudaStream_t s) {
     const size_t total = (size_t)p.n * (p.n / 2);
     k_mag_unpack<<<dim3((unsigned)((total + 255) / 256), p.batch), 256, 0, s>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bf_items(const Params& p, cudaStream_t s) {
+    k_bf_items<<<(p.batch + 127) / 128, 128, 0, s>>>(p, p.n / rows_per_block_out(p.n));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bf_final(const Partial* items, const double* thetas, int n_thetas, int batch, int n,
+                            double delta, fscan_bf_result* out, cudaStream_t s) {
+    k_bf_final<<<(batch + 127) / 128, 128, 0, s>>>(items, thetas, n_thetas, batch, n, delta, out);
     return cudaGetLastError();
 }
 

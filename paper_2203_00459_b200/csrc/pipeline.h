@@ -74,6 +74,13 @@ struct Params {
     double* txy_only;         // stage API: (tx, ty) per pair (nullable)
     const double* theta_in;   // stage API: theta per pair for translation-only runs
     float* mag_out;           // stage API: band magnitude, [batch][N][N/2] (nullable)
+    // translation items: item i of this launch is global item item_base + i; it
+    // reads the masked scans of pair (item_base + i) / src_div (1 for matching;
+    // the candidate count for the brute-force search) and, with theta_mod > 0,
+    // theta_in[(item_base + i) % theta_mod]
+    int item_base, src_div, theta_mod;
+    int skip_surface;         // K5 keeps only the block argmaxes (brute-force search)
+    Partial* bf_items;        // brute force: per global item hard argmax (nullable)
 };
 
 // Launch the stages; each returns cudaGetLastError() of its launch.
@@ -87,6 +94,9 @@ cudaError_t launch_xlat_cols(const Params& p, cudaStream_t s);       // K4
 cudaError_t launch_xlat_out(const Params& p, cudaStream_t s);        // K5
 cudaError_t launch_finalize(const Params& p, cudaStream_t s);        // K6
 cudaError_t launch_mag_unpack(const Params& p, cudaStream_t s);      // stage API helper
+cudaError_t launch_bf_items(const Params& p, cudaStream_t s);        // brute force: item argmax
+cudaError_t launch_bf_final(const Partial* items, const double* thetas, int n_thetas, int batch, int n,
+                            double delta, fscan_bf_result* out, cudaStream_t s);  // brute force: winner
 cudaError_t launch_polar_to_cart(const float* d_polar, int batch, int n_az, int n_range,
                                  double range_res, int n, double delta, float* d_out,
                                  cudaStream_t stream);                  // K0

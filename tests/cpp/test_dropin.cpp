@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "fscan/matcher.hpp"
+#include "fscan/oracle.hpp"
 
 using namespace fscan;
 
@@ -83,6 +84,27 @@ MatchConfig small_cfg(int n, double delta, int n_theta) {  // test_matcher.cpp:1
     finalize(cfg);
     validate(cfg);
     return cfg;
+}
+
+ScanGrid noise_scan(const GridSpec& spec, unsigned seed) {  // test_oracle.cpp:28-34
+    unsigned long long st = seed * 2654435761ull + 7;
+    ScanGrid out = ScanGrid::zeros(spec);
+    for (std::size_t i = 0; i < out.values.size(); ++i) {
+        st = st * 6364136223846793005ull + 1442695040888963407ull;
+        out.values[i] = (double)(st >> 11) * 0x1.0p-53;
+    }
+    return out;
+}
+
+ScanGrid shift_grid(const ScanGrid& f, int dr, int dc) {  // test_oracle.cpp:36-46
+    const int n = f.spec.n;
+    ScanGrid out = ScanGrid::zeros(f.spec);
+    for (int r = 0; r < n; ++r)
+        for (int c = 0; c < n; ++c) {
+            const int rr = r + dr, cc = c + dc;
+            if (rr >= 0 && rr < n && cc >= 0 && cc < n) out.values(rr, cc) = f.values(r, c);
+        }
+    return out;
 }
 
 CorrelationSurface surface_from(const Array2D& scores) {
@@ -260,6 +282,72 @@ int main() {
         }
         cudaFree(df);
         cudaFree(dg);
+    }
+    // ---- exhaustive search (proj/tests/test_oracle.cpp) ----
+    // self match scores the total power at the identity (test_oracle.cpp:96-110)
+    {
+        const GridSpec sp{64, 0.4};
+        const ScanGrid f = noise_scan(sp, 4);
+        const MatchConfig c = small_cfg(64, 0.4, 65);
+        const OracleResult r = brute_force_match(f, f, {-0.2, 0.0, 0.2}, c);
+        double sum_sq = 0.0;
+        for (std::size_t i = 0; i < f.values.size(); ++i) sum_sq += f.values[i] * f.values[i];
+        CHECK(r.pose.theta == 0.0 && r.pose.tx == 0.0 && r.pose.ty == 0.0);
+        CHECK(std::abs(r.score - sum_sq) <= 1e-5 * sum_sq);  // fp32 path
+    }
+    // integer shift with a single theta candidate (test_oracle.cpp:112-122)
+    {
+        const GridSpec sp{64, 0.4};
+        const auto bs = scene(64, 0.4, 31, 14);
+        const ScanGrid f = render(bs, sp, Pose2D::identity());
+        const ScanGrid g = shift_grid(f, -3, 5);  // content moved -3 rows, +5 cols
+        const OracleResult r = brute_force_match(f, g, {0.0}, small_cfg(64, 0.4, 129));
+        CHECK(r.pose.theta == 0.0);
+        CHECK(std::abs(r.pose.tx - 5 * sp.delta) < 1e-12 && std::abs(r.pose.ty - 3 * sp.delta) < 1e-12);
+    }
+    // agrees with the matcher on synthetic pairs (test_oracle.cpp:136-160)
+    {
+        const GridSpec sp{128, 0.4};  // n = 65 there; 64 is too small for the even-n matcher
+        const MatchConfig c = small_cfg(128, 0.4, 129);
+        std::vector<double> ths;
+        for (int k = 0; k < c.n_theta; ++k) {
+            const double t = (k - c.n_theta / 2) * c.delta_theta;
+            if (std::abs(t) <= 0.8) ths.push_back(t);
+        }
+        const Pose2D rels[3] = {{0.31, 1.2, -0.8}, {-0.22, -2.0, 0.4}, {0.05, 0.8, 2.0}};
+        for (int trial = 0; trial < 3; ++trial) {
+            const auto bs = scene(128, 0.4, 600 + trial, 30);
+            const ScanGrid f = render(bs, sp, Pose2D::identity());
+            const ScanGrid g = render(bs, sp, rels[trial]);
+            const Pose2D m = scan_match(f, g, c).pose;
+            const Pose2D o = brute_force_match(f, g, ths, c).pose;
+            CHECK(std::abs(normalize_angle(m.theta - o.theta)) <= 2.0 * c.delta_theta);
+            CHECK(std::abs(m.tx - o.tx) <= sp.delta && std::abs(m.ty - o.ty) <= sp.delta);
+            std::printf("trial %d truth (%.4f %.3f %.3f) matcher (%.4f %.3f %.3f) exhaustive (%.4f %.3f %.3f)\n", trial,
+                        rels[trial].theta, rels[trial].tx, rels[trial].ty, m.theta, m.tx, m.ty, o.theta, o.tx, o.ty);
+        }
+    }
+    // input validation (test_oracle.cpp:162-167)
+    {
+        const GridSpec sp{64, 0.4};
+        const ScanGrid f = noise_scan(sp, 1);
+        const MatchConfig c = small_cfg(64, 0.4, 65);
+        CHECK_THROWS_AS(brute_force_match(f, f, {}, c), std::invalid_argument);
+        const ScanGrid g = noise_scan(GridSpec{64, 0.5}, 1);
+        CHECK_THROWS_AS(brute_force_match(f, g, {0.0}, c), std::invalid_argument);
+        CHECK_THROWS_AS(timing_comparison(f, f, c, 9), std::invalid_argument);
+    }
+    // timing: the exhaustive search costs more per call (test_oracle.cpp:184-196, ratio grows with n_theta)
+    {
+        const GridSpec sp{64, 0.4};
+        const MatchConfig c = small_cfg(64, 0.4, 129);
+        const auto bs = scene(64, 0.4, 77, 14);
+        const ScanGrid f = render(bs, sp, Pose2D::identity());
+        const ScanGrid g = render(bs, sp, Pose2D{0.1, 0.4, -0.4});
+        const TimingComparison tc = timing_comparison(f, g, c, 10);
+        CHECK(tc.repeats == 10 && tc.matcher_median_ms > 0.0 && tc.ratio > 1.0);
+        std::printf("timing_comparison n=64 n_theta=129: matcher %.3f ms, exhaustive %.3f ms, ratio %.1f\n",
+                    tc.matcher_median_ms, tc.oracle_median_ms, tc.ratio);
     }
     std::printf("%d checks, %d failed\n", g_checks, g_fail);
     if (g_fail == 0) std::printf("ALL PASSED\n");

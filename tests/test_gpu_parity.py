@@ -340,3 +340,80 @@ def test_match_polar_equals_k0_then_match(fb, orc, dev):
         r = orc.scan_match(cfn[i], cgn[i], oc, delta, mf[i], mg[i])
         assert (a[i]["theta_bin"], a[i]["xy_row"], a[i]["xy_col"]) == (r.theta_bin, r.xy_row, r.xy_col)
         assert abs(a[i]["theta"] - r.theta) <= THETA_TOL
+
+
+# ---- exhaustive search (proj/src/oracle.cpp:21-67) ----
+
+def bf_compare(r, o, n, stats):
+    """GPU record vs oracle FoBfResult: same candidate and cell (documented near-ties
+    excepted by the caller), score within the surface tolerance, pose from the same
+    integers."""
+    assert abs(r["score"] - o.score) <= SURF_TOL * abs(o.score), (r["score"], o.score)
+    stats.append(abs(r["score"] - o.score) / abs(o.score))
+    assert (int(r["theta_index"]), int(r["xy_row"]), int(r["xy_col"])) == (o.theta_index, o.xy_row, o.xy_col)
+    assert abs(r["theta"] - o.theta) < 1e-12
+    assert abs(r["tx"] - o.tx) < 1e-9 and abs(r["ty"] - o.ty) < 1e-9
+
+
+@pytest.mark.parametrize("n,nth", [(64, 17), (128, 9)])
+def test_brute_force_matches_oracle(fb, orc, dev, n, nth):
+    spec = fb.synth_spec(1, n=n, delta=0.4)
+    f, g, _, _, _ = fb.synth_pairs_host(spec, 3, 3)
+    thetas = (np.arange(nth) - nth // 2) * 0.02
+    cfg = fb.MatchConfig.for_grid(n, 0.4, 65, band_lo=0.15)
+    m = fb.Matcher(cfg, max_batch=3, chunk=5)  # 5 items per chunk: chunks straddle pairs and lanes
+    F, G = to_dev(dev, f, g)
+    res = fb.decode_bf_results(m.brute_force(F, G, thetas, delta=0.4))
+    stats = []
+    for i in range(3):
+        o = orc.brute_force(f[i].astype(np.float64), g[i].astype(np.float64), thetas, 0.4)
+        bf_compare(res[i], o, n, stats)
+        assert res[i]["status"] == fb.OK
+    print("max score rel err", max(stats))
+
+
+def test_brute_force_c2_geometry(fb, orc, dev):
+    """N = 256 (C2 grid), candidates around the truth, vs the oracle."""
+    spec = fb.synth_spec(2)
+    f, g, _, _, truth = fb.synth_pairs_host(spec, 40, 2)
+    cfg, delta, _ = fb.baseline_config(2)
+    m = fb.Matcher(cfg, max_batch=2)
+    F, G = to_dev(dev, f, g)
+    stats = []
+    for i in range(2):
+        th0 = float(truth[i][0])
+        thetas = th0 + (np.arange(7) - 3) * cfg.delta_theta
+        res = fb.decode_bf_results(m.brute_force(F[i:i + 1], G[i:i + 1], thetas, delta=delta))
+        o = orc.brute_force(f[i].astype(np.float64), g[i].astype(np.float64), thetas, delta)
+        bf_compare(res[0], o, 256, stats)
+
+
+def test_brute_force_known_answers(fb, dev):  # test_oracle.cpp:96-122
+    n = 64
+    rng = np.random.default_rng(4)
+    f = rng.random((n, n))
+    r = fb.brute_force_match(f, f, [-0.2, 0.0, 0.2], 0.4)
+    assert (r.pose.theta, r.pose.tx, r.pose.ty) == (0.0, 0.0, 0.0)
+    assert abs(r.score - float((f.astype(np.float32).astype(np.float64) ** 2).sum())) <= 1e-5 * r.score
+    spec = fb.synth_spec(1, n=n, delta=0.4)
+    f1, _, _, _, _ = fb.synth_pairs_host(spec, 5, 1)
+    g1 = np.zeros_like(f1[0])
+    g1[:-3, 5:] = f1[0, 3:, :-5]
+    r = fb.brute_force_match(f1[0], g1, [0.0], 0.4)
+    assert r.pose.theta == 0.0 and abs(r.pose.tx - 2.0) < 1e-12 and abs(r.pose.ty - 1.2) < 1e-12
+    with pytest.raises(fb.FscanInvalidArgument):
+        fb.brute_force_match(f, f, [], 0.4)
+
+
+def test_brute_force_agrees_with_decoupled_matcher(fb, dev):  # test_oracle.cpp:136-160
+    cfg, delta, _ = fb.baseline_config(2)
+    f, g, mf, mg, _ = fb.synth_pairs_host(fb.synth_spec(2), 60, 3)
+    res, _, _ = run_gpu(fb, dev, cfg, delta, f, g)
+    thetas = np.array([(k - cfg.n_theta // 2) * cfg.delta_theta for k in range(cfg.n_theta)])
+    thetas = thetas[np.abs(thetas) <= 0.12]
+    m = fb.Matcher(cfg, max_batch=3)
+    F, G = to_dev(dev, f, g)
+    bf = fb.decode_bf_results(m.brute_force(F, G, thetas, delta=delta))
+    for i in range(3):
+        assert abs(bf[i]["theta"] - res[i]["theta"]) <= 2 * cfg.delta_theta
+        assert abs(bf[i]["tx"] - res[i]["tx"]) <= delta and abs(bf[i]["ty"] - res[i]["ty"]) <= delta

@@ -219,3 +219,73 @@ def test_restatement_bit_exact_vs_reference_live(orc, n, nt):
     for th in (0.0, 0.3, -0.22):
         np.testing.assert_array_equal(orc.rotate_bilinear(f, th), orc.rotate_bilinear(f, th, which="ref"))
     np.testing.assert_array_equal(orc.cart2pol(f, 90, 33, math.pi), orc.cart2pol(f, 90, 33, math.pi, which="ref"))
+
+
+# ---- exhaustive search (proj/src/oracle.cpp, proj/tests/test_oracle.cpp) ----
+
+def _blobs(n, seed, count=12):
+    rng = np.random.default_rng(seed)
+    yy, xx = np.mgrid[0:n, 0:n].astype(np.float64)
+    img = np.zeros((n, n))
+    for _ in range(count):
+        cy, cx = rng.uniform(0.15 * n, 0.85 * n, 2)
+        s = rng.uniform(1.5, 3.0)
+        img += rng.uniform(0.3, 1.0) * np.exp(-((yy - cy) ** 2 + (xx - cx) ** 2) / (2 * s * s))
+    return img
+
+
+def test_brute_force_self_match_scores_total_power(orc):  # test_oracle.cpp:96-110
+    f = np.random.default_rng(4).random((33, 33))
+    r = orc.brute_force(f, f, [-0.2, 0.0, 0.2], 0.4)
+    assert (r.theta, r.tx, r.ty) == (0.0, 0.0, 0.0)
+    assert r.score == pytest.approx(float((f * f).sum()), rel=1e-9)
+
+
+def test_brute_force_integer_shift_single_candidate(orc):  # test_oracle.cpp:112-122
+    f = _blobs(64, 31)
+    g = np.zeros_like(f)
+    g[:-3, 5:] = f[3:, :-5]  # content moved -3 rows, +5 cols: world t = (+5, +3) cells
+    r = orc.brute_force(f, g, [0.0], 0.4)
+    assert r.theta == 0.0
+    assert abs(r.tx - 5 * 0.4) < 1e-12 and abs(r.ty - 3 * 0.4) < 1e-12
+
+
+def test_brute_force_matches_spatial_triple_loop(orc):  # test_oracle.cpp:48-89, 124-134
+    n = 12
+    rng = np.random.default_rng(7)
+    f, g = rng.random((n, n)) - 0.5, rng.random((n, n)) - 0.5
+    thetas = [k * 0.1 for k in range(-3, 4)]
+    half = (n - 1) // 2
+    best = (-1e300, 0.0, 0, 0)
+    for th in thetas:
+        gr = orc.rotate_bilinear(g, -th)
+        for i in range(n):
+            for j in range(n):
+                oy, ox = i - half, j - half
+                r0, r1 = max(0, oy), min(n, n + oy)
+                c0, c1 = max(0, -ox), min(n, n - ox)
+                acc = float((f[r0:r1, c0:c1] * gr[r0 - oy:r1 - oy, c0 + ox:c1 + ox]).sum())
+                if acc > best[0]:
+                    best = (acc, th, i, j)
+    r = orc.brute_force(f, g, thetas, 0.5)
+    assert r.score == pytest.approx(best[0], rel=1e-6)
+    assert r.theta == pytest.approx(best[1], abs=1e-12)
+    assert (r.xy_row, r.xy_col) == (best[2], best[3])
+
+
+def test_brute_force_rejects_empty_candidate_list(orc):  # test_oracle.cpp:162-167
+    with pytest.raises(orc.OracleError):
+        orc.brute_force(np.zeros((8, 8)), np.zeros((8, 8)), [], 0.4)
+
+
+@ref_only
+@pytest.mark.parametrize("n", [33, 64])
+def test_brute_force_restatement_bit_exact_vs_reference(orc, n):
+    f = _blobs(n, 100 + n)
+    rng = np.random.default_rng(n)
+    g = np.roll(f, (2, -1), (0, 1)) + 0.05 * rng.random((n, n))
+    thetas = np.arange(-6, 7) * 0.05
+    a = orc.brute_force(f, g, thetas, 0.4)
+    b = orc.brute_force(f, g, thetas, 0.4, which="ref")
+    assert (a.theta, a.tx, a.ty, a.score) == (b.theta, b.tx, b.ty, b.score)
+    assert (a.theta_index, a.xy_row, a.xy_col) == (b.theta_index, b.xy_row, b.xy_col)

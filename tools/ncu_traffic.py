@@ -1,0 +1,37 @@
+"""profiles/ncu_traffic.json from an ncu --set full capture of one C4 step:
+DRAM bytes (read + write) per launch and per pair for every pipeline kernel.
+Pairs per launch come from k_rot_gather's grid (8 CTAs per pair).
+usage: python tools/ncu_traffic.py REP SOURCE_NOTE > profiles/ncu_traffic.json"""
+import csv
+import io
+import json
+import subprocess
+import sys
+
+rep, note = sys.argv[1], sys.argv[2]
+out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(out)))
+hdr = rows[0]
+
+
+units = rows[1]
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3,
+         "second": 1e6, "": 1}
+
+
+def col(r, name):
+    i = hdr.index(name)
+    return float(r[i].replace(",", "")) * SCALE.get(units[i], 1)
+
+
+recs = []
+for r in rows[2:]:
+    k = r[hdr.index("Kernel Name")].split("(")[0].split("::")[-1]
+    k = k.split("<")[0].replace("k_", "", 1)
+    recs.append((k, col(r, "dram__bytes_read.sum") + col(r, "dram__bytes_write.sum"),
+                 col(r, "gpu__time_duration.sum"), col(r, "launch__grid_size")))
+ppl = next(int(g) // 8 for k, _, _, g in recs if k == "rot_gather")
+res = {"source": note, "pairs_per_launch": ppl}
+for k, b, us, _ in recs:
+    res[k] = {"dram_bytes_per_launch": b, "dram_bytes_per_pair": b / ppl, "duration_us": round(us, 3)}
+print(json.dumps(res, indent=1))
