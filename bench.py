@@ -79,7 +79,7 @@ def kernel_alg_bytes(name: str, n: int) -> float:
         "mag_unpack": 0.0,
         "bf_items": 0.0,
         "bf_final": 0.0,
-        "polar_to_cart": 4 * 400 * 3768 + 4 * nn,         # one raw sweep in, one grid out (per launch: f or g)
+        "polar_to_cart": 2 * (4 * 400 * 3768 + 4 * nn),   # both raw sweeps in, both grids out
     }[name]
 
 

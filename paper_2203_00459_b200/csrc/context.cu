@@ -38,6 +38,9 @@ struct Lane {
     // host-API staging
     float* in = nullptr;  // 4 grids x chunk
     float* cart = nullptr;  // K0 output (polar API): 2 grids x chunk
+    void* k0tab = nullptr;  // K0 tap table of the last polar geometry (built on this lane's stream)
+    int k0_naz = 0;
+    double k0_res = 0.0, k0_delta = 0.0;
     fscan_pair_result* res = nullptr;
     double* tsurf = nullptr;
     float* xsurf = nullptr;
@@ -217,6 +220,7 @@ void free_lane(Lane& l) {
     cudaFree(l.flags);
     cudaFree(l.in);
     cudaFree(l.cart);
+    cudaFree(l.k0tab);
     cudaFree(l.res);
     cudaFree(l.tsurf);
     cudaFree(l.xsurf);
@@ -615,19 +619,22 @@ fscan_status fscan_match_batch_polar(fscan_ctx* ctx, const float* d_pf, const fl
     if (batch == 0) return FSCAN_OK;
     const size_t nn = (size_t)ctx->n * ctx->n, np = (size_t)n_az * n_range;
     const int nt = ctx->cfg.n_theta;
-    for (Lane& l : LaneRange{ctx})
+    for (Lane& l : LaneRange{ctx}) {
         if (!l.cart) CK(cudaMalloc(&l.cart, 2 * nn * sizeof(float) * ctx->alloc_chunk));
+        if (!l.k0tab) CK(cudaMalloc(&l.k0tab, polar_tap_bytes(ctx->n)));
+        if (l.k0_naz != n_az || l.k0_res != range_res || l.k0_delta != delta) {  // K0 geometry changed
+            CK(launch_polar_taps(n_az, range_res, ctx->n, delta, l.k0tab, l.stream));
+            l.k0_naz = n_az;
+            l.k0_res = range_res;
+            l.k0_delta = delta;
+        }
+    }
     return drive(ctx, batch, (cudaStream_t)stream, [&](Lane& l, int off, int cnt) {
         // K0: both sweeps of the chunk -> Cartesian grids in the lane's staging buffer
         fscan_status s2;
         if ((s2 = launch(ctx, l, kPolarToCart, [&] {
-                 return launch_polar_to_cart(d_pf + off * np, cnt, n_az, n_range, range_res, ctx->n, delta,
-                                             l.cart, l.stream);
-             }, &ctx->launches_last)) != FSCAN_OK)
-            return s2;
-        if ((s2 = launch(ctx, l, kPolarToCart, [&] {
-                 return launch_polar_to_cart(d_pg + off * np, cnt, n_az, n_range, range_res, ctx->n, delta,
-                                             l.cart + nn * cnt, l.stream);
+                 return launch_polar_to_cart(d_pf + off * np, d_pg + off * np, cnt, n_az, n_range, range_res,
+                                             ctx->n, delta, l.cart, l.cart + nn * cnt, l.stream, l.k0tab);
              }, &ctx->launches_last)) != FSCAN_OK)
             return s2;
         Params p = base_params(ctx, l, cnt, delta);
@@ -854,8 +861,8 @@ fscan_status fscan_polar_to_cart_batch(const float* d_polar, int batch, int n_az
     if (!d_polar || !d_out || batch < 0 || n_az < 1 || n_range < 1 || n < 1 || !(range_res > 0) || !(delta > 0))
         return FSCAN_ERR_INVALID_ARGUMENT;
     if (batch == 0) return FSCAN_OK;
-    cudaError_t e = launch_polar_to_cart(d_polar, batch, n_az, n_range, range_res, n, delta, d_out,
-                                         (cudaStream_t)stream);
+    cudaError_t e = launch_polar_to_cart(d_polar, nullptr, batch, n_az, n_range, range_res, n, delta, d_out,
+                                         nullptr, (cudaStream_t)stream);
     return e == cudaSuccess ? FSCAN_OK : FSCAN_ERR_CUDA;
 }
 

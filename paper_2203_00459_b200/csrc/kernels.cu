@@ -868,14 +868,22 @@ __global__ void k_mag_unpack(Params p) {
     p.mag_out[(size_t)pair * n * (n / 2) + idx] = m[((size_t)(u >> 3) * n + vc) * 8 + (u & 7)];
 }
 
-__global__ void k_polar_to_cart(const float* polar, int n_az, int n_range, double res, int n,
-                                double delta, float* out) {
+// K0 in two steps: the cell geometry (fp64 atan2 / sqrt, identical for every
+// sweep of a call) once into a table, then a pure gather per sweep.
+__global__ void k_polar_taps(int n_az, double res, int n, double delta, fscan_k0::PolarTap* tab) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= n * n) return;
+    tab[idx] = fscan_k0::polar_tap(n_az, res, n, delta, idx / n, idx % n);
+}
+
+__global__ void k_polar_to_cart(const float* polar0, const float* polar1, int n_az, int n_range, int n,
+                                const fscan_k0::PolarTap* __restrict__ tab, float* out0, float* out1) {
     const int pair = blockIdx.y;
-    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= (size_t)n * n) return;
-    const int r = (int)(idx / n), c = (int)(idx % n);
-    out[(size_t)pair * n * n + idx] = (float)fscan_k0::polar_cell(
-        polar + (size_t)pair * n_az * n_range, n_az, n_range, res, n, delta, r, c);
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= n * n) return;
+    const float* polar = (blockIdx.z ? polar1 : polar0) + (size_t)pair * n_az * n_range;
+    float* out = blockIdx.z ? out1 : out0;
+    out[(size_t)pair * n * n + idx] = (float)fscan_k0::polar_sample(polar, n_range, tab[idx]);
 }
 
 // Brute-force correlative search (oracle.cpp:21-67): per (pair, candidate)
@@ -1047,12 +1055,32 @@ cudaError_t launch_bf_final(const Partial* items, const double* thetas, int n_th
     return cudaGetLastError();
 }
 
-cudaError_t launch_polar_to_cart(const float* d_polar, int batch, int n_az, int n_range, double range_res,
-                                 int n, double delta, float* d_out, cudaStream_t stream) {
-    const size_t total = (size_t)n * n;
-    k_polar_to_cart<<<dim3((unsigned)((total + 255) / 256), batch), 256, 0, stream>>>(
-        d_polar, n_az, n_range, range_res, n, delta, d_out);
+size_t polar_tap_bytes(int n) { return sizeof(fscan_k0::PolarTap) * (size_t)n * n; }
+
+cudaError_t launch_polar_taps(int n_az, double range_res, int n, double delta, void* tab, cudaStream_t stream) {
+    const int total = n * n;
+    k_polar_taps<<<(total + 255) / 256, 256, 0, stream>>>(n_az, range_res, n, delta,
+                                                           static_cast<fscan_k0::PolarTap*>(tab));
     return cudaGetLastError();
+}
+
+cudaError_t launch_polar_to_cart(const float* d_polar0, const float* d_polar1, int batch, int n_az,
+                                 int n_range, double range_res, int n, double delta, float* d_out0,
+                                 float* d_out1, cudaStream_t stream, const void* tab) {
+    const int total = n * n;
+    void* own = nullptr;
+    if (!tab) {  // no cached table: build one for this call
+        cudaError_t e = cudaMallocAsync(&own, polar_tap_bytes(n), stream);
+        if (e != cudaSuccess) return e;
+        e = launch_polar_taps(n_az, range_res, n, delta, own, stream);
+        if (e != cudaSuccess) return e;
+        tab = own;
+    }
+    k_polar_to_cart<<<dim3((unsigned)((total + 255) / 256), batch, d_polar1 ? 2 : 1), 256, 0, stream>>>(
+        d_polar0, d_polar1, n_az, n_range, n, static_cast<const fscan_k0::PolarTap*>(tab), d_out0, d_out1);
+    cudaError_t e = cudaGetLastError();
+    if (own) cudaFreeAsync(own, stream);
+    return e;
 }
 
 }  // namespace fscan_detail

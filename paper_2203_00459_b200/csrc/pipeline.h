@@ -97,9 +97,14 @@ cudaError_t launch_mag_unpack(const Params& p, cudaStream_t s);      // stage AP
 cudaError_t launch_bf_items(const Params& p, cudaStream_t s);        // brute force: item argmax
 cudaError_t launch_bf_final(const Partial* items, const double* thetas, int n_thetas, int batch, int n,
                             double delta, fscan_bf_result* out, cudaStream_t s);  // brute force: winner
-cudaError_t launch_polar_to_cart(const float* d_polar, int batch, int n_az, int n_range,
-                                 double range_res, int n, double delta, float* d_out,
-                                 cudaStream_t stream);                  // K0
+// K0: one or two sweep batches (d_polar1 nullable) -> Cartesian grids through
+// a per-geometry tap table `tab` (polar_tap_bytes(n), built by
+// launch_polar_taps; nullptr: a temporary one is built for the call)
+size_t polar_tap_bytes(int n);
+cudaError_t launch_polar_taps(int n_az, double range_res, int n, double delta, void* tab, cudaStream_t stream);
+cudaError_t launch_polar_to_cart(const float* d_polar0, const float* d_polar1, int batch, int n_az,
+                                 int n_range, double range_res, int n, double delta, float* d_out0,
+                                 float* d_out1, cudaStream_t stream, const void* tab = nullptr);
 int rows_per_block_out(int n);  // K5 rows per CTA (partials per pair = n / this)
 
 }  // namespace fscan_detail

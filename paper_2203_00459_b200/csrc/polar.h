@@ -21,8 +21,15 @@
 
 namespace fscan_k0 {
 
-FS_HD double polar_cell(const float* polar, int n_az, int n_range, double res, int n,
-                        double delta, int r, int c) {
+// Geometry of one cell (independent of the sweep values): the two azimuth
+// rows, the first range bin and the bilinear weights.
+struct PolarTap {
+    int a0, a1;   // azimuth rows (a1 = a0 + 1 wrapped)
+    int k0, pad;  // first range bin (may be outside [0, n_range))
+    double wa, wk;
+};
+
+FS_HD PolarTap polar_tap(int n_az, double res, int n, double delta, int r, int c) {
     const double two_pi = 6.283185307179586;
     const int half = (n - 1) / 2;
     const double x = (c - half) * delta;
@@ -33,19 +40,34 @@ FS_HD double polar_cell(const float* polar, int n_az, int n_range, double res, i
     const double fa = phi * (n_az / two_pi);
     const double fk = rho / res - 0.5;
     const double a0f = floor(fa);
-    const double wa = fa - a0f;
     const long a0 = (long)a0f % n_az;
-    const long a1 = (a0 + 1) % n_az;
     const double k0f = floor(fk);
-    const long k0 = (long)k0f;
-    const double wk = fk - k0f;
-    const float* p0 = polar + (size_t)a0 * n_range;
-    const float* p1 = polar + (size_t)a1 * n_range;
-    const double v00 = (k0 < 0 || k0 >= n_range) ? 0.0 : (double)p0[k0];
-    const double v01 = (k0 + 1 < 0 || k0 + 1 >= n_range) ? 0.0 : (double)p0[k0 + 1];
-    const double v10 = (k0 < 0 || k0 >= n_range) ? 0.0 : (double)p1[k0];
-    const double v11 = (k0 + 1 < 0 || k0 + 1 >= n_range) ? 0.0 : (double)p1[k0 + 1];
+    PolarTap t;
+    t.a0 = (int)a0;
+    t.a1 = (int)((a0 + 1) % n_az);
+    t.k0 = (int)(long)k0f;
+    t.pad = 0;
+    t.wa = fa - a0f;
+    t.wk = fk - k0f;
+    return t;
+}
+
+FS_HD double polar_sample(const float* polar, int n_range, const PolarTap& t) {
+    const float* p0 = polar + (size_t)t.a0 * n_range;
+    const float* p1 = polar + (size_t)t.a1 * n_range;
+    const int k0 = t.k0;
+    const bool in0 = k0 >= 0 && k0 < n_range, in1 = k0 + 1 >= 0 && k0 + 1 < n_range;
+    const double v00 = in0 ? (double)p0[k0] : 0.0;
+    const double v01 = in1 ? (double)p0[k0 + 1] : 0.0;
+    const double v10 = in0 ? (double)p1[k0] : 0.0;
+    const double v11 = in1 ? (double)p1[k0 + 1] : 0.0;
+    const double wa = t.wa, wk = t.wk;
     return (1.0 - wa) * ((1.0 - wk) * v00 + wk * v01) + wa * ((1.0 - wk) * v10 + wk * v11);
+}
+
+FS_HD double polar_cell(const float* polar, int n_az, int n_range, double res, int n, double delta, int r,
+                        int c) {
+    return polar_sample(polar, n_range, polar_tap(n_az, res, n, delta, r, c));
 }
 
 }  // namespace fscan_k0

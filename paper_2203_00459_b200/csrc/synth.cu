@@ -25,9 +25,9 @@
 namespace fscan_detail {
 // Product K0 kernel launcher (kernels.cu); used to turn device-rendered polar
 // sweeps into Cartesian scans the same way the C3 hot path does.
-cudaError_t launch_polar_to_cart(const float* d_polar, int batch, int n_az, int n_range,
-                                 double range_res, int n, double delta, float* d_out,
-                                 cudaStream_t stream);
+cudaError_t launch_polar_to_cart(const float* d_polar0, const float* d_polar1, int batch, int n_az,
+                                 int n_range, double range_res, int n, double delta, float* d_out0,
+                                 float* d_out1, cudaStream_t stream, const void* tab);
 }  // namespace fscan_detail
 
 using fsynth::Object;
@@ -485,11 +485,8 @@ int fscan_synth_pairs_device(const fscan_synth_spec* s, int first, int count, fl
                 e = (cudaError_t)rc;
                 break;
             }
-            e = fscan_detail::launch_polar_to_cart(pa, cnt, s->n_az, s->n_range, s->range_res, s->n, s->delta,
-                                                   d_f + i * nn, st);
-            if (e == cudaSuccess)
-                e = fscan_detail::launch_polar_to_cart(pb, cnt, s->n_az, s->n_range, s->range_res, s->n,
-                                                       s->delta, d_g + i * nn, st);
+            e = fscan_detail::launch_polar_to_cart(pa, pb, cnt, s->n_az, s->n_range, s->range_res, s->n, s->delta,
+                                                   d_f + i * nn, d_g + i * nn, st, nullptr);
             if (e == cudaSuccess) e = cudaStreamSynchronize(st);
         }
         cudaFree(pa);
