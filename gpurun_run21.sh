@@ -1,1 +1,1 @@
-VARS="M O" bash gpurun_ab.sh
+VARS="M2 P" bash gpurun_ab.sh

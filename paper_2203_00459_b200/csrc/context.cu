@@ -202,9 +202,9 @@ bool build_taps(int n, const fscan_config& cfg, const std::vector<unsigned char>
         jhi = 0;
     }
     *n_live = jhi - jlo + 1;
-    taps.resize((size_t)nt * (*n_live));
+    taps.resize((size_t)nt * (*n_live));  // radius-major: [n_live][n_theta] (K2a lanes walk azimuth)
     for (int i = 0; i < nt; ++i)
-        for (int j = jlo; j <= jhi; ++j) taps[(size_t)i * (*n_live) + (j - jlo)] = all[(size_t)i * nr + j];
+        for (int j = jlo; j <= jhi; ++j) taps[(size_t)(j - jlo) * nt + i] = all[(size_t)i * nr + j];
     return true;
 }
 

@@ -153,58 +153,50 @@ __device__ __forceinline__ float tile_at(const float* m, int n, int r, int u) {
     return __ldg(m + ((size_t)(u >> 3) * n + r) * 8 + (u & 7));
 }
 
-// K2a: radial sums of the bilinear polar resample (cart2pol) of |F| and |G|,
-// one warp per azimuth row, kGatherCtas CTAs per pair; fp64 sums written to
-// p.prof[pair][2][n_theta].
-constexpr int kGatherCtas = 8;
+// K2a: radial sums of the bilinear polar resample (cart2pol) of |F| and |G|:
+// one thread per azimuth row, walking its radii. The lanes of a warp are 32
+// adjacent rays at the same radius, which sit within a few pixels of each
+// other, so a warp-wide tap load touches ~2-4 magnitude-tile lines instead of
+// the ~10 a ray's consecutive radii span. fp64 sums per row, written to
+// p.prof[pair][2][n_theta]; the tap table is radius-major ([n_live][n_theta]).
+constexpr int kGatherThreads = 128;
 
-__global__ void __launch_bounds__(kPolarThreads) k_rot_gather(Params p) {
+__global__ void __launch_bounds__(kGatherThreads) k_rot_gather(Params p) {
     const int pair = blockIdx.y;
-    const int nt = p.n_theta, n = p.n;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nwarps = kPolarThreads / 32;
+    const int nt = p.n_theta, n = p.n, n_live = p.n_live;
+    const int i = blockIdx.x * kGatherThreads + threadIdx.x;
+    if (i >= nt) return;
     const float* mf = p.mag + (size_t)pair * 2 * n * (n / 2);
     const float* mg = mf + (size_t)n * (n / 2);
-    double* prof = p.prof + (size_t)pair * 2 * nt;
-    for (int i = blockIdx.x * nwarps + warp; i < nt; i += gridDim.x * nwarps) {
-        double af = 0.0, ag = 0.0;
-        const PolarTap* row = p.taps + (size_t)i * p.n_live;
-        constexpr int U = 4;  // independent entries in flight per lane (memory-level parallelism)
-        for (int j0 = 0; j0 < p.n_live; j0 += 32 * U) {
-            PolarTap e[U];
+    const PolarTap* col = p.taps + i;
+    double af = 0.0, ag = 0.0;
+    constexpr int U = 4;  // independent entries in flight per thread (memory-level parallelism)
+    for (int j0 = 0; j0 < n_live; j0 += U) {
+        PolarTap e[U];
 #pragma unroll
-            for (int q = 0; q < U; ++q) {
-                const int jj = j0 + q * 32 + lane;
-                e[q] = jj < p.n_live ? row[jj] : PolarTap{0, 0.f, 0.f, 0.f};  // flags 0: contributes 0
-            }
-            float fv[U][4], gv[U][4];
+        for (int q = 0; q < U; ++q)
+            e[q] = j0 + q < n_live ? col[(size_t)(j0 + q) * nt] : PolarTap{0, 0.f, 0.f, 0.f};  // flags 0: 0
+        float fv[U][4], gv[U][4];
 #pragma unroll
-            for (int q = 0; q < U; ++q) {
-                const int r0 = e[q].packed & 0xFFF, u = (e[q].packed >> 12) & 0xFFF, fl = e[q].packed >> 24;
+        for (int q = 0; q < U; ++q) {
+            const int r0 = e[q].packed & 0xFFF, u = (e[q].packed >> 12) & 0xFFF, fl = e[q].packed >> 24;
 #pragma unroll
-                for (int tp = 0; tp < 4; ++tp) {
-                    const bool on = (fl >> tp) & 1;
-                    const int rr = r0 + (tp >> 1), uu = u + (tp & 1);
-                    fv[q][tp] = on ? tile_at(mf, n, rr, uu) : 0.f;
-                    gv[q][tp] = on ? tile_at(mg, n, rr, uu) : 0.f;
-                }
-            }
-#pragma unroll
-            for (int q = 0; q < U; ++q) {
-                af += (double)bilerp(e[q].fr, e[q].fc, fv[q][0], fv[q][1], fv[q][2], fv[q][3]);
-                ag += (double)bilerp(e[q].fr, e[q].fc, gv[q][0], gv[q][1], gv[q][2], gv[q][3]);
+            for (int tp = 0; tp < 4; ++tp) {
+                const bool on = (fl >> tp) & 1;
+                const int rr = r0 + (tp >> 1), uu = u + (tp & 1);
+                fv[q][tp] = on ? tile_at(mf, n, rr, uu) : 0.f;
+                gv[q][tp] = on ? tile_at(mg, n, rr, uu) : 0.f;
             }
         }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            af += __shfl_xor_sync(0xffffffffu, af, o);
-            ag += __shfl_xor_sync(0xffffffffu, ag, o);
-        }
-        if (lane == 0) {
-            prof[i] = af;
-            prof[nt + i] = ag;
+        for (int q = 0; q < U; ++q) {
+            af += (double)bilerp(e[q].fr, e[q].fc, fv[q][0], fv[q][1], fv[q][2], fv[q][3]);
+            ag += (double)bilerp(e[q].fr, e[q].fc, gv[q][0], gv[q][1], gv[q][2], gv[q][3]);
         }
     }
+    double* prof = p.prof + (size_t)pair * 2 * nt;
+    prof[i] = af;
+    prof[nt + i] = ag;
 }
 
 // K2b: angular correlation of the profiles, hard + soft argmax over theta.
@@ -426,7 +418,10 @@ struct XRowGeom {
     }
 };
 
-template <int N>
+// MANY: items of a multi-candidate launch (brute-force search) read the scans
+// of pair (item_base + item) / src_div; a separate instantiation keeps the
+// matcher's gather loop free of that indexing.
+template <int N, bool MANY>
 __global__ void __launch_bounds__(kXThreads) k_xlat_rows(Params p) {
     constexpr int K = N / 2, M = 3 * K, H = M / 2;
     using X = XRowGeom<N>;
@@ -439,7 +434,7 @@ __global__ void __launch_bounds__(kXThreads) k_xlat_rows(Params p) {
     const int pair = blockIdx.y;
     const int y0 = blockIdx.x * ROWS;
     const RotState rs = p.rot[pair];
-    const int src = (p.item_base + pair) / p.src_div;  // pair whose scans this item reads
+    const int src = MANY ? (p.item_base + pair) / p.src_div : pair;  // pair whose scans this item reads
     const float* ft = p.ft + (size_t)src * N * N;
     const float* gt = p.gt + (size_t)src * N * N;
     const float c0f32 = (N - 1) / 2.0f;  // exact
@@ -969,9 +964,13 @@ cudaError_t rot_cols(const Params& p, cudaStream_t s) {
 template <int N>
 cudaError_t xlat_rows(const Params& p, cudaStream_t s) {
     using X = XRowGeom<N>;
-    cudaError_t e = set_smem(k_xlat_rows<N>, X::SMEM);
+    const bool many = p.src_div != 1;
+    cudaError_t e = many ? set_smem(k_xlat_rows<N, true>, X::SMEM) : set_smem(k_xlat_rows<N, false>, X::SMEM);
     if (e != cudaSuccess) return e;
-    k_xlat_rows<N><<<dim3(N / X::ROWS, p.batch), kXThreads, X::SMEM, s>>>(p);
+    if (many)
+        k_xlat_rows<N, true><<<dim3(N / X::ROWS, p.batch), kXThreads, X::SMEM, s>>>(p);
+    else
+        k_xlat_rows<N, false><<<dim3(N / X::ROWS, p.batch), kXThreads, X::SMEM, s>>>(p);
     return cudaGetLastError();
 }
 
@@ -1015,7 +1014,7 @@ cudaError_t launch_xlat_out(const Params& p, cudaStream_t s) { FSCAN_DISPATCH_N(
 
 cudaError_t launch_rot_gather(const Params& p, cudaStream_t s) {
     if (p.n_theta == 1) return cudaSuccess;
-    k_rot_gather<<<dim3(kGatherCtas, p.batch), kPolarThreads, 0, s>>>(p);
+    k_rot_gather<<<dim3((p.n_theta + kGatherThreads - 1) / kGatherThreads, p.batch), kGatherThreads, 0, s>>>(p);
     return cudaGetLastError();
 }
 

@@ -59,7 +59,7 @@ struct Params {
     const float2* tw_m;   // exp(-2 pi i k / M), M = 3N/2
     const float* hann;    // N
     const int2* band;     // per centred row: [u_lo, u_hi] in band (empty: lo > hi)
-    const PolarTap* taps; // [n_theta][n_live]
+    const PolarTap* taps; // [n_live][n_theta] (radius-major)
     int n_live;
     int zcols;            // K1b computes columns u < zcols (multiple of 8); K1a stores only those and their mirrors
     // config

@@ -1,6 +1,6 @@
 """profiles/ncu_traffic.json from an ncu --set full capture of one C4 step:
 DRAM bytes (read + write) per launch and per pair for every pipeline kernel.
-Pairs per launch come from k_rot_gather's grid (8 CTAs per pair).
+Pairs per launch come from k_finalize's grid (one CTA per pair).
 usage: python tools/ncu_traffic.py REP SOURCE_NOTE > profiles/ncu_traffic.json"""
 import csv
 import io
@@ -30,7 +30,7 @@ for r in rows[2:]:
     k = k.split("<")[0].replace("k_", "", 1)
     recs.append((k, col(r, "dram__bytes_read.sum") + col(r, "dram__bytes_write.sum"),
                  col(r, "gpu__time_duration.sum"), col(r, "launch__grid_size")))
-ppl = next(int(g) // 8 for k, _, _, g in recs if k == "rot_gather")
+ppl = next(int(g) for k, _, _, g in recs if k == "finalize")
 res = {"source": note, "pairs_per_launch": ppl}
 for k, b, us, _ in recs:
     res[k] = {"dram_bytes_per_launch": b, "dram_bytes_per_pair": b / ppl, "duration_us": round(us, 3)}
