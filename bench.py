@@ -306,6 +306,29 @@ def run_ours(args):
                       "api": "fscan_brute_force_batch (unmasked scans, matcher theta grid)"}
         del mb
 
+    # odometry chaining: the same number of pairs registered as
+    # consecutive scans of one sequence, each scan's rotation spectrum shared by its
+    # two pairs; reported beside the independent-pair value
+    chain = None
+    if rank == 0 and not args.no_odometry and not polar:
+        seq = torch.cat([f, g[-1:]])  # per + 1 scans -> per pairs
+        seqm = torch.cat([mf, mg[-1:]])
+        mo = fb.Matcher(cfg, max_batch=per, device=local, chunk=args.chunk)
+        oout = torch.empty(per * fb.RESULT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+        mo.odometry(seq, seqm, delta=delta, out=oout, stream=stream)  # warm
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = max(1, min(args.steps, 5))
+        e0.record(stream)
+        for _ in range(reps):
+            mo.odometry(seq, seqm, delta=delta, out=oout, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        rate = per * reps / (e0.elapsed_time(e1) / 1e3)
+        chain = {"value": round(rate, 1), "unit": UNIT, "pairs": per, "steps": reps,
+                 "vs_independent_pairs": round(rate / (value / world), 3),
+                 "api": "fscan_odometry_batch (scan k vs scan k+1 of one sequence, masks per scan)"}
+        del mo, seq, seqm, oout
+
     # e2e through the public host API (H2D + compute + D2H each step)
     e2e = None
     if not args.no_e2e:
@@ -358,7 +381,7 @@ def run_ours(args):
                        "l2": "inputs 16 GiB per pass >> 126 MB L2; no flush needed",
                        "parallelism": f"dp{world} (pairs sharded by index, no collective on the hot path)"},
             "roofline": roofline, "hbm_pipeline": pipeline, "cpu_baseline": cpu, "e2e": e2e,
-            "exhaustive_search": exhaustive,
+            "exhaustive_search": exhaustive, "odometry_chain": chain,
             "clocks": clk.summary(), "gpu_launches": launches_per_step * args.steps,
             "bad_pairs": bad, "impl": "ours",
         }
@@ -418,6 +441,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-exhaustive", action="store_true", help="skip the brute-force comparison leg")
+    ap.add_argument("--no-odometry", action="store_true", help="skip the chained-sequence leg")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

@@ -143,6 +143,18 @@ fscan_status fscan_polar_to_cart_batch(const float* d_polar, int batch, int n_az
                                        double range_res, int n, double delta, float* d_out,
                                        void* stream);
 
+/* Odometry over a scan sequence (the pairwise loop of proj/tools/main.cpp:124-131):
+ * d_scans holds n_scans consecutive N x N grids (device), d_masks the per-scan
+ * masks or NULL; pair k = scan_match(scan k, scan k+1) for k < n_scans - 1, with
+ * the reference's per-pair semantics (d_out[k], optional surfaces per pair).
+ * Each scan's rotation-stage spectrum and masked copy are computed once and
+ * shared by its two pairs (half the K1 work of independent pairs). The host
+ * side composes the trajectory (fscan/odometry.hpp: integrate of the inverse
+ * poses). Asynchronous on `stream`; n_scans - 1 <= max_batch. */
+fscan_status fscan_odometry_batch(fscan_ctx* ctx, const float* d_scans, const float* d_masks, int n_scans,
+                                  double delta, fscan_pair_result* d_out, double* d_theta_surface,
+                                  float* d_xy_surface, void* stream);
+
 /* Brute-force correlative search (the reference's oracle, proj/src/oracle.cpp:21-67,
  * proj/include/fscan/oracle.hpp:10-23): for every candidate theta (in list
  * order) g is de-rotated by -theta and the zero-padded translation correlation

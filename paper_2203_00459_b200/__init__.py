@@ -124,6 +124,7 @@ SYMBOLS = {
     "fscan_estimate_translation_batch": (C.c_int, [_P, _P, _P, C.c_int, C.c_double, _P, _P, _P, _P]),
     "fscan_band_magnitude_batch": (C.c_int, [_P, _P, C.c_int, _P, _P]),
     "fscan_brute_force_batch": (C.c_int, [_P, _P, _P, C.c_int, _P, C.c_int, C.c_double, _P, _P]),
+    "fscan_odometry_batch": (C.c_int, [_P, _P, _P, C.c_int, C.c_double, _P, _P, _P, _P]),
     "fscan_polar_to_cart_batch": (C.c_int, [_P, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int,
                                             C.c_double, _P, _P]),
     "fscan_check_results": (C.c_int, [_P, C.c_int, _P, C.POINTER(C.c_int)]),
@@ -365,6 +366,19 @@ class Matcher:
         self._check(st, "fscan_estimate_translation_batch")
         return txy
 
+    def odometry(self, scans, masks=None, *, delta: float, out=None, theta_surface=None, xy_surface=None,
+                 stream=None):
+        """Pairs (scan k, scan k+1) of a CUDA sequence [S, N, N] (masks per scan or None):
+        S-1 result records, each scan's rotation spectrum computed once."""
+        import torch
+        s = int(scans.shape[0])
+        if out is None:
+            out = torch.empty(max(s - 1, 0) * RESULT_DTYPE.itemsize, dtype=torch.uint8, device=scans.device)
+        st = lib().fscan_odometry_batch(self._h, _ptr(scans), _ptr(masks), s, float(delta), _ptr(out),
+                                        _ptr(theta_surface), _ptr(xy_surface), _stream_ptr(stream))
+        self._check(st, "fscan_odometry_batch")
+        return out
+
     def brute_force(self, f, g, thetas, *, delta: float, out=None, stream=None):
         """Exhaustive search over the theta candidates (oracle.cpp:40-67) for a batch
         of CUDA pairs [B, N, N]; returns a uint8 device buffer of BF_DTYPE records
@@ -458,6 +472,49 @@ def scan_match(f, g, delta: float, config: MatchConfig | None = None, mask_f=Non
         if cfg.n_theta > 1 else np.zeros(1)
     return MatchResult(Pose2D(float(r["theta"]), float(r["tx"]), float(r["ty"])), ts[0][:, None], coords,
                        xs[0].astype(np.float64), r)
+
+
+def compose(a: Pose2D, b: Pose2D) -> Pose2D:
+    """geometry.cpp compose: a then b (b expressed in a's frame)."""
+    c, s = math.cos(a.theta), math.sin(a.theta)
+    return Pose2D(_normalize_angle(a.theta + b.theta), a.tx + c * b.tx - s * b.ty, a.ty + s * b.tx + c * b.ty)
+
+
+def inverse(p: Pose2D) -> Pose2D:
+    c, s = math.cos(p.theta), math.sin(p.theta)
+    return Pose2D(_normalize_angle(-p.theta), -(c * p.tx + s * p.ty), -(-s * p.tx + c * p.ty))
+
+
+def _normalize_angle(t: float) -> float:
+    t = math.fmod(t, 2 * math.pi)
+    if t <= -math.pi:
+        t += 2 * math.pi
+    if t > math.pi:
+        t -= 2 * math.pi
+    return t
+
+
+def odometry(scans, delta: float, config: MatchConfig | None = None, masks=None):
+    """The odometry command's matching loop (tools/main.cpp:124-135) on the GPU:
+    scans [S, N, N] (numpy) -> (absolute poses [S] starting at the identity,
+    per-pair result records). rel[k] = inverse(scan_match(scan k, scan k+1).pose)."""
+    import torch
+    scans = np.ascontiguousarray(scans, dtype=np.float32)
+    n_s, n = int(scans.shape[0]), int(scans.shape[1])
+    cfg = MatchConfig(**(config or MatchConfig(n_xy=n, delta_xy=delta, n_radius=0)).__dict__).finalize()
+    cfg.validate()
+    m = Matcher(cfg, max_batch=max(1, n_s - 1))
+    dev = torch.device("cuda", m.device)
+    s_d = torch.from_numpy(scans).to(dev)
+    m_d = None if masks is None else torch.from_numpy(np.ascontiguousarray(masks, dtype=np.float32)).to(dev)
+    res = decode_results(m.odometry(s_d, m_d, delta=delta))
+    bad = np.nonzero(res["status"] != OK)[0]
+    if bad.size:
+        _raise(int(res["status"][bad[0]]), f"odometry: pair {int(bad[0])} rejected")
+    poses = [Pose2D()]
+    for r in res:
+        poses.append(compose(poses[-1], inverse(Pose2D(float(r["theta"]), float(r["tx"]), float(r["ty"])))))
+    return poses, res
 
 
 @dataclass

@@ -39,6 +39,7 @@ struct Lane {
     float* in = nullptr;  // 4 grids x chunk
     float* cart = nullptr;  // K0 output (polar API): 2 grids x chunk
     void* k0tab = nullptr;  // K0 tap table of the last polar geometry (built on this lane's stream)
+    float* chain_ms = nullptr;  // odometry: masked scans of a chunk (chunk + 2 grids)
     int k0_naz = 0;
     double k0_res = 0.0, k0_delta = 0.0;
     fscan_pair_result* res = nullptr;
@@ -221,6 +222,7 @@ void free_lane(Lane& l) {
     cudaFree(l.in);
     cudaFree(l.cart);
     cudaFree(l.k0tab);
+    cudaFree(l.chain_ms);
     cudaFree(l.res);
     cudaFree(l.tsurf);
     cudaFree(l.xsurf);
@@ -238,7 +240,7 @@ fscan_status alloc_lane(fscan_ctx* ctx, Lane& l, int chunk) {
     CK(cudaMalloc(&l.part, sizeof(Partial) * nparts * chunk));
     CK(cudaMalloc(&l.rot, sizeof(RotState) * chunk));
     CK(cudaMalloc(&l.prof, sizeof(double) * 2 * std::max(1, ctx->cfg.n_theta) * chunk));
-    CK(cudaMalloc(&l.flags, sizeof(int) * chunk));
+    CK(cudaMalloc(&l.flags, sizeof(int) * (chunk + 2)));  // chain mode: one per scan
     return FSCAN_OK;
 }
 
@@ -747,6 +749,53 @@ fscan_status fscan_brute_force_batch(fscan_ctx* ctx, const float* d_f, const flo
     CK(launch_bf_final(ctx->bf_items, ctx->bf_thetas, nth, batch, ctx->n, delta, d_out, user));
     ++ctx->launches_last;
     return FSCAN_OK;
+}
+
+fscan_status fscan_odometry_batch(fscan_ctx* ctx, const float* d_scans, const float* d_masks, int n_scans,
+                                  double delta, fscan_pair_result* d_out, double* d_tsurf, float* d_xsurf,
+                                  void* stream) {
+    const int pairs = n_scans - 1;
+    fscan_status st = check_ctx(ctx, std::max(0, pairs));
+    if (st != FSCAN_OK) return st;
+    std::lock_guard<std::mutex> g(ctx->mu);
+    if (!ctx->tw_n) return fail(ctx, FSCAN_ERR_INVALID_ARGUMENT, "context was not created successfully");
+    if (n_scans < 0 || !(delta > 0.0)) return fail(ctx, FSCAN_ERR_INVALID_ARGUMENT, "fscan_odometry_batch: bad count or delta");
+    if (pairs <= 0) return FSCAN_OK;  // 0 or 1 scans: no pairs
+    if (!d_scans || !d_out) return fail(ctx, FSCAN_ERR_INVALID_ARGUMENT, "fscan_odometry_batch: bad pointers");
+    const size_t nn = (size_t)ctx->n * ctx->n;
+    const int nt = ctx->cfg.n_theta;
+    for (Lane& l : LaneRange{ctx})
+        if (!l.chain_ms) CK(cudaMalloc(&l.chain_ms, (ctx->alloc_chunk + 2) * nn * sizeof(float)));
+    return drive(ctx, pairs, (cudaStream_t)stream, [&](Lane& l, int off, int cnt) {
+        // pairs off .. off+cnt-1 register scans off .. off+cnt
+        Params p = base_params(ctx, l, cnt, delta);
+        p.f = d_scans + off * nn;
+        p.mf = d_masks ? d_masks + off * nn : nullptr;
+        p.chain = 1;
+        p.n_scans = cnt + 1;
+        p.ft = l.chain_ms;       // masked scan s of the chunk at ft + s*nn
+        p.gt = l.chain_ms + nn;  // pair k reads scans k (ft) and k+1 (gt)
+        p.out = d_out + off;
+        p.theta_surf = d_tsurf ? d_tsurf + (size_t)off * nt : nullptr;
+        p.xy_surf = d_xsurf ? d_xsurf + off * nn : nullptr;
+        Params r = p;  // rotation-stage spectra: one packed transform per two scans
+        r.batch = (cnt + 2) / 2;
+        cudaStream_t s = l.stream;
+        CK(cudaMemsetAsync(l.flags, 0, sizeof(int) * (cnt + 1), s));
+        fscan_status e;
+#define FSCAN_LAUNCH(kid, call, P)                                                           \
+    if ((e = launch(ctx, l, kid, [&] { return call(P, s); }, &ctx->launches_last)) != FSCAN_OK) return e;
+        FSCAN_LAUNCH(kRotRows, launch_rot_rows, r);
+        if (nt > 1) FSCAN_LAUNCH(kRotCols, launch_rot_cols, r);
+        if (nt > 1) FSCAN_LAUNCH(kRotGather, launch_rot_gather, p);
+        FSCAN_LAUNCH(kRotPolar, launch_rot_polar, p);
+        FSCAN_LAUNCH(kXlatRows, launch_xlat_rows, p);
+        FSCAN_LAUNCH(kXlatCols, launch_xlat_cols, p);
+        FSCAN_LAUNCH(kXlatOut, launch_xlat_out, p);
+        FSCAN_LAUNCH(kFinalize, launch_finalize, p);
+#undef FSCAN_LAUNCH
+        return FSCAN_OK;
+    });
 }
 
 fscan_status fscan_band_magnitude_batch(fscan_ctx* ctx, const float* d_img, int batch, float* d_out,

@@ -6,6 +6,7 @@
 //   soft_argmax                      matcher.cpp:57-93 (host utility on a given surface)
 //   geometry helpers                 proj/src/geometry.cpp:9-70
 //   brute_force_match / timing_comparison   proj/src/oracle.cpp:40-101
+//   trajectory helpers + odometry    proj/src/odometry.cpp:8-102, tools/main.cpp:124-135
 // Single-pair calls convert the fp64 grids to fp32, run the batch pipeline on
 // device 0 with a cached per-config context, and return surfaces as doubles.
 #include <cuda_runtime.h>
@@ -13,6 +14,8 @@
 #include <algorithm>
 #include <charconv>
 #include <chrono>
+#include <cmath>
+#include <optional>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -23,6 +26,7 @@
 #include <vector>
 
 #include "fscan/matcher.hpp"
+#include "fscan/odometry.hpp"
 #include "fscan/oracle.hpp"
 #include "fscan_cuda.h"
 
@@ -366,6 +370,120 @@ void scan_match_batch(const float* d_f, const float* d_g, const float* d_mf, con
             d.xy_col = h[i].xy_col;
         }
     }
+}
+
+// ---- trajectories (odometry.cpp:8-102) ----
+
+Trajectory integrate(const std::vector<Pose2D>& relatives) {
+    Trajectory t;
+    t.poses.reserve(relatives.size() + 1);
+    t.cumulative_distance.reserve(relatives.size() + 1);
+    Pose2D cur = Pose2D::identity();
+    double dist = 0.0;
+    t.poses.push_back(cur);
+    t.cumulative_distance.push_back(dist);
+    for (const Pose2D& r : relatives) {
+        cur = compose(cur, r);
+        dist += r.translation().norm();
+        t.poses.push_back(cur);
+        t.cumulative_distance.push_back(dist);
+    }
+    return t;
+}
+
+std::vector<Pose2D> difference(const Trajectory& t) {
+    std::vector<Pose2D> out;
+    for (std::size_t k = 1; k < t.poses.size(); ++k) out.push_back(compose(inverse(t.poses[k - 1]), t.poses[k]));
+    return out;
+}
+
+Trajectory from_poses(std::vector<Pose2D> poses) {
+    Trajectory t;
+    t.poses = std::move(poses);
+    double dist = 0.0;
+    for (std::size_t k = 0; k < t.poses.size(); ++k) {
+        if (k) dist += (t.poses[k].translation() - t.poses[k - 1].translation()).norm();
+        t.cumulative_distance.push_back(dist);
+    }
+    return t;
+}
+
+std::optional<DriftReport> kitti_drift(const Trajectory& est, const Trajectory& truth,
+                                       const std::vector<double>& lengths, int stride, DriftAveraging avg) {
+    const std::size_t frames = truth.poses.size();
+    if (est.poses.size() != frames) throw std::invalid_argument("kitti_drift: trajectory lengths differ");
+    if (frames < 2) throw std::invalid_argument("kitti_drift: need >= 2 frames");
+    if (stride < 1) throw std::invalid_argument("kitti_drift: stride must be >= 1");
+    if (truth.cumulative_distance.size() != frames)
+        throw std::invalid_argument("kitti_drift: truth lacks cumulative distance");
+    const std::vector<double>& d = truth.cumulative_distance;
+    double all_t = 0.0, all_r = 0.0, mean_t = 0.0, mean_r = 0.0;
+    int all_n = 0, used_lengths = 0;
+    for (const double len : lengths) {
+        if (!(len > 0.0)) throw std::invalid_argument("kitti_drift: segment lengths must be positive");
+        double st = 0.0, sr = 0.0;
+        int cnt = 0;
+        std::size_t end = 0;
+        for (std::size_t first = 0; first < frames; first += stride) {
+            end = std::max(end, first);  // distance is non-decreasing: the end only moves forward
+            while (end < frames && d[end] - d[first] < len) ++end;
+            if (end == frames) break;
+            const Pose2D e = compose(inverse(compose(inverse(truth.poses[first]), truth.poses[end])),
+                                     compose(inverse(est.poses[first]), est.poses[end]));
+            const double seg = d[end] - d[first];
+            st += e.translation().norm() / seg * 100.0;
+            sr += std::abs(e.theta) * (180.0 / kPi) / (seg / 1000.0);
+            ++cnt;
+        }
+        if (cnt) {
+            all_t += st;
+            all_r += sr;
+            all_n += cnt;
+            mean_t += st / cnt;
+            mean_r += sr / cnt;
+            ++used_lengths;
+        }
+    }
+    if (!all_n) return std::nullopt;
+    DriftReport r;
+    r.segments = all_n;
+    r.translation_percent = avg == DriftAveraging::pooled ? all_t / all_n : mean_t / used_lengths;
+    r.rotation_deg_per_km = avg == DriftAveraging::pooled ? all_r / all_n : mean_r / used_lengths;
+    return r;
+}
+
+std::vector<double> default_segment_lengths() { return {100, 200, 300, 400, 500, 600, 700, 800}; }
+
+Trajectory odometry(const std::vector<ScanGrid>& scans, const MatchConfig& cfg, const std::vector<MaskGrid>* masks) {
+    validate(cfg);
+    if (scans.size() < 2) throw std::invalid_argument("odometry: need at least 2 scans");
+    const GridSpec spec = scans[0].spec;
+    for (const ScanGrid& s : scans)
+        if (!(s.spec == spec)) throw std::invalid_argument("scan_match: grid specs differ");
+    if (masks && masks->size() != scans.size()) throw std::invalid_argument("odometry: one mask per scan");
+    if (spec.n != cfg.n_xy) throw std::invalid_argument("estimate_rotation: grid size != config n_xy");
+    const int ns = (int)scans.size(), pairs = ns - 1;
+    const std::size_t nn = (std::size_t)spec.n * spec.n;
+    fscan_ctx* ctx = context_for(cfg, 0, pairs);
+    DevBuf<float> ds(ns * nn), dm(masks ? ns * nn : 1);
+    DevBuf<fscan_pair_result> res(pairs);
+    for (int k = 0; k < ns; ++k) {
+        upload(scans[k].values, ds.p + k * nn);
+        if (masks) upload((*masks)[k].values, dm.p + k * nn);
+    }
+    check(fscan_odometry_batch(ctx, ds.p, masks ? dm.p : nullptr, ns, spec.delta, res.p, nullptr, nullptr, nullptr),
+          ctx, "odometry");
+    std::vector<fscan_pair_result> h(pairs);
+    ck(cudaMemcpy(h.data(), res.p, sizeof(fscan_pair_result) * pairs, cudaMemcpyDeviceToHost), "D2H");
+    std::vector<Pose2D> rels(pairs);
+    for (int k = 0; k < pairs; ++k) {
+        if (h[k].status != FSCAN_OK)
+            raise((fscan_status)h[k].status, h[k].status == FSCAN_ERR_MASK_RANGE
+                                                 ? "MaskGrid: values must lie in [0, 1]"
+                                                 : "scan_match: input grids contain non-finite values");
+        rels[k] = inverse(Pose2D{h[k].theta, h[k].tx, h[k].ty});  // main.cpp:131
+    }
+    return integrate(rels);
 }
 
 // ---- exhaustive search (oracle.cpp:40-101) ----

@@ -66,23 +66,51 @@ __global__ void __launch_bounds__(kRowThreads) k_rot_rows(Params p) {
     const int y = blockIdx.x * G::PER_CTA + tr;
     const auto lay = G::lay(smem, tr);
     const size_t base = ((size_t)pair * N + y) * N;
+    // the two real grids packed into this transform: scans `pair` of f and g, or
+    // in chain mode (odometry) scans 2*pair and 2*pair+1 of one sequence (the
+    // last one duplicated for an odd count), masked copies written per scan
+    const float *fp, *gp, *mfp = nullptr, *mgp = nullptr;
+    float *ftp, *gtp;
+    const size_t row = (size_t)y * N;
+    if (p.chain) {
+        const size_t fi = 2 * (size_t)pair, gi = (size_t)min(2 * pair + 1, p.n_scans - 1);
+        fp = p.f + fi * N * N + row;
+        gp = p.f + gi * N * N + row;
+        if (p.mf) {
+            mfp = p.mf + fi * N * N + row;
+            mgp = p.mf + gi * N * N + row;
+        }
+        ftp = p.ft + fi * N * N + row;
+        gtp = p.ft + gi * N * N + row;
+    } else {
+        fp = p.f + base;
+        gp = p.g + base;
+        if (p.mf) {
+            mfp = p.mf + base;
+            mgp = p.mg + base;
+        }
+        ftp = p.ft + base;
+        gtp = p.gt + base;
+    }
     const float hy = p.hann[y];
-    int bad = 0;
+    int badf = 0, badg = 0;  // bit0 non-finite, bit1 mask outside [0, 1]
     float2 v[16];
 #pragma unroll
     for (int m = 0; m < 16; ++m) {
         const int x = t + m * T;
-        float fv = __ldg(p.f + base + x);
-        float gv = __ldg(p.g + base + x);
-        if (p.mf) {
-            const float a = __ldg(p.mf + base + x), b = __ldg(p.mg + base + x);
-            if (!(a >= 0.0f && a <= 1.0f) || !(b >= 0.0f && b <= 1.0f)) bad |= 2;
+        float fv = __ldg(fp + x);
+        float gv = __ldg(gp + x);
+        if (mfp) {
+            const float a = __ldg(mfp + x), b = __ldg(mgp + x);
+            if (!(a >= 0.0f && a <= 1.0f)) badf |= 2;
+            if (!(b >= 0.0f && b <= 1.0f)) badg |= 2;
             fv *= a;
             gv *= b;
         }
-        if (!isfinite(fv) || !isfinite(gv)) bad |= 1;
-        p.ft[base + x] = fv;
-        p.gt[base + x] = gv;
+        if (!isfinite(fv)) badf |= 1;
+        if (!isfinite(gv)) badg |= 1;
+        ftp[x] = fv;
+        gtp[x] = gv;
         const float w = hy * __ldg(p.hann + x);
         v[m] = make_float2(fv * w, gv * w);
     }
@@ -92,7 +120,12 @@ __global__ void __launch_bounds__(kRowThreads) k_rot_rows(Params p) {
         const int x = t + m * T;
         if (x < p.zcols || x > N - p.zcols) p.zbuf[base + x] = v[m];  // columns K1b reads
     }
-    if (bad) atomicOr(p.flags + pair, bad);
+    if (p.chain) {  // flags per scan of the sequence
+        if (badf) atomicOr(p.flags + 2 * pair, badf);
+        if (badg) atomicOr(p.flags + min(2 * pair + 1, p.n_scans - 1), badg);
+    } else if (badf | badg) {
+        atomicOr(p.flags + pair, badf | badg);
+    }
 }
 
 // ---------------------------------------------------------------- K1b
@@ -166,7 +199,9 @@ __global__ void __launch_bounds__(kGatherThreads) k_rot_gather(Params p) {
     const int nt = p.n_theta, n = p.n, n_live = p.n_live;
     const int i = blockIdx.x * kGatherThreads + threadIdx.x;
     if (i >= nt) return;
-    const float* mf = p.mag + (size_t)pair * 2 * n * (n / 2);
+    // |F| of the pair's first scan and |G| of its second: planes 2*pair, 2*pair+1,
+    // or in chain mode (one plane per scan of the sequence) planes pair, pair+1
+    const float* mf = p.mag + (size_t)pair * (p.chain ? 1 : 2) * n * (n / 2);
     const float* mg = mf + (size_t)n * (n / 2);
     const PolarTap* col = p.taps + i;
     double af = 0.0, ag = 0.0;
@@ -845,7 +880,7 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(Params p, int nparts) 
             o.theta_bin = rs.bin;
             o.xy_row = pr;
             o.xy_col = pc;
-            const int fl = p.flags[pair];
+            const int fl = p.chain ? (p.flags[pair] | p.flags[pair + 1]) : p.flags[pair];
             o.status = (fl & 2) ? FSCAN_ERR_MASK_RANGE : ((fl & 1) ? FSCAN_ERR_NONFINITE : FSCAN_OK);
             p.out[pair] = o;
         }

@@ -51,7 +51,7 @@ struct Params {
     Partial* part; // K5 per-block argmax [batch][N / rows_per_block]
     RotState* rot; // [batch]
     double* prof;  // K2a radial-sum profiles [batch][2][n_theta]
-    int* flags;    // [batch] bit0 non-finite, bit1 mask out of [0,1]
+    int* flags;    // [batch] (chain mode: [n_scans]) bit0 non-finite, bit1 mask out of [0,1]
     // tables
     const float2* tw_n;   // exp(-2 pi i k / N), k < N
     const float2* tw_k;   // exp(-2 pi i k / K), K = N/2
@@ -80,6 +80,11 @@ struct Params {
     // theta_in[(item_base + i) % theta_mod]
     int item_base, src_div, theta_mod;
     int skip_surface;         // K5 keeps only the block argmaxes (brute-force search)
+    // chain mode (odometry): pair k registers scan k against scan k+1 of one
+    // sequence f (masks mf); K1a/K1b run once per two scans (n_scans of them in
+    // this launch), the masked scans go to ft[scan], the magnitude planes and
+    // the flags are one per scan
+    int chain, n_scans;
     Partial* bf_items;        // brute force: per global item hard argmax (nullable)
 };
 

@@ -7,10 +7,12 @@
 #include <cmath>
 #include <cstdio>
 #include <limits>
+#include <optional>
 #include <stdexcept>
 #include <vector>
 
 #include "fscan/matcher.hpp"
+#include "fscan/odometry.hpp"
 #include "fscan/oracle.hpp"
 
 using namespace fscan;
@@ -351,6 +353,107 @@ int main() {
         CHECK(tc.ratio > 1.0);
         std::printf("timing_comparison n=64 n_theta=129: matcher %.3f ms, exhaustive %.3f ms, ratio %.1f\n",
                     tc.matcher_median_ms, tc.oracle_median_ms, tc.ratio);
+    }
+    // ---- trajectories (proj/tests/test_odometry.cpp) ----
+    {
+        auto lcg = [st = 12345ull]() mutable {
+            st = st * 6364136223846793005ull + 1442695040888963407ull;
+            return (double)(st >> 11) * 0x1.0p-53;
+        };
+        // identity relatives stand still; constant forward motion is a line (test_odometry.cpp:25-47)
+        const Trajectory still = integrate(std::vector<Pose2D>(5, Pose2D::identity()));
+        CHECK(still.poses.size() == 6 && still.poses.back().tx == 0.0 && still.cumulative_distance.back() == 0.0);
+        const Trajectory line = integrate(std::vector<Pose2D>(10, Pose2D{0.0, 1.0, 0.0}));
+        for (std::size_t k = 0; k < line.poses.size(); ++k)
+            CHECK(std::abs(line.poses[k].tx - (double)k) < 1e-12 && std::abs(line.cumulative_distance[k] - (double)k) < 1e-12);
+        // difference inverts integrate (49-65)
+        std::vector<Pose2D> rels;
+        for (int i = 0; i < 40; ++i) rels.push_back({-0.3 + 0.6 * lcg(), 0.2 + 1.8 * lcg(), -0.5 + lcg()});
+        const Trajectory tr = integrate(rels);
+        const std::vector<Pose2D> back = difference(tr);
+        CHECK(back.size() == rels.size());
+        for (std::size_t k = 0; k < rels.size(); ++k)
+            CHECK(std::abs(normalize_angle(back[k].theta - rels[k].theta)) < 1e-10 &&
+                  std::abs(back[k].tx - rels[k].tx) < 1e-9 && std::abs(back[k].ty - rels[k].ty) < 1e-9);
+        // from_poses recomputes chord distance (67-76)
+        const Trajectory ch = from_poses({Pose2D{0, 0, 0}, Pose2D{0.5, 3.0, 4.0}, Pose2D{-0.25, 3.0, 9.0}});
+        CHECK(ch.cumulative_distance[1] == 5.0 && ch.cumulative_distance[2] == 10.0);
+        // perfect estimate scores zero; constant bias closed form (78-107)
+        const Trajectory t300 = integrate(std::vector<Pose2D>(300, Pose2D{0.0, 1.0, 0.0}));
+        const auto z = kitti_drift(t300, t300, {100.0, 200.0});
+        CHECK(z.has_value() && z->translation_percent == 0.0 && z->rotation_deg_per_km == 0.0 && z->segments > 0);
+        const Trajectory truth = integrate(std::vector<Pose2D>(500, Pose2D{0.0, 1.0, 0.0}));
+        const Trajectory est = integrate(std::vector<Pose2D>(500, Pose2D{0.0, 1.03, 0.0}));
+        for (const auto avg : {DriftAveraging::pooled, DriftAveraging::per_length}) {
+            const auto r = kitti_drift(est, truth, default_segment_lengths(), 1, avg);
+            CHECK(r.has_value() && std::abs(r->translation_percent - 3.0) < 1e-8 && std::abs(r->rotation_deg_per_km) < 1e-9);
+        }
+        // invariant to a global rigid transform (109-139)
+        std::vector<Pose2D> noisy = rels;
+        for (Pose2D& q : noisy) {
+            q.theta += 0.002 * (lcg() - 0.5);
+            q.tx += 0.02 * (lcg() - 0.5);
+        }
+        const Trajectory et = integrate(noisy);
+        const auto b0 = kitti_drift(et, tr, {5.0, 10.0});
+        const Pose2D world{0.7, 100.0, -40.0};
+        auto moved = [&](const Trajectory& t) {
+            std::vector<Pose2D> ps;
+            for (const Pose2D& q : t.poses) ps.push_back(compose(world, q));
+            Trajectory o = from_poses(ps);
+            o.cumulative_distance = t.cumulative_distance;
+            return o;
+        };
+        const auto b1 = kitti_drift(moved(et), moved(tr), {5.0, 10.0});
+        CHECK(b0 && b1 && std::abs(b0->translation_percent - b1->translation_percent) < 1e-9 * (1 + b0->translation_percent) &&
+              b0->segments == b1->segments);
+        // stride subsamples; too short is empty; validation (158-186)
+        const Trajectory t200 = integrate(std::vector<Pose2D>(200, Pose2D{0.0, 1.0, 0.0}));
+        const auto dense = kitti_drift(t200, t200, {50.0}, 1), sparse = kitti_drift(t200, t200, {50.0}, 10);
+        CHECK(dense && sparse && dense->segments > sparse->segments && sparse->segments >= dense->segments / 10);
+        const Trajectory t5 = integrate(std::vector<Pose2D>(5, Pose2D{0.0, 1.0, 0.0}));
+        CHECK(!kitti_drift(t5, t5, {100.0}).has_value());
+        const Trajectory a10 = integrate(std::vector<Pose2D>(10, Pose2D{0.0, 1.0, 0.0}));
+        const Trajectory a11 = integrate(std::vector<Pose2D>(11, Pose2D{0.0, 1.0, 0.0}));
+        CHECK_THROWS_AS(kitti_drift(a10, a11, {5.0}), std::invalid_argument);
+        CHECK_THROWS_AS(kitti_drift(a10, a10, {5.0}, 0), std::invalid_argument);
+        CHECK_THROWS_AS(kitti_drift(a10, a10, {-5.0}), std::invalid_argument);
+        const Trajectory one = integrate({});
+        CHECK_THROWS_AS(kitti_drift(one, one, {5.0}), std::invalid_argument);
+        // pooled and per-length averaging differ on unevenly populated lengths (188-206)
+        std::vector<Pose2D> r100(100, Pose2D{0.0, 1.0, 0.0}), e100 = r100;
+        for (int i = 80; i < 100; ++i) e100[i].ty = 0.3;
+        const auto po = kitti_drift(integrate(e100), integrate(r100), {10.0, 50.0}, 1, DriftAveraging::pooled);
+        const auto pl = kitti_drift(integrate(e100), integrate(r100), {10.0, 50.0}, 1, DriftAveraging::per_length);
+        CHECK(po && pl && std::abs(po->translation_percent - pl->translation_percent) > 1e-6);
+    }
+    // odometry over a rendered drive (the matching loop of main.cpp:124-135)
+    {
+        const int N = 128;
+        const GridSpec sp{N, 0.4};
+        const MatchConfig c = small_cfg(N, 0.4, 129);
+        const auto bs = scene(N, 0.4, 4242, 40);
+        std::vector<Pose2D> truth{Pose2D::identity()};
+        const Pose2D step{0.03, 0.8, 0.2};
+        for (int k = 0; k < 6; ++k) truth.push_back(compose(truth.back(), step));
+        // scan k is the scene seen from pose k: objects at inverse(pose_k) applied to world points
+        std::vector<ScanGrid> scans;
+        for (const Pose2D& pk : truth) scans.push_back(render(bs, sp, inverse(pk)));
+        const Trajectory t = odometry(scans, c);
+        CHECK(t.poses.size() == truth.size());
+        for (std::size_t k = 0; k < truth.size(); ++k) {
+            const Pose2D e = compose(inverse(truth[k]), t.poses[k]);
+            CHECK(std::abs(e.theta) <= 2.0 * (double)k * c.delta_theta + 1e-12);
+            CHECK(std::abs(e.tx) <= 0.5 * k * sp.delta + 1e-12 && std::abs(e.ty) <= 0.5 * k * sp.delta + 1e-12);
+        }
+        // the chained batch gives the pairwise scan_match results
+        for (int k = 0; k + 1 < (int)scans.size(); ++k) {
+            const Pose2D m = inverse(scan_match(scans[k], scans[k + 1], c).pose);
+            const Pose2D r = difference(t)[k];
+            CHECK(std::abs(normalize_angle(m.theta - r.theta)) < 1e-6 && std::abs(m.tx - r.tx) < 1e-4 &&
+                  std::abs(m.ty - r.ty) < 1e-4);
+        }
+        CHECK_THROWS_AS(odometry(std::vector<ScanGrid>(1, scans[0]), c), std::invalid_argument);
     }
     std::printf("%d checks, %d failed\n", g_checks, g_fail);
     if (g_fail == 0) std::printf("ALL PASSED\n");

@@ -417,3 +417,69 @@ def test_brute_force_agrees_with_decoupled_matcher(fb, dev):  # test_oracle.cpp:
     for i in range(3):
         assert abs(bf[i]["theta"] - res[i]["theta"]) <= 2 * cfg.delta_theta
         assert abs(bf[i]["tx"] - res[i]["tx"]) <= delta and abs(bf[i]["ty"] - res[i]["ty"]) <= delta
+
+
+# ---- odometry chaining (tools/main.cpp:124-135) ----
+
+def _sequence(fb, cid, count, first=30):
+    """count scans with masks: f0, g0, f1, g1, ... of the config's generator."""
+    spec = fb.synth_spec(cid)
+    f, g, mf, mg, _ = fb.synth_pairs_host(spec, first, (count + 1) // 2)
+    scans = np.stack([x for pair in zip(f, g) for x in pair])[:count]
+    masks = np.stack([x for pair in zip(mf, mg) for x in pair])[:count]
+    return scans, masks
+
+
+@pytest.mark.parametrize("count,chunk", [(9, 0), (8, 3), (2, 0)])
+def test_odometry_batch_equals_pairwise_matching(fb, dev, count, chunk):
+    """Pair k of the chained batch == scan_match(scan k, scan k+1): same bins (the
+    shared spectra differ only in fp32 rounding), surfaces within 1e-5."""
+    cfg, delta, _ = fb.baseline_config(2)
+    scans, masks = _sequence(fb, 2, count)
+    S, M = to_dev(dev, scans, masks)
+    n = cfg.n_xy
+    m = fb.Matcher(cfg, max_batch=count - 1, chunk=chunk)
+    ts = torch.zeros((count - 1, cfg.n_theta), dtype=torch.float64, device=dev)
+    xs = torch.zeros((count - 1, n, n), dtype=torch.float32, device=dev)
+    odo = fb.decode_results(m.odometry(S, M, delta=delta, theta_surface=ts, xy_surface=xs))
+    ref, rts, rxs = run_gpu(fb, dev, cfg, delta, scans[:-1], scans[1:], masks[:-1], masks[1:])
+    t, x = ts.cpu().numpy(), xs.cpu().numpy()
+    assert np.abs(t - rts).max() <= 1e-5 * np.abs(rts).max()
+    assert np.abs(x - rxs).max() <= 1e-5 * np.abs(rxs).max()
+    assert (odo["status"] == fb.OK).all()
+    for k in range(count - 1):
+        assert (odo[k]["theta_bin"], odo[k]["xy_row"], odo[k]["xy_col"]) == \
+            (ref[k]["theta_bin"], ref[k]["xy_row"], ref[k]["xy_col"])
+        assert abs(odo[k]["theta"] - ref[k]["theta"]) < THETA_TOL
+        assert abs(odo[k]["tx"] - ref[k]["tx"]) < PX_TOL * delta and abs(odo[k]["ty"] - ref[k]["ty"]) < PX_TOL * delta
+
+
+def test_odometry_batch_matches_oracle_and_flags(fb, orc, dev):
+    cfg, delta, _ = fb.baseline_config(2)
+    scans, masks = _sequence(fb, 2, 4, first=50)
+    oc = oracle_cfg(orc, cfg)
+    S, M = to_dev(dev, scans, masks)
+    m = fb.Matcher(cfg, max_batch=3)
+    odo = fb.decode_results(m.odometry(S, M, delta=delta))
+    for k in range(3):
+        o = orc.scan_match(scans[k].astype(np.float64), scans[k + 1].astype(np.float64), oc, delta,
+                           masks[k].astype(np.float64), masks[k + 1].astype(np.float64))
+        assert (odo[k]["theta_bin"], odo[k]["xy_row"], odo[k]["xy_col"]) == (o.theta_bin, o.xy_row, o.xy_col)
+    # a bad value in scan 2 flags exactly the two pairs that use it
+    bad = scans.copy()
+    bad[2, 5, 5] = np.nan
+    B, = to_dev(dev, bad)
+    st = fb.decode_results(m.odometry(B, M, delta=delta))["status"]
+    assert list(st) == [fb.OK, fb.ERR_NONFINITE, fb.ERR_NONFINITE]
+    # fewer than two scans: no pairs, no error
+    m.odometry(S[:1], M[:1], delta=delta)
+
+
+def test_odometry_python_trajectory(fb, dev):
+    cfg, delta, _ = fb.baseline_config(2)
+    scans, masks = _sequence(fb, 2, 5, first=70)
+    poses, res = fb.odometry(scans, delta, cfg, masks)
+    assert len(poses) == 5 and poses[0] == fb.Pose2D()
+    # poses[k+1] = poses[k] o inverse(pose of pair k)
+    p1 = fb.compose(poses[0], fb.inverse(fb.Pose2D(res[0]["theta"], res[0]["tx"], res[0]["ty"])))
+    assert abs(p1.theta - poses[1].theta) < 1e-12 and abs(p1.tx - poses[1].tx) < 1e-12
