@@ -311,8 +311,8 @@ def run_ours(args):
     # two pairs; reported beside the independent-pair value
     chain = None
     if rank == 0 and not args.no_odometry and not polar:
-        seq = torch.cat([f, g[-1:]])  # per + 1 scans -> per pairs
-        seqm = torch.cat([mf, mg[-1:]])
+        # a generated drive: per + 1 scans of one scene, consecutive scans related
+        seq, seqm, _ = fb.synth_sequence_device(spec, first, per + 1, device=local)
         mo = fb.Matcher(cfg, max_batch=per, device=local, chunk=args.chunk)
         oout = torch.empty(per * fb.RESULT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
         mo.odometry(seq, seqm, delta=delta, out=oout, stream=stream)  # warm
@@ -326,7 +326,7 @@ def run_ours(args):
         rate = per * reps / (e0.elapsed_time(e1) / 1e3)
         chain = {"value": round(rate, 1), "unit": UNIT, "pairs": per, "steps": reps,
                  "vs_independent_pairs": round(rate / (value / world), 3),
-                 "api": "fscan_odometry_batch (scan k vs scan k+1 of one sequence, masks per scan)"}
+                 "api": "fscan_odometry_batch (scan k vs scan k+1 of a generated drive, masks per scan)"}
         del mo, seq, seqm, oout
 
     # e2e through the public host API (H2D + compute + D2H each step)

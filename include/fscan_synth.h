@@ -66,6 +66,16 @@ int fscan_synth_polar_host(const fscan_synth_spec* spec, int first, int count, f
 int fscan_synth_pairs_device(const fscan_synth_spec* spec, int first, int count, float* d_f,
                              float* d_g, float* d_mf, float* d_mg, double* truth, void* stream);
 
+/* Device rendering of a scan SEQUENCE (odometry workloads): `count` scans of
+ * the scene of pair `seq`, scan k seen after pose P_k (P_0 = identity, P_k the
+ * pose pair seq + k would draw: independent and bounded, so consecutive scans
+ * differ like generator pairs, up to twice the pose range). d_scans (and
+ * d_masks, per scan, may be NULL) hold count * n * n floats; truth (host, may
+ * be NULL) receives P_k as theta, tx, ty per scan; the relative pose of
+ * (scan k, scan k+1) in the matcher's convention is P_{k+1} o inverse(P_k). */
+int fscan_synth_sequence_device(const fscan_synth_spec* spec, int seq, int count, float* d_scans,
+                                float* d_masks, double* truth, void* stream);
+
 /* Device rendering of raw polar sweeps into device buffers. */
 int fscan_synth_polar_device(const fscan_synth_spec* spec, int first, int count, float* d_pf,
                              float* d_pg, double* truth, void* stream);

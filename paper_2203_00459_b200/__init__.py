@@ -138,6 +138,7 @@ SYMBOLS = {
     "fscan_synth_pairs_device": (C.c_int, [C.POINTER(CSynthSpec), C.c_int, C.c_int, _P, _P, _P, _P, _P,
                                            _P]),
     "fscan_synth_polar_device": (C.c_int, [C.POINTER(CSynthSpec), C.c_int, C.c_int, _P, _P, _P, _P]),
+    "fscan_synth_sequence_device": (C.c_int, [C.POINTER(CSynthSpec), C.c_int, C.c_int, _P, _P, _P, _P]),
 }
 
 
@@ -602,6 +603,24 @@ def synth_pairs_device(spec: CSynthSpec, first: int, count: int, device: int = 0
         raise RuntimeError(f"fscan_synth_pairs_device failed ({st})")
     torch.cuda.synchronize(dev)
     return f, g, mf, mg, truth
+
+
+def synth_sequence_device(spec: CSynthSpec, seq: int, count: int, device: int = 0):
+    """Device-rendered scan sequence (odometry workload) as CUDA tensors (scans, masks)
+    [count, N, N] and the host absolute poses [count, 3] (fscan_synth.h)."""
+    import torch
+    n = spec.n
+    dev = torch.device("cuda", device)
+    scans = torch.empty((count, n, n), dtype=torch.float32, device=dev)
+    masks = torch.empty_like(scans)
+    truth = np.empty((count, 3), np.float64)
+    torch.cuda.synchronize(dev)
+    st = lib().fscan_synth_sequence_device(C.byref(spec), seq, count, scans.data_ptr(), masks.data_ptr(),
+                                           truth.ctypes.data, torch.cuda.current_stream(dev).cuda_stream)
+    if st:
+        raise RuntimeError(f"fscan_synth_sequence_device failed ({st})")
+    torch.cuda.synchronize(dev)
+    return scans, masks, truth
 
 
 def synth_polar_device(spec: CSynthSpec, first: int, count: int, device: int = 0):

@@ -276,13 +276,55 @@ __global__ void fill_ones_kernel(float* p, size_t count) {
     if (i < count) p[i] = 1.0f;
 }
 
+// Sequence mode (seq >= 0): scan k (= 2 * local pair + scan) of ONE scene,
+// the scene of pair `seq`, with its objects moved by pose P_k, P_0 = identity
+// and P_k (k > 0) the pose pair seq + k would use: independent bounded poses,
+// so consecutive scans differ by at most twice the pair pose range.
+void sequence_scan(const fscan_synth_spec& s, int seq, int k, const PairScene& base, std::vector<Object>* out,
+                   double* pose) {
+    double th = 0.0, tx = 0.0, ty = 0.0;
+    if (k > 0) {
+        PairScene pk;
+        build_scene(s, seq + k, &pk);
+        th = pk.theta;
+        tx = pk.tx;
+        ty = pk.ty;
+    }
+    const double c = std::cos(th), sn = std::sin(th);
+    out->clear();
+    for (Object o : base.a) {
+        const double x0 = c * o.x0 - sn * o.y0 + tx, y0 = sn * o.x0 + c * o.y0 + ty;
+        const double x1 = c * o.x1 - sn * o.y1 + tx, y1 = sn * o.x1 + c * o.y1 + ty;
+        o.x0 = x0;
+        o.y0 = y0;
+        o.x1 = x1;
+        o.y1 = y1;
+        out->push_back(o);
+    }
+    if (pose) {
+        pose[0] = th;
+        pose[1] = tx;
+        pose[2] = ty;
+    }
+}
+
 // Upload per-scan object lists (scan_idx = 2 * local pair + scan).
 cudaError_t upload_scenes(const fscan_synth_spec& s, int first, int count, double* truth,
-                          cudaStream_t st, Object** d_objs, int** d_off) {
+                          cudaStream_t st, Object** d_objs, int** d_off, int seq = -1) {
     std::vector<Object> all;
     std::vector<int> off(1, 0);
-    PairScene ps;
+    PairScene ps, base;
+    std::vector<Object> tmp;
+    if (seq >= 0) build_scene(s, seq, &base);
     for (int i = 0; i < count; ++i) {
+        if (seq >= 0) {  // truth: the absolute pose of every scan
+            for (int sc = 0; sc < 2; ++sc) {
+                sequence_scan(s, seq, 2 * (first + i) + sc, base, &tmp, truth ? truth + 6 * i + 3 * sc : nullptr);
+                all.insert(all.end(), tmp.begin(), tmp.end());
+                off.push_back((int)all.size());
+            }
+            continue;
+        }
         build_scene(s, first + i, &ps);
         all.insert(all.end(), ps.a.begin(), ps.a.end());
         off.push_back((int)all.size());
@@ -441,13 +483,13 @@ int fscan_synth_pairs_host(const fscan_synth_spec* s, int first, int count, floa
     return 0;
 }
 
-int fscan_synth_polar_device(const fscan_synth_spec* s, int first, int count, float* d_pf,
-                             float* d_pg, double* truth, void* stream) {
+static int polar_device(const fscan_synth_spec* s, int first, int count, float* d_pf, float* d_pg,
+                        double* truth, void* stream, int seq) {
     if (!s->polar) return -1;
     cudaStream_t st = (cudaStream_t)stream;
     Object* objs = nullptr;
     int* off = nullptr;
-    cudaError_t e = upload_scenes(*s, first, count, truth, st, &objs, &off);
+    cudaError_t e = upload_scenes(*s, first, count, truth, st, &objs, &off, seq);
     if (e == cudaSuccess) {
         // gridDim.z <= 65535 scans per launch
         const int per = 16384;
@@ -467,8 +509,13 @@ int fscan_synth_polar_device(const fscan_synth_spec* s, int first, int count, fl
     return e == cudaSuccess ? 0 : (int)e;
 }
 
-int fscan_synth_pairs_device(const fscan_synth_spec* s, int first, int count, float* d_f, float* d_g,
-                             float* d_mf, float* d_mg, double* truth, void* stream) {
+int fscan_synth_polar_device(const fscan_synth_spec* s, int first, int count, float* d_pf,
+                             float* d_pg, double* truth, void* stream) {
+    return polar_device(s, first, count, d_pf, d_pg, truth, stream, -1);
+}
+
+static int pairs_device(const fscan_synth_spec* s, int first, int count, float* d_f, float* d_g, float* d_mf,
+                        float* d_mg, double* truth, void* stream, int seq) {
     cudaStream_t st = (cudaStream_t)stream;
     const size_t nn = (size_t)s->n * s->n;
     cudaError_t e = cudaSuccess;
@@ -480,7 +527,8 @@ int fscan_synth_pairs_device(const fscan_synth_spec* s, int first, int count, fl
         if (e == cudaSuccess) e = cudaMalloc(&pb, np * sizeof(float) * chunk);
         for (int i = 0; i < count && e == cudaSuccess; i += chunk) {
             const int cnt = std::min(chunk, count - i);
-            const int rc = fscan_synth_polar_device(s, first + i, cnt, pa, pb, truth ? truth + 3 * i : nullptr, st);
+            const int rc = polar_device(s, first + i, cnt, pa, pb,
+                                        truth ? truth + (seq >= 0 ? 6 : 3) * i : nullptr, st, seq);
             if (rc != 0) {
                 e = (cudaError_t)rc;
                 break;
@@ -494,7 +542,7 @@ int fscan_synth_pairs_device(const fscan_synth_spec* s, int first, int count, fl
     } else {
         Object* objs = nullptr;
         int* off = nullptr;
-        e = upload_scenes(*s, first, count, truth, st, &objs, &off);
+        e = upload_scenes(*s, first, count, truth, st, &objs, &off, seq);
         const int per = 16384;
         for (int i = 0; i < count && e == cudaSuccess; i += per) {
             const int cnt = std::min(per, count - i);
@@ -511,6 +559,43 @@ int fscan_synth_pairs_device(const fscan_synth_spec* s, int first, int count, fl
     }
     if (e == cudaSuccess && d_mf && d_mg) e = device_masks(*s, first, count, d_mf, d_mg, st);
     return e == cudaSuccess ? 0 : (int)e;
+}
+
+int fscan_synth_pairs_device(const fscan_synth_spec* s, int first, int count, float* d_f, float* d_g,
+                             float* d_mf, float* d_mg, double* truth, void* stream) {
+    return pairs_device(s, first, count, d_f, d_g, d_mf, d_mg, truth, stream, -1);
+}
+
+int fscan_synth_sequence_device(const fscan_synth_spec* s, int seq, int count, float* d_scans, float* d_masks,
+                                double* truth, void* stream) {
+    if (count < 1 || seq < 0) return -1;
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t nn = (size_t)s->n * s->n;
+    const int pairs = (count + 1) / 2;  // rendered as pairs (even scans, odd scans), then interleaved
+    float *ev = nullptr, *od = nullptr, *mev = nullptr, *mod = nullptr;
+    std::vector<double> tr(truth ? 6 * (size_t)pairs : 0);
+    cudaError_t e = cudaMalloc(&ev, 2 * nn * sizeof(float) * pairs);
+    if (e == cudaSuccess && d_masks) e = cudaMalloc(&mev, 2 * nn * sizeof(float) * pairs);
+    od = ev + nn * pairs;
+    if (mev) mod = mev + nn * pairs;
+    int rc = e == cudaSuccess ? pairs_device(s, 0, pairs, ev, od, mev, mod, truth ? tr.data() : nullptr, st, seq)
+                              : (int)e;
+    if (rc == 0) {
+        const size_t row = nn * sizeof(float);
+        e = cudaMemcpy2DAsync(d_scans, 2 * row, ev, row, row, pairs, cudaMemcpyDeviceToDevice, st);
+        if (e == cudaSuccess && count / 2)
+            e = cudaMemcpy2DAsync(d_scans + nn, 2 * row, od, row, row, count / 2, cudaMemcpyDeviceToDevice, st);
+        if (e == cudaSuccess && d_masks)
+            e = cudaMemcpy2DAsync(d_masks, 2 * row, mev, row, row, pairs, cudaMemcpyDeviceToDevice, st);
+        if (e == cudaSuccess && d_masks && count / 2)
+            e = cudaMemcpy2DAsync(d_masks + nn, 2 * row, mod, row, row, count / 2, cudaMemcpyDeviceToDevice, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        rc = (int)e;
+    }
+    if (truth && rc == 0) std::memcpy(truth, tr.data(), sizeof(double) * 3 * count);
+    cudaFree(ev);
+    cudaFree(mev);
+    return rc;
 }
 
 }  // extern "C"

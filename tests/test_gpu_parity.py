@@ -483,3 +483,19 @@ def test_odometry_python_trajectory(fb, dev):
     # poses[k+1] = poses[k] o inverse(pose of pair k)
     p1 = fb.compose(poses[0], fb.inverse(fb.Pose2D(res[0]["theta"], res[0]["tx"], res[0]["ty"])))
     assert abs(p1.theta - poses[1].theta) < 1e-12 and abs(p1.tx - poses[1].tx) < 1e-12
+
+
+def test_odometry_on_generated_drive_recovers_relative_poses(fb, dev):
+    """fscan_synth_sequence_device: consecutive scans related by P_{k+1} o inverse(P_k)."""
+    cfg, delta, _ = fb.baseline_config(2)
+    spec = fb.synth_spec(2)
+    scans, masks, truth = fb.synth_sequence_device(spec, 7, 6)
+    m = fb.Matcher(cfg, max_batch=5)
+    odo = fb.decode_results(m.odometry(scans, masks, delta=delta))
+    ok = 0
+    for k in range(5):
+        pk, pk1 = (fb.Pose2D(*truth[j]) for j in (k, k + 1))
+        rel = fb.compose(pk1, fb.inverse(pk))
+        ok += abs(odo[k]["theta"] - rel.theta) <= 2 * cfg.delta_theta and \
+            abs(odo[k]["tx"] - rel.tx) <= 2 * delta and abs(odo[k]["ty"] - rel.ty) <= 2 * delta
+    assert ok >= 4, (odo[["theta", "tx", "ty"]], truth)
