@@ -278,7 +278,6 @@ Params base_params(fscan_ctx* ctx, Lane& l, int batch, double delta) {
     p.n_live = ctx->n_live;
     p.zcols = 8 * ctx->rot_col_blocks;
     p.src_div = 1;
-    p.scan_stride = (long long)ctx->n * ctx->n;
     p.n_theta = ctx->cfg.n_theta;
     p.pad = ctx->cfg.pad_angle;
     p.L = ctx->cfg.n_theta + 2 * ctx->cfg.pad_angle;
@@ -765,11 +764,8 @@ fscan_status fscan_odometry_batch(fscan_ctx* ctx, const float* d_scans, const fl
     if (!d_scans || !d_out) return fail(ctx, FSCAN_ERR_INVALID_ARGUMENT, "fscan_odometry_batch: bad pointers");
     const size_t nn = (size_t)ctx->n * ctx->n;
     const int nt = ctx->cfg.n_theta;
-    // masked scans of a chunk, padded apart (pair k reads scans k and k+1 together)
-    static const size_t pad = std::getenv("FSCAN_CHAIN_PAD") ? std::atol(std::getenv("FSCAN_CHAIN_PAD")) : 0;
-    const size_t sstride = nn + pad;
     for (Lane& l : LaneRange{ctx})
-        if (!l.chain_ms) CK(cudaMalloc(&l.chain_ms, (ctx->alloc_chunk + 2) * sstride * sizeof(float)));
+        if (!l.chain_ms) CK(cudaMalloc(&l.chain_ms, (ctx->alloc_chunk + 2) * nn * sizeof(float)));
     return drive(ctx, pairs, (cudaStream_t)stream, [&](Lane& l, int off, int cnt) {
         // pairs off .. off+cnt-1 register scans off .. off+cnt
         Params p = base_params(ctx, l, cnt, delta);
@@ -777,9 +773,8 @@ fscan_status fscan_odometry_batch(fscan_ctx* ctx, const float* d_scans, const fl
         p.mf = d_masks ? d_masks + off * nn : nullptr;
         p.chain = 1;
         p.n_scans = cnt + 1;
-        p.scan_stride = (long long)sstride;
-        p.ft = l.chain_ms;            // masked scan s of the chunk at ft + s*sstride
-        p.gt = l.chain_ms + sstride;  // pair k reads scans k (ft) and k+1 (gt)
+        p.ft = l.chain_ms;       // masked scan s of the chunk at ft + s*nn
+        p.gt = l.chain_ms + nn;  // pair k reads scans k (ft) and k+1 (gt)
         p.out = d_out + off;
         p.theta_surf = d_tsurf ? d_tsurf + (size_t)off * nt : nullptr;
         p.xy_surf = d_xsurf ? d_xsurf + off * nn : nullptr;

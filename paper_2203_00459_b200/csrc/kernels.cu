@@ -36,7 +36,9 @@ using fscan_fft::part_floats;
 
 namespace {
 
-constexpr int kRowThreads = 256;
+// K1a CTA size: 128 threads (4 rows at N = 512) leave room for K1a CTAs next
+// to the compute-bound translation kernels of the other lane (measured -5% K1a)
+constexpr int kRowThreads = 128;
 
 template <int N>
 using RowG = Geom<N, kRowThreads>;
@@ -80,8 +82,8 @@ __global__ void __launch_bounds__(kRowThreads) k_rot_rows(Params p) {
             mfp = p.mf + fi * N * N + row;
             mgp = p.mf + gi * N * N + row;
         }
-        ftp = p.ft + fi * p.scan_stride + row;
-        gtp = p.ft + gi * p.scan_stride + row;
+        ftp = p.ft + fi * N * N + row;
+        gtp = p.ft + gi * N * N + row;
     } else {
         fp = p.f + base;
         gp = p.g + base;
@@ -470,8 +472,8 @@ __global__ void __launch_bounds__(kXThreads) k_xlat_rows(Params p) {
     const int y0 = blockIdx.x * ROWS;
     const RotState rs = p.rot[pair];
     const int src = MANY ? (p.item_base + pair) / p.src_div : pair;  // pair whose scans this item reads
-    const float* ft = p.ft + (size_t)src * p.scan_stride;
-    const float* gt = p.gt + (size_t)src * p.scan_stride;
+    const float* ft = p.ft + (size_t)src * N * N;
+    const float* gt = p.gt + (size_t)src * N * N;
     const float c0f32 = (N - 1) / 2.0f;  // exact
     // rotate_bilinear(g~, -theta); -theta == 0.0 returns g~ itself, which st = 0,
     // ct = 1 reproduce exactly (integer source coordinates, zero fractions)

@@ -85,7 +85,6 @@ struct Params {
     // this launch), the masked scans go to ft[scan], the magnitude planes and
     // the flags are one per scan
     int chain, n_scans;
-    long long scan_stride;    // floats between consecutive masked scans in ft / gt (N*N; chain mode: padded)
     Partial* bf_items;        // brute force: per global item hard argmax (nullable)
 };
 
