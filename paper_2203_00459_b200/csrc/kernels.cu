@@ -177,12 +177,20 @@ __global__ void __launch_bounds__(N) k_rot_cols(Params p) {
 // ---------------------------------------------------------------- K2
 constexpr int kPolarThreads = 512;
 
-// q-range split of the angular correlation so that (lag quads) x parts fills the CTA
+// K2b angular correlation: each thread owns kLags consecutive lags over one of
+// polar_parts(nt) q-ranges, so that (lag blocks) x parts fills the CTA.
+constexpr int kLags = 8;
+
 __host__ __device__ inline int polar_parts(int nt) {
-    const int quads = (nt + 3) / 4;
-    const int np = kPolarThreads / (quads > 0 ? quads : 1);
-    return np < 1 ? 1 : (np > 8 ? 8 : np);
+    const int blocks = (nt + kLags - 1) / kLags;
+    const int np = kPolarThreads / (blocks > 0 ? blocks : 1);
+    return np < 1 ? 1 : (np > 16 ? 16 : np);
 }
+
+// Bx is stored skewed by one double per 8 (lane stride kLags = 8 doubles maps
+// to 9: conflict-free 64-bit shared loads)
+__host__ __device__ inline int bx_skew(int j) { return j + (j >> 3); }
+__host__ __device__ inline int bx_len(int L, int nt) { return bx_skew(L + nt + 2 * kLags) + 1; }
 
 __device__ __forceinline__ float tile_at(const float* m, int n, int r, int u) {
     return __ldg(m + ((size_t)(u >> 3) * n + r) * 8 + (u & 7));
@@ -241,10 +249,10 @@ __global__ void __launch_bounds__(kPolarThreads) k_rot_polar(Params p) {
     extern __shared__ double dsm[];
     const int pair = blockIdx.x;
     const int nt = p.n_theta, L = p.L, pad = p.pad;
-    double* A = dsm;                 // wrap-extended radial-sum profiles, length L
-    double* B = dsm + L;             // length L + nt + 4 (see below)
-    double* s = B + L + nt + 4;      // theta surface, n_theta
-    double* red_v;                   // block reduction scratch (32 entries each), after the partials
+    double* A = dsm;                      // wrap-extended radial-sum profiles, length L
+    double* B = dsm + L;                  // skewed circular extension, bx_len(L, nt)
+    double* s = B + bx_len(L, nt);        // theta surface, n_theta
+    double* red_v;                        // block reduction scratch (32 entries each), after the partials
     int* red_i;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nwarps = kPolarThreads / 32;
@@ -268,10 +276,10 @@ __global__ void __launch_bounds__(kPolarThreads) k_rot_polar(Params p) {
     // wrap_pad (imageops.cpp:101-113): padded row q holds profile row (q - pad) mod nt.
     // B is stored circularly extended, Bx[j] = B[(j - nt/2) mod L], so the score
     // s[k] = (1/C) sum_q A[q] B[(q + k - nt/2) mod L] is
-    // sum_q A[q] Bx[q + k] without modular indexing.
+    // sum_q A[q] Bx[q + k] without modular indexing (Bx[j] lives at bx_skew(j)).
     const double* prof = p.prof + (size_t)pair * 2 * nt;
     const int np = polar_parts(nt);
-    double* Bx = B;                        // L + nt + 4 (tail padding for the last lag quad)
+    double* Bx = B;
     double* part = s + nt;                 // np x nt partial sums
     red_v = part + (size_t)np * nt;
     red_i = (int*)(red_v + 32);
@@ -280,38 +288,54 @@ __global__ void __launch_bounds__(kPolarThreads) k_rot_polar(Params p) {
         if (i < 0) i += nt;
         A[q] = prof[i];
     }
-    for (int j = threadIdx.x; j < L + nt + 4; j += kPolarThreads) {
+    for (int j = threadIdx.x; j < L + nt + 2 * kLags; j += kPolarThreads) {
         int qq = (j - nt / 2) % L;
         if (qq < 0) qq += L;
         int i = (qq - pad) % nt;
         if (i < 0) i += nt;
-        Bx[j] = prof[nt + i];
+        Bx[bx_skew(j)] = prof[nt + i];
     }
     __syncthreads();
-    // register-blocked: each item owns 4 consecutive lags over one of np q-ranges
+    // register-blocked: each item owns kLags consecutive lags over one of np
+    // q-ranges; a 15-value window of Bx slides over 8 q per step (64 DFMA per
+    // 8 A and 8 Bx loads)
     {
-        const int quads = (nt + 3) / 4;
+        const int blocks = (nt + kLags - 1) / kLags;
         const int item = threadIdx.x;
-        if (item < quads * np) {
-            const int k0 = 4 * (item % quads), pi = item / quads;
+        if (item < blocks * np) {
+            const int k0 = kLags * (item % blocks), pi = item / blocks;
             const int q0 = (int)((long)L * pi / np), q1 = (int)((long)L * (pi + 1) / np);
-            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-            double b0 = Bx[q0 + k0], b1 = Bx[q0 + k0 + 1], b2 = Bx[q0 + k0 + 2];
-            for (int q = q0; q < q1; ++q) {
-                const double a = A[q], b3 = Bx[q + k0 + 3];
-                a0 = fma(a, b0, a0);
-                a1 = fma(a, b1, a1);
-                a2 = fma(a, b2, a2);
-                a3 = fma(a, b3, a3);
-                b0 = b1;
-                b1 = b2;
-                b2 = b3;
+            double acc[kLags];
+#pragma unroll
+            for (int c = 0; c < kLags; ++c) acc[c] = 0.0;
+            double w[2 * kLags - 1];
+#pragma unroll
+            for (int c = 0; c < kLags - 1; ++c) w[c] = Bx[bx_skew(q0 + k0 + c)];
+            int q = q0;
+            for (; q + kLags <= q1; q += kLags) {
+#pragma unroll
+                for (int c = 0; c < kLags; ++c) w[kLags - 1 + c] = Bx[bx_skew(q + k0 + kLags - 1 + c)];
+#pragma unroll
+                for (int u = 0; u < kLags; ++u) {
+                    const double a = A[q + u];
+#pragma unroll
+                    for (int c = 0; c < kLags; ++c) acc[c] = fma(a, w[u + c], acc[c]);
+                }
+#pragma unroll
+                for (int c = 0; c < kLags - 1; ++c) w[c] = w[kLags + c];
+            }
+            for (; q < q1; ++q) {  // tail: one q at a time
+                w[kLags - 1] = Bx[bx_skew(q + k0 + kLags - 1)];
+                const double a = A[q];
+#pragma unroll
+                for (int c = 0; c < kLags; ++c) acc[c] = fma(a, w[c], acc[c]);
+#pragma unroll
+                for (int c = 0; c < kLags - 1; ++c) w[c] = w[c + 1];
             }
             double* pr = part + (size_t)pi * nt + k0;
-            if (k0 < nt) pr[0] = a0;
-            if (k0 + 1 < nt) pr[1] = a1;
-            if (k0 + 2 < nt) pr[2] = a2;
-            if (k0 + 3 < nt) pr[3] = a3;
+#pragma unroll
+            for (int c = 0; c < kLags; ++c)
+                if (k0 + c < nt) pr[c] = acc[c];
         }
     }
     __syncthreads();
@@ -1056,7 +1080,8 @@ cudaError_t launch_rot_gather(const Params& p, cudaStream_t s) {
 }
 
 cudaError_t launch_rot_polar(const Params& p, cudaStream_t s) {
-    const size_t sm = (size_t)(2 * p.L + 4 + p.n_theta * (2 + polar_parts(p.n_theta)) + 32) * sizeof(double) +
+    const size_t sm = (size_t)(p.L + bx_len(p.L, p.n_theta) + p.n_theta * (1 + polar_parts(p.n_theta)) + 32) *
+                          sizeof(double) +
                       32 * sizeof(int);
     cudaError_t e = set_smem(k_rot_polar, sm);
     if (e != cudaSuccess) return e;
