@@ -26,8 +26,8 @@
 //
 // Twiddles come from a fp32 table tw[i] = exp(-2*pi*i*i/N) (rounded from fp64
 // on the host); SIGN = +1 uses the conjugate. Transforms are unnormalised,
-// matching FFTW_FORWARD / FFTW_BACKWARD. Every thread of the CTA must call
-// fft_regs the same number of times (it contains __syncthreads()).
+// matching FFTW_FORWARD / FFTW_BACKWARD. Exchanges synchronise the warp when
+// the transform lives in one warp (fft_regs<..., WARP = true>), else the CTA.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -263,7 +263,18 @@ __device__ __forceinline__ float2 twiddle(const float2* __restrict__ tw, int idx
 }
 
 // One Stockham stage. Ns = span before this stage, R = radix.
-template <int N, int R, int Ns, bool LAST, int SIGN, typename L>
+// Exchange barrier: a warp barrier when every thread of the transform (and of
+// any transform sharing its buffer) is in one warp, else the CTA barrier.
+template <bool WARP>
+__device__ __forceinline__ void exchange_sync() {
+    if constexpr (WARP) {
+        __syncwarp();
+    } else {
+        __syncthreads();
+    }
+}
+
+template <int N, int R, int Ns, bool LAST, int SIGN, bool WARP, typename L>
 __device__ __forceinline__ void stage(float2 (&v)[16], int t, const L& lay, const float2* __restrict__ tw) {
     constexpr int T = N / 16;
     constexpr int NB = 16 / R;
@@ -290,26 +301,30 @@ __device__ __forceinline__ void stage(float2 (&v)[16], int t, const L& lay, cons
         }
     }
     if constexpr (!LAST) {
-        __syncthreads();
+        exchange_sync<WARP>();
 #pragma unroll
         for (int m = 0; m < 16; ++m) v[m] = lay.get(t + m * T);
-        __syncthreads();
+        exchange_sync<WARP>();
     }
 }
 
-// In-register FFT of one length-N transform (see header comment).
-template <int N, int SIGN, typename L>
+// In-register FFT of one length-N transform (see header comment). WARP: the
+// caller guarantees the transform's threads and exchange buffer live in one
+// warp (row layouts with T <= 32), so the exchanges need only __syncwarp;
+// otherwise every thread of the CTA must call fft_regs the same number of times.
+template <int N, int SIGN, bool WARP = false, typename L>
 __device__ __forceinline__ void fft_regs(float2 (&v)[16], int t, const L& lay, const float2* __restrict__ tw) {
     static_assert(N >= 16 && (N & (N - 1)) == 0, "power-of-two length >= 16");
+    static_assert(!WARP || N / 16 <= 32, "a warp-synchronous transform fits in one warp");
     if constexpr (N == 16) {
-        stage<N, 16, 1, true, SIGN>(v, t, lay, tw);
+        stage<N, 16, 1, true, SIGN, WARP>(v, t, lay, tw);
     } else if constexpr (N <= 256) {
-        stage<N, 16, 1, false, SIGN>(v, t, lay, tw);
-        stage<N, N / 16, 16, true, SIGN>(v, t, lay, tw);
+        stage<N, 16, 1, false, SIGN, WARP>(v, t, lay, tw);
+        stage<N, N / 16, 16, true, SIGN, WARP>(v, t, lay, tw);
     } else {
-        stage<N, 16, 1, false, SIGN>(v, t, lay, tw);
-        stage<N, 16, 16, false, SIGN>(v, t, lay, tw);
-        stage<N, N / 256, 256, true, SIGN>(v, t, lay, tw);
+        stage<N, 16, 1, false, SIGN, WARP>(v, t, lay, tw);
+        stage<N, 16, 16, false, SIGN, WARP>(v, t, lay, tw);
+        stage<N, N / 256, 256, true, SIGN, WARP>(v, t, lay, tw);
     }
 }
 

@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(kRowThreads) k_rot_rows(Params p) {
         const float w = hy * __ldg(p.hann + x);
         v[m] = make_float2(fv * w, gv * w);
     }
-    fft_regs<N, -1>(v, t, lay, p.tw_n);
+    fft_regs<N, -1, (G::T <= 32)>(v, t, lay, p.tw_n);  // a row per warp (or two warps at N = 1024)
 #pragma unroll
     for (int m = 0; m < 16; ++m) {
         const int x = t + m * T;
@@ -562,7 +562,7 @@ __global__ void __launch_bounds__(kXThreads) k_xlat_rows(Params p) {
             v[m] = q ? cmul(wm(p.tw_m, n0 * q), s) : s;
         }
         const auto b = G::lay(xbase, tr);
-        fft_regs<K, -1>(v, t, b, p.tw_k);
+        fft_regs<K, -1, true>(v, t, b, p.tw_k);  // T <= 32: each transform within a warp
 #pragma unroll
         for (int m = 0; m < 16; ++m) b.put(t + m * T, v[m]);
     }
@@ -636,7 +636,7 @@ __global__ void __launch_bounds__(XColGeom<N>::THREADS) k_xlat_cols(Params p) {
         const float2 s = cadd(make_float2(u0.x, u0.y), cmul(w3q, make_float2(u1.x, u1.y)));
         a[m] = q ? cmul(wm(p.tw_m, n0 * q), s) : s;
     }
-    fft_regs<K, -1>(a, t, bufA, p.tw_k);
+    fft_regs<K, -1, true>(a, t, bufA, p.tw_k);  // transforms of a warp share a buffer group
 #pragma unroll
     for (int m = 0; m < 16; ++m) bufA.put(t + m * T, a[m]);  // park F_q (own slots)
 #pragma unroll
@@ -646,10 +646,10 @@ __global__ void __launch_bounds__(XColGeom<N>::THREADS) k_xlat_cols(Params p) {
         const float2 s = cadd(make_float2(u0.z, u0.w), cmul(w3q, make_float2(u1.z, u1.w)));
         a[m] = q ? cmul(wm(p.tw_m, n0 * q), s) : s;
     }
-    fft_regs<K, -1>(a, t, bufB, p.tw_k);
+    fft_regs<K, -1, true>(a, t, bufB, p.tw_k);
 #pragma unroll
     for (int m = 0; m < 16; ++m) a[m] = cmul(cconj(bufA.get(t + m * T)), a[m]);  // conj(F) G
-    fft_regs<K, +1>(a, t, bufB, p.tw_k);
+    fft_regs<K, +1, true>(a, t, bufB, p.tw_k);
 #pragma unroll
     for (int m = 0; m < 16; ++m) bufB.put(t + m * T, a[m]);
     __syncthreads();
@@ -741,7 +741,7 @@ __global__ void __launch_bounds__(XOutGeom<N>::THREADS) k_xlat_out(Params p) {
             const float2 B = cmul(csub(a, b), cconj(wm(p.tw_m, k)));
             v[m] = make_float2(A.x - B.y, A.y + B.x);  // A + iB
         }
-        fft_regs<X::K2, +1>(v, t, buf, p.tw_k2);
+        fft_regs<X::K2, +1, true>(v, t, buf, p.tw_k2);
 #pragma unroll
         for (int m = 0; m < 16; ++m) buf.put(t + m * T, v[m]);
     }
