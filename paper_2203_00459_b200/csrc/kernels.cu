@@ -461,7 +461,10 @@ struct XRowGeom {
     static constexpr int ROWS = G::PER_CTA / 3;
     static constexpr int SP0 = N + N / 32;
     static constexpr int SP = (SP0 % 32 == 0) ? SP0 + 16 : SP0;  // stash row stride (floats)
-    static constexpr size_t SMEM = ((size_t)2 * ROWS * SP + G::FLOATS) * sizeof(float);
+    // the FFT exchange buffers alias the gather stash (dead once v[] is loaded):
+    // ~50 KB per CTA, three CTAs per SM
+    static constexpr size_t STASH = (size_t)2 * ROWS * SP;
+    static constexpr size_t SMEM = (STASH > (size_t)G::FLOATS ? STASH : (size_t)G::FLOATS) * sizeof(float);
     static_assert(G::PER_CTA % 3 == 0, "three transforms per row");
     // separation loop: a half-warp reads R rows x KB consecutive k. Row ol's
     // buffers start at 3 * ol * stride, i.e. bank offset o * ol (mod 16); R =
@@ -482,8 +485,11 @@ struct XRowGeom {
 // MANY: items of a multi-candidate launch (brute-force search) read the scans
 // of pair (item_base + item) / src_div; a separate instantiation keeps the
 // matcher's gather loop free of that indexing.
+// Three CTAs per SM (56 registers): the gather is latency bound, occupancy
+// beats per-thread memory-level parallelism here (measured: 2 CTAs x 6 cells
+// in flight 8.1 ms, 3 CTAs x 4 cells 7.7 ms per 4096 C4 pairs).
 template <int N, bool MANY>
-__global__ void __launch_bounds__(kXThreads) k_xlat_rows(Params p) {
+__global__ void __launch_bounds__(kXThreads, 3) k_xlat_rows(Params p) {
     constexpr int K = N / 2, M = 3 * K, H = M / 2;
     using X = XRowGeom<N>;
     using G = typename X::G;
@@ -491,7 +497,7 @@ __global__ void __launch_bounds__(kXThreads) k_xlat_rows(Params p) {
     extern __shared__ float smem[];
     float* st_re = smem;
     float* st_im = smem + ROWS * SP;
-    float* xbase = smem + 2 * ROWS * SP;
+    float* xbase = smem;  // aliases the stash (see XRowGeom::SMEM)
     const int pair = blockIdx.y;
     const int y0 = blockIdx.x * ROWS;
     const RotState rs = p.rot[pair];
@@ -506,7 +512,7 @@ __global__ void __launch_bounds__(kXThreads) k_xlat_rows(Params p) {
     // consecutive x; U cells per thread per round with every load issued
     // before any use (memory-level parallelism for the L2/DRAM latency)
     constexpr int CELLS = ROWS * N;
-    constexpr int U = 6;
+    constexpr int U = 4;
 #pragma unroll 1
     for (int e0 = threadIdx.x; e0 < CELLS; e0 += U * kXThreads) {
         float fv[U], tap[U][4], frs[U], fcs[U];
@@ -561,6 +567,7 @@ __global__ void __launch_bounds__(kXThreads) k_xlat_rows(Params p) {
             const float2 s = cadd(make_float2(st_re[a0], st_im[a0]), cmul(w3q, make_float2(st_re[a1], st_im[a1])));
             v[m] = q ? cmul(wm(p.tw_m, n0 * q), s) : s;
         }
+        __syncthreads();  // every stash read done before the exchange buffers are written
         const auto b = G::lay(xbase, tr);
         fft_regs<K, -1, true>(v, t, b, p.tw_k);  // T <= 32: each transform within a warp
 #pragma unroll
