@@ -134,7 +134,8 @@ __global__ void __launch_bounds__(kRowThreads) k_rot_rows(Params p) {
 // 8 output columns u in [u0, u0+8) plus their mirrors (N-u) mod N, 16
 // interleaved column FFTs (column index fastest in the warp, Lay<16>);
 // F = (Z[v,u] + conj Z[-v,-u]) / 2, G = (Z[v,u] - conj Z[-v,-u]) / 2i;
-// |F|, |G| times the annular band, written as an [N centred rows][8] tile.
+// |F|, |G| times the annular band, written as an [N centred rows][8] tile of
+// (|F|, |G|) pairs.
 template <int N>
 __global__ void __launch_bounds__(N) k_rot_cols(Params p) {
     constexpr int T = N / 16;
@@ -154,8 +155,8 @@ __global__ void __launch_bounds__(N) k_rot_cols(Params p) {
 #pragma unroll
     for (int m = 0; m < 16; ++m) lay.put(t + m * T, v[m]);
     __syncthreads();
-    float* outf = p.mag + (((size_t)pair * 2 + 0) * (N / 16) + blockIdx.x) * (size_t)(N * 8);
-    float* outg = p.mag + (((size_t)pair * 2 + 1) * (N / 16) + blockIdx.x) * (size_t)(N * 8);
+    // (|F|, |G|) interleaved: one 8-byte load per tap in K2a
+    float2* out = reinterpret_cast<float2*>(p.mag) + ((size_t)pair * (N / 16) + blockIdx.x) * (size_t)(N * 8);
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
         const int o = threadIdx.x + q * N;  // o = v_c * 8 + cc
@@ -169,8 +170,8 @@ __global__ void __launch_bounds__(N) k_rot_cols(Params p) {
         const int2 bd = __ldg(p.band + vc);
         const int u = u0 + cc;
         const bool in = (u >= bd.x) && (u <= bd.y);
-        outf[o] = in ? 0.5f * sqrtf(fr * fr + fi * fi) : 0.0f;
-        outg[o] = in ? 0.5f * sqrtf(gr * gr + gi * gi) : 0.0f;
+        out[o] = in ? make_float2(0.5f * sqrtf(fr * fr + fi * fi), 0.5f * sqrtf(gr * gr + gi * gi))
+                    : make_float2(0.0f, 0.0f);
     }
 }
 
@@ -192,27 +193,25 @@ __host__ __device__ inline int polar_parts(int nt) {
 __host__ __device__ inline int bx_skew(int j) { return j + (j >> 3); }
 __host__ __device__ inline int bx_len(int L, int nt) { return bx_skew(L + nt + 2 * kLags) + 1; }
 
-__device__ __forceinline__ float tile_at(const float* m, int n, int r, int u) {
-    return __ldg(m + ((size_t)(u >> 3) * n + r) * 8 + (u & 7));
+__device__ __forceinline__ const float2* tile_at(const float2* m, int n, int r, int u) {
+    return m + ((size_t)(u >> 3) * n + r) * 8 + (u & 7);
 }
 
 // K2a: radial sums of the bilinear polar resample (cart2pol) of |F| and |G|:
 // one thread per azimuth row, walking its radii. The lanes of a warp are 32
 // adjacent rays at the same radius, which sit within a few pixels of each
-// other, so a warp-wide tap load touches ~2-4 magnitude-tile lines instead of
-// the ~10 a ray's consecutive radii span. fp64 sums per row, written to
-// p.prof[pair][2][n_theta]; the tap table is radius-major ([n_live][n_theta]).
+// other, so a warp-wide tap load touches few magnitude-tile lines (4 rows x 4
+// (|F|,|G|) columns each) instead of the many a ray's consecutive radii span.
+// fp64 sums per row, written to p.prof[pair][2][n_theta]; the tap table is
+// radius-major ([n_live][n_theta]).
 constexpr int kGatherThreads = 128;
 
-__global__ void __launch_bounds__(kGatherThreads) k_rot_gather(Params p) {
-    const int pair = blockIdx.y;
+// SPLIT (chain mode, odd pair k): |F| of scan k is the .y of transform k/2,
+// |G| of scan k+1 the .x of transform k/2 + 1.
+template <bool SPLIT>
+__device__ __forceinline__ void gather_sums(const Params& p, const float2* m, int i, double* prof) {
     const int nt = p.n_theta, n = p.n, n_live = p.n_live;
-    const int i = blockIdx.x * kGatherThreads + threadIdx.x;
-    if (i >= nt) return;
-    // |F| of the pair's first scan and |G| of its second: planes 2*pair, 2*pair+1,
-    // or in chain mode (one plane per scan of the sequence) planes pair, pair+1
-    const float* mf = p.mag + (size_t)pair * (p.chain ? 1 : 2) * n * (n / 2);
-    const float* mg = mf + (size_t)n * (n / 2);
+    const float2* m2 = m + (size_t)n * (n / 2);
     const PolarTap* col = p.taps + i;
     double af = 0.0, ag = 0.0;
     constexpr int U = 4;  // independent entries in flight per thread (memory-level parallelism)
@@ -229,8 +228,14 @@ __global__ void __launch_bounds__(kGatherThreads) k_rot_gather(Params p) {
             for (int tp = 0; tp < 4; ++tp) {
                 const bool on = (fl >> tp) & 1;
                 const int rr = r0 + (tp >> 1), uu = u + (tp & 1);
-                fv[q][tp] = on ? tile_at(mf, n, rr, uu) : 0.f;
-                gv[q][tp] = on ? tile_at(mg, n, rr, uu) : 0.f;
+                if constexpr (SPLIT) {
+                    fv[q][tp] = on ? __ldg(&tile_at(m, n, rr, uu)->y) : 0.f;
+                    gv[q][tp] = on ? __ldg(&tile_at(m2, n, rr, uu)->x) : 0.f;
+                } else {
+                    const float2 v = on ? __ldg(tile_at(m, n, rr, uu)) : make_float2(0.f, 0.f);
+                    fv[q][tp] = v.x;
+                    gv[q][tp] = v.y;
+                }
             }
         }
 #pragma unroll
@@ -239,9 +244,24 @@ __global__ void __launch_bounds__(kGatherThreads) k_rot_gather(Params p) {
             ag += (double)bilerp(e[q].fr, e[q].fc, gv[q][0], gv[q][1], gv[q][2], gv[q][3]);
         }
     }
-    double* prof = p.prof + (size_t)pair * 2 * nt;
     prof[i] = af;
     prof[nt + i] = ag;
+}
+
+__global__ void __launch_bounds__(kGatherThreads) k_rot_gather(Params p) {
+    const int pair = blockIdx.y;
+    const int nt = p.n_theta, n = p.n;
+    const int i = blockIdx.x * kGatherThreads + threadIdx.x;
+    if (i >= nt) return;
+    // the K1b transform holding the pair's |F| (and |G|): one per pair, or in
+    // chain mode one per two scans of the sequence
+    const int tr = p.chain ? pair / 2 : pair;
+    const float2* m = reinterpret_cast<const float2*>(p.mag) + (size_t)tr * n * (n / 2);
+    double* prof = p.prof + (size_t)pair * 2 * nt;
+    if (p.chain && (pair & 1))
+        gather_sums<true>(p, m, i, prof);
+    else
+        gather_sums<false>(p, m, i, prof);
 }
 
 // K2b: angular correlation of the profiles, hard + soft argmax over theta.
@@ -927,8 +947,8 @@ __global__ void k_mag_unpack(Params p) {
     const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (size_t)n * (n / 2)) return;
     const int vc = (int)(idx / (n / 2)), u = (int)(idx % (n / 2));
-    const float* m = p.mag + (size_t)pair * 2 * n * (n / 2);
-    p.mag_out[(size_t)pair * n * (n / 2) + idx] = m[((size_t)(u >> 3) * n + vc) * 8 + (u & 7)];
+    const float2* m = reinterpret_cast<const float2*>(p.mag) + (size_t)pair * n * (n / 2);
+    p.mag_out[(size_t)pair * n * (n / 2) + idx] = tile_at(m, n, vc, u)->x;
 }
 
 // K0 in two steps: the cell geometry (fp64 atan2 / sqrt, identical for every
