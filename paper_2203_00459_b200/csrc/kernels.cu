@@ -53,6 +53,13 @@ __device__ __forceinline__ float bilerp(float fr, float fc, float a00, float a01
     return (1.0f - fr) * ((1.0f - fc) * a00 + fc * a01) + fr * ((1.0f - fc) * a10 + fc * a11);
 }
 
+// (|F|,|G|) columns per magnitude tile row (4 measured equal: faster K2a
+// gather, slower K1b stores)
+constexpr int kTileW = 8;
+__device__ __forceinline__ const float2* tile_at(const float2* m, int n, int r, int u) {
+    return m + ((size_t)(u / kTileW) * n + r) * kTileW + (u % kTileW);
+}
+
 // ---------------------------------------------------------------- K1a
 // rows of f~ = f*mf and g~ = g*mg: write the masked scans (translation stage
 // input), window by the separable Hann w[r]*w[c], FFT the packed row
@@ -170,8 +177,9 @@ __global__ void __launch_bounds__(N) k_rot_cols(Params p) {
         const int2 bd = __ldg(p.band + vc);
         const int u = u0 + cc;
         const bool in = (u >= bd.x) && (u <= bd.y);
-        out[o] = in ? make_float2(0.5f * sqrtf(fr * fr + fi * fi), 0.5f * sqrtf(gr * gr + gi * gi))
-                    : make_float2(0.0f, 0.0f);
+        const float2 mv = in ? make_float2(0.5f * sqrtf(fr * fr + fi * fi), 0.5f * sqrtf(gr * gr + gi * gi))
+                             : make_float2(0.0f, 0.0f);
+        out[o] = mv;  // tile [u0 / 8][v_c][cc]
     }
 }
 
@@ -193,9 +201,6 @@ __host__ __device__ inline int polar_parts(int nt) {
 __host__ __device__ inline int bx_skew(int j) { return j + (j >> 3); }
 __host__ __device__ inline int bx_len(int L, int nt) { return bx_skew(L + nt + 2 * kLags) + 1; }
 
-__device__ __forceinline__ const float2* tile_at(const float2* m, int n, int r, int u) {
-    return m + ((size_t)(u >> 3) * n + r) * 8 + (u & 7);
-}
 
 // K2a: radial sums of the bilinear polar resample (cart2pol) of |F| and |G|:
 // one thread per azimuth row, walking its radii. The lanes of a warp are 32
