@@ -39,7 +39,8 @@ typedef enum fscan_status {
     FSCAN_ERR_MASK_RANGE = 3,       /* mask value outside [0, 1]            */
     FSCAN_ERR_UNSUPPORTED = 4,      /* valid for the reference, not here    */
     FSCAN_ERR_CUDA = 5,             /* CUDA runtime / launch failure        */
-    FSCAN_ERR_NO_DEVICE = 6         /* no usable sm_100 device              */
+    FSCAN_ERR_NO_DEVICE = 6,        /* no usable sm_100 device              */
+    FSCAN_ERR_IO = 7                /* scan file missing / malformed (fscan_io.h) */
 } fscan_status;
 
 /* fscan::MatchConfig (matcher.hpp:13-26), field for field. */

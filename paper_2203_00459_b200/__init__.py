@@ -23,9 +23,9 @@ ROOT = os.path.dirname(HERE)
 # FSCAN_LIB: load an alternative build of the same library (A/B kernel timing)
 LIB_PATH = os.environ.get("FSCAN_LIB") or os.path.join(HERE, "libfscan_b200.so")
 
-OK, ERR_INVALID_ARGUMENT, ERR_NONFINITE, ERR_MASK_RANGE, ERR_UNSUPPORTED, ERR_CUDA, ERR_NO_DEVICE = range(7)
+OK, ERR_INVALID_ARGUMENT, ERR_NONFINITE, ERR_MASK_RANGE, ERR_UNSUPPORTED, ERR_CUDA, ERR_NO_DEVICE, ERR_IO = range(8)
 _STATUS = {0: "OK", 1: "INVALID_ARGUMENT", 2: "NONFINITE", 3: "MASK_RANGE", 4: "UNSUPPORTED",
-           5: "CUDA", 6: "NO_DEVICE"}
+           5: "CUDA", 6: "NO_DEVICE", 7: "IO"}
 
 
 class FscanError(RuntimeError):
@@ -131,6 +131,11 @@ SYMBOLS = {
     "fscan_ctx_launches_last": (C.c_int, [_P]),
     "fscan_ctx_set_profiling": (C.c_int, [_P, C.c_int]),
     "fscan_ctx_kernel_times": (C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_int), C.c_int]),
+    "fscan_fscn_read_header": (C.c_int, [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_double), C.c_char_p,
+                                         C.c_size_t]),
+    "fscan_fscn_read_batch": (C.c_int, [C.POINTER(C.c_char_p), C.c_int, C.c_int, _P, _P, C.c_int, C.c_char_p,
+                                        C.c_size_t]),
+    "fscan_fscn_write": (C.c_int, [C.c_char_p, _P, C.c_int, C.c_double, C.c_char_p, C.c_size_t]),
     "fscan_synth_preset": (C.c_int, [C.c_int, C.POINTER(CSynthSpec)]),
     "fscan_synth_pairs_host": (C.c_int, [C.POINTER(CSynthSpec), C.c_int, C.c_int, _P, _P, _P, _P, _P,
                                          C.c_int]),
@@ -226,14 +231,27 @@ def baseline_config(cid: int) -> tuple[MatchConfig, float, int]:
 # ---------------------------------------------------------------- matcher
 
 def _ptr(t) -> int | None:
-    """Device pointer of a CUDA torch tensor (or None)."""
+    """Device pointer of a CUDA torch tensor, or of any CUDA array exporting
+    __dlpack__ (CuPy, JAX, ...: viewed zero-copy through torch.from_dlpack)."""
     if t is None:
         return None
+    if not hasattr(t, "is_cuda") and hasattr(t, "__dlpack__"):
+        import torch
+        t = torch.from_dlpack(t)
     if not t.is_cuda:
         raise ValueError("expected a CUDA tensor")
     if not t.is_contiguous():
         raise ValueError("expected a contiguous tensor")
     return t.data_ptr()
+
+
+def _as_tensor(x):
+    """torch view of a foreign CUDA array exporting __dlpack__ (zero-copy); other
+    inputs pass through."""
+    if x is not None and not hasattr(x, "is_cuda") and hasattr(x, "__dlpack__"):
+        import torch
+        return torch.from_dlpack(x)
+    return x
 
 
 def _stream_ptr(stream) -> int | None:
@@ -305,6 +323,7 @@ class Matcher:
         ``out`` is a uint8 CUDA tensor of B * sizeof(result) bytes (allocated if
         None) and is returned; decode with :func:`decode_results` after sync.
         """
+        f, g, mf, mg = _as_tensor(f), _as_tensor(g), _as_tensor(mf), _as_tensor(mg)
         import torch
         b = int(f.shape[0])
         if out is None:
@@ -317,6 +336,7 @@ class Matcher:
     def match_polar(self, pf, pg, mf=None, mg=None, *, range_res: float, delta: float, out=None,
                     theta_surface=None, xy_surface=None, stream=None):
         """Config-3 path: raw polar sweeps [B, n_az, n_range] (CUDA tensors) -> K0 -> match."""
+        pf, pg, mf, mg = _as_tensor(pf), _as_tensor(pg), _as_tensor(mf), _as_tensor(mg)
         import torch
         b, n_az, n_range = (int(x) for x in pf.shape)
         if out is None:
@@ -349,6 +369,7 @@ class Matcher:
         return (res, ts, xs) if surfaces else res
 
     def estimate_rotation(self, f, g, *, theta=None, theta_surface=None, stream=None):
+        f, g = _as_tensor(f), _as_tensor(g)
         import torch
         b = int(f.shape[0])
         if theta is None:
@@ -359,6 +380,7 @@ class Matcher:
         return theta
 
     def estimate_translation(self, f, g, theta, *, delta: float, xy_surface=None, stream=None):
+        f, g, theta = _as_tensor(f), _as_tensor(g), _as_tensor(theta)
         import torch
         b = int(f.shape[0])
         txy = torch.empty((b, 2), dtype=torch.float64, device=f.device)
@@ -371,6 +393,7 @@ class Matcher:
                  stream=None):
         """Pairs (scan k, scan k+1) of a CUDA sequence [S, N, N] (masks per scan or None):
         S-1 result records, each scan's rotation spectrum computed once."""
+        scans, masks = _as_tensor(scans), _as_tensor(masks)
         import torch
         s = int(scans.shape[0])
         if out is None:
@@ -384,6 +407,7 @@ class Matcher:
         """Exhaustive search over the theta candidates (oracle.cpp:40-67) for a batch
         of CUDA pairs [B, N, N]; returns a uint8 device buffer of BF_DTYPE records
         (decode with decode_bf_results)."""
+        f, g = _as_tensor(f), _as_tensor(g)
         import torch
         b = int(f.shape[0])
         th = np.ascontiguousarray(np.asarray(thetas, dtype=np.float64).ravel())
@@ -395,6 +419,7 @@ class Matcher:
         return out
 
     def band_magnitude(self, img, *, stream=None):
+        img = _as_tensor(img)
         import torch
         b, n = int(img.shape[0]), int(img.shape[1])
         out = torch.empty((b, n, n // 2), dtype=torch.float32, device=img.device)
@@ -547,6 +572,67 @@ def brute_force_match(f, g, thetas, delta: float, config: MatchConfig | None = N
     gt = torch.as_tensor(np.ascontiguousarray(g, dtype=np.float32)).to(dev)[None]
     r = decode_bf_results(m.brute_force(ft, gt, thetas, delta=delta))[0]
     return OracleResult(Pose2D(float(r["theta"]), float(r["tx"]), float(r["ty"])), float(r["score"]), r)
+
+
+# ---------------------------------------------------------------- scan files (.fscn)
+
+def write_scan(path: str, grid, delta: float) -> None:
+    """write_scan of proj/src/io.cpp:84-101 (float32 payload)."""
+    g = np.ascontiguousarray(grid, dtype=np.float32)
+    err = C.create_string_buffer(512)
+    st = lib().fscan_fscn_write(os.fsencode(path), g.ctypes.data, int(g.shape[0]), float(delta), err, 512)
+    if st != OK:
+        _raise(st, err.value.decode() or f"{path}: write failed")
+
+
+def read_scans(paths, *, threads: int = 0, pinned: bool = False):
+    """Read .fscn files (all one grid size) concurrently into one float32 buffer:
+    ([B, N, N] numpy array, or a pinned torch tensor for fast H2D, deltas [B])."""
+    paths = [os.fsencode(p) for p in paths]
+    if not paths:
+        return np.zeros((0, 0, 0), np.float32), np.zeros(0)
+    n, delta, err = C.c_int(), C.c_double(), C.create_string_buffer(1024)
+    st = lib().fscan_fscn_read_header(paths[0], C.byref(n), C.byref(delta), err, 1024)
+    if st != OK:
+        _raise(st, err.value.decode())
+    shape = (len(paths), n.value, n.value)
+    if pinned:
+        import torch
+        buf = torch.empty(shape, dtype=torch.float32, pin_memory=True)
+        ptr = buf.data_ptr()
+    else:
+        buf = np.empty(shape, np.float32)
+        ptr = buf.ctypes.data
+    deltas = np.empty(len(paths), np.float64)
+    arr = (C.c_char_p * len(paths))(*paths)
+    st = lib().fscan_fscn_read_batch(arr, len(paths), n.value, ptr, deltas.ctypes.data, int(threads), err, 1024)
+    if st != OK:
+        _raise(st, err.value.decode())
+    return buf, deltas
+
+
+def odometry_files(paths, config: MatchConfig | None = None):
+    """The odometry command's ingestion + matching (tools/main.cpp:104-135): sorted
+    .fscn paths -> (absolute poses, per-pair records). Files are read in parallel
+    into pinned memory and copied to the device once."""
+    import torch
+    paths = sorted(paths)
+    if len(paths) < 2:
+        _raise(ERR_INVALID_ARGUMENT, f"odometry: need at least 2 scans, found {len(paths)}")
+    buf, deltas = read_scans(paths, pinned=True)
+    n, delta = int(buf.shape[1]), float(deltas[0])
+    cfg = MatchConfig(**(config or MatchConfig(n_xy=n, delta_xy=delta, n_radius=0)).__dict__).finalize()
+    cfg.validate()
+    m = Matcher(cfg, max_batch=len(paths) - 1)
+    scans = buf.to(torch.device("cuda", m.device), non_blocking=True)
+    res = decode_results(m.odometry(scans, None, delta=delta))
+    bad = np.nonzero(res["status"] != OK)[0]
+    if bad.size:
+        _raise(int(res["status"][bad[0]]), f"odometry: pair {int(bad[0])} rejected")
+    poses = [Pose2D()]
+    for r in res:
+        poses.append(compose(poses[-1], inverse(Pose2D(float(r["theta"]), float(r["tx"]), float(r["ty"])))))
+    return poses, res
 
 
 # ---------------------------------------------------------------- synthetic inputs

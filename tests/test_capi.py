@@ -5,6 +5,7 @@ import math
 import os
 import re
 
+import numpy as np
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -16,17 +17,18 @@ def declared_functions(header):
     return sorted(set(re.findall(r"\b(fscan_[a-z0-9_]+)\s*\(", text)))
 
 
-@pytest.mark.parametrize("header", ["fscan_cuda.h", "fscan_synth.h"])
+@pytest.mark.parametrize("header", ["fscan_cuda.h", "fscan_synth.h", "fscan_io.h"])
 def test_library_exports_every_declared_symbol(fb, header):
     names = declared_functions(header)
-    assert len(names) >= 5
+    assert len(names) >= 3
     lib = C.CDLL(fb.LIB_PATH)
     missing = [n for n in names if not hasattr(lib, n)]
     assert not missing, missing
 
 
 def test_python_binding_covers_the_header(fb):
-    names = set(declared_functions("fscan_cuda.h")) | set(declared_functions("fscan_synth.h"))
+    names = set(declared_functions("fscan_cuda.h")) | set(declared_functions("fscan_synth.h")) | \
+        set(declared_functions("fscan_io.h"))
     assert names <= set(fb.SYMBOLS), names - set(fb.SYMBOLS)
 
 
@@ -36,7 +38,9 @@ def test_drop_in_cpp_symbols_exported(fb):
     for sym in ("fscan::scan_match(fscan::ScanGrid const&, fscan::ScanGrid const&, fscan::MatchConfig const&)",
                 "fscan::estimate_rotation(", "fscan::estimate_translation(", "fscan::soft_argmax(",
                 "fscan::finalize(fscan::MatchConfig&)", "fscan::validate(fscan::MatchConfig const&)",
-                "fscan::scan_match_batch("):
+                "fscan::scan_match_batch(", "fscan::brute_force_match(", "fscan::timing_comparison(",
+                "fscan::kitti_drift(", "fscan::integrate(", "fscan::odometry(", "fscan::read_scan(",
+                "fscan::write_scan(", "fscan::read_scans_f32("):
         assert sym in out, sym
 
 
@@ -106,3 +110,45 @@ def test_shard_ranges_cover_and_partition():
             for (f0, c0), (f1, _) in zip(spans, spans[1:]):
                 assert f0 + c0 == f1
             assert max(c for _, c in spans) - min(c for _, c in spans) <= 1
+
+
+# ---- .fscn ingestion (proj/src/io.cpp:84-131, proj/tests/test_io.cpp:33-61); CPU only ----
+
+def test_fscn_round_trip_and_layout(fb, tmp_path):  # test_io.cpp:33-45
+    rng = np.random.default_rng(99)
+    a = (np.floor(rng.random((17, 17)) * 4096.0) / 256.0).astype(np.float32)  # exact in f32
+    path = str(tmp_path / "roundtrip.fscn")
+    fb.write_scan(path, a, 0.25)
+    assert os.path.getsize(path) == 16 + 17 * 17 * 4
+    b, d = fb.read_scans([path])
+    assert b.shape == (1, 17, 17) and d[0] == 0.25
+    np.testing.assert_array_equal(a, b[0])
+
+
+def test_fscn_reader_rejects_malformed_files(fb, tmp_path):  # test_io.cpp:47-61
+    bad = tmp_path / "bad_magic.fscn"
+    bad.write_bytes(b"PNGX0000000000000000")
+    with pytest.raises(fb.FscanError, match="bad magic"):
+        fb.read_scans([str(bad)])
+    tr = str(tmp_path / "truncated.fscn")
+    fb.write_scan(tr, np.ones((17, 17), np.float32), 0.25)
+    with open(tr, "r+b") as fh:
+        fh.truncate(16 + 40)
+    with pytest.raises(fb.FscanError, match="truncated"):
+        fb.read_scans([tr])
+    with pytest.raises(fb.FscanError, match="cannot open"):
+        fb.read_scans([str(tmp_path / "does_not_exist.fscn")])
+
+
+def test_fscn_batch_reads_many_files_in_order(fb, tmp_path):
+    grids = [np.full((8, 8), k, np.float32) for k in range(40)]
+    paths = []
+    for k, g in enumerate(grids):
+        paths.append(str(tmp_path / f"s{k:03d}.fscn"))
+        fb.write_scan(paths[-1], g, 0.5)
+    buf, deltas = fb.read_scans(paths, threads=7)
+    assert buf.shape == (40, 8, 8) and (deltas == 0.5).all()
+    assert all((buf[k] == k).all() for k in range(40))
+    fb.write_scan(str(tmp_path / "odd.fscn"), np.zeros((4, 4), np.float32), 0.5)
+    with pytest.raises(fb.FscanError, match="grid size"):
+        fb.read_scans(paths + [str(tmp_path / "odd.fscn")])

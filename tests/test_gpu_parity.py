@@ -499,3 +499,36 @@ def test_odometry_on_generated_drive_recovers_relative_poses(fb, dev):
         ok += abs(odo[k]["theta"] - rel.theta) <= 2 * cfg.delta_theta and \
             abs(odo[k]["tx"] - rel.tx) <= 2 * delta and abs(odo[k]["ty"] - rel.ty) <= 2 * delta
     assert ok >= 4, (odo[["theta", "tx", "ty"]], truth)
+
+
+class _DLPackOnly:
+    """A foreign CUDA array: only the DLPack protocol (like CuPy / JAX arrays)."""
+
+    def __init__(self, t):
+        self._t = t
+
+    def __dlpack__(self, stream=None):
+        return self._t.__dlpack__()
+
+    def __dlpack_device__(self):
+        return self._t.__dlpack_device__()
+
+
+def test_fscn_files_to_trajectory_and_dlpack_inputs(fb, dev, tmp_path):
+    """.fscn ingestion (io.cpp format, tools/main.cpp:104-135) gives the same
+    odometry as the in-memory sequence; DLPack-only arrays are accepted zero-copy."""
+    cfg, delta, _ = fb.baseline_config(2)
+    spec = fb.synth_spec(2)
+    scans, _, _ = fb.synth_sequence_device(spec, 11, 5)
+    host = scans.cpu().numpy()
+    paths = []
+    for k in range(5):
+        paths.append(str(tmp_path / f"scan_{k:04d}.fscn"))
+        fb.write_scan(paths[-1], host[k], delta)
+    poses_f, res_f = fb.odometry_files(list(reversed(paths)), cfg)  # sorted inside
+    m = fb.Matcher(cfg, max_batch=4)
+    res_m = fb.decode_results(m.odometry(_DLPackOnly(scans), None, delta=delta))
+    np.testing.assert_array_equal(res_f["theta_bin"], res_m["theta_bin"])
+    np.testing.assert_array_equal(res_f["xy_row"], res_m["xy_row"])
+    np.testing.assert_allclose(res_f["theta"], res_m["theta"], rtol=0, atol=1e-12)
+    assert len(poses_f) == 5
