@@ -184,6 +184,14 @@ fscan_status fscan_check_results(const fscan_pair_result* d_out, int batch, void
 /* Number of kernels the last fscan_match_batch launched (for bench accounting). */
 int fscan_ctx_launches_last(const fscan_ctx* ctx);
 
+/* Opt-in phase correlation (no reference code): the translation
+ * stage normalises the cross-power spectrum, X / |X| (0 where X = 0), before
+ * the inverse, sharpening the xy surface to a delta-like peak. The transform
+ * is the GPU's length-3N/2 circular correlation (DESIGN.md §3.8 — the
+ * normalisation, unlike the plain correlation, depends on that size). Off by
+ * default; applies to every later call on the context. */
+fscan_status fscan_ctx_set_phase_correlation(fscan_ctx* ctx, int on);
+
 /* Profiling mode: subsequent calls run their chunks serially on one stream
  * with CUDA events around every kernel. fscan_ctx_kernel_times() synchronises
  * and returns, per kernel kind (0 rot_rows, 1 rot_cols, 2 rot_polar,

@@ -99,6 +99,11 @@ def lib(which: str = "oracle") -> C.CDLL:
         L.fo_brute_force.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int, C.c_double,
                                      C.POINTER(C.c_double), C.c_int, C.POINTER(FoBfResult)]
         L.fo_brute_force.restype = C.c_int
+        L.fo_estimate_translation_ex.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int, C.c_double,
+                                                 C.c_double, C.POINTER(FoConfig), C.c_int, C.c_int,
+                                                 C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                                 C.POINTER(C.c_double)]
+        L.fo_estimate_translation_ex.restype = C.c_int
     else:
         L.ref_brute_force.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int, C.c_double,
                                       C.POINTER(C.c_double), C.c_int, C.POINTER(FoBfResult), C.c_char_p,
@@ -210,6 +215,20 @@ def brute_force(f, g, thetas, delta: float, which: str = "oracle") -> FoBfResult
         if rc != 0:
             raise OracleError(err.value.decode())
     return res
+
+
+def estimate_translation_ex(f, g, theta, cfg: FoConfig, delta: float, pad_size: int = 0, phase: bool = False):
+    """Translation stage with padded size pad_size (0: the reference's) and optional
+    phase correlation (restatement only): (tx, ty, surface)."""
+    L = lib("oracle")
+    n = int(f.shape[0])
+    f = np.ascontiguousarray(f, dtype=np.float64)
+    g = np.ascontiguousarray(g, dtype=np.float64)
+    s = np.zeros((n, n))
+    tx, ty = C.c_double(), C.c_double()
+    L.fo_estimate_translation_ex(_p(f), _p(g), n, delta, float(theta), C.byref(cfg), int(pad_size), int(phase),
+                                 C.byref(tx), C.byref(ty), _p(s))
+    return tx.value, ty.value, s
 
 
 def band_magnitude(img, band_lo, band_hi, which="oracle"):

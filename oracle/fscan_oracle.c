@@ -179,7 +179,10 @@ static void dft2_magnitude(const double* g, int n, double* mag) {
 }
 
 /* spectral.cpp:119-153: c[k] = sum_x a[x] b[x+k], zero lag at (rows/2, cols/2) */
-int fo_xcorr(const double* a, const double* b, int rows, int cols, double* out) {
+/* phase != 0: the normalised cross-power X/|X| (0 where X = 0) before the
+ * inverse — the opt-in phase correlation of SURVEY a21 (no reference code;
+ * own spec). */
+static int xcorr_impl(const double* a, const double* b, int rows, int cols, int phase, double* out) {
     const size_t sz = (size_t)rows * cols;
     cplx* fa = (cplx*)malloc(sizeof(cplx) * sz);
     cplx* buf = (cplx*)malloc(sizeof(cplx) * sz);
@@ -187,7 +190,13 @@ int fo_xcorr(const double* a, const double* b, int rows, int cols, double* out) 
     fft64_exec_2d(rows, cols, (double*)fa, -1);
     for (size_t i = 0; i < sz; ++i) buf[i] = b[i];
     fft64_exec_2d(rows, cols, (double*)buf, -1);
-    for (size_t i = 0; i < sz; ++i) buf[i] *= conj(fa[i]);
+    for (size_t i = 0; i < sz; ++i) {
+        buf[i] *= conj(fa[i]);
+        if (phase) {
+            const double m = cabs(buf[i]);
+            buf[i] = m > 0.0 ? buf[i] / m : 0.0;
+        }
+    }
     fft64_exec_2d(rows, cols, (double*)buf, +1);
     const double scale = 1.0 / ((double)rows * cols);
     const int hr = rows / 2, hc = cols / 2;
@@ -199,6 +208,10 @@ int fo_xcorr(const double* a, const double* b, int rows, int cols, double* out) 
     free(fa);
     free(buf);
     return 0;
+}
+
+int fo_xcorr(const double* a, const double* b, int rows, int cols, double* out) {
+    return xcorr_impl(a, b, rows, cols, 0, out);
 }
 
 /* ---- matcher.cpp ---- */
@@ -341,6 +354,43 @@ int fo_estimate_translation(const double* f, const double* g, int n, double delt
     double sy, sx;
     fo_soft_argmax(s, n, n, rc, cc, cfg->t_xy, cfg->softargmax_window, cfg->normalize_scores, &sy, &sx);
     /* rotate_vec, geometry.cpp:31-35 */
+    const double c = cos(theta), sn = sin(theta);
+    *tx = c * sx - sn * sy;
+    *ty = sn * sx + c * sy;
+    if (!surface) free(s);
+    free(gr); free(fp); free(gp); free(raw); free(rc); free(cc);
+    return 0;
+}
+
+/* Translation stage with a chosen padded size P (0: next_fast_size(2n-1), the
+ * reference) and optional phase correlation; surface and soft-argmax as
+ * estimate_translation (matcher.cpp:155-187). The GPU correlates on
+ * P = 3n/2, which equals the reference's linear correlation on the kept lags
+ * but not under the (size-dependent) phase normalisation: its phase-correlation
+ * parity is against P = 3n/2 here. */
+int fo_estimate_translation_ex(const double* f, const double* g, int n, double delta, double theta,
+                               const fo_config* cfg, int pad_size, int phase, double* tx, double* ty,
+                               double* surface) {
+    const size_t nn = (size_t)n * n;
+    double* gr = (double*)malloc(sizeof(double) * nn);
+    fo_rotate_bilinear(g, n, -theta, gr);
+    const int big = pad_size > 0 ? pad_size : fo_next_fast_size(2 * n - 1);
+    double* fp = zero_pad(f, n, big);
+    double* gp = zero_pad(gr, n, big);
+    double* raw = (double*)malloc(sizeof(double) * (size_t)big * big);
+    xcorr_impl(fp, gp, big, big, phase, raw);
+    const int h = big / 2, half = (n - 1) / 2;
+    double* s = surface ? surface : (double*)malloc(sizeof(double) * nn);
+    double* rc = (double*)malloc(sizeof(double) * n);
+    double* cc = (double*)malloc(sizeof(double) * n);
+    for (int i = 0; i < n; ++i) {
+        const int off_y = i - half;
+        for (int j = 0; j < n; ++j) s[(size_t)i * n + j] = raw[(size_t)(h - off_y) * big + h + (j - half)];
+        rc[i] = off_y * delta;
+    }
+    for (int j = 0; j < n; ++j) cc[j] = (j - half) * delta;
+    double sy, sx;
+    fo_soft_argmax(s, n, n, rc, cc, cfg->t_xy, cfg->softargmax_window, cfg->normalize_scores, &sy, &sx);
     const double c = cos(theta), sn = sin(theta);
     *tx = c * sx - sn * sy;
     *ty = sn * sx + c * sy;

@@ -130,6 +130,7 @@ SYMBOLS = {
     "fscan_check_results": (C.c_int, [_P, C.c_int, _P, C.POINTER(C.c_int)]),
     "fscan_ctx_launches_last": (C.c_int, [_P]),
     "fscan_ctx_set_profiling": (C.c_int, [_P, C.c_int]),
+    "fscan_ctx_set_phase_correlation": (C.c_int, [_P, C.c_int]),
     "fscan_ctx_kernel_times": (C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_int), C.c_int]),
     "fscan_fscn_read_header": (C.c_int, [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_double), C.c_char_p,
                                          C.c_size_t]),
@@ -304,6 +305,10 @@ class Matcher:
 
     KERNELS = ("rot_rows", "rot_cols", "rot_polar", "theta_in", "xlat_rows", "xlat_cols", "xlat_out",
                "finalize", "rot_gather", "polar_to_cart", "mag_unpack", "bf_items", "bf_final")
+
+    def set_phase_correlation(self, on: bool):
+        """Opt-in phase correlation in the translation stage (fscan_cuda.h)."""
+        self._check(lib().fscan_ctx_set_phase_correlation(self._h, int(bool(on))), "set_phase_correlation")
 
     def set_profiling(self, on: bool):
         self._check(lib().fscan_ctx_set_profiling(self._h, int(bool(on))), "set_profiling")

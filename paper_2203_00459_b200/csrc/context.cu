@@ -58,6 +58,7 @@ struct fscan_ctx {
     int alloc_chunk = 0; // workspace capacity (pairs)
     int n_live = 0;
     int rot_col_blocks = 0;  // K1b column blocks (8 columns each) the polar taps read
+    int phase = 0;           // opt-in phase correlation in the translation stage
     // brute-force search scratch (grown on demand)
     double* bf_thetas = nullptr;
     int bf_theta_cap = 0;
@@ -278,6 +279,7 @@ Params base_params(fscan_ctx* ctx, Lane& l, int batch, double delta) {
     p.n_live = ctx->n_live;
     p.zcols = 8 * ctx->rot_col_blocks;
     p.src_div = 1;
+    p.phase = ctx->phase;
     p.n_theta = ctx->cfg.n_theta;
     p.pad = ctx->cfg.pad_angle;
     p.L = ctx->cfg.n_theta + 2 * ctx->cfg.pad_angle;
@@ -876,6 +878,13 @@ fscan_status fscan_match_batch_host(fscan_ctx* ctx, const float* f, const float*
                         bad == FSCAN_ERR_MASK_RANGE ? "MaskGrid: values must lie in [0, 1]"
                                                     : "scan_match: input grids contain non-finite values");
         }
+    return FSCAN_OK;
+}
+
+fscan_status fscan_ctx_set_phase_correlation(fscan_ctx* ctx, int on) {
+    if (!ctx) return FSCAN_ERR_INVALID_ARGUMENT;
+    std::lock_guard<std::mutex> g(ctx->mu);
+    ctx->phase = on ? 1 : 0;
     return FSCAN_OK;
 }
 

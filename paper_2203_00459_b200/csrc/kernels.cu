@@ -681,6 +681,14 @@ __global__ void __launch_bounds__(XColGeom<N>::THREADS) k_xlat_cols(Params p) {
     fft_regs<K, -1, true>(a, t, bufB, p.tw_k);
 #pragma unroll
     for (int m = 0; m < 16; ++m) a[m] = cmul(cconj(bufA.get(t + m * T)), a[m]);  // conj(F) G
+    if (p.phase) {  // opt-in phase correlation: X / |X| (0 where X = 0), SURVEY a21
+#pragma unroll
+        for (int m = 0; m < 16; ++m) {
+            const float mag = sqrtf(a[m].x * a[m].x + a[m].y * a[m].y);
+            const float inv = mag > 0.0f ? 1.0f / mag : 0.0f;
+            a[m] = make_float2(a[m].x * inv, a[m].y * inv);
+        }
+    }
     fft_regs<K, +1, true>(a, t, bufB, p.tw_k);
 #pragma unroll
     for (int m = 0; m < 16; ++m) bufB.put(t + m * T, a[m]);

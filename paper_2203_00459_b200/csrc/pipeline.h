@@ -80,6 +80,7 @@ struct Params {
     // theta_in[(item_base + i) % theta_mod]
     int item_base, src_div, theta_mod;
     int skip_surface;         // K5 keeps only the block argmaxes (brute-force search)
+    int phase;                // opt-in phase correlation (K4 normalises the cross-power)
     // chain mode (odometry): pair k registers scan k against scan k+1 of one
     // sequence f (masks mf); K1a/K1b run once per two scans (n_scans of them in
     // this launch), the masked scans go to ft[scan], the magnitude planes and

@@ -532,3 +532,29 @@ def test_fscn_files_to_trajectory_and_dlpack_inputs(fb, dev, tmp_path):
     np.testing.assert_array_equal(res_f["xy_row"], res_m["xy_row"])
     np.testing.assert_allclose(res_f["theta"], res_m["theta"], rtol=0, atol=1e-12)
     assert len(poses_f) == 5
+
+
+def test_phase_correlation_matches_restatement(fb, orc, dev):
+    """Opt-in phase correlation (own spec): GPU vs the fp64 restatement
+    on the same 3N/2 transform; peak cell equal, surfaces within 1e-3 of the peak."""
+    cfg, delta, _ = fb.baseline_config(2)
+    f, g, mf, mg, _ = fb.synth_pairs_host(fb.synth_spec(2), 80, 3)
+    oc = oracle_cfg(orc, cfg)
+    n = cfg.n_xy
+    m = fb.Matcher(cfg, max_batch=3)
+    m.set_phase_correlation(True)
+    F, G = to_dev(dev, f, g)
+    theta = torch.tensor([0.02, -0.01, 0.0], dtype=torch.float64, device=dev)
+    xs = torch.zeros((3, n, n), dtype=torch.float32, device=dev)
+    txy = m.estimate_translation(F, G, theta, delta=delta, xy_surface=xs).cpu().numpy()
+    xs = xs.cpu().numpy()
+    for i in range(3):
+        tx, ty, s = orc.estimate_translation_ex(f[i].astype(np.float64), g[i].astype(np.float64),
+                                                float(theta[i]), oc, delta, 3 * n // 2, True)
+        assert np.unravel_index(np.argmax(xs[i]), xs[i].shape) == np.unravel_index(np.argmax(s), s.shape)
+        assert np.abs(xs[i] - s).max() <= 1e-3 * s.max()
+        assert abs(txy[i, 0] - tx) < PX_TOL * delta and abs(txy[i, 1] - ty) < PX_TOL * delta
+    m.set_phase_correlation(False)  # back to the reference's plain correlation
+    plain = m.estimate_translation(F, G, theta, delta=delta).cpu().numpy()
+    tx0, ty0, _ = orc.estimate_translation_ex(f[0].astype(np.float64), g[0].astype(np.float64), 0.02, oc, delta)
+    assert abs(plain[0, 0] - tx0) < PX_TOL * delta

@@ -289,3 +289,19 @@ def test_brute_force_restatement_bit_exact_vs_reference(orc, n):
     b = orc.brute_force(f, g, thetas, 0.4, which="ref")
     assert (a.theta, a.tx, a.ty, a.score) == (b.theta, b.tx, b.ty, b.score)
     assert (a.theta_index, a.xy_row, a.xy_col) == (b.theta_index, b.xy_row, b.xy_col)
+
+
+def test_restatement_three_halves_padding_equals_reference_size(orc):
+    """The GPU's length-3N/2 circular correlation equals the reference's
+    next_fast_size(2N-1) zero-padded one on every kept lag."""
+    n = 64
+    rng = np.random.default_rng(3)
+    f = rng.random((n, n))
+    g = np.roll(f, (2, -3), (0, 1)) + 0.1 * rng.random((n, n))
+    cfg = orc.make_config(n_xy=n, delta_xy=0.4, n_theta=90, delta_theta=math.pi / 90, n_radius=0, pad_angle=-1,
+                          band_lo=0.15)
+    orc.finalize(cfg)
+    a = orc.estimate_translation_ex(f, g, 0.1, cfg, 0.4, 0, False)
+    b = orc.estimate_translation_ex(f, g, 0.1, cfg, 0.4, 3 * n // 2, False)
+    assert np.abs(a[2] - b[2]).max() <= 1e-12 * np.abs(a[2]).max()
+    assert abs(a[0] - b[0]) < 1e-12 and abs(a[1] - b[1]) < 1e-12
