@@ -262,6 +262,17 @@ __device__ __forceinline__ float2 twiddle(const float2* __restrict__ tw, int idx
     return SIGN < 0 ? w : make_float2(w.x, -w.y);
 }
 
+// A twiddle table staged in shared memory (plain 64-bit shared loads).
+struct SmemTw {
+    const float2* p;
+};
+
+template <int SIGN>
+__device__ __forceinline__ float2 twiddle(const SmemTw& tw, int idx) {
+    const float2 w = tw.p[idx];
+    return SIGN < 0 ? w : make_float2(w.x, -w.y);
+}
+
 // One Stockham stage. Ns = span before this stage, R = radix.
 // Exchange barrier: a warp barrier when every thread of the transform (and of
 // any transform sharing its buffer) is in one warp, else the CTA barrier.
@@ -274,8 +285,8 @@ __device__ __forceinline__ void exchange_sync() {
     }
 }
 
-template <int N, int R, int Ns, bool LAST, int SIGN, bool WARP, typename L>
-__device__ __forceinline__ void stage(float2 (&v)[16], int t, const L& lay, const float2* __restrict__ tw) {
+template <int N, int R, int Ns, bool LAST, int SIGN, bool WARP, typename L, typename TW>
+__device__ __forceinline__ void stage(float2 (&v)[16], int t, const L& lay, const TW& tw) {
     constexpr int T = N / 16;
     constexpr int NB = 16 / R;
 #pragma unroll
@@ -312,8 +323,8 @@ __device__ __forceinline__ void stage(float2 (&v)[16], int t, const L& lay, cons
 // caller guarantees the transform's threads and exchange buffer live in one
 // warp (row layouts with T <= 32), so the exchanges need only __syncwarp;
 // otherwise every thread of the CTA must call fft_regs the same number of times.
-template <int N, int SIGN, bool WARP = false, typename L>
-__device__ __forceinline__ void fft_regs(float2 (&v)[16], int t, const L& lay, const float2* __restrict__ tw) {
+template <int N, int SIGN, bool WARP = false, typename L, typename TW>
+__device__ __forceinline__ void fft_regs(float2 (&v)[16], int t, const L& lay, const TW& tw) {
     static_assert(N >= 16 && (N & (N - 1)) == 0, "power-of-two length >= 16");
     static_assert(!WARP || N / 16 <= 32, "a warp-synchronous transform fits in one warp");
     if constexpr (N == 16) {

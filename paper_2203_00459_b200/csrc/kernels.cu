@@ -639,7 +639,10 @@ struct XColGeom {
     using G = fscan_fft::GeomSoA<N / 2, THREADS>;
     static constexpr size_t FFT_FLOATS = (size_t)2 * G::FLOATS;
     static constexpr size_t TILE_FLOATS = (size_t)2 * N * PITCH;
-    static constexpr size_t SMEM = (FFT_FLOATS > TILE_FLOATS ? FFT_FLOATS : TILE_FLOATS) * sizeof(float);
+    static constexpr size_t WORK_FLOATS = FFT_FLOATS > TILE_FLOATS ? FFT_FLOATS : TILE_FLOATS;
+    // twiddle tables staged behind the work area: W_K (K entries) and W_M (3K)
+    static constexpr size_t TW_FLOATS = (size_t)2 * (N / 2) * 4;
+    static constexpr size_t SMEM = (WORK_FLOATS + TW_FLOATS) * sizeof(float);
 };
 
 template <int N>
@@ -659,6 +662,14 @@ __global__ void __launch_bounds__(XColGeom<N>::THREADS) k_xlat_cols(Params p) {
     const auto bufA = G::lay(smem, tr);
     const auto bufB = G::lay(smem + G::FLOATS, tr);
     const float4* src = p.fgt + ((size_t)pair * (H + 1) + kq) * N;
+    // stage the twiddle tables in shared memory (latency: the FFT stages and
+    // input/combine twiddles read them ~90 times per thread)
+    float2* stw_k = reinterpret_cast<float2*>(smem + X::WORK_FLOATS);
+    float2* stw_m = stw_k + K;
+    for (int i = threadIdx.x; i < K; i += X::THREADS) stw_k[i] = __ldg(p.tw_k + i);
+    for (int i = threadIdx.x; i < M; i += X::THREADS) stw_m[i] = __ldg(p.tw_m + i);
+    __syncthreads();
+    const fscan_fft::SmemTw twk{stw_k};
     const float2 w3q = w3(q);
     float2 a[16];
 #pragma unroll
@@ -666,9 +677,9 @@ __global__ void __launch_bounds__(XColGeom<N>::THREADS) k_xlat_cols(Params p) {
         const int n0 = t + m * T;
         const float4 u0 = src[n0], u1 = src[n0 + K];
         const float2 s = cadd(make_float2(u0.x, u0.y), cmul(w3q, make_float2(u1.x, u1.y)));
-        a[m] = q ? cmul(wm(p.tw_m, n0 * q), s) : s;
+        a[m] = q ? cmul(stw_m[n0 * q], s) : s;
     }
-    fft_regs<K, -1, true>(a, t, bufA, p.tw_k);  // transforms of a warp share a buffer group
+    fft_regs<K, -1, true>(a, t, bufA, twk);  // transforms of a warp share a buffer group
 #pragma unroll
     for (int m = 0; m < 16; ++m) bufA.put(t + m * T, a[m]);  // park F_q (own slots)
 #pragma unroll
@@ -676,9 +687,9 @@ __global__ void __launch_bounds__(XColGeom<N>::THREADS) k_xlat_cols(Params p) {
         const int n0 = t + m * T;
         const float4 u0 = src[n0], u1 = src[n0 + K];
         const float2 s = cadd(make_float2(u0.z, u0.w), cmul(w3q, make_float2(u1.z, u1.w)));
-        a[m] = q ? cmul(wm(p.tw_m, n0 * q), s) : s;
+        a[m] = q ? cmul(stw_m[n0 * q], s) : s;
     }
-    fft_regs<K, -1, true>(a, t, bufB, p.tw_k);
+    fft_regs<K, -1, true>(a, t, bufB, twk);
 #pragma unroll
     for (int m = 0; m < 16; ++m) a[m] = cmul(cconj(bufA.get(t + m * T)), a[m]);  // conj(F) G
     if (p.phase) {  // opt-in phase correlation: X / |X| (0 where X = 0), SURVEY a21
@@ -689,7 +700,7 @@ __global__ void __launch_bounds__(XColGeom<N>::THREADS) k_xlat_cols(Params p) {
             a[m] = make_float2(a[m].x * inv, a[m].y * inv);
         }
     }
-    fft_regs<K, +1, true>(a, t, bufB, p.tw_k);
+    fft_regs<K, +1, true>(a, t, bufB, twk);
 #pragma unroll
     for (int m = 0; m < 16; ++m) bufB.put(t + m * T, a[m]);
     __syncthreads();
@@ -704,8 +715,8 @@ __global__ void __launch_bounds__(XColGeom<N>::THREADS) k_xlat_cols(Params p) {
         if (m < 16) {
             const int n0 = t + m * T;
             const float2 x0 = e0.get(n0);
-            const float2 x1 = cmul(cconj(wm(p.tw_m, n0)), e1.get(n0));
-            const float2 x2 = cmul(cconj(wm(p.tw_m, 2 * n0)), e2.get(n0));
+            const float2 x1 = cmul(cconj(stw_m[n0]), e1.get(n0));
+            const float2 x2 = cmul(cconj(stw_m[2 * n0]), e2.get(n0));
             accp[j] = cadd(x0, cadd(x1, x2));
             accn[j] = cadd(x0, cadd(cmul(w31, x1), cmul(w32, x2)));
         }
