@@ -13,9 +13,12 @@
  * paper_2203_00459_b200/csrc — there is no CPU fallback.
  *
  * Data layout: a batch of B pairs is B consecutive N x N row-major float32
- * grids per argument (f, g, mask_f, mask_g). Grid N must be a power of two in
- * [64, 1024] on this build (FSCAN_ERR_UNSUPPORTED otherwise; the reference
- * requires odd N, see SURVEY.md D1 and DESIGN.md §6).
+ * grids per argument (f, g, mask_f, mask_g). Any grid side N in [33, 1024] is
+ * supported (FSCAN_ERR_UNSUPPORTED otherwise): powers of two >= 64 take the
+ * radix fast path, other sides — including the reference's own odd sizes —
+ * use Bluestein DFTs in the rotation stage and a zero-embedded power-of-two
+ * translation stage. The exhaustive search and the odometry
+ * chain are power-of-two only.
  *
  * Errors: every call returns an fscan_status; fscan_ctx_last_error() gives the
  * message. The C++ drop-in maps FSCAN_ERR_INVALID_ARGUMENT, _NONFINITE and
@@ -132,7 +135,7 @@ fscan_status fscan_estimate_translation_batch(fscan_ctx* ctx, const float* d_f, 
 
 /* Stage-1 intermediate for parity tests: band-passed magnitude spectrum of
  * hann(img) on the half plane u >= 0, centred rows (matcher.cpp:113-126 /
- * spectral.cpp:73-117): d_out is batch x N x (N/2) floats, element
+ * spectral.cpp:73-117): d_out is batch x N x W floats, W = N - N/2, element
  * [v_c][u] = |dft2(hann * img)|[v_c][N/2 + u] * band[v_c][N/2 + u]. */
 fscan_status fscan_band_magnitude_batch(fscan_ctx* ctx, const float* d_img, int batch,
                                         float* d_out, void* stream);

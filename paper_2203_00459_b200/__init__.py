@@ -427,7 +427,7 @@ class Matcher:
         img = _as_tensor(img)
         import torch
         b, n = int(img.shape[0]), int(img.shape[1])
-        out = torch.empty((b, n, n // 2), dtype=torch.float32, device=img.device)
+        out = torch.empty((b, n, n - n // 2), dtype=torch.float32, device=img.device)  # u >= 0 half plane
         st = lib().fscan_band_magnitude_batch(self._h, _ptr(img), b, _ptr(out), _stream_ptr(stream))
         self._check(st, "fscan_band_magnitude_batch")
         return out

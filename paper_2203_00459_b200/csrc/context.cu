@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <complex>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -59,6 +60,16 @@ struct fscan_ctx {
     int n_live = 0;
     int rot_col_blocks = 0;  // K1b column blocks (8 columns each) the polar taps read
     int phase = 0;           // opt-in phase correlation in the translation stage
+    // grid geometry: np = n for powers of two; otherwise the
+    // rotation stage runs Bluestein DFTs of length bs_L at n and the
+    // translation stage runs at np = 2^k >= n + 1 on zero-embedded scans
+    int np = 0;
+    int bs_L = 0;
+    int nw = 0;               // half-plane width n - n/2
+    long long mag_plane = 0;  // float2 per (|F|,|G|) tile set
+    float2* bs_chirp = nullptr;
+    float2* bs_kern = nullptr;
+    float2* tw_L = nullptr;
     // brute-force search scratch (grown on demand)
     double* bf_thetas = nullptr;
     int bf_theta_cap = 0;
@@ -114,18 +125,38 @@ bool is_pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
 
 // bandpass_mask (imageops.cpp:44-59) restricted to the u >= 0 half plane:
 // per centred row, the interval of u in [0, n/2) inside the band.
+// In-place fp64 radix-2 FFT (forward, unnormalised) for the Bluestein kernel.
+void fft_inplace(std::vector<std::complex<double>>& a) {
+    const size_t n = a.size();
+    for (size_t i = 1, j = 0; i < n; ++i) {
+        size_t bit = n >> 1;
+        for (; j & bit; bit >>= 1) j ^= bit;
+        j ^= bit;
+        if (i < j) std::swap(a[i], a[j]);
+    }
+    for (size_t len = 2; len <= n; len <<= 1) {
+        for (size_t i = 0; i < n; i += len)
+            for (size_t k = 0; k < len / 2; ++k) {
+                const std::complex<double> w = std::polar(1.0, -2.0 * kPi * (double)k / (double)len);
+                const std::complex<double> u = a[i + k], v = a[i + k + len / 2] * w;
+                a[i + k] = u + v;
+                a[i + k + len / 2] = u - v;
+            }
+    }
+}
+
 bool build_band(int n, double lo, double hi, std::vector<int2>& out, std::vector<unsigned char>& inband) {
-    const int c = n / 2;
+    const int c = n / 2, W = n - n / 2;  // half plane: centred columns c .. n-1
     const double nyq = n / 2.0;
     out.assign(n, make_int2(1, 0));
-    inband.assign((size_t)n * (n / 2), 0);
+    inband.assign((size_t)n * W, 0);
     for (int i = 0; i < n; ++i) {
         int first = -1, last = -2;
-        for (int u = 0; u < n / 2; ++u) {
+        for (int u = 0; u < W; ++u) {
             const int j = c + u;
             const double rho = std::hypot(double(i - c), double(j - c)) / nyq;
             const bool in = (rho >= lo && rho <= hi);
-            inband[(size_t)i * (n / 2) + u] = in;
+            inband[(size_t)i * W + u] = in;
             if (in) {
                 if (first < 0) first = u;
                 else if (last != u - 1) return false;  // not an interval
@@ -149,7 +180,7 @@ bool build_taps(int n, const fscan_config& cfg, const std::vector<unsigned char>
     const double span = nt * cfg.delta_theta;
     const int c = n / 2;
     const double r_max = n / 2.0;
-    const int W = n / 2;
+    const int W = n - n / 2;  // half-plane width (n/2 for even n)
     std::vector<PolarTap> all((size_t)nt * nr);
     int jlo = nr, jhi = -1;
     *u_hi = 0;
@@ -231,13 +262,20 @@ void free_lane(Lane& l) {
 }
 
 fscan_status alloc_lane(fscan_ctx* ctx, Lane& l, int chunk) {
-    const size_t n = (size_t)ctx->n, nn = n * n;
-    const int nparts = ctx->n / rows_per_block_out(ctx->n);
-    CK(cudaMalloc(&l.ft, nn * sizeof(float) * chunk));
-    CK(cudaMalloc(&l.gt, nn * sizeof(float) * chunk));
-    CK(cudaMalloc(&l.zbuf, n * n * sizeof(float2) * chunk));
-    CK(cudaMalloc(&l.mag, nn * sizeof(float) * chunk));
-    CK(cudaMalloc(&l.fgt, (3 * n / 4 + 1) * n * sizeof(float4) * chunk));
+    const size_t n = (size_t)ctx->n, np = (size_t)ctx->np, npp = np * np;
+    const int nparts = ctx->np / rows_per_block_out(ctx->np);
+    // translation buffers at np (zero-embedded scans: the padding stays zero)
+    CK(cudaMalloc(&l.ft, npp * sizeof(float) * chunk));
+    CK(cudaMalloc(&l.gt, npp * sizeof(float) * chunk));
+    if (np != n) {
+        CK(cudaMemset(l.ft, 0, npp * sizeof(float) * chunk));
+        CK(cudaMemset(l.gt, 0, npp * sizeof(float) * chunk));
+    }
+    // zbuf: K1 spectra (n x n) then the K4 -> K5 rows (np x (3np/4 + 1))
+    CK(cudaMalloc(&l.zbuf, std::max(n * n, np * (3 * np / 4 + 1)) * sizeof(float2) * chunk));
+    // mag: the (|F|,|G|) tiles, later the np x np surface
+    CK(cudaMalloc(&l.mag, std::max((size_t)ctx->mag_plane * 2, npp) * sizeof(float) * chunk));
+    CK(cudaMalloc(&l.fgt, (3 * np / 4 + 1) * np * sizeof(float4) * chunk));
     CK(cudaMalloc(&l.part, sizeof(Partial) * nparts * chunk));
     CK(cudaMalloc(&l.rot, sizeof(RotState) * chunk));
     CK(cudaMalloc(&l.prof, sizeof(double) * 2 * std::max(1, ctx->cfg.n_theta) * chunk));
@@ -258,6 +296,16 @@ fscan_status alloc_host_staging(fscan_ctx* ctx, Lane& l, int chunk) {
 Params base_params(fscan_ctx* ctx, Lane& l, int batch, double delta) {
     Params p{};
     p.n = ctx->n;
+    p.np = ctx->np;
+    p.embed = ctx->np != ctx->n;
+    p.c0 = (float)((ctx->n - 1) / 2.0);
+    p.win_off = (ctx->np / 2 - 1) - (ctx->n - 1) / 2;
+    p.nw = ctx->nw;
+    p.mag_plane = ctx->mag_plane;
+    p.bs_L = ctx->bs_L;
+    p.bs_chirp = ctx->bs_chirp;
+    p.bs_kern = ctx->bs_kern;
+    p.tw_L = ctx->tw_L;
     p.batch = batch;
     p.ft = l.ft;
     p.gt = l.gt;
@@ -316,14 +364,17 @@ fscan_status run_chunk(fscan_ctx* ctx, Lane& l, Params p, Stages what, int* laun
     fscan_status st;
 #define FSCAN_LAUNCH(kid, call)                                                              \
     if ((st = launch(ctx, l, kid, [&] { return call(p, s); }, launches)) != FSCAN_OK) return st;
-    FSCAN_LAUNCH(kRotRows, launch_rot_rows);
+    // K1: power-of-two radix FFTs, or Bluestein DFTs for other sizes
+    auto k1a = ctx->bs_L ? launch_rot_rows_bs : launch_rot_rows;
+    auto k1b = ctx->bs_L ? launch_rot_cols_bs : launch_rot_cols;
+    FSCAN_LAUNCH(kRotRows, k1a);
     if (what == Stages::Magnitude) {
-        FSCAN_LAUNCH(kRotCols, launch_rot_cols);
+        FSCAN_LAUNCH(kRotCols, k1b);
         FSCAN_LAUNCH(kMagUnpack, launch_mag_unpack);
         return FSCAN_OK;
     }
     if (what != Stages::Translation) {
-        if (ctx->cfg.n_theta > 1) FSCAN_LAUNCH(kRotCols, launch_rot_cols);
+        if (ctx->cfg.n_theta > 1) FSCAN_LAUNCH(kRotCols, k1b);
         if (ctx->cfg.n_theta > 1) FSCAN_LAUNCH(kRotGather, launch_rot_gather);
         FSCAN_LAUNCH(kRotPolar, launch_rot_polar);
     } else {
@@ -457,8 +508,22 @@ fscan_status fscan_ctx_create(int device, const fscan_config* cfg_in, int max_ba
         return st;
     }
     *out = ctx;
-    if (!is_pow2(ctx->n) || ctx->n < 64 || ctx->n > 1024)
-        return fail(ctx, FSCAN_ERR_UNSUPPORTED, "n_xy must be a power of two in [64, 1024] on the GPU path");
+    {  // grid geometry: powers of two 64..1024 (fast path) or any other n in [33, 1023]
+        const int n = ctx->n;
+        int np = 64;
+        while (np < (is_pow2(n) ? n : n + 1)) np <<= 1;
+        if (n < 33 || n > 1024 || np > 1024)
+            return fail(ctx, FSCAN_ERR_UNSUPPORTED,
+                        "n_xy must lie in [33, 1024] on the GPU path (powers of two >= 64 take the fast path)");
+        ctx->np = np;
+        ctx->nw = n - n / 2;
+        ctx->mag_plane = (long long)n * 8 * ((ctx->nw + 7) / 8);
+        if (!is_pow2(n)) {
+            int L = 128;
+            while (L < 2 * n - 1) L <<= 1;
+            ctx->bs_L = L;
+        }
+    }
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
         return fail(ctx, FSCAN_ERR_NO_DEVICE, "no CUDA device " + std::to_string(device));
@@ -479,7 +544,9 @@ fscan_status fscan_ctx_create(int device, const fscan_config* cfg_in, int max_ba
         }
         return t;
     };
-    const std::vector<float2> tw = table(n), twk = table(n / 2), twk2 = table(n / 4), twm = table(3 * n / 2);
+    const int np = ctx->np;  // translation stage size
+    const std::vector<float2> tw = table(ctx->bs_L ? ctx->bs_L : n), twk = table(np / 2), twk2 = table(np / 4),
+                              twm = table(3 * np / 2);
     std::vector<float> hann(n, 1.0f);  // imageops.cpp:30-42
     if (n > 1)
         for (int i = 0; i < n; ++i) hann[i] = (float)(0.5 * (1.0 - std::cos(2.0 * kPi * i / (n - 1))));
@@ -492,13 +559,33 @@ fscan_status fscan_ctx_create(int device, const fscan_config* cfg_in, int max_ba
         std::string why;
         int u_hi = 0;
         if (!build_taps(n, cfg, inband, taps, &ctx->n_live, &u_hi, &why)) return fail(ctx, FSCAN_ERR_UNSUPPORTED, why);
-        ctx->rot_col_blocks = std::min(n / 16, u_hi / 8 + 1);
+        ctx->rot_col_blocks = std::min((ctx->nw + 7) / 8, u_hi / 8 + 1);
     } else {
         taps.resize(1);
         ctx->n_live = 1;
-        ctx->rot_col_blocks = n / 16;
+        ctx->rot_col_blocks = (ctx->nw + 7) / 8;
     }
-    CK(cudaMalloc(&ctx->tw_n, sizeof(float2) * n));
+    if (ctx->bs_L) {  // Bluestein tables (generic_n.cu): chirp w[k] and FFT_L(conj kernel) / L
+        const int L = ctx->bs_L;
+        std::vector<std::complex<double>> w(n), b(L, 0.0);
+        for (int k = 0; k < n; ++k) {
+            const long long e = (long long)k * k % (2LL * n);  // exact phase reduction
+            w[k] = std::polar(1.0, -kPi * (double)e / n);
+        }
+        for (int m = 0; m < n; ++m) {
+            b[m] = std::conj(w[m]);
+            if (m) b[L - m] = std::conj(w[m]);
+        }
+        fft_inplace(b);
+        std::vector<float2> chirp(n), kern(L);
+        for (int k = 0; k < n; ++k) chirp[k] = make_float2((float)w[k].real(), (float)w[k].imag());
+        for (int k = 0; k < L; ++k) kern[k] = make_float2((float)(b[k].real() / L), (float)(b[k].imag() / L));
+        CK(cudaMalloc(&ctx->bs_chirp, sizeof(float2) * n));
+        CK(cudaMalloc(&ctx->bs_kern, sizeof(float2) * L));
+        CK(cudaMemcpy(ctx->bs_chirp, chirp.data(), sizeof(float2) * n, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(ctx->bs_kern, kern.data(), sizeof(float2) * L, cudaMemcpyHostToDevice));
+    }
+    CK(cudaMalloc(&ctx->tw_n, sizeof(float2) * tw.size()));
     CK(cudaMalloc(&ctx->tw_k, sizeof(float2) * twk.size()));
     CK(cudaMalloc(&ctx->tw_k2, sizeof(float2) * twk2.size()));
     CK(cudaMalloc(&ctx->tw_m, sizeof(float2) * twm.size()));
@@ -508,7 +595,8 @@ fscan_status fscan_ctx_create(int device, const fscan_config* cfg_in, int max_ba
     CK(cudaMalloc(&ctx->hann, sizeof(float) * n));
     CK(cudaMalloc(&ctx->band, sizeof(int2) * n));
     CK(cudaMalloc(&ctx->taps, sizeof(PolarTap) * taps.size()));
-    CK(cudaMemcpy(ctx->tw_n, tw.data(), sizeof(float2) * n, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->tw_n, tw.data(), sizeof(float2) * tw.size(), cudaMemcpyHostToDevice));
+    ctx->tw_L = ctx->bs_L ? ctx->tw_n : nullptr;  // the length-L table for the Bluestein FFTs
     CK(cudaMemcpy(ctx->hann, hann.data(), sizeof(float) * n, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(ctx->band, band.data(), sizeof(int2) * n, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(ctx->taps, taps.data(), sizeof(PolarTap) * taps.size(), cudaMemcpyHostToDevice));
@@ -550,6 +638,8 @@ void fscan_ctx_destroy(fscan_ctx* ctx) {
     cudaFree(ctx->hann);
     cudaFree(ctx->band);
     cudaFree(ctx->taps);
+    cudaFree(ctx->bs_chirp);
+    cudaFree(ctx->bs_kern);
     cudaFree(ctx->bf_thetas);
     cudaFree(ctx->bf_items);
     delete ctx;
@@ -701,6 +791,8 @@ fscan_status fscan_brute_force_batch(fscan_ctx* ctx, const float* d_f, const flo
     if (!ctx->tw_n) return fail(ctx, FSCAN_ERR_INVALID_ARGUMENT, "context was not created successfully");
     if (!d_f || !d_g || !d_out || !(delta > 0.0))
         return fail(ctx, FSCAN_ERR_INVALID_ARGUMENT, "fscan_brute_force_batch: bad pointers or delta");
+    if (ctx->np != ctx->n)
+        return fail(ctx, FSCAN_ERR_UNSUPPORTED, "brute_force_match: power-of-two grids only on the GPU path");
     if (!thetas || nth < 1)  // oracle.cpp:46-47
         return fail(ctx, FSCAN_ERR_INVALID_ARGUMENT, "brute_force_match: empty theta candidate list");
     if ((long long)batch * nth > (1LL << 30))
@@ -763,6 +855,8 @@ fscan_status fscan_odometry_batch(fscan_ctx* ctx, const float* d_scans, const fl
     if (!ctx->tw_n) return fail(ctx, FSCAN_ERR_INVALID_ARGUMENT, "context was not created successfully");
     if (n_scans < 0 || !(delta > 0.0)) return fail(ctx, FSCAN_ERR_INVALID_ARGUMENT, "fscan_odometry_batch: bad count or delta");
     if (pairs <= 0) return FSCAN_OK;  // 0 or 1 scans: no pairs
+    if (ctx->np != ctx->n)
+        return fail(ctx, FSCAN_ERR_UNSUPPORTED, "fscan_odometry_batch: power-of-two grids only on the GPU path");
     if (!d_scans || !d_out) return fail(ctx, FSCAN_ERR_INVALID_ARGUMENT, "fscan_odometry_batch: bad pointers");
     const size_t nn = (size_t)ctx->n * ctx->n;
     const int nt = ctx->cfg.n_theta;
@@ -813,7 +907,7 @@ fscan_status fscan_band_magnitude_batch(fscan_ctx* ctx, const float* d_img, int 
         p.f = d_img + off * nn;
         p.g = d_img + off * nn;
         p.mag_out = d_out + off * (nn / 2);
-        p.zcols = ctx->n / 2;  // the whole half plane
+        p.zcols = ctx->nw;  // the whole half plane
         return run_chunk(ctx, l, p, Stages::Magnitude, &ctx->launches_last);
     });
 }

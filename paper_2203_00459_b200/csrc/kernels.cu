@@ -216,7 +216,7 @@ constexpr int kGatherThreads = 128;
 template <bool SPLIT>
 __device__ __forceinline__ void gather_sums(const Params& p, const float2* m, int i, double* prof) {
     const int nt = p.n_theta, n = p.n, n_live = p.n_live;
-    const float2* m2 = m + (size_t)n * (n / 2);
+    const float2* m2 = m + p.mag_plane;  // the next transform's tiles (chain mode)
     const PolarTap* col = p.taps + i;
     double af = 0.0, ag = 0.0;
     constexpr int U = 4;  // independent entries in flight per thread (memory-level parallelism)
@@ -255,13 +255,13 @@ __device__ __forceinline__ void gather_sums(const Params& p, const float2* m, in
 
 __global__ void __launch_bounds__(kGatherThreads) k_rot_gather(Params p) {
     const int pair = blockIdx.y;
-    const int nt = p.n_theta, n = p.n;
+    const int nt = p.n_theta;
     const int i = blockIdx.x * kGatherThreads + threadIdx.x;
     if (i >= nt) return;
     // the K1b transform holding the pair's |F| (and |G|): one per pair, or in
     // chain mode one per two scans of the sequence
     const int tr = p.chain ? pair / 2 : pair;
-    const float2* m = reinterpret_cast<const float2*>(p.mag) + (size_t)tr * n * (n / 2);
+    const float2* m = reinterpret_cast<const float2*>(p.mag) + (size_t)tr * p.mag_plane;
     double* prof = p.prof + (size_t)pair * 2 * nt;
     if (p.chain && (pair & 1))
         gather_sums<true>(p, m, i, prof);
@@ -513,7 +513,10 @@ struct XRowGeom {
 // Three CTAs per SM (56 registers): the gather is latency bound, occupancy
 // beats per-thread memory-level parallelism here (measured: 2 CTAs x 6 cells
 // in flight 8.1 ms, 3 CTAs x 4 cells 7.7 ms per 4096 C4 pairs).
-template <int N, bool MANY>
+// EMB: the scans are zero-embedded in the N x N (power-of-two) grid, valid
+// size p.n < N and rotation centre p.c0 (grid sides that are not powers of
+// two): g~r is zero outside the valid grid.
+template <int N, bool MANY, bool EMB>
 __global__ void __launch_bounds__(kXThreads, 3) k_xlat_rows(Params p) {
     constexpr int K = N / 2, M = 3 * K, H = M / 2;
     using X = XRowGeom<N>;
@@ -529,7 +532,8 @@ __global__ void __launch_bounds__(kXThreads, 3) k_xlat_rows(Params p) {
     const int src = MANY ? (p.item_base + pair) / p.src_div : pair;  // pair whose scans this item reads
     const float* ft = p.ft + (size_t)src * N * N;
     const float* gt = p.gt + (size_t)src * N * N;
-    const float c0f32 = (N - 1) / 2.0f;  // exact
+    const float c0f32 = EMB ? p.c0 : (N - 1) / 2.0f;  // exact (half-integer or integer)
+    const int nvalid = EMB ? p.n : N;
     // rotate_bilinear(g~, -theta); -theta == 0.0 returns g~ itself, which st = 0,
     // ct = 1 reproduce exactly (integer source coordinates, zero fractions)
     const float stf = rs.identity ? 0.0f : (float)rs.st, ctf = rs.identity ? 1.0f : (float)rs.ct;
@@ -544,9 +548,9 @@ __global__ void __launch_bounds__(kXThreads, 3) k_xlat_rows(Params p) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int e = e0 + u * kXThreads;
-            const bool live = e < CELLS;
             const int yl = e / N, x = e % N;
             const int y = y0 + yl;
+            const bool live = e < CELLS && (!EMB || (x < nvalid && y < nvalid));
             // src_row = c + st*u + ct*v, src_col = c + ct*u - st*v (imageops.cpp:70-73)
             // in fp32 FMAs: <= 5e-5 cell coordinate error, i.e. <= 5e-5 relative per
             // bilinear sample (far inside the 1e-4 surface gate)
@@ -760,7 +764,10 @@ struct XOutGeom {
     static constexpr size_t SMEM = (size_t)G::FLOATS * sizeof(float);
 };
 
-template <int N>
+// EMB: only the lag window [win_off, win_off + p.n)^2 of the embedded surface
+// competes for the argmax, and the surface stays in the workspace (K6 copies
+// the window out).
+template <int N, bool EMB>
 __global__ void __launch_bounds__(XOutGeom<N>::THREADS) k_xlat_out(Params p) {
     constexpr int K = N / 2, M = 3 * K, H = M / 2;
     using X = XOutGeom<N>;
@@ -798,13 +805,15 @@ __global__ void __launch_bounds__(XOutGeom<N>::THREADS) k_xlat_out(Params p) {
     }
     __syncthreads();
     const float scale = 1.0f / ((float)M * (float)M);
-    float* srow = (p.xy_surf ? p.xy_surf : p.surf) + ((size_t)pair * N + i) * N;
+    float* srow = ((p.xy_surf && !EMB) ? p.xy_surf : p.surf) + ((size_t)pair * N + i) * N;
+    const bool row_in = !EMB || (i >= p.win_off && i < p.win_off + p.n);
     float best_v = -INFINITY;
     int best_i = 0x7fffffff;
     auto emit = [&](int kx, float val) {
         const int j = kx + half;
         if (!p.skip_surface) srow[j] = val;
         const int li = i * N + j;
+        if (EMB && !(row_in && j >= p.win_off && j < p.win_off + p.n)) return;
         if (val > best_v || (val == best_v && li < best_i)) {
             best_v = val;
             best_i = li;
@@ -887,7 +896,7 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(Params p, int nparts) 
     __shared__ float pk_v;
     __shared__ int pk_i;
     const int pair = blockIdx.x;
-    const int n = p.n;
+    const int n = p.np;
     if (threadIdx.x == 0) {
         const Partial* pp = p.part + (size_t)pair * nparts;
         float bv = pp[0].val;
@@ -901,11 +910,14 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(Params p, int nparts) 
         pk_i = bi;
     }
     __syncthreads();
-    const float* surf = (p.xy_surf ? p.xy_surf : p.surf) + (size_t)pair * n * n;
+    // the surface is n x n (pitch n = np); embedded grids keep
+    // the reference's window of nv x nv lags at offset off
+    const int nv = p.embed ? p.n : n, off = p.embed ? p.win_off : 0;
+    const float* surf = ((p.xy_surf && !p.embed) ? p.xy_surf : p.surf) + (size_t)pair * n * n;
     const int pr = pk_i / n, pc = pk_i % n;
     const int w = p.window;
-    const int r0 = max(0, pr - w), r1 = min(n - 1, pr + w);
-    const int c0 = max(0, pc - w), c1 = min(n - 1, pc + w);
+    const int r0 = max(off, pr - w), r1 = min(off + nv - 1, pr + w);
+    const int c0 = max(off, pc - w), c1 = min(off + nv - 1, pc + w);
     const int wr = r1 - r0 + 1, wc = c1 - c0 + 1;
     double scale = 1.0;
     if (p.normalize) {
@@ -955,24 +967,29 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(Params p, int nparts) 
             o.xy_hard_y = (pr - half) * p.delta;
             o.xy_peak = (double)pk_v;
             o.theta_bin = rs.bin;
-            o.xy_row = pr;
-            o.xy_col = pc;
+            o.xy_row = pr - off;
+            o.xy_col = pc - off;
             const int fl = p.chain ? (p.flags[pair] | p.flags[pair + 1]) : p.flags[pair];
             o.status = (fl & 2) ? FSCAN_ERR_MASK_RANGE : ((fl & 1) ? FSCAN_ERR_NONFINITE : FSCAN_OK);
             p.out[pair] = o;
         }
     }
+    if (p.embed && p.xy_surf) {  // the reference's nv x nv lag window of the embedded surface
+        float* dst = p.xy_surf + (size_t)pair * nv * nv;
+        for (int q = threadIdx.x; q < nv * nv; q += kFinThreads)
+            dst[q] = surf[(size_t)(off + q / nv) * n + off + q % nv];
+    }
 }
 
 // band magnitude stage output: tiled [2][N/16][N][8] (f only) -> [N][N/2]
 __global__ void k_mag_unpack(Params p) {
-    const int n = p.n;
+    const int n = p.n, w = p.nw;  // half plane u < W = n - n/2
     const int pair = blockIdx.y;
     const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= (size_t)n * (n / 2)) return;
-    const int vc = (int)(idx / (n / 2)), u = (int)(idx % (n / 2));
-    const float2* m = reinterpret_cast<const float2*>(p.mag) + (size_t)pair * n * (n / 2);
-    p.mag_out[(size_t)pair * n * (n / 2) + idx] = tile_at(m, n, vc, u)->x;
+    if (idx >= (size_t)n * w) return;
+    const int vc = (int)(idx / w), u = (int)(idx % w);
+    const float2* m = reinterpret_cast<const float2*>(p.mag) + (size_t)pair * p.mag_plane;
+    p.mag_out[(size_t)pair * n * w + idx] = tile_at(m, n, vc, u)->x;
 }
 
 // K0 in two steps: the cell geometry (fp64 atan2 / sqrt, identical for every
@@ -1076,14 +1093,15 @@ cudaError_t rot_cols(const Params& p, cudaStream_t s) {
 template <int N>
 cudaError_t xlat_rows(const Params& p, cudaStream_t s) {
     using X = XRowGeom<N>;
-    const bool many = p.src_div != 1;
-    cudaError_t e = many ? set_smem(k_xlat_rows<N, true>, X::SMEM) : set_smem(k_xlat_rows<N, false>, X::SMEM);
-    if (e != cudaSuccess) return e;
-    if (many)
-        k_xlat_rows<N, true><<<dim3(N / X::ROWS, p.batch), kXThreads, X::SMEM, s>>>(p);
-    else
-        k_xlat_rows<N, false><<<dim3(N / X::ROWS, p.batch), kXThreads, X::SMEM, s>>>(p);
-    return cudaGetLastError();
+    const dim3 grid(N / X::ROWS, p.batch);
+    auto go = [&](auto kernel) {
+        cudaError_t e = set_smem(kernel, X::SMEM);
+        if (e != cudaSuccess) return e;
+        kernel<<<grid, kXThreads, X::SMEM, s>>>(p);
+        return cudaGetLastError();
+    };
+    if (p.src_div != 1) return go(k_xlat_rows<N, true, false>);  // exhaustive search (power-of-two grids)
+    return p.embed ? go(k_xlat_rows<N, false, true>) : go(k_xlat_rows<N, false, false>);
 }
 
 template <int N>
@@ -1099,10 +1117,14 @@ cudaError_t xlat_cols(const Params& p, cudaStream_t s) {
 template <int N>
 cudaError_t xlat_out(const Params& p, cudaStream_t s) {
     using X = XOutGeom<N>;
-    cudaError_t e = set_smem(k_xlat_out<N>, X::SMEM);
-    if (e != cudaSuccess) return e;
-    k_xlat_out<N><<<dim3(N / X::ROWS, p.batch), X::THREADS, X::SMEM, s>>>(p);
-    return cudaGetLastError();
+    const dim3 grid(N / X::ROWS, p.batch);
+    auto go = [&](auto kernel) {
+        cudaError_t e = set_smem(kernel, X::SMEM);
+        if (e != cudaSuccess) return e;
+        kernel<<<grid, X::THREADS, X::SMEM, s>>>(p);
+        return cudaGetLastError();
+    };
+    return p.embed ? go(k_xlat_out<N, true>) : go(k_xlat_out<N, false>);
 }
 
 }  // namespace
@@ -1120,9 +1142,9 @@ int rows_per_block_out(int n) {
 
 cudaError_t launch_rot_rows(const Params& p, cudaStream_t s) { FSCAN_DISPATCH_N(p.n, rot_rows) }
 cudaError_t launch_rot_cols(const Params& p, cudaStream_t s) { FSCAN_DISPATCH_N(p.n, rot_cols) }
-cudaError_t launch_xlat_rows(const Params& p, cudaStream_t s) { FSCAN_DISPATCH_N(p.n, xlat_rows) }
-cudaError_t launch_xlat_cols(const Params& p, cudaStream_t s) { FSCAN_DISPATCH_N(p.n, xlat_cols) }
-cudaError_t launch_xlat_out(const Params& p, cudaStream_t s) { FSCAN_DISPATCH_N(p.n, xlat_out) }
+cudaError_t launch_xlat_rows(const Params& p, cudaStream_t s) { FSCAN_DISPATCH_N(p.np, xlat_rows) }
+cudaError_t launch_xlat_cols(const Params& p, cudaStream_t s) { FSCAN_DISPATCH_N(p.np, xlat_cols) }
+cudaError_t launch_xlat_out(const Params& p, cudaStream_t s) { FSCAN_DISPATCH_N(p.np, xlat_out) }
 
 cudaError_t launch_rot_gather(const Params& p, cudaStream_t s) {
     if (p.n_theta == 1) return cudaSuccess;
@@ -1146,18 +1168,18 @@ cudaError_t launch_theta_in(const Params& p, cudaStream_t s) {
 }
 
 cudaError_t launch_finalize(const Params& p, cudaStream_t s) {
-    k_finalize<<<p.batch, kFinThreads, 0, s>>>(p, p.n / rows_per_block_out(p.n));
+    k_finalize<<<p.batch, kFinThreads, 0, s>>>(p, p.np / rows_per_block_out(p.np));
     return cudaGetLastError();
 }
 
 cudaError_t launch_mag_unpack(const Params& p, cudaStream_t s) {
-    const size_t total = (size_t)p.n * (p.n / 2);
+    const size_t total = (size_t)p.n * p.nw;
     k_mag_unpack<<<dim3((unsigned)((total + 255) / 256), p.batch), 256, 0, s>>>(p);
     return cudaGetLastError();
 }
 
 cudaError_t launch_bf_items(const Params& p, cudaStream_t s) {
-    k_bf_items<<<(p.batch + 127) / 128, 128, 0, s>>>(p, p.n / rows_per_block_out(p.n));
+    k_bf_items<<<(p.batch + 127) / 128, 128, 0, s>>>(p, p.np / rows_per_block_out(p.np));
     return cudaGetLastError();
 }
 

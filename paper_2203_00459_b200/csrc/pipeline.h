@@ -87,6 +87,21 @@ struct Params {
     // the flags are one per scan
     int chain, n_scans;
     Partial* bf_items;        // brute force: per global item hard argmax (nullable)
+    // Grid sides that are not powers of two (the reference's odd sizes), see
+    // DESIGN.md §3.9. The rotation stage runs at N = n with Bluestein DFTs of
+    // length bs_L; the translation stage runs at np (a power of two >= N + 1)
+    // on zero-embedded scans: rotation centre c0, valid grid n, lag window at
+    // offset win_off in the np x np surface. pow2: n == np, c0 = (n-1)/2, off 0.
+    int np;
+    float c0;
+    int win_off;
+    int embed;                // 1: translation stage embedded (n < np)
+    int nw;                   // half-plane width W = n - n/2 (u in [0, W))
+    long long mag_plane;      // float2 per (|F|,|G|) tile set: n * 8 * ceil(W / 8)
+    int bs_L;                 // Bluestein transform length (0: pow2 fast path)
+    const float2* bs_chirp;   // exp(-i pi k^2 / n), k < n
+    const float2* bs_kern;    // FFT_L of the chirp kernel, / L
+    const float2* tw_L;       // exp(-2 pi i k / L), k < L
 };
 
 // Launch the stages; each returns cudaGetLastError() of its launch.
@@ -101,6 +116,8 @@ cudaError_t launch_xlat_out(const Params& p, cudaStream_t s);        // K5
 cudaError_t launch_finalize(const Params& p, cudaStream_t s);        // K6
 cudaError_t launch_mag_unpack(const Params& p, cudaStream_t s);      // stage API helper
 cudaError_t launch_bf_items(const Params& p, cudaStream_t s);        // brute force: item argmax
+cudaError_t launch_rot_rows_bs(const Params& p, cudaStream_t s);     // K1a, Bluestein (any n)
+cudaError_t launch_rot_cols_bs(const Params& p, cudaStream_t s);     // K1b, Bluestein (any n)
 cudaError_t launch_bf_final(const Partial* items, const double* thetas, int n_thetas, int batch, int n,
                             double delta, fscan_bf_result* out, cudaStream_t s);  // brute force: winner
 // K0: one or two sweep batches (d_polar1 nullable) -> Cartesian grids through

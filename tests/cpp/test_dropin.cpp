@@ -250,11 +250,25 @@ int main() {
         badv(0, 0) = 1.5;
         CHECK_THROWS_AS(MaskGrid(spec, badv), std::invalid_argument);
     }
-    // GPU-path limits are reported, not silently handled: odd n is unsupported here
+    // odd grid sides (the reference's own sizes, test_matcher.cpp:331-347 at n = 65)
     {
-        MatchConfig c = small_cfg(65, delta, 129);
-        const GridSpec s65{65, delta};
-        const ScanGrid f = ScanGrid::zeros(s65);
+        const int n65 = 65;
+        const GridSpec s65{n65, delta};
+        MatchConfig c = small_cfg(n65, delta, 129);
+        const auto bs = scene(n65, delta, 101, 14);
+        const Pose2D rel{0.12, 0.8, -0.4};
+        const ScanGrid f = render(bs, s65, Pose2D::identity());
+        const ScanGrid g = render(bs, s65, rel);
+        const MatchResult r = scan_match(f, g, c);
+        CHECK(std::abs(normalize_angle(r.pose.theta - rel.theta)) <= 2.0 * c.delta_theta);
+        CHECK(std::abs(r.pose.tx - rel.tx) <= s65.delta && std::abs(r.pose.ty - rel.ty) <= s65.delta);
+        CHECK(r.xy_surface.scores.rows() == (std::size_t)n65 && r.xy_surface.scores.cols() == (std::size_t)n65);
+    }
+    // GPU-path limits are reported, not silently handled: sides below 33 are unsupported
+    {
+        MatchConfig c = small_cfg(31, delta, 65);
+        const GridSpec s31{31, delta};
+        const ScanGrid f = ScanGrid::zeros(s31);
         CHECK_THROWS_AS(scan_match(f, f, c), std::runtime_error);
     }
     // batched extension on device pointers

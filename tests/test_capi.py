@@ -88,8 +88,11 @@ def test_context_without_gpu_fails_loudly(fb):
     assert ei.value.status in (fb.ERR_NO_DEVICE, fb.ERR_CUDA)
 
 
-def test_unsupported_grid_sizes_are_rejected(fb):
-    cfg = fb.MatchConfig.for_grid(255, 0.4, 733)  # the reference's own default (odd n)
+@pytest.mark.parametrize("n", [31, 2048])
+def test_unsupported_grid_sizes_are_rejected(fb, n):
+    """Grid sides outside [33, 1024] are refused before any device work (odd
+    sides such as the reference's default 255 are supported: DESIGN.md §3.9)."""
+    cfg = fb.MatchConfig.for_grid(n, 0.4, 733)
     with pytest.raises(fb.FscanError) as ei:
         fb.Matcher(cfg, max_batch=1)
     assert ei.value.status == fb.ERR_UNSUPPORTED

@@ -75,7 +75,7 @@ def compare(res, ts, xs, ref_bins, ref_pose, ref_ts, ref_xs, delta, stats):
 
 # ---------------------------------------------------------------- stage 1
 
-@pytest.mark.parametrize("n", [64, 128, 256, 512, 1024])
+@pytest.mark.parametrize("n", [64, 128, 256, 512, 1024, 65, 255, 300, 1023])
 def test_band_magnitude_matches_oracle(fb, orc, dev, n):
     rng = np.random.default_rng(n)
     img = rng.random((2, n, n)).astype(np.float32)
@@ -85,7 +85,8 @@ def test_band_magnitude_matches_oracle(fb, orc, dev, n):
     got = m.band_magnitude(I).cpu().numpy()
     for i in range(2):
         ref = orc.band_magnitude(img[i].astype(np.float64), cfg.band_lo, cfg.band_hi)[:, n // 2:]
-        assert np.abs(got[i] - ref).max() <= 1e-5 * np.abs(ref).max()
+        tol = 1e-5 if (n & (n - 1)) == 0 else 2e-5  # Bluestein DFTs for other sides
+        assert np.abs(got[i] - ref).max() <= tol * np.abs(ref).max()
         assert np.all(got[i][ref == 0.0] == 0.0)  # identical band support
 
 
@@ -558,3 +559,42 @@ def test_phase_correlation_matches_restatement(fb, orc, dev):
     plain = m.estimate_translation(F, G, theta, delta=delta).cpu().numpy()
     tx0, ty0, _ = orc.estimate_translation_ex(f[0].astype(np.float64), g[0].astype(np.float64), 0.02, oc, delta)
     assert abs(plain[0, 0] - tx0) < PX_TOL * delta
+
+
+
+# ---- grid sides that are not powers of two (the reference's own odd sizes) ----
+
+@pytest.mark.parametrize("n,nt", [(65, 129), (129, 90), (255, 733), (300, 360), (511, 720)])
+def test_scan_match_other_grid_sides_match_oracle(fb, orc, dev, n, nt):
+    spec = fb.synth_spec(2, n=n, delta=0.5 * 256 / n)
+    cfg = fb.MatchConfig.for_grid(n, spec.delta, nt, t_theta=2.0, t_xy=1.0)
+    count = 2 if n >= 255 else 4
+    f, g, mf, mg, _ = fb.synth_pairs_host(spec, 5, count)
+    res, ts, xs = run_gpu(fb, dev, cfg, spec.delta, f, g, mf, mg)
+    assert xs.shape == (count, n, n)
+    oc = oracle_cfg(orc, cfg)
+    stats = []
+    for i in range(count):
+        r = orc.scan_match(f[i], g[i], oc, spec.delta, mf[i], mg[i])
+        compare(res[i], ts[i], xs[i], (r.theta_bin, r.xy_row, r.xy_col), (r.theta, r.tx, r.ty), r.theta_surface,
+                r.xy_surface, spec.delta, stats)
+        assert res[i]["status"] == fb.OK
+    print("max surface errors", np.max(stats, axis=0))
+
+
+def test_odd_grid_stage_apis_and_reference_default(fb, orc, dev):
+    """The reference's default configuration (n_xy = 255, 733 bins) end to end,
+    plus the translation stage API on the embedded grid."""
+    cfg = fb.MatchConfig()  # matcher.hpp:13-26 defaults: n 255, delta 0.4, 733 bins, pad 92
+    spec = fb.synth_spec(2, n=255, delta=0.4)
+    f, g, mf, mg, _ = fb.synth_pairs_host(spec, 9, 1)
+    r = fb.scan_match(f[0], g[0], 0.4, cfg)
+    o = orc.scan_match(f[0].astype(np.float64), g[0].astype(np.float64), oracle_cfg(orc, cfg), 0.4)
+    assert abs(r.pose.theta - o.theta) < THETA_TOL
+    assert abs(r.pose.tx - o.tx) < PX_TOL * 0.4 and abs(r.pose.ty - o.ty) < PX_TOL * 0.4
+    m = fb.Matcher(cfg, max_batch=1)
+    F, G = to_dev(dev, f, g)
+    txy = m.estimate_translation(F, G, torch.tensor([0.03], dtype=torch.float64, device=dev), delta=0.4)
+    tx, ty, _ = orc.estimate_translation_ex(f[0].astype(np.float64), g[0].astype(np.float64), 0.03,
+                                            oracle_cfg(orc, cfg), 0.4)
+    assert abs(float(txy[0, 0]) - tx) < PX_TOL * 0.4 and abs(float(txy[0, 1]) - ty) < PX_TOL * 0.4
