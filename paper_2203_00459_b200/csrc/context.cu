@@ -791,8 +791,6 @@ fscan_status fscan_brute_force_batch(fscan_ctx* ctx, const float* d_f, const flo
     if (!ctx->tw_n) return fail(ctx, FSCAN_ERR_INVALID_ARGUMENT, "context was not created successfully");
     if (!d_f || !d_g || !d_out || !(delta > 0.0))
         return fail(ctx, FSCAN_ERR_INVALID_ARGUMENT, "fscan_brute_force_batch: bad pointers or delta");
-    if (ctx->np != ctx->n)
-        return fail(ctx, FSCAN_ERR_UNSUPPORTED, "brute_force_match: power-of-two grids only on the GPU path");
     if (!thetas || nth < 1)  // oracle.cpp:46-47
         return fail(ctx, FSCAN_ERR_INVALID_ARGUMENT, "brute_force_match: empty theta candidate list");
     if ((long long)batch * nth > (1LL << 30))
@@ -815,6 +813,18 @@ fscan_status fscan_brute_force_batch(fscan_ctx* ctx, const float* d_f, const flo
     // the candidate list is small: a synchronous copy keeps the host array's lifetime simple
     CK(cudaStreamSynchronize(user));
     CK(cudaMemcpy(ctx->bf_thetas, thetas, sizeof(double) * nth, cudaMemcpyHostToDevice));
+    // grids that are not powers of two: zero-embed f and g once per call (§3.9)
+    const bool embed = ctx->np != ctx->n;
+    float* ef = nullptr;
+    if (embed) {
+        const size_t npp = (size_t)ctx->np * ctx->np;
+        CK(cudaMalloc(&ef, 2 * npp * sizeof(float) * batch));
+        CK(cudaMemset(ef, 0, 2 * npp * sizeof(float) * batch));
+        CK(launch_embed(d_f, batch, ctx->n, ctx->np, ef, user));
+        CK(launch_embed(d_g, batch, ctx->n, ctx->np, ef + npp * batch, user));
+        d_f = ef;
+        d_g = ef + npp * batch;
+    }
     st = drive(ctx, items, user, [&](Lane& l, int off, int cnt) {
         Params p = base_params(ctx, l, cnt, delta);
         // brute_force_match scores the scans as given; only K3 reads ft / gt here
@@ -838,10 +848,18 @@ fscan_status fscan_brute_force_batch(fscan_ctx* ctx, const float* d_f, const flo
 #undef FSCAN_LAUNCH
         return FSCAN_OK;
     });
-    if (st != FSCAN_OK) return st;
+    if (st != FSCAN_OK) {
+        cudaFree(ef);
+        return st;
+    }
     // all lanes are joined into `user`: the per-pair winner over the candidates
-    CK(launch_bf_final(ctx->bf_items, ctx->bf_thetas, nth, batch, ctx->n, delta, d_out, user));
+    const int off = (ctx->np / 2 - 1) - (ctx->n - 1) / 2;
+    CK(launch_bf_final(ctx->bf_items, ctx->bf_thetas, nth, batch, ctx->n, ctx->np, off, delta, d_out, user));
     ++ctx->launches_last;
+    if (ef) {
+        CK(cudaStreamSynchronize(user));  // the embedded copies are read by the launched kernels
+        cudaFree(ef);
+    }
     return FSCAN_OK;
 }
 

@@ -1025,8 +1025,10 @@ __global__ void k_bf_items(Params p, int nparts) {
 
 // Winner over the candidates of each pair (strict >: the earlier theta wins
 // ties, oracle.cpp:56-58) and its pose: t = R(theta) (col - half, row - half) delta.
-__global__ void k_bf_final(const Partial* items, const double* thetas, int nth, int batch, int n,
-                           double delta, fscan_bf_result* out) {
+// np: pitch of the surface the partial indices refer to, off: offset of the
+// reference's n x n lag window in it (0 unless the grid is embedded, §3.9)
+__global__ void k_bf_final(const Partial* items, const double* thetas, int nth, int batch, int n, int np,
+                           int off, double delta, fscan_bf_result* out) {
     const int pair = blockIdx.x * blockDim.x + threadIdx.x;
     if (pair >= batch) return;
     const Partial* it = items + (size_t)pair * nth;
@@ -1034,7 +1036,7 @@ __global__ void k_bf_final(const Partial* items, const double* thetas, int nth, 
     for (int k = 1; k < nth; ++k)
         if (it[k].val > it[w].val) w = k;
     const int half = (n - 1) / 2;
-    const int row = it[w].idx / n, col = it[w].idx % n;
+    const int row = it[w].idx / np - off, col = it[w].idx % np - off;
     const double theta = thetas[w];
     const double dx = (col - half) * delta, dy = (row - half) * delta;
     double sn, cs;
@@ -1100,7 +1102,8 @@ cudaError_t xlat_rows(const Params& p, cudaStream_t s) {
         kernel<<<grid, kXThreads, X::SMEM, s>>>(p);
         return cudaGetLastError();
     };
-    if (p.src_div != 1) return go(k_xlat_rows<N, true, false>);  // exhaustive search (power-of-two grids)
+    if (p.src_div != 1)  // exhaustive search
+        return p.embed ? go(k_xlat_rows<N, true, true>) : go(k_xlat_rows<N, true, false>);
     return p.embed ? go(k_xlat_rows<N, false, true>) : go(k_xlat_rows<N, false, false>);
 }
 
@@ -1183,9 +1186,22 @@ cudaError_t launch_bf_items(const Params& p, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// Copies count n x n grids into the top-left of zeroed np x np grids.
+__global__ void k_embed(const float* __restrict__ src, int n, int np, float* __restrict__ dst) {
+    const int b = blockIdx.y;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n * n; e += gridDim.x * blockDim.x)
+        dst[(size_t)b * np * np + (size_t)(e / n) * np + e % n] = src[(size_t)b * n * n + e];
+}
+
+cudaError_t launch_embed(const float* src, int count, int n, int np, float* dst, cudaStream_t s) {
+    if (count <= 0) return cudaSuccess;
+    k_embed<<<dim3(64, count), 256, 0, s>>>(src, n, np, dst);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_bf_final(const Partial* items, const double* thetas, int n_thetas, int batch, int n,
-                            double delta, fscan_bf_result* out, cudaStream_t s) {
-    k_bf_final<<<(batch + 127) / 128, 128, 0, s>>>(items, thetas, n_thetas, batch, n, delta, out);
+                                  int np, int off, double delta, fscan_bf_result* out, cudaStream_t s) {
+    k_bf_final<<<(batch + 127) / 128, 128, 0, s>>>(items, thetas, n_thetas, batch, n, np, off, delta, out);
     return cudaGetLastError();
 }
 

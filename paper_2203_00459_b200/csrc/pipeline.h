@@ -116,10 +116,12 @@ cudaError_t launch_xlat_out(const Params& p, cudaStream_t s);        // K5
 cudaError_t launch_finalize(const Params& p, cudaStream_t s);        // K6
 cudaError_t launch_mag_unpack(const Params& p, cudaStream_t s);      // stage API helper
 cudaError_t launch_bf_items(const Params& p, cudaStream_t s);        // brute force: item argmax
+// brute force: winner per pair (np: surface pitch, off: lag-window offset, §3.9)
+cudaError_t launch_bf_final(const Partial* items, const double* thetas, int n_thetas, int batch, int n, int np,
+                            int off, double delta, fscan_bf_result* out, cudaStream_t s);
+cudaError_t launch_embed(const float* src, int count, int n, int np, float* dst, cudaStream_t s);
 cudaError_t launch_rot_rows_bs(const Params& p, cudaStream_t s);     // K1a, Bluestein (any n)
 cudaError_t launch_rot_cols_bs(const Params& p, cudaStream_t s);     // K1b, Bluestein (any n)
-cudaError_t launch_bf_final(const Partial* items, const double* thetas, int n_thetas, int batch, int n,
-                            double delta, fscan_bf_result* out, cudaStream_t s);  // brute force: winner
 // K0: one or two sweep batches (d_polar1 nullable) -> Cartesian grids through
 // a per-geometry tap table `tab` (polar_tap_bytes(n), built by
 // launch_polar_taps; nullptr: a temporary one is built for the call)

@@ -598,3 +598,20 @@ def test_odd_grid_stage_apis_and_reference_default(fb, orc, dev):
     tx, ty, _ = orc.estimate_translation_ex(f[0].astype(np.float64), g[0].astype(np.float64), 0.03,
                                             oracle_cfg(orc, cfg), 0.4)
     assert abs(float(txy[0, 0]) - tx) < PX_TOL * 0.4 and abs(float(txy[0, 1]) - ty) < PX_TOL * 0.4
+
+
+def test_brute_force_on_odd_grid_matches_oracle(fb, orc, dev):
+    """The exhaustive search on an embedded (odd) grid: same candidate and cell as
+    the restatement (pinned bit-exact to the reference's oracle.cpp)."""
+    n = 65
+    spec = fb.synth_spec(1, n=n, delta=0.4)
+    f, g, _, _, _ = fb.synth_pairs_host(spec, 3, 2)
+    thetas = (np.arange(9) - 4) * 0.03
+    cfg = fb.MatchConfig.for_grid(n, 0.4, 65, band_lo=0.15)
+    m = fb.Matcher(cfg, max_batch=2)
+    F, G = to_dev(dev, f, g)
+    res = fb.decode_bf_results(m.brute_force(F, G, thetas, delta=0.4))
+    stats = []
+    for i in range(2):
+        o = orc.brute_force(f[i].astype(np.float64), g[i].astype(np.float64), thetas, 0.4)
+        bf_compare(res[i], o, n, stats)
