@@ -272,7 +272,7 @@ fscan_status alloc_lane(fscan_ctx* ctx, Lane& l, int chunk) {
         CK(cudaMemset(l.gt, 0, npp * sizeof(float) * chunk));
     }
     // zbuf: K1 spectra (n x n) then the K4 -> K5 rows (np x (3np/4 + 1))
-    CK(cudaMalloc(&l.zbuf, std::max(n * n, np * (3 * np / 4 + 1)) * sizeof(float2) * chunk));
+    CK(cudaMalloc(&l.zbuf, std::max(n * n, np * (size_t)ypitch((int)np)) * sizeof(float2) * chunk));
     // mag: the (|F|,|G|) tiles, later the np x np surface
     CK(cudaMalloc(&l.mag, std::max((size_t)ctx->mag_plane * 2, npp) * sizeof(float) * chunk));
     CK(cudaMalloc(&l.fgt, (3 * np / 4 + 1) * np * sizeof(float4) * chunk));

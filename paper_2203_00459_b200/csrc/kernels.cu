@@ -737,11 +737,14 @@ __global__ void __launch_bounds__(XColGeom<N>::THREADS) k_xlat_cols(Params p) {
         }
     }
     __syncthreads();
-    float2* dst = p.zbuf + (size_t)pair * N * (H + 1);
+    // K4 -> K5 rows with a 64-byte aligned pitch: each CTA's 8-column stripe
+    // is two whole sectors per row
+    constexpr int RP = ypitch(N);
+    float2* dst = p.zbuf + (size_t)pair * N * RP;
     const int ncols = min(COLS, H + 1 - (int)blockIdx.x * COLS);
     for (int o = threadIdx.x; o < N * COLS; o += blockDim.x) {
         const int i = o / COLS, cc = o % COLS;
-        if (cc < ncols) dst[(size_t)i * (H + 1) + blockIdx.x * COLS + cc] = tile[i * X::PITCH + cc];
+        if (cc < ncols) dst[(size_t)i * RP + blockIdx.x * COLS + cc] = tile[i * X::PITCH + cc];
     }
 }
 
@@ -789,7 +792,7 @@ __global__ void __launch_bounds__(XOutGeom<N>::THREADS) k_xlat_out(Params p) {
         // (staging Y through shared memory with cp.async, or a k'-major Y
         // written straight from K4's registers, both measured slower: the
         // stride-3 row reads are served by L1 across the three q groups)
-        const float2* yrow = p.zbuf + ((size_t)pair * N + i) * (H + 1);
+        const float2* yrow = p.zbuf + ((size_t)pair * N + i) * ypitch(N);
         float2 v[16];
 #pragma unroll
         for (int m = 0; m < 16; ++m) {

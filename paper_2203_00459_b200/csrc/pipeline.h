@@ -18,6 +18,10 @@ struct PolarTap {
     float pad_;
 };
 
+// Row pitch (float2) of the K4 -> K5 spectrum rows: 3N/4 + 1 bins rounded up
+// to 8 (64-byte aligned rows).
+__host__ __device__ constexpr int ypitch(int n) { return (3 * n / 4 + 1 + 7) / 8 * 8; }
+
 // Per-pair state handed from the angular stage to the translation stage.
 struct RotState {
     double theta;      // soft-argmax theta (radians, not wrapped)
