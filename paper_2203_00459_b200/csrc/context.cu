@@ -680,10 +680,10 @@ fscan_status fscan_match_batch(fscan_ctx* ctx, const float* d_f, const float* d_
     fscan_status st = check_ctx(ctx, batch);
     if (st != FSCAN_OK) return st;
     std::lock_guard<std::mutex> g(ctx->mu);
+    if (batch == 0) return FSCAN_OK;  // empty batches may pass null pointers
     if (!ctx->tw_n) return fail(ctx, FSCAN_ERR_INVALID_ARGUMENT, "context was not created successfully");
     if (!d_f || !d_g || !d_out || ((d_mf == nullptr) != (d_mg == nullptr)) || !(delta > 0.0))
         return fail(ctx, FSCAN_ERR_INVALID_ARGUMENT, "fscan_match_batch: bad pointers or delta");
-    if (batch == 0) return FSCAN_OK;
     const size_t nn = (size_t)ctx->n * ctx->n;
     const int nt = ctx->cfg.n_theta;
     return drive(ctx, batch, (cudaStream_t)stream, [&](Lane& l, int off, int cnt) {
@@ -706,11 +706,11 @@ fscan_status fscan_match_batch_polar(fscan_ctx* ctx, const float* d_pf, const fl
     fscan_status st = check_ctx(ctx, batch);
     if (st != FSCAN_OK) return st;
     std::lock_guard<std::mutex> g(ctx->mu);
+    if (batch == 0) return FSCAN_OK;  // empty batches may pass null pointers
     if (!ctx->tw_n) return fail(ctx, FSCAN_ERR_INVALID_ARGUMENT, "context was not created successfully");
     if (!d_pf || !d_pg || !d_out || ((d_mf == nullptr) != (d_mg == nullptr)) || !(delta > 0.0) || n_az < 1 ||
         n_range < 1 || !(range_res > 0.0))
         return fail(ctx, FSCAN_ERR_INVALID_ARGUMENT, "fscan_match_batch_polar: bad pointers or geometry");
-    if (batch == 0) return FSCAN_OK;
     const size_t nn = (size_t)ctx->n * ctx->n, np = (size_t)n_az * n_range;
     const int nt = ctx->cfg.n_theta;
     for (Lane& l : LaneRange{ctx}) {
@@ -748,8 +748,8 @@ fscan_status fscan_estimate_rotation_batch(fscan_ctx* ctx, const float* d_f, con
     fscan_status st = check_ctx(ctx, batch);
     if (st != FSCAN_OK) return st;
     std::lock_guard<std::mutex> g(ctx->mu);
+    if (batch == 0) return FSCAN_OK;  // empty batches may pass null pointers
     if (!d_f || !d_g || !d_theta) return fail(ctx, FSCAN_ERR_INVALID_ARGUMENT, "bad pointers");
-    if (batch == 0) return FSCAN_OK;
     const size_t nn = (size_t)ctx->n * ctx->n;
     return drive(ctx, batch, (cudaStream_t)stream, [&](Lane& l, int off, int cnt) {
         Params p = base_params(ctx, l, cnt, 1.0);
@@ -767,9 +767,9 @@ fscan_status fscan_estimate_translation_batch(fscan_ctx* ctx, const float* d_f, 
     fscan_status st = check_ctx(ctx, batch);
     if (st != FSCAN_OK) return st;
     std::lock_guard<std::mutex> g(ctx->mu);
+    if (batch == 0) return FSCAN_OK;  // empty batches may pass null pointers
     if (!d_f || !d_g || !d_theta || !d_txy || !(delta > 0.0))
         return fail(ctx, FSCAN_ERR_INVALID_ARGUMENT, "bad pointers or delta");
-    if (batch == 0) return FSCAN_OK;
     const size_t nn = (size_t)ctx->n * ctx->n;
     return drive(ctx, batch, (cudaStream_t)stream, [&](Lane& l, int off, int cnt) {
         Params p = base_params(ctx, l, cnt, delta);
@@ -788,6 +788,7 @@ fscan_status fscan_brute_force_batch(fscan_ctx* ctx, const float* d_f, const flo
     fscan_status st = check_ctx(ctx, batch);
     if (st != FSCAN_OK) return st;
     std::lock_guard<std::mutex> g(ctx->mu);
+    if (batch == 0) return FSCAN_OK;  // empty batches may pass null pointers
     if (!ctx->tw_n) return fail(ctx, FSCAN_ERR_INVALID_ARGUMENT, "context was not created successfully");
     if (!d_f || !d_g || !d_out || !(delta > 0.0))
         return fail(ctx, FSCAN_ERR_INVALID_ARGUMENT, "fscan_brute_force_batch: bad pointers or delta");
@@ -795,7 +796,6 @@ fscan_status fscan_brute_force_batch(fscan_ctx* ctx, const float* d_f, const flo
         return fail(ctx, FSCAN_ERR_INVALID_ARGUMENT, "brute_force_match: empty theta candidate list");
     if ((long long)batch * nth > (1LL << 30))
         return fail(ctx, FSCAN_ERR_INVALID_ARGUMENT, "fscan_brute_force_batch: too many (pair, theta) items");
-    if (batch == 0) return FSCAN_OK;
     cudaStream_t user = (cudaStream_t)stream;
     const int items = batch * nth;
     if (ctx->bf_theta_cap < nth) {
@@ -917,8 +917,8 @@ fscan_status fscan_band_magnitude_batch(fscan_ctx* ctx, const float* d_img, int 
     fscan_status st = check_ctx(ctx, batch);
     if (st != FSCAN_OK) return st;
     std::lock_guard<std::mutex> g(ctx->mu);
+    if (batch == 0) return FSCAN_OK;  // empty batches may pass null pointers
     if (!d_img || !d_out) return fail(ctx, FSCAN_ERR_INVALID_ARGUMENT, "bad pointers");
-    if (batch == 0) return FSCAN_OK;
     const size_t nn = (size_t)ctx->n * ctx->n;
     return drive(ctx, batch, (cudaStream_t)stream, [&](Lane& l, int off, int cnt) {
         Params p = base_params(ctx, l, cnt, 1.0);
@@ -936,10 +936,10 @@ fscan_status fscan_match_batch_host(fscan_ctx* ctx, const float* f, const float*
     fscan_status st = check_ctx(ctx, batch);
     if (st != FSCAN_OK) return st;
     std::lock_guard<std::mutex> guard(ctx->mu);
+    if (batch == 0) return FSCAN_OK;  // empty batches may pass null pointers
     if (!ctx->tw_n) return fail(ctx, FSCAN_ERR_INVALID_ARGUMENT, "context was not created successfully");
     if (!f || !g || !out || ((mf == nullptr) != (mg == nullptr)) || !(delta > 0.0))
         return fail(ctx, FSCAN_ERR_INVALID_ARGUMENT, "fscan_match_batch_host: bad pointers or delta");
-    if (batch == 0) return FSCAN_OK;
     const size_t nn = (size_t)ctx->n * ctx->n;
     const int nt = ctx->cfg.n_theta;
     for (Lane& l : LaneRange{ctx}) {

@@ -615,3 +615,85 @@ def test_brute_force_on_odd_grid_matches_oracle(fb, orc, dev):
     for i in range(2):
         o = orc.brute_force(f[i].astype(np.float64), g[i].astype(np.float64), thetas, 0.4)
         bf_compare(res[i], o, n, stats)
+
+
+# ---- configuration sweep: every MatchConfig knob against the oracle ----
+
+@pytest.mark.parametrize("kw", [
+    dict(normalize_scores=False),
+    dict(softargmax_window=1),
+    dict(softargmax_window=40),
+    dict(t_theta=0.25, t_xy=4.0),
+    dict(band_lo=0.0, band_hi=1.0),
+    dict(band_lo=0.2, band_hi=0.5),
+    dict(pad_angle=0),
+    dict(n_radius=17),
+    dict(n_theta=90, delta_theta=math.pi / 180),   # span pi/2: partial angular range
+    dict(n_theta=91),                              # odd bin count
+], ids=lambda kw: ",".join(f"{k}={v:.3g}" if isinstance(v, float) else f"{k}={v}" for k, v in kw.items()))
+def test_config_knobs_match_oracle(fb, orc, dev, kw):
+    n = 128
+    spec = fb.synth_spec(2, n=n, delta=1.0)
+    base = dict(n_theta=180, delta_theta=math.pi / 180, n_xy=n, delta_xy=1.0, n_radius=0, pad_angle=-1)
+    base.update(kw)
+    if "n_theta" in kw and "delta_theta" not in kw:
+        base["delta_theta"] = math.pi / kw["n_theta"]
+    cfg = fb.MatchConfig(**base).finalize()
+    cfg.validate()
+    f, g, mf, mg, _ = fb.synth_pairs_host(spec, 21, 3)
+    res, ts, xs = run_gpu(fb, dev, cfg, 1.0, f, g, mf, mg)
+    oc = oracle_cfg(orc, cfg)
+    stats = []
+    for i in range(3):
+        r = orc.scan_match(f[i], g[i], oc, 1.0, mf[i], mg[i])
+        compare(res[i], ts[i], xs[i], (r.theta_bin, r.xy_row, r.xy_col), (r.theta, r.tx, r.ty), r.theta_surface,
+                r.xy_surface, 1.0, stats)
+
+
+def test_degenerate_inputs_match_oracle(fb, orc, dev):
+    """All-zero and constant scans (flat surfaces: ties everywhere, zero scale in the
+    soft-argmax normalisation) and masks of zeros give the oracle's answers."""
+    n = 64
+    cfg = fb.MatchConfig.for_grid(n, 0.5, 90, band_lo=0.15)
+    z = np.zeros((n, n), np.float32)
+    c = np.full((n, n), 3.0, np.float32)
+    ones = np.ones((n, n), np.float32)
+    cases = [(z, z, ones, ones), (c, c, ones, ones), (c, z, ones, ones), (c, c, z, ones)]
+    f = np.stack([k[0] for k in cases])
+    g = np.stack([k[1] for k in cases])
+    mf = np.stack([k[2] for k in cases])
+    mg = np.stack([k[3] for k in cases])
+    res, ts, xs = run_gpu(fb, dev, cfg, 0.5, f, g, mf, mg)
+    oc = oracle_cfg(orc, cfg)
+    for i in range(len(cases)):
+        r = orc.scan_match(f[i], g[i], oc, 0.5, mf[i], mg[i])
+        assert res[i]["status"] == fb.OK and np.isfinite([res[i]["theta"], res[i]["tx"], res[i]["ty"]]).all()
+        xy_flat = r.xy_surface.max() == r.xy_surface.min()
+        if xy_flat and r.xy_surface.max() == 0.0 and xs[i].max() != 0.0:
+            # the reference's surface is exactly zero (a zero scan after masking);
+            # the packed real-pair FFT leaves ~1e-7 relative residue of the other
+            # scan in it: every cell is an exact tie, a documented near-tie
+            energy = float(((f[i] * mf[i]) ** 2).sum() + ((g[i] * mg[i]) ** 2).sum())
+            assert np.abs(xs[i]).max() <= 1e-6 * max(1.0, energy)
+            continue
+        assert (res[i]["theta_bin"], res[i]["xy_row"], res[i]["xy_col"]) == (r.theta_bin, r.xy_row, r.xy_col), i
+        assert abs(res[i]["theta"] - r.theta) < THETA_TOL and abs(res[i]["tx"] - r.tx) < PX_TOL * 0.5
+        assert abs(res[i]["ty"] - r.ty) < PX_TOL * 0.5
+
+
+def test_batch_edge_sizes(fb, dev):
+    """batch 0 is a no-op; a batch of exactly max_batch over many small chunks equals
+    one big chunk."""
+    cfg, delta, _ = fb.baseline_config(2)
+    f, g, mf, mg, _ = fb.synth_pairs_host(fb.synth_spec(2), 0, 7)
+    F, G, MF, MG = to_dev(dev, f, g, mf, mg)
+    m = fb.Matcher(cfg, max_batch=7, chunk=2)
+    out0 = torch.empty(0, dtype=torch.uint8, device=dev)
+    m.match_device(F[:0], G[:0], MF[:0], MG[:0], delta=delta, out=out0)
+    a = fb.decode_results(m.match_device(F, G, MF, MG, delta=delta))
+    m.set_chunk(7)
+    b = fb.decode_results(m.match_device(F, G, MF, MG, delta=delta))
+    assert (a["theta_bin"] == b["theta_bin"]).all() and (a["xy_row"] == b["xy_row"]).all()
+    np.testing.assert_array_equal(a["theta"], b["theta"])
+    with pytest.raises(fb.FscanError):
+        fb.Matcher(cfg, max_batch=3).match_device(F, G, MF, MG, delta=delta)  # batch > max_batch
