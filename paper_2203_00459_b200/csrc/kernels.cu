@@ -644,13 +644,31 @@ struct XColGeom {
     static constexpr size_t FFT_FLOATS = (size_t)2 * G::FLOATS;
     static constexpr size_t TILE_FLOATS = (size_t)2 * N * PITCH;
     static constexpr size_t WORK_FLOATS = FFT_FLOATS > TILE_FLOATS ? FFT_FLOATS : TILE_FLOATS;
-    // twiddle tables staged behind the work area: W_K (K entries) and W_M (3K)
-    static constexpr size_t TW_FLOATS = (size_t)2 * (N / 2) * 4;
+    // twiddle tables staged behind the work area: W_K (K entries) and, below
+    // N = 1024, W_M (3K; at 1024 it would push the CTA past half an SM's smem)
+    static constexpr bool SMEM_WM = N <= 512;
+    static constexpr size_t TW_FLOATS = (size_t)2 * (N / 2) * (SMEM_WM ? 4 : 1);
     static constexpr size_t SMEM = (WORK_FLOATS + TW_FLOATS) * sizeof(float);
+    // explicit residency targets where ptxas' own choice leaves the SM
+    // register-bound (N = 256: 4 CTAs of 192 threads; N = 1024: 2 of 384)
+    static constexpr int MIN_BLOCKS = N == 1024 ? 2 : (N == 256 ? 4 : 0);
 };
 
 template <int N>
+__device__ __forceinline__ void xlat_cols_body(const Params& p);
+
+template <int N>
 __global__ void __launch_bounds__(XColGeom<N>::THREADS) k_xlat_cols(Params p) {
+    xlat_cols_body<N>(p);
+}
+
+template <int N, int MINB>
+__global__ void __launch_bounds__(XColGeom<N>::THREADS, MINB) k_xlat_cols_mb(Params p) {
+    xlat_cols_body<N>(p);
+}
+
+template <int N>
+__device__ __forceinline__ void xlat_cols_body(const Params& p) {
     constexpr int K = N / 2, M = 3 * K, H = M / 2;
     using X = XColGeom<N>;
     using G = typename X::G;
@@ -669,9 +687,11 @@ __global__ void __launch_bounds__(XColGeom<N>::THREADS) k_xlat_cols(Params p) {
     // stage the twiddle tables in shared memory (latency: the FFT stages and
     // input/combine twiddles read them ~90 times per thread)
     float2* stw_k = reinterpret_cast<float2*>(smem + X::WORK_FLOATS);
-    float2* stw_m = stw_k + K;
+    float2* stw_m_s = stw_k + K;
     for (int i = threadIdx.x; i < K; i += X::THREADS) stw_k[i] = __ldg(p.tw_k + i);
-    for (int i = threadIdx.x; i < M; i += X::THREADS) stw_m[i] = __ldg(p.tw_m + i);
+    if constexpr (X::SMEM_WM)
+        for (int i = threadIdx.x; i < M; i += X::THREADS) stw_m_s[i] = __ldg(p.tw_m + i);
+    auto stw_m_at = [&](int e) { return X::SMEM_WM ? stw_m_s[e] : __ldg(p.tw_m + e); };
     __syncthreads();
     const fscan_fft::SmemTw twk{stw_k};
     const float2 w3q = w3(q);
@@ -681,7 +701,7 @@ __global__ void __launch_bounds__(XColGeom<N>::THREADS) k_xlat_cols(Params p) {
         const int n0 = t + m * T;
         const float4 u0 = src[n0], u1 = src[n0 + K];
         const float2 s = cadd(make_float2(u0.x, u0.y), cmul(w3q, make_float2(u1.x, u1.y)));
-        a[m] = q ? cmul(stw_m[n0 * q], s) : s;
+        a[m] = q ? cmul(stw_m_at(n0 * q), s) : s;
     }
     fft_regs<K, -1, true>(a, t, bufA, twk);  // transforms of a warp share a buffer group
 #pragma unroll
@@ -691,7 +711,7 @@ __global__ void __launch_bounds__(XColGeom<N>::THREADS) k_xlat_cols(Params p) {
         const int n0 = t + m * T;
         const float4 u0 = src[n0], u1 = src[n0 + K];
         const float2 s = cadd(make_float2(u0.z, u0.w), cmul(w3q, make_float2(u1.z, u1.w)));
-        a[m] = q ? cmul(stw_m[n0 * q], s) : s;
+        a[m] = q ? cmul(stw_m_at(n0 * q), s) : s;
     }
     fft_regs<K, -1, true>(a, t, bufB, twk);
 #pragma unroll
@@ -719,8 +739,8 @@ __global__ void __launch_bounds__(XColGeom<N>::THREADS) k_xlat_cols(Params p) {
         if (m < 16) {
             const int n0 = t + m * T;
             const float2 x0 = e0.get(n0);
-            const float2 x1 = cmul(cconj(stw_m[n0]), e1.get(n0));
-            const float2 x2 = cmul(cconj(stw_m[2 * n0]), e2.get(n0));
+            const float2 x1 = cmul(cconj(stw_m_at(n0)), e1.get(n0));
+            const float2 x2 = cmul(cconj(stw_m_at(2 * n0)), e2.get(n0));
             accp[j] = cadd(x0, cadd(x1, x2));
             accn[j] = cadd(x0, cadd(cmul(w31, x1), cmul(w32, x2)));
         }
@@ -1114,10 +1134,17 @@ template <int N>
 cudaError_t xlat_cols(const Params& p, cudaStream_t s) {
     using X = XColGeom<N>;
     constexpr int H = 3 * N / 4;
-    cudaError_t e = set_smem(k_xlat_cols<N>, X::SMEM);
-    if (e != cudaSuccess) return e;
-    k_xlat_cols<N><<<dim3((H + 1 + X::COLS - 1) / X::COLS, p.batch), X::THREADS, X::SMEM, s>>>(p);
-    return cudaGetLastError();
+    const dim3 grid((H + 1 + X::COLS - 1) / X::COLS, p.batch);
+    auto go = [&](auto kernel) {
+        cudaError_t e = set_smem(kernel, X::SMEM);
+        if (e != cudaSuccess) return e;
+        kernel<<<grid, X::THREADS, X::SMEM, s>>>(p);
+        return cudaGetLastError();
+    };
+    if constexpr (X::MIN_BLOCKS > 0)
+        return go(k_xlat_cols_mb<N, (X::MIN_BLOCKS > 0 ? X::MIN_BLOCKS : 1)>);
+    else
+        return go(k_xlat_cols<N>);
 }
 
 template <int N>
