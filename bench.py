@@ -215,6 +215,10 @@ def run_ours(args):
     cfg, delta, total = fb.baseline_config(args.config)
     if args.pairs:
         total = args.pairs
+    # weak scaling (default): every rank registers the config's batch, a disjoint
+    # block of pair indices of a world x batch job; --strong splits one batch
+    if not args.strong:
+        total *= world
     from paper_2203_00459_b200.shard import gather_results, shard_range
     first, per = shard_range(total, world, rank)
     spec = fb.synth_spec(args.config)
@@ -375,7 +379,8 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 3), "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded generator)",
+            "scaling": "strong" if args.strong else "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded generator)",
             "config": {"workload": workload_desc(args.config), "pairs": total, "pairs_per_rank": per,
                        "n_xy": cfg.n_xy, "n_theta": cfg.n_theta, "chunk": args.chunk or "auto",
                        "l2": "inputs 16 GiB per pass >> 126 MB L2; no flush needed",
@@ -417,7 +422,7 @@ def run_reference(args):
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(1e3 * tot / args.steps, 1), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator)",
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator)",
         "config": {"workload": workload_desc(args.config), "pairs_per_step": sample, "n_xy": cfg.n_xy,
                    "n_theta": cfg.n_theta},
         "impl": "reference",
@@ -442,6 +447,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-exhaustive", action="store_true", help="skip the brute-force comparison leg")
     ap.add_argument("--no-odometry", action="store_true", help="skip the chained-sequence leg")
+    ap.add_argument("--strong", action="store_true",
+                    help="split the config's batch over the ranks (default: weak scaling, one batch per rank)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
