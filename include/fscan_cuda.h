@@ -17,7 +17,7 @@
  * supported (FSCAN_ERR_UNSUPPORTED otherwise): powers of two >= 64 take the
  * radix fast path, other sides — including the reference's own odd sizes —
  * use Bluestein DFTs in the rotation stage and a zero-embedded power-of-two
- * translation stage. The odometry chain is power-of-two only.
+ * translation stage, in the odometry chain as well.
  *
  * Errors: every call returns an fscan_status; fscan_ctx_last_error() gives the
  * message. The C++ drop-in maps FSCAN_ERR_INVALID_ARGUMENT, _NONFINITE and

@@ -873,13 +873,15 @@ fscan_status fscan_odometry_batch(fscan_ctx* ctx, const float* d_scans, const fl
     if (!ctx->tw_n) return fail(ctx, FSCAN_ERR_INVALID_ARGUMENT, "context was not created successfully");
     if (n_scans < 0 || !(delta > 0.0)) return fail(ctx, FSCAN_ERR_INVALID_ARGUMENT, "fscan_odometry_batch: bad count or delta");
     if (pairs <= 0) return FSCAN_OK;  // 0 or 1 scans: no pairs
-    if (ctx->np != ctx->n)
-        return fail(ctx, FSCAN_ERR_UNSUPPORTED, "fscan_odometry_batch: power-of-two grids only on the GPU path");
     if (!d_scans || !d_out) return fail(ctx, FSCAN_ERR_INVALID_ARGUMENT, "fscan_odometry_batch: bad pointers");
     const size_t nn = (size_t)ctx->n * ctx->n;
+    const size_t npp = (size_t)ctx->np * ctx->np;  // masked scans live in the translation grid (embedded)
     const int nt = ctx->cfg.n_theta;
     for (Lane& l : LaneRange{ctx})
-        if (!l.chain_ms) CK(cudaMalloc(&l.chain_ms, (ctx->alloc_chunk + 2) * nn * sizeof(float)));
+        if (!l.chain_ms) {
+            CK(cudaMalloc(&l.chain_ms, (ctx->alloc_chunk + 2) * npp * sizeof(float)));
+            if (npp != nn) CK(cudaMemset(l.chain_ms, 0, (ctx->alloc_chunk + 2) * npp * sizeof(float)));
+        }
     return drive(ctx, pairs, (cudaStream_t)stream, [&](Lane& l, int off, int cnt) {
         // pairs off .. off+cnt-1 register scans off .. off+cnt
         Params p = base_params(ctx, l, cnt, delta);
@@ -887,8 +889,8 @@ fscan_status fscan_odometry_batch(fscan_ctx* ctx, const float* d_scans, const fl
         p.mf = d_masks ? d_masks + off * nn : nullptr;
         p.chain = 1;
         p.n_scans = cnt + 1;
-        p.ft = l.chain_ms;       // masked scan s of the chunk at ft + s*nn
-        p.gt = l.chain_ms + nn;  // pair k reads scans k (ft) and k+1 (gt)
+        p.ft = l.chain_ms;        // masked scan s of the chunk at ft + s * np^2
+        p.gt = l.chain_ms + npp;  // pair k reads scans k (ft) and k+1 (gt)
         p.out = d_out + off;
         p.theta_surf = d_tsurf ? d_tsurf + (size_t)off * nt : nullptr;
         p.xy_surf = d_xsurf ? d_xsurf + off * nn : nullptr;
@@ -899,8 +901,10 @@ fscan_status fscan_odometry_batch(fscan_ctx* ctx, const float* d_scans, const fl
         fscan_status e;
 #define FSCAN_LAUNCH(kid, call, P)                                                           \
     if ((e = launch(ctx, l, kid, [&] { return call(P, s); }, &ctx->launches_last)) != FSCAN_OK) return e;
-        FSCAN_LAUNCH(kRotRows, launch_rot_rows, r);
-        if (nt > 1) FSCAN_LAUNCH(kRotCols, launch_rot_cols, r);
+        auto k1a = ctx->bs_L ? launch_rot_rows_bs : launch_rot_rows;
+        auto k1b = ctx->bs_L ? launch_rot_cols_bs : launch_rot_cols;
+        FSCAN_LAUNCH(kRotRows, k1a, r);
+        if (nt > 1) FSCAN_LAUNCH(kRotCols, k1b, r);
         if (nt > 1) FSCAN_LAUNCH(kRotGather, launch_rot_gather, p);
         FSCAN_LAUNCH(kRotPolar, launch_rot_polar, p);
         FSCAN_LAUNCH(kXlatRows, launch_xlat_rows, p);

@@ -41,26 +41,54 @@ __global__ void __launch_bounds__(kBsRowThreads) k_rot_rows_bs(Params p) {
     const int y = blockIdx.x * PER + tr;
     const bool row_ok = tr < PER && y < n;
     const Lay<1> lay{reinterpret_cast<float2*>(smem) + tr * STRIDE, 0};
-    const size_t in_base = ((size_t)pair * n + (row_ok ? y : 0)) * n;
-    const size_t out_base = (size_t)pair * np * np + (size_t)(row_ok ? y : 0) * np;
-    const float hy = p.hann[row_ok ? y : 0];
-    int bad = 0;
+    const size_t yy = (size_t)(row_ok ? y : 0);
+    // the two real grids of this transform: scans `pair` of f and g, or in chain
+    // mode (odometry) scans 2*pair and 2*pair+1 of one sequence (the last one
+    // duplicated for an odd count) with their masked copies stored per scan
+    const float *fp, *gp, *mfp = nullptr, *mgp = nullptr;
+    float *ftp, *gtp;
+    size_t fi = pair, gi = pair;
+    if (p.chain) {
+        fi = 2 * (size_t)pair;
+        gi = (size_t)min(2 * pair + 1, p.n_scans - 1);
+        fp = p.f + fi * n * n + yy * n;
+        gp = p.f + gi * n * n + yy * n;
+        if (p.mf) {
+            mfp = p.mf + fi * n * n + yy * n;
+            mgp = p.mf + gi * n * n + yy * n;
+        }
+        ftp = p.ft + fi * np * np + yy * np;
+        gtp = p.ft + gi * np * np + yy * np;
+    } else {
+        fp = p.f + ((size_t)pair * n + yy) * n;
+        gp = p.g + ((size_t)pair * n + yy) * n;
+        if (p.mf) {
+            mfp = p.mf + ((size_t)pair * n + yy) * n;
+            mgp = p.mg + ((size_t)pair * n + yy) * n;
+        }
+        ftp = p.ft + (size_t)pair * np * np + yy * np;
+        gtp = p.gt + (size_t)pair * np * np + yy * np;
+    }
+    const float hy = p.hann[yy];
+    int badf = 0, badg = 0;
     float2 v[16];
 #pragma unroll
     for (int m = 0; m < 16; ++m) {
         const int x = t + m * T;
         float2 a = make_float2(0.f, 0.f);
         if (row_ok && x < n) {
-            float fv = __ldg(p.f + in_base + x), gv = __ldg(p.g + in_base + x);
-            if (p.mf) {
-                const float ma = __ldg(p.mf + in_base + x), mb = __ldg(p.mg + in_base + x);
-                if (!(ma >= 0.0f && ma <= 1.0f) || !(mb >= 0.0f && mb <= 1.0f)) bad |= 2;
+            float fv = __ldg(fp + x), gv = __ldg(gp + x);
+            if (mfp) {
+                const float ma = __ldg(mfp + x), mb = __ldg(mgp + x);
+                if (!(ma >= 0.0f && ma <= 1.0f)) badf |= 2;
+                if (!(mb >= 0.0f && mb <= 1.0f)) badg |= 2;
                 fv *= ma;
                 gv *= mb;
             }
-            if (!isfinite(fv) || !isfinite(gv)) bad |= 1;
-            p.ft[out_base + x] = fv;
-            p.gt[out_base + x] = gv;
+            if (!isfinite(fv)) badf |= 1;
+            if (!isfinite(gv)) badg |= 1;
+            ftp[x] = fv;
+            gtp[x] = gv;
             const float w = hy * __ldg(p.hann + x);
             a = cmul(make_float2(fv * w, gv * w), __ldg(p.bs_chirp + x));
         }
@@ -78,7 +106,12 @@ __global__ void __launch_bounds__(kBsRowThreads) k_rot_rows_bs(Params p) {
             if (k < n) z[k] = cmul(v[m], __ldg(p.bs_chirp + k));
         }
     }
-    if (bad) atomicOr(p.flags + pair, bad);
+    if (p.chain) {  // flags per scan of the sequence
+        if (badf) atomicOr(p.flags + fi, badf);
+        if (badg) atomicOr(p.flags + gi, badg);
+    } else if (badf | badg) {
+        atomicOr(p.flags + pair, badf | badg);
+    }
 }
 
 // K1b (any N): 4 output columns u0..u0+3 and their mirrors (N - u) mod N as 8

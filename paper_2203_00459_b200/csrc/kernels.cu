@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(kPolarThreads) k_rot_polar(Params p) {
                 best_i = red_i[w];
             }
         // soft_argmax over the n_theta x 1 surface (matcher.cpp:57-93)
-        const int pk = best_i;
+        const int pk = best_i == 0x7fffffff ? 0 : best_i;  // all-NaN surface: the first bin, as the reference's scan
         const int r0 = max(0, pk - p.window), r1 = min(nt - 1, pk + p.window);
         double scale = 1.0;
         if (p.normalize) {
@@ -929,8 +929,11 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(Params p, int nparts) 
                 bv = pp[b].val;
                 bi = pp[b].idx;
             }
+        // no ordered maximum (an all-NaN surface): the reference's strict-> scan
+        // keeps its first cell, the window's (0, 0)
+        const int o0 = p.embed ? p.win_off : 0;
         pk_v = bv;
-        pk_i = bi;
+        pk_i = bi == 0x7fffffff ? o0 * n + o0 : bi;
     }
     __syncthreads();
     // the surface is n x n (pitch n = np); embedded grids keep
@@ -1059,7 +1062,8 @@ __global__ void k_bf_final(const Partial* items, const double* thetas, int nth, 
     for (int k = 1; k < nth; ++k)
         if (it[k].val > it[w].val) w = k;
     const int half = (n - 1) / 2;
-    const int row = it[w].idx / np - off, col = it[w].idx % np - off;
+    const int idx = it[w].idx == 0x7fffffff ? off * np + off : it[w].idx;  // all-NaN: first cell
+    const int row = idx / np - off, col = idx % np - off;
     const double theta = thetas[w];
     const double dx = (col - half) * delta, dy = (row - half) * delta;
     double sn, cs;

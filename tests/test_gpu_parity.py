@@ -253,6 +253,27 @@ def test_nonfinite_and_mask_range_are_per_pair_errors(fb, dev):  # test_matcher.
         m.match_host(f[:1], g2[:1], delta=delta)
 
 
+@pytest.mark.parametrize("n", [64, 65, 128, 255])
+def test_nonfinite_pairs_are_contained(fb, dev, n):
+    """NaN/inf in one pair poisons only that pair's surfaces: the kernels stay
+    in bounds (an all-NaN surface has no ordered maximum; the first cell is
+    kept, like the reference's strict-> scans), neighbours are unaffected."""
+    spec = fb.synth_spec(2, n=n, delta=0.5 * 256 / n)
+    cfg = fb.MatchConfig.for_grid(n, spec.delta, 360, t_theta=2.0, t_xy=1.0)
+    f, g, mf, mg, _ = fb.synth_pairs_host(spec, 3, 4)
+    clean, _, _ = run_gpu(fb, dev, cfg, spec.delta, f, g, mf, mg)
+    f[1, 2, 2] = np.inf
+    g[2, :, :] = np.nan
+    res, _, _ = run_gpu(fb, dev, cfg, spec.delta, f, g, mf, mg)
+    assert list(res["status"]) == [fb.OK, fb.ERR_NONFINITE, fb.ERR_NONFINITE, fb.OK]
+    for i in (0, 3):
+        for k in ("theta", "tx", "ty", "theta_bin", "xy_row", "xy_col"):
+            assert res[i][k] == clean[i][k]
+    for i in (1, 2):
+        assert 0 <= res[i]["theta_bin"] < cfg.n_theta
+        assert 0 <= res[i]["xy_row"] < n and 0 <= res[i]["xy_col"] < n
+
+
 def test_masked_equals_premasked(fb, dev):  # test_matcher.cpp:374-387
     cfg, delta, _ = fb.baseline_config(2)
     f, g, mf, mg, _ = fb.synth_pairs_host(fb.synth_spec(2), 9, 2)
@@ -615,6 +636,43 @@ def test_brute_force_on_odd_grid_matches_oracle(fb, orc, dev):
     for i in range(2):
         o = orc.brute_force(f[i].astype(np.float64), g[i].astype(np.float64), thetas, 0.4)
         bf_compare(res[i], o, n, stats)
+
+
+@pytest.mark.parametrize("n,count,chunk", [(255, 5, 0), (65, 8, 3)])
+def test_odometry_on_odd_grid_equals_pairwise_matching(fb, orc, dev, n, count, chunk):
+    """The odometry chain on an embedded grid (Bluestein rotation stage, masked
+    scans stored once per scan at np^2): pair k == scan_match(scan k, scan k+1)
+    and the oracle's bins; a bad value flags exactly the pairs that use the scan."""
+    spec = fb.synth_spec(2, n=n, delta=0.5 * 256 / n)
+    cfg = fb.MatchConfig.for_grid(n, spec.delta, 360, t_theta=2.0, t_xy=1.0)
+    f, g, mf, mg, _ = fb.synth_pairs_host(spec, 40, (count + 1) // 2)
+    scans = np.stack([x for pair in zip(f, g) for x in pair])[:count]
+    masks = np.stack([x for pair in zip(mf, mg) for x in pair])[:count]
+    S, M = to_dev(dev, scans, masks)
+    m = fb.Matcher(cfg, max_batch=count - 1, chunk=chunk)
+    ts = torch.zeros((count - 1, cfg.n_theta), dtype=torch.float64, device=dev)
+    xs = torch.zeros((count - 1, n, n), dtype=torch.float32, device=dev)
+    odo = fb.decode_results(m.odometry(S, M, delta=spec.delta, theta_surface=ts, xy_surface=xs))
+    ref, rts, rxs = run_gpu(fb, dev, cfg, spec.delta, scans[:-1], scans[1:], masks[:-1], masks[1:])
+    t, x = ts.cpu().numpy(), xs.cpu().numpy()
+    assert np.abs(t - rts).max() <= 1e-5 * np.abs(rts).max()
+    assert np.abs(x - rxs).max() <= 1e-5 * np.abs(rxs).max()
+    assert (odo["status"] == fb.OK).all()
+    oc = oracle_cfg(orc, cfg)
+    stats = []
+    for k in range(count - 1):
+        assert (odo[k]["theta_bin"], odo[k]["xy_row"], odo[k]["xy_col"]) == \
+            (ref[k]["theta_bin"], ref[k]["xy_row"], ref[k]["xy_col"])
+        if k < 2:
+            o = orc.scan_match(scans[k].astype(np.float64), scans[k + 1].astype(np.float64), oc, spec.delta,
+                               masks[k].astype(np.float64), masks[k + 1].astype(np.float64))
+            compare(odo[k], t[k], x[k], (o.theta_bin, o.xy_row, o.xy_col), (o.theta, o.tx, o.ty),
+                    o.theta_surface, o.xy_surface, spec.delta, stats)
+    bad = scans.copy()
+    bad[2, 5, 5] = np.inf
+    B, = to_dev(dev, bad)
+    st = fb.decode_results(m.odometry(B, M, delta=spec.delta))["status"]
+    assert list(st) == [fb.OK, fb.ERR_NONFINITE, fb.ERR_NONFINITE] + [fb.OK] * (count - 4)
 
 
 # ---- configuration sweep: every MatchConfig knob against the oracle ----
