@@ -193,6 +193,278 @@ cudaError_t cols_bs(const Params& p, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+
+// ---------------------------------------------------------------- N = 255
+// The reference's default grid (matcher.hpp:13-26: n_xy = 255) gets an exact
+// prime-factor DFT instead of Bluestein: 255 = 15 * 17 (coprime), so by the
+// Good-Thomas map n = (17 n1 + 15 n2) mod 255, k = (136 k1 + 120 k2) mod 255
+// (136 = 17 * (17^-1 mod 15), 120 = 15 * (15^-1 mod 17)) the DFT is 15
+// 17-point DFTs over n2 followed by 17 15-point DFTs over n1 with no twiddles
+// (15 = 3 * 5 by the same map: n1 = (5a + 3b) mod 15, k1 = (10c + 6d) mod 15).
+// The small DFTs are straight-line code with compile-time constants: ~31 flops
+// per point against ~180 for the two length-512 Bluestein transforms.
+constexpr int kPfaN = 255;
+
+__device__ __forceinline__ float2 f2(float x, float y) { return make_float2(x, y); }
+
+// 3-point DFT, SIGN = -1 forward / +1 inverse (unnormalised)
+template <int SIGN>
+__device__ __forceinline__ void dft3(float2& x0, float2& x1, float2& x2) {
+    constexpr float h = 8.660254038e-01f;  // sqrt(3)/2
+    const float2 t1 = cadd(x1, x2), t2 = csub(x1, x2);
+    const float2 m = f2(fmaf(-0.5f, t1.x, x0.x), fmaf(-0.5f, t1.y, x0.y));
+    x0 = cadd(x0, t1);
+    // X1 = m + SIGN * i * h * t2, X2 = m - SIGN * i * h * t2
+    const float2 r = SIGN < 0 ? f2(h * t2.y, -h * t2.x) : f2(-h * t2.y, h * t2.x);
+    x1 = cadd(m, r);
+    x2 = csub(m, r);
+}
+
+// 5-point DFT
+template <int SIGN>
+__device__ __forceinline__ void dft5(float2& x0, float2& x1, float2& x2, float2& x3, float2& x4) {
+    constexpr float c1 = 3.090169944e-01f, c2 = -8.090169944e-01f;  // cos(2 pi / 5), cos(4 pi / 5)
+    constexpr float s1 = 9.510565163e-01f, s2 = 5.877852523e-01f;   // sin(2 pi / 5), sin(4 pi / 5)
+    const float2 t1 = cadd(x1, x4), t2 = cadd(x2, x3), t3 = csub(x1, x4), t4 = csub(x2, x3);
+    const float2 a1 = f2(fmaf(c2, t2.x, fmaf(c1, t1.x, x0.x)), fmaf(c2, t2.y, fmaf(c1, t1.y, x0.y)));
+    const float2 a2 = f2(fmaf(c1, t2.x, fmaf(c2, t1.x, x0.x)), fmaf(c1, t2.y, fmaf(c2, t1.y, x0.y)));
+    const float2 b1 = f2(fmaf(s2, t4.x, s1 * t3.x), fmaf(s2, t4.y, s1 * t3.y));
+    const float2 b2 = f2(fmaf(-s1, t4.x, s2 * t3.x), fmaf(-s1, t4.y, s2 * t3.y));
+    x0 = cadd(x0, cadd(t1, t2));
+    // forward: X1 = a1 - i b1, X4 = a1 + i b1, X2 = a2 - i b2, X3 = a2 + i b2
+    const float2 r1 = SIGN < 0 ? f2(b1.y, -b1.x) : f2(-b1.y, b1.x);
+    const float2 r2 = SIGN < 0 ? f2(b2.y, -b2.x) : f2(-b2.y, b2.x);
+    x1 = cadd(a1, r1);
+    x4 = csub(a1, r1);
+    x2 = cadd(a2, r2);
+    x3 = csub(a2, r2);
+}
+
+// 15-point DFT (natural order in and out) as 3 x 5 prime factor
+template <int SIGN>
+__device__ __forceinline__ void dft15(float2 (&x)[15]) {
+    float2 t[3][5];
+#pragma unroll
+    for (int b = 0; b < 5; ++b) {
+        float2 u0 = x[(3 * b) % 15], u1 = x[(5 + 3 * b) % 15], u2 = x[(10 + 3 * b) % 15];
+        dft3<SIGN>(u0, u1, u2);
+        t[0][b] = u0;
+        t[1][b] = u1;
+        t[2][b] = u2;
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        dft5<SIGN>(t[c][0], t[c][1], t[c][2], t[c][3], t[c][4]);
+#pragma unroll
+        for (int d = 0; d < 5; ++d) x[(10 * c + 6 * d) % 15] = t[c][d];
+    }
+}
+
+// 17-point DFT (natural order in and out), symmetric form:
+// X[k] = x0 + sum_j (x_j + x_{17-j}) cos(2 pi jk/17) -/+ i (x_j - x_{17-j}) sin(2 pi jk/17)
+template <int SIGN>
+__device__ __forceinline__ void dft17(float2 (&x)[17]) {
+    constexpr float C[9] = {1.000000000e+00f, 9.324722294e-01f, 7.390089172e-01f, 4.457383558e-01f, 9.226835946e-02f,
+                            -2.736629901e-01f, -6.026346364e-01f, -8.502171357e-01f, -9.829730997e-01f};
+    constexpr float S[9] = {0.000000000e+00f, 3.612416662e-01f, 6.736956436e-01f, 8.951632914e-01f, 9.957341763e-01f,
+                            9.618256432e-01f, 7.980172273e-01f, 5.264321629e-01f, 1.837495178e-01f};
+    float2 a[8], b[8];
+#pragma unroll
+    for (int j = 1; j <= 8; ++j) {
+        a[j - 1] = cadd(x[j], x[17 - j]);
+        b[j - 1] = csub(x[j], x[17 - j]);
+    }
+    const float2 x0 = x[0];
+    float2 s0 = x0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s0 = cadd(s0, a[j]);
+    x[0] = s0;
+#pragma unroll
+    for (int k = 1; k <= 8; ++k) {
+        float ax = x0.x, ay = x0.y, bx = 0.f, by = 0.f;
+#pragma unroll
+        for (int j = 1; j <= 8; ++j) {
+            const int m = (j * k) % 17;
+            const float cm = m <= 8 ? C[m] : C[17 - m];
+            const float sm = m <= 8 ? S[m] : -S[17 - m];
+            ax = fmaf(cm, a[j - 1].x, ax);
+            ay = fmaf(cm, a[j - 1].y, ay);
+            bx = fmaf(sm, b[j - 1].y, bx);
+            by = fmaf(sm, b[j - 1].x, by);
+        }
+        // forward: X[k] = (ax + bx, ay - by), X[17 - k] = (ax - bx, ay + by)
+        if (SIGN < 0) {
+            x[k] = f2(ax + bx, ay - by);
+            x[17 - k] = f2(ax - bx, ay + by);
+        } else {
+            x[k] = f2(ax - bx, ay + by);
+            x[17 - k] = f2(ax + bx, ay - by);
+        }
+    }
+}
+
+// One 255-point DFT per 17 threads (slot s of transform buffer `buf`, natural
+// order in and out, in place). Every thread of the CTA must call it (it holds
+// __syncthreads); `live` masks the threads outside a transform.
+template <int SIGN>
+__device__ __forceinline__ void dft255_smem(float2* buf, int s, bool live) {
+    if (live && s < 15) {  // 15 17-point DFTs over n2 for n1 = s, in place
+        float2 x[17];
+        const int base = 17 * s;
+#pragma unroll
+        for (int n2 = 0; n2 < 17; ++n2) {
+            int i = base + 15 * n2;
+            i -= i >= kPfaN ? kPfaN : 0;
+            x[n2] = buf[i];
+        }
+        dft17<SIGN>(x);
+#pragma unroll
+        for (int n2 = 0; n2 < 17; ++n2) {
+            int i = base + 15 * n2;
+            i -= i >= kPfaN ? kPfaN : 0;
+            buf[i] = x[n2];
+        }
+    }
+    __syncthreads();
+    float2 y[15];
+    if (live) {  // 17 15-point DFTs over n1 for k2 = s
+        const int base = 15 * s;
+#pragma unroll
+        for (int n1 = 0; n1 < 15; ++n1) {
+            int i = base + 17 * n1;
+            i -= i >= kPfaN ? kPfaN : 0;
+            y[n1] = buf[i];
+        }
+        dft15<SIGN>(y);
+    }
+    __syncthreads();
+    if (live) {  // X[(136 k1 + 120 s) mod 255]
+        int i = (120 * s) % kPfaN;
+#pragma unroll
+        for (int k1 = 0; k1 < 15; ++k1) {
+            buf[i] = y[k1];
+            i += 136;
+            i -= i >= kPfaN ? kPfaN : 0;
+        }
+    }
+    __syncthreads();
+}
+
+constexpr int kPfaRows = 15;         // K1a: rows per CTA (17 CTAs per pair)
+constexpr int kPfaSP = kPfaN + 1;    // float2 per transform buffer
+constexpr int kPfaRowThreads = 256;  // 15 transforms x 17 slots (+1 idle)
+
+// K1a, N = 255: as k_rot_rows_bs with the prime-factor DFT; stores only the
+// columns K1b reads (k < zcols and their mirrors k > N - zcols).
+__global__ void __launch_bounds__(kPfaRowThreads) k_rot_rows_pfa255(Params p) {
+    __shared__ float2 buf[kPfaRows * kPfaSP];
+    constexpr int n = kPfaN;
+    const int np = p.np, pair = blockIdx.y, y0 = blockIdx.x * kPfaRows;
+    const int x = threadIdx.x;
+    const bool xin = x < n;
+    const float hx = xin ? __ldg(p.hann + x) : 0.f;
+    int badf = 0, badg = 0;
+    size_t fi = pair, gi = pair;
+    if (p.chain) {
+        fi = 2 * (size_t)pair;
+        gi = (size_t)min(2 * pair + 1, p.n_scans - 1);
+    }
+#pragma unroll 3
+    for (int r = 0; r < kPfaRows; ++r) {
+        const int y = y0 + r;
+        const float *fp, *gp, *mfp = nullptr, *mgp = nullptr;
+        float *ftp, *gtp;
+        if (p.chain) {
+            fp = p.f + (fi * n + y) * n;
+            gp = p.f + (gi * n + y) * n;
+            if (p.mf) {
+                mfp = p.mf + (fi * n + y) * n;
+                mgp = p.mf + (gi * n + y) * n;
+            }
+            ftp = p.ft + fi * np * np + (size_t)y * np;
+            gtp = p.ft + gi * np * np + (size_t)y * np;
+        } else {
+            fp = p.f + ((size_t)pair * n + y) * n;
+            gp = p.g + ((size_t)pair * n + y) * n;
+            if (p.mf) {
+                mfp = p.mf + ((size_t)pair * n + y) * n;
+                mgp = p.mg + ((size_t)pair * n + y) * n;
+            }
+            ftp = p.ft + (size_t)pair * np * np + (size_t)y * np;
+            gtp = p.gt + (size_t)pair * np * np + (size_t)y * np;
+        }
+        if (xin) {
+            float fv = __ldg(fp + x), gv = __ldg(gp + x);
+            if (mfp) {
+                const float ma = __ldg(mfp + x), mb = __ldg(mgp + x);
+                if (!(ma >= 0.0f && ma <= 1.0f)) badf |= 2;
+                if (!(mb >= 0.0f && mb <= 1.0f)) badg |= 2;
+                fv *= ma;
+                gv *= mb;
+            }
+            if (!isfinite(fv)) badf |= 1;
+            if (!isfinite(gv)) badg |= 1;
+            ftp[x] = fv;
+            gtp[x] = gv;
+            const float w = __ldg(p.hann + y) * hx;
+            buf[r * kPfaSP + x] = f2(fv * w, gv * w);
+        }
+    }
+    __syncthreads();
+    const int tr = threadIdx.x / 17, s = threadIdx.x % 17;
+    const bool live = tr < kPfaRows;
+    dft255_smem<-1>(buf + (live ? tr : 0) * kPfaSP, s, live);
+    // the columns K1b reads, coalesced per row
+    const int zc = p.zcols;
+#pragma unroll 3
+    for (int r = 0; r < kPfaRows; ++r)
+        if (xin && (x < zc || x > n - zc)) p.zbuf[((size_t)pair * n + y0 + r) * n + x] = buf[r * kPfaSP + x];
+    if (p.chain) {
+        if (badf) atomicOr(p.flags + fi, badf);
+        if (badg) atomicOr(p.flags + gi, badg);
+    } else if (badf | badg) {
+        atomicOr(p.flags + pair, badf | badg);
+    }
+}
+
+constexpr int kPfaColThreads = 288;  // 16 transforms (8 columns u, 8 mirrors) x 17 slots
+
+// K1b, N = 255: 8 columns u0..u0+7 and their mirrors (N - u) mod N, F/G
+// separation, |F|, |G| times the band into the (|F|,|G|) tiles (as k_rot_cols_bs).
+__global__ void __launch_bounds__(kPfaColThreads) k_rot_cols_pfa255(Params p) {
+    __shared__ float2 buf[16 * kPfaSP];
+    constexpr int n = kPfaN;
+    const int W = p.nw, pair = blockIdx.y, u0 = blockIdx.x * 8;
+    const int ulim = min(W, p.zcols);
+    const float2* z = p.zbuf + (size_t)pair * n * n;
+    for (int e = threadIdx.x; e < n * 16; e += kPfaColThreads) {
+        const int row = e >> 4, c = e & 15;
+        const int u = u0 + (c & 7);
+        const int col = c < 8 ? u : (n - u) % n;
+        buf[c * kPfaSP + row] = u < ulim ? z[(size_t)row * n + col] : f2(0.f, 0.f);
+    }
+    __syncthreads();
+    const int tr = threadIdx.x / 17, s = threadIdx.x % 17;
+    const bool live = tr < 16;
+    dft255_smem<-1>(buf + (live ? tr : 0) * kPfaSP, s, live);
+    const int cn = n / 2;
+    float2* out = reinterpret_cast<float2*>(p.mag) + (size_t)pair * p.mag_plane;
+    for (int o = threadIdx.x; o < n * 8; o += kPfaColThreads) {
+        const int cc = o & 7, vc = o >> 3;
+        const int uu = u0 + cc;
+        if (uu >= W) continue;
+        const int vn = (vc - cn + n) % n;  // natural row of centred row vc
+        const int vm = (n - vn) % n;       // row of -v
+        const float2 z1 = buf[cc * kPfaSP + vn];
+        const float2 z2 = buf[(8 + cc) * kPfaSP + vm];
+        const float fr = z1.x + z2.x, fi = z1.y - z2.y;  // Z1 + conj(Z2)
+        const float gr = z1.x - z2.x, gi = z1.y + z2.y;  // Z1 - conj(Z2)
+        const int2 bd = __ldg(p.band + vc);
+        const bool in = (uu >= bd.x) && (uu <= bd.y);
+        out[((size_t)(uu >> 3) * n + vc) * 8 + (uu & 7)] =
+            in ? make_float2(0.5f * sqrtf(fr * fr + fi * fi), 0.5f * sqrtf(gr * gr + gi * gi)) : make_float2(0.f, 0.f);
+    }
+}
 }  // namespace
 
 #define FSCAN_DISPATCH_L(FN)                      \
@@ -205,7 +477,19 @@ cudaError_t cols_bs(const Params& p, cudaStream_t s) {
         default: return cudaErrorInvalidValue;    \
     }
 
-cudaError_t launch_rot_rows_bs(const Params& p, cudaStream_t s) { FSCAN_DISPATCH_L(rows_bs) }
-cudaError_t launch_rot_cols_bs(const Params& p, cudaStream_t s) { FSCAN_DISPATCH_L(cols_bs) }
+cudaError_t launch_rot_rows_bs(const Params& p, cudaStream_t s) {
+    if (p.n == kPfaN) {
+        k_rot_rows_pfa255<<<dim3(kPfaN / kPfaRows, p.batch), kPfaRowThreads, 0, s>>>(p);
+        return cudaGetLastError();
+    }
+    FSCAN_DISPATCH_L(rows_bs)
+}
+cudaError_t launch_rot_cols_bs(const Params& p, cudaStream_t s) {
+    if (p.n == kPfaN) {
+        k_rot_cols_pfa255<<<dim3((p.zcols + 7) / 8, p.batch), kPfaColThreads, 0, s>>>(p);
+        return cudaGetLastError();
+    }
+    FSCAN_DISPATCH_L(cols_bs)
+}
 
 }  // namespace fscan_detail
