@@ -351,7 +351,7 @@ __device__ __forceinline__ void dft255_smem(float2* buf, int s, bool live) {
 }
 
 constexpr int kPfaRows = 15;         // K1a: rows per CTA (17 CTAs per pair)
-constexpr int kPfaSP = kPfaN + 1;    // float2 per transform buffer
+constexpr int kPfaSP = kPfaN + 2;    // float2 per transform buffer (odd: rows on distinct banks)
 constexpr int kPfaRowThreads = 256;  // 15 transforms x 17 slots (+1 idle)
 
 // K1a, N = 255: as k_rot_rows_bs with the prime-factor DFT; stores only the
@@ -369,45 +369,43 @@ __global__ void __launch_bounds__(kPfaRowThreads) k_rot_rows_pfa255(Params p) {
         fi = 2 * (size_t)pair;
         gi = (size_t)min(2 * pair + 1, p.n_scans - 1);
     }
-#pragma unroll 3
-    for (int r = 0; r < kPfaRows; ++r) {
-        const int y = y0 + r;
-        const float *fp, *gp, *mfp = nullptr, *mgp = nullptr;
-        float *ftp, *gtp;
-        if (p.chain) {
-            fp = p.f + (fi * n + y) * n;
-            gp = p.f + (gi * n + y) * n;
-            if (p.mf) {
-                mfp = p.mf + (fi * n + y) * n;
-                mgp = p.mf + (gi * n + y) * n;
-            }
-            ftp = p.ft + fi * np * np + (size_t)y * np;
-            gtp = p.ft + gi * np * np + (size_t)y * np;
-        } else {
-            fp = p.f + ((size_t)pair * n + y) * n;
-            gp = p.g + ((size_t)pair * n + y) * n;
-            if (p.mf) {
-                mfp = p.mf + ((size_t)pair * n + y) * n;
-                mgp = p.mg + ((size_t)pair * n + y) * n;
-            }
-            ftp = p.ft + (size_t)pair * np * np + (size_t)y * np;
-            gtp = p.gt + (size_t)pair * np * np + (size_t)y * np;
+    // five rows per round with every load issued before any use (the stores of
+    // f~, g~ could alias the inputs for the compiler, so it would not hoist them)
+    constexpr int RB = 5;
+#pragma unroll 1
+    for (int r0 = 0; r0 < kPfaRows; r0 += RB) {
+        float fv[RB], gv[RB], ma[RB], mb[RB];
+#pragma unroll
+        for (int i = 0; i < RB; ++i) {
+            const int y = y0 + r0 + i;
+            const size_t fo = (p.chain ? fi * n + y : (size_t)pair * n + y) * n + x;
+            const size_t go = (p.chain ? gi * n + y : (size_t)pair * n + y) * n + x;
+            const float* gsrc = p.chain ? p.f : p.g;
+            const float* mgsrc = p.chain ? p.mf : p.mg;
+            fv[i] = xin ? __ldg(p.f + fo) : 0.f;
+            gv[i] = xin ? __ldg(gsrc + go) : 0.f;
+            ma[i] = (xin && p.mf) ? __ldg(p.mf + fo) : 1.f;
+            mb[i] = (xin && p.mf) ? __ldg(mgsrc + go) : 1.f;
         }
-        if (xin) {
-            float fv = __ldg(fp + x), gv = __ldg(gp + x);
-            if (mfp) {
-                const float ma = __ldg(mfp + x), mb = __ldg(mgp + x);
-                if (!(ma >= 0.0f && ma <= 1.0f)) badf |= 2;
-                if (!(mb >= 0.0f && mb <= 1.0f)) badg |= 2;
-                fv *= ma;
-                gv *= mb;
+#pragma unroll
+        for (int i = 0; i < RB; ++i) {
+            const int y = y0 + r0 + i;
+            if (!xin) continue;
+            float a = fv[i], b = gv[i];
+            if (p.mf) {
+                if (!(ma[i] >= 0.0f && ma[i] <= 1.0f)) badf |= 2;
+                if (!(mb[i] >= 0.0f && mb[i] <= 1.0f)) badg |= 2;
+                a *= ma[i];
+                b *= mb[i];
             }
-            if (!isfinite(fv)) badf |= 1;
-            if (!isfinite(gv)) badg |= 1;
-            ftp[x] = fv;
-            gtp[x] = gv;
+            if (!isfinite(a)) badf |= 1;
+            if (!isfinite(b)) badg |= 1;
+            float* ftp = p.ft + (p.chain ? fi : (size_t)pair) * np * np + (size_t)y * np;
+            float* gtp = (p.chain ? p.ft + gi * np * np : p.gt + (size_t)pair * np * np) + (size_t)y * np;
+            ftp[x] = a;
+            gtp[x] = b;
             const float w = __ldg(p.hann + y) * hx;
-            buf[r * kPfaSP + x] = f2(fv * w, gv * w);
+            buf[(r0 + i) * kPfaSP + x] = f2(a * w, b * w);
         }
     }
     __syncthreads();
@@ -427,26 +425,39 @@ __global__ void __launch_bounds__(kPfaRowThreads) k_rot_rows_pfa255(Params p) {
     }
 }
 
+constexpr int kPfaCSP = kPfaN + 2;    // K1b buffer stride: the 16 columns of a row on distinct banks
 constexpr int kPfaColThreads = 288;  // 16 transforms (8 columns u, 8 mirrors) x 17 slots
 
 // K1b, N = 255: 8 columns u0..u0+7 and their mirrors (N - u) mod N, F/G
 // separation, |F|, |G| times the band into the (|F|,|G|) tiles (as k_rot_cols_bs).
 __global__ void __launch_bounds__(kPfaColThreads) k_rot_cols_pfa255(Params p) {
-    __shared__ float2 buf[16 * kPfaSP];
+    __shared__ float2 buf[16 * kPfaCSP];
     constexpr int n = kPfaN;
     const int W = p.nw, pair = blockIdx.y, u0 = blockIdx.x * 8;
     const int ulim = min(W, p.zcols);
     const float2* z = p.zbuf + (size_t)pair * n * n;
-    for (int e = threadIdx.x; e < n * 16; e += kPfaColThreads) {
-        const int row = e >> 4, c = e & 15;
-        const int u = u0 + (c & 7);
-        const int col = c < 8 ? u : (n - u) % n;
-        buf[c * kPfaSP + row] = u < ulim ? z[(size_t)row * n + col] : f2(0.f, 0.f);
+    constexpr int U = 5;  // loads in flight per thread
+#pragma unroll 1
+    for (int e0 = threadIdx.x; e0 < n * 16; e0 += U * kPfaColThreads) {
+        float2 v[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            const int e = e0 + k * kPfaColThreads;
+            const int row = e >> 4, c = e & 15;
+            const int u = u0 + (c & 7);
+            const int col = c < 8 ? u : (n - u) % n;
+            v[k] = (e < n * 16 && u < ulim) ? z[(size_t)row * n + col] : f2(0.f, 0.f);
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            const int e = e0 + k * kPfaColThreads;
+            if (e < n * 16) buf[(e & 15) * kPfaCSP + (e >> 4)] = v[k];
+        }
     }
     __syncthreads();
     const int tr = threadIdx.x / 17, s = threadIdx.x % 17;
     const bool live = tr < 16;
-    dft255_smem<-1>(buf + (live ? tr : 0) * kPfaSP, s, live);
+    dft255_smem<-1>(buf + (live ? tr : 0) * kPfaCSP, s, live);
     const int cn = n / 2;
     float2* out = reinterpret_cast<float2*>(p.mag) + (size_t)pair * p.mag_plane;
     for (int o = threadIdx.x; o < n * 8; o += kPfaColThreads) {
@@ -455,8 +466,8 @@ __global__ void __launch_bounds__(kPfaColThreads) k_rot_cols_pfa255(Params p) {
         if (uu >= W) continue;
         const int vn = (vc - cn + n) % n;  // natural row of centred row vc
         const int vm = (n - vn) % n;       // row of -v
-        const float2 z1 = buf[cc * kPfaSP + vn];
-        const float2 z2 = buf[(8 + cc) * kPfaSP + vm];
+        const float2 z1 = buf[cc * kPfaCSP + vn];
+        const float2 z2 = buf[(8 + cc) * kPfaCSP + vm];
         const float fr = z1.x + z2.x, fi = z1.y - z2.y;  // Z1 + conj(Z2)
         const float gr = z1.x - z2.x, gi = z1.y + z2.y;  // Z1 - conj(Z2)
         const int2 bd = __ldg(p.band + vc);
