@@ -32,6 +32,8 @@
 
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 namespace fscan_fft {
 
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
@@ -273,6 +275,11 @@ __device__ __forceinline__ float2 twiddle(const SmemTw& tw, int idx) {
     return SIGN < 0 ? w : make_float2(w.x, -w.y);
 }
 
+// Radix-16 twiddles as powers of one table read (global tables) or all read
+// from the table (shared-memory tables).
+template <typename TW>
+constexpr bool kTwPow = !std::is_same_v<TW, SmemTw>;
+
 // One Stockham stage. Ns = span before this stage, R = radix.
 // Exchange barrier: a warp barrier when every thread of the transform (and of
 // any transform sharing its buffer) is in one warp, else the CTA barrier.
@@ -298,8 +305,29 @@ __device__ __forceinline__ void stage(float2 (&v)[16], int t, const L& lay, cons
         const int k = b & (Ns - 1);
         if constexpr (Ns > 1) {
             constexpr int q = N / (Ns * R);  // W_{Ns R}^x = tw[x * q]
+            if constexpr (R == 16 && kTwPow<TW>) {
+                // the 15 powers w^r of w = W_{16 Ns}^k from four table reads (w, w^2,
+                // w^4, w^8) and 11 products: the exchanges and twiddle reads share
+                // the L1 data pipe these kernels are bound by, the FMA pipe has room
+                // (global tables only: K4's shared-memory table measured faster as is;
+                // <= 3 rounded products per twiddle, surfaces stay ~2e-7 of the oracle)
+                float2 w[16];
+                w[1] = twiddle<SIGN>(tw, k * q);
+                w[2] = twiddle<SIGN>(tw, 2 * k * q);
+                w[4] = twiddle<SIGN>(tw, 4 * k * q);
+                w[8] = twiddle<SIGN>(tw, 8 * k * q);
+                w[3] = cmul(w[1], w[2]);
+                w[5] = cmul(w[4], w[1]);
+                w[6] = cmul(w[4], w[2]);
+                w[7] = cmul(w[4], w[3]);
 #pragma unroll
-            for (int r = 1; r < R; ++r) u[r] = cmul(u[r], twiddle<SIGN>(tw, r * k * q));
+                for (int r = 9; r < 16; ++r) w[r] = cmul(w[8], w[r - 8]);
+#pragma unroll
+                for (int r = 1; r < R; ++r) u[r] = cmul(u[r], w[r]);
+            } else {
+#pragma unroll
+                for (int r = 1; r < R; ++r) u[r] = cmul(u[r], twiddle<SIGN>(tw, r * k * q));
+            }
         }
         dft_r<R, SIGN>(u);
         if constexpr (LAST) {
