@@ -82,6 +82,7 @@ struct fscan_ctx {
     float2* tw_n = nullptr;
     float2* tw_k = nullptr;
     float2* tw_k2 = nullptr;
+    float2* tw_rk = nullptr;  // W_256^{r k} at (r-1)*16 + k (K4's radix-16 stage)
     float2* tw_m = nullptr;
     float* hann = nullptr;
     int2* band = nullptr;
@@ -320,6 +321,7 @@ Params base_params(fscan_ctx* ctx, Lane& l, int batch, double delta) {
     p.tw_n = ctx->tw_n;
     p.tw_k = ctx->tw_k;
     p.tw_k2 = ctx->tw_k2;
+    p.tw_rk = ctx->tw_rk;
     p.tw_m = ctx->tw_m;
     p.hann = ctx->hann;
     p.band = ctx->band;
@@ -591,6 +593,16 @@ fscan_status fscan_ctx_create(int device, const fscan_config* cfg_in, int max_ba
     CK(cudaMalloc(&ctx->tw_m, sizeof(float2) * twm.size()));
     CK(cudaMemcpy(ctx->tw_k, twk.data(), sizeof(float2) * twk.size(), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(ctx->tw_k2, twk2.data(), sizeof(float2) * twk2.size(), cudaMemcpyHostToDevice));
+    {
+        std::vector<float2> rk(240);
+        for (int r = 1; r < 16; ++r)
+            for (int k = 0; k < 16; ++k) {
+                const double a = -2.0 * kPi * ((r * k) % 256) / 256.0;
+                rk[(r - 1) * 16 + k] = make_float2((float)std::cos(a), (float)std::sin(a));
+            }
+        CK(cudaMalloc(&ctx->tw_rk, sizeof(float2) * rk.size()));
+        CK(cudaMemcpy(ctx->tw_rk, rk.data(), sizeof(float2) * rk.size(), cudaMemcpyHostToDevice));
+    }
     CK(cudaMemcpy(ctx->tw_m, twm.data(), sizeof(float2) * twm.size(), cudaMemcpyHostToDevice));
     CK(cudaMalloc(&ctx->hann, sizeof(float) * n));
     CK(cudaMalloc(&ctx->band, sizeof(int2) * n));
@@ -634,6 +646,7 @@ void fscan_ctx_destroy(fscan_ctx* ctx) {
     cudaFree(ctx->tw_n);
     cudaFree(ctx->tw_k);
     cudaFree(ctx->tw_k2);
+    cudaFree(ctx->tw_rk);
     cudaFree(ctx->tw_m);
     cudaFree(ctx->hann);
     cudaFree(ctx->band);

@@ -275,10 +275,28 @@ __device__ __forceinline__ float2 twiddle(const SmemTw& tw, int idx) {
     return SIGN < 0 ? w : make_float2(w.x, -w.y);
 }
 
+// Shared-memory twiddles with the span-16 stage's factors as a [r][k] matrix
+// rk[(r-1)*16 + k] = W_256^{r k}: the 16 lanes' k are consecutive, so each read
+// is one conflict-free wavefront (the linear table's r*k pattern is gcd(r, 16)-
+// way conflicted); `lin` is the linear table W_L for the other stages.
+struct SmemTwRK {
+    const float2* rk;
+    const float2* lin;
+};
+
+template <int SIGN>
+__device__ __forceinline__ float2 twiddle(const SmemTwRK& tw, int idx) {
+    const float2 w = tw.lin[idx];
+    return SIGN < 0 ? w : make_float2(w.x, -w.y);
+}
+
+template <typename TW>
+constexpr bool kTwRK = std::is_same_v<TW, SmemTwRK>;
+
 // Radix-16 twiddles as powers of one table read (global tables) or all read
 // from the table (shared-memory tables).
 template <typename TW>
-constexpr bool kTwPow = !std::is_same_v<TW, SmemTw>;
+constexpr bool kTwPow = !std::is_same_v<TW, SmemTw> && !kTwRK<TW>;
 
 // One Stockham stage. Ns = span before this stage, R = radix.
 // Exchange barrier: a warp barrier when every thread of the transform (and of
@@ -305,7 +323,14 @@ __device__ __forceinline__ void stage(float2 (&v)[16], int t, const L& lay, cons
         const int k = b & (Ns - 1);
         if constexpr (Ns > 1) {
             constexpr int q = N / (Ns * R);  // W_{Ns R}^x = tw[x * q]
-            if constexpr (R == 16 && kTwPow<TW>) {
+            if constexpr (Ns == 16 && kTwRK<TW>) {
+                // W_{16 R}^{r k} = W_256^{(16/R) r k}
+#pragma unroll
+                for (int r = 1; r < R; ++r) {
+                    const float2 w = tw.rk[((16 / R) * r - 1) * 16 + k];
+                    u[r] = cmul(u[r], SIGN < 0 ? w : make_float2(w.x, -w.y));
+                }
+            } else if constexpr (R == 16 && kTwPow<TW>) {
                 // the 15 powers w^r of w = W_{16 Ns}^k from four table reads (w, w^2,
                 // w^4, w^8) and 11 products: the exchanges and twiddle reads share
                 // the L1 data pipe these kernels are bound by, the FMA pipe has room

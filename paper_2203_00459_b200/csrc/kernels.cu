@@ -646,8 +646,11 @@ struct XColGeom {
     static constexpr size_t WORK_FLOATS = FFT_FLOATS > TILE_FLOATS ? FFT_FLOATS : TILE_FLOATS;
     // twiddle tables staged behind the work area: W_K (K entries) and, below
     // N = 1024, W_M (3K; at 1024 it would push the CTA past half an SM's smem)
+    // (the K-point FFTs read the span-16 stage's factors from a [r][k] table,
+    // 240 entries, and, at K = 512 only, the last stage's from the linear W_K)
     static constexpr bool SMEM_WM = N <= 512;
-    static constexpr size_t TW_FLOATS = (size_t)2 * (N / 2) * (SMEM_WM ? 4 : 1);
+    static constexpr int TW_LIN = N / 2 > 256 ? N / 2 : 0;
+    static constexpr size_t TW_FLOATS = (size_t)2 * (240 + TW_LIN + (SMEM_WM ? 3 * (N / 2) : 0));
     static constexpr size_t SMEM = (WORK_FLOATS + TW_FLOATS) * sizeof(float);
     // explicit residency targets where ptxas' own choice leaves the SM
     // register-bound (N = 256: 4 CTAs of 192 threads; N = 1024: 2 of 384)
@@ -686,14 +689,16 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
     const float4* src = p.fgt + ((size_t)pair * (H + 1) + kq) * N;
     // stage the twiddle tables in shared memory (latency: the FFT stages and
     // input/combine twiddles read them ~90 times per thread)
-    float2* stw_k = reinterpret_cast<float2*>(smem + X::WORK_FLOATS);
-    float2* stw_m_s = stw_k + K;
-    for (int i = threadIdx.x; i < K; i += X::THREADS) stw_k[i] = __ldg(p.tw_k + i);
+    float2* stw_rk = reinterpret_cast<float2*>(smem + X::WORK_FLOATS);
+    float2* stw_k = stw_rk + 240;
+    float2* stw_m_s = stw_k + X::TW_LIN;
+    for (int i = threadIdx.x; i < 240; i += X::THREADS) stw_rk[i] = __ldg(p.tw_rk + i);
+    for (int i = threadIdx.x; i < X::TW_LIN; i += X::THREADS) stw_k[i] = __ldg(p.tw_k + i);
     if constexpr (X::SMEM_WM)
         for (int i = threadIdx.x; i < M; i += X::THREADS) stw_m_s[i] = __ldg(p.tw_m + i);
     auto stw_m_at = [&](int e) { return X::SMEM_WM ? stw_m_s[e] : __ldg(p.tw_m + e); };
     __syncthreads();
-    const fscan_fft::SmemTw twk{stw_k};
+    const fscan_fft::SmemTwRK twk{stw_rk, stw_k};
     const float2 w3q = w3(q);
     float2 a[16];
 #pragma unroll
