@@ -650,7 +650,11 @@ struct XColGeom {
     // 240 entries, and, at K = 512 only, the last stage's from the linear W_K)
     static constexpr bool SMEM_WM = N <= 512;
     static constexpr int TW_LIN = N / 2 > 256 ? N / 2 : 0;
-    static constexpr size_t TW_FLOATS = (size_t)2 * (240 + TW_LIN + (SMEM_WM ? 3 * (N / 2) : 0));
+    // W_M staged as two contiguous K-entry tables W_M^{n0}, W_M^{2 n0} below
+    // N = 512 (conflict-free; at N = 256 ptxas also keeps K4 spill-free at four
+    // CTAs/SM, +10% C2), as the linear M-entry table at 512 (measured faster)
+    static constexpr bool SPLIT_WM = N < 512;
+    static constexpr size_t TW_FLOATS = (size_t)2 * (240 + TW_LIN + (SMEM_WM ? (SPLIT_WM ? 2 : 3) * (N / 2) : 0));
     static constexpr size_t SMEM = (WORK_FLOATS + TW_FLOATS) * sizeof(float);
     // explicit residency targets where ptxas' own choice leaves the SM
     // register-bound (N = 256: 4 CTAs of 192 threads; N = 1024: 2 of 384)
@@ -694,9 +698,19 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
     float2* stw_m_s = stw_k + X::TW_LIN;
     for (int i = threadIdx.x; i < 240; i += X::THREADS) stw_rk[i] = __ldg(p.tw_rk + i);
     for (int i = threadIdx.x; i < X::TW_LIN; i += X::THREADS) stw_k[i] = __ldg(p.tw_k + i);
-    if constexpr (X::SMEM_WM)
+    if constexpr (X::SMEM_WM && X::SPLIT_WM) {
+        for (int i = threadIdx.x; i < K; i += X::THREADS) {
+            stw_m_s[i] = __ldg(p.tw_m + i);
+            stw_m_s[K + i] = __ldg(p.tw_m + 2 * i);
+        }
+    } else if constexpr (X::SMEM_WM) {
         for (int i = threadIdx.x; i < M; i += X::THREADS) stw_m_s[i] = __ldg(p.tw_m + i);
-    auto stw_m_at = [&](int e) { return X::SMEM_WM ? stw_m_s[e] : __ldg(p.tw_m + e); };
+    }
+    auto wq = [&](int n0, int qq) {
+        if constexpr (X::SMEM_WM && X::SPLIT_WM) return stw_m_s[(qq - 1) * K + n0];
+        else if constexpr (X::SMEM_WM) return stw_m_s[qq * n0];
+        else return __ldg(p.tw_m + qq * n0);
+    };
     __syncthreads();
     const fscan_fft::SmemTwRK twk{stw_rk, stw_k};
     const float2 w3q = w3(q);
@@ -706,7 +720,7 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
         const int n0 = t + m * T;
         const float4 u0 = src[n0], u1 = src[n0 + K];
         const float2 s = cadd(make_float2(u0.x, u0.y), cmul(w3q, make_float2(u1.x, u1.y)));
-        a[m] = q ? cmul(stw_m_at(n0 * q), s) : s;
+        a[m] = q ? cmul(wq(n0, q), s) : s;
     }
     fft_regs<K, -1, true>(a, t, bufA, twk);  // transforms of a warp share a buffer group
 #pragma unroll
@@ -716,7 +730,7 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
         const int n0 = t + m * T;
         const float4 u0 = src[n0], u1 = src[n0 + K];
         const float2 s = cadd(make_float2(u0.z, u0.w), cmul(w3q, make_float2(u1.z, u1.w)));
-        a[m] = q ? cmul(stw_m_at(n0 * q), s) : s;
+        a[m] = q ? cmul(wq(n0, q), s) : s;
     }
     fft_regs<K, -1, true>(a, t, bufB, twk);
 #pragma unroll
@@ -744,8 +758,8 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
         if (m < 16) {
             const int n0 = t + m * T;
             const float2 x0 = e0.get(n0);
-            const float2 x1 = cmul(cconj(stw_m_at(n0)), e1.get(n0));
-            const float2 x2 = cmul(cconj(stw_m_at(2 * n0)), e2.get(n0));
+            const float2 x1 = cmul(cconj(wq(n0, 1)), e1.get(n0));
+            const float2 x2 = cmul(cconj(wq(n0, 2)), e2.get(n0));
             accp[j] = cadd(x0, cadd(x1, x2));
             accn[j] = cadd(x0, cadd(cmul(w31, x1), cmul(w32, x2)));
         }
