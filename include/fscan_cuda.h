@@ -203,6 +203,20 @@ fscan_status fscan_ctx_set_phase_correlation(fscan_ctx* ctx, int on);
 fscan_status fscan_ctx_set_profiling(fscan_ctx* ctx, int on);
 fscan_status fscan_ctx_kernel_times(fscan_ctx* ctx, double* ms, int* launches, int n_kinds);
 
+/* CUDA-graph replay of repeated calls (off by default). When on,
+ * fscan_match_batch and fscan_odometry_batch capture their whole launch
+ * sequence (every chunk, every lane) into a CUDA graph the first time they
+ * see a given argument set (pointers, batch, delta, outputs) and replay it
+ * with one cudaGraphLaunch on later identical calls: small batches, e.g. one
+ * pair per radar sweep, stop paying ~10 launches of host overhead per call.
+ * Up to 8 graphs are cached (least recently used evicted); changing the
+ * context's configuration (phase correlation) or turning graphs off drops
+ * them. Results are identical to the non-graph path. Profiling mode bypasses
+ * graphs. */
+fscan_status fscan_ctx_set_graphs(fscan_ctx* ctx, int on);
+/* Graph cache statistics: captures and replays since the context was created. */
+fscan_status fscan_ctx_graph_stats(const fscan_ctx* ctx, int* captures, int* replays);
+
 #ifdef __cplusplus
 }
 #endif

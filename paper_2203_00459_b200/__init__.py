@@ -130,6 +130,8 @@ SYMBOLS = {
     "fscan_check_results": (C.c_int, [_P, C.c_int, _P, C.POINTER(C.c_int)]),
     "fscan_ctx_launches_last": (C.c_int, [_P]),
     "fscan_ctx_set_profiling": (C.c_int, [_P, C.c_int]),
+    "fscan_ctx_set_graphs": (C.c_int, [_P, C.c_int]),
+    "fscan_ctx_graph_stats": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "fscan_ctx_set_phase_correlation": (C.c_int, [_P, C.c_int]),
     "fscan_ctx_kernel_times": (C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_int), C.c_int]),
     "fscan_fscn_read_header": (C.c_int, [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_double), C.c_char_p,
@@ -309,6 +311,16 @@ class Matcher:
     def set_phase_correlation(self, on: bool):
         """Opt-in phase correlation in the translation stage (fscan_cuda.h)."""
         self._check(lib().fscan_ctx_set_phase_correlation(self._h, int(bool(on))), "set_phase_correlation")
+
+    def set_graphs(self, on: bool):
+        """CUDA-graph replay of repeated identical calls (fscan_ctx_set_graphs)."""
+        self._check(lib().fscan_ctx_set_graphs(self._h, int(bool(on))), "set_graphs")
+
+    def graph_stats(self) -> tuple:
+        """(captures, replays) of the graph cache."""
+        c, r = C.c_int(), C.c_int()
+        self._check(lib().fscan_ctx_graph_stats(self._h, C.byref(c), C.byref(r)), "graph_stats")
+        return c.value, r.value
 
     def set_profiling(self, on: bool):
         self._check(lib().fscan_ctx_set_profiling(self._h, int(bool(on))), "set_profiling")

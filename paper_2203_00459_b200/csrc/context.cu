@@ -97,6 +97,27 @@ struct fscan_ctx {
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof;
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_used = 0;
+    // CUDA-graph replay (fscan_ctx_set_graphs): cached executable graphs keyed
+    // by the call's arguments, captured on `cap`; ordering against non-graph
+    // work on the lanes and against replays on other streams through
+    // `lane_sync` (per lane) and `graph_ev`
+    struct GraphSlot {
+        std::vector<uintptr_t> key;
+        cudaGraphExec_t exec = nullptr;
+        unsigned long long used = 0;
+        int launches = 0;
+    };
+    int use_graphs = 0;
+    std::vector<GraphSlot> graphs;
+    unsigned long long graph_clock = 0;
+    int graph_captures = 0, graph_replays = 0;
+    cudaStream_t cap = nullptr;
+    cudaEvent_t graph_ev = nullptr;
+    cudaEvent_t lane_sync[kMaxLanes] = {};
+    cudaStream_t last_graph_stream = nullptr;
+    bool graph_launched = false;   // graph_ev holds the last replay
+    bool lanes_since_graph = false; // non-graph work was queued on the lanes since
+    bool capturing = false;
 };
 
 namespace {
@@ -428,7 +449,12 @@ fscan_status check_ctx(fscan_ctx* ctx, int batch) {
 template <typename F>
 fscan_status drive(fscan_ctx* ctx, int batch, cudaStream_t user, F&& per_chunk) {
     CK(cudaEventRecord(ctx->start_ev, user));
-    for (Lane& l : LaneRange{ctx}) CK(cudaStreamWaitEvent(l.stream, ctx->start_ev, 0));
+    for (Lane& l : LaneRange{ctx}) {
+        CK(cudaStreamWaitEvent(l.stream, ctx->start_ev, 0));
+        // after a graph replay on another stream, the lanes' workspace is free only once it ends
+        if (ctx->graph_launched && !ctx->capturing) CK(cudaStreamWaitEvent(l.stream, ctx->graph_ev, 0));
+    }
+    if (!ctx->capturing) ctx->lanes_since_graph = true;
     ctx->launches_last = 0;
     ctx->prof.clear();
     ctx->ev_used = 0;
@@ -444,6 +470,84 @@ fscan_status drive(fscan_ctx* ctx, int batch, cudaStream_t user, F&& per_chunk) 
         CK(cudaStreamWaitEvent(user, l.done, 0));
     }
     return FSCAN_OK;
+}
+
+constexpr size_t kMaxGraphs = 8;
+
+void drop_graphs(fscan_ctx* ctx) {
+    for (auto& g : ctx->graphs) cudaGraphExecDestroy(g.exec);
+    ctx->graphs.clear();
+}
+
+// drive() through the graph cache (fscan_ctx_set_graphs): replay the graph
+// captured for `key`, or capture drive()'s whole launch sequence on the
+// context's capture stream, instantiate it and replay it.
+template <typename F>
+fscan_status drive_graph(fscan_ctx* ctx, std::vector<uintptr_t> key, int batch, cudaStream_t user, F&& per_chunk) {
+    if (!ctx->use_graphs || ctx->profiling) return drive(ctx, batch, user, per_chunk);
+    if (!ctx->cap) {
+        CK(cudaStreamCreateWithFlags(&ctx->cap, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&ctx->graph_ev, cudaEventDisableTiming));
+        for (int i = 0; i < kMaxLanes; ++i) CK(cudaEventCreateWithFlags(&ctx->lane_sync[i], cudaEventDisableTiming));
+    }
+    fscan_ctx::GraphSlot* slot = nullptr;
+    for (auto& g : ctx->graphs)
+        if (g.key == key) slot = &g;
+    if (!slot) {
+        ctx->capturing = true;
+        cudaError_t e = cudaStreamBeginCapture(ctx->cap, cudaStreamCaptureModeThreadLocal);
+        if (e != cudaSuccess) {
+            ctx->capturing = false;
+            return cuda_fail(ctx, e, "cudaStreamBeginCapture");
+        }
+        fscan_status st = drive(ctx, batch, ctx->cap, per_chunk);
+        cudaGraph_t graph = nullptr;
+        e = cudaStreamEndCapture(ctx->cap, &graph);
+        ctx->capturing = false;
+        if (st != FSCAN_OK) {
+            if (graph) cudaGraphDestroy(graph);
+            return st;
+        }
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaStreamEndCapture");
+        cudaGraphExec_t exec = nullptr;
+        e = cudaGraphInstantiate(&exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaGraphInstantiate");
+        if (ctx->graphs.size() >= kMaxGraphs) {
+            auto lru = std::min_element(ctx->graphs.begin(), ctx->graphs.end(),
+                                        [](const auto& a, const auto& b) { return a.used < b.used; });
+            cudaGraphExecDestroy(lru->exec);
+            ctx->graphs.erase(lru);
+        }
+        ctx->graphs.push_back({std::move(key), exec, 0, ctx->launches_last});
+        slot = &ctx->graphs.back();
+        ++ctx->graph_captures;
+    } else {
+        ++ctx->graph_replays;
+    }
+    slot->used = ++ctx->graph_clock;
+    ctx->launches_last = slot->launches;
+    // order after non-graph work still queued on the lanes, and after a replay
+    // on another stream (both use the context's workspace)
+    if (ctx->lanes_since_graph) {
+        for (int i = 0; i < ctx->nlanes; ++i) {
+            CK(cudaEventRecord(ctx->lane_sync[i], ctx->lanes_[i].stream));
+            CK(cudaStreamWaitEvent(user, ctx->lane_sync[i], 0));
+        }
+        ctx->lanes_since_graph = false;
+    }
+    if (ctx->graph_launched && ctx->last_graph_stream != user) CK(cudaStreamWaitEvent(user, ctx->graph_ev, 0));
+    CK(cudaGraphLaunch(slot->exec, user));
+    CK(cudaEventRecord(ctx->graph_ev, user));
+    ctx->graph_launched = true;
+    ctx->last_graph_stream = user;
+    return FSCAN_OK;
+}
+
+uintptr_t key_bits(double d) {
+    uintptr_t u = 0;
+    std::memcpy(&u, &d, sizeof(double) < sizeof(u) ? sizeof(double) : sizeof(u));
+    return u;
 }
 
 }  // namespace
@@ -643,6 +747,12 @@ void fscan_ctx_destroy(fscan_ctx* ctx) {
     }
     if (ctx->start_ev) cudaEventDestroy(ctx->start_ev);
     for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
+    if (ctx->cap) cudaStreamSynchronize(ctx->cap);
+    drop_graphs(ctx);
+    if (ctx->cap) cudaStreamDestroy(ctx->cap);
+    if (ctx->graph_ev) cudaEventDestroy(ctx->graph_ev);
+    for (cudaEvent_t e : ctx->lane_sync)
+        if (e) cudaEventDestroy(e);
     cudaFree(ctx->tw_n);
     cudaFree(ctx->tw_k);
     cudaFree(ctx->tw_k2);
@@ -699,7 +809,17 @@ fscan_status fscan_match_batch(fscan_ctx* ctx, const float* d_f, const float* d_
         return fail(ctx, FSCAN_ERR_INVALID_ARGUMENT, "fscan_match_batch: bad pointers or delta");
     const size_t nn = (size_t)ctx->n * ctx->n;
     const int nt = ctx->cfg.n_theta;
-    return drive(ctx, batch, (cudaStream_t)stream, [&](Lane& l, int off, int cnt) {
+    std::vector<uintptr_t> key{1,
+                               (uintptr_t)d_f,
+                               (uintptr_t)d_g,
+                               (uintptr_t)d_mf,
+                               (uintptr_t)d_mg,
+                               (uintptr_t)batch,
+                               key_bits(delta),
+                               (uintptr_t)d_out,
+                               (uintptr_t)d_tsurf,
+                               (uintptr_t)d_xsurf};
+    return drive_graph(ctx, std::move(key), batch, (cudaStream_t)stream, [&](Lane& l, int off, int cnt) {
         Params p = base_params(ctx, l, cnt, delta);
         p.f = d_f + off * nn;
         p.g = d_g + off * nn;
@@ -895,7 +1015,15 @@ fscan_status fscan_odometry_batch(fscan_ctx* ctx, const float* d_scans, const fl
             CK(cudaMalloc(&l.chain_ms, (ctx->alloc_chunk + 2) * npp * sizeof(float)));
             if (npp != nn) CK(cudaMemset(l.chain_ms, 0, (ctx->alloc_chunk + 2) * npp * sizeof(float)));
         }
-    return drive(ctx, pairs, (cudaStream_t)stream, [&](Lane& l, int off, int cnt) {
+    std::vector<uintptr_t> key{2,
+                               (uintptr_t)d_scans,
+                               (uintptr_t)d_masks,
+                               (uintptr_t)n_scans,
+                               key_bits(delta),
+                               (uintptr_t)d_out,
+                               (uintptr_t)d_tsurf,
+                               (uintptr_t)d_xsurf};
+    return drive_graph(ctx, std::move(key), pairs, (cudaStream_t)stream, [&](Lane& l, int off, int cnt) {
         // pairs off .. off+cnt-1 register scans off .. off+cnt
         Params p = base_params(ctx, l, cnt, delta);
         p.f = d_scans + off * nn;
@@ -1013,7 +1141,23 @@ fscan_status fscan_match_batch_host(fscan_ctx* ctx, const float* f, const float*
 fscan_status fscan_ctx_set_phase_correlation(fscan_ctx* ctx, int on) {
     if (!ctx) return FSCAN_ERR_INVALID_ARGUMENT;
     std::lock_guard<std::mutex> g(ctx->mu);
+    if (ctx->phase != (on ? 1 : 0)) drop_graphs(ctx);  // captured with the old setting
     ctx->phase = on ? 1 : 0;
+    return FSCAN_OK;
+}
+
+fscan_status fscan_ctx_set_graphs(fscan_ctx* ctx, int on) {
+    if (!ctx) return FSCAN_ERR_INVALID_ARGUMENT;
+    std::lock_guard<std::mutex> g(ctx->mu);
+    ctx->use_graphs = on ? 1 : 0;
+    if (!on) drop_graphs(ctx);
+    return FSCAN_OK;
+}
+
+fscan_status fscan_ctx_graph_stats(const fscan_ctx* ctx, int* captures, int* replays) {
+    if (!ctx || !captures || !replays) return FSCAN_ERR_INVALID_ARGUMENT;
+    *captures = ctx->graph_captures;
+    *replays = ctx->graph_replays;
     return FSCAN_OK;
 }
 

@@ -583,6 +583,77 @@ def test_phase_correlation_matches_restatement(fb, orc, dev):
 
 
 
+# ---- CUDA-graph replay (fscan_ctx_set_graphs) ----
+
+def test_graph_replay_equals_direct_calls(fb, dev):
+    """Replayed graphs give byte-identical results, see in-place input updates,
+    re-capture on new arguments, interleave with non-graph calls and are
+    dropped when the configuration changes."""
+    cfg, delta, _ = fb.baseline_config(2)
+    f, g, mf, mg, _ = fb.synth_pairs_host(fb.synth_spec(2), 11, 3)
+    F, G, MF, MG = to_dev(dev, f, g, mf, mg)
+    m = fb.Matcher(cfg, max_batch=3, chunk=2)  # two chunks: both lanes in the graph
+    direct = m.match_device(F, G, MF, MG, delta=delta).clone()
+    torch.cuda.synchronize()
+    m.set_graphs(True)
+    out = torch.zeros_like(direct)
+    ts = torch.zeros((3, cfg.n_theta), dtype=torch.float64, device=dev)
+    for _ in range(3):
+        out.zero_()
+        m.match_device(F, G, MF, MG, delta=delta, out=out, theta_surface=ts)
+        torch.cuda.synchronize()
+        assert torch.equal(out, direct)
+    assert m.graph_stats() == (1, 2)
+    # the graph reads the buffers at replay time: new data in the same tensors
+    F2, G2 = G.clone(), F.clone()
+    direct2 = None
+    m.set_graphs(False)
+    direct2 = m.match_device(F2, G2, MG, MF, delta=delta).clone()
+    m.set_graphs(True)
+    F.copy_(F2)
+    G.copy_(G2)
+    MF2, MG2 = MG.clone(), MF.clone()
+    MF.copy_(MF2)
+    MG.copy_(MG2)
+    m.match_device(F, G, MF, MG, delta=delta, out=out, theta_surface=ts)
+    torch.cuda.synchronize()
+    assert torch.equal(out, direct2)
+    # a different output buffer is a different graph; a side stream works too
+    out2 = torch.zeros_like(direct)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        m.match_device(F, G, MF, MG, delta=delta, out=out2, stream=s)
+    s.synchronize()
+    assert torch.equal(out2, direct2)
+    caps = m.graph_stats()[0]
+    m.match_device(F, G, MF, MG, delta=delta, out=out2, stream=s)
+    assert m.graph_stats()[0] == caps
+    # phase correlation drops the cache (captured with the old setting)
+    m.set_phase_correlation(True)
+    m.match_device(F, G, MF, MG, delta=delta, out=out, theta_surface=ts)
+    torch.cuda.synchronize()
+    assert m.graph_stats()[0] == caps + 1
+    m.set_graphs(False)
+    ph = m.match_device(F, G, MF, MG, delta=delta)
+    torch.cuda.synchronize()
+    assert torch.equal(out, ph)
+
+
+def test_graph_replay_odometry(fb, dev):
+    cfg, delta, _ = fb.baseline_config(2)
+    scans, masks = _sequence(fb, 2, 6)
+    S, M = to_dev(dev, scans, masks)
+    m = fb.Matcher(cfg, max_batch=5, chunk=2)
+    direct = m.odometry(S, M, delta=delta).clone()
+    m.set_graphs(True)
+    out = torch.zeros_like(direct)
+    for _ in range(2):
+        m.odometry(S, M, delta=delta, out=out)
+        torch.cuda.synchronize()
+        assert torch.equal(out, direct)
+    assert m.graph_stats() == (1, 1)
+
+
 # ---- grid sides that are not powers of two (the reference's own odd sizes; DESIGN.md §3.9) ----
 
 @pytest.mark.parametrize("n,nt", [(65, 129), (129, 90), (255, 733), (300, 360), (511, 720)])
