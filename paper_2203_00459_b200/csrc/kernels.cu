@@ -214,17 +214,23 @@ constexpr int kGatherThreads = 128;
 // SPLIT (chain mode, odd pair k): |F| of scan k is the .y of transform k/2,
 // |G| of scan k+1 the .x of transform k/2 + 1.
 template <bool SPLIT>
-__device__ __forceinline__ void gather_sums(const Params& p, const float2* m, int i, double* prof) {
+__device__ __forceinline__ void gather_sums(const Params& p, const float2* m, int i, bool live, int rsub,
+                                            double* prof) {
     const int nt = p.n_theta, n = p.n, n_live = p.n_live;
     const float2* m2 = m + p.mag_plane;  // the next transform's tiles (chain mode)
-    const PolarTap* col = p.taps + i;
+    const PolarTap* col = p.taps + (live ? i : 0);
     double af = 0.0, ag = 0.0;
+    // a warp covers 8 azimuths x 4 radii per step (lane = 4 * azimuth + radius
+    // phase): the 32 samples of one load instruction form a compact patch of the
+    // magnitude plane instead of a 32-azimuth arc, so they touch fewer cache lines
     constexpr int U = 4;  // independent entries in flight per thread (memory-level parallelism)
-    for (int j0 = 0; j0 < n_live; j0 += U) {
+    for (int j0 = rsub; j0 < n_live; j0 += 4 * U) {
         PolarTap e[U];
 #pragma unroll
-        for (int q = 0; q < U; ++q)
-            e[q] = j0 + q < n_live ? col[(size_t)(j0 + q) * nt] : PolarTap{0, 0.f, 0.f, 0.f};  // flags 0: 0
+        for (int q = 0; q < U; ++q) {
+            const int j = j0 + 4 * q;
+            e[q] = (live && j < n_live) ? col[(size_t)j * nt] : PolarTap{0, 0.f, 0.f, 0.f};  // flags 0: 0
+        }
         float fv[U][4], gv[U][4];
 #pragma unroll
         for (int q = 0; q < U; ++q) {
@@ -249,24 +255,32 @@ __device__ __forceinline__ void gather_sums(const Params& p, const float2* m, in
             ag += (double)bilerp(e[q].fr, e[q].fc, gv[q][0], gv[q][1], gv[q][2], gv[q][3]);
         }
     }
-    prof[i] = af;
-    prof[nt + i] = ag;
+    // the four radius phases of an azimuth, summed in a fixed order
+    af += __shfl_xor_sync(0xffffffffu, af, 1);
+    ag += __shfl_xor_sync(0xffffffffu, ag, 1);
+    af += __shfl_xor_sync(0xffffffffu, af, 2);
+    ag += __shfl_xor_sync(0xffffffffu, ag, 2);
+    if (live && rsub == 0) {
+        prof[i] = af;
+        prof[nt + i] = ag;
+    }
 }
 
 __global__ void __launch_bounds__(kGatherThreads) k_rot_gather(Params p) {
     const int pair = blockIdx.y;
     const int nt = p.n_theta;
-    const int i = blockIdx.x * kGatherThreads + threadIdx.x;
-    if (i >= nt) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int i = blockIdx.x * (kGatherThreads / 4) + warp * 8 + (lane >> 2);
+    const bool live = i < nt;
     // the K1b transform holding the pair's |F| (and |G|): one per pair, or in
     // chain mode one per two scans of the sequence
     const int tr = p.chain ? pair / 2 : pair;
     const float2* m = reinterpret_cast<const float2*>(p.mag) + (size_t)tr * p.mag_plane;
     double* prof = p.prof + (size_t)pair * 2 * nt;
     if (p.chain && (pair & 1))
-        gather_sums<true>(p, m, i, prof);
+        gather_sums<true>(p, m, i, live, lane & 3, prof);
     else
-        gather_sums<false>(p, m, i, prof);
+        gather_sums<false>(p, m, i, live, lane & 3, prof);
 }
 
 // K2b: angular correlation of the profiles, hard + soft argmax over theta.
@@ -1204,7 +1218,7 @@ cudaError_t launch_xlat_out(const Params& p, cudaStream_t s) { FSCAN_DISPATCH_N(
 
 cudaError_t launch_rot_gather(const Params& p, cudaStream_t s) {
     if (p.n_theta == 1) return cudaSuccess;
-    k_rot_gather<<<dim3((p.n_theta + kGatherThreads - 1) / kGatherThreads, p.batch), kGatherThreads, 0, s>>>(p);
+    k_rot_gather<<<dim3((p.n_theta + kGatherThreads / 4 - 1) / (kGatherThreads / 4), p.batch), kGatherThreads, 0, s>>>(p);
     return cudaGetLastError();
 }
 
