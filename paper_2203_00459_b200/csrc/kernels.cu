@@ -676,6 +676,10 @@ struct XColGeom {
     // explicit residency targets where ptxas' own choice leaves the SM
     // register-bound (N = 256: 4 CTAs of 192 threads; N = 1024: 2 of 384)
     static constexpr int MIN_BLOCKS = N == 1024 ? 2 : (N == 256 ? 4 : 0);
+    // inputs loaded and folded once per (column, n0) site for all three q and
+    // parked in shared memory (N = 1024: C5 +3%); below, every q group loads and
+    // folds its own elements (the shared fold measured 1% slower at N = 512)
+    static constexpr bool FOLD1 = N >= 1024;
 };
 
 template <int N>
@@ -732,22 +736,70 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
     const fscan_fft::SmemTwRK twk{stw_rk, stw_k};
     const float2 w3q = w3(q);
     float2 a[16];
+    if constexpr (X::FOLD1) {
+        // one thread per (column, n0): (F, G) at n0 and n0 + K loaded once, the
+        // three q inputs of both transforms formed together (a radix-3 butterfly
+        // with x2 = 0) and parked in the transforms' exchange buffers (F in A, G
+        // in B); the q groups then read their inputs from shared memory (instead
+        // of each loading and folding every element itself: 3x fewer global loads)
+        constexpr int SITES = COLS * K, ITER = (SITES + X::THREADS - 1) / X::THREADS;
+        float4 v0[ITER], v1[ITER];  // every load in flight before the first use
 #pragma unroll
-    for (int m = 0; m < 16; ++m) {
-        const int n0 = t + m * T;
-        const float4 u0 = src[n0], u1 = src[n0 + K];
-        const float2 s = cadd(make_float2(u0.x, u0.y), cmul(w3q, make_float2(u1.x, u1.y)));
-        a[m] = q ? cmul(wq(n0, q), s) : s;
+        for (int it = 0; it < ITER; ++it) {
+            const int e = threadIdx.x + it * X::THREADS;
+            if (SITES % X::THREADS == 0 || e < SITES) {
+                const int cc = e / K, n0 = e % K;
+                const int kc = min((int)blockIdx.x * COLS + cc, H);
+                const float4* s4 = p.fgt + ((size_t)pair * (H + 1) + kc) * N;
+                v0[it] = s4[n0];
+                v1[it] = s4[n0 + K];
+            }
+        }
+#pragma unroll
+        for (int it = 0; it < ITER; ++it) {
+            const int e = threadIdx.x + it * X::THREADS;
+            if (!(SITES % X::THREADS == 0 || e < SITES)) break;
+            const int cc = e / K, n0 = e % K;
+            const float4 u0 = v0[it], u1 = v1[it];
+            const float2 w1 = wq(n0, 1), w2 = wq(n0, 2);
+            auto fold = [&](float2 x0, float2 x1, float* base) {
+                const float2 tt = make_float2(fmaf(-0.5f, x1.x, x0.x), fmaf(-0.5f, x1.y, x0.y));
+                const float2 ss = make_float2(kS3 * x1.x, kS3 * x1.y);
+                G::lay(base, 3 * cc).put(n0, cadd(x0, x1));
+                G::lay(base, 3 * cc + 1).put(n0, cmul(w1, make_float2(tt.x + ss.y, tt.y - ss.x)));
+                G::lay(base, 3 * cc + 2).put(n0, cmul(w2, make_float2(tt.x - ss.y, tt.y + ss.x)));
+            };
+            fold(make_float2(u0.x, u0.y), make_float2(u1.x, u1.y), smem);
+            fold(make_float2(u0.z, u0.w), make_float2(u1.z, u1.w), smem + G::FLOATS);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int m = 0; m < 16; ++m) a[m] = bufA.get(t + m * T);
+        __syncwarp();  // every input read before the transform's exchange writes
+    } else {
+#pragma unroll
+        for (int m = 0; m < 16; ++m) {
+            const int n0 = t + m * T;
+            const float4 u0 = src[n0], u1 = src[n0 + K];
+            const float2 s = cadd(make_float2(u0.x, u0.y), cmul(w3q, make_float2(u1.x, u1.y)));
+            a[m] = q ? cmul(wq(n0, q), s) : s;
+        }
     }
     fft_regs<K, -1, true>(a, t, bufA, twk);  // transforms of a warp share a buffer group
 #pragma unroll
     for (int m = 0; m < 16; ++m) bufA.put(t + m * T, a[m]);  // park F_q (own slots)
+    if constexpr (X::FOLD1) {
 #pragma unroll
-    for (int m = 0; m < 16; ++m) {
-        const int n0 = t + m * T;
-        const float4 u0 = src[n0], u1 = src[n0 + K];
-        const float2 s = cadd(make_float2(u0.z, u0.w), cmul(w3q, make_float2(u1.z, u1.w)));
-        a[m] = q ? cmul(wq(n0, q), s) : s;
+        for (int m = 0; m < 16; ++m) a[m] = bufB.get(t + m * T);
+        __syncwarp();
+    } else {
+#pragma unroll
+        for (int m = 0; m < 16; ++m) {
+            const int n0 = t + m * T;
+            const float4 u0 = src[n0], u1 = src[n0 + K];
+            const float2 s = cadd(make_float2(u0.z, u0.w), cmul(w3q, make_float2(u1.z, u1.w)));
+            a[m] = q ? cmul(wq(n0, q), s) : s;
+        }
     }
     fft_regs<K, -1, true>(a, t, bufB, twk);
 #pragma unroll

@@ -1,5 +1,5 @@
 """Aggregate ncu warp-stall samples per CUDA source line for one kernel.
-usage: python tools/ncu_lines.py report.ncu-rep kernel_regex [top]"""
+usage: python tools/ncu_lines.py report.ncu-rep kernel_regex [top] [inst]  (inst: sort by instructions)"""
 import csv
 import io
 import subprocess
@@ -34,7 +34,7 @@ for r in csv.reader(io.StringIO(out)):
     itot[0] += ninst
     stalls = [(int(r[i]), hdr[i][6:]) for i in range(len(hdr)) if hdr[i].startswith("stall_") and "Not Issued" not in hdr[i] and r[i].isdigit()]
     agg.append((n, f"{fname}:{r[0]}", r[1].strip()[:70], sorted(stalls, reverse=True)[:3], ninst))
-agg.sort(reverse=True)
+agg.sort(reverse=True, key=(lambda a: a[4]) if 'inst' in sys.argv[4:] else None)
 it = globals().get("itot", [1])[0]
 print(f"total samples {tot}, warp instructions {it}")
 for n, ln, src, st, ni in agg[:top]:
