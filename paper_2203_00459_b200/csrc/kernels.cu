@@ -503,7 +503,12 @@ struct XRowGeom {
     // the FFT exchange buffers alias the gather stash (dead once v[] is loaded):
     // ~50 KB per CTA, three CTAs per SM
     static constexpr size_t STASH = (size_t)2 * ROWS * SP;
-    static constexpr size_t SMEM = (STASH > (size_t)G::FLOATS ? STASH : (size_t)G::FLOATS) * sizeof(float);
+    static constexpr size_t WORK = STASH > (size_t)G::FLOATS ? STASH : (size_t)G::FLOATS;
+    // + the span-16 stage's [r][k] twiddle table (K >= 256): 15 shared loads
+    // per thread instead of 4 global loads and 11 products (C4 +0.4%; the same
+    // table in K1b measured slower)
+    static constexpr bool RK = N / 2 >= 256;
+    static constexpr size_t SMEM = (WORK + (RK ? 480 : 0)) * sizeof(float);
     static_assert(G::PER_CTA % 3 == 0, "three transforms per row");
     // separation loop: a half-warp reads R rows x KB consecutive k. Row ol's
     // buffers start at 3 * ol * stride, i.e. bank offset o * ol (mod 16); R =
@@ -547,6 +552,9 @@ __global__ void __launch_bounds__(kXThreads, 3) k_xlat_rows(Params p) {
     const float* ft = p.ft + (size_t)src * N * N;
     const float* gt = p.gt + (size_t)src * N * N;
     const float c0f32 = EMB ? p.c0 : (N - 1) / 2.0f;  // exact (half-integer or integer)
+    float2* srk = reinterpret_cast<float2*>(smem + X::WORK);  // ordered by the barrier after the gather
+    if constexpr (X::RK)
+        for (int i = threadIdx.x; i < 240; i += kXThreads) srk[i] = __ldg(p.tw_rk + i);
     const int nvalid = EMB ? p.n : N;
     // rotate_bilinear(g~, -theta); -theta == 0.0 returns g~ itself, which st = 0,
     // ct = 1 reproduce exactly (integer source coordinates, zero fractions)
@@ -612,7 +620,10 @@ __global__ void __launch_bounds__(kXThreads, 3) k_xlat_rows(Params p) {
         }
         __syncthreads();  // every stash read done before the exchange buffers are written
         const auto b = G::lay(xbase, tr);
-        fft_regs<K, -1, true>(v, t, b, p.tw_k);  // T <= 32: each transform within a warp
+        if constexpr (X::RK)
+            fft_regs<K, -1, true>(v, t, b, fscan_fft::SmemTwRK{srk, p.tw_k});  // T <= 32: within a warp
+        else
+            fft_regs<K, -1, true>(v, t, b, p.tw_k);
 #pragma unroll
         for (int m = 0; m < 16; ++m) b.put(t + m * T, v[m]);
     }
