@@ -356,7 +356,22 @@ def run_ours(args):
                    "h2d_bytes_per_step": int(4 * f.numel() * 4 * world),
                    "d2h_bytes_per_step": int(total * fb.RESULT_DTYPE.itemsize), "steps": steps_e2e,
                    "api": "fscan_match_batch_host (pinned host buffers)"}
-            del hf, hg, hmf, hmg
+            # what bounds it: this rank's H2D rate inside the e2e steps against a
+            # plain pinned -> device copy of one input grid set on the same link
+            e2e["h2d_gbs"] = round(4 * f.numel() * 4 * steps_e2e / dt / 1e9, 1)
+            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            dst = torch.empty_like(f)
+            dst.copy_(hf, non_blocking=True)
+            torch.cuda.synchronize()
+            best = float("inf")
+            for _ in range(3):
+                c0.record()
+                dst.copy_(hf, non_blocking=True)
+                c1.record()
+                c1.synchronize()
+                best = min(best, c0.elapsed_time(c1) / 1e3)
+            e2e["pinned_copy_h2d_gbs"] = round(hf.numel() * 4 / best / 1e9, 1)
+            del hf, hg, hmf, hmg, dst
         except Exception as exc:  # report, never fake
             e2e = {"value": None, "unit": UNIT, "error": str(exc)[:200]}
 
