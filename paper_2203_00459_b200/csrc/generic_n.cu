@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(8 * (L / 16)) k_rot_cols_bs(Params p) {
         const int2 bd = __ldg(p.band + vc);
         const bool in = (uu >= bd.x) && (uu <= bd.y);
         out[((size_t)(uu >> 3) * n + vc) * 8 + (uu & 7)] =
-            in ? make_float2(0.5f * sqrtf(fr * fr + fi * fi), 0.5f * sqrtf(gr * gr + gi * gi)) : make_float2(0.f, 0.f);
+            in ? make_float2(0.5f * fscan_fft::sqrt_fast(fr * fr + fi * fi), 0.5f * fscan_fft::sqrt_fast(gr * gr + gi * gi)) : make_float2(0.f, 0.f);
     }
 }
 
@@ -473,7 +473,7 @@ __global__ void __launch_bounds__(kPfaColThreads) k_rot_cols_pfa255(Params p) {
         const int2 bd = __ldg(p.band + vc);
         const bool in = (uu >= bd.x) && (uu <= bd.y);
         out[((size_t)(uu >> 3) * n + vc) * 8 + (uu & 7)] =
-            in ? make_float2(0.5f * sqrtf(fr * fr + fi * fi), 0.5f * sqrtf(gr * gr + gi * gi)) : make_float2(0.f, 0.f);
+            in ? make_float2(0.5f * fscan_fft::sqrt_fast(fr * fr + fi * fi), 0.5f * fscan_fft::sqrt_fast(gr * gr + gi * gi)) : make_float2(0.f, 0.f);
     }
 }
 }  // namespace

@@ -177,7 +177,7 @@ __global__ void __launch_bounds__(N) k_rot_cols(Params p) {
         const int2 bd = __ldg(p.band + vc);
         const int u = u0 + cc;
         const bool in = (u >= bd.x) && (u <= bd.y);
-        const float2 mv = in ? make_float2(0.5f * sqrtf(fr * fr + fi * fi), 0.5f * sqrtf(gr * gr + gi * gi))
+        const float2 mv = in ? make_float2(0.5f * fscan_fft::sqrt_fast(fr * fr + fi * fi), 0.5f * fscan_fft::sqrt_fast(gr * gr + gi * gi))
                              : make_float2(0.0f, 0.0f);
         out[o] = mv;  // tile [u0 / 8][v_c][cc]
     }
