@@ -153,6 +153,22 @@ def ncu_traffic(kernel: str) -> float | None:
         return None
 
 
+def ncu_issue(kernel: str) -> dict | None:
+    """What bounds `kernel` when DRAM does not: its issue-slot and DRAM utilisation
+    in the committed ncu --set full capture (profiles/r01/ncu_full_summary.json)."""
+    path = os.path.join(ROOT, "profiles", "r01", "ncu_full_summary.json")
+    try:
+        with open(path) as fh:
+            for k in json.load(fh)["kernels"]:
+                if k["kernel"].split("<")[0] == "k_" + kernel:
+                    return {"issue_active_frac": round(k["issue_pct"] / 100, 3),
+                            "dram_frac": round(k["dram_pct"] / 100, 3),
+                            "source": "ncu --set full, profiles/r01/ncu_full_summary.json"}
+    except Exception:
+        return None
+    return None
+
+
 def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -282,7 +298,10 @@ def run_ours(args):
                 "frac": round(achieved / peak, 4), "peak_source": peak_src,
                 "traffic": None if traffic is None else traffic * pairs_per_launch,
                 "alg_bytes_per_launch": alg, "avg_launch_ms": dom_ms / dom_launches,
-                "kernel_share": round(dom_ms / sum(v[0] for v in kt.values()), 3)}
+                "kernel_share": round(dom_ms / sum(v[0] for v in kt.values()), 3),
+                # the dominant kernel is FFT-issue-bound, not DRAM-bound: its ncu issue
+                # utilisation says how close it runs to its own ceiling
+                "ncu": ncu_issue(dom)}
     bpair = pair_bytes(cfg.n_xy, cfg.n_theta, cfg.pad_angle,
                        s_in=(8.0 * spec.n_az * spec.n_range) if polar else None)
     pipeline = {"b_pair_bytes": bpair, "achieved_gbs": round(value * bpair / 1e9 / world, 1),
