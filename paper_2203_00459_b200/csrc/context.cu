@@ -35,6 +35,7 @@ struct Lane {
     Partial* part = nullptr;
     RotState* rot = nullptr;
     double* prof = nullptr;
+    double* theta_ws = nullptr;
     int* flags = nullptr;
     // host-API staging
     float* in = nullptr;  // 4 grids x chunk
@@ -272,6 +273,7 @@ void free_lane(Lane& l) {
     cudaFree(l.part);
     cudaFree(l.rot);
     cudaFree(l.prof);
+    cudaFree(l.theta_ws);
     cudaFree(l.flags);
     cudaFree(l.in);
     cudaFree(l.cart);
@@ -301,6 +303,7 @@ fscan_status alloc_lane(fscan_ctx* ctx, Lane& l, int chunk) {
     CK(cudaMalloc(&l.part, sizeof(Partial) * nparts * chunk));
     CK(cudaMalloc(&l.rot, sizeof(RotState) * chunk));
     CK(cudaMalloc(&l.prof, sizeof(double) * 2 * std::max(1, ctx->cfg.n_theta) * chunk));
+    CK(cudaMalloc(&l.theta_ws, sizeof(double) * std::max(1, ctx->cfg.n_theta) * chunk));
     CK(cudaMalloc(&l.flags, sizeof(int) * (chunk + 2)));  // chain mode: one per scan
     return FSCAN_OK;
 }
@@ -338,6 +341,7 @@ Params base_params(fscan_ctx* ctx, Lane& l, int batch, double delta) {
     p.part = l.part;
     p.rot = l.rot;
     p.prof = l.prof;
+    p.theta_ws = l.theta_ws;
     p.flags = l.flags;
     p.tw_n = ctx->tw_n;
     p.tw_k = ctx->tw_k;

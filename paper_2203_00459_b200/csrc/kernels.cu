@@ -16,6 +16,8 @@
 // each 2N-point transform of a half-zero signal is two N-point transforms
 // (even outputs: FFT_N(x); odd outputs: FFT_N(x * W_2N^n)).
 #include <cuda_runtime.h>
+
+#include <algorithm>
 #include <math.h>
 #include <stdint.h>
 
@@ -185,6 +187,9 @@ __global__ void __launch_bounds__(N) k_rot_cols(Params p) {
 
 // ---------------------------------------------------------------- K2
 constexpr int kPolarThreads = 512;
+#ifndef FSCAN_K2B_SPLIT_BELOW
+#define FSCAN_K2B_SPLIT_BELOW 64  // batches below this split K2b over several CTAs per pair
+#endif
 
 // K2b angular correlation: each thread owns kLags consecutive lags over one of
 // polar_parts(nt) q-ranges, so that (lag blocks) x parts fills the CTA.
@@ -283,115 +288,76 @@ __global__ void __launch_bounds__(kGatherThreads) k_rot_gather(Params p) {
         gather_sums<false>(p, m, i, live, lane & 3, prof);
 }
 
-// K2b: angular correlation of the profiles, hard + soft argmax over theta.
-__global__ void __launch_bounds__(kPolarThreads) k_rot_polar(Params p) {
-    extern __shared__ double dsm[];
-    const int pair = blockIdx.x;
-    const int nt = p.n_theta, L = p.L, pad = p.pad;
-    double* A = dsm;                      // wrap-extended radial-sum profiles, length L
-    double* B = dsm + L;                  // skewed circular extension, bx_len(L, nt)
-    double* s = B + bx_len(L, nt);        // theta surface, n_theta
-    double* red_v;                        // block reduction scratch (32 entries each), after the partials
-    int* red_i;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nwarps = kPolarThreads / 32;
-    RotState* rs = p.rot + pair;
-
-    if (nt == 1) {  // matcher.cpp:103-110
-        if (threadIdx.x == 0) {
-            rs->theta = 0.0;
-            rs->st = 0.0;
-            rs->ct = 1.0;
-            rs->peak = 0.0;
-            rs->hard = 0.0;
-            rs->bin = 0;
-            rs->identity = 1;
-            if (p.theta_surf) p.theta_surf[pair] = 0.0;
-            if (p.theta_only) p.theta_only[pair] = 0.0;
+// One K2b work item: kLags consecutive lags k0.. over the q-range [q0, q1);
+// a 15-value window of Bx slides over 8 q per step (64 DFMA per 8 A and 8 Bx loads).
+__device__ __forceinline__ void polar_item(const double* A, const double* Bx, int q0, int q1, int k0,
+                                           double (&acc)[kLags]) {
+#pragma unroll
+    for (int c = 0; c < kLags; ++c) acc[c] = 0.0;
+    double w[2 * kLags - 1];
+#pragma unroll
+    for (int c = 0; c < kLags - 1; ++c) w[c] = Bx[bx_skew(q0 + k0 + c)];
+    int q = q0;
+    for (; q + kLags <= q1; q += kLags) {
+#pragma unroll
+        for (int c = 0; c < kLags; ++c) w[kLags - 1 + c] = Bx[bx_skew(q + k0 + kLags - 1 + c)];
+#pragma unroll
+        for (int u = 0; u < kLags; ++u) {
+            const double a = A[q + u];
+#pragma unroll
+            for (int c = 0; c < kLags; ++c) acc[c] = fma(a, w[u + c], acc[c]);
         }
-        return;
+#pragma unroll
+        for (int c = 0; c < kLags - 1; ++c) w[c] = w[kLags + c];
     }
+    for (; q < q1; ++q) {  // tail: one q at a time
+        w[kLags - 1] = Bx[bx_skew(q + k0 + kLags - 1)];
+        const double a = A[q];
+#pragma unroll
+        for (int c = 0; c < kLags; ++c) acc[c] = fma(a, w[c], acc[c]);
+#pragma unroll
+        for (int c = 0; c < kLags - 1; ++c) w[c] = w[c + 1];
+    }
+}
 
-    // wrap_pad (imageops.cpp:101-113): padded row q holds profile row (q - pad) mod nt.
-    // B is stored circularly extended, Bx[j] = B[(j - nt/2) mod L], so the score
-    // s[k] = (1/C) sum_q A[q] B[(q + k - nt/2) mod L] is
-    // sum_q A[q] Bx[q + k] without modular indexing (Bx[j] lives at bx_skew(j)).
+// wrap_pad (imageops.cpp:101-113) of one pair's profiles into shared memory:
+// padded row q holds profile row (q - pad) mod nt. B is stored circularly
+// extended, Bx[j] = B[(j - nt/2) mod L], so the score
+// s[k] = (1/C) sum_q A[q] B[(q + k - nt/2) mod L] is
+// sum_q A[q] Bx[q + k] without modular indexing (Bx[j] lives at bx_skew(j)).
+__device__ __forceinline__ void polar_profiles(const Params& p, int pair, double* A, double* Bx) {
+    const int nt = p.n_theta, L = p.L, pad = p.pad;
     const double* prof = p.prof + (size_t)pair * 2 * nt;
-    const int np = polar_parts(nt);
-    double* Bx = B;
-    double* part = s + nt;                 // np x nt partial sums
-    red_v = part + (size_t)np * nt;
-    red_i = (int*)(red_v + 32);
-    for (int q = threadIdx.x; q < L; q += kPolarThreads) {
+    for (int q = threadIdx.x; q < L; q += blockDim.x) {
         int i = (q - pad) % nt;
         if (i < 0) i += nt;
         A[q] = prof[i];
     }
-    for (int j = threadIdx.x; j < L + nt + 2 * kLags; j += kPolarThreads) {
+    for (int j = threadIdx.x; j < L + nt + 2 * kLags; j += blockDim.x) {
         int qq = (j - nt / 2) % L;
         if (qq < 0) qq += L;
         int i = (qq - pad) % nt;
         if (i < 0) i += nt;
         Bx[bx_skew(j)] = prof[nt + i];
     }
-    __syncthreads();
-    // register-blocked: each item owns kLags consecutive lags over one of np
-    // q-ranges; a 15-value window of Bx slides over 8 q per step (64 DFMA per
-    // 8 A and 8 Bx loads)
-    {
-        const int blocks = (nt + kLags - 1) / kLags;
-        const int item = threadIdx.x;
-        if (item < blocks * np) {
-            const int k0 = kLags * (item % blocks), pi = item / blocks;
-            const int q0 = (int)((long)L * pi / np), q1 = (int)((long)L * (pi + 1) / np);
-            double acc[kLags];
-#pragma unroll
-            for (int c = 0; c < kLags; ++c) acc[c] = 0.0;
-            double w[2 * kLags - 1];
-#pragma unroll
-            for (int c = 0; c < kLags - 1; ++c) w[c] = Bx[bx_skew(q0 + k0 + c)];
-            int q = q0;
-            for (; q + kLags <= q1; q += kLags) {
-#pragma unroll
-                for (int c = 0; c < kLags; ++c) w[kLags - 1 + c] = Bx[bx_skew(q + k0 + kLags - 1 + c)];
-#pragma unroll
-                for (int u = 0; u < kLags; ++u) {
-                    const double a = A[q + u];
-#pragma unroll
-                    for (int c = 0; c < kLags; ++c) acc[c] = fma(a, w[u + c], acc[c]);
-                }
-#pragma unroll
-                for (int c = 0; c < kLags - 1; ++c) w[c] = w[kLags + c];
-            }
-            for (; q < q1; ++q) {  // tail: one q at a time
-                w[kLags - 1] = Bx[bx_skew(q + k0 + kLags - 1)];
-                const double a = A[q];
-#pragma unroll
-                for (int c = 0; c < kLags; ++c) acc[c] = fma(a, w[c], acc[c]);
-#pragma unroll
-                for (int c = 0; c < kLags - 1; ++c) w[c] = w[c + 1];
-            }
-            double* pr = part + (size_t)pi * nt + k0;
-#pragma unroll
-            for (int c = 0; c < kLags; ++c)
-                if (k0 + c < nt) pr[c] = acc[c];
-        }
-    }
-    __syncthreads();
-    const double invC = 1.0 / (double)p.C;
+}
+
+// The theta scores s[0..nt) of a pair (shared memory, complete) -> hard argmax
+// (strict >, lowest index, matcher.cpp:47-53), windowed soft-argmax
+// (matcher.cpp:57-93), the pair's RotState and optional surface copy. Every
+// thread of the CTA calls it; red_v / red_i: 32 entries of scratch each.
+__device__ void polar_finish(const Params& p, int pair, const double* s, double* red_v, int* red_i) {
+    const int nt = p.n_theta;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nwarps = blockDim.x / 32;
+    RotState* rs = p.rot + pair;
     double best_v = -INFINITY;
     int best_i = 0x7fffffff;
-    for (int k = threadIdx.x; k < nt; k += kPolarThreads) {
-        double acc = 0.0;
-        for (int pi = 0; pi < np; ++pi) acc += part[(size_t)pi * nt + k];  // fixed order: deterministic
-        const double sv = acc * invC;
-        s[k] = sv;
-        if (sv > best_v) {  // k increases per thread: strict > keeps the lowest index
-            best_v = sv;
+    for (int k = threadIdx.x; k < nt; k += blockDim.x)
+        if (s[k] > best_v) {  // k increases per thread: strict > keeps the lowest index
+            best_v = s[k];
             best_i = k;
         }
-    }
-    // block argmax, ties -> lowest index (matcher.cpp:47-53)
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         const double ov = __shfl_xor_sync(0xffffffffu, best_v, o);
@@ -440,10 +406,121 @@ __global__ void __launch_bounds__(kPolarThreads) k_rot_polar(Params p) {
         rs->bin = pk;
         if (p.theta_only) p.theta_only[pair] = theta;
     }
-    if (p.theta_surf) {
-        __syncthreads();
-        for (int k = threadIdx.x; k < nt; k += kPolarThreads) p.theta_surf[(size_t)pair * nt + k] = s[k];
+    if (p.theta_surf)
+        for (int k = threadIdx.x; k < nt; k += blockDim.x) p.theta_surf[(size_t)pair * nt + k] = s[k];
+}
+
+// K2b: angular correlation of the profiles, hard + soft argmax over theta.
+__global__ void __launch_bounds__(kPolarThreads) k_rot_polar(Params p) {
+    extern __shared__ double dsm[];
+    const int pair = blockIdx.x;
+    const int nt = p.n_theta, L = p.L;
+    double* A = dsm;                      // wrap-extended radial-sum profiles, length L
+    double* B = dsm + L;                  // skewed circular extension, bx_len(L, nt)
+    double* s = B + bx_len(L, nt);        // theta surface, n_theta
+    double* red_v;                        // block reduction scratch (32 entries each), after the partials
+    int* red_i;
+    RotState* rs = p.rot + pair;
+
+    if (nt == 1) {  // matcher.cpp:103-110
+        if (threadIdx.x == 0) {
+            rs->theta = 0.0;
+            rs->st = 0.0;
+            rs->ct = 1.0;
+            rs->peak = 0.0;
+            rs->hard = 0.0;
+            rs->bin = 0;
+            rs->identity = 1;
+            if (p.theta_surf) p.theta_surf[pair] = 0.0;
+            if (p.theta_only) p.theta_only[pair] = 0.0;
+        }
+        return;
     }
+
+    const int np = polar_parts(nt);
+    double* Bx = B;
+    double* part = s + nt;                 // np x nt partial sums
+    red_v = part + (size_t)np * nt;
+    red_i = (int*)(red_v + 32);
+    polar_profiles(p, pair, A, Bx);
+    __syncthreads();
+    // register-blocked: each item owns kLags consecutive lags over one of np
+    // q-ranges (polar_item)
+    {
+        const int blocks = (nt + kLags - 1) / kLags;
+        const int item = threadIdx.x;
+        if (item < blocks * np) {
+            const int k0 = kLags * (item % blocks), pi = item / blocks;
+            const int q0 = (int)((long)L * pi / np), q1 = (int)((long)L * (pi + 1) / np);
+            double acc[kLags];
+            polar_item(A, Bx, q0, q1, k0, acc);
+            double* pr = part + (size_t)pi * nt + k0;
+#pragma unroll
+            for (int c = 0; c < kLags; ++c)
+                if (k0 + c < nt) pr[c] = acc[c];
+        }
+    }
+    __syncthreads();
+    const double invC = 1.0 / (double)p.C;
+    for (int k = threadIdx.x; k < nt; k += kPolarThreads) {
+        double acc = 0.0;
+        for (int pi = 0; pi < np; ++pi) acc += part[(size_t)pi * nt + k];  // fixed order: deterministic
+        s[k] = acc * invC;
+    }
+    __syncthreads();
+    polar_finish(p, pair, s, red_v, red_i);
+}
+
+// K2b split over S CTAs per pair (small batches: one CTA per pair would leave
+// the GPU nearly idle for ~25 us): CTA `part` of a pair owns a contiguous range
+// of lag blocks and writes their scores to theta_ws; k_rot_polar_fin then runs
+// the argmaxes per pair.
+__global__ void __launch_bounds__(kPolarThreads) k_rot_polar_part(Params p, int S) {
+    extern __shared__ double dsm[];
+    const int pair = blockIdx.x / S, part_id = blockIdx.x % S;
+    const int nt = p.n_theta, L = p.L;
+    const int blocks = (nt + kLags - 1) / kLags, per = (blocks + S - 1) / S;
+    const int b0 = part_id * per, nb = min(blocks, b0 + per) - b0;
+    if (nb <= 0) return;
+    // the fused kernel's q partition and summation order: bit-identical scores
+    // whatever the batch size (results do not depend on batching)
+    const int np = polar_parts(nt);
+    double* A = dsm;
+    double* Bx = A + L;
+    double* part = Bx + bx_len(L, nt);  // np x (nb * kLags)
+    const int W = nb * kLags;
+    polar_profiles(p, pair, A, Bx);
+    __syncthreads();
+    const int item = threadIdx.x;
+    if (item < nb * np) {
+        const int kk0 = kLags * (item % nb), pi = item / nb;
+        const int q0 = (int)((long)L * pi / np), q1 = (int)((long)L * (pi + 1) / np);
+        double acc[kLags];
+        polar_item(A, Bx, q0, q1, kLags * b0 + kk0, acc);
+#pragma unroll
+        for (int c = 0; c < kLags; ++c) part[(size_t)pi * W + kk0 + c] = acc[c];
+    }
+    __syncthreads();
+    const double invC = 1.0 / (double)p.C;
+    for (int kk = threadIdx.x; kk < W; kk += kPolarThreads) {
+        const int k = kLags * b0 + kk;
+        if (k < nt) {
+            double acc = 0.0;
+            for (int pi = 0; pi < np; ++pi) acc += part[(size_t)pi * W + kk];  // fixed order: deterministic
+            p.theta_ws[(size_t)pair * nt + k] = acc * invC;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kPolarThreads) k_rot_polar_fin(Params p) {
+    extern __shared__ double dsm[];
+    const int pair = blockIdx.x, nt = p.n_theta;
+    double* s = dsm;
+    double* red_v = s + nt;
+    int* red_i = (int*)(red_v + 32);
+    for (int k = threadIdx.x; k < nt; k += kPolarThreads) s[k] = p.theta_ws[(size_t)pair * nt + k];
+    __syncthreads();
+    polar_finish(p, pair, s, red_v, red_i);
 }
 
 __global__ void k_theta_in(Params p) {
@@ -1307,7 +1384,27 @@ cudaError_t launch_rot_gather(const Params& p, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// CTAs per pair for K2b: one when the batch fills the GPU, else up to 16
+int polar_split(int batch, int nt) {
+    if (nt <= 1 || batch >= FSCAN_K2B_SPLIT_BELOW) return 1;
+    return std::min(16, (148 + batch - 1) / batch);
+}
+
 cudaError_t launch_rot_polar(const Params& p, cudaStream_t s) {
+    const int S = polar_split(p.batch, p.n_theta);
+    if (S > 1) {
+        const int blocks = (p.n_theta + kLags - 1) / kLags, per = (blocks + S - 1) / S;
+        const size_t sm = (size_t)(p.L + bx_len(p.L, p.n_theta) + (size_t)polar_parts(p.n_theta) * per * kLags) *
+                          sizeof(double);
+        cudaError_t e = set_smem(k_rot_polar_part, sm);
+        if (e != cudaSuccess) return e;
+        k_rot_polar_part<<<p.batch * S, kPolarThreads, sm, s>>>(p, S);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        const size_t fm = (size_t)(p.n_theta + 32) * sizeof(double) + 32 * sizeof(int);
+        if ((e = set_smem(k_rot_polar_fin, fm)) != cudaSuccess) return e;
+        k_rot_polar_fin<<<p.batch, kPolarThreads, fm, s>>>(p);
+        return cudaGetLastError();
+    }
     const size_t sm = (size_t)(p.L + bx_len(p.L, p.n_theta) + p.n_theta * (1 + polar_parts(p.n_theta)) + 32) *
                           sizeof(double) +
                       32 * sizeof(int);

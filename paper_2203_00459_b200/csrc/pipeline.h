@@ -55,6 +55,7 @@ struct Params {
     Partial* part; // K5 per-block argmax [batch][N / rows_per_block]
     RotState* rot; // [batch]
     double* prof;  // K2a radial-sum profiles [batch][2][n_theta]
+    double* theta_ws;  // K2b split over several CTAs per pair (small batches): scores [batch][n_theta]
     int* flags;    // [batch] (chain mode: [n_scans]) bit0 non-finite, bit1 mask out of [0,1]
     // tables
     const float2* tw_n;   // exp(-2 pi i k / N), k < N
