@@ -153,14 +153,17 @@ def ncu_traffic(kernel: str) -> float | None:
         return None
 
 
-def ncu_issue(kernel: str) -> dict | None:
+def ncu_issue(kernel: str, n: int) -> dict | None:
     """What bounds `kernel` when DRAM does not: its issue-slot and DRAM utilisation
-    in the committed ncu --set full capture (profiles/r01/ncu_full_summary.json)."""
+    in the committed ncu --set full capture (profiles/r01/ncu_full_summary.json,
+    the C4 grid side; None for a kernel or grid side it did not capture)."""
     path = os.path.join(ROOT, "profiles", "r01", "ncu_full_summary.json")
     try:
         with open(path) as fh:
             for k in json.load(fh)["kernels"]:
-                if k["kernel"].split("<")[0] == "k_" + kernel:
+                if n != 512:  # the capture is of one C4 chunk (N = 512)
+                    return None
+                if k["kernel"].partition("<")[0] == "k_" + kernel:
                     return {"issue_active_frac": round(k["issue_pct"] / 100, 3),
                             "dram_frac": round(k["dram_pct"] / 100, 3),
                             "source": "ncu --set full, profiles/r01/ncu_full_summary.json"}
@@ -301,7 +304,7 @@ def run_ours(args):
                 "kernel_share": round(dom_ms / sum(v[0] for v in kt.values()), 3),
                 # the dominant kernel is FFT-issue-bound, not DRAM-bound: its ncu issue
                 # utilisation says how close it runs to its own ceiling
-                "ncu": ncu_issue(dom)}
+                "ncu": ncu_issue(dom, cfg.n_xy)}
     bpair = pair_bytes(cfg.n_xy, cfg.n_theta, cfg.pad_angle,
                        s_in=(8.0 * spec.n_az * spec.n_range) if polar else None)
     pipeline = {"b_pair_bytes": bpair, "achieved_gbs": round(value * bpair / 1e9 / world, 1),
