@@ -739,7 +739,9 @@ struct XColGeom {
     // (N = 512 at 4 columns: three 192-thread CTAs per SM instead of two of
     // 384; the kernel alone is 3% slower, but the pipeline is 0.6% faster, its
     // shorter CTAs interleaving better with the other lane's kernels)
-    static constexpr int COLS = (T >= 16) ? 4 : ((T >= 4) ? 8 : 16);
+    // (N = 1024 at 2 columns: 192-thread CTAs, three per SM at 96 registers;
+    // C5 +8% over 4 columns in 384 threads at 80 registers)
+    static constexpr int COLS = (T >= 32) ? 2 : ((T >= 16) ? 4 : ((T >= 4) ? 8 : 16));
     static constexpr int PITCH = COLS + 1;  // output tile [N rows][PITCH] float2
     static constexpr int THREADS = 3 * COLS * T;
     // split re/im exchange: with 64-bit accesses this kernel's allocation grows
@@ -762,8 +764,8 @@ struct XColGeom {
     static constexpr size_t TW_FLOATS = (size_t)2 * (240 + TW_LIN + (SMEM_WM ? (SPLIT_WM ? 2 : 3) * (N / 2) : 0));
     static constexpr size_t SMEM = (WORK_FLOATS + TW_FLOATS) * sizeof(float);
     // explicit residency targets where ptxas' own choice leaves the SM
-    // register-bound (N = 256: 4 CTAs of 192 threads; N = 1024: 2 of 384)
-    static constexpr int MIN_BLOCKS = N == 1024 ? 2 : (N == 256 ? 4 : 0);
+    // register-bound (N = 256: 4 CTAs of 192 threads; N = 1024: 3 of 192)
+    static constexpr int MIN_BLOCKS = N == 1024 ? 3 : (N == 256 ? 4 : 0);
     // inputs loaded and folded once per (column, n0) site for all three q and
     // parked in shared memory (N = 1024: C5 +3%); below, every q group loads and
     // folds its own elements (the shared fold measured 1% slower at N = 512)
