@@ -140,22 +140,30 @@ __global__ void __launch_bounds__(kRowThreads) k_rot_rows(Params p) {
 }
 
 // ---------------------------------------------------------------- K1b
-// 8 output columns u in [u0, u0+8) plus their mirrors (N-u) mod N, 16
-// interleaved column FFTs (column index fastest in the warp, Lay<16>);
+// k1b_u<N>() output columns u in [u0, u0 + U) plus their mirrors (N-u) mod N,
+// 2U interleaved column FFTs (column index fastest in the warp);
 // F = (Z[v,u] + conj Z[-v,-u]) / 2, G = (Z[v,u] - conj Z[-v,-u]) / 2i;
-// |F|, |G| times the annular band, written as an [N centred rows][8] tile of
-// (|F|, |G|) pairs.
+// |F|, |G| times the annular band, written into the [N centred rows][8] tiles
+// of (|F|, |G|) pairs (a CTA fills U of a tile's 8 columns).
+// (N = 1024 at 4 columns: 512 threads instead of 1024; C5 +0.4%; N = 512 at
+// 4 columns measured 0.8% slower than 8)
 template <int N>
-__global__ void __launch_bounds__(N) k_rot_cols(Params p) {
+__host__ __device__ constexpr int k1b_u() {
+    return N >= 1024 ? 4 : 8;
+}
+
+template <int N>
+__global__ void __launch_bounds__(N / 16 * 2 * k1b_u<N>()) k_rot_cols(Params p) {
+    constexpr int U = k1b_u<N>(), CW = 2 * U;  // CW interleaved transforms per CTA
     constexpr int T = N / 16;
-    constexpr int PART = part_floats<N, 16>();
+    constexpr int THREADS = T * CW;
     extern __shared__ float smem[];
     const int pair = blockIdx.y;
-    const int u0 = blockIdx.x * 8;
-    const int c = threadIdx.x % 16, t = threadIdx.x / 16;
-    const int col = c < 8 ? (u0 + c) : ((N - (u0 + c - 8)) & (N - 1));
+    const int u0 = blockIdx.x * U;
+    const int c = threadIdx.x % CW, t = threadIdx.x / CW;
+    const int col = c < U ? (u0 + c) : ((N - (u0 + c - U)) & (N - 1));
     float2* sbuf = reinterpret_cast<float2*>(smem);
-    const Lay<16> lay{sbuf, c};
+    const Lay<CW> lay{sbuf, c};
     const float2* z = p.zbuf + (size_t)pair * N * N;
     float2 v[16];
 #pragma unroll
@@ -165,15 +173,15 @@ __global__ void __launch_bounds__(N) k_rot_cols(Params p) {
     for (int m = 0; m < 16; ++m) lay.put(t + m * T, v[m]);
     __syncthreads();
     // (|F|, |G|) interleaved: one 8-byte load per tap in K2a
-    float2* out = reinterpret_cast<float2*>(p.mag) + ((size_t)pair * (N / 16) + blockIdx.x) * (size_t)(N * 8);
+    float2* out = reinterpret_cast<float2*>(p.mag) + ((size_t)pair * (N / 16) + u0 / 8) * (size_t)(N * 8) + (u0 & 7);
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-        const int o = threadIdx.x + q * N;  // o = v_c * 8 + cc
-        const int cc = o & 7, vc = o >> 3;
+    for (int q = 0; q < N * U / THREADS; ++q) {
+        const int o = threadIdx.x + q * THREADS;  // o = v_c * U + cc
+        const int cc = o % U, vc = o / U;
         const int vn = (vc + N / 2) & (N - 1);  // natural row of centred row vc
         const int vm = (N - vn) & (N - 1);      // row of -v
-        const float2 z1 = Lay<16>{sbuf, cc}.get(vn);
-        const float2 z2 = Lay<16>{sbuf, 8 + cc}.get(vm);
+        const float2 z1 = Lay<CW>{sbuf, cc}.get(vn);
+        const float2 z2 = Lay<CW>{sbuf, U + cc}.get(vm);
         const float fr = z1.x + z2.x, fi = z1.y - z2.y;  // Z1 + conj(Z2)
         const float gr = z1.x - z2.x, gi = z1.y + z2.y;  // Z1 - conj(Z2)
         const int2 bd = __ldg(p.band + vc);
@@ -181,7 +189,7 @@ __global__ void __launch_bounds__(N) k_rot_cols(Params p) {
         const bool in = (u >= bd.x) && (u <= bd.y);
         const float2 mv = in ? make_float2(0.5f * fscan_fft::sqrt_fast(fr * fr + fi * fi), 0.5f * fscan_fft::sqrt_fast(gr * gr + gi * gi))
                              : make_float2(0.0f, 0.0f);
-        out[o] = mv;  // tile [u0 / 8][v_c][cc]
+        out[vc * 8 + cc] = mv;  // tile [u0 / 8][v_c][u0 % 8 + cc]
     }
 }
 
@@ -1309,10 +1317,11 @@ cudaError_t rot_rows(const Params& p, cudaStream_t s) {
 
 template <int N>
 cudaError_t rot_cols(const Params& p, cudaStream_t s) {
-    const size_t sm = (size_t)part_floats<N, 16>() * sizeof(float);
+    constexpr int U = k1b_u<N>();
+    const size_t sm = (size_t)part_floats<N, 2 * U>() * sizeof(float);
     cudaError_t e = set_smem(k_rot_cols<N>, sm);
     if (e != cudaSuccess) return e;
-    k_rot_cols<N><<<dim3(p.zcols / 8, p.batch), N, sm, s>>>(p);
+    k_rot_cols<N><<<dim3(p.zcols / U, p.batch), N / 16 * 2 * U, sm, s>>>(p);
     return cudaGetLastError();
 }
 
