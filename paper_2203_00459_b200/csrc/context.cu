@@ -1077,7 +1077,7 @@ fscan_status fscan_band_magnitude_batch(fscan_ctx* ctx, const float* d_img, int 
         Params p = base_params(ctx, l, cnt, 1.0);
         p.f = d_img + off * nn;
         p.g = d_img + off * nn;
-        p.mag_out = d_out + off * (nn / 2);
+        p.mag_out = d_out + off * ((size_t)ctx->n * ctx->nw);  // [batch][n][n - n/2]
         p.zcols = ctx->nw;  // the whole half plane
         return run_chunk(ctx, l, p, Stages::Magnitude, &ctx->launches_last);
     });
