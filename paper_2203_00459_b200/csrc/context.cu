@@ -728,8 +728,9 @@ fscan_status fscan_ctx_create(int device, const fscan_config* cfg_in, int max_ba
     const double per_pair = (double)n * n * (8 + 4 + 8) + (double)n * (3 * n / 4 + 1) * 16;
     int chunk = (int)std::max(1.0, std::floor((1024.0 * 1024 * 1024) / per_pair));
     // a batch smaller than the lanes' chunks is spread over all lanes (C2, 64
-    // pairs: +7% over one 64-pair chunk)
-    chunk = std::min(chunk, (max_batch + ctx->nlanes - 1) / ctx->nlanes);
+    // pairs: +7% over one 64-pair chunk); tiny contexts keep whole-batch chunks
+    // (the exhaustive search runs pair x candidate items through them)
+    if (max_batch >= 16 * ctx->nlanes) chunk = std::min(chunk, (max_batch + ctx->nlanes - 1) / ctx->nlanes);
     if (const char* e = std::getenv("FSCAN_CHUNK")) chunk = std::max(1, std::atoi(e));
     chunk = std::min(chunk, max_batch);
     ctx->chunk = chunk;
