@@ -4,22 +4,29 @@
 Workload (BASELINE.json configs[3], "C4"): 4096 scan pairs, 512x512 fp32
 Cartesian grids produced from raw polar sweeps by the config-3 generator
 (device-rendered, then the product K0 kernel), per-pixel sigmoid masks,
-720 azimuth bins, soft-argmax T=1, sharded by pair index over the ranks.
-A step = one full pass of the hot path (rotation + translation search, pose
-out) over the rank's shard, inputs resident in HBM (16 GiB > 126 MB L2, so no
-L2 flush is needed between steps).
+720 azimuth bins, soft-argmax T=1. A step = one full pass of the hot path
+(rotation + translation search, pose out, poses gathered to rank 0) over the
+job's pairs, inputs resident in HBM (16 GiB > 126 MB L2, so no L2 flush is
+needed between steps).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 4]
 
-Under torchrun each rank takes pairs [r*B/N, (r+1)*B/N); timing is CUDA
-events on the launching stream, barrier + synchronize on both sides, max over
-ranks; rank 0 prints one JSON line. `--impl reference` times the reference's
-own CPU implementation (oracle/_ref: the reference sources + FFTW-API shim)
-on the host cores instead (rank 0 only).
+Multi-GPU (torchrun, one rank per GPU): BASELINE's C4 is ONE 4096-pair batch
+sharded by pair index, so by default rank r takes pairs shard_range(4096, N, r)
+(strong scaling; --weak gives every rank a full batch). There is no collective
+on the hot path; the per-pair result rows are gathered to rank 0 inside every
+timed step. Timing is CUDA events on the launching stream, barrier +
+synchronize on both sides, max over ranks; rank 0 prints one JSON line.
+
+`--impl reference` times the reference's own CPU implementation (oracle/_ref:
+the reference sources + FFTW-API shim) on the host cores, on inputs from the
+same seeded generator (oracle/libsynth_gen.so) — that process maps no product
+library. Its `config` object is the one this arm prints.
 """
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import math
 import os
@@ -36,8 +43,10 @@ sys.path.insert(0, ROOT)
 
 METRIC = "scan-pair registrations/sec (rot+trans search)"
 UNIT = "pairs/s"
-KERNEL_NAMES = ("rot_rows", "rot_cols", "rot_polar", "theta_in", "xlat_rows", "xlat_cols", "xlat_out",
-                "finalize", "rot_gather", "polar_to_cart", "mag_unpack", "bf_items", "bf_final")
+# (n, n_theta, masks, batch) of BASELINE.json configs 1..5
+CONFIGS = {1: (256, 360, False, 1), 2: (256, 360, True, 64), 3: (512, 720, True, 64),
+           4: (512, 720, True, 4096), 5: (1024, 1440, True, 1024)}
+POLAR_Q = 400 * 3768  # samples per raw polar sweep (C3)
 
 
 def workload_desc(cid: int) -> str:
@@ -51,6 +60,32 @@ def workload_desc(cid: int) -> str:
     }[cid]
 
 
+def job_pairs(args, world: int) -> int:
+    base = args.pairs or CONFIGS[args.config][3]
+    return base * world if args.weak else base
+
+
+def input_bytes_per_rank(cid: int, per: int) -> int:
+    n, _, masks, _ = CONFIGS[cid]
+    grids = (2 * POLAR_Q if cid == 3 else 2 * n * n) + (2 * n * n if masks else 0)
+    return 4 * grids * per
+
+
+def job_config(args, world: int) -> dict:
+    """The `config` object both arms print (identical for the same command line)."""
+    n, nt, masks, _ = CONFIGS[args.config]
+    total = job_pairs(args, world)
+    per = -(-total // world)
+    ib = input_bytes_per_rank(args.config, per)
+    l2 = (f"inputs {ib / 2**30:.1f} GiB per rank per step >> 126 MB L2; no flush needed" if ib >= (512 << 20)
+          else f"inputs {ib / 2**20:.0f} MiB per rank per step < 4x L2: L2 flushed (a 256 MiB buffer written) between "
+               "timed steps, each step timed by its own events")
+    return {"workload": workload_desc(args.config), "pairs": total, "n_xy": n, "n_theta": nt, "masks": masks,
+            "parallelism": f"dp{world}: pairs sharded by index ({'weak, a full batch per rank' if args.weak else 'strong, one batch split over the ranks'}), "
+                           "no collective on the hot path, result rows gathered to rank 0 every step",
+            "l2": l2}
+
+
 def pair_bytes(n: int, n_theta: int, pad: int, masks: bool = True, s_in: float | None = None) -> float:
     """SURVEY.md §8(d) algorithmic bytes per pair of the canonical staged dataflow."""
     P = 2 * n
@@ -62,24 +97,24 @@ def pair_bytes(n: int, n_theta: int, pad: int, masks: bool = True, s_in: float |
     return s_in + 8 * (1 if masks else 0) * n * n + 16 * n * n + 16 * HN + 32 * HP + 8 * L + 16
 
 
-def kernel_alg_bytes(name: str, n: int) -> float:
-    """Compulsory DRAM bytes per pair of each of OUR kernels."""
+def kernel_alg_bytes(name: str, n: int, wcols: int, masks: bool = True) -> float:
+    """Compulsory DRAM bytes per pair of each of OUR kernels.
+    wcols = spectrum columns u < W the rotation stage keeps (fscan_ctx_rot_columns):
+    K1a stores 2W - 1 columns of the packed spectrum, K1b writes W columns of the
+    two magnitude half planes."""
     nn = n * n
     h1 = 3 * n // 4 + 1  # M/2 + 1 spectral bins of the length M = 3N/2 translation transforms
+    zc = 2 * wcols - 1
     return {
-        "rot_rows": 16 * nn + 8 * nn + 8 * nn,            # f,g,mf,mg in; f~,g~ out; Z out
-        "rot_cols": 8 * nn + 4 * nn,                      # Z in; |F|,|G| half planes out
-        "rot_gather": 4 * nn,                             # magnitude planes in (polar gather)
+        "rot_rows": (16 if masks else 8) * nn + 8 * nn + 8 * n * zc,  # f,g(,mf,mg) in; f~,g~ out; Z columns out
+        "rot_cols": 8 * n * zc + 8 * n * wcols,           # Z columns in; |F|,|G| (W columns) out
+        "rot_gather": 8 * n * wcols,                      # magnitude planes in (polar gather; upper bound)
         "rot_polar": 0.0,                                 # profiles only (fp64 correlation)
         "xlat_rows": 8 * nn + 16 * n * h1,                # f~,g~ in; row spectra (F,G; M/2+1 bins) out
         "xlat_cols": 16 * n * h1 + 8 * n * h1,            # row spectra in; Y (N lags x M/2+1) out
         "xlat_out": 8 * n * h1 + 4 * nn,                  # Y in; surface out
-        "finalize": 0.0,
-        "theta_in": 0.0,
-        "mag_unpack": 0.0,
-        "bf_items": 0.0,
-        "bf_final": 0.0,
-        "polar_to_cart": 2 * (4 * 400 * 3768 + 4 * nn),   # both raw sweeps in, both grids out
+        "finalize": 0.0, "theta_in": 0.0, "mag_unpack": 0.0, "bf_items": 0.0, "bf_final": 0.0,
+        "polar_to_cart": 2 * (4 * POLAR_Q + 4 * nn),      # both raw sweeps in, both grids out
     }[name]
 
 
@@ -108,7 +143,7 @@ class ClockSampler:
                     self.rows.append([x.strip() for x in out.split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.1)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -142,45 +177,50 @@ def peaks() -> tuple[float, str]:
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic(kernel: str) -> float | None:
-    """DRAM bytes per launch of `kernel` from the committed ncu --set full summary, if any."""
-    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+NCU_TRAFFIC = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+
+
+def ncu_traffic(kernel: str, n: int) -> float | None:
+    """DRAM bytes per pair of `kernel` from the committed ncu --set full capture of a
+    C4 chunk (profiles/ncu_traffic.json; None for other grid sides)."""
     try:
-        with open(path) as fh:
+        with open(NCU_TRAFFIC) as fh:
             d = json.load(fh)
+        if d.get("n_xy", 512) != n:
+            return None
         return d.get(kernel, {}).get("dram_bytes_per_pair")
     except Exception:
         return None
 
 
 def ncu_issue(kernel: str, n: int) -> dict | None:
-    """What bounds `kernel` when DRAM does not: its issue-slot and DRAM utilisation
-    in the committed ncu --set full capture (profiles/r01/ncu_full_summary.json,
-    the C4 grid side; None for a kernel or grid side it did not capture)."""
-    path = os.path.join(ROOT, "profiles", "r01", "ncu_full_summary.json")
+    """What bounds `kernel` when DRAM does not: its issue-slot and DRAM utilisation in
+    the same committed capture (None for a kernel or grid side it did not capture)."""
     try:
-        with open(path) as fh:
-            for k in json.load(fh)["kernels"]:
-                if n != 512:  # the capture is of one C4 chunk (N = 512)
-                    return None
-                if k["kernel"].partition("<")[0] == "k_" + kernel:
-                    return {"issue_active_frac": round(k["issue_pct"] / 100, 3),
-                            "dram_frac": round(k["dram_pct"] / 100, 3),
-                            "source": "ncu --set full, profiles/r01/ncu_full_summary.json"}
+        with open(NCU_TRAFFIC) as fh:
+            d = json.load(fh)
+        if d.get("n_xy", 512) != n or kernel not in d or "issue_pct" not in d[kernel]:
+            return None
+        k = d[kernel]
+        return {"issue_active_frac": round(k["issue_pct"] / 100, 3), "dram_frac": round(k["dram_pct"] / 100, 3),
+                "warps_active_frac": round(k["warps_active_pct"] / 100, 3), "source": d.get("source", NCU_TRAFFIC)}
     except Exception:
         return None
-    return None
 
 
-def dist_setup():
+def dist_setup(backend: str):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch
         import torch.distributed as dist
+        local = local % max(1, torch.cuda.device_count())
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     return world, rank, local
 
 
@@ -195,7 +235,8 @@ def allmax(world, x: float, device) -> float:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device=device)
+    on_dev = dist.get_backend() == "nccl"
+    t = torch.tensor([x], dtype=torch.float64, device=device if on_dev else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -207,19 +248,107 @@ def cpu_threads() -> int:
         return os.cpu_count() or 1
 
 
-def ref_cpu_run(f, g, mf, mg, cfg, delta, threads):
-    """The reference's own scan_match over a batch (oracle/_ref, parallel_for)."""
+def loaded_libraries() -> list[str]:
+    """Repo .so files mapped into this process (what ran, for the record)."""
+    libs = set()
+    try:
+        with open("/proc/self/maps") as fh:
+            for line in fh:
+                p = line.split()[-1] if line.strip() else ""
+                if p.endswith(".so") and p.startswith(ROOT):
+                    libs.add(os.path.relpath(p, ROOT))
+    except OSError:
+        pass
+    return sorted(libs)
+
+
+def file_sha16(path: str) -> str | None:
+    try:
+        with open(path, "rb") as fh:
+            return hashlib.sha256(fh.read()).hexdigest()[:16]
+    except OSError:
+        return None
+
+
+def pct(xs, q):
+    xs = sorted(xs)
+    if not xs:
+        return None
+    k = min(len(xs) - 1, max(0, int(math.ceil(q / 100.0 * len(xs))) - 1))
+    return xs[k]
+
+
+def ref_batch(f, g, mf, mg, oc, delta, threads):
+    """The reference's own scan_match over a batch (oracle/_ref, parallel_for):
+    (seconds, kind, per-pair FoResult array)."""
     import oracle
-    oc = oracle.make_config(**{k: (int(v) if isinstance(v, bool) else v) for k, v in cfg.__dict__.items()})
     if oracle.have_ref():
         t0 = time.perf_counter()
-        oracle.ref_batch_f32(f, g, mf, mg, oc, delta, threads)
-        return time.perf_counter() - t0, "reference"
-    # port fallback (restatement), single thread per call
-    t0 = time.perf_counter()
+        res = oracle.ref_batch_f32(f, g, mf, mg, oc, delta, threads)
+        return time.perf_counter() - t0, "reference", res
+    t0 = time.perf_counter()  # the fp64 restatement (port), one pair at a time
+    res = [oracle.scan_match(f[i], g[i], oc, delta, None if mf is None else mf[i], None if mg is None else mg[i])
+           for i in range(f.shape[0])]
+    return time.perf_counter() - t0, "port", res
+
+
+def cpu_single_thread(f, g, mf, mg, oc, delta, budget_s: float = 6.0) -> dict:
+    """Reference scan_match on ONE thread, pair by pair (median / p95 ms per pair)."""
+    times = []
+    kind = "reference"
+    t_end = time.perf_counter() + budget_s
     for i in range(f.shape[0]):
-        oracle.scan_match(f[i], g[i], oc, delta, mf[i], mg[i])
-    return time.perf_counter() - t0, "port"
+        s, kind, _ = ref_batch(f[i:i + 1], g[i:i + 1], None if mf is None else mf[i:i + 1],
+                               None if mg is None else mg[i:i + 1], oc, delta, 1)
+        times.append(s * 1e3)
+        if time.perf_counter() > t_end and len(times) >= 2:
+            break
+    return {"value": round(1e3 / statistics.mean(times), 4), "unit": UNIT, "cores": 1, "kind": kind,
+            "ms_per_pair_median": round(statistics.median(times), 1), "ms_per_pair_p95": round(pct(times, 95), 1),
+            "sample": f"first {len(times)} pairs, one at a time on one thread"}
+
+
+# ---------------------------------------------------------------- parity (GPU vs the reference, same inputs)
+
+SURF_NEAR_TIE = 4 * 4e-7  # 4x the largest surface error |GPU - oracle| / max|ref| seen in the parity suite
+
+
+def parity_block(f, g, mf, mg, gpu_rows, ref_rows, oc, delta, kind) -> dict:
+    """Integer bins / cells and soft poses of the GPU rows against the reference's own
+    scan_match on the same (device-rendered) inputs (BASELINE north_star gates). A
+    mismatched bin counts as a documented near-tie only if the reference's top-2 gap
+    on that surface is below SURF_NEAR_TIE (SURVEY.md §8(d) rule)."""
+    import oracle
+    cnt = len(ref_rows)
+    tb = np.array([r.theta_bin for r in ref_rows])
+    cells = np.array([(r.xy_row, r.xy_col) for r in ref_rows])
+    rpose = np.array([(r.theta, r.tx, r.ty) for r in ref_rows])
+    gb = gpu_rows["theta_bin"][:cnt]
+    gc = np.stack([gpu_rows["xy_row"][:cnt], gpu_rows["xy_col"][:cnt]], 1)
+    gpose = np.stack([gpu_rows["theta"][:cnt], gpu_rows["tx"][:cnt], gpu_rows["ty"][:cnt]], 1)
+    bins_eq = gb == tb
+    cells_eq = (gc == cells).all(1)
+    ok = bins_eq & cells_eq
+    near, unexplained = [], []
+    for i in np.nonzero(~ok)[0][:8]:  # surfaces of the (rare) mismatches, both sides
+        r = oracle.scan_match(f[i], g[i], oc, delta, mf[i], mg[i], which="ref" if kind == "reference" else "oracle")
+        ts = r.theta_surface
+        xs = r.xy_surface
+        gap_t = (ts[r.theta_bin] - ts[int(gb[i])]) / np.abs(ts).max()
+        gap_x = (xs[r.xy_row, r.xy_col] - xs[int(gc[i][0]), int(gc[i][1])]) / np.abs(xs).max()
+        (near if max(gap_t, gap_x) < SURF_NEAR_TIE else unexplained).append(
+            {"pair": int(i), "theta_gap": float(gap_t), "xy_gap": float(gap_x)})
+    unexplained += [{"pair": int(i)} for i in np.nonzero(~ok)[0][8:]]
+    d = np.abs(gpose[ok] - rpose[ok]) if ok.any() else np.zeros((0, 3))
+    return {"pairs": int(cnt), "bins_equal": int(bins_eq.sum()), "cells_equal": int(cells_eq.sum()),
+            "near_ties": near, "unexplained": unexplained,
+            "max_dtheta_rad": float(d[:, 0].max()) if len(d) else None,
+            "max_dt_px": float(d[:, 1:].max() / delta) if len(d) else None,
+            "gates": {"theta_rad": 1e-3, "t_px": 1e-2},
+            "pass": bool(not unexplained and (not len(d) or (d[:, 0].max() <= 1e-3 and d[:, 1:].max() <= 1e-2 * delta))),
+            "reference": ("oracle/_ref: the reference's own scan_match (FFTW-API shim)" if kind == "reference"
+                          else "fp64 C restatement (oracle/_ref not built)"),
+            "inputs": "the GPU run's own device-rendered inputs, copied to the host"}
 
 
 # ---------------------------------------------------------------- our arm
@@ -227,29 +356,26 @@ def ref_cpu_run(f, g, mf, mg, cfg, delta, threads):
 def run_ours(args):
     import torch
     import paper_2203_00459_b200 as fb
+    from paper_2203_00459_b200.shard import gather_results, shard_range
 
-    world, rank, local = dist_setup()
+    world, rank, local = dist_setup(args.backend)
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-    cfg, delta, total = fb.baseline_config(args.config)
-    if args.pairs:
-        total = args.pairs
-    # weak scaling (default): every rank registers the config's batch, a disjoint
-    # block of pair indices of a world x batch job; --strong splits one batch
-    if not args.strong:
-        total *= world
-    from paper_2203_00459_b200.shard import gather_results, shard_range
+    cfg, delta, _ = fb.baseline_config(args.config)
+    total = job_pairs(args, world)
     first, per = shard_range(total, world, rank)
     spec = fb.synth_spec(args.config)
+    polar = args.config == 3
 
     # inputs: device-rendered shard (pairs first .. first+per)
     f, g, mf, mg, truth = fb.synth_pairs_device(spec, first, per, device=local)
-    m = fb.Matcher(cfg, max_batch=per, device=local, chunk=args.chunk)
+    if not spec.masks:
+        mf = mg = None
+    m = fb.Matcher(cfg, max_batch=max(per, 1), device=local, chunk=args.chunk)
     if not args.no_graphs:
         m.set_graphs(True)  # replay the call's launch sequence as one CUDA graph (fscan_ctx_set_graphs)
     out = torch.empty(per * fb.RESULT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
-    polar = args.config == 3
     if polar:  # C3: the raw sweeps are the input; K0 runs inside every step
         pf, pg, _ = fb.synth_polar_device(spec, first, per, device=local)
 
@@ -258,52 +384,53 @@ def run_ours(args):
             return m.match_polar(pf, pg, mf, mg, range_res=spec.range_res, delta=delta, out=out, stream=stream)
         return m.match_device(f, g, mf, mg, delta=delta, out=out, stream=stream)
 
+    rows = out.view(per, fb.RESULT_DTYPE.itemsize)
+
+    def gather():  # pose gather to rank 0 (inside the timed step)
+        return gather_results(rows, total, world, rank)
+
     for _ in range(args.warmup):
         step()
+        gather()
     torch.cuda.synchronize(dev)
     launches_per_step = m.launches_last
-    res = fb.decode_results(out)
-    bad = int((res["status"] != 0).sum())
 
-    # inputs that fit in the 126 MB L2 (C2: 64 pairs of 256^2) are timed step by
-    # step with a 256 MB buffer written between the steps, outside the events
-    in_bytes = sum(t.numel() * t.element_size() for t in ((pf, pg) if polar else (f, g)) + (mf, mg)
-                   if t is not None)
-    flush = torch.empty(64 << 20, dtype=torch.float32, device=dev) if in_bytes < (512 << 20) else None
-    l2_note = (f"inputs {in_bytes / 2**20:.0f} MiB per step < 2x L2: a 256 MiB buffer written between timed "
-               "steps, each step timed by its own events" if flush is not None else
-               f"inputs {in_bytes / 2**30:.1f} GiB per step >> 126 MB L2; no flush needed")
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # inputs that fit in the 126 MB L2 (C1/C2) are timed step by step with a 256 MiB
+    # buffer written between the steps, outside the events
+    flush = None
+    if input_bytes_per_rank(args.config, per) < (512 << 20):
+        flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps)]
     barrier(world)
     torch.cuda.synchronize(dev)
+    gathered = None
     with ClockSampler(local) as clk:
-        if flush is None:
-            ev0.record(stream)
-            for _ in range(args.steps):
-                step()
-            ev1.record(stream)
-            torch.cuda.synchronize(dev)
-            ms = ev0.elapsed_time(ev1)
-        else:
-            ms = 0.0
-            for _ in range(args.steps):
+        for i in range(args.steps):
+            if flush is not None:
                 with torch.cuda.stream(stream):
                     flush.fill_(1.0)
-                ev0.record(stream)
-                step()
-                ev1.record(stream)
-                torch.cuda.synchronize(dev)
-                ms += ev0.elapsed_time(ev1)
+            if flush is not None or i == 0:
+                evs[2 * i].record(stream)
+            step()
+            gathered = gather()
+            evs[2 * i + 1].record(stream)
+        torch.cuda.synchronize(dev)
+    if flush is None:  # back to back: step i spans end(i-1) .. end(i)
+        ends = [evs[2 * i + 1] for i in range(args.steps)]
+        step_ms = [evs[0].elapsed_time(ends[0])] + [ends[i - 1].elapsed_time(ends[i]) for i in range(1, args.steps)]
+    else:
+        step_ms = [evs[2 * i].elapsed_time(evs[2 * i + 1]) for i in range(args.steps)]
+    ms = sum(step_ms)
     barrier(world)
     ms_max = allmax(world, ms, dev)
     value = total * args.steps / (ms_max / 1e3)
-
-    # pose gather to rank 0 (off the timed region): [total, sizeof(result)] bytes in pair order
-    rows = out.view(per, fb.RESULT_DTYPE.itemsize)
-    gathered = gather_results(rows, total, world, rank)
+    bad = None
+    res0 = None
     if rank == 0:
-        allres = fb.decode_results(gathered.reshape(-1))
-        bad = int((allres["status"] != 0).sum())
+        res0 = fb.decode_results(gathered.reshape(-1))
+        bad = int((res0["status"] != 0).sum())
+    if args.dump_results and rank == 0:
+        np.save(args.dump_results, res0)
 
     # per-kernel breakdown: one instrumented step (events around every kernel)
     m.set_profiling(True)
@@ -314,24 +441,51 @@ def run_ours(args):
     dom = max(kt.items(), key=lambda kv: kv[1][0])[0]
     dom_ms, dom_launches = kt[dom]
     pairs_per_launch = per / dom_launches
-    alg = kernel_alg_bytes(dom, cfg.n_xy) * pairs_per_launch
+    wcols = m.rot_columns
+    alg = kernel_alg_bytes(dom, cfg.n_xy, wcols, mf is not None) * pairs_per_launch
     achieved = alg / (dom_ms / dom_launches / 1e3) / 1e9
     peak, peak_src = peaks()
-    traffic = ncu_traffic(dom)
+    traffic = ncu_traffic(dom, cfg.n_xy)
     roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "peak_source": peak_src,
                 "traffic": None if traffic is None else traffic * pairs_per_launch,
-                "alg_bytes_per_launch": alg, "avg_launch_ms": dom_ms / dom_launches,
+                "alg_bytes_per_launch": alg, "pairs_per_launch": round(pairs_per_launch, 2),
+                "avg_launch_ms": dom_ms / dom_launches,
                 "kernel_share": round(dom_ms / sum(v[0] for v in kt.values()), 3),
                 # the dominant kernel is FFT-issue-bound, not DRAM-bound: its ncu issue
                 # utilisation says how close it runs to its own ceiling
                 "ncu": ncu_issue(dom, cfg.n_xy)}
-    bpair = pair_bytes(cfg.n_xy, cfg.n_theta, cfg.pad_angle,
+    bpair = pair_bytes(cfg.n_xy, cfg.n_theta, cfg.pad_angle, masks=mf is not None,
                        s_in=(8.0 * spec.n_az * spec.n_range) if polar else None)
     pipeline = {"b_pair_bytes": bpair, "achieved_gbs": round(value * bpair / 1e9 / world, 1),
                 "frac_of_measured_peak_per_gpu": round(value * bpair / world / (peak * 1e9), 4),
                 "frac_of_8TBps_per_gpu": round(value * bpair / world / 8e12, 4),
-                "kernel_ms_per_step": {k: round(v[0], 3) for k, v in kt.items()}}
+                "kernel_ms_per_step": {k: round(v[0], 3) for k, v in kt.items()},
+                "kernel_alg_gbs": {k: round(kernel_alg_bytes(k, cfg.n_xy, wcols, mf is not None) * per
+                                            / (v[0] / 1e3) / 1e9, 1) for k, v in kt.items()
+                                   if kernel_alg_bytes(k, cfg.n_xy, wcols, mf is not None) > 0}}
+
+    # per-GPU efficiency at the 4- and 8-GPU shard sizes of this job (1-GPU proxy
+    # of the strong-scaling curve before 8-GPU hardware is available)
+    proxy = None
+    if rank == 0 and world == 1 and not args.no_proxy and not polar and total >= 256:
+        proxy = {}
+        for shard in sorted({total // 8, total // 4, total // 2}):
+            so = torch.empty(shard * fb.RESULT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+            call = lambda: m.match_device(f[:shard], g[:shard], None if mf is None else mf[:shard],  # noqa: E731
+                                          None if mg is None else mg[:shard], delta=delta, out=so, stream=stream)
+            for _ in range(3):
+                call()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = max(3, args.steps)
+            e0.record(stream)
+            for _ in range(reps):
+                call()
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            rate = shard * reps / (e0.elapsed_time(e1) / 1e3)
+            proxy[str(shard)] = {"pairs_per_s": round(rate, 1), "per_gpu_efficiency": round(rate / value, 3),
+                                 "as_shard_of": f"{total // shard} GPUs"}
 
     # the paper's central comparison: the exhaustive correlative search (the
     # reference's brute_force_match, oracle.cpp:40-67) over the matcher's full theta
@@ -357,8 +511,7 @@ def run_ours(args):
     # consecutive scans of one sequence, each scan's rotation spectrum shared by its
     # two pairs; reported beside the independent-pair value
     chain = None
-    if rank == 0 and not args.no_odometry and not polar:
-        # a generated drive: per + 1 scans of one scene, consecutive scans related
+    if rank == 0 and not args.no_odometry and not polar and per >= 2:
         seq, seqm, _ = fb.synth_sequence_device(spec, first, per + 1, device=local)
         mo = fb.Matcher(cfg, max_batch=per, device=local, chunk=args.chunk)
         oout = torch.empty(per * fb.RESULT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
@@ -378,116 +531,139 @@ def run_ours(args):
 
     # e2e through the public host API (H2D + compute + D2H each step)
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not polar:
         try:
             import psutil
-            need = 4 * f.numel() * 4 * 1.2
+            grids = 4 if mf is not None else 2
+            need = grids * f.numel() * 4 * 1.2
             if psutil.virtual_memory().available < need + (8 << 30):
                 raise MemoryError("not enough host RAM for pinned inputs")
-            hf, hg, hmf, hmg = (torch.empty(f.shape, dtype=torch.float32, pin_memory=True) for _ in range(4))
-            for h, d in ((hf, f), (hg, g), (hmf, mf), (hmg, mg)):
+            hs = [torch.empty(f.shape, dtype=torch.float32, pin_memory=True) for _ in range(grids)]
+            for h, d in zip(hs, (f, g, mf, mg)):
                 h.copy_(d)
-            nf, ng, nmf, nmg = (h.numpy() for h in (hf, hg, hmf, hmg))
-            m.match_host(nf, ng, nmf, nmg, delta=delta)  # warm
-            steps_e2e = max(1, min(args.steps, 3))
+            nps = [h.numpy() for h in hs] + [None] * (4 - grids)
+            m.match_host(*nps, delta=delta)  # warm
+            steps_e2e = max(1, min(args.steps, 10))
             barrier(world)
             t0 = time.perf_counter()
             for _ in range(steps_e2e):
-                m.match_host(nf, ng, nmf, nmg, delta=delta)
+                m.match_host(*nps, delta=delta)
             dt = allmax(world, time.perf_counter() - t0, dev)
             e2e = {"value": round(total * steps_e2e / dt, 1), "unit": UNIT,
-                   "h2d_bytes_per_step": int(4 * f.numel() * 4 * world),
+                   "h2d_bytes_per_step": int(grids * f.numel() * 4 * world),
                    "d2h_bytes_per_step": int(total * fb.RESULT_DTYPE.itemsize), "steps": steps_e2e,
                    "api": "fscan_match_batch_host (pinned host buffers)"}
             # what bounds it: this rank's H2D rate inside the e2e steps against a
             # plain pinned -> device copy of one input grid set on the same link
-            e2e["h2d_gbs"] = round(4 * f.numel() * 4 * steps_e2e / dt / 1e9, 1)
+            e2e["h2d_gbs"] = round(grids * f.numel() * 4 * steps_e2e / dt / 1e9, 1)
             c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             dst = torch.empty_like(f)
-            dst.copy_(hf, non_blocking=True)
+            dst.copy_(hs[0], non_blocking=True)
             torch.cuda.synchronize()
             best = float("inf")
             for _ in range(3):
                 c0.record()
-                dst.copy_(hf, non_blocking=True)
+                dst.copy_(hs[0], non_blocking=True)
                 c1.record()
                 c1.synchronize()
                 best = min(best, c0.elapsed_time(c1) / 1e3)
-            e2e["pinned_copy_h2d_gbs"] = round(hf.numel() * 4 / best / 1e9, 1)
-            del hf, hg, hmf, hmg, dst
+            e2e["pinned_copy_h2d_gbs"] = round(hs[0].numel() * 4 / best / 1e9, 1)
+            del hs, nps, dst
         except Exception as exc:  # report, never fake
             e2e = {"value": None, "unit": UNIT, "error": str(exc)[:200]}
 
-    # CPU baseline: the reference on the host cores, bounded sample (rank 0, N=1)
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    # CPU baseline + parity: the reference on the host cores on a bounded sample of
+    # this run's own inputs (rank 0, N=1), results compared with the GPU's rows
+    cpu = parity = None
+    if rank == 0 and world == 1 and not args.no_cpu and not polar:
+        import oracle
+        oc = oracle.make_config(**{k: (int(v) if isinstance(v, bool) else v) for k, v in cfg.__dict__.items()})
         threads = cpu_threads()
-        # pilot of one pair per thread, then a sample sized for ~15 s of CPU work
+        # pilot of one pair per thread, then a sample sized for ~12 s of CPU work
         pilot = int(min(per, threads))
-        hs = [x[:pilot].cpu().numpy() for x in (f, g, mf, mg)]
-        psecs, _ = ref_cpu_run(*hs, cfg, delta, threads)
-        sample = int(min(per, max(pilot, round(15.0 * pilot / max(psecs, 1e-3) / threads) * threads)))
-        hs = [x[:sample].cpu().numpy() for x in (f, g, mf, mg)]
-        secs, kind = ref_cpu_run(*hs, cfg, delta, threads)
+        host = lambda k: [None if x is None else x[:k].cpu().numpy() for x in (f, g, mf, mg)]  # noqa: E731
+        psecs, _, _ = ref_batch(*host(pilot), oc, delta, threads)
+        sample = int(min(per, max(pilot, round(12.0 * pilot / max(psecs, 1e-3) / threads) * threads)))
+        hs = host(sample)
+        secs, kind, ref_rows = ref_batch(*hs, oc, delta, threads)
         cpu = {"value": round(sample / secs, 3), "unit": UNIT, "cores": threads, "kind": kind,
                "sample": f"first {sample} pairs of the {workload_desc(args.config).split(':')[0]} workload "
-                         f"({secs:.1f} s wall, reference scan_match via parallel_for, FFTW-API shim not FFTW)"}
+                         f"({secs:.1f} s wall, reference scan_match via parallel_for, FFTW-API shim not FFTW)",
+               "single_thread": cpu_single_thread(*hs, oc, delta),
+               "host": oracle.host_descriptor()}
+        gpu_rows = fb.decode_results(out)
+        parity = parity_block(*hs, gpu_rows, ref_rows, oc, delta, kind)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 3), "higher_is_better": True,
-            "scaling": "strong" if args.strong else "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (seeded generator)",
-            "config": {"workload": workload_desc(args.config), "pairs": total, "pairs_per_rank": per,
-                       "n_xy": cfg.n_xy, "n_theta": cfg.n_theta, "chunk": args.chunk or "auto",
-                       "l2": l2_note, "graphs": not args.no_graphs,
-                       "parallelism": f"dp{world} (pairs sharded by index, no collective on the hot path)"},
-            "roofline": roofline, "hbm_pipeline": pipeline, "cpu_baseline": cpu, "e2e": e2e,
-            "exhaustive_search": exhaustive, "odometry_chain": chain,
+            "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 3),
+            "step_ms": {"median": round(statistics.median(step_ms), 3), "p95": round(pct(step_ms, 95), 3),
+                        "min": round(min(step_ms), 3)},
+            "higher_is_better": True, "scaling": "weak" if args.weak else "strong", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic (seeded generator)",
+            "config": job_config(args, world),
+            "impl_config": {"chunk": args.chunk or "auto", "graphs": not args.no_graphs,
+                            "pairs_per_rank": per, "backend": args.backend if world > 1 else None},
+            "roofline": roofline, "hbm_pipeline": pipeline, "cpu_baseline": cpu, "parity": parity,
+            "e2e": e2e, "shard_proxy": proxy, "exhaustive_search": exhaustive, "odometry_chain": chain,
             "clocks": clk.summary(), "gpu_launches": launches_per_step * args.steps,
             "bad_pairs": bad, "impl": "ours",
+            "library": {"path": os.path.relpath(fb.LIB_PATH, ROOT), "sha16": file_sha16(fb.LIB_PATH),
+                        "loaded": loaded_libraries()},
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
+        dist.barrier()
         dist.destroy_process_group()
 
 
 # ---------------------------------------------------------------- reference arm
 
 def run_reference(args):
+    """The reference's own CPU scan_match (oracle/_ref) on the host cores: every step a
+    bounded sample of the job (one pair per host thread), inputs from the same seeded
+    generator (oracle/libsynth_gen.so). Maps no product library."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     import oracle
-    import paper_2203_00459_b200 as fb  # config + host generator only (no GPU code runs)
-    cfg, delta, total = fb.baseline_config(args.config)
+    oc, delta, _ = oracle.baseline_config(args.config)
     threads = cpu_threads()
-    sample = int(max(8, min(threads, 128)))
-    spec = fb.synth_spec(args.config)
-    f, g, mf, mg, _ = fb.synth_pairs_host(spec, 0, sample, threads=threads)
-    kind = "reference" if oracle.have_ref() else "port"
+    sample = threads
+    if args.config == 1:
+        sample = 1
+    f, g, mf, mg, _ = oracle.synth_pairs_host(args.config, 0, sample, threads=threads)
+    if not CONFIGS[args.config][2]:
+        mf = mg = None
     for _ in range(args.warmup):
-        ref_cpu_run(f[:threads], g[:threads], mf[:threads], mg[:threads], cfg, delta, threads)
+        ref_batch(f, g, mf, mg, oc, delta, threads)
     secs = []
+    kind = "reference"
     for _ in range(args.steps):
-        s, kind = ref_cpu_run(f, g, mf, mg, cfg, delta, threads)
+        s, kind, _ = ref_batch(f, g, mf, mg, oc, delta, threads)
         secs.append(s)
     tot = sum(secs)
     value = sample * args.steps / tot
+    single = cpu_single_thread(f, g, mf, mg, oc, delta, budget_s=5.0)
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(1e3 * tot / args.steps, 1), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator)",
-        "config": {"workload": workload_desc(args.config), "pairs_per_step": sample, "n_xy": cfg.n_xy,
-                   "n_theta": cfg.n_theta},
+        "warmup": args.warmup, "ms_per_step": round(1e3 * tot / args.steps, 1),
+        "step_ms": {"median": round(1e3 * statistics.median(secs), 1), "p95": round(1e3 * pct(secs, 95), 1),
+                    "min": round(1e3 * min(secs), 1)},
+        "higher_is_better": True, "scaling": "weak" if args.weak else "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded generator)",
+        "config": job_config(args, world),
         "impl": "reference",
         "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": threads, "kind": kind,
-                         "sample": f"{sample} pairs of the workload per step, reference scan_match via "
-                                   f"parallel_for on {threads} threads (FFTW-API shim, not FFTW)"},
+                         "sample": f"{sample} pairs of the job per step (pairs 0..{sample - 1}, one per host "
+                                   f"thread), reference scan_match via parallel_for on {threads} threads "
+                                   "(FFTW-API shim, not FFTW)",
+                         "single_thread": single, "host": oracle.host_descriptor()},
         "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "library": {"loaded": loaded_libraries()},
     }
     print(json.dumps(line), flush=True)
 
@@ -503,12 +679,16 @@ def main():
     ap.add_argument("--chunk", type=int, default=0, help="pairs per pipeline chunk (0 = auto)")
     ap.add_argument("--no-graphs", action="store_true", help="launch the kernels directly instead of "
                     "replaying the match call's CUDA graph")
+    ap.add_argument("--weak", action="store_true",
+                    help="every rank registers a full batch (default: the batch is split over the ranks)")
+    ap.add_argument("--backend", choices=("nccl", "gloo"), default="nccl",
+                    help="torch.distributed backend for N > 1 (gloo: the CPU-side test of the multi-rank path)")
+    ap.add_argument("--dump-results", default="", help="rank 0 saves the gathered result rows (.npy)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-proxy", action="store_true", help="skip the per-shard-size proxy lines")
     ap.add_argument("--no-exhaustive", action="store_true", help="skip the brute-force comparison leg")
     ap.add_argument("--no-odometry", action="store_true", help="skip the chained-sequence leg")
-    ap.add_argument("--strong", action="store_true",
-                    help="split the config's batch over the ranks (default: weak scaling, one batch per rank)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

@@ -185,6 +185,11 @@ fscan_status fscan_check_results(const fscan_pair_result* d_out, int batch, void
 
 /* Number of kernels the last fscan_match_batch launched (for bench accounting). */
 int fscan_ctx_launches_last(const fscan_ctx* ctx);
+/* Spectrum columns u in [0, W) the rotation stage keeps per scan pair (the
+ * columns any polar tap reads, rounded up to the column-kernel block); the row
+ * kernel stores 2W - 1 columns (u < W and their mirrors). For the bench's
+ * algorithmic-byte accounting. */
+int fscan_ctx_rot_columns(const fscan_ctx* ctx);
 
 /* Opt-in phase correlation (no reference code): the translation
  * stage normalises the cross-power spectrum, X / |X| (0 where X = 0), before

@@ -17,6 +17,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_ORACLE = os.path.join(HERE, "liboracle.so")
 LIB_REF = os.path.join(HERE, "_ref", "libfscan_ref.so")
+LIB_GEN = os.path.join(HERE, "libsynth_gen.so")
 REF_SRC = "/root/reference/proj"
 
 
@@ -301,3 +302,84 @@ def ref_batch_f32(f, g, mf, mg, cfg: FoConfig, delta: float, threads: int):
     if rc != 0:
         raise OracleError(f"ref batch failed rc={rc}")
     return out
+
+
+# ---------------------------------------------------------------- inputs for the CPU arm
+# bench.py's reference arm must not map the product library; it builds its
+# inputs with libsynth_gen.so (the product's host renderer compiled on its own,
+# oracle/Makefile) and its configs with the restated finalize (fo_finalize).
+
+class SynthSpec(C.Structure):
+    """fscan_synth_spec (include/fscan_synth.h)."""
+    _fields_ = [
+        ("polar", C.c_int), ("n", C.c_int), ("delta", C.c_double),
+        ("n_reflectors", C.c_int), ("n_segments", C.c_int),
+        ("sigma_lo_px", C.c_double), ("sigma_hi_px", C.c_double), ("seg_sigma_px", C.c_double),
+        ("extent_frac", C.c_double), ("theta_max", C.c_double), ("t_max", C.c_double),
+        ("speckle", C.c_double), ("masks", C.c_int), ("mask_sigma", C.c_double),
+        ("n_az", C.c_int), ("n_range", C.c_int), ("range_res", C.c_double), ("att_r0", C.c_double),
+        ("seed", C.c_uint64),
+    ]
+
+
+def gen_lib() -> C.CDLL:
+    if "gen" in _libs:
+        return _libs["gen"]
+    if not os.path.exists(LIB_GEN):
+        build(ref=False)
+    L = C.CDLL(LIB_GEN)
+    L.fscan_synth_preset.argtypes = [C.c_int, C.POINTER(SynthSpec)]
+    L.fscan_synth_preset.restype = C.c_int
+    L.fscan_synth_pairs_host.argtypes = [C.POINTER(SynthSpec), C.c_int, C.c_int] + [C.c_void_p] * 5 + [C.c_int]
+    L.fscan_synth_pairs_host.restype = C.c_int
+    _libs["gen"] = L
+    return L
+
+
+def synth_pairs_host(config_id: int, first: int, count: int, threads: int = 0, **overrides):
+    """(f, g, mf, mg, truth) of BASELINE config `config_id`, pairs [first, first + count)."""
+    L = gen_lib()
+    spec = SynthSpec()
+    if L.fscan_synth_preset(int(config_id), C.byref(spec)) != 0:
+        raise ValueError(f"unknown config {config_id}")
+    for k, v in overrides.items():
+        setattr(spec, k, v)
+    n = spec.n
+    f = np.empty((count, n, n), np.float32)
+    g, mf, mg = np.empty_like(f), np.empty_like(f), np.empty_like(f)
+    truth = np.empty((count, 3), np.float64)
+    rc = L.fscan_synth_pairs_host(C.byref(spec), first, count, f.ctypes.data, g.ctypes.data, mf.ctypes.data,
+                                  mg.ctypes.data, truth.ctypes.data, int(threads))
+    if rc:
+        raise RuntimeError(f"fscan_synth_pairs_host failed ({rc})")
+    return f, g, mf, mg, truth
+
+
+# (n, grid delta [m], n_theta, t_theta = t_xy or None for the defaults, batch) of
+# BASELINE.json configs 1..5 (SURVEY.md Appendix A)
+BASELINE = {1: (256, 0.5, 360, None, 1), 2: (256, 0.5, 360, 1.0, 64), 3: (512, 0.25, 720, 1.0, 64),
+            4: (512, 0.25, 720, 1.0, 4096), 5: (1024, 0.125, 1440, 0.5, 1024)}
+
+
+def baseline_config(cid: int) -> tuple[FoConfig, float, int]:
+    """(finalized FoConfig, grid delta, batch) of BASELINE config `cid` (delta_theta =
+    pi / n_theta, n_radius / pad_angle resolved by finalize, matcher.cpp:11-15)."""
+    n, delta, nt, t, batch = BASELINE[cid]
+    kw = dict(n_theta=nt, delta_theta=np.pi / nt, n_xy=n, delta_xy=delta, n_radius=0, pad_angle=-1)
+    if t is not None:
+        kw.update(t_theta=t, t_xy=t)
+    return finalize(make_config(**kw)), delta, batch
+
+
+def host_descriptor() -> dict:
+    """CPU model + logical core count (the reference's host_descriptor, bench.cpp:84-105)."""
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "logical_cores": os.cpu_count() or 1}

@@ -20,8 +20,14 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-# FSCAN_LIB: load an alternative build of the same library (A/B kernel timing)
-LIB_PATH = os.environ.get("FSCAN_LIB") or os.path.join(HERE, "libfscan_b200.so")
+# FSCAN_LIB: load an alternative build of the same library for A/B kernel timing;
+# only builds under <repo>/ab/ (tools/ab_build.sh) are accepted, and bench.py
+# records the path it loaded
+_AB_DIR = os.path.join(ROOT, "ab") + os.sep
+_ENV_LIB = os.environ.get("FSCAN_LIB")
+if _ENV_LIB and not os.path.abspath(_ENV_LIB).startswith(_AB_DIR):
+    raise RuntimeError(f"FSCAN_LIB must point at an A/B build under {_AB_DIR} (got {_ENV_LIB})")
+LIB_PATH = os.path.abspath(_ENV_LIB) if _ENV_LIB else os.path.join(HERE, "libfscan_b200.so")
 
 OK, ERR_INVALID_ARGUMENT, ERR_NONFINITE, ERR_MASK_RANGE, ERR_UNSUPPORTED, ERR_CUDA, ERR_NO_DEVICE, ERR_IO = range(8)
 _STATUS = {0: "OK", 1: "INVALID_ARGUMENT", 2: "NONFINITE", 3: "MASK_RANGE", 4: "UNSUPPORTED",
@@ -129,6 +135,7 @@ SYMBOLS = {
                                             C.c_double, _P, _P]),
     "fscan_check_results": (C.c_int, [_P, C.c_int, _P, C.POINTER(C.c_int)]),
     "fscan_ctx_launches_last": (C.c_int, [_P]),
+    "fscan_ctx_rot_columns": (C.c_int, [_P]),
     "fscan_ctx_set_profiling": (C.c_int, [_P, C.c_int]),
     "fscan_ctx_set_graphs": (C.c_int, [_P, C.c_int]),
     "fscan_ctx_graph_stats": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
@@ -257,6 +264,26 @@ def _as_tensor(x):
     return x
 
 
+def _check_tensor(t, name: str, shape: tuple, dtype: str = "float32"):
+    """Reject a CUDA input/output the kernels would read or write out of bounds:
+    wrong dtype, wrong shape, or (outputs given as raw bytes) too few bytes."""
+    if t is None:
+        return
+    if str(t.dtype).replace("torch.", "") != dtype:
+        raise ValueError(f"{name}: expected dtype {dtype}, got {t.dtype}")
+    if tuple(int(x) for x in t.shape) != tuple(shape):
+        raise ValueError(f"{name}: expected shape {tuple(shape)}, got {tuple(t.shape)}")
+
+
+def _check_bytes(t, name: str, nbytes: int):
+    """An output buffer must hold at least nbytes (any dtype, contiguous)."""
+    if t is None:
+        return
+    have = t.numel() * t.element_size()
+    if have < nbytes:
+        raise ValueError(f"{name}: buffer holds {have} bytes, needs {nbytes}")
+
+
 def _stream_ptr(stream) -> int | None:
     if stream is None:
         import torch
@@ -305,6 +332,11 @@ class Matcher:
     def launches_last(self) -> int:
         return lib().fscan_ctx_launches_last(self._h)
 
+    @property
+    def rot_columns(self) -> int:
+        """Spectrum columns u < W the rotation stage keeps (fscan_ctx_rot_columns)."""
+        return lib().fscan_ctx_rot_columns(self._h)
+
     KERNELS = ("rot_rows", "rot_cols", "rot_polar", "theta_in", "xlat_rows", "xlat_cols", "xlat_out",
                "finalize", "rot_gather", "polar_to_cart", "mag_unpack", "bf_items", "bf_final")
 
@@ -343,21 +375,48 @@ class Matcher:
         f, g, mf, mg = _as_tensor(f), _as_tensor(g), _as_tensor(mf), _as_tensor(mg)
         import torch
         b = int(f.shape[0])
+        self._check_pairs(b, f=f, g=g, mf=mf, mg=mg)
         if out is None:
             out = torch.empty(b * RESULT_DTYPE.itemsize, dtype=torch.uint8, device=f.device)
+        self._check_outputs(b, out, theta_surface, xy_surface)
         st = lib().fscan_match_batch(self._h, _ptr(f), _ptr(g), _ptr(mf), _ptr(mg), b, float(delta),
                                      _ptr(out), _ptr(theta_surface), _ptr(xy_surface), _stream_ptr(stream))
         self._check(st, "fscan_match_batch")
         return out
+
+    def _check_pairs(self, b: int, **grids):
+        """Every grid [b, n, n] float32 (masks both or neither; the reference
+        throws 'grid specs differ' for mismatched grids)."""
+        if b > self.max_batch:
+            raise ValueError(f"batch {b} exceeds the context's max_batch {self.max_batch}")
+        if ("mf" in grids) and ((grids["mf"] is None) != (grids.get("mg") is None)):
+            raise ValueError("masks: pass both mf and mg, or neither")
+        for name, t in grids.items():
+            _check_tensor(t, name, (b, self.n, self.n))
+
+    def _check_outputs(self, b: int, out, theta_surface=None, xy_surface=None):
+        _check_bytes(out, "out", b * RESULT_DTYPE.itemsize)
+        if theta_surface is not None:
+            if str(theta_surface.dtype) != "torch.float64":
+                raise ValueError(f"theta_surface: expected dtype float64, got {theta_surface.dtype}")
+            _check_bytes(theta_surface, "theta_surface", b * max(1, self.cfg.n_theta) * 8)
+        if xy_surface is not None:
+            _check_tensor(xy_surface, "xy_surface", (b, self.n, self.n))
 
     def match_polar(self, pf, pg, mf=None, mg=None, *, range_res: float, delta: float, out=None,
                     theta_surface=None, xy_surface=None, stream=None):
         """Config-3 path: raw polar sweeps [B, n_az, n_range] (CUDA tensors) -> K0 -> match."""
         pf, pg, mf, mg = _as_tensor(pf), _as_tensor(pg), _as_tensor(mf), _as_tensor(mg)
         import torch
+        if pf.dim() != 3:
+            raise ValueError("pf: expected [B, n_az, n_range]")
         b, n_az, n_range = (int(x) for x in pf.shape)
+        _check_tensor(pf, "pf", (b, n_az, n_range))
+        _check_tensor(pg, "pg", (b, n_az, n_range))
+        self._check_pairs(b, mf=mf, mg=mg)
         if out is None:
             out = torch.empty(b * RESULT_DTYPE.itemsize, dtype=torch.uint8, device=pf.device)
+        self._check_outputs(b, out, theta_surface, xy_surface)
         st = lib().fscan_match_batch_polar(self._h, _ptr(pf), _ptr(pg), n_az, n_range, float(range_res), _ptr(mf),
                                            _ptr(mg), b, float(delta), _ptr(out), _ptr(theta_surface),
                                            _ptr(xy_surface), _stream_ptr(stream))
@@ -369,6 +428,13 @@ class Matcher:
         """Synchronous batched scan_match on host float32 arrays [B, N, N]."""
         f = np.ascontiguousarray(f, dtype=np.float32)
         g = np.ascontiguousarray(g, dtype=np.float32)
+        if f.shape != g.shape or f.ndim not in (2, 3) or f.shape[-1] != self.n or f.shape[-2] != self.n:
+            _raise(ERR_INVALID_ARGUMENT, "scan_match: grid specs differ")
+        for m in (mf, mg):
+            if m is not None and np.shape(m) != f.shape:
+                _raise(ERR_INVALID_ARGUMENT, "MaskGrid: shape mismatch")
+        if (mf is None) != (mg is None):
+            _raise(ERR_INVALID_ARGUMENT, "masks: pass both mask_f and mask_g, or neither")
         if f.ndim == 2:
             f, g = f[None], g[None]
             mf = None if mf is None else np.ascontiguousarray(mf, dtype=np.float32)[None]
@@ -376,6 +442,8 @@ class Matcher:
         mf = None if mf is None else np.ascontiguousarray(mf, dtype=np.float32)
         mg = None if mg is None else np.ascontiguousarray(mg, dtype=np.float32)
         b, n = f.shape[0], f.shape[1]
+        if b > self.max_batch:
+            _raise(ERR_INVALID_ARGUMENT, f"batch {b} exceeds the context's max_batch {self.max_batch}")
         res = np.zeros(b, dtype=RESULT_DTYPE)
         ts = np.zeros((b, max(1, self.cfg.n_theta)), dtype=np.float64) if surfaces else None
         xs = np.zeros((b, n, n), dtype=np.float32) if surfaces else None
@@ -389,8 +457,11 @@ class Matcher:
         f, g = _as_tensor(f), _as_tensor(g)
         import torch
         b = int(f.shape[0])
+        self._check_pairs(b, f=f, g=g)
         if theta is None:
             theta = torch.empty(b, dtype=torch.float64, device=f.device)
+        _check_tensor(theta, "theta", (b,), "float64")
+        _check_bytes(theta_surface, "theta_surface", b * max(1, self.cfg.n_theta) * 8)
         st = lib().fscan_estimate_rotation_batch(self._h, _ptr(f), _ptr(g), b, _ptr(theta), _ptr(theta_surface),
                                                  _stream_ptr(stream))
         self._check(st, "fscan_estimate_rotation_batch")
@@ -400,6 +471,10 @@ class Matcher:
         f, g, theta = _as_tensor(f), _as_tensor(g), _as_tensor(theta)
         import torch
         b = int(f.shape[0])
+        self._check_pairs(b, f=f, g=g)
+        _check_tensor(theta, "theta", (b,), "float64")
+        if xy_surface is not None:
+            _check_tensor(xy_surface, "xy_surface", (b, self.n, self.n))
         txy = torch.empty((b, 2), dtype=torch.float64, device=f.device)
         st = lib().fscan_estimate_translation_batch(self._h, _ptr(f), _ptr(g), b, float(delta), _ptr(theta),
                                                     _ptr(txy), _ptr(xy_surface), _stream_ptr(stream))
@@ -413,8 +488,13 @@ class Matcher:
         scans, masks = _as_tensor(scans), _as_tensor(masks)
         import torch
         s = int(scans.shape[0])
+        _check_tensor(scans, "scans", (s, self.n, self.n))
+        _check_tensor(masks, "masks", (s, self.n, self.n))
+        if s - 1 > self.max_batch:
+            raise ValueError(f"{s - 1} pairs exceed the context's max_batch {self.max_batch}")
         if out is None:
             out = torch.empty(max(s - 1, 0) * RESULT_DTYPE.itemsize, dtype=torch.uint8, device=scans.device)
+        self._check_outputs(max(s - 1, 0), out, theta_surface, xy_surface)
         st = lib().fscan_odometry_batch(self._h, _ptr(scans), _ptr(masks), s, float(delta), _ptr(out),
                                         _ptr(theta_surface), _ptr(xy_surface), _stream_ptr(stream))
         self._check(st, "fscan_odometry_batch")
@@ -427,9 +507,11 @@ class Matcher:
         f, g = _as_tensor(f), _as_tensor(g)
         import torch
         b = int(f.shape[0])
+        self._check_pairs(b, f=f, g=g)
         th = np.ascontiguousarray(np.asarray(thetas, dtype=np.float64).ravel())
         if out is None:
             out = torch.empty(b * BF_DTYPE.itemsize, dtype=torch.uint8, device=f.device)
+        _check_bytes(out, "out", b * BF_DTYPE.itemsize)
         st = lib().fscan_brute_force_batch(self._h, _ptr(f), _ptr(g), b, th.ctypes.data, int(th.size),
                                            float(delta), _ptr(out), _stream_ptr(stream))
         self._check(st, "fscan_brute_force_batch")
@@ -439,6 +521,7 @@ class Matcher:
         img = _as_tensor(img)
         import torch
         b, n = int(img.shape[0]), int(img.shape[1])
+        self._check_pairs(b, img=img)
         out = torch.empty((b, n, n - n // 2), dtype=torch.float32, device=img.device)  # u >= 0 half plane
         st = lib().fscan_band_magnitude_batch(self._h, _ptr(img), b, _ptr(out), _stream_ptr(stream))
         self._check(st, "fscan_band_magnitude_batch")
@@ -498,6 +581,13 @@ def scan_match(f, g, delta: float, config: MatchConfig | None = None, mask_f=Non
     Without a config, the stock config with the grid geometry swapped in.
     """
     f = np.asarray(f)
+    if f.ndim != 2 or f.shape[0] != f.shape[1]:
+        _raise(ERR_INVALID_ARGUMENT, "ScanGrid: expected a square n x n grid")
+    if np.shape(g) != f.shape:
+        _raise(ERR_INVALID_ARGUMENT, "scan_match: grid specs differ")
+    for m in (mask_f, mask_g):
+        if m is not None and np.shape(m) != f.shape:
+            _raise(ERR_INVALID_ARGUMENT, "MaskGrid: shape mismatch")
     n = int(f.shape[0])
     if config is None:
         config = MatchConfig(n_xy=n, delta_xy=delta, n_radius=0)

@@ -75,6 +75,8 @@ struct fscan_ctx {
     double* bf_thetas = nullptr;
     int bf_theta_cap = 0;
     Partial* bf_items = nullptr;
+    cudaEvent_t bf_done = nullptr;  // recorded after the last exhaustive search's final kernel
+    bool bf_done_valid = false;
     int bf_item_cap = 0;
     int launches_last = 0;
     std::string err;
@@ -748,6 +750,10 @@ fscan_status fscan_ctx_create(int device, const fscan_config* cfg_in, int max_ba
 void fscan_ctx_destroy(fscan_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
+    // work queued on user streams (graph replays, the exhaustive search's final
+    // kernel) reads the workspace freed below
+    if (ctx->graph_launched) cudaEventSynchronize(ctx->graph_ev);
+    if (ctx->bf_done_valid) cudaEventSynchronize(ctx->bf_done);
     for (Lane& l : LaneRange{ctx}) {
         if (l.stream) cudaStreamSynchronize(l.stream);
         free_lane(l);
@@ -774,6 +780,7 @@ void fscan_ctx_destroy(fscan_ctx* ctx) {
     cudaFree(ctx->bs_kern);
     cudaFree(ctx->bf_thetas);
     cudaFree(ctx->bf_items);
+    if (ctx->bf_done) cudaEventDestroy(ctx->bf_done);
     delete ctx;
 }
 
@@ -783,12 +790,18 @@ int fscan_ctx_n(const fscan_ctx* ctx) { return ctx ? ctx->n : 0; }
 
 int fscan_ctx_launches_last(const fscan_ctx* ctx) { return ctx ? ctx->launches_last : 0; }
 
+int fscan_ctx_rot_columns(const fscan_ctx* ctx) { return ctx ? 8 * ctx->rot_col_blocks : 0; }
+
 fscan_status fscan_ctx_set_chunk(fscan_ctx* ctx, int pairs) {
     if (!ctx || pairs < 0) return FSCAN_ERR_INVALID_ARGUMENT;
     std::lock_guard<std::mutex> g(ctx->mu);
     if (pairs == 0) pairs = ctx->alloc_chunk;
+    // cached graphs bake in the chunking and the lane workspace pointers
+    if (pairs != ctx->chunk || pairs > ctx->alloc_chunk) drop_graphs(ctx);
     if (pairs > ctx->alloc_chunk) {
         cudaSetDevice(ctx->device);
+        // a graph replay on a user stream may still be using the workspace
+        if (ctx->graph_launched) cudaEventSynchronize(ctx->graph_ev);
         for (Lane& l : LaneRange{ctx}) {
             cudaStreamSynchronize(l.stream);
             const bool had_host = l.in != nullptr;
@@ -952,7 +965,10 @@ fscan_status fscan_brute_force_batch(fscan_ctx* ctx, const float* d_f, const flo
         CK(cudaMalloc(&ctx->bf_items, sizeof(Partial) * items));
         ctx->bf_item_cap = items;
     }
-    // the candidate list is small: a synchronous copy keeps the host array's lifetime simple
+    // the candidate list is small: a synchronous copy keeps the host array's lifetime
+    // simple; the previous call's kernels (on whatever stream it was given) must be
+    // done with bf_thetas / bf_items before they are overwritten
+    if (ctx->bf_done_valid) CK(cudaEventSynchronize(ctx->bf_done));
     CK(cudaStreamSynchronize(user));
     CK(cudaMemcpy(ctx->bf_thetas, thetas, sizeof(double) * nth, cudaMemcpyHostToDevice));
     // grids that are not powers of two: zero-embed f and g once per call (§3.9)
@@ -998,6 +1014,9 @@ fscan_status fscan_brute_force_batch(fscan_ctx* ctx, const float* d_f, const flo
     const int off = (ctx->np / 2 - 1) - (ctx->n - 1) / 2;
     CK(launch_bf_final(ctx->bf_items, ctx->bf_thetas, nth, batch, ctx->n, ctx->np, off, delta, d_out, user));
     ++ctx->launches_last;
+    if (!ctx->bf_done) CK(cudaEventCreateWithFlags(&ctx->bf_done, cudaEventDisableTiming));
+    CK(cudaEventRecord(ctx->bf_done, user));
+    ctx->bf_done_valid = true;
     if (ef) {
         CK(cudaStreamSynchronize(user));  // the embedded copies are read by the launched kernels
         cudaFree(ef);
@@ -1100,6 +1119,11 @@ fscan_status fscan_match_batch_host(fscan_ctx* ctx, const float* f, const float*
         fscan_status a = alloc_host_staging(ctx, l, ctx->alloc_chunk);
         if (a != FSCAN_OK) return a;
     }
+    // a graph replay of fscan_match_batch / fscan_odometry_batch on a user stream
+    // may still be using the lane workspace: order the lanes after it
+    if (ctx->graph_launched)
+        for (Lane& l : LaneRange{ctx}) CK(cudaStreamWaitEvent(l.stream, ctx->graph_ev, 0));
+    ctx->lanes_since_graph = true;
     ctx->launches_last = 0;
     int li = 0;
     // lane-alternating chunks: H2D(i+1) overlaps compute(i) on the other lane

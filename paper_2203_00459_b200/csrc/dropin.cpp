@@ -18,6 +18,7 @@
 #include <optional>
 #include <cstdio>
 #include <cstring>
+#include <list>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -96,7 +97,7 @@ Pose2D parse_pose_csv(const std::string& line) {
 namespace {
 
 fscan_config to_c(const MatchConfig& m) {
-    fscan_config c;
+    fscan_config c{};
     c.n_theta = m.n_theta;
     c.delta_theta = m.delta_theta;
     c.t_theta = m.t_theta;
@@ -131,21 +132,42 @@ struct CtxDeleter {
 };
 
 // One context per (device, config, batch capacity), cached per thread: the
-// reference API is re-entrant and callers fan out over threads.
+// reference API is re-entrant and callers fan out over threads. The key is
+// built from the named config fields (no struct padding bytes); capacities are
+// rounded up to a power of two so nearby batch sizes share a context, and each
+// thread keeps at most kCtxCache contexts (least recently used evicted).
+constexpr std::size_t kCtxCache = 4;
+
+std::string config_key(const fscan_config& c, int device, int cap) {
+    char buf[512];
+    std::snprintf(buf, sizeof buf, "%d|%a|%a|%d|%a|%a|%a|%a|%d|%d|%d|%d|dev%d|cap%d", c.n_theta, c.delta_theta,
+                  c.t_theta, c.n_xy, c.delta_xy, c.t_xy, c.band_lo, c.band_hi, c.n_radius, c.pad_angle,
+                  c.softargmax_window, c.normalize_scores, device, cap);
+    return buf;
+}
+
 fscan_ctx* context_for(const MatchConfig& cfg, int device, int batch) {
-    thread_local std::map<std::string, std::unique_ptr<fscan_ctx, CtxDeleter>> cache;
+    struct Entry {
+        std::string key;
+        std::unique_ptr<fscan_ctx, CtxDeleter> ctx;
+    };
+    thread_local std::list<Entry> cache;  // front = most recently used
     const fscan_config c = to_c(cfg);
-    std::string key(reinterpret_cast<const char*>(&c), sizeof c);
-    key += std::to_string(device) + ":" + std::to_string(batch);
-    auto it = cache.find(key);
-    if (it != cache.end()) return it->second.get();
+    int cap = 1;
+    while (cap < batch) cap <<= 1;
+    const std::string key = config_key(c, device, cap);
+    for (auto it = cache.begin(); it != cache.end(); ++it)
+        if (it->key == key) {
+            cache.splice(cache.begin(), cache, it);
+            return cache.front().ctx.get();
+        }
     fscan_ctx* ctx = nullptr;
-    const fscan_status st = fscan_ctx_create(device, &c, batch, &ctx);
+    const fscan_status st = fscan_ctx_create(device, &c, cap, &ctx);
     std::unique_ptr<fscan_ctx, CtxDeleter> own(ctx);
     if (st != FSCAN_OK) raise(st, std::string("fscan_ctx_create: ") + (ctx ? fscan_ctx_last_error(ctx) : ""));
-    fscan_ctx* raw = own.get();
-    cache.emplace(key, std::move(own));
-    return raw;
+    while (cache.size() >= kCtxCache) cache.pop_back();
+    cache.push_front(Entry{key, std::move(own)});
+    return cache.front().ctx.get();
 }
 
 template <typename T>

@@ -21,6 +21,8 @@ def gather_results(local, total: int, world: int, rank: int, group=None):
 
     if world == 1:
         return local
+    if dist.get_backend(group) == "gloo":  # gloo gathers host tensors only
+        local = local.cpu()
     counts = [shard_range(total, world, r)[1] for r in range(world)]
     width = max(counts)
     pad = torch.zeros((width,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)

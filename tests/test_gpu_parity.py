@@ -123,7 +123,9 @@ def test_scan_match_small_grids_and_odd_bin_counts(fb, orc, dev, n, nt):
                 r.xy_surface, spec.delta, stats)
 
 
-GOLDEN = sorted(glob.glob(os.path.join(ROOT, "tests", "golden", "*.npz")))
+GOLDEN = sorted(p for p in glob.glob(os.path.join(ROOT, "tests", "golden", "*.npz"))
+                if not os.path.basename(p).startswith("baseline_"))
+BASELINE_GOLDEN = sorted(glob.glob(os.path.join(ROOT, "tests", "golden", "baseline_*.npz")))
 CFG_KEYS = ("n_theta", "delta_theta", "t_theta", "n_xy", "delta_xy", "t_xy", "band_lo", "band_hi", "n_radius",
             "pad_angle", "softargmax_window", "normalize_scores")
 
@@ -147,6 +149,75 @@ def test_golden_vectors_from_the_reference(fb, dev, path):
                                    [z["diag"][i][0], z["diag"][i][2], z["diag"][i][3]], atol=1e-9)
         assert abs(res[i]["theta_peak"] - z["diag"][i][1]) <= SURF_TOL * abs(z["diag"][i][1])
         assert abs(res[i]["xy_peak"] - z["diag"][i][4]) <= SURF_TOL * abs(z["diag"][i][4])
+
+
+def golden_match_config(fb, z):
+    vals = dict(zip(CFG_KEYS, z["cfg"]))
+    ints = ("n_theta", "n_xy", "n_radius", "pad_angle", "softargmax_window")
+    return fb.MatchConfig(**{k: (int(v) if k in ints else (bool(v) if k == "normalize_scores" else float(v)))
+                             for k, v in vals.items()})
+
+
+@pytest.mark.parametrize("path", BASELINE_GOLDEN, ids=[os.path.basename(p) for p in BASELINE_GOLDEN])
+def test_baseline_size_golden_from_the_reference(fb, dev, path):
+    """BASELINE configs 2/4/5 at full size (N = 256 / 512 / 1024) against the
+    reference's own scan_match outputs (tests/golden/make_golden.py --baseline;
+    inputs regenerated by the seeded generator and pinned by SHA-256): integer
+    bins bit-exact (or a documented near-tie), theta surface and the xy surface
+    window around the peak within 1e-4 of max|ref|, poses within 1e-3 rad / 1e-2 px."""
+    import hashlib
+    z = np.load(path)
+    cfg = golden_match_config(fb, z)
+    delta = float(z["delta"])
+    spec = fb.synth_spec(int(z["config_id"]))
+    pairs = [int(p) for p in z["pairs"]]
+    ins = [fb.synth_pairs_host(spec, p, 1) for p in pairs]
+    f = np.concatenate([x[0] for x in ins])
+    g = np.concatenate([x[1] for x in ins])
+    mf = np.concatenate([x[2] for x in ins]) if int(z["masks"]) else None
+    mg = np.concatenate([x[3] for x in ins]) if int(z["masks"]) else None
+    for i in range(len(pairs)):
+        h = hashlib.sha256()
+        for a in (f[i], g[i]) + ((mf[i], mg[i]) if mf is not None else ()):
+            h.update(np.ascontiguousarray(a, dtype=np.float32).tobytes())
+        assert h.hexdigest() == str(z["input_sha256"][i]), "generator output changed: regenerate the fixture"
+    res, ts, xs = run_gpu(fb, dev, cfg, delta, f, g, mf, mg)
+    w = int(z["win"])
+    near = 0
+    for i in range(len(pairs)):
+        tb, tr, tc = (int(x) for x in z["bins"][i])
+        ref_ts = z["theta_surface"][i]
+        tsd = np.abs(ts[i] - ref_ts).max() / np.abs(ref_ts).max()
+        assert tsd <= SURF_TOL, tsd
+        # the xy window around the reference peak (zero-padded at the borders)
+        xp = np.pad(xs[i].astype(np.float64), w)
+        win = xp[tr:tr + 2 * w + 1, tc:tc + 2 * w + 1]
+        xsd = np.abs(win - z["xy_window"][i]).max() / z["xy_absmax"][i]
+        assert xsd <= SURF_TOL, xsd
+        assert abs(np.abs(xs[i]).max() - z["xy_absmax"][i]) <= SURF_TOL * z["xy_absmax"][i]
+        r = res[i]
+        assert r["status"] == 0
+        is_near = False
+        if r["theta_bin"] != tb:
+            gap = (ref_ts[tb] - ref_ts[r["theta_bin"]]) / np.abs(ref_ts).max()
+            assert gap < 4 * tsd + 1e-12, (pairs[i], "theta bin", r["theta_bin"], tb, gap)
+            is_near = True
+        if (r["xy_row"], r["xy_col"]) != (tr, tc):
+            dr, dc = r["xy_row"] - tr + w, r["xy_col"] - tc + w
+            assert 0 <= dr <= 2 * w and 0 <= dc <= 2 * w, (pairs[i], "xy cell far from the reference peak")
+            gap = (z["xy_window"][i][w, w] - z["xy_window"][i][dr, dc]) / z["xy_absmax"][i]
+            assert is_near or gap < 4 * xsd + 1e-12, (pairs[i], "xy cell", gap)
+            is_near = True
+        near += is_near
+        if not is_near:
+            assert abs(r["theta"] - z["pose"][i][0]) <= THETA_TOL
+            assert abs(r["tx"] - z["pose"][i][1]) <= PX_TOL * delta
+            assert abs(r["ty"] - z["pose"][i][2]) <= PX_TOL * delta
+            np.testing.assert_allclose([r["theta_hard"], r["xy_hard_x"], r["xy_hard_y"]],
+                                       [z["diag"][i][0], z["diag"][i][2], z["diag"][i][3]], atol=1e-9)
+            assert abs(r["theta_peak"] - z["diag"][i][1]) <= SURF_TOL * abs(z["diag"][i][1])
+            assert abs(r["xy_peak"] - z["diag"][i][4]) <= SURF_TOL * abs(z["diag"][i][4])
+    assert near <= max(1, len(pairs) // 8)
 
 
 # ---------------------------------------------------------------- config 3: raw polar sweeps (K0)
@@ -824,5 +895,101 @@ def test_batch_edge_sizes(fb, dev):
     b = fb.decode_results(m.match_device(F, G, MF, MG, delta=delta))
     assert (a["theta_bin"] == b["theta_bin"]).all() and (a["xy_row"] == b["xy_row"]).all()
     np.testing.assert_array_equal(a["theta"], b["theta"])
-    with pytest.raises(fb.FscanError):
+    with pytest.raises(ValueError, match="max_batch"):  # caught by the binding before the C ABI
         fb.Matcher(cfg, max_batch=3).match_device(F, G, MF, MG, delta=delta)  # batch > max_batch
+    m3 = fb.Matcher(cfg, max_batch=3)
+    st = fb.lib().fscan_match_batch(m3._h, F.data_ptr(), G.data_ptr(), MF.data_ptr(), MG.data_ptr(), 7, delta,
+                                    torch.empty(7 * 80, dtype=torch.uint8, device=dev).data_ptr(), None, None, None)
+    assert st == fb.ERR_INVALID_ARGUMENT  # ... and by the C ABI itself
+
+
+def test_set_chunk_drops_cached_graphs(fb, dev):
+    """fscan_ctx_set_chunk reallocates the lane workspace; a graph
+    captured before it must not be replayed into the freed buffers."""
+    cfg, delta, _ = fb.baseline_config(2)
+    f, g, mf, mg, _ = fb.synth_pairs_host(fb.synth_spec(2), 0, 6)
+    F, G, MF, MG = to_dev(dev, f, g, mf, mg)
+    m = fb.Matcher(cfg, max_batch=6, chunk=2)
+    direct = m.match_device(F, G, MF, MG, delta=delta).clone()
+    torch.cuda.synchronize()
+    m.set_graphs(True)
+    out = torch.zeros_like(direct)
+    m.match_device(F, G, MF, MG, delta=delta, out=out)
+    torch.cuda.synchronize()
+    caps = m.graph_stats()[0]
+    for chunk in (6, 3, 1):  # grow (reallocates), then shrink (re-chunks)
+        m.set_chunk(chunk)
+        out.zero_()
+        m.match_device(F, G, MF, MG, delta=delta, out=out)
+        torch.cuda.synchronize()
+        assert torch.equal(out, direct), chunk
+    assert m.graph_stats()[0] == caps + 3  # every new chunking was captured afresh
+
+
+def test_host_call_after_graph_replay_on_side_stream(fb, dev):
+    """fscan_match_batch_host must wait for a graph replay still
+    running on a user stream before reusing the lane workspace."""
+    cfg, delta, _ = fb.baseline_config(2)
+    f, g, mf, mg, _ = fb.synth_pairs_host(fb.synth_spec(2), 10, 4)
+    F, G, MF, MG = to_dev(dev, f, g, mf, mg)
+    m = fb.Matcher(cfg, max_batch=4, chunk=2)
+    ref = fb.decode_results(m.match_device(F, G, MF, MG, delta=delta))
+    m.set_graphs(True)
+    s = torch.cuda.Stream()
+    outs = []
+    for _ in range(3):
+        with torch.cuda.stream(s):
+            outs.append(m.match_device(F, G, MF, MG, delta=delta, stream=s))
+        host = m.match_host(f, g, mf, mg, delta=delta)  # queued while the replay may run
+        assert np.array_equal(host["theta_bin"], ref["theta_bin"])
+        assert np.array_equal(host["xy_row"], ref["xy_row"]) and np.array_equal(host["xy_col"], ref["xy_col"])
+    s.synchronize()
+    for o in outs:
+        r = fb.decode_results(o)
+        assert np.array_equal(r["theta_bin"], ref["theta_bin"]) and np.array_equal(r["xy_col"], ref["xy_col"])
+
+
+def test_python_entry_points_validate_buffers(fb, dev):
+    """dtype / shape / size errors are raised before any kernel
+    could read or write out of bounds."""
+    cfg, delta, _ = fb.baseline_config(2)
+    n = cfg.n_xy
+    m = fb.Matcher(cfg, max_batch=2)
+    F = torch.zeros((2, n, n), dtype=torch.float32, device=dev)
+    with pytest.raises(ValueError, match="dtype"):
+        m.match_device(F.double(), F, delta=delta)
+    with pytest.raises(ValueError, match="shape"):
+        m.match_device(F, torch.zeros((2, n, n - 1), dtype=torch.float32, device=dev), delta=delta)
+    with pytest.raises(ValueError, match="shape"):
+        m.match_device(F, F, F[:1], F[:1], delta=delta)
+    with pytest.raises(ValueError, match="both"):
+        m.match_device(F, F, F, None, delta=delta)
+    with pytest.raises(ValueError, match="bytes"):
+        m.match_device(F, F, delta=delta, out=torch.empty(10, dtype=torch.uint8, device=dev))
+    with pytest.raises(ValueError, match="bytes"):
+        m.match_device(F, F, delta=delta, theta_surface=torch.empty(3, dtype=torch.float64, device=dev))
+    with pytest.raises(ValueError, match="max_batch"):
+        m.match_device(torch.zeros((3, n, n), device=dev), torch.zeros((3, n, n), device=dev), delta=delta)
+    with pytest.raises(fb.FscanInvalidArgument, match="grid specs differ"):
+        m.match_host(np.zeros((n, n)), np.zeros((n, n - 2)), delta=delta)
+    with pytest.raises(fb.FscanInvalidArgument, match="grid specs differ"):
+        fb.scan_match(np.zeros((n, n)), np.zeros((n - 2, n - 2)), delta)
+
+
+def test_brute_force_calls_on_two_streams(fb, dev):
+    """back-to-back exhaustive searches on different streams do not
+    overwrite each other's candidate list / item scores."""
+    cfg, delta, _ = fb.baseline_config(2)
+    f, g, _, _, _ = fb.synth_pairs_host(fb.synth_spec(2), 3, 2)
+    F, G = to_dev(dev, f, g)
+    m = fb.Matcher(cfg, max_batch=2)
+    th_a = np.linspace(-0.05, 0.05, 33)
+    th_b = np.linspace(-0.2, 0.2, 7)
+    ref_a = fb.decode_bf_results(m.brute_force(F, G, th_a, delta=delta))
+    ref_b = fb.decode_bf_results(m.brute_force(F, G, th_b, delta=delta))
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    oa = m.brute_force(F, G, th_a, delta=delta, stream=s1)
+    ob = m.brute_force(F, G, th_b, delta=delta, stream=s2)
+    torch.cuda.synchronize()
+    assert np.array_equal(fb.decode_bf_results(oa), ref_a)
+    assert np.array_equal(fb.decode_bf_results(ob), ref_b)

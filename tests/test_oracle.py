@@ -12,7 +12,9 @@ import pytest
 
 from conftest import oracle_cfg
 
-GOLDEN = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz")))
+GOLDEN = sorted(p for p in glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz"))
+                if not os.path.basename(p).startswith("baseline_"))
+BASELINE_GOLDEN = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "baseline_*.npz")))
 CFG_KEYS = ("n_theta", "delta_theta", "t_theta", "n_xy", "delta_xy", "t_xy", "band_lo", "band_hi", "n_radius",
             "pad_angle", "softargmax_window", "normalize_scores")
 
@@ -305,3 +307,31 @@ def test_restatement_three_halves_padding_equals_reference_size(orc):
     b = orc.estimate_translation_ex(f, g, 0.1, cfg, 0.4, 3 * n // 2, False)
     assert np.abs(a[2] - b[2]).max() <= 1e-12 * np.abs(a[2]).max()
     assert abs(a[0] - b[0]) < 1e-12 and abs(a[1] - b[1]) < 1e-12
+
+
+@pytest.mark.parametrize("path", BASELINE_GOLDEN, ids=[os.path.basename(p) for p in BASELINE_GOLDEN])
+def test_restatement_matches_baseline_size_golden(orc, path):
+    """The fp64 restatement against the reference's own outputs at the BASELINE
+    sizes (N = 256 / 512 / 1024; tests/golden/make_golden.py --baseline). Inputs are
+    regenerated by the seeded generator (oracle/libsynth_gen.so) and pinned by the
+    fixture's SHA-256; the first two pairs of each fixture keep the CPU suite short
+    (the GPU test runs them all)."""
+    import hashlib
+    z = np.load(path)
+    cfg = golden_cfg(orc, z)
+    delta = float(z["delta"])
+    w = int(z["win"])
+    for i, p in enumerate(int(x) for x in z["pairs"][:2]):
+        f, g, mf, mg, _ = orc.synth_pairs_host(int(z["config_id"]), p, 1)
+        if not int(z["masks"]):
+            mf = mg = None
+        h = hashlib.sha256()
+        for a in (f[0], g[0]) + ((mf[0], mg[0]) if mf is not None else ()):
+            h.update(a.tobytes())
+        assert h.hexdigest() == str(z["input_sha256"][i])
+        r = orc.scan_match(f[0], g[0], cfg, delta, None if mf is None else mf[0], None if mg is None else mg[0])
+        np.testing.assert_array_equal([r.theta_bin, r.xy_row, r.xy_col], z["bins"][i])
+        np.testing.assert_allclose([r.theta, r.tx, r.ty], z["pose"][i], rtol=0, atol=1e-12)
+        np.testing.assert_allclose(r.theta_surface, z["theta_surface"][i], rtol=1e-12, atol=0)
+        win = np.pad(r.xy_surface, w)[r.xy_row:r.xy_row + 2 * w + 1, r.xy_col:r.xy_col + 2 * w + 1]
+        assert np.abs(win - z["xy_window"][i]).max() <= 1e-12 * z["xy_absmax"][i]

@@ -1,7 +1,9 @@
 """profiles/ncu_traffic.json from an ncu --set full capture of one C4 step:
 DRAM bytes (read + write) per launch and per pair for every pipeline kernel.
 Pairs per launch come from k_finalize's grid (one CTA per pair).
-usage: python tools/ncu_traffic.py REP SOURCE_NOTE > profiles/ncu_traffic.json"""
+Also records each kernel's issue-slot, warps-active and DRAM utilisation (what
+bench.py's roofline.ncu quotes).
+usage: python tools/ncu_traffic.py REP SOURCE_NOTE [PAIRS_PER_LAUNCH] > profiles/ncu_traffic.json"""
 import csv
 import io
 import json
@@ -28,10 +30,17 @@ recs = []
 for r in rows[2:]:
     k = r[hdr.index("Kernel Name")].split("(")[0].split("::")[-1]
     k = k.split("<")[0].replace("k_", "", 1)
+    pc = {m: col(r, c) for m, c in (("issue_pct", "smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                                     ("warps_active_pct", "sm__warps_active.avg.pct_of_peak_sustained_active"),
+                                     ("dram_pct", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"))}
     recs.append((k, col(r, "dram__bytes_read.sum") + col(r, "dram__bytes_write.sum"),
-                 col(r, "gpu__time_duration.sum"), col(r, "launch__grid_size")))
-ppl = next(int(g) for k, _, _, g in recs if k == "finalize")
-res = {"source": note, "pairs_per_launch": ppl}
-for k, b, us, _ in recs:
-    res[k] = {"dram_bytes_per_launch": b, "dram_bytes_per_pair": b / ppl, "duration_us": round(us, 3)}
+                 col(r, "gpu__time_duration.sum"), col(r, "launch__grid_size"), pc))
+if len(sys.argv) > 3:
+    ppl = int(sys.argv[3])
+else:
+    ppl = next(int(g) for k, _, _, g, _ in recs if k == "finalize")
+res = {"source": note, "pairs_per_launch": ppl, "n_xy": 512}
+for k, b, us, _, pc in recs:
+    res[k] = {"dram_bytes_per_launch": b, "dram_bytes_per_pair": b / ppl, "duration_us": round(us, 3),
+              **{m: round(v, 1) for m, v in pc.items()}}
 print(json.dumps(res, indent=1))
