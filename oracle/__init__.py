@@ -116,6 +116,11 @@ def lib(which: str = "oracle") -> C.CDLL:
             C.POINTER(C.c_float), C.POINTER(C.c_float), C.POINTER(C.c_float), C.POINTER(C.c_float),
             C.c_int, C.c_int, C.c_double, C.POINTER(FoConfig), C.c_int, C.POINTER(FoResult)]
         L.ref_scan_match_batch_f32.restype = C.c_int
+        L.ref_write_scan.argtypes = [C.c_char_p, C.POINTER(C.c_float), C.c_int, C.c_double, C.c_char_p, C.c_int]
+        L.ref_write_scan.restype = C.c_int
+        L.ref_read_scan.argtypes = [C.c_char_p, C.POINTER(C.c_float), C.c_int, C.POINTER(C.c_int),
+                                    C.POINTER(C.c_double), C.c_char_p, C.c_int]
+        L.ref_read_scan.restype = C.c_int
     _libs[which] = L
     return L
 
@@ -383,3 +388,21 @@ def host_descriptor() -> dict:
     except OSError:
         pass
     return {"cpu_model": model, "logical_cores": os.cpu_count() or 1}
+
+
+def ref_write_scan(path: str, grid, delta: float) -> None:
+    """The reference's own write_scan (io.cpp:82-100)."""
+    g = np.ascontiguousarray(grid, dtype=np.float32)
+    err = C.create_string_buffer(512)
+    if lib("ref").ref_write_scan(os.fsencode(path), _pf(g), int(g.shape[0]), float(delta), err, 512) != 0:
+        raise OracleError(err.value.decode())
+
+
+def ref_read_scan(path: str, n_max: int = 4096):
+    """The reference's own read_scan (io.cpp:102-131): (float32 grid, delta)."""
+    buf = np.empty(n_max * n_max, np.float32)
+    n, d = C.c_int(), C.c_double()
+    err = C.create_string_buffer(512)
+    if lib("ref").ref_read_scan(os.fsencode(path), _pf(buf), n_max, C.byref(n), C.byref(d), err, 512) != 0:
+        raise OracleError(err.value.decode())
+    return buf[: n.value * n.value].reshape(n.value, n.value).copy(), d.value

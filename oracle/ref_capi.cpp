@@ -12,6 +12,7 @@
 //   verify suites         proj/src/verify.cpp:73,115
 //   parallel_for          proj/src/parallel.cpp:24-45
 //   brute_force_match     proj/src/oracle.cpp:40-67
+//   write_scan/read_scan  proj/src/io.cpp:82-131 (.fscn files)
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -22,6 +23,7 @@
 
 #include "fscan/grid.hpp"
 #include "fscan/imageops.hpp"
+#include "fscan/io.hpp"
 #include "fscan/matcher.hpp"
 #include "fscan/oracle.hpp"
 #include "fscan/parallel.hpp"
@@ -249,6 +251,25 @@ int ref_scan_match_batch_f32(const float* f, const float* g, const float* mf, co
     for (int c : codes)
         if (c != 0) return c;
     return 0;
+}
+
+// .fscn writer / reader of the reference (io.cpp:82-131); values as float32
+int ref_write_scan(const char* path, const float* values, int n, double delta, char* err, int errlen) {
+    return guard(err, errlen, [&] {
+        Array2D a(n, n);
+        for (std::size_t i = 0; i < a.size(); ++i) a.data()[i] = values[i];
+        write_scan(path, ScanGrid(GridSpec{n, delta}, std::move(a)));
+    });
+}
+
+int ref_read_scan(const char* path, float* values, int n_max, int* n, double* delta, char* err, int errlen) {
+    return guard(err, errlen, [&] {
+        const ScanGrid s = read_scan(path);
+        *n = s.spec.n;
+        *delta = s.spec.delta;
+        if (s.spec.n > n_max) throw std::runtime_error("ref_read_scan: buffer too small");
+        for (std::size_t i = 0; i < s.values.size(); ++i) values[i] = static_cast<float>(s.values.data()[i]);
+    });
 }
 
 }  // extern "C"

@@ -22,6 +22,11 @@ namespace {
 
 constexpr double kPi = 3.141592653589793;  // std::numbers::pi (geometry.hpp:11)
 constexpr int kMaxLanes = 8;               // concurrent chunk pipelines (FSCAN_LANES, default 3)
+#ifdef FSCAN_NO_TEX_GATHER
+constexpr bool kNoTexGather = true;  // A/B: K3 gathers with plain loads
+#else
+constexpr bool kNoTexGather = false;
+#endif
 
 struct Lane {
     cudaStream_t stream = nullptr;
@@ -37,6 +42,7 @@ struct Lane {
     double* prof = nullptr;
     double* theta_ws = nullptr;
     int* flags = nullptr;
+    cudaTextureObject_t gtex = 0;  // K3 texture over gt (pow2 grids whose chunk fits one 2-D texture)
     // host-API staging
     float* in = nullptr;  // 4 grids x chunk
     float* cart = nullptr;  // K0 output (polar API): 2 grids x chunk
@@ -267,6 +273,7 @@ bool build_taps(int n, const fscan_config& cfg, const std::vector<unsigned char>
 }
 
 void free_lane(Lane& l) {
+    if (l.gtex) cudaDestroyTextureObject(l.gtex);
     cudaFree(l.ft);
     cudaFree(l.gt);
     cudaFree(l.zbuf);
@@ -307,6 +314,25 @@ fscan_status alloc_lane(fscan_ctx* ctx, Lane& l, int chunk) {
     CK(cudaMalloc(&l.prof, sizeof(double) * 2 * std::max(1, ctx->cfg.n_theta) * chunk));
     CK(cudaMalloc(&l.theta_ws, sizeof(double) * std::max(1, ctx->cfg.n_theta) * chunk));
     CK(cudaMalloc(&l.flags, sizeof(int) * (chunk + 2)));  // chain mode: one per scan
+    // K3 gathers g~ through a texture (tld4, zero border) when the chunk fits one
+    // pitch-2D texture (rows = chunk * np)
+    int max_h = 0;
+    CK(cudaDeviceGetAttribute(&max_h, cudaDevAttrMaxTexture2DLinearHeight, ctx->device));
+    if (np == n && !kNoTexGather && (long long)chunk * (long long)np <= max_h) {
+        cudaResourceDesc rd{};
+        rd.resType = cudaResourceTypePitch2D;
+        rd.res.pitch2D.devPtr = l.gt;
+        rd.res.pitch2D.desc = cudaCreateChannelDesc<float>();
+        rd.res.pitch2D.width = np;
+        rd.res.pitch2D.height = np * chunk;
+        rd.res.pitch2D.pitchInBytes = np * sizeof(float);
+        cudaTextureDesc td{};
+        td.addressMode[0] = td.addressMode[1] = cudaAddressModeBorder;  // taps off the grid read 0
+        td.filterMode = cudaFilterModePoint;
+        td.readMode = cudaReadModeElementType;
+        td.normalizedCoords = 0;
+        CK(cudaCreateTextureObject(&l.gtex, &rd, &td, nullptr));
+    }
     return FSCAN_OK;
 }
 
@@ -336,6 +362,8 @@ Params base_params(fscan_ctx* ctx, Lane& l, int batch, double delta) {
     p.batch = batch;
     p.ft = l.ft;
     p.gt = l.gt;
+    p.gtex = l.gtex;
+    p.gtex_base = l.gtex ? l.gt : nullptr;
     p.zbuf = l.zbuf;
     p.mag = l.mag;
     p.fgt = l.fgt;
@@ -735,6 +763,11 @@ fscan_status fscan_ctx_create(int device, const fscan_config* cfg_in, int max_ba
     if (max_batch >= 16 * ctx->nlanes) chunk = std::min(chunk, (max_batch + ctx->nlanes - 1) / ctx->nlanes);
     if (const char* e = std::getenv("FSCAN_CHUNK")) chunk = std::max(1, std::atoi(e));
     chunk = std::min(chunk, max_batch);
+    if (ctx->np == ctx->n && !kNoTexGather) {  // keep the chunk inside one K3 gather texture
+        int max_h = 0;
+        CK(cudaDeviceGetAttribute(&max_h, cudaDevAttrMaxTexture2DLinearHeight, device));
+        if (max_h >= ctx->np) chunk = std::min(chunk, max_h / ctx->np);
+    }
     ctx->chunk = chunk;
     ctx->alloc_chunk = chunk;
     CK(cudaEventCreateWithFlags(&ctx->start_ev, cudaEventDisableTiming));

@@ -29,6 +29,7 @@
 #include "fscan/matcher.hpp"
 #include "fscan/odometry.hpp"
 #include "fscan/oracle.hpp"
+#include "fscan/spectral.hpp"
 #include "fscan_cuda.h"
 
 namespace fscan {
@@ -218,6 +219,16 @@ CorrelationSurface xy_surface(const std::vector<float>& s, int n, double delta) 
 }
 
 }  // namespace
+
+int next_fast_size(int n) {  // spectral.cpp:155-163: strip the factors 2, 3, 5, 7
+    if (n < 1) return 1;
+    for (int cand = n;; ++cand) {
+        int rest = cand;
+        for (const int p : {2, 3, 5, 7})
+            while (rest % p == 0) rest /= p;
+        if (rest == 1) return cand;
+    }
+}
 
 void finalize(MatchConfig& cfg) {
     fscan_config c = to_c(cfg);

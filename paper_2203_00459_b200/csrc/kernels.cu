@@ -25,6 +25,7 @@
 #include "pipeline.h"
 #include "polar.h"
 
+
 namespace fscan_detail {
 
 using fscan_fft::cadd;
@@ -620,7 +621,10 @@ struct XRowGeom {
 // EMB: the scans are zero-embedded in the N x N (power-of-two) grid, valid
 // size p.n < N and rotation centre p.c0 (grid sides that are not powers of
 // two): g~r is zero outside the valid grid.
-template <int N, bool MANY, bool EMB>
+// TEX: the four taps of a cell come from ONE texture gather (tld4) on the lane's
+// g~ texture (pitch 2-D, rows pair * N + r, zero border for the columns; rows
+// outside the pair's grid are zeroed here), instead of four 32-bit loads.
+template <int N, bool MANY, bool EMB, bool TEX = false>
 __global__ void __launch_bounds__(kXThreads, 3) k_xlat_rows(Params p) {
     constexpr int K = N / 2, M = 3 * K, H = M / 2;
     using X = XRowGeom<N>;
@@ -671,12 +675,24 @@ __global__ void __launch_bounds__(kXThreads, 3) k_xlat_rows(Params p) {
             const int r0 = (int)r0f, cc0 = (int)cf;
             const bool r0in = live && (unsigned)r0 < (unsigned)N, r1in = live && (unsigned)(r0 + 1) < (unsigned)N;
             const bool c0in = (unsigned)cc0 < (unsigned)N, c1in = (unsigned)(cc0 + 1) < (unsigned)N;
-            const float* gp = gt + (r0 * N + cc0);  // 32-bit offset, one address per cell
             fv[u] = live ? ft[y * N + x] : 0.f;
-            tap[u][0] = (r0in && c0in) ? gp[0] : 0.f;
-            tap[u][1] = (r0in && c1in) ? gp[1] : 0.f;
-            tap[u][2] = (r1in && c0in) ? gp[N] : 0.f;
-            tap[u][3] = (r1in && c1in) ? gp[N + 1] : 0.f;
+            if constexpr (TEX) {
+                // texel (c, row) at coordinate (c + 1.0, row + 1.0): the gather's
+                // footprint starts at floor(coord - 0.5) = (cc0, r0); component
+                // order (c0, r1), (c1, r1), (c1, r0), (c0, r0)
+                const float4 g4 = tex2Dgather<float4>((cudaTextureObject_t)p.gtex, cf + 1.0f,
+                                                     (float)(pair * N + r0) + 1.0f, 0);
+                tap[u][0] = r0in ? g4.w : 0.f;
+                tap[u][1] = r0in ? g4.z : 0.f;
+                tap[u][2] = r1in ? g4.x : 0.f;
+                tap[u][3] = r1in ? g4.y : 0.f;
+            } else {
+                const float* gp = gt + (r0 * N + cc0);  // 32-bit offset, one address per cell
+                tap[u][0] = (r0in && c0in) ? gp[0] : 0.f;
+                tap[u][1] = (r0in && c1in) ? gp[1] : 0.f;
+                tap[u][2] = (r1in && c0in) ? gp[N] : 0.f;
+                tap[u][3] = (r1in && c1in) ? gp[N + 1] : 0.f;
+            }
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -740,6 +756,24 @@ __global__ void __launch_bounds__(kXThreads, 3) k_xlat_rows(Params p) {
 // stored by surface row i = half - ky (the flip of matcher.cpp:171-182)
 // through a shared-memory tile (a k'-major output written straight from the
 // registers measured slower: K4 grows to 120 registers and K5's loads scatter).
+// K4 twiddles W_M^{q n0} for n0 = t + m T (T = K/16, so W_M^T = W_48):
+// W_M^{q t} (one global-table read per thread) times W_48^{q m}, a
+// constant-bank table (two distinct q per warp: at most two addresses per
+// LDC). No W_M table is staged in shared memory (FSCAN_K4_TABLES restores the
+// staged M-entry table for A/B runs).
+__constant__ float kW48re[48] = {1.0f, 0.9914448857307434f, 0.9659258127212524f, 0.9238795042037964f, 0.8660253882408142f, 0.7933533191680908f, 0.7071067690849304f, 0.6087614297866821f, 0.5f, 0.3826834261417389f, 0.258819043636322f, 0.13052618503570557f, 0.0f, -0.13052618503570557f, -0.258819043636322f, -0.3826834261417389f, -0.5f, -0.6087614297866821f, -0.7071067690849304f, -0.7933533191680908f, -0.8660253882408142f, -0.9238795042037964f, -0.9659258127212524f, -0.9914448857307434f, -1.0f, -0.9914448857307434f, -0.9659258127212524f, -0.9238795042037964f, -0.8660253882408142f, -0.7933533191680908f, -0.7071067690849304f, -0.6087614297866821f, -0.5f, -0.3826834261417389f, -0.258819043636322f, -0.13052618503570557f, 0.0f, 0.13052618503570557f, 0.258819043636322f, 0.3826834261417389f, 0.5f, 0.6087614297866821f, 0.7071067690849304f, 0.7933533191680908f, 0.8660253882408142f, 0.9238795042037964f, 0.9659258127212524f, 0.9914448857307434f};
+__constant__ float kW48im[48] = {0.0f, -0.13052618503570557f, -0.258819043636322f, -0.3826834261417389f, -0.5f, -0.6087614297866821f, -0.7071067690849304f, -0.7933533191680908f, -0.8660253882408142f, -0.9238795042037964f, -0.9659258127212524f, -0.9914448857307434f, -1.0f, -0.9914448857307434f, -0.9659258127212524f, -0.9238795042037964f, -0.8660253882408142f, -0.7933533191680908f, -0.7071067690849304f, -0.6087614297866821f, -0.5f, -0.3826834261417389f, -0.258819043636322f, -0.13052618503570557f, 0.0f, 0.13052618503570557f, 0.258819043636322f, 0.3826834261417389f, 0.5f, 0.6087614297866821f, 0.7071067690849304f, 0.7933533191680908f, 0.8660253882408142f, 0.9238795042037964f, 0.9659258127212524f, 0.9914448857307434f, 1.0f, 0.9914448857307434f, 0.9659258127212524f, 0.9238795042037964f, 0.8660253882408142f, 0.7933533191680908f, 0.7071067690849304f, 0.6087614297866821f, 0.5f, 0.3826834261417389f, 0.258819043636322f, 0.13052618503570557f};
+
+__device__ __forceinline__ float2 w48(int k) { return make_float2(kW48re[k], kW48im[k]); }  // k < 48
+#ifdef FSCAN_K4_TABLES
+constexpr bool kK4W48 = false;
+#else
+constexpr bool kK4W48 = true;
+#endif
+#ifndef FSCAN_K4_MINB512
+#define FSCAN_K4_MINB512 3
+#endif
+
 template <int N>
 struct XColGeom {
     static constexpr int T = N / 32;
@@ -763,7 +797,7 @@ struct XColGeom {
     // N = 1024, W_M (3K; at 1024 it would push the CTA past half an SM's smem)
     // (the K-point FFTs read the span-16 stage's factors from a [r][k] table,
     // 240 entries, and, at K = 512 only, the last stage's from the linear W_K)
-    static constexpr bool SMEM_WM = N <= 512;
+    static constexpr bool SMEM_WM = N <= 512 && !kK4W48;
     static constexpr int TW_LIN = N / 2 > 256 ? N / 2 : 0;
     // W_M staged as two contiguous K-entry tables W_M^{n0}, W_M^{2 n0} below
     // N = 512 (conflict-free; at N = 256 ptxas also keeps K4 spill-free at four
@@ -773,7 +807,10 @@ struct XColGeom {
     static constexpr size_t SMEM = (WORK_FLOATS + TW_FLOATS) * sizeof(float);
     // explicit residency targets where ptxas' own choice leaves the SM
     // register-bound (N = 256: 4 CTAs of 192 threads; N = 1024: 3 of 192)
-    static constexpr int MIN_BLOCKS = N == 1024 ? 3 : (N == 256 ? 4 : 0);
+    // (N = 512 without the staged W_M table: 54 KB of shared memory, three CTAs
+    // per SM at <= 96 registers: C4 +2% over the staged table at 80; four CTAs
+    // at 80 registers run the kernel alone faster but the pipeline 1.5% slower)
+    static constexpr int MIN_BLOCKS = N == 1024 ? 3 : (N == 256 ? 4 : (kK4W48 ? FSCAN_K4_MINB512 : 0));
     // inputs loaded and folded once per (column, n0) site for all three q and
     // parked in shared memory (N = 1024: C5 +3%); below, every q group loads and
     // folds its own elements (the shared fold measured 1% slower at N = 512)
@@ -830,6 +867,14 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
         else if constexpr (X::SMEM_WM) return stw_m_s[qq * n0];
         else return __ldg(p.tw_m + qq * n0);
     };
+    // kK4W48: the thread's twiddle bases (see the W_48 table above)
+    const float2 bq = X::FOLD1 ? make_float2(1.f, 0.f) : __ldg(p.tw_m + q * t);  // W_M^{q t}
+    const float2 b1 = X::FOLD1 ? make_float2(1.f, 0.f) : __ldg(p.tw_m + t);      // W_M^{t}
+    const float2 b2 = X::FOLD1 ? make_float2(1.f, 0.f) : __ldg(p.tw_m + 2 * t);  // W_M^{2 t}
+    auto wq_m = [&](int m, int n0) {  // W_M^{q n0}, n0 = t + m T
+        if constexpr (kK4W48 && !X::FOLD1) return cmul(bq, w48(q * m));
+        else return wq(n0, q);
+    };
     __syncthreads();
     const fscan_fft::SmemTwRK twk{stw_rk, stw_k};
     const float2 w3q = w3(q);
@@ -880,7 +925,7 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
             const int n0 = t + m * T;
             const float4 u0 = src[n0], u1 = src[n0 + K];
             const float2 s = cadd(make_float2(u0.x, u0.y), cmul(w3q, make_float2(u1.x, u1.y)));
-            a[m] = q ? cmul(wq(n0, q), s) : s;
+            a[m] = q ? cmul(wq_m(m, n0), s) : s;
         }
     }
     fft_regs<K, -1, true>(a, t, bufA, twk);  // transforms of a warp share a buffer group
@@ -896,7 +941,7 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
             const int n0 = t + m * T;
             const float4 u0 = src[n0], u1 = src[n0 + K];
             const float2 s = cadd(make_float2(u0.z, u0.w), cmul(w3q, make_float2(u1.z, u1.w)));
-            a[m] = q ? cmul(wq(n0, q), s) : s;
+            a[m] = q ? cmul(wq_m(m, n0), s) : s;
         }
     }
     fft_regs<K, -1, true>(a, t, bufB, twk);
@@ -924,15 +969,28 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
         const int m = q + 3 * j;
         if (m < 16) {
             const int n0 = t + m * T;
+            float2 v1, v2;  // W_M^{n0}, W_M^{2 n0}
+            if constexpr (kK4W48 && !X::FOLD1) {
+                v1 = cmul(b1, w48(m));
+                v2 = cmul(b2, w48(2 * m));
+            } else {
+                v1 = wq(n0, 1);
+                v2 = wq(n0, 2);
+            }
             const float2 x0 = e0.get(n0);
-            const float2 x1 = cmul(cconj(wq(n0, 1)), e1.get(n0));
-            const float2 x2 = cmul(cconj(wq(n0, 2)), e2.get(n0));
+            const float2 x1 = cmul(cconj(v1), e1.get(n0));
+            const float2 x2 = cmul(cconj(v2), e2.get(n0));
             accp[j] = cadd(x0, cadd(x1, x2));
             accn[j] = cadd(x0, cadd(cmul(w31, x1), cmul(w32, x2)));
         }
     }
     __syncthreads();  // the buffers become the output tile
     float2* tile = reinterpret_cast<float2*>(smem);  // [N rows][PITCH]
+    // K4 -> K5 rows with a 64-byte aligned pitch: each CTA's column stripe is
+    // whole sectors per row
+    constexpr int RP = ypitch(N);
+    float2* dst = p.zbuf + (size_t)pair * N * RP;
+    const int ncols = min(COLS, H + 1 - (int)blockIdx.x * COLS);
 #pragma unroll
     for (int j = 0; j < 6; ++j) {
         const int m = q + 3 * j;
@@ -943,11 +1001,6 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
         }
     }
     __syncthreads();
-    // K4 -> K5 rows with a 64-byte aligned pitch: each CTA's 8-column stripe
-    // is two whole sectors per row
-    constexpr int RP = ypitch(N);
-    float2* dst = p.zbuf + (size_t)pair * N * RP;
-    const int ncols = min(COLS, H + 1 - (int)blockIdx.x * COLS);
     for (int o = threadIdx.x; o < N * COLS; o += blockDim.x) {
         const int i = o / COLS, cc = o % COLS;
         if (cc < ncols) dst[(size_t)i * RP + blockIdx.x * COLS + cc] = tile[i * X::PITCH + cc];
@@ -1337,7 +1390,9 @@ cudaError_t xlat_rows(const Params& p, cudaStream_t s) {
     };
     if (p.src_div != 1)  // exhaustive search
         return p.embed ? go(k_xlat_rows<N, true, true>) : go(k_xlat_rows<N, true, false>);
-    return p.embed ? go(k_xlat_rows<N, false, true>) : go(k_xlat_rows<N, false, false>);
+    if (p.embed) return go(k_xlat_rows<N, false, true>);
+    if (p.gtex && p.gt == p.gtex_base) return go(k_xlat_rows<N, false, false, true>);  // the lane's own g~
+    return go(k_xlat_rows<N, false, false>);
 }
 
 template <int N>

@@ -108,6 +108,11 @@ struct Params {
     const float2* bs_chirp;   // exp(-i pi k^2 / n), k < n
     const float2* bs_kern;    // FFT_L of the chirp kernel, / L
     const float2* tw_L;       // exp(-2 pi i k / L), k < L
+    // K3's de-rotation gather through the texture path (tld4: the 2x2 taps of a
+    // cell in one fetch): a pitch-2D texture over the lane's masked-g buffer,
+    // rows pair * np + r; used only while gt == gtex_base (0: plain loads)
+    unsigned long long gtex;
+    const float* gtex_base;
 };
 
 // Launch the stages; each returns cudaGetLastError() of its launch.

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "fscan/matcher.hpp"
+#include "fscan/spectral.hpp"
 #include "fscan/odometry.hpp"
 #include "fscan/oracle.hpp"
 
@@ -120,6 +121,12 @@ CorrelationSurface surface_from(const Array2D& scores) {
 }  // namespace
 
 int main() {
+    // next_fast_size (test_spectral.cpp:231-240): 2^a 3^b 5^c 7^d only
+    {
+        CHECK(next_fast_size(1) == 1 && next_fast_size(509) == 512 && next_fast_size(511) == 512);
+        CHECK(next_fast_size(1023) == 1024 && next_fast_size(2047) == 2048 && next_fast_size(11) == 12);
+        CHECK(next_fast_size(13) == 14 && next_fast_size(0) == 1 && next_fast_size(97) == 98);
+    }
     // config validation and derived defaults (test_matcher.cpp:60-103)
     {
         MatchConfig cfg;

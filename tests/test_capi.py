@@ -40,7 +40,7 @@ def test_drop_in_cpp_symbols_exported(fb):
                 "fscan::finalize(fscan::MatchConfig&)", "fscan::validate(fscan::MatchConfig const&)",
                 "fscan::scan_match_batch(", "fscan::brute_force_match(", "fscan::timing_comparison(",
                 "fscan::kitti_drift(", "fscan::integrate(", "fscan::odometry(", "fscan::read_scan(",
-                "fscan::write_scan(", "fscan::read_scans_f32("):
+                "fscan::write_scan(", "fscan::read_scans_f32(", "fscan::next_fast_size(int)"):
         assert sym in out, sym
 
 
@@ -155,3 +155,62 @@ def test_fscn_batch_reads_many_files_in_order(fb, tmp_path):
     fb.write_scan(str(tmp_path / "odd.fscn"), np.zeros((4, 4), np.float32), 0.5)
     with pytest.raises(fb.FscanError, match="grid size"):
         fb.read_scans(paths + [str(tmp_path / "odd.fscn")])
+
+
+# ---- .fscn files against the reference's OWN reader / writer (io.cpp:82-131, oracle/_ref) ----
+
+def _ref_or_skip():
+    import oracle
+    if not oracle.have_ref():
+        pytest.skip("oracle/_ref not built")
+    return oracle
+
+
+def test_fscn_reference_writer_to_our_reader_and_back(fb, tmp_path):
+    """Files written by the reference's write_scan read bit-identically through
+    fscan_fscn_read_batch, and files we write read bit-identically through the
+    reference's read_scan (header fields and float32 payload)."""
+    orc = _ref_or_skip()
+    rng = np.random.default_rng(7)
+    grids = [rng.standard_normal((n, n)).astype(np.float32) for n in (33, 64, 64)]
+    # reference -> ours
+    paths = []
+    for k, (g, d) in enumerate(zip(grids[1:], (0.25, 0.125))):
+        paths.append(str(tmp_path / f"ref_{k}.fscn"))
+        orc.ref_write_scan(paths[-1], g, d)
+    buf, deltas = fb.read_scans(paths)
+    np.testing.assert_array_equal(buf[0], grids[1])
+    np.testing.assert_array_equal(buf[1], grids[2])
+    assert list(deltas) == [0.25, 0.125]
+    # ours -> reference (odd and even sides; the byte layout is the same)
+    for k, (g, d) in enumerate(((grids[0], 0.4), (grids[1], 0.5))):
+        p = str(tmp_path / f"ours_{k}.fscn")
+        fb.write_scan(p, g, d)
+        r, rd = orc.ref_read_scan(p)
+        np.testing.assert_array_equal(r, g)
+        assert rd == np.float32(d)
+        with open(p, "rb") as fh:
+            ours = fh.read()
+        q = str(tmp_path / f"ref_again_{k}.fscn")
+        orc.ref_write_scan(q, g, d)
+        with open(q, "rb") as fh:
+            assert fh.read() == ours  # byte-identical files
+
+
+def test_fscn_malformed_files_fail_like_the_reference(fb, tmp_path):
+    """Bad magic, truncated payload, implausible size: both readers reject the file
+    with the same reason (io.cpp:113-126 messages)."""
+    orc = _ref_or_skip()
+    bad = tmp_path / "bad.fscn"
+    bad.write_bytes(b"PNGX" + b"\0" * 16)
+    tr = str(tmp_path / "trunc.fscn")
+    orc.ref_write_scan(tr, np.ones((16, 16), np.float32), 0.5)
+    with open(tr, "r+b") as fh:
+        fh.truncate(16 + 100)
+    huge = tmp_path / "huge.fscn"
+    huge.write_bytes(b"FSCN" + np.uint32(1 << 16).tobytes() + np.float32(0.5).tobytes() + b"\0" * 4)
+    for path, why in ((str(bad), "bad magic"), (tr, "truncated"), (str(huge), "implausible grid size")):
+        with pytest.raises(orc.OracleError, match=why):
+            orc.ref_read_scan(path)
+        with pytest.raises(fb.FscanError, match=why):
+            fb.read_scans([path])

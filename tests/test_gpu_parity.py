@@ -993,3 +993,66 @@ def test_brute_force_calls_on_two_streams(fb, dev):
     torch.cuda.synchronize()
     assert np.array_equal(fb.decode_bf_results(oa), ref_a)
     assert np.array_equal(fb.decode_bf_results(ob), ref_b)
+
+
+# ---- rows with no reference code, pinned against third-party algorithms ----
+
+def test_k0_polar_to_cart_equals_scipy_bilinear(fb, dev):
+    """K0 against scipy.ndimage.map_coordinates(order=1) on the C3
+    geometry (400 x 3768 sweeps at 0.0438 m, 512^2 at 0.25 m), fp32 output."""
+    from test_oracle import _polar_to_cart_scipy
+    spec = fb.synth_spec(3)
+    pf, _, _ = fb.synth_polar_host(spec, 5, 1)
+    out = fb.polar_to_cart(to_dev(dev, pf)[0], range_res=spec.range_res, n=512, delta=0.25)
+    torch.cuda.synchronize()
+    ref = _polar_to_cart_scipy(pf[0].astype(np.float64), spec.range_res, 512, 0.25)
+    assert np.abs(out.cpu().numpy()[0] - ref).max() <= 1e-6 * np.abs(ref).max()
+
+
+def test_phase_correlation_equals_numpy_fft(fb, orc, dev):
+    """Opt-in phase correlation against numpy.fft on the length-3N/2
+    grid: surfaces within 1e-4 of the peak, the same peak cell."""
+    from test_oracle import _phase_corr_numpy
+    cfg, delta, _ = fb.baseline_config(2)
+    n = cfg.n_xy
+    f, g, _, _, _ = fb.synth_pairs_host(fb.synth_spec(2), 90, 2)
+    m = fb.Matcher(cfg, max_batch=2)
+    m.set_phase_correlation(True)
+    F, G = to_dev(dev, f, g)
+    theta = torch.tensor([0.0, 0.017], dtype=torch.float64, device=dev)
+    xs = torch.zeros((2, n, n), dtype=torch.float32, device=dev)
+    m.estimate_translation(F, G, theta, delta=delta, xy_surface=xs)
+    xs = xs.cpu().numpy()
+    for i in range(2):
+        gr = orc.rotate_bilinear(g[i].astype(np.float64), -float(theta[i]))
+        ref = _phase_corr_numpy(f[i].astype(np.float64), gr, n)
+        assert np.abs(xs[i] - ref).max() <= 1e-4 * ref.max()
+        assert np.unravel_index(np.argmax(xs[i]), ref.shape) == np.unravel_index(np.argmax(ref), ref.shape)
+
+
+def test_reference_written_fscn_files_to_trajectory(fb, orc, dev, tmp_path):
+    """Scans written by the reference's own write_scan (io.cpp:82-100, oracle/_ref)
+    go through fscan_fscn_read_batch -> fscan_odometry_batch -> trajectory; every
+    relative pose matches the fp64 oracle's scan_match on the same scans, and the
+    chained poses match the oracle's composition (tools/main.cpp:124-135)."""
+    if not orc.have_ref():
+        pytest.skip("oracle/_ref not built")
+    cfg, delta, _ = fb.baseline_config(2)
+    spec = fb.synth_spec(2)
+    scans, _, _ = fb.synth_sequence_device(spec, 21, 4)
+    host = scans.cpu().numpy()
+    paths = []
+    for k in range(4):
+        paths.append(str(tmp_path / f"scan_{k:04d}.fscn"))
+        orc.ref_write_scan(paths[-1], host[k], delta)
+    poses, res = fb.odometry_files(paths, cfg)
+    oc = oracle_cfg(orc, cfg)
+    acc = fb.Pose2D()
+    for k in range(3):
+        r = orc.scan_match(host[k], host[k + 1], oc, delta)
+        assert (res[k]["theta_bin"], res[k]["xy_row"], res[k]["xy_col"]) == (r.theta_bin, r.xy_row, r.xy_col)
+        assert abs(res[k]["theta"] - r.theta) <= THETA_TOL
+        assert abs(res[k]["tx"] - r.tx) <= PX_TOL * delta and abs(res[k]["ty"] - r.ty) <= PX_TOL * delta
+        acc = fb.compose(acc, fb.inverse(fb.Pose2D(r.theta, r.tx, r.ty)))
+        assert abs(poses[k + 1].theta - acc.theta) <= THETA_TOL
+        assert abs(poses[k + 1].tx - acc.tx) <= 3 * PX_TOL * delta and abs(poses[k + 1].ty - acc.ty) <= 3 * PX_TOL * delta

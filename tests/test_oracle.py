@@ -335,3 +335,81 @@ def test_restatement_matches_baseline_size_golden(orc, path):
         np.testing.assert_allclose(r.theta_surface, z["theta_surface"][i], rtol=1e-12, atol=0)
         win = np.pad(r.xy_surface, w)[r.xy_row:r.xy_row + 2 * w + 1, r.xy_col:r.xy_col + 2 * w + 1]
         assert np.abs(win - z["xy_window"][i]).max() <= 1e-12 * z["xy_absmax"][i]
+
+
+# ---------------------------------------------------------------- pins for the rows with no reference code
+# SURVEY a20 (polar -> Cartesian, K0) and a21 (phase correlation) have no
+# reference implementation; the C restatement is pinned here against
+# independent third-party algorithms (scipy.ndimage bilinear, numpy.fft).
+
+def _polar_to_cart_scipy(polar, res, n, delta):
+    """K0 spec through scipy.ndimage.map_coordinates(order=1):
+    cell (r, c) at x = (c - (n-1)//2) delta, y = -(r - (n-1)//2) delta; azimuth
+    bin a centred on 2 pi a / n_az (wrapping), range bin k on (k + 0.5) res,
+    range taps outside [0, n_range) read 0. The azimuth wrap and the zero range
+    border are made explicit by padding (one wrapped row each side, one zero
+    column each side) so one mode='constant' call covers both axes."""
+    from scipy import ndimage
+    n_az, n_range = polar.shape
+    half = (n - 1) // 2
+    c, r = np.meshgrid(np.arange(n), np.arange(n))
+    x = (c - half) * delta
+    y = -(r - half) * delta
+    phi = np.mod(np.arctan2(y, x), 2 * np.pi)
+    fa = phi * n_az / (2 * np.pi)
+    fk = np.hypot(x, y) / res - 0.5
+    padded = np.zeros((n_az + 2, n_range + 2))
+    padded[1:-1, 1:-1] = polar
+    padded[0, 1:-1] = polar[-1]
+    padded[-1, 1:-1] = polar[0]
+    coords = np.stack([fa + 1.0, fk + 1.0])
+    return ndimage.map_coordinates(padded, coords, order=1, mode="constant", cval=0.0, prefilter=False)
+
+
+@pytest.mark.parametrize("n_az,n_range,res,n,delta", [(400, 3768, 0.0438, 64, 2.0), (37, 120, 0.5, 48, 1.3),
+                                                      (400, 300, 0.0438, 96, 0.2)])
+def test_polar_to_cart_restatement_equals_scipy_bilinear(orc, n_az, n_range, res, n, delta):
+    rng = np.random.default_rng(n_az + n)
+    polar = rng.random((n_az, n_range))
+    ours = orc.polar_to_cart(polar, res, n, delta)
+    ref = _polar_to_cart_scipy(polar, res, n, delta)
+    assert np.abs(ours - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max())
+    # the last case runs off the end of the sweep: those cells are exactly zero in both
+    assert (ref == 0).any() == ((ours == 0).any())
+
+
+def _phase_corr_numpy(f, gr, n):
+    """Phase correlation on the length-3n/2 grid with numpy.fft:
+    X = conj(F) G / |conj(F) G| (0 where 0), c = real(ifft2(X)) (1/M^2 scaling as
+    xcorr, spectral.cpp:146-151), centred (fftshift), cropped and flipped like
+    matcher.cpp:171-182: s[i, j] = raw[M/2 - (i - half), M/2 + (j - half)]."""
+    m = 3 * n // 2
+    off = (m - n) // 2
+    fp = np.zeros((m, m))
+    gp = np.zeros((m, m))
+    fp[off:off + n, off:off + n] = f
+    gp[off:off + n, off:off + n] = gr
+    x = np.conj(np.fft.fft2(fp)) * np.fft.fft2(gp)
+    mag = np.abs(x)
+    x = np.where(mag > 0, x / np.where(mag > 0, mag, 1), 0)
+    raw = np.fft.fftshift(np.real(np.fft.ifft2(x)))
+    half, h = (n - 1) // 2, m // 2
+    i, j = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+    return raw[h - (i - half), h + (j - half)]
+
+
+@pytest.mark.parametrize("n,theta", [(64, 0.0), (64, 0.031), (128, -0.02)])
+def test_phase_correlation_restatement_equals_numpy_fft(orc, n, theta):
+    rng = np.random.default_rng(n)
+    f = rng.random((n, n))
+    g = np.roll(f, (3, -4), (0, 1)) + 0.05 * rng.random((n, n))
+    cfg = orc.make_config(n_theta=90, delta_theta=np.pi / 90, n_xy=n, delta_xy=0.5, n_radius=0, pad_angle=-1)
+    orc.finalize(cfg)
+    tx, ty, s = orc.estimate_translation_ex(f, g, theta, cfg, 0.5, 3 * n // 2, True)
+    gr = orc.rotate_bilinear(g, -theta)  # rotate_bilinear is pinned to the reference elsewhere
+    ref = _phase_corr_numpy(f, gr, n)
+    assert np.abs(s - ref).max() <= 1e-12 * np.abs(ref).max()
+    if theta == 0.0:  # a pure circular shift: the phase-correlation peak is the shift,
+        r, c = np.unravel_index(np.argmax(s), s.shape)  # rows flipped (matcher.cpp:171-182)
+        half = (n - 1) // 2
+        assert (half - r, c - half) == (3, -4)
