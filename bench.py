@@ -351,6 +351,46 @@ def parity_block(f, g, mf, mg, gpu_rows, ref_rows, oc, delta, kind) -> dict:
             "inputs": "the GPU run's own device-rendered inputs, copied to the host"}
 
 
+# ---------------------------------------------------------------- small-batch legs (C1, C2)
+
+def small_config_leg(fb, cid: int, device: int, reps: int) -> dict:
+    """BASELINE config `cid` (1: one pair, 2: 64 pairs) timed call by call on this
+    GPU: a 256 MiB buffer is written before every call (the inputs would sit in
+    L2 otherwise), each call timed by its own events on the launching stream;
+    median / p95 per call and pairs/s at the median (the reference's run_bench
+    protocol, bench.cpp:53-82: burn-in, then per-call timings)."""
+    import torch
+    cfg, delta, batch = fb.baseline_config(cid)
+    spec = fb.synth_spec(cid)
+    f, g, mf, mg, _ = fb.synth_pairs_device(spec, 0, batch, device=device)
+    if not spec.masks:
+        mf = mg = None
+    m = fb.Matcher(cfg, max_batch=batch, device=device)
+    m.set_graphs(True)
+    dev = torch.device("cuda", device)
+    stream = torch.cuda.current_stream(dev)
+    out = torch.empty(batch * fb.RESULT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+    flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)
+    for _ in range(50):  # burn-in (bench.cpp:56-62)
+        m.match_device(f, g, mf, mg, delta=delta, out=out, stream=stream)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    us = []
+    for _ in range(reps):
+        flush.fill_(1.0)
+        e0.record(stream)
+        m.match_device(f, g, mf, mg, delta=delta, out=out, stream=stream)
+        e1.record(stream)
+        e1.synchronize()
+        us.append(e0.elapsed_time(e1) * 1e3)
+    res = fb.decode_results(out)
+    med = statistics.median(us)
+    return {"workload": workload_desc(cid), "value": round(batch / (med / 1e6), 1), "unit": UNIT,
+            "us_per_call_median": round(med, 2), "us_per_call_p95": round(pct(us, 95), 2),
+            "us_per_pair_median": round(med / batch, 3), "calls": reps, "launches_per_call": m.launches_last,
+            "bad_pairs": int((res["status"] != 0).sum()),
+            "timing": "per call: L2 flushed before, CUDA events around the graph replay (device time)"}
+
+
 # ---------------------------------------------------------------- our arm
 
 def run_ours(args):
@@ -487,6 +527,12 @@ def run_ours(args):
             proxy[str(shard)] = {"pairs_per_s": round(rate, 1), "per_gpu_efficiency": round(rate / value, 3),
                                  "as_shard_of": f"{total // shard} GPUs"}
 
+    # BASELINE C1 (single-pair latency) and C2 (64-pair batch) measured in the
+    # same run (rank 0, N = 1, on the default C4 job)
+    small = None
+    if rank == 0 and world == 1 and args.config == 4 and not args.no_small:
+        small = {"c1": small_config_leg(fb, 1, local, 200), "c2": small_config_leg(fb, 2, local, 100)}
+
     # the paper's central comparison: the exhaustive correlative search (the
     # reference's brute_force_match, oracle.cpp:40-67) over the matcher's full theta
     # grid on the same GPU, a few pairs (every candidate is one translation stage)
@@ -606,7 +652,8 @@ def run_ours(args):
             "impl_config": {"chunk": args.chunk or "auto", "graphs": not args.no_graphs,
                             "pairs_per_rank": per, "backend": args.backend if world > 1 else None},
             "roofline": roofline, "hbm_pipeline": pipeline, "cpu_baseline": cpu, "parity": parity,
-            "e2e": e2e, "shard_proxy": proxy, "exhaustive_search": exhaustive, "odometry_chain": chain,
+            "e2e": e2e, "shard_proxy": proxy, "small_batches": small, "exhaustive_search": exhaustive,
+            "odometry_chain": chain,
             "clocks": clk.summary(), "gpu_launches": launches_per_step * args.steps,
             "bad_pairs": bad, "impl": "ours",
             "library": {"path": os.path.relpath(fb.LIB_PATH, ROOT), "sha16": file_sha16(fb.LIB_PATH),
@@ -687,6 +734,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-proxy", action="store_true", help="skip the per-shard-size proxy lines")
+    ap.add_argument("--no-small", action="store_true", help="skip the C1 latency / C2 batch legs")
     ap.add_argument("--no-exhaustive", action="store_true", help="skip the brute-force comparison leg")
     ap.add_argument("--no-odometry", action="store_true", help="skip the chained-sequence leg")
     args = ap.parse_args()

@@ -26,6 +26,10 @@
 #include "polar.h"
 
 
+#ifndef FSCAN_K3_U
+#define FSCAN_K3_U 4  // K3 gather: cells per thread with their loads in flight together
+#endif
+
 namespace fscan_detail {
 
 using fscan_fft::cadd;
@@ -652,7 +656,7 @@ __global__ void __launch_bounds__(kXThreads, 3) k_xlat_rows(Params p) {
     // consecutive x; U cells per thread per round with every load issued
     // before any use (memory-level parallelism for the L2/DRAM latency)
     constexpr int CELLS = ROWS * N;
-    constexpr int U = 4;
+    constexpr int U = FSCAN_K3_U;
 #pragma unroll 1
     for (int e0 = threadIdx.x; e0 < CELLS; e0 += U * kXThreads) {
         float fv[U], tap[U][4], frs[U], fcs[U];
@@ -784,8 +788,12 @@ struct XColGeom {
     // (N = 1024 at 2 columns: 192-thread CTAs, three per SM at 96 registers;
     // C5 +8% over 4 columns in 384 threads at 80 registers)
     static constexpr int COLS = (T >= 32) ? 2 : ((T >= 16) ? 4 : ((T >= 4) ? 8 : 16));
-    static constexpr int PITCH = COLS + 1;  // output tile [N rows][PITCH] float2
     static constexpr int THREADS = 3 * COLS * T;
+    // output tile [N rows][PITCH] float2, copied out one element per thread so
+    // that consecutive lanes fill whole 32-byte sectors (a row-per-thread copy
+    // with 128-bit loads / stores at PITCH 6 measured K4 10% slower: every
+    // store instruction then writes 32 half sectors)
+    static constexpr int PITCH = COLS + 1;
     // split re/im exchange: with 64-bit accesses this kernel's allocation grows
     // past two CTAs per SM (note: an explicit minBlocks=1 launch bound also
     // changes ptxas' choice, 80 -> 167 registers)
@@ -1015,6 +1023,35 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
 //   x[2n] = Re z[n], x[2n+1] = Im z[n];
 // group q inverts Z_q; scaled by 1/M^2, cropped to lags kx in [-(N/2-1), N/2]
 // (surface col j = kx + half), plus this block's hard argmax (lowest index on ties).
+// one-shot mbarrier + TMA bulk copy global -> shared (cp.async.bulk)
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+
+#ifdef FSCAN_K5_LDG
+constexpr bool kK5Tma = false;  // A/B: every thread loads its Y elements from global
+#else
+constexpr bool kK5Tma = true;
+#endif
+
 template <int N>
 struct XOutGeom {
     static constexpr int K2 = N / 4;
@@ -1026,7 +1063,11 @@ struct XOutGeom {
     static constexpr int ROWS = ROWS0 < N ? ROWS0 : N;
     static constexpr int THREADS = 3 * ROWS * T;
     using G = Geom<K2, THREADS>;
-    static constexpr size_t SMEM = (size_t)G::FLOATS * sizeof(float);
+    // the CTA's ROWS rows of Y (contiguous at pitch ypitch(N)) arrive by one TMA
+    // bulk copy into the same shared memory the FFT exchange uses afterwards
+    static constexpr size_t YBYTES = (size_t)ROWS * ypitch(N) * sizeof(float2);
+    static constexpr size_t FFT_BYTES = (size_t)G::FLOATS * sizeof(float);
+    static constexpr size_t SMEM = (kK5Tma && YBYTES > FFT_BYTES) ? YBYTES : FFT_BYTES;
 };
 
 // EMB: only the lag window [win_off, win_off + p.n)^2 of the embedded surface
@@ -1041,7 +1082,7 @@ __global__ void __launch_bounds__(XOutGeom<N>::THREADS) k_xlat_out(Params p) {
     constexpr int NW = THREADS / 32;
     constexpr int T = G::T;
     constexpr int half = N / 2 - 1;
-    extern __shared__ float smem[];
+    extern __shared__ __align__(128) float smem[];
     __shared__ float red_v[NW];
     __shared__ int red_i[NW];
     const int pair = blockIdx.y;
@@ -1051,10 +1092,23 @@ __global__ void __launch_bounds__(XOutGeom<N>::THREADS) k_xlat_out(Params p) {
     const int i = blockIdx.x * ROWS + rl;
     const auto buf = G::lay(smem, tr);
     {
-        // (staging Y through shared memory with cp.async, or a k'-major Y
-        // written straight from K4's registers, both measured slower: the
-        // stride-3 row reads are served by L1 across the three q groups)
-        const float2* yrow = p.zbuf + ((size_t)pair * N + i) * ypitch(N);
+        // kK5Tma: the block's rows by one bulk copy (the per-thread global loads
+        // of the stride-3 pattern left every warp waiting on its own loads; a
+        // per-thread cp.async staging and a k'-major Y written straight from
+        // K4's registers measured slower than those loads)
+        const float2* yrow;
+        if constexpr (kK5Tma) {
+            __shared__ uint64_t mbar;
+            if (threadIdx.x == 0) mbar_init(&mbar, 1);
+            __syncthreads();
+            if (threadIdx.x == 0)
+                bulk_load(smem, p.zbuf + ((size_t)pair * N + blockIdx.x * ROWS) * ypitch(N), (unsigned)X::YBYTES,
+                          &mbar);
+            mbar_wait(&mbar, 0);
+            yrow = reinterpret_cast<const float2*>(smem) + (size_t)rl * ypitch(N);
+        } else {
+            yrow = p.zbuf + ((size_t)pair * N + i) * ypitch(N);
+        }
         float2 v[16];
 #pragma unroll
         for (int m = 0; m < 16; ++m) {
@@ -1064,6 +1118,7 @@ __global__ void __launch_bounds__(XOutGeom<N>::THREADS) k_xlat_out(Params p) {
             const float2 B = cmul(csub(a, b), cconj(wm(p.tw_m, k)));
             v[m] = make_float2(A.x - B.y, A.y + B.x);  // A + iB
         }
+        if constexpr (kK5Tma) __syncthreads();  // Y reads done before the exchange reuses the bytes
         fft_regs<X::K2, +1, true>(v, t, buf, p.tw_k2);
 #pragma unroll
         for (int m = 0; m < 16; ++m) buf.put(t + m * T, v[m]);
