@@ -146,16 +146,30 @@ __device__ __forceinline__ void dft_r(float2* x) {
 // Exchange-buffer layout of one transform (see header comment): complex
 // values as float2 (one 64-bit shared access per element), XOR-swizzled inside
 // each 16-element line so every exchange pattern is bank-conflict free.
+#ifdef FSCAN_SWIZZLE_WIDE
+constexpr bool kSwizzleWide = true;  // A/B: keep the XOR swizzle for W >= 16
+#else
+constexpr bool kSwizzleWide = false;
+#endif
+
 template <int W>
 struct Lay {
     float2* buf;
     int sub;  // transform index inside an interleaved group (W > 1)
     __device__ __forceinline__ int at(int i) const {
-        const int j = (i & ~15) | ((i & 15) ^ ((i >> 4) & 15));
-        if constexpr (W == 1) {
-            return j;
+        if constexpr (W >= 16 && !kSwizzleWide) {
+            // W >= 16 interleaved transforms: element i of every transform of a
+            // half-warp sits in its own bank pair (sub) whatever i is, so the
+            // swizzle buys nothing; a plain W * i + sub leaves the exchange
+            // loops with compile-time offsets from one per-thread base
+            return W * i + sub;
         } else {
-            return W * j + sub;
+            const int j = (i & ~15) | ((i & 15) ^ ((i >> 4) & 15));
+            if constexpr (W == 1) {
+                return j;
+            } else {
+                return W * j + sub;
+            }
         }
     }
     __device__ __forceinline__ void put(int i, float2 v) const { buf[at(i)] = v; }

@@ -760,6 +760,35 @@ __global__ void __launch_bounds__(kXThreads, 3) k_xlat_rows(Params p) {
 // stored by surface row i = half - ky (the flip of matcher.cpp:171-182)
 // through a shared-memory tile (a k'-major output written straight from the
 // registers measured slower: K4 grows to 120 registers and K5's loads scatter).
+// one-shot mbarrier + TMA bulk copy global -> shared (cp.async.bulk)
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+
+#ifdef FSCAN_K4_TMA
+constexpr bool kK4Tma = true;  // A/B: the block's fgt columns by one TMA bulk copy (measured slower)
+#else
+constexpr bool kK4Tma = false;
+#endif
+
 // K4 twiddles W_M^{q n0} for n0 = t + m T (T = K/16, so W_M^T = W_48):
 // W_M^{q t} (one global-table read per thread) times W_48^{q m}, a
 // constant-bank table (two distinct q per warp: at most two addresses per
@@ -798,7 +827,17 @@ struct XColGeom {
     // past two CTAs per SM (note: an explicit minBlocks=1 launch bound also
     // changes ptxas' choice, 80 -> 167 registers)
     using G = fscan_fft::GeomSoA<N / 2, THREADS>;
-    static constexpr size_t FFT_FLOATS = (size_t)2 * G::FLOATS;
+    // kK4Tma (below N = 1024; off by default): the CTA's COLS columns of fgt (one
+    // contiguous COLS x N float4 block) arrive by one TMA bulk copy into an input
+    // area that buffer B aliases once both folds have read it. Measured C4 -0.7%
+    // and C2 -2.5% (K4 9.4 -> 9.7 ms): unlike K5, whose one load phase it
+    // shortens, here every warp then waits for the whole block before its first
+    // fold instead of for its own loads, and the larger CTA (61 KB) costs C2's
+    // N = 256 kernel its fourth CTA per SM.
+    static constexpr bool TMA = kK4Tma && N <= 512;
+    static constexpr size_t IN_FLOATS = (size_t)4 * COLS * N;
+    static constexpr size_t B_FLOATS = (TMA && IN_FLOATS > (size_t)G::FLOATS) ? IN_FLOATS : (size_t)G::FLOATS;
+    static constexpr size_t FFT_FLOATS = (size_t)G::FLOATS + B_FLOATS;
     static constexpr size_t TILE_FLOATS = (size_t)2 * N * PITCH;
     static constexpr size_t WORK_FLOATS = FFT_FLOATS > TILE_FLOATS ? FFT_FLOATS : TILE_FLOATS;
     // twiddle tables staged behind the work area: W_K (K entries) and, below
@@ -845,7 +884,7 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
     using G = typename X::G;
     constexpr int T = G::T, COLS = X::COLS;
     constexpr int half = N / 2 - 1;
-    extern __shared__ float smem[];
+    extern __shared__ __align__(128) float smem[];
     const int pair = blockIdx.y;
     int tr, t;
     G::map(threadIdx.x, tr, t);
@@ -855,6 +894,16 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
     const auto bufA = G::lay(smem, tr);
     const auto bufB = G::lay(smem + G::FLOATS, tr);
     const float4* src = p.fgt + ((size_t)pair * (H + 1) + kq) * N;
+    __shared__ uint64_t mbar;
+    if constexpr (X::TMA) {  // the block's columns: one bulk copy, read by both folds
+        const int ncols_in = min(COLS, H + 1 - (int)blockIdx.x * COLS);
+        if (threadIdx.x == 0) {
+            mbar_init(&mbar, 1);
+            bulk_load(smem + G::FLOATS, p.fgt + ((size_t)pair * (H + 1) + blockIdx.x * COLS) * N,
+                      (unsigned)(ncols_in * N * sizeof(float4)), &mbar);
+        }
+        src = reinterpret_cast<const float4*>(smem + G::FLOATS) + (size_t)min(c, ncols_in - 1) * N;
+    }
     // stage the twiddle tables in shared memory (latency: the FFT stages and
     // input/combine twiddles read them ~90 times per thread)
     float2* stw_rk = reinterpret_cast<float2*>(smem + X::WORK_FLOATS);
@@ -928,6 +977,7 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
         for (int m = 0; m < 16; ++m) a[m] = bufA.get(t + m * T);
         __syncwarp();  // every input read before the transform's exchange writes
     } else {
+        if constexpr (X::TMA) mbar_wait(&mbar, 0);  // (the barrier above published the init)
 #pragma unroll
         for (int m = 0; m < 16; ++m) {
             const int n0 = t + m * T;
@@ -951,6 +1001,7 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
             const float2 s = cadd(make_float2(u0.z, u0.w), cmul(w3q, make_float2(u1.z, u1.w)));
             a[m] = q ? cmul(wq_m(m, n0), s) : s;
         }
+        if constexpr (X::TMA) __syncthreads();  // every fold read of the input area before buffer B reuses it
     }
     fft_regs<K, -1, true>(a, t, bufB, twk);
 #pragma unroll
@@ -1023,29 +1074,6 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
 //   x[2n] = Re z[n], x[2n+1] = Im z[n];
 // group q inverts Z_q; scaled by 1/M^2, cropped to lags kx in [-(N/2-1), N/2]
 // (surface col j = kx + half), plus this block's hard argmax (lowest index on ties).
-// one-shot mbarrier + TMA bulk copy global -> shared (cp.async.bulk)
-__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-        "r"(phase)
-        : "memory");
-}
-
 #ifdef FSCAN_K5_LDG
 constexpr bool kK5Tma = false;  // A/B: every thread loads its Y elements from global
 #else
