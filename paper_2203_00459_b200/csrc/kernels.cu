@@ -43,6 +43,35 @@ using fscan_fft::part_floats;
 
 namespace {
 
+// one-shot mbarrier + TMA bulk copy global -> shared (cp.async.bulk)
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+
+#ifdef FSCAN_K3_FT_LDG
+constexpr bool kK3FtTma = false;  // A/B: K3 loads f~ per thread from global
+#else
+constexpr bool kK3FtTma = true;
+#endif
+
 // K1a CTA size: 128 threads (4 rows at N = 512) leave room for K1a CTAs next
 // to the compute-bound translation kernels of the other lane (measured -5% K1a)
 constexpr int kRowThreads = 128;
@@ -593,7 +622,11 @@ struct XRowGeom {
     // the FFT exchange buffers alias the gather stash (dead once v[] is loaded):
     // ~50 KB per CTA, three CTAs per SM
     static constexpr size_t STASH = (size_t)2 * ROWS * SP;
-    static constexpr size_t WORK = STASH > (size_t)G::FLOATS ? STASH : (size_t)G::FLOATS;
+    // + the CTA's ROWS rows of f~ (dense, one TMA bulk copy) behind the stash
+    // (texture-gather instantiation only)
+    static constexpr size_t FT_OFF = STASH;
+    static constexpr size_t STAGE = kK3FtTma ? STASH + (size_t)ROWS * N : STASH;
+    static constexpr size_t WORK = STAGE > (size_t)G::FLOATS ? STAGE : (size_t)G::FLOATS;
     // + the span-16 stage's [r][k] twiddle table (K >= 256): 15 shared loads
     // per thread instead of 4 global loads and 11 products (C4 +0.4%; the same
     // table in K1b measured slower)
@@ -634,7 +667,7 @@ __global__ void __launch_bounds__(kXThreads, 3) k_xlat_rows(Params p) {
     using X = XRowGeom<N>;
     using G = typename X::G;
     constexpr int T = G::T, ROWS = X::ROWS, SP = X::SP;
-    extern __shared__ float smem[];
+    extern __shared__ __align__(128) float smem[];
     float* st_re = smem;
     float* st_im = smem + ROWS * SP;
     float* xbase = smem;  // aliases the stash (see XRowGeom::SMEM)
@@ -643,6 +676,18 @@ __global__ void __launch_bounds__(kXThreads, 3) k_xlat_rows(Params p) {
     const RotState rs = p.rot[pair];
     const int src = MANY ? (p.item_base + pair) / p.src_div : pair;  // pair whose scans this item reads
     const float* ft = p.ft + (size_t)src * N * N;
+    // TEX (the lane's own workspace): the block's ROWS rows of f~ by one TMA bulk
+    // copy into a dense stage; the gather reads them from there
+    constexpr bool FT_TMA = TEX && kK3FtTma;
+    __shared__ uint64_t ft_bar;
+    const float* fst = smem + X::FT_OFF;
+    if constexpr (FT_TMA) {
+        if (threadIdx.x == 0) {
+            mbar_init(&ft_bar, 1);
+            bulk_load(smem + X::FT_OFF, ft + (size_t)y0 * N, (unsigned)(ROWS * N * sizeof(float)), &ft_bar);
+        }
+        __syncthreads();  // publishes the barrier's initialisation
+    }
     const float* gt = p.gt + (size_t)src * N * N;
     const float c0f32 = EMB ? p.c0 : (N - 1) / 2.0f;  // exact (half-integer or integer)
     float2* srk = reinterpret_cast<float2*>(smem + X::WORK);  // ordered by the barrier after the gather
@@ -679,7 +724,7 @@ __global__ void __launch_bounds__(kXThreads, 3) k_xlat_rows(Params p) {
             const int r0 = (int)r0f, cc0 = (int)cf;
             const bool r0in = live && (unsigned)r0 < (unsigned)N, r1in = live && (unsigned)(r0 + 1) < (unsigned)N;
             const bool c0in = (unsigned)cc0 < (unsigned)N, c1in = (unsigned)(cc0 + 1) < (unsigned)N;
-            fv[u] = live ? ft[y * N + x] : 0.f;
+            if constexpr (!FT_TMA) fv[u] = live ? ft[y * N + x] : 0.f;
             if constexpr (TEX) {
                 // texel (c, row) at coordinate (c + 1.0, row + 1.0): the gather's
                 // footprint starts at floor(coord - 0.5) = (cc0, r0); component
@@ -696,6 +741,14 @@ __global__ void __launch_bounds__(kXThreads, 3) k_xlat_rows(Params p) {
                 tap[u][1] = (r0in && c1in) ? gp[1] : 0.f;
                 tap[u][2] = (r1in && c0in) ? gp[N] : 0.f;
                 tap[u][3] = (r1in && c1in) ? gp[N + 1] : 0.f;
+            }
+        }
+        if constexpr (FT_TMA) {
+            if (e0 == threadIdx.x) mbar_wait(&ft_bar, 0);  // first round: after its texture fetches are issued
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int e = e0 + u * kXThreads;
+                fv[u] = e < CELLS ? fst[e] : 0.f;  // dense [ROWS][N]: e = yl * N + x
             }
         }
 #pragma unroll
@@ -760,29 +813,6 @@ __global__ void __launch_bounds__(kXThreads, 3) k_xlat_rows(Params p) {
 // stored by surface row i = half - ky (the flip of matcher.cpp:171-182)
 // through a shared-memory tile (a k'-major output written straight from the
 // registers measured slower: K4 grows to 120 registers and K5's loads scatter).
-// one-shot mbarrier + TMA bulk copy global -> shared (cp.async.bulk)
-__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-        "r"(phase)
-        : "memory");
-}
-
 #ifdef FSCAN_K4_TMA
 constexpr bool kK4Tma = true;  // A/B: the block's fgt columns by one TMA bulk copy (measured slower)
 #else
@@ -802,6 +832,11 @@ __device__ __forceinline__ float2 w48(int k) { return make_float2(kW48re[k], kW4
 constexpr bool kK4W48 = false;
 #else
 constexpr bool kK4W48 = true;
+#endif
+#ifdef FSCAN_K4_W48_FOLD1
+constexpr bool kK4W48Fold1 = true;  // A/B: W_48 combine twiddles at N = 1024 too
+#else
+constexpr bool kK4W48Fold1 = false;
 #endif
 #ifndef FSCAN_K4_MINB512
 #define FSCAN_K4_MINB512 3
@@ -926,8 +961,8 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
     };
     // kK4W48: the thread's twiddle bases (see the W_48 table above)
     const float2 bq = X::FOLD1 ? make_float2(1.f, 0.f) : __ldg(p.tw_m + q * t);  // W_M^{q t}
-    const float2 b1 = X::FOLD1 ? make_float2(1.f, 0.f) : __ldg(p.tw_m + t);      // W_M^{t}
-    const float2 b2 = X::FOLD1 ? make_float2(1.f, 0.f) : __ldg(p.tw_m + 2 * t);  // W_M^{2 t}
+    const float2 b1 = (X::FOLD1 && !kK4W48Fold1) ? make_float2(1.f, 0.f) : __ldg(p.tw_m + t);      // W_M^{t}
+    const float2 b2 = (X::FOLD1 && !kK4W48Fold1) ? make_float2(1.f, 0.f) : __ldg(p.tw_m + 2 * t);  // W_M^{2 t}
     auto wq_m = [&](int m, int n0) {  // W_M^{q n0}, n0 = t + m T
         if constexpr (kK4W48 && !X::FOLD1) return cmul(bq, w48(q * m));
         else return wq(n0, q);
@@ -1029,7 +1064,7 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
         if (m < 16) {
             const int n0 = t + m * T;
             float2 v1, v2;  // W_M^{n0}, W_M^{2 n0}
-            if constexpr (kK4W48 && !X::FOLD1) {
+            if constexpr (kK4W48 && (!X::FOLD1 || kK4W48Fold1)) {
                 v1 = cmul(b1, w48(m));
                 v2 = cmul(b2, w48(2 * m));
             } else {
