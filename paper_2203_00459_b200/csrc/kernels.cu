@@ -1252,15 +1252,29 @@ __global__ void __launch_bounds__(XOutGeom<N>::THREADS) k_xlat_out(Params p) {
 // ---------------------------------------------------------------- K6
 constexpr int kFinThreads = 256;
 
-__device__ __forceinline__ double block_sum(double v, double* sh) {
+// three sums in one pass (one pair of barriers instead of three); every value is
+// reduced in the same order as block_sum
+__device__ __forceinline__ void block_sum3(double& a, double& b, double& c, double* sh) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        b += __shfl_xor_sync(0xffffffffu, b, o);
+        c += __shfl_xor_sync(0xffffffffu, c, o);
+    }
+    constexpr int NW = kFinThreads / 32;
     __syncthreads();
-    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+    if ((threadIdx.x & 31) == 0) {
+        sh[threadIdx.x >> 5] = a;
+        sh[NW + (threadIdx.x >> 5)] = b;
+        sh[2 * NW + (threadIdx.x >> 5)] = c;
+    }
     __syncthreads();
-    double r = 0.0;
-    for (int w = 0; w < kFinThreads / 32; ++w) r += sh[w];
-    return r;
+    a = b = c = 0.0;
+    for (int w = 0; w < NW; ++w) {
+        a += sh[w];
+        b += sh[NW + w];
+        c += sh[2 * NW + w];
+    }
 }
 
 __device__ __forceinline__ double block_max(double v, double* sh) {
@@ -1276,6 +1290,7 @@ __device__ __forceinline__ double block_max(double v, double* sh) {
 
 __global__ void __launch_bounds__(kFinThreads) k_finalize(Params p, int nparts) {
     __shared__ double sh[kFinThreads / 32];
+    __shared__ double sh3[3 * (kFinThreads / 32)];
     __shared__ float pk_v;
     __shared__ int pk_i;
     const int pair = blockIdx.x;
@@ -1339,9 +1354,7 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(Params p, int nparts) 
         rsum += wgt * ((r - half) * p.delta);
         csum += wgt * ((cc - half) * p.delta);
     }
-    ws = block_sum(ws, sh);
-    rsum = block_sum(rsum, sh);
-    csum = block_sum(csum, sh);
+    block_sum3(ws, rsum, csum, sh3);
     if (threadIdx.x == 0) {
         const RotState rs = p.rot[pair];
         const double ty_ = rsum / ws, tx_ = csum / ws;
@@ -1569,8 +1582,12 @@ cudaError_t launch_rot_gather(const Params& p, cudaStream_t s) {
 }
 
 // CTAs per pair for K2b: one when the batch fills the GPU, else up to 16
+#ifndef FSCAN_K2B_BIG_SPLIT
+#define FSCAN_K2B_BIG_SPLIT 1  // CTAs per pair for batches that fill the GPU
+#endif
 int polar_split(int batch, int nt) {
-    if (nt <= 1 || batch >= FSCAN_K2B_SPLIT_BELOW) return 1;
+    if (nt <= 1) return 1;
+    if (batch >= FSCAN_K2B_SPLIT_BELOW) return FSCAN_K2B_BIG_SPLIT;
     return std::min(16, (148 + batch - 1) / batch);
 }
 
