@@ -74,7 +74,15 @@ constexpr bool kK3FtTma = true;
 
 // K1a CTA size: 128 threads (4 rows at N = 512) leave room for K1a CTAs next
 // to the compute-bound translation kernels of the other lane (measured -5% K1a)
-constexpr int kRowThreads = 128;
+#ifndef FSCAN_K1A_THREADS
+#define FSCAN_K1A_THREADS 128
+#endif
+constexpr int kRowThreads = FSCAN_K1A_THREADS;
+#ifdef FSCAN_K1A_MINB
+#define FSCAN_K1A_BOUNDS __launch_bounds__(kRowThreads, FSCAN_K1A_MINB)
+#else
+#define FSCAN_K1A_BOUNDS __launch_bounds__(kRowThreads)  // (an explicit minBlocks = 1 makes ptxas use 132 registers)
+#endif
 
 template <int N>
 using RowG = Geom<N, kRowThreads>;
@@ -101,7 +109,7 @@ __device__ __forceinline__ const float2* tile_at(const float2* m, int n, int r, 
 // input), window by the separable Hann w[r]*w[c], FFT the packed row
 // z = f~w + i g~w.
 template <int N>
-__global__ void __launch_bounds__(kRowThreads) k_rot_rows(Params p) {
+__global__ void FSCAN_K1A_BOUNDS k_rot_rows(Params p) {
     using G = RowG<N>;
     constexpr int T = G::T;
     extern __shared__ float smem[];
