@@ -321,6 +321,72 @@ __device__ __forceinline__ void gather_sums(const Params& p, const float2* m, in
     }
 }
 
+// PB pairs per CTA (independent pairs only): every tap-table entry is loaded once
+// for PB magnitude planes (the table read is a third of K2a's load bytes), and a
+// thread keeps PB x U taps in flight
+#ifndef FSCAN_K2A_PB
+#define FSCAN_K2A_PB 2
+#endif
+template <int PB>
+__global__ void __launch_bounds__(kGatherThreads) k_rot_gather_multi(Params p) {
+    const int pair0 = blockIdx.y * PB;
+    const int nt = p.n_theta, n = p.n, n_live = p.n_live;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int i = blockIdx.x * (kGatherThreads / 4) + warp * 8 + (lane >> 2);
+    const int rsub = lane & 3;
+    const bool live = i < nt;
+    const float2* m0 = reinterpret_cast<const float2*>(p.mag) + (size_t)pair0 * p.mag_plane;
+    const PolarTap* col = p.taps + (live ? i : 0);
+    double af[PB], ag[PB];
+#pragma unroll
+    for (int b = 0; b < PB; ++b) af[b] = ag[b] = 0.0;
+    const int np = min(PB, p.batch - pair0);
+    constexpr int U = PB >= 4 ? 1 : 4 / PB;
+    for (int j0 = rsub; j0 < n_live; j0 += 4 * U) {
+        PolarTap e[U];
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+            const int j = j0 + 4 * q;
+            e[q] = (live && j < n_live) ? col[(size_t)j * nt] : PolarTap{0, 0.f, 0.f, 0.f};  // flags 0: 0
+        }
+        float2 tv[PB][U][4];
+#pragma unroll
+        for (int b = 0; b < PB; ++b) {
+            const float2* m = m0 + (size_t)(b < np ? b : 0) * p.mag_plane;
+#pragma unroll
+            for (int q = 0; q < U; ++q) {
+                const int r0 = e[q].packed & 0xFFF, u = (e[q].packed >> 12) & 0xFFF, fl = e[q].packed >> 24;
+#pragma unroll
+                for (int tp = 0; tp < 4; ++tp) {
+                    const bool on = (fl >> tp) & 1;
+                    tv[b][q][tp] = on ? __ldg(tile_at(m, n, r0 + (tp >> 1), u + (tp & 1))) : make_float2(0.f, 0.f);
+                }
+            }
+        }
+#pragma unroll
+        for (int b = 0; b < PB; ++b)
+#pragma unroll
+            for (int q = 0; q < U; ++q) {
+                af[b] += (double)bilerp(e[q].fr, e[q].fc, tv[b][q][0].x, tv[b][q][1].x, tv[b][q][2].x, tv[b][q][3].x);
+                ag[b] += (double)bilerp(e[q].fr, e[q].fc, tv[b][q][0].y, tv[b][q][1].y, tv[b][q][2].y, tv[b][q][3].y);
+            }
+    }
+#pragma unroll
+    for (int b = 0; b < PB; ++b) {
+        // the four radius phases of an azimuth, summed in a fixed order
+        double a = af[b], g = ag[b];
+        a += __shfl_xor_sync(0xffffffffu, a, 1);
+        g += __shfl_xor_sync(0xffffffffu, g, 1);
+        a += __shfl_xor_sync(0xffffffffu, a, 2);
+        g += __shfl_xor_sync(0xffffffffu, g, 2);
+        if (live && rsub == 0 && b < np) {
+            double* prof = p.prof + (size_t)(pair0 + b) * 2 * nt;
+            prof[i] = a;
+            prof[nt + i] = g;
+        }
+    }
+}
+
 __global__ void __launch_bounds__(kGatherThreads) k_rot_gather(Params p) {
     const int pair = blockIdx.y;
     const int nt = p.n_theta;
@@ -1585,6 +1651,13 @@ cudaError_t launch_xlat_out(const Params& p, cudaStream_t s) { FSCAN_DISPATCH_N(
 
 cudaError_t launch_rot_gather(const Params& p, cudaStream_t s) {
     if (p.n_theta == 1) return cudaSuccess;
+    if (FSCAN_K2A_PB > 1 && !p.chain) {
+        constexpr int PB = FSCAN_K2A_PB > 1 ? FSCAN_K2A_PB : 2;
+        k_rot_gather_multi<PB><<<dim3((p.n_theta + kGatherThreads / 4 - 1) / (kGatherThreads / 4),
+                                      (p.batch + PB - 1) / PB),
+                                 kGatherThreads, 0, s>>>(p);
+        return cudaGetLastError();
+    }
     k_rot_gather<<<dim3((p.n_theta + kGatherThreads / 4 - 1) / (kGatherThreads / 4), p.batch), kGatherThreads, 0, s>>>(p);
     return cudaGetLastError();
 }
