@@ -1183,6 +1183,11 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
 //   x[2n] = Re z[n], x[2n+1] = Im z[n];
 // group q inverts Z_q; scaled by 1/M^2, cropped to lags kx in [-(N/2-1), N/2]
 // (surface col j = kx + half), plus this block's hard argmax (lowest index on ties).
+#ifdef FSCAN_K5_ROWMAJOR
+constexpr bool kK5QMajor = false;  // A/B: transforms ordered row-major (3 rl + q)
+#else
+constexpr bool kK5QMajor = true;
+#endif
 #ifdef FSCAN_K5_LDG
 constexpr bool kK5Tma = false;  // A/B: every thread loads its Y elements from global
 #else
@@ -1225,7 +1230,11 @@ __global__ void __launch_bounds__(XOutGeom<N>::THREADS) k_xlat_out(Params p) {
     const int pair = blockIdx.y;
     int tr, t;
     G::map(threadIdx.x, tr, t);
-    const int rl = tr / 3, q = tr % 3;
+    // q-major transform order (kK5QMajor): the two transforms of a half-warp
+    // are one q group of two adjacent rows, whose stride-3 reads of the staged
+    // Y rows (pitch = 8 mod 16 bank pairs) then fall on disjoint banks; in
+    // row-major order they were two q groups of one row (2-way conflicts)
+    const int rl = kK5QMajor ? tr % ROWS : tr / 3, q = kK5QMajor ? tr / ROWS : tr % 3;
     const int i = blockIdx.x * ROWS + rl;
     const auto buf = G::lay(smem, tr);
     {
@@ -1276,7 +1285,8 @@ __global__ void __launch_bounds__(XOutGeom<N>::THREADS) k_xlat_out(Params p) {
             best_i = li;
         }
     };
-    const auto e0 = G::lay(smem, 3 * rl), e1 = G::lay(smem, 3 * rl + 1), e2 = G::lay(smem, 3 * rl + 2);
+    auto tr_of = [&](int qq) { return kK5QMajor ? qq * ROWS + rl : 3 * rl + qq; };
+    const auto e0 = G::lay(smem, tr_of(0)), e1 = G::lay(smem, tr_of(1)), e2 = G::lay(smem, tr_of(2));
     const float2 w31 = w3(1), w32 = w3(2);
 #pragma unroll
     for (int j = 0; j < 6; ++j) {
