@@ -907,6 +907,11 @@ constexpr bool kK4W48 = false;
 #else
 constexpr bool kK4W48 = true;
 #endif
+#ifdef FSCAN_K4_QMAJOR
+constexpr bool kK4QMajor = true;  // A/B (measured slower): K4 transforms ordered q-major
+#else
+constexpr bool kK4QMajor = false;
+#endif
 #ifdef FSCAN_K4_W48_FOLD1
 constexpr bool kK4W48Fold1 = true;  // A/B: W_48 combine twiddles at N = 1024 too
 #else
@@ -997,7 +1002,13 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
     const int pair = blockIdx.y;
     int tr, t;
     G::map(threadIdx.x, tr, t);
-    const int c = tr / 3, q = tr % 3;
+    // (kK4QMajor, off: q-major transform order — a warp's two transforms one q
+    // group of two adjacent columns — makes the radix-3 combine conflict-free
+    // (bank model 162 -> 96 wavefronts) and q warp-uniform, but measured K4
+    // 9.2 -> 9.6 ms and C2 -3%: the three q groups of a column no longer load
+    // their shared fgt column from the same warp)
+    constexpr bool QM = kK4QMajor && !X::FOLD1;
+    const int c = QM ? tr % COLS : tr / 3, q = QM ? tr / COLS : tr % 3;
     const int kp = blockIdx.x * COLS + c;
     const int kq = kp <= H ? kp : H;  // the last block may hold fewer columns
     const auto bufA = G::lay(smem, tr);
@@ -1128,8 +1139,9 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
     for (int m = 0; m < 16; ++m) bufB.put(t + m * T, a[m]);
     __syncthreads();
     // radix-3 combine: group q handles the slots m = q, q+3, ... of its column
-    const auto e0 = G::lay(smem + G::FLOATS, 3 * c), e1 = G::lay(smem + G::FLOATS, 3 * c + 1),
-               e2 = G::lay(smem + G::FLOATS, 3 * c + 2);
+    auto tr_of = [&](int qq) { return QM ? qq * COLS + c : 3 * c + qq; };
+    const auto e0 = G::lay(smem + G::FLOATS, tr_of(0)), e1 = G::lay(smem + G::FLOATS, tr_of(1)),
+               e2 = G::lay(smem + G::FLOATS, tr_of(2));
     const float2 w31 = w3(1), w32 = w3(2);
     float2 accp[6], accn[6];
 #pragma unroll
