@@ -193,6 +193,25 @@ __host__ __device__ constexpr int part_floats() {
 // are chosen for the row-separation loop of K3, see XRowGeom). Verified
 // conflict-free for all exchange and combine patterns with an access-pattern
 // model.
+// Padded per-transform layout of the row kernels (kGeomPad): one float2 of
+// padding per 16 elements, addr = i + i/16. Both exchange patterns of the
+// radix-16 Stockham stages (stride-16 puts i = 16 b + r, unit-stride gets
+// i = t + m T) then land on distinct bank pairs, and every address is a
+// per-thread base plus a compile-time offset: no per-access XOR (the swizzled
+// Lay<1> spends a LOP3 and an add on every exchange access).
+struct LayPad {
+    float2* buf;
+    __device__ __forceinline__ static int at(int i) { return i + (i >> 4); }
+    __device__ __forceinline__ void put(int i, float2 v) const { buf[at(i)] = v; }
+    __device__ __forceinline__ float2 get(int i) const { return buf[at(i)]; }
+};
+
+#ifdef FSCAN_GEOM_XOR
+constexpr bool kGeomPad = false;  // A/B: the XOR-swizzled Lay<1>
+#else
+constexpr bool kGeomPad = true;
+#endif
+
 template <int N, int THREADS>
 struct Geom {
     static constexpr int T = N / 16;
@@ -201,23 +220,36 @@ struct Geom {
     static constexpr int GROUPS = PER_CTA / W;
     static_assert(GROUPS >= 1 && PER_CTA % W == 0, "a CTA must hold whole warps of transforms");
     // float2 elements per transform buffer holding length-LEN data
+    // kGeomPad: LEN + LEN/16 elements; for T < 16 that is = T (mod 16), which
+    // puts the W transforms of a half-warp on disjoint bank pairs; T = 16 adds 2
+    // so that K3's row-separation loop keeps the same bank offset per row (O = 6)
     template <int LEN>
     __host__ __device__ static constexpr int stride_len() {
-        return LEN + (T < 16 ? T : (T == 16 ? 2 : 12));
+        if constexpr (kGeomPad)
+            return LEN + LEN / 16 + (T == 16 ? 2 : 0);
+        else
+            return LEN + (T < 16 ? T : (T == 16 ? 2 : 12));
     }
     static constexpr int FLOATS = PER_CTA * 2 * stride_len<N>();  // one exchange buffer per transform
+    using L = std::conditional_t<kGeomPad, LayPad, Lay<1>>;
     __device__ __forceinline__ static void map(int tid, int& tr, int& t) {
         tr = tid / T;
         t = tid % T;
     }
+    __device__ __forceinline__ static L make(float2* p) {
+        if constexpr (kGeomPad)
+            return LayPad{p};
+        else
+            return Lay<1>{p, 0};
+    }
     // layout of transform tr inside buffer `base` (FLOATS floats, 8-byte aligned)
-    __device__ __forceinline__ static Lay<1> lay(float* base, int tr) {
-        return Lay<1>{reinterpret_cast<float2*>(base) + tr * stride_len<N>(), 0};
+    __device__ __forceinline__ static L lay(float* base, int tr) {
+        return make(reinterpret_cast<float2*>(base) + tr * stride_len<N>());
     }
     // layout of transform tr for a buffer holding length-LEN data per transform
     template <int LEN>
-    __device__ __forceinline__ static Lay<1> lay_len(float* base, int tr) {
-        return Lay<1>{reinterpret_cast<float2*>(base) + tr * stride_len<LEN>(), 0};
+    __device__ __forceinline__ static L lay_len(float* base, int tr) {
+        return make(reinterpret_cast<float2*>(base) + tr * stride_len<LEN>());
     }
     template <int LEN>
     __host__ __device__ static constexpr int floats_len() {

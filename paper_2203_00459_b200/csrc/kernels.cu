@@ -78,10 +78,17 @@ constexpr bool kK3FtTma = true;
 #define FSCAN_K1A_THREADS 128
 #endif
 constexpr int kRowThreads = FSCAN_K1A_THREADS;
+// K1a residency: at N = 512, 7 CTAs of 128 threads per SM (<= 72 registers);
+// without a bound ptxas takes 80 with the padded layout (and 132 with an
+// explicit minBlocks of 1)
+template <int N>
+__host__ __device__ constexpr int k1a_minb() {
+    return N >= 1024 ? 6 : (N == 512 ? 7 : 8);
+}
 #ifdef FSCAN_K1A_MINB
 #define FSCAN_K1A_BOUNDS __launch_bounds__(kRowThreads, FSCAN_K1A_MINB)
 #else
-#define FSCAN_K1A_BOUNDS __launch_bounds__(kRowThreads)  // (an explicit minBlocks = 1 makes ptxas use 132 registers)
+#define FSCAN_K1A_BOUNDS __launch_bounds__(kRowThreads, k1a_minb<N>())
 #endif
 
 template <int N>
