@@ -30,6 +30,9 @@ recs = []
 for r in rows[2:]:
     k = r[hdr.index("Kernel Name")].split("(")[0].split("::")[-1]
     k = k.split("<")[0].replace("k_", "", 1)
+    for suffix in ("_mb", "_multi"):  # launch-bound / multi-pair instantiations report under the stage name
+        if k.endswith(suffix):
+            k = k[: -len(suffix)]
     pc = {m: col(r, c) for m, c in (("issue_pct", "smsp__issue_active.avg.pct_of_peak_sustained_active"),
                                      ("warps_active_pct", "sm__warps_active.avg.pct_of_peak_sustained_active"),
                                      ("dram_pct", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"))}
