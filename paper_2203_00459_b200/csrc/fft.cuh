@@ -221,12 +221,13 @@ struct Geom {
     static_assert(GROUPS >= 1 && PER_CTA % W == 0, "a CTA must hold whole warps of transforms");
     // float2 elements per transform buffer holding length-LEN data
     // kGeomPad: LEN + LEN/16 elements; for T < 16 that is = T (mod 16), which
-    // puts the W transforms of a half-warp on disjoint bank pairs; T = 16 adds 2
-    // so that K3's row-separation loop keeps the same bank offset per row (O = 6)
+    // puts the W transforms of a half-warp on disjoint bank pairs; T = 16 / 32
+    // add 2 / 12 so that K3's row-separation loop keeps the bank offset per row
+    // it has with the swizzled layout (O = 6 at N = 512, 4 at N = 1024)
     template <int LEN>
     __host__ __device__ static constexpr int stride_len() {
         if constexpr (kGeomPad)
-            return LEN + LEN / 16 + (T == 16 ? 2 : 0);
+            return LEN + LEN / 16 + (T < 16 ? 0 : (T == 16 ? 2 : 12));
         else
             return LEN + (T < 16 ? T : (T == 16 ? 2 : 12));
     }

@@ -101,6 +101,8 @@ def k5(qmajor, at=xor_at, stride=136, T=8, ROWS=8, TH=192, RPS=392, H=384):
 if __name__ == "__main__":
     print("K3 XOR layout, stride 258:", k3(xor_at, 258))
     print("K3 padded layout, stride 274:", k3(pad_at, 274))
+    print("K3 N=1024 XOR layout, stride 524:", k3(xor_at, 524, K=512, T=32, TH=384, ROWS=4, H=768))
+    print("K3 N=1024 padded layout, stride 556:", k3(pad_at, 556, K=512, T=32, TH=384, ROWS=4, H=768))
     print("K5 row-major:", k5(False))
     print("K5 q-major:", k5(True))
     print("K5 q-major, padded layout (stride 136):", k5(True, pad_at, 136))
