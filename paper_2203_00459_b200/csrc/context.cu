@@ -752,11 +752,14 @@ fscan_status fscan_ctx_create(int device, const fscan_config* cfg_in, int max_ba
     CK(cudaMemcpy(ctx->taps, taps.data(), sizeof(PolarTap) * taps.size(), cudaMemcpyHostToDevice));
 
     // lanes (concurrent chunk pipelines) and chunk size: FSCAN_LANES / FSCAN_CHUNK
-    // override the defaults (3 lanes, ~1 GiB of workspace per lane; 3 lanes
+    // override the defaults (3 lanes, ~2 GiB of workspace per lane; 3 lanes
     // measured +0.9% over 2 at C4, 4-8 lanes or other chunk sizes no better)
     if (const char* e = std::getenv("FSCAN_LANES")) ctx->nlanes = std::clamp(std::atoi(e), 1, kMaxLanes);
     const double per_pair = (double)n * n * (8 + 4 + 8) + (double)n * (3 * n / 4 + 1) * 16;
-    int chunk = (int)std::max(1.0, std::floor((1024.0 * 1024 * 1024) / per_pair));
+    // ~2 GiB of workspace per lane: 126 pairs at N = 512 (then the texture cap
+    // below), 63 at N = 1024 (C5 +2% over 1 GiB / 31 pairs: larger grids, and K2b
+    // leaves its small-batch split path)
+    int chunk = (int)std::max(1.0, std::floor((2048.0 * 1024 * 1024) / per_pair));
     // a batch smaller than the lanes' chunks is spread over all lanes (C2, 64
     // pairs: +7% over one 64-pair chunk); tiny contexts keep whole-batch chunks
     // (the exhaustive search runs pair x candidate items through them)
