@@ -939,11 +939,9 @@ struct XColGeom {
     // C5 +8% over 4 columns in 384 threads at 80 registers)
     static constexpr int COLS = (T >= 32) ? 2 : ((T >= 16) ? 4 : ((T >= 4) ? 8 : 16));
     static constexpr int THREADS = 3 * COLS * T;
-    // output tile [N rows][PITCH] float2, copied out one element per thread so
-    // that consecutive lanes fill whole 32-byte sectors (a row-per-thread copy
-    // with 128-bit loads / stores at PITCH 6 measured K4 10% slower: every
-    // store instruction then writes 32 half sectors)
-    static constexpr int PITCH = COLS + 1;
+    // (outputs are stored from registers into the blocked Y layout, y_at; round
+    // 1-2 staged them in an [N][COLS + 1] shared tile copied out row-major,
+    // ~12% of K4's warp samples)
     // split re/im exchange: with 64-bit accesses this kernel's allocation grows
     // past two CTAs per SM (note: an explicit minBlocks=1 launch bound also
     // changes ptxas' choice, 80 -> 167 registers)
@@ -959,8 +957,7 @@ struct XColGeom {
     static constexpr size_t IN_FLOATS = (size_t)4 * COLS * N;
     static constexpr size_t B_FLOATS = (TMA && IN_FLOATS > (size_t)G::FLOATS) ? IN_FLOATS : (size_t)G::FLOATS;
     static constexpr size_t FFT_FLOATS = (size_t)G::FLOATS + B_FLOATS;
-    static constexpr size_t TILE_FLOATS = (size_t)2 * N * PITCH;
-    static constexpr size_t WORK_FLOATS = FFT_FLOATS > TILE_FLOATS ? FFT_FLOATS : TILE_FLOATS;
+    static constexpr size_t WORK_FLOATS = FFT_FLOATS;
     // twiddle tables staged behind the work area: W_K (K entries) and, below
     // N = 1024, W_M (3K; at 1024 it would push the CTA past half an SM's smem)
     // (the K-point FFTs read the span-16 stage's factors from a [r][k] table,
@@ -1150,7 +1147,11 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
     const auto e0 = G::lay(smem + G::FLOATS, tr_of(0)), e1 = G::lay(smem + G::FLOATS, tr_of(1)),
                e2 = G::lay(smem + G::FLOATS, tr_of(2));
     const float2 w31 = w3(1), w32 = w3(2);
-    float2 accp[6], accn[6];
+    // outputs straight into K5's row blocks (y_at; stored by surface row
+    // i = half - ky, the flip of matcher.cpp:171-182): the 16 lanes of a
+    // transform hold 16 consecutive rows of one bin, whole RB-row runs
+    float2* dst = p.zbuf + (size_t)pair * N * (H + 1);
+    const bool store = kp <= H;  // the last block's clamped duplicates store nothing
 #pragma unroll
     for (int j = 0; j < 6; ++j) {
         const int m = q + 3 * j;
@@ -1167,30 +1168,11 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
             const float2 x0 = e0.get(n0);
             const float2 x1 = cmul(cconj(v1), e1.get(n0));
             const float2 x2 = cmul(cconj(v2), e2.get(n0));
-            accp[j] = cadd(x0, cadd(x1, x2));
-            accn[j] = cadd(x0, cadd(cmul(w31, x1), cmul(w32, x2)));
+            if (store) {
+                dst[y_at<N>(half - n0, kp)] = cadd(x0, cadd(x1, x2));
+                dst[y_at<N>(half - (n0 - K), kp)] = cadd(x0, cadd(cmul(w31, x1), cmul(w32, x2)));
+            }
         }
-    }
-    __syncthreads();  // the buffers become the output tile
-    float2* tile = reinterpret_cast<float2*>(smem);  // [N rows][PITCH]
-    // K4 -> K5 rows with a 64-byte aligned pitch: each CTA's column stripe is
-    // whole sectors per row
-    constexpr int RP = ypitch(N);
-    float2* dst = p.zbuf + (size_t)pair * N * RP;
-    const int ncols = min(COLS, H + 1 - (int)blockIdx.x * COLS);
-#pragma unroll
-    for (int j = 0; j < 6; ++j) {
-        const int m = q + 3 * j;
-        if (m < 16) {
-            const int n0 = t + m * T;
-            tile[(half - n0) * X::PITCH + c] = accp[j];
-            tile[(half - (n0 - K)) * X::PITCH + c] = accn[j];
-        }
-    }
-    __syncthreads();
-    for (int o = threadIdx.x; o < N * COLS; o += blockDim.x) {
-        const int i = o / COLS, cc = o % COLS;
-        if (cc < ncols) dst[(size_t)i * RP + blockIdx.x * COLS + cc] = tile[i * X::PITCH + cc];
     }
 }
 
@@ -1224,9 +1206,10 @@ struct XOutGeom {
     static constexpr int ROWS = ROWS0 < N ? ROWS0 : N;
     static constexpr int THREADS = 3 * ROWS * T;
     using G = Geom<K2, THREADS>;
-    // the CTA's ROWS rows of Y (contiguous at pitch ypitch(N)) arrive by one TMA
-    // bulk copy into the same shared memory the FFT exchange uses afterwards
-    static constexpr size_t YBYTES = (size_t)ROWS * ypitch(N) * sizeof(float2);
+    static_assert(ROWS == y_rows(N), "one K5 CTA inverts one block of the Y layout");
+    // the CTA's block of Y (ROWS rows, [k'][ROWS] contiguous, y_at) arrives by one
+    // TMA bulk copy into the same shared memory the FFT exchange uses afterwards
+    static constexpr size_t YBYTES = (size_t)ROWS * (3 * N / 4 + 1) * sizeof(float2);
     static constexpr size_t FFT_BYTES = (size_t)G::FLOATS * sizeof(float);
     static constexpr size_t SMEM = (kK5Tma && YBYTES > FFT_BYTES) ? YBYTES : FFT_BYTES;
 };
@@ -1249,36 +1232,31 @@ __global__ void __launch_bounds__(XOutGeom<N>::THREADS) k_xlat_out(Params p) {
     const int pair = blockIdx.y;
     int tr, t;
     G::map(threadIdx.x, tr, t);
-    // q-major transform order (kK5QMajor): the two transforms of a half-warp
-    // are one q group of two adjacent rows, whose stride-3 reads of the staged
-    // Y rows (pitch = 8 mod 16 bank pairs) then fall on disjoint banks; in
-    // row-major order they were two q groups of one row (2-way conflicts)
+    // q-major transform order (kK5QMajor): the transforms of a half-warp are one
+    // q group of adjacent rows; with the row permutation of the Y blocks their
+    // stride-3 bin reads fall on distinct bank pairs (y_swz)
     const int rl = kK5QMajor ? tr % ROWS : tr / 3, q = kK5QMajor ? tr / ROWS : tr % 3;
     const int i = blockIdx.x * ROWS + rl;
     const auto buf = G::lay(smem, tr);
     {
-        // kK5Tma: the block's rows by one bulk copy (the per-thread global loads
-        // of the stride-3 pattern left every warp waiting on its own loads; a
-        // per-thread cp.async staging and a k'-major Y written straight from
-        // K4's registers measured slower than those loads)
-        const float2* yrow;
+        // kK5Tma: the block by one bulk copy (the per-thread global loads of the
+        // stride-3 pattern left every warp waiting on its own loads; a per-thread
+        // cp.async staging measured slower than those loads)
+        const float2* yblk = p.zbuf + ((size_t)pair * N + blockIdx.x * ROWS) * (H + 1);
         if constexpr (kK5Tma) {
             __shared__ uint64_t mbar;
             if (threadIdx.x == 0) mbar_init(&mbar, 1);
             __syncthreads();
-            if (threadIdx.x == 0)
-                bulk_load(smem, p.zbuf + ((size_t)pair * N + blockIdx.x * ROWS) * ypitch(N), (unsigned)X::YBYTES,
-                          &mbar);
+            if (threadIdx.x == 0) bulk_load(smem, yblk, (unsigned)X::YBYTES, &mbar);
             mbar_wait(&mbar, 0);
-            yrow = reinterpret_cast<const float2*>(smem) + (size_t)rl * ypitch(N);
-        } else {
-            yrow = p.zbuf + ((size_t)pair * N + i) * ypitch(N);
+            yblk = reinterpret_cast<const float2*>(smem);
         }
+        auto y = [&](int k) { return yblk[k * ROWS + (rl ^ y_swz(ROWS, k))]; };  // Y[i][k]
         float2 v[16];
 #pragma unroll
         for (int m = 0; m < 16; ++m) {
             const int k = 3 * (t + m * T) + q;
-            const float2 a = yrow[k], b = cconj(yrow[H - k]);
+            const float2 a = y(k), b = cconj(y(H - k));
             const float2 A = cadd(a, b);
             const float2 B = cmul(csub(a, b), cconj(wm(p.tw_m, k)));
             v[m] = make_float2(A.x - B.y, A.y + B.x);  // A + iB

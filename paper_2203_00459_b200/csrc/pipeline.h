@@ -19,8 +19,27 @@ struct PolarTap {
 };
 
 // Row pitch (float2) of the K4 -> K5 spectrum rows: 3N/4 + 1 bins rounded up
-// to 8 (64-byte aligned rows).
+// to 8 (64-byte aligned rows). (Sizes the workspace; the layout is y_at below.)
 __host__ __device__ constexpr int ypitch(int n) { return (3 * n / 4 + 1 + 7) / 8 * 8; }
+
+// K4 -> K5 spectrum rows Y[row i][bin k'] (k' in [0, 3N/4]), stored in blocks of
+// RB = y_rows(N) surface rows — exactly the rows one K5 CTA inverts — each block
+// [k'][RB] float2 with the RB rows XOR-permuted per bin: K4 stores its column
+// outputs straight from registers (RB consecutive rows of one bin are one
+// contiguous, fully written RB * 8-byte run: no shared-memory transpose), K5
+// fetches its block with one bulk copy and reads the stride-3 bins of its
+// transforms conflict-free (the permutation spreads the bins a half-warp reads
+// over distinct bank pairs; checked for every N by tools/bank_model.py k5y).
+__host__ __device__ constexpr int y_rows(int n) { return 4096 / n < n ? 4096 / n : n; }
+__host__ __device__ constexpr int y_swz(int rb, int k) {
+    return (rb / 4) * ((k >> (rb >= 16 ? 0 : (rb == 8 ? 1 : 2))) & 3);
+}
+// float2 offset of Y[i][k] inside one pair's rows
+template <int N>
+__host__ __device__ constexpr int y_at(int i, int k) {
+    constexpr int RB = y_rows(N), H1 = 3 * N / 4 + 1;
+    return ((i / RB) * H1 + k) * RB + ((i % RB) ^ y_swz(RB, k));
+}
 
 // Per-pair state handed from the angular stage to the translation stage.
 struct RotState {
