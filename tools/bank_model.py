@@ -6,8 +6,10 @@ costs the largest number of distinct addresses sharing a bank pair) for:
   * K3 (N = 512): the radix-16 exchange puts/gets and the row-separation loop,
     XOR-swizzled layout (stride 258) vs padded layout (addr = i + i/16),
   * K5 (N = 512): the stride-3 reads of the TMA-staged Y rows and the radix-3
-    combine, row-major vs q-major transform order.
-usage: python tools/bank_model.py"""
+    combine, row-major vs q-major transform order,
+  * K5 (every N): the stride-3 bin reads of the blocked, row-permuted Y layout
+    K4 stores (pipeline.h y_at / y_swz), and that the permutation is one.
+usage: python tools/bank_model.py [k5y]"""
 from collections import Counter
 
 
@@ -98,7 +100,41 @@ def k5(qmajor, at=xor_at, stride=136, T=8, ROWS=8, TH=192, RPS=392, H=384):
     return dict(tot), dict(ideal)
 
 
+def y_swz(rb, k):  # pipeline.h
+    return (rb // 4) * ((k >> (0 if rb >= 16 else (1 if rb == 8 else 2))) & 3)
+
+
+def k5y(N):
+    """Y[i][k] at k * RB + (rl ^ y_swz(RB, k)) inside the CTA's block; q-major K5."""
+    K2, H = N // 4, 3 * N // 4
+    T = K2 // 16
+    RB = min(4096 // N, N)
+    TH = 3 * RB * T
+    for k in range(H + 1):
+        assert sorted(r ^ y_swz(RB, k) for r in range(RB)) == list(range(RB))
+    tot = ideal = 0
+    for w in range(TH // 32):
+        for m in range(16):
+            for mirror in (False, True):
+                for h in range(2):
+                    a = []
+                    for lane in range(16 * h, 16 * h + 16):
+                        tr, t = divmod(w * 32 + lane, T)
+                        rl, q = tr % RB, tr // RB
+                        k = 3 * (t + m * T) + q
+                        k = H - k if mirror else k
+                        a.append(k * RB + (rl ^ y_swz(RB, k)))
+                    tot += cost(a)
+                    ideal += 1
+    return tot, ideal
+
+
 if __name__ == "__main__":
+    import sys
+    if sys.argv[1:] == ["k5y"]:
+        for n in (64, 128, 256, 512, 1024):
+            print(f"K5 blocked Y, N={n}: wavefronts {k5y(n)[0]} (conflict-free: {k5y(n)[1]})")
+        sys.exit(0)
     print("K3 XOR layout, stride 258:", k3(xor_at, 258))
     print("K3 padded layout, stride 274:", k3(pad_at, 274))
     print("K3 N=1024 XOR layout, stride 524:", k3(xor_at, 524, K=512, T=32, TH=384, ROWS=4, H=768))
