@@ -92,6 +92,7 @@ struct fscan_ctx {
     float2* tw_k = nullptr;
     float2* tw_k2 = nullptr;
     float2* tw_rk = nullptr;  // W_256^{r k} at (r-1)*16 + k (K4's radix-16 stage)
+    float2* tw_k4 = nullptr;  // W_M^{a j} at a*48 + j, M = 3 np / 2 (K4's merged twiddles)
     float2* tw_m = nullptr;
     float* hann = nullptr;
     int2* band = nullptr;
@@ -377,6 +378,7 @@ Params base_params(fscan_ctx* ctx, Lane& l, int batch, double delta) {
     p.tw_k = ctx->tw_k;
     p.tw_k2 = ctx->tw_k2;
     p.tw_rk = ctx->tw_rk;
+    p.tw_k4 = ctx->tw_k4;
     p.tw_m = ctx->tw_m;
     p.hann = ctx->hann;
     p.band = ctx->band;
@@ -740,6 +742,16 @@ fscan_status fscan_ctx_create(int device, const fscan_config* cfg_in, int max_ba
             }
         CK(cudaMalloc(&ctx->tw_rk, sizeof(float2) * rk.size()));
         CK(cudaMemcpy(ctx->tw_rk, rk.data(), sizeof(float2) * rk.size(), cudaMemcpyHostToDevice));
+        // K4's merged twiddle table (fft.cuh SmemTwQF / SmemTwQI), exact phase reduction
+        const long long m3 = 3LL * ctx->np / 2;
+        std::vector<float2> k4(16 * 48);
+        for (int a = 0; a < 16; ++a)
+            for (int j = 0; j < 48; ++j) {
+                const double e = -2.0 * kPi * (double)((a * j) % m3) / (double)m3;
+                k4[a * 48 + j] = make_float2((float)std::cos(e), (float)std::sin(e));
+            }
+        CK(cudaMalloc(&ctx->tw_k4, sizeof(float2) * k4.size()));
+        CK(cudaMemcpy(ctx->tw_k4, k4.data(), sizeof(float2) * k4.size(), cudaMemcpyHostToDevice));
     }
     CK(cudaMemcpy(ctx->tw_m, twm.data(), sizeof(float2) * twm.size(), cudaMemcpyHostToDevice));
     CK(cudaMalloc(&ctx->hann, sizeof(float) * n));
@@ -808,6 +820,7 @@ void fscan_ctx_destroy(fscan_ctx* ctx) {
     cudaFree(ctx->tw_k);
     cudaFree(ctx->tw_k2);
     cudaFree(ctx->tw_rk);
+    cudaFree(ctx->tw_k4);
     cudaFree(ctx->tw_m);
     cudaFree(ctx->hann);
     cudaFree(ctx->band);

@@ -348,10 +348,32 @@ __device__ __forceinline__ float2 twiddle(const SmemTwRK& tw, int idx) {
 template <typename TW>
 constexpr bool kTwRK = std::is_same_v<TW, SmemTwRK>;
 
+// K4's merged twiddles (a K = 16 R point transform, K <= 256, inside a length
+// M = 3K transform split into three q groups). One shared table
+// F[a][j] = W_M^{a j} (a < 16, j < 48, row stride kQS), `f` = F + q:
+//  * forward (QF): the group's input twiddle W_M^{n q}, n = t + m T, is split
+//    into W_M^{m T q} (applied to the inputs) and W_M^{t q}, which is constant
+//    over a thread's first-stage butterfly and so rides on its outputs into the
+//    last stage: input r of butterfly k there carries W_M^{r q} W_K^{r k} =
+//    F[r][3k + q] (one table read, as the plain W_K^{r k} did);
+//  * inverse (QI): the combine's output twiddle W_M^{-n q}, n = k + 16 r', is
+//    split into W_M^{-16 r' q} (applied to the outputs) and W_M^{-k q}, constant
+//    over the last-stage butterfly k, which joins its input twiddles:
+//    W_K^{-r k} W_M^{-k q} = conj(F[k][3r + q]) (r = 0 included).
+constexpr int kQS = 49;  // odd row stride: the inverse's column reads F[k][.] spread over banks
+struct SmemTwQF {
+    const float2* f;
+};
+struct SmemTwQI {
+    const float2* f;
+};
+template <typename TW>
+constexpr bool kTwQ = std::is_same_v<TW, SmemTwQF> || std::is_same_v<TW, SmemTwQI>;
+
 // Radix-16 twiddles as powers of one table read (global tables) or all read
 // from the table (shared-memory tables).
 template <typename TW>
-constexpr bool kTwPow = !std::is_same_v<TW, SmemTw> && !kTwRK<TW>;
+constexpr bool kTwPow = !std::is_same_v<TW, SmemTw> && !kTwRK<TW> && !kTwQ<TW>;
 
 // One Stockham stage. Ns = span before this stage, R = radix.
 // Exchange barrier: a warp barrier when every thread of the transform (and of
@@ -378,7 +400,15 @@ __device__ __forceinline__ void stage(float2 (&v)[16], int t, const L& lay, cons
         const int k = b & (Ns - 1);
         if constexpr (Ns > 1) {
             constexpr int q = N / (Ns * R);  // W_{Ns R}^x = tw[x * q]
-            if constexpr (Ns == 16 && kTwRK<TW>) {
+            if constexpr (std::is_same_v<TW, SmemTwQF>) {
+                static_assert(Ns == 16 && LAST, "merged twiddles: two-stage transforms only");
+#pragma unroll
+                for (int r = 1; r < R; ++r) u[r] = cmul(u[r], tw.f[r * kQS + 3 * k]);
+            } else if constexpr (std::is_same_v<TW, SmemTwQI>) {
+                static_assert(Ns == 16 && LAST, "merged twiddles: two-stage transforms only");
+#pragma unroll
+                for (int r = 0; r < R; ++r) u[r] = cmul(u[r], cconj(tw.f[k * kQS + 3 * r]));
+            } else if constexpr (Ns == 16 && kTwRK<TW>) {
                 // W_{16 R}^{r k} = W_256^{(16/R) r k}
 #pragma unroll
                 for (int r = 1; r < R; ++r) {

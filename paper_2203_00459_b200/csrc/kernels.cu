@@ -924,8 +924,23 @@ constexpr bool kK4W48Fold1 = true;  // A/B: W_48 combine twiddles at N = 1024 to
 #else
 constexpr bool kK4W48Fold1 = false;
 #endif
+#ifndef FSCAN_K4_F2_MIN
+#define FSCAN_K4_F2_MIN 64
+#endif
 #ifndef FSCAN_K4_MINB512
 #define FSCAN_K4_MINB512 3
+#endif
+#ifdef FSCAN_K4_EARLYSYNC
+constexpr bool kK4LateSync = false;  // A/B: the table barrier before the first fold's loads
+#else
+constexpr bool kK4LateSync = true;
+#endif
+// kK4Merge (off: measured C4 +0.4% = noise, C2 -2% — the table costs N = 256 its
+// fourth CTA per SM; ncu: 8% fewer FP32 instructions, L1 busy 66 -> 81%)
+#ifdef FSCAN_K4_MERGE
+constexpr bool kK4Merge = true;  // A/B: twiddles merged into the last FFT stage (xlat_cols_merged)
+#else
+constexpr bool kK4Merge = false;
 #endif
 
 template <int N>
@@ -945,7 +960,9 @@ struct XColGeom {
     // split re/im exchange: with 64-bit accesses this kernel's allocation grows
     // past two CTAs per SM (note: an explicit minBlocks=1 launch bound also
     // changes ptxas' choice, 80 -> 167 registers)
-    using G = fscan_fft::GeomSoA<N / 2, THREADS>;
+    // (FSCAN_K4_F2_MIN: float2 exchange buffers, one per transform, at N >= it)
+    using G = std::conditional_t<(N >= FSCAN_K4_F2_MIN), fscan_fft::Geom<N / 2, THREADS>,
+                                 fscan_fft::GeomSoA<N / 2, THREADS>>;
     // kK4Tma (below N = 1024; off by default): the CTA's COLS columns of fgt (one
     // contiguous COLS x N float4 block) arrive by one TMA bulk copy into an input
     // area that buffer B aliases once both folds have read it. Measured C4 -0.7%
@@ -980,6 +997,10 @@ struct XColGeom {
     // parked in shared memory (N = 1024: C5 +3%); below, every q group loads and
     // folds its own elements (the shared fold measured 1% slower at N = 512)
     static constexpr bool FOLD1 = N >= 1024;
+    // merged-twiddle path (xlat_cols_merged, two-stage K-point transforms):
+    // the exchange buffers + the [16][kQS] table W_M^{a j}
+    static constexpr bool MERGE = kK4Merge && !FOLD1 && !TMA && N / 2 <= 256;
+    static constexpr size_t SMEM_MERGE = (FFT_FLOATS + 2 * 16 * fscan_fft::kQS) * sizeof(float);
 };
 
 template <int N>
@@ -996,7 +1017,14 @@ __global__ void __launch_bounds__(XColGeom<N>::THREADS, MINB) k_xlat_cols_mb(Par
 }
 
 template <int N>
+__device__ __forceinline__ void xlat_cols_merged(const Params& p);
+
+template <int N>
 __device__ __forceinline__ void xlat_cols_body(const Params& p) {
+    if constexpr (XColGeom<N>::MERGE) {
+        xlat_cols_merged<N>(p);
+        return;
+    }
     constexpr int K = N / 2, M = 3 * K, H = M / 2;
     using X = XColGeom<N>;
     using G = typename X::G;
@@ -1056,8 +1084,16 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
         if constexpr (kK4W48 && !X::FOLD1) return cmul(bq, w48(q * m));
         else return wq(n0, q);
     };
-    __syncthreads();
+    // LATE: the F fold reads no staged table, so its global loads are issued
+    // before the barrier that publishes the twiddle tables (the table and input
+    // load latencies overlap instead of following one another)
+    constexpr bool LATE = kK4LateSync && !X::FOLD1 && !X::TMA && !X::SMEM_WM;
+    if constexpr (!LATE) __syncthreads();
+#ifdef FSCAN_K4_TWPOW
+    const float2* twk = p.tw_k;  // A/B: powers of four global-table reads (fft.cuh kTwPow)
+#else
     const fscan_fft::SmemTwRK twk{stw_rk, stw_k};
+#endif
     const float2 w3q = w3(q);
     float2 a[16];
     if constexpr (X::FOLD1) {
@@ -1109,6 +1145,7 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
             const float2 s = cadd(make_float2(u0.x, u0.y), cmul(w3q, make_float2(u1.x, u1.y)));
             a[m] = q ? cmul(wq_m(m, n0), s) : s;
         }
+        if constexpr (LATE) __syncthreads();
     }
     fft_regs<K, -1, true>(a, t, bufA, twk);  // transforms of a warp share a buffer group
 #pragma unroll
@@ -1171,6 +1208,109 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
             if (store) {
                 dst[y_at<N>(half - n0, kp)] = cadd(x0, cadd(x1, x2));
                 dst[y_at<N>(half - (n0 - K), kp)] = cadd(x0, cadd(cmul(w31, x1), cmul(w32, x2)));
+            }
+        }
+    }
+}
+
+// K4 with merged twiddles (N <= 512): the same transforms and combine as
+// xlat_cols_body, with every W_M factor either folded into the last FFT stage's
+// twiddles (fft.cuh SmemTwQF / SmemTwQI) or applied once per value:
+//   F_q: inputs W_M^{mTq} (x[n] + W_3^q x[n+K]), last stage F[r][3k+q];
+//   e_q: last stage conj(F[k][3r+q]), outputs W_M^{-16 r' q} — so e_q arrives
+//        pre-multiplied by the combine twiddle W_M^{-n q};
+//   combine: sum_q x_q and x_0 - (x_1 + x_2)/2 - i (sqrt 3/2)(x_1 - x_2).
+// The fold W_3^q product is two FMAs per component with per-thread constants.
+template <int N>
+__device__ __forceinline__ void xlat_cols_merged(const Params& p) {
+    constexpr int K = N / 2, H = 3 * K / 2;
+    using X = XColGeom<N>;
+    using G = typename X::G;
+    constexpr int T = G::T, COLS = X::COLS;
+    constexpr int R = K / 16, NB = 16 / R;  // last-stage radix and butterflies per thread
+    constexpr int QS = fscan_fft::kQS;
+    constexpr int half = N / 2 - 1;
+    static_assert(K >= 32 && K <= 256 && R * 16 == K, "two-stage K-point transforms");
+    extern __shared__ __align__(128) float smem[];
+    const int pair = blockIdx.y;
+    int tr, t;
+    G::map(threadIdx.x, tr, t);
+    const int c = tr / 3, q = tr % 3;
+    const int kp = blockIdx.x * COLS + c;
+    const int kq = kp <= H ? kp : H;  // the last block may hold fewer columns
+    const auto bufA = G::lay(smem, tr);
+    const auto bufB = G::lay(smem + G::FLOATS, tr);
+    const float4* src = p.fgt + ((size_t)pair * (H + 1) + kq) * N;
+    float2* tab = reinterpret_cast<float2*>(smem + X::FFT_FLOATS);  // [16][QS]
+    for (int i = threadIdx.x; i < 16 * 48; i += X::THREADS) tab[(i / 48) * QS + i % 48] = __ldg(p.tw_k4 + i);
+    // W_3^q = (c1, wi): s = x0 + W_3^q x1 in four FMAs
+    const float c1 = q ? -0.5f : 1.0f, wi = q == 0 ? 0.0f : (q == 1 ? -kS3 : kS3);
+    const float2* fq = tab + q;          // F[.][3k + q]
+#ifdef FSCAN_K4_MERGE_SMEMF
+    const float2* fin = tab + T * q;     // F[m][T q] = W_M^{m T q}
+    const float2* fout = tab + 16 * q;   // F[r'][16 q] = W_M^{16 r' q}
+    auto win = [&](int m) { return fin[m * QS]; };
+    auto wout = [&](int r) { return fout[r * QS]; };
+#else
+    // W_M^{m T q} = W_48^{m q} and W_M^{16 r' q} = W_48^{(16 / R) r' q} from the
+    // constant-bank table (two addresses per warp; shared-memory reads of them
+    // are 2-way bank conflicts: the two q of a warp sit 16 float2 apart)
+    auto win = [&](int m) { return w48(m * q); };
+    auto wout = [&](int r) { return w48((16 / R) * r * q); };
+#endif
+    auto fold = [&](float2 x0, float2 x1, int m) {
+        const float2 sv = make_float2(fmaf(-wi, x1.y, fmaf(c1, x1.x, x0.x)), fmaf(wi, x1.x, fmaf(c1, x1.y, x0.y)));
+        return cmul(sv, win(m));
+    };
+    if constexpr (!kK4LateSync) __syncthreads();
+    float2 a[16];
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+        const int n0 = t + m * T;
+        const float4 u0 = src[n0], u1 = src[n0 + K];
+        a[m] = fold(make_float2(u0.x, u0.y), make_float2(u1.x, u1.y), m);
+    }
+    if constexpr (kK4LateSync) __syncthreads();  // the table (the fold reads none of it)
+    fft_regs<K, -1, true>(a, t, bufA, fscan_fft::SmemTwQF{fq});
+#pragma unroll
+    for (int m = 0; m < 16; ++m) bufA.put(t + m * T, a[m]);  // park F_q (own slots)
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+        const int n0 = t + m * T;
+        const float4 u0 = src[n0], u1 = src[n0 + K];
+        a[m] = fold(make_float2(u0.z, u0.w), make_float2(u1.z, u1.w), m);
+    }
+    fft_regs<K, -1, true>(a, t, bufB, fscan_fft::SmemTwQF{fq});
+#pragma unroll
+    for (int m = 0; m < 16; ++m) a[m] = cmul(cconj(bufA.get(t + m * T)), a[m]);  // conj(F) G
+    if (p.phase) {  // opt-in phase correlation: X / |X| (0 where X = 0), SURVEY a21
+#pragma unroll
+        for (int m = 0; m < 16; ++m) {
+            const float mag = sqrtf(a[m].x * a[m].x + a[m].y * a[m].y);
+            const float inv = mag > 0.0f ? 1.0f / mag : 0.0f;
+            a[m] = make_float2(a[m].x * inv, a[m].y * inv);
+        }
+    }
+    fft_regs<K, +1, true>(a, t, bufB, fscan_fft::SmemTwQI{fq});
+#pragma unroll
+    for (int m = 0; m < 16; ++m) bufB.put(t + m * T, cmul(a[m], cconj(wout(m / NB))));
+    __syncthreads();
+    // radix-3 combine of the pre-twiddled e_q; group q handles slots m = q, q+3, ...
+    const auto e0 = G::lay(smem + G::FLOATS, 3 * c), e1 = G::lay(smem + G::FLOATS, 3 * c + 1),
+               e2 = G::lay(smem + G::FLOATS, 3 * c + 2);
+    float2* dst = p.zbuf + (size_t)pair * N * (H + 1);
+    const bool store = kp <= H;
+#pragma unroll
+    for (int j = 0; j < 6; ++j) {
+        const int m = q + 3 * j;
+        if (m < 16) {
+            const int n0 = t + m * T;
+            const float2 x0 = e0.get(n0), x1 = e1.get(n0), x2 = e2.get(n0);
+            const float2 sa = cadd(x1, x2), df = csub(x1, x2);
+            if (store) {
+                dst[y_at<N>(half - n0, kp)] = cadd(x0, sa);
+                dst[y_at<N>(half - (n0 - K), kp)] = make_float2(fmaf(kS3, df.y, fmaf(-0.5f, sa.x, x0.x)),
+                                                                fmaf(-kS3, df.x, fmaf(-0.5f, sa.y, x0.y)));
             }
         }
     }
@@ -1612,10 +1752,11 @@ cudaError_t xlat_cols(const Params& p, cudaStream_t s) {
     using X = XColGeom<N>;
     constexpr int H = 3 * N / 4;
     const dim3 grid((H + 1 + X::COLS - 1) / X::COLS, p.batch);
+    constexpr size_t SMEM = X::MERGE ? X::SMEM_MERGE : X::SMEM;
     auto go = [&](auto kernel) {
-        cudaError_t e = set_smem(kernel, X::SMEM);
+        cudaError_t e = set_smem(kernel, SMEM);
         if (e != cudaSuccess) return e;
-        kernel<<<grid, X::THREADS, X::SMEM, s>>>(p);
+        kernel<<<grid, X::THREADS, SMEM, s>>>(p);
         return cudaGetLastError();
     };
     if constexpr (X::MIN_BLOCKS > 0)

@@ -82,6 +82,7 @@ struct Params {
     const float2* tw_k2;  // exp(-2 pi i k / (K/2))
     const float2* tw_m;   // exp(-2 pi i k / M), M = 3N/2
     const float2* tw_rk;  // exp(-2 pi i r k / 256) at (r-1)*16 + k, r < 16, k < 16
+    const float2* tw_k4;  // K4 merged twiddles W_M^{a j} at a*48 + j, a < 16, j < 48 (fft.cuh SmemTwQF)
     const float* hann;    // N
     const int2* band;     // per centred row: [u_lo, u_hi] in band (empty: lo > hi)
     const PolarTap* taps; // [n_live][n_theta] (radius-major)
