@@ -693,13 +693,22 @@ __device__ __forceinline__ float2 wm(const float2* __restrict__ tw_m, int e) { r
 // F = (Z[k'] + conj Z[M-k'])/2, G = (Z[k'] - conj Z[M-k'])/2i, Z[3k+q] = E_q[k],
 // for k' in [0, M/2] are written transposed as fgt[k'][y].
 constexpr int kXThreads = 384;
+#ifdef FSCAN_K3_STASH_SOA
+constexpr bool kK3StashSoA = true;  // A/B: split re / im stash (rounds 1-2)
+#else
+constexpr bool kK3StashSoA = false;
+#endif
 
 template <int N>
 struct XRowGeom {
     using G = Geom<N / 2, kXThreads>;
     static constexpr int ROWS = G::PER_CTA / 3;
+    // stash: z = f~ + i g~r as float2 rows (one 64-bit access per cell on both
+    // sides; a half-warp touches 16 consecutive cells of one row, or the end of
+    // one row and the start of the next: conflict-free at any multiple-of-16
+    // stride). kK3StashSoA (A/B): split re / im float rows, padded every 32.
     static constexpr int SP0 = N + N / 32;
-    static constexpr int SP = (SP0 % 32 == 0) ? SP0 + 16 : SP0;  // stash row stride (floats)
+    static constexpr int SP = kK3StashSoA ? ((SP0 % 32 == 0) ? SP0 + 16 : SP0) : N;  // row stride (floats / float2)
     // the FFT exchange buffers alias the gather stash (dead once v[] is loaded):
     // ~50 KB per CTA, three CTAs per SM
     static constexpr size_t STASH = (size_t)2 * ROWS * SP;
@@ -749,8 +758,9 @@ __global__ void __launch_bounds__(kXThreads, 3) k_xlat_rows(Params p) {
     using G = typename X::G;
     constexpr int T = G::T, ROWS = X::ROWS, SP = X::SP;
     extern __shared__ __align__(128) float smem[];
-    float* st_re = smem;
-    float* st_im = smem + ROWS * SP;
+    [[maybe_unused]] float* st_re = smem;
+    [[maybe_unused]] float* st_im = smem + ROWS * SP;
+    [[maybe_unused]] float2* st2 = reinterpret_cast<float2*>(smem);
     float* xbase = smem;  // aliases the stash (see XRowGeom::SMEM)
     const int pair = blockIdx.y;
     const int y0 = blockIdx.x * ROWS;
@@ -837,9 +847,14 @@ __global__ void __launch_bounds__(kXThreads, 3) k_xlat_rows(Params p) {
             const int e = e0 + u * kXThreads;
             if (e < CELLS) {
                 const int yl = e / N, x = e % N;
-                const int a = yl * SP + x + (x >> 5);
-                st_re[a] = fv[u];
-                st_im[a] = bilerp(frs[u], fcs[u], tap[u][0], tap[u][1], tap[u][2], tap[u][3]);
+                const float gi = bilerp(frs[u], fcs[u], tap[u][0], tap[u][1], tap[u][2], tap[u][3]);
+                if constexpr (kK3StashSoA) {
+                    const int a = yl * SP + x + (x >> 5);
+                    st_re[a] = fv[u];
+                    st_im[a] = gi;
+                } else {
+                    st2[yl * SP + x] = make_float2(fv[u], gi);
+                }
             }
         }
     }
@@ -853,8 +868,16 @@ __global__ void __launch_bounds__(kXThreads, 3) k_xlat_rows(Params p) {
 #pragma unroll
         for (int m = 0; m < 16; ++m) {
             const int n0 = t + m * T, n1 = n0 + K;
-            const int a0 = yl * SP + n0 + (n0 >> 5), a1 = yl * SP + n1 + (n1 >> 5);
-            const float2 s = cadd(make_float2(st_re[a0], st_im[a0]), cmul(w3q, make_float2(st_re[a1], st_im[a1])));
+            float2 z0, z1;
+            if constexpr (kK3StashSoA) {
+                const int a0 = yl * SP + n0 + (n0 >> 5), a1 = yl * SP + n1 + (n1 >> 5);
+                z0 = make_float2(st_re[a0], st_im[a0]);
+                z1 = make_float2(st_re[a1], st_im[a1]);
+            } else {
+                z0 = st2[yl * SP + n0];
+                z1 = st2[yl * SP + n1];
+            }
+            const float2 s = cadd(z0, cmul(w3q, z1));
             v[m] = q ? cmul(wm(p.tw_m, n0 * q), s) : s;
         }
         __syncthreads();  // every stash read done before the exchange buffers are written
