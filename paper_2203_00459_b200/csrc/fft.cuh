@@ -258,13 +258,14 @@ struct Geom {
     }
 };
 
-// Split real/imag exchange layout of the column kernel K4 (two 32-bit
-// accesses per element: fewer live 64-bit operands keep K4 at 80 registers and
-// two CTAs per SM). W transforms interleaved element-wise (transform index =
-// lane % W fastest in the warp): addr = W*(i + i/16) + sub; W == 1: XOR of the
-// 5-bit offset inside each 32-float line by (line & 15) | bit3(line) << 4.
-// (A per-transform layout with the lane/T mapping of Geom removes the last
-// radix-3-combine conflicts but measured 4% slower in K4.)
+// Split real/imag exchange layout (rounds 1-2 of the column kernel K4; now an
+// A/B alternative, FSCAN_K4_F2_MIN): two 32-bit accesses per element, W
+// transforms interleaved element-wise (transform index = lane % W fastest in
+// the warp): addr = W*(i + i/16) + sub; W == 1: XOR of the 5-bit offset inside
+// each 32-float line by (line & 15) | bit3(line) << 4. It moves the same
+// shared-memory wavefronts as the float2 layout of Geom with twice the LSU
+// instructions; once K4 stopped being register-bound the float2 layout won
+// (ncu: MIO-throttle stalls on the exchange lines; C5 +5%, C4 +1%, C2 +2.6%).
 template <int W>
 struct LaySoA {
     float* re;

@@ -958,12 +958,16 @@ constexpr bool kK4LateSync = false;  // A/B: the table barrier before the first 
 #else
 constexpr bool kK4LateSync = true;
 #endif
-// kK4Merge (off: measured C4 +0.4% = noise, C2 -2% — the table costs N = 256 its
-// fourth CTA per SM; ncu: 8% fewer FP32 instructions, L1 busy 66 -> 81%)
-#ifdef FSCAN_K4_MERGE
-constexpr bool kK4Merge = true;  // A/B: twiddles merged into the last FFT stage (xlat_cols_merged)
+// kK4Merge: twiddles merged into the last FFT stage (xlat_cols_merged) at
+// N = 512: C4 +1.3% with the float2 exchange layout (a half-warp is one
+// transform, so every table read is conflict-free; with the split re/im
+// layout the two q of a half-warp made them 2-way conflicts and the merge
+// measured neutral). Not at N = 256: the table costs C2's kernel its fourth
+// CTA per SM (-1%).
+#ifdef FSCAN_K4_NOMERGE
+constexpr bool kK4Merge = false;  // A/B
 #else
-constexpr bool kK4Merge = false;
+constexpr bool kK4Merge = true;
 #endif
 
 template <int N>
@@ -980,10 +984,11 @@ struct XColGeom {
     // (outputs are stored from registers into the blocked Y layout, y_at; round
     // 1-2 staged them in an [N][COLS + 1] shared tile copied out row-major,
     // ~12% of K4's warp samples)
-    // split re/im exchange: with 64-bit accesses this kernel's allocation grows
-    // past two CTAs per SM (note: an explicit minBlocks=1 launch bound also
-    // changes ptxas' choice, 80 -> 167 registers)
-    // (FSCAN_K4_F2_MIN: float2 exchange buffers, one per transform, at N >= it)
+    // float2 exchange buffers, one per transform (Geom: the T lanes of a
+    // transform contiguous, a half-warp = one transform at N >= 512): one LSU
+    // instruction per exchanged value. FSCAN_K4_F2_MIN > N restores the split
+    // re/im layout of rounds 1-2 (GeomSoA), which issues twice the shared-memory
+    // instructions for the same wavefronts (MIO-throttle bound at N = 1024).
     using G = std::conditional_t<(N >= FSCAN_K4_F2_MIN), fscan_fft::Geom<N / 2, THREADS>,
                                  fscan_fft::GeomSoA<N / 2, THREADS>>;
     // kK4Tma (below N = 1024; off by default): the CTA's COLS columns of fgt (one
@@ -1022,7 +1027,7 @@ struct XColGeom {
     static constexpr bool FOLD1 = N >= 1024;
     // merged-twiddle path (xlat_cols_merged, two-stage K-point transforms):
     // the exchange buffers + the [16][kQS] table W_M^{a j}
-    static constexpr bool MERGE = kK4Merge && !FOLD1 && !TMA && N / 2 <= 256;
+    static constexpr bool MERGE = kK4Merge && !FOLD1 && !TMA && N == 512;
     static constexpr size_t SMEM_MERGE = (FFT_FLOATS + 2 * 16 * fscan_fft::kQS) * sizeof(float);
 };
 
