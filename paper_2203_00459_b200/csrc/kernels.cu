@@ -1089,8 +1089,30 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
     float2* stw_rk = reinterpret_cast<float2*>(smem + X::WORK_FLOATS);
     float2* stw_k = stw_rk + 240;
     float2* stw_m_s = stw_k + X::TW_LIN;
-    for (int i = threadIdx.x; i < 240; i += X::THREADS) stw_rk[i] = __ldg(p.tw_rk + i);
-    for (int i = threadIdx.x; i < X::TW_LIN; i += X::THREADS) stw_k[i] = __ldg(p.tw_k + i);
+    // PF: every table load issued up front into registers and stored after the
+    // first fold (a load -> store loop waits out one L2 round trip per trip)
+    constexpr bool PF = !X::SMEM_WM && !X::TMA;
+    constexpr int TE = 240 + X::TW_LIN, TPT = PF ? (TE + X::THREADS - 1) / X::THREADS : 1;
+    [[maybe_unused]] float2 tv[TPT];
+    if constexpr (PF) {
+#pragma unroll
+        for (int k = 0; k < TPT; ++k) {
+            const int i = threadIdx.x + k * X::THREADS;
+            if (TE % X::THREADS == 0 || i < TE) tv[k] = __ldg(i < 240 ? p.tw_rk + i : p.tw_k + (i - 240));
+        }
+    } else {
+        for (int i = threadIdx.x; i < 240; i += X::THREADS) stw_rk[i] = __ldg(p.tw_rk + i);
+        for (int i = threadIdx.x; i < X::TW_LIN; i += X::THREADS) stw_k[i] = __ldg(p.tw_k + i);
+    }
+    auto tw_store = [&]() {  // stw_k follows stw_rk
+        if constexpr (PF) {
+#pragma unroll
+            for (int k = 0; k < TPT; ++k) {
+                const int i = threadIdx.x + k * X::THREADS;
+                if (TE % X::THREADS == 0 || i < TE) stw_rk[i] = tv[k];
+            }
+        }
+    };
     if constexpr (X::SMEM_WM && X::SPLIT_WM) {
         for (int i = threadIdx.x; i < K; i += X::THREADS) {
             stw_m_s[i] = __ldg(p.tw_m + i);
@@ -1116,7 +1138,10 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
     // before the barrier that publishes the twiddle tables (the table and input
     // load latencies overlap instead of following one another)
     constexpr bool LATE = kK4LateSync && !X::FOLD1 && !X::TMA && !X::SMEM_WM;
-    if constexpr (!LATE) __syncthreads();
+    if constexpr (!LATE && !X::FOLD1) {
+        tw_store();
+        __syncthreads();
+    }
 #ifdef FSCAN_K4_TWPOW
     const float2* twk = p.tw_k;  // A/B: powers of four global-table reads (fft.cuh kTwPow)
 #else
@@ -1160,7 +1185,8 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
             fold(make_float2(u0.x, u0.y), make_float2(u1.x, u1.y), smem);
             fold(make_float2(u0.z, u0.w), make_float2(u1.z, u1.w), smem + G::FLOATS);
         }
-        __syncthreads();
+        tw_store();
+        __syncthreads();  // the folded inputs and the tables
 #pragma unroll
         for (int m = 0; m < 16; ++m) a[m] = bufA.get(t + m * T);
         __syncwarp();  // every input read before the transform's exchange writes
@@ -1173,7 +1199,10 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
             const float2 s = cadd(make_float2(u0.x, u0.y), cmul(w3q, make_float2(u1.x, u1.y)));
             a[m] = q ? cmul(wq_m(m, n0), s) : s;
         }
-        if constexpr (LATE) __syncthreads();
+        if constexpr (LATE) {
+            tw_store();
+            __syncthreads();
+        }
     }
     fft_regs<K, -1, true>(a, t, bufA, twk);  // transforms of a warp share a buffer group
 #pragma unroll
@@ -1270,27 +1299,27 @@ __device__ __forceinline__ void xlat_cols_merged(const Params& p) {
     const auto bufB = G::lay(smem + G::FLOATS, tr);
     const float4* src = p.fgt + ((size_t)pair * (H + 1) + kq) * N;
     float2* tab = reinterpret_cast<float2*>(smem + X::FFT_FLOATS);  // [16][QS]
-    for (int i = threadIdx.x; i < 16 * 48; i += X::THREADS) tab[(i / 48) * QS + i % 48] = __ldg(p.tw_k4 + i);
+    // the table's global loads are all issued first and stored to shared memory
+    // only after the first fold (a load -> store loop waited out one L2 round
+    // trip per iteration: ~15% of K4's warp samples)
+    constexpr int TE = 16 * 48, TPT = (TE + X::THREADS - 1) / X::THREADS;
+    float2 tv[TPT];
+#pragma unroll
+    for (int k = 0; k < TPT; ++k) {
+        const int i = threadIdx.x + k * X::THREADS;
+        if (TE % X::THREADS == 0 || i < TE) tv[k] = __ldg(p.tw_k4 + i);
+    }
     // W_3^q = (c1, wi): s = x0 + W_3^q x1 in four FMAs
     const float c1 = q ? -0.5f : 1.0f, wi = q == 0 ? 0.0f : (q == 1 ? -kS3 : kS3);
-    const float2* fq = tab + q;          // F[.][3k + q]
-#ifdef FSCAN_K4_MERGE_SMEMF
-    const float2* fin = tab + T * q;     // F[m][T q] = W_M^{m T q}
-    const float2* fout = tab + 16 * q;   // F[r'][16 q] = W_M^{16 r' q}
-    auto win = [&](int m) { return fin[m * QS]; };
-    auto wout = [&](int r) { return fout[r * QS]; };
-#else
+    const float2* fq = tab + q;  // F[.][3k + q]
     // W_M^{m T q} = W_48^{m q} and W_M^{16 r' q} = W_48^{(16 / R) r' q} from the
-    // constant-bank table (two addresses per warp; shared-memory reads of them
-    // are 2-way bank conflicts: the two q of a warp sit 16 float2 apart)
+    // constant-bank table (one address per half-warp)
     auto win = [&](int m) { return w48(m * q); };
     auto wout = [&](int r) { return w48((16 / R) * r * q); };
-#endif
     auto fold = [&](float2 x0, float2 x1, int m) {
         const float2 sv = make_float2(fmaf(-wi, x1.y, fmaf(c1, x1.x, x0.x)), fmaf(wi, x1.x, fmaf(c1, x1.y, x0.y)));
         return cmul(sv, win(m));
     };
-    if constexpr (!kK4LateSync) __syncthreads();
     float2 a[16];
 #pragma unroll
     for (int m = 0; m < 16; ++m) {
@@ -1298,7 +1327,12 @@ __device__ __forceinline__ void xlat_cols_merged(const Params& p) {
         const float4 u0 = src[n0], u1 = src[n0 + K];
         a[m] = fold(make_float2(u0.x, u0.y), make_float2(u1.x, u1.y), m);
     }
-    if constexpr (kK4LateSync) __syncthreads();  // the table (the fold reads none of it)
+#pragma unroll
+    for (int k = 0; k < TPT; ++k) {
+        const int i = threadIdx.x + k * X::THREADS;
+        if (TE % X::THREADS == 0 || i < TE) tab[(i / 48) * QS + i % 48] = tv[k];
+    }
+    __syncthreads();  // the table (the fold reads none of it)
     fft_regs<K, -1, true>(a, t, bufA, fscan_fft::SmemTwQF{fq});
 #pragma unroll
     for (int m = 0; m < 16; ++m) bufA.put(t + m * T, a[m]);  // park F_q (own slots)
