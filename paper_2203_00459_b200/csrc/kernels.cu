@@ -782,8 +782,12 @@ __global__ void __launch_bounds__(kXThreads, 3) k_xlat_rows(Params p) {
     const float* gt = p.gt + (size_t)src * N * N;
     const float c0f32 = EMB ? p.c0 : (N - 1) / 2.0f;  // exact (half-integer or integer)
     float2* srk = reinterpret_cast<float2*>(smem + X::WORK);  // ordered by the barrier after the gather
+    // the [r][k] table: loaded now, stored after the gather (a load -> store
+    // here would wait out an L2 round trip before the gather's first fetch)
+    static_assert(kXThreads >= 240, "one table entry per thread");
+    [[maybe_unused]] float2 rkv;
     if constexpr (X::RK)
-        for (int i = threadIdx.x; i < 240; i += kXThreads) srk[i] = __ldg(p.tw_rk + i);
+        if (threadIdx.x < 240) rkv = __ldg(p.tw_rk + threadIdx.x);
     const int nvalid = EMB ? p.n : N;
     // rotate_bilinear(g~, -theta); -theta == 0.0 returns g~ itself, which st = 0,
     // ct = 1 reproduce exactly (integer source coordinates, zero fractions)
@@ -858,6 +862,8 @@ __global__ void __launch_bounds__(kXThreads, 3) k_xlat_rows(Params p) {
             }
         }
     }
+    if constexpr (X::RK)
+        if (threadIdx.x < 240) srk[threadIdx.x] = rkv;
     __syncthreads();
     int tr, t;
     G::map(threadIdx.x, tr, t);
