@@ -21,6 +21,7 @@ using namespace fscan_detail;
 namespace {
 
 constexpr double kPi = 3.141592653589793;  // std::numbers::pi (geometry.hpp:11)
+constexpr int kHostSlots = 4;              // fscan_match_batch_host input staging ring
 constexpr int kMaxLanes = 8;               // concurrent chunk pipelines (FSCAN_LANES, default 3)
 #ifdef FSCAN_NO_TEX_GATHER
 constexpr bool kNoTexGather = true;  // A/B: K3 gathers with plain loads
@@ -43,8 +44,7 @@ struct Lane {
     double* theta_ws = nullptr;
     int* flags = nullptr;
     cudaTextureObject_t gtex = 0;  // K3 texture over gt (pow2 grids whose chunk fits one 2-D texture)
-    // host-API staging
-    float* in = nullptr;  // 4 grids x chunk
+    // host-API staging (the inputs go through fscan_ctx::hslot)
     float* cart = nullptr;  // K0 output (polar API): 2 grids x chunk
     void* k0tab = nullptr;  // K0 tap table of the last polar geometry (built on this lane's stream)
     float* chain_ms = nullptr;  // odometry: masked scans of a chunk (chunk + 2 grids)
@@ -128,6 +128,25 @@ struct fscan_ctx {
     bool graph_launched = false;   // graph_ev holds the last replay
     bool lanes_since_graph = false; // non-graph work was queued on the lanes since
     bool capturing = false;
+    // fscan_match_batch_host input staging: a ring of kHostSlots chunk buffers
+    // filled in order on one copy stream (`h2d`), each released by an event
+    // recorded after the chunk that read it; the copy of chunk k + 1 never waits
+    // for the compute of chunk k (with the inputs staged in the lane, the next
+    // copy of a lane queued behind its compute and the link idled between
+    // rounds of chunks)
+    struct HostSlot {
+        float* in = nullptr;
+        cudaEvent_t copied = nullptr, used = nullptr;
+        bool pending = false;  // `used` recorded and not yet waited on
+    };
+    HostSlot hslot[kHostSlots];
+    int hslot_chunk = 0;  // capacity of every slot (pairs)
+    cudaStream_t h2d = nullptr;
+    // pinned landing area of the per-chunk result rows: a device -> pageable
+    // copy is synchronous for the host thread, which then could not queue the
+    // next chunk's H2D copy until the previous chunk had finished
+    fscan_pair_result* hres = nullptr;
+    int hres_cap = 0;
 };
 
 namespace {
@@ -285,7 +304,6 @@ void free_lane(Lane& l) {
     cudaFree(l.prof);
     cudaFree(l.theta_ws);
     cudaFree(l.flags);
-    cudaFree(l.in);
     cudaFree(l.cart);
     cudaFree(l.k0tab);
     cudaFree(l.chain_ms);
@@ -338,12 +356,37 @@ fscan_status alloc_lane(fscan_ctx* ctx, Lane& l, int chunk) {
 }
 
 fscan_status alloc_host_staging(fscan_ctx* ctx, Lane& l, int chunk) {
-    if (l.in) return FSCAN_OK;
+    if (l.res) return FSCAN_OK;
     const size_t nn = (size_t)ctx->n * ctx->n;
-    CK(cudaMalloc(&l.in, 4 * nn * sizeof(float) * chunk));
     CK(cudaMalloc(&l.res, sizeof(fscan_pair_result) * chunk));
     CK(cudaMalloc(&l.tsurf, sizeof(double) * std::max(1, ctx->cfg.n_theta) * chunk));
     CK(cudaMalloc(&l.xsurf, nn * sizeof(float) * chunk));
+    return FSCAN_OK;
+}
+
+void free_host_slots(fscan_ctx* ctx) {
+    if (ctx->h2d) cudaStreamSynchronize(ctx->h2d);
+    for (auto& h : ctx->hslot) {
+        if (h.used) cudaEventSynchronize(h.used);
+        cudaFree(h.in);
+        if (h.copied) cudaEventDestroy(h.copied);
+        if (h.used) cudaEventDestroy(h.used);
+        h = {};
+    }
+    ctx->hslot_chunk = 0;
+}
+
+fscan_status alloc_host_slots(fscan_ctx* ctx, int chunk) {
+    if (ctx->hslot_chunk >= chunk) return FSCAN_OK;
+    free_host_slots(ctx);
+    if (!ctx->h2d) CK(cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking));
+    const size_t nn = (size_t)ctx->n * ctx->n;
+    for (auto& h : ctx->hslot) {
+        CK(cudaMalloc(&h.in, 4 * nn * sizeof(float) * chunk));
+        CK(cudaEventCreateWithFlags(&h.copied, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&h.used, cudaEventDisableTiming));
+    }
+    ctx->hslot_chunk = chunk;
     return FSCAN_OK;
 }
 
@@ -816,6 +859,9 @@ void fscan_ctx_destroy(fscan_ctx* ctx) {
     if (ctx->graph_ev) cudaEventDestroy(ctx->graph_ev);
     for (cudaEvent_t e : ctx->lane_sync)
         if (e) cudaEventDestroy(e);
+    free_host_slots(ctx);
+    if (ctx->h2d) cudaStreamDestroy(ctx->h2d);
+    if (ctx->hres) cudaFreeHost(ctx->hres);
     cudaFree(ctx->tw_n);
     cudaFree(ctx->tw_k);
     cudaFree(ctx->tw_k2);
@@ -853,7 +899,7 @@ fscan_status fscan_ctx_set_chunk(fscan_ctx* ctx, int pairs) {
         if (ctx->graph_launched) cudaEventSynchronize(ctx->graph_ev);
         for (Lane& l : LaneRange{ctx}) {
             cudaStreamSynchronize(l.stream);
-            const bool had_host = l.in != nullptr;
+            const bool had_host = l.res != nullptr;
             free_lane(l);
             fscan_status a = alloc_lane(ctx, l, pairs);
             if (a != FSCAN_OK) return a;
@@ -1168,28 +1214,44 @@ fscan_status fscan_match_batch_host(fscan_ctx* ctx, const float* f, const float*
         fscan_status a = alloc_host_staging(ctx, l, ctx->alloc_chunk);
         if (a != FSCAN_OK) return a;
     }
+    {
+        fscan_status a = alloc_host_slots(ctx, ctx->alloc_chunk);
+        if (a != FSCAN_OK) return a;
+    }
+    if (ctx->hres_cap < batch) {
+        if (ctx->hres) CK(cudaFreeHost(ctx->hres));
+        ctx->hres = nullptr;
+        ctx->hres_cap = 0;
+        CK(cudaMallocHost(&ctx->hres, sizeof(fscan_pair_result) * batch));
+        ctx->hres_cap = batch;
+    }
     // a graph replay of fscan_match_batch / fscan_odometry_batch on a user stream
     // may still be using the lane workspace: order the lanes after it
     if (ctx->graph_launched)
         for (Lane& l : LaneRange{ctx}) CK(cudaStreamWaitEvent(l.stream, ctx->graph_ev, 0));
     ctx->lanes_since_graph = true;
     ctx->launches_last = 0;
-    int li = 0;
-    // lane-alternating chunks: H2D(i+1) overlaps compute(i) on the other lane
-    for (int off = 0; off < batch; off += ctx->chunk, li = (li + 1) % ctx->nlanes) {
+    int li = 0, si = 0;
+    // chunks over the lanes; their inputs through the staging ring on the copy
+    // stream, so the H2D copies run back to back while the lanes compute
+    for (int off = 0; off < batch; off += ctx->chunk, li = (li + 1) % ctx->nlanes, si = (si + 1) % kHostSlots) {
         Lane& l = ctx->lanes_[li];
+        auto& hs = ctx->hslot[si];
         const int cnt = std::min(ctx->chunk, batch - off);
         cudaStream_t s = l.stream;
-        float* df = l.in;
-        float* dg = l.in + nn * cnt;
-        float* dmf = mf ? l.in + 2 * nn * cnt : nullptr;
-        float* dmg = mf ? l.in + 3 * nn * cnt : nullptr;
-        CK(cudaMemcpyAsync(df, f + off * nn, nn * cnt * sizeof(float), cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(dg, g + off * nn, nn * cnt * sizeof(float), cudaMemcpyHostToDevice, s));
+        if (hs.pending) CK(cudaStreamWaitEvent(ctx->h2d, hs.used, 0));
+        float* df = hs.in;
+        float* dg = hs.in + nn * cnt;
+        float* dmf = mf ? hs.in + 2 * nn * cnt : nullptr;
+        float* dmg = mf ? hs.in + 3 * nn * cnt : nullptr;
+        CK(cudaMemcpyAsync(df, f + off * nn, nn * cnt * sizeof(float), cudaMemcpyHostToDevice, ctx->h2d));
+        CK(cudaMemcpyAsync(dg, g + off * nn, nn * cnt * sizeof(float), cudaMemcpyHostToDevice, ctx->h2d));
         if (mf) {
-            CK(cudaMemcpyAsync(dmf, mf + off * nn, nn * cnt * sizeof(float), cudaMemcpyHostToDevice, s));
-            CK(cudaMemcpyAsync(dmg, mg + off * nn, nn * cnt * sizeof(float), cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(dmf, mf + off * nn, nn * cnt * sizeof(float), cudaMemcpyHostToDevice, ctx->h2d));
+            CK(cudaMemcpyAsync(dmg, mg + off * nn, nn * cnt * sizeof(float), cudaMemcpyHostToDevice, ctx->h2d));
         }
+        CK(cudaEventRecord(hs.copied, ctx->h2d));
+        CK(cudaStreamWaitEvent(s, hs.copied, 0));
         Params p = base_params(ctx, l, cnt, delta);
         p.f = df;
         p.g = dg;
@@ -1200,16 +1262,19 @@ fscan_status fscan_match_batch_host(fscan_ctx* ctx, const float* f, const float*
         p.xy_surf = xsurf ? l.xsurf : nullptr;
         fscan_status r = run_chunk(ctx, l, p, Stages::Full, &ctx->launches_last);
         if (r != FSCAN_OK) return r;
-        CK(cudaMemcpyAsync(out + off, l.res, sizeof(fscan_pair_result) * cnt, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(ctx->hres + off, l.res, sizeof(fscan_pair_result) * cnt, cudaMemcpyDeviceToHost, s));
         if (tsurf)
             CK(cudaMemcpyAsync(tsurf + (size_t)off * nt, l.tsurf, sizeof(double) * nt * cnt,
                                cudaMemcpyDeviceToHost, s));
         if (xsurf)
             CK(cudaMemcpyAsync(xsurf + off * nn, l.xsurf, sizeof(float) * nn * cnt, cudaMemcpyDeviceToHost, s));
-        // the staging buffers of this lane are reused two chunks later: the
-        // stream order already serialises that reuse.
+        CK(cudaEventRecord(hs.used, s));  // the slot is free once this chunk's kernels ran
+        hs.pending = true;
     }
     for (Lane& l : LaneRange{ctx}) CK(cudaStreamSynchronize(l.stream));
+    CK(cudaStreamSynchronize(ctx->h2d));
+    for (auto& h : ctx->hslot) h.pending = false;
+    std::memcpy(out, ctx->hres, sizeof(fscan_pair_result) * batch);
     for (int i = 0; i < batch; ++i)
         if (out[i].status != FSCAN_OK) {
             const fscan_status bad = (fscan_status)out[i].status;
