@@ -21,6 +21,11 @@ using namespace fscan_detail;
 namespace {
 
 constexpr double kPi = 3.141592653589793;  // std::numbers::pi (geometry.hpp:11)
+#ifndef FSCAN_PDL_DEFAULT
+#define FSCAN_PDL_DEFAULT 1
+#endif
+constexpr int kPdlDefault = FSCAN_PDL_DEFAULT;
+constexpr int kPdlChunk = 64;
 constexpr int kHostSlots = 4;              // fscan_match_batch_host input staging ring
 constexpr int kMaxLanes = 8;               // concurrent chunk pipelines (FSCAN_LANES, default 3)
 #ifdef FSCAN_NO_TEX_GATHER
@@ -67,6 +72,12 @@ struct fscan_ctx {
     int n_live = 0;
     int rot_col_blocks = 0;  // K1b column blocks (8 columns each) the polar taps read
     int phase = 0;           // opt-in phase correlation in the translation stage
+    // programmatic dependent launch of the pipeline kernels (kernels.cu
+    // pdl_enter): 0 off, 1 for chunks of at most kPdlChunk pairs, 2 always
+    // (FSCAN_PDL overrides). Default 1: one-pair latency 65.6 -> 61.5 us, C5
+    // (63-pair chunks) +1.3%; at C4's 126-pair chunks neutral to -0.3% (the
+    // early CTAs of the next kernel hold SM slots the other lanes could use)
+    int pdl_mode = kPdlDefault;
     // grid geometry: np = n for powers of two; otherwise the
     // rotation stage runs Bluestein DFTs of length bs_L at n and the
     // translation stage runs at np = 2^k >= n + 1 on zero-embedded scans
@@ -395,6 +406,7 @@ Params base_params(fscan_ctx* ctx, Lane& l, int batch, double delta) {
     p.n = ctx->n;
     p.np = ctx->np;
     p.embed = ctx->np != ctx->n;
+    p.pdl = ctx->pdl_mode == 2 || (ctx->pdl_mode == 1 && batch <= kPdlChunk);
     p.c0 = (float)((ctx->n - 1) / 2.0);
     p.win_off = (ctx->np / 2 - 1) - (ctx->n - 1) / 2;
     p.nw = ctx->nw;
@@ -810,6 +822,7 @@ fscan_status fscan_ctx_create(int device, const fscan_config* cfg_in, int max_ba
     // override the defaults (3 lanes, ~2 GiB of workspace per lane; 3 lanes
     // measured +0.9% over 2 at C4, 4-8 lanes or other chunk sizes no better)
     if (const char* e = std::getenv("FSCAN_LANES")) ctx->nlanes = std::clamp(std::atoi(e), 1, kMaxLanes);
+    if (const char* e = std::getenv("FSCAN_PDL")) ctx->pdl_mode = std::clamp(std::atoi(e), 0, 2);
     const double per_pair = (double)n * n * (8 + 4 + 8) + (double)n * (3 * n / 4 + 1) * 16;
     // ~2 GiB of workspace per lane: 126 pairs at N = 512 (then the texture cap
     // below), 63 at N = 1024 (C5 +2% over 1 GiB / 31 pairs: larger grids, and K2b

@@ -45,6 +45,24 @@ namespace {
 
 // one-shot mbarrier + TMA bulk copy global -> shared (cp.async.bulk)
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+// Programmatic dependent launch (griddepcontrol, sm_90+): the pipeline kernels
+// of a chunk are launched with programmatic stream serialisation when the
+// context asks for it (Params::pdl), so a kernel's CTAs are scheduled while its
+// predecessor on the stream drains instead of after it has completed and the
+// launch has gone through the front end. pdl_wait() blocks until the
+// predecessor grid has completed and its writes are visible: every read of data
+// another kernel produced, and every global write, comes after it (only kernel
+// parameters and the context's constant tables are read before). pdl_trigger()
+// lets this grid's own dependent launch once every CTA of this grid runs
+// (after pdl_wait, so at most one grid per stream is waiting). Both are no-ops
+// for a launch without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_enter() {
+    pdl_wait();
+    pdl_trigger();
+}
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -117,6 +135,7 @@ __device__ __forceinline__ const float2* tile_at(const float2* m, int n, int r, 
 // z = f~w + i g~w.
 template <int N>
 __global__ void FSCAN_K1A_BOUNDS k_rot_rows(Params p) {
+    pdl_enter();
     using G = RowG<N>;
     constexpr int T = G::T;
     extern __shared__ float smem[];
@@ -203,6 +222,7 @@ __host__ __device__ constexpr int k1b_u() {
 
 template <int N>
 __global__ void __launch_bounds__(N / 16 * 2 * k1b_u<N>()) k_rot_cols(Params p) {
+    pdl_enter();
     constexpr int U = k1b_u<N>(), CW = 2 * U;  // CW interleaved transforms per CTA
     constexpr int T = N / 16;
     constexpr int THREADS = T * CW;
@@ -336,6 +356,7 @@ __device__ __forceinline__ void gather_sums(const Params& p, const float2* m, in
 #endif
 template <int PB>
 __global__ void __launch_bounds__(kGatherThreads) k_rot_gather_multi(Params p) {
+    pdl_enter();
     const int pair0 = blockIdx.y * PB;
     const int nt = p.n_theta, n = p.n, n_live = p.n_live;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -395,6 +416,7 @@ __global__ void __launch_bounds__(kGatherThreads) k_rot_gather_multi(Params p) {
 }
 
 __global__ void __launch_bounds__(kGatherThreads) k_rot_gather(Params p) {
+    pdl_enter();
     const int pair = blockIdx.y;
     const int nt = p.n_theta;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -535,6 +557,7 @@ __device__ void polar_finish(const Params& p, int pair, const double* s, double*
 
 // K2b: angular correlation of the profiles, hard + soft argmax over theta.
 __global__ void __launch_bounds__(kPolarThreads) k_rot_polar(Params p) {
+    pdl_enter();
     extern __shared__ double dsm[];
     const int pair = blockIdx.x;
     const int nt = p.n_theta, L = p.L;
@@ -599,6 +622,7 @@ __global__ void __launch_bounds__(kPolarThreads) k_rot_polar(Params p) {
 // of lag blocks and writes their scores to theta_ws; k_rot_polar_fin then runs
 // the argmaxes per pair.
 __global__ void __launch_bounds__(kPolarThreads) k_rot_polar_part(Params p, int S) {
+    pdl_enter();
     extern __shared__ double dsm[];
     const int pair = blockIdx.x / S, part_id = blockIdx.x % S;
     const int nt = p.n_theta, L = p.L;
@@ -636,6 +660,7 @@ __global__ void __launch_bounds__(kPolarThreads) k_rot_polar_part(Params p, int 
 }
 
 __global__ void __launch_bounds__(kPolarThreads) k_rot_polar_fin(Params p) {
+    pdl_enter();
     extern __shared__ double dsm[];
     const int pair = blockIdx.x, nt = p.n_theta;
     double* s = dsm;
@@ -762,6 +787,14 @@ __global__ void __launch_bounds__(kXThreads, 3) k_xlat_rows(Params p) {
     [[maybe_unused]] float* st_im = smem + ROWS * SP;
     [[maybe_unused]] float2* st2 = reinterpret_cast<float2*>(smem);
     float* xbase = smem;  // aliases the stash (see XRowGeom::SMEM)
+    // the [r][k] table (a constant of the context): loaded before the
+    // dependency wait, stored after the gather (a load -> store here would wait
+    // out an L2 round trip before the gather's first fetch)
+    static_assert(kXThreads >= 240, "one table entry per thread");
+    [[maybe_unused]] float2 rkv;
+    if constexpr (X::RK)
+        if (threadIdx.x < 240) rkv = __ldg(p.tw_rk + threadIdx.x);
+    pdl_enter();
     const int pair = blockIdx.y;
     const int y0 = blockIdx.x * ROWS;
     const RotState rs = p.rot[pair];
@@ -782,12 +815,6 @@ __global__ void __launch_bounds__(kXThreads, 3) k_xlat_rows(Params p) {
     const float* gt = p.gt + (size_t)src * N * N;
     const float c0f32 = EMB ? p.c0 : (N - 1) / 2.0f;  // exact (half-integer or integer)
     float2* srk = reinterpret_cast<float2*>(smem + X::WORK);  // ordered by the barrier after the gather
-    // the [r][k] table: loaded now, stored after the gather (a load -> store
-    // here would wait out an L2 round trip before the gather's first fetch)
-    static_assert(kXThreads >= 240, "one table entry per thread");
-    [[maybe_unused]] float2 rkv;
-    if constexpr (X::RK)
-        if (threadIdx.x < 240) rkv = __ldg(p.tw_rk + threadIdx.x);
     const int nvalid = EMB ? p.n : N;
     // rotate_bilinear(g~, -theta); -theta == 0.0 returns g~ itself, which st = 0,
     // ct = 1 reproduce exactly (integer source coordinates, zero fractions)
@@ -1081,6 +1108,7 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
     const auto bufB = G::lay(smem + G::FLOATS, tr);
     const float4* src = p.fgt + ((size_t)pair * (H + 1) + kq) * N;
     __shared__ uint64_t mbar;
+    if constexpr (X::TMA) pdl_enter();  // (otherwise after the constant tables' loads below)
     if constexpr (X::TMA) {  // the block's columns: one bulk copy, read by both folds
         const int ncols_in = min(COLS, H + 1 - (int)blockIdx.x * COLS);
         if (threadIdx.x == 0) {
@@ -1140,6 +1168,7 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
         if constexpr (kK4W48 && !X::FOLD1) return cmul(bq, w48(q * m));
         else return wq(n0, q);
     };
+    if constexpr (!X::TMA) pdl_enter();
     // LATE: the F fold reads no staged table, so its global loads are issued
     // before the barrier that publishes the twiddle tables (the table and input
     // load latencies overlap instead of following one another)
@@ -1315,6 +1344,7 @@ __device__ __forceinline__ void xlat_cols_merged(const Params& p) {
         const int i = threadIdx.x + k * X::THREADS;
         if (TE % X::THREADS == 0 || i < TE) tv[k] = __ldg(p.tw_k4 + i);
     }
+    pdl_enter();
     // W_3^q = (c1, wi): s = x0 + W_3^q x1 in four FMAs
     const float c1 = q ? -0.5f : 1.0f, wi = q == 0 ? 0.0f : (q == 1 ? -kS3 : kS3);
     const float2* fq = tab + q;  // F[.][3k + q]
@@ -1427,6 +1457,7 @@ struct XOutGeom {
 // the window out).
 template <int N, bool EMB>
 __global__ void __launch_bounds__(XOutGeom<N>::THREADS) k_xlat_out(Params p) {
+    pdl_enter();
     constexpr int K = N / 2, M = 3 * K, H = M / 2;
     using X = XOutGeom<N>;
     using G = typename X::G;
@@ -1578,6 +1609,7 @@ __device__ __forceinline__ double block_max(double v, double* sh) {
 }
 
 __global__ void __launch_bounds__(kFinThreads) k_finalize(Params p, int nparts) {
+    pdl_enter();
     __shared__ double sh[kFinThreads / 32];
     __shared__ double sh3[3 * (kFinThreads / 32)];
     __shared__ float pk_v;
@@ -1779,13 +1811,30 @@ cudaError_t set_smem(K kernel, size_t bytes) {
         default: return cudaErrorInvalidValue;    \
     }
 
+// Launch of a pipeline kernel (one that starts with pdl_enter / pdl_wait):
+// with programmatic stream serialisation when the context asks for it.
+template <typename... KA, typename... A>
+cudaError_t launch_k(void (*kernel)(KA...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, const Params& p,
+                     A... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = p.pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 template <int N>
 cudaError_t rot_rows(const Params& p, cudaStream_t s) {
     const size_t sm = (size_t)RowG<N>::FLOATS * sizeof(float);
     cudaError_t e = set_smem(k_rot_rows<N>, sm);
     if (e != cudaSuccess) return e;
-    k_rot_rows<N><<<dim3(N / RowG<N>::PER_CTA, p.batch), kRowThreads, sm, s>>>(p);
-    return cudaGetLastError();
+    return launch_k(k_rot_rows<N>, dim3(N / RowG<N>::PER_CTA, p.batch), dim3(kRowThreads), sm, s, p, p);
 }
 
 template <int N>
@@ -1794,8 +1843,7 @@ cudaError_t rot_cols(const Params& p, cudaStream_t s) {
     const size_t sm = (size_t)part_floats<N, 2 * U>() * sizeof(float);
     cudaError_t e = set_smem(k_rot_cols<N>, sm);
     if (e != cudaSuccess) return e;
-    k_rot_cols<N><<<dim3(p.zcols / U, p.batch), N / 16 * 2 * U, sm, s>>>(p);
-    return cudaGetLastError();
+    return launch_k(k_rot_cols<N>, dim3(p.zcols / U, p.batch), dim3(N / 16 * 2 * U), sm, s, p, p);
 }
 
 template <int N>
@@ -1805,8 +1853,7 @@ cudaError_t xlat_rows(const Params& p, cudaStream_t s) {
     auto go = [&](auto kernel) {
         cudaError_t e = set_smem(kernel, X::SMEM);
         if (e != cudaSuccess) return e;
-        kernel<<<grid, kXThreads, X::SMEM, s>>>(p);
-        return cudaGetLastError();
+        return launch_k(kernel, grid, dim3(kXThreads), X::SMEM, s, p, p);
     };
     if (p.src_div != 1)  // exhaustive search
         return p.embed ? go(k_xlat_rows<N, true, true>) : go(k_xlat_rows<N, true, false>);
@@ -1824,8 +1871,7 @@ cudaError_t xlat_cols(const Params& p, cudaStream_t s) {
     auto go = [&](auto kernel) {
         cudaError_t e = set_smem(kernel, SMEM);
         if (e != cudaSuccess) return e;
-        kernel<<<grid, X::THREADS, SMEM, s>>>(p);
-        return cudaGetLastError();
+        return launch_k(kernel, grid, dim3(X::THREADS), SMEM, s, p, p);
     };
     if constexpr (X::MIN_BLOCKS > 0)
         return go(k_xlat_cols_mb<N, (X::MIN_BLOCKS > 0 ? X::MIN_BLOCKS : 1)>);
@@ -1840,8 +1886,7 @@ cudaError_t xlat_out(const Params& p, cudaStream_t s) {
     auto go = [&](auto kernel) {
         cudaError_t e = set_smem(kernel, X::SMEM);
         if (e != cudaSuccess) return e;
-        kernel<<<grid, X::THREADS, X::SMEM, s>>>(p);
-        return cudaGetLastError();
+        return launch_k(kernel, grid, dim3(X::THREADS), X::SMEM, s, p, p);
     };
     return p.embed ? go(k_xlat_out<N, true>) : go(k_xlat_out<N, false>);
 }
@@ -1869,13 +1914,12 @@ cudaError_t launch_rot_gather(const Params& p, cudaStream_t s) {
     if (p.n_theta == 1) return cudaSuccess;
     if (FSCAN_K2A_PB > 1 && !p.chain) {
         constexpr int PB = FSCAN_K2A_PB > 1 ? FSCAN_K2A_PB : 2;
-        k_rot_gather_multi<PB><<<dim3((p.n_theta + kGatherThreads / 4 - 1) / (kGatherThreads / 4),
-                                      (p.batch + PB - 1) / PB),
-                                 kGatherThreads, 0, s>>>(p);
-        return cudaGetLastError();
+        return launch_k(k_rot_gather_multi<PB>,
+                        dim3((p.n_theta + kGatherThreads / 4 - 1) / (kGatherThreads / 4), (p.batch + PB - 1) / PB),
+                        dim3(kGatherThreads), 0, s, p, p);
     }
-    k_rot_gather<<<dim3((p.n_theta + kGatherThreads / 4 - 1) / (kGatherThreads / 4), p.batch), kGatherThreads, 0, s>>>(p);
-    return cudaGetLastError();
+    return launch_k(k_rot_gather, dim3((p.n_theta + kGatherThreads / 4 - 1) / (kGatherThreads / 4), p.batch),
+                    dim3(kGatherThreads), 0, s, p, p);
 }
 
 // CTAs per pair for K2b: one when the batch fills the GPU, else up to 16
@@ -1896,20 +1940,18 @@ cudaError_t launch_rot_polar(const Params& p, cudaStream_t s) {
                           sizeof(double);
         cudaError_t e = set_smem(k_rot_polar_part, sm);
         if (e != cudaSuccess) return e;
-        k_rot_polar_part<<<p.batch * S, kPolarThreads, sm, s>>>(p, S);
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        if ((e = launch_k(k_rot_polar_part, dim3(p.batch * S), dim3(kPolarThreads), sm, s, p, p, S)) != cudaSuccess)
+            return e;
         const size_t fm = (size_t)(p.n_theta + 32) * sizeof(double) + 32 * sizeof(int);
         if ((e = set_smem(k_rot_polar_fin, fm)) != cudaSuccess) return e;
-        k_rot_polar_fin<<<p.batch, kPolarThreads, fm, s>>>(p);
-        return cudaGetLastError();
+        return launch_k(k_rot_polar_fin, dim3(p.batch), dim3(kPolarThreads), fm, s, p, p);
     }
     const size_t sm = (size_t)(p.L + bx_len(p.L, p.n_theta) + p.n_theta * (1 + polar_parts(p.n_theta)) + 32) *
                           sizeof(double) +
                       32 * sizeof(int);
     cudaError_t e = set_smem(k_rot_polar, sm);
     if (e != cudaSuccess) return e;
-    k_rot_polar<<<p.batch, kPolarThreads, sm, s>>>(p);
-    return cudaGetLastError();
+    return launch_k(k_rot_polar, dim3(p.batch), dim3(kPolarThreads), sm, s, p, p);
 }
 
 cudaError_t launch_theta_in(const Params& p, cudaStream_t s) {
@@ -1918,8 +1960,7 @@ cudaError_t launch_theta_in(const Params& p, cudaStream_t s) {
 }
 
 cudaError_t launch_finalize(const Params& p, cudaStream_t s) {
-    k_finalize<<<p.batch, kFinThreads, 0, s>>>(p, p.np / rows_per_block_out(p.np));
-    return cudaGetLastError();
+    return launch_k(k_finalize, dim3(p.batch), dim3(kFinThreads), 0, s, p, p, p.np / rows_per_block_out(p.np));
 }
 
 cudaError_t launch_mag_unpack(const Params& p, cudaStream_t s) {

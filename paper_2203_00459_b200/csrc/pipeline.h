@@ -122,6 +122,7 @@ struct Params {
     float c0;
     int win_off;
     int embed;                // 1: translation stage embedded (n < np)
+    int pdl;                  // 1: pipeline kernels launched with programmatic stream serialisation
     int nw;                   // half-plane width W = n - n/2 (u in [0, W))
     long long mag_plane;      // float2 per (|F|,|G|) tile set: n * 8 * ceil(W / 8)
     int bs_L;                 // Bluestein transform length (0: pow2 fast path)
