@@ -704,6 +704,21 @@ __device__ __forceinline__ float2 w3(int q) {  // W_3^q = exp(-2 pi i q / 3)
     return q == 0 ? make_float2(1.f, 0.f) : (q == 1 ? make_float2(-0.5f, -kS3) : make_float2(-0.5f, kS3));
 }
 
+// K4 twiddles W_M^{q n0} for n0 = t + m T (T = K/16, so W_M^T = W_48):
+// W_M^{q t} (one global-table read per thread) times W_48^{q m}, a
+// constant-bank table (two distinct q per warp: at most two addresses per
+// LDC). No W_M table is staged in shared memory (FSCAN_K4_TABLES restores the
+// staged M-entry table for A/B runs).
+__constant__ float kW48re[48] = {1.0f, 0.9914448857307434f, 0.9659258127212524f, 0.9238795042037964f, 0.8660253882408142f, 0.7933533191680908f, 0.7071067690849304f, 0.6087614297866821f, 0.5f, 0.3826834261417389f, 0.258819043636322f, 0.13052618503570557f, 0.0f, -0.13052618503570557f, -0.258819043636322f, -0.3826834261417389f, -0.5f, -0.6087614297866821f, -0.7071067690849304f, -0.7933533191680908f, -0.8660253882408142f, -0.9238795042037964f, -0.9659258127212524f, -0.9914448857307434f, -1.0f, -0.9914448857307434f, -0.9659258127212524f, -0.9238795042037964f, -0.8660253882408142f, -0.7933533191680908f, -0.7071067690849304f, -0.6087614297866821f, -0.5f, -0.3826834261417389f, -0.258819043636322f, -0.13052618503570557f, 0.0f, 0.13052618503570557f, 0.258819043636322f, 0.3826834261417389f, 0.5f, 0.6087614297866821f, 0.7071067690849304f, 0.7933533191680908f, 0.8660253882408142f, 0.9238795042037964f, 0.9659258127212524f, 0.9914448857307434f};
+__constant__ float kW48im[48] = {0.0f, -0.13052618503570557f, -0.258819043636322f, -0.3826834261417389f, -0.5f, -0.6087614297866821f, -0.7071067690849304f, -0.7933533191680908f, -0.8660253882408142f, -0.9238795042037964f, -0.9659258127212524f, -0.9914448857307434f, -1.0f, -0.9914448857307434f, -0.9659258127212524f, -0.9238795042037964f, -0.8660253882408142f, -0.7933533191680908f, -0.7071067690849304f, -0.6087614297866821f, -0.5f, -0.3826834261417389f, -0.258819043636322f, -0.13052618503570557f, 0.0f, 0.13052618503570557f, 0.258819043636322f, 0.3826834261417389f, 0.5f, 0.6087614297866821f, 0.7071067690849304f, 0.7933533191680908f, 0.8660253882408142f, 0.9238795042037964f, 0.9659258127212524f, 0.9914448857307434f, 1.0f, 0.9914448857307434f, 0.9659258127212524f, 0.9238795042037964f, 0.8660253882408142f, 0.7933533191680908f, 0.7071067690849304f, 0.6087614297866821f, 0.5f, 0.3826834261417389f, 0.258819043636322f, 0.13052618503570557f};
+
+__device__ __forceinline__ float2 w48(int k) { return make_float2(kW48re[k], kW48im[k]); }  // k < 48
+
+// W_32^m (m < 16), for K5's input twiddles (see k_xlat_out)
+__constant__ float kW32re[16] = {1.0f, 0.9807852506637573f, 0.9238795042037964f, 0.8314695954322815f, 0.7071067690849304f, 0.5555702447891235f, 0.3826834261417389f, 0.19509032368659973f, 0.0f, -0.19509032368659973f, -0.3826834261417389f, -0.5555702447891235f, -0.7071067690849304f, -0.8314695954322815f, -0.9238795042037964f, -0.9807852506637573f};
+__constant__ float kW32im[16] = {0.0f, -0.19509032368659973f, -0.3826834261417389f, -0.5555702447891235f, -0.7071067690849304f, -0.8314695954322815f, -0.9238795042037964f, -0.9807852506637573f, -1.0f, -0.9807852506637573f, -0.9238795042037964f, -0.8314695954322815f, -0.7071067690849304f, -0.5555702447891235f, -0.3826834261417389f, -0.19509032368659973f};
+__device__ __forceinline__ float2 w32(int k) { return make_float2(kW32re[k], kW32im[k]); }  // k < 16
+
 // W_M^e for 0 <= e < M (every caller passes a reduced exponent)
 __device__ __forceinline__ float2 wm(const float2* __restrict__ tw_m, int e) { return __ldg(tw_m + e); }
 
@@ -718,6 +733,11 @@ __device__ __forceinline__ float2 wm(const float2* __restrict__ tw_m, int e) { r
 // F = (Z[k'] + conj Z[M-k'])/2, G = (Z[k'] - conj Z[M-k'])/2i, Z[3k+q] = E_q[k],
 // for k' in [0, M/2] are written transposed as fgt[k'][y].
 constexpr int kXThreads = 384;
+#ifdef FSCAN_K3_TW_TABLE
+constexpr bool kK3TwTable = true;  // A/B: fold twiddles read from the W_M table per element
+#else
+constexpr bool kK3TwTable = false;
+#endif
 #ifdef FSCAN_K3_STASH_SOA
 constexpr bool kK3StashSoA = true;  // A/B: split re / im stash (rounds 1-2)
 #else
@@ -897,6 +917,10 @@ __global__ void __launch_bounds__(kXThreads, 3) k_xlat_rows(Params p) {
     const int yl = tr / 3, q = tr % 3;
     {
         const float2 w3q = w3(q);
+        // W_M^{q n0}, n0 = t + m T (M = 48 T): the thread's base W_M^{q t} times
+        // W_48^{q m} from the constant bank (a scattered table read per element
+        // cost an L1 wavefront per 16 bytes)
+        const float2 bq = kK3TwTable ? make_float2(1.f, 0.f) : wm(p.tw_m, q * t);
         float2 v[16];
 #pragma unroll
         for (int m = 0; m < 16; ++m) {
@@ -911,7 +935,10 @@ __global__ void __launch_bounds__(kXThreads, 3) k_xlat_rows(Params p) {
                 z1 = st2[yl * SP + n1];
             }
             const float2 s = cadd(z0, cmul(w3q, z1));
-            v[m] = q ? cmul(wm(p.tw_m, n0 * q), s) : s;
+            if constexpr (kK3TwTable)
+                v[m] = q ? cmul(wm(p.tw_m, n0 * q), s) : s;
+            else
+                v[m] = cmul(cmul(bq, w48(q * m)), s);
         }
         __syncthreads();  // every stash read done before the exchange buffers are written
         const auto b = G::lay(xbase, tr);
@@ -956,15 +983,6 @@ constexpr bool kK4Tma = true;  // A/B: the block's fgt columns by one TMA bulk c
 constexpr bool kK4Tma = false;
 #endif
 
-// K4 twiddles W_M^{q n0} for n0 = t + m T (T = K/16, so W_M^T = W_48):
-// W_M^{q t} (one global-table read per thread) times W_48^{q m}, a
-// constant-bank table (two distinct q per warp: at most two addresses per
-// LDC). No W_M table is staged in shared memory (FSCAN_K4_TABLES restores the
-// staged M-entry table for A/B runs).
-__constant__ float kW48re[48] = {1.0f, 0.9914448857307434f, 0.9659258127212524f, 0.9238795042037964f, 0.8660253882408142f, 0.7933533191680908f, 0.7071067690849304f, 0.6087614297866821f, 0.5f, 0.3826834261417389f, 0.258819043636322f, 0.13052618503570557f, 0.0f, -0.13052618503570557f, -0.258819043636322f, -0.3826834261417389f, -0.5f, -0.6087614297866821f, -0.7071067690849304f, -0.7933533191680908f, -0.8660253882408142f, -0.9238795042037964f, -0.9659258127212524f, -0.9914448857307434f, -1.0f, -0.9914448857307434f, -0.9659258127212524f, -0.9238795042037964f, -0.8660253882408142f, -0.7933533191680908f, -0.7071067690849304f, -0.6087614297866821f, -0.5f, -0.3826834261417389f, -0.258819043636322f, -0.13052618503570557f, 0.0f, 0.13052618503570557f, 0.258819043636322f, 0.3826834261417389f, 0.5f, 0.6087614297866821f, 0.7071067690849304f, 0.7933533191680908f, 0.8660253882408142f, 0.9238795042037964f, 0.9659258127212524f, 0.9914448857307434f};
-__constant__ float kW48im[48] = {0.0f, -0.13052618503570557f, -0.258819043636322f, -0.3826834261417389f, -0.5f, -0.6087614297866821f, -0.7071067690849304f, -0.7933533191680908f, -0.8660253882408142f, -0.9238795042037964f, -0.9659258127212524f, -0.9914448857307434f, -1.0f, -0.9914448857307434f, -0.9659258127212524f, -0.9238795042037964f, -0.8660253882408142f, -0.7933533191680908f, -0.7071067690849304f, -0.6087614297866821f, -0.5f, -0.3826834261417389f, -0.258819043636322f, -0.13052618503570557f, 0.0f, 0.13052618503570557f, 0.258819043636322f, 0.3826834261417389f, 0.5f, 0.6087614297866821f, 0.7071067690849304f, 0.7933533191680908f, 0.8660253882408142f, 0.9238795042037964f, 0.9659258127212524f, 0.9914448857307434f, 1.0f, 0.9914448857307434f, 0.9659258127212524f, 0.9238795042037964f, 0.8660253882408142f, 0.7933533191680908f, 0.7071067690849304f, 0.6087614297866821f, 0.5f, 0.3826834261417389f, 0.258819043636322f, 0.13052618503570557f};
-
-__device__ __forceinline__ float2 w48(int k) { return make_float2(kW48re[k], kW48im[k]); }  // k < 48
 #ifdef FSCAN_K4_TABLES
 constexpr bool kK4W48 = false;
 #else
@@ -1427,6 +1445,11 @@ constexpr bool kK5QMajor = false;  // A/B: transforms ordered row-major (3 rl + 
 #else
 constexpr bool kK5QMajor = true;
 #endif
+#ifdef FSCAN_K5_TW_TABLE
+constexpr bool kK5TwTable = true;  // A/B: input / combine twiddles read from the W_M table per element
+#else
+constexpr bool kK5TwTable = false;
+#endif
 #ifdef FSCAN_K5_LDG
 constexpr bool kK5Tma = false;  // A/B: every thread loads its Y elements from global
 #else
@@ -1491,13 +1514,18 @@ __global__ void __launch_bounds__(XOutGeom<N>::THREADS) k_xlat_out(Params p) {
             yblk = reinterpret_cast<const float2*>(smem);
         }
         auto y = [&](int k) { return yblk[k * ROWS + (rl ^ y_swz(ROWS, k))]; };  // Y[i][k]
+        // W_M^k, k = 3 (t + m T) + q (M = 96 T): the thread's base W_M^{3t+q}
+        // times W_32^m, a compile-time constant-bank address (kK5TwTable: one
+        // scattered W_M table read per element, ~40% of K5's L1 wavefronts)
+        const float2 bk = kK5TwTable ? make_float2(1.f, 0.f) : wm(p.tw_m, 3 * t + q);
         float2 v[16];
 #pragma unroll
         for (int m = 0; m < 16; ++m) {
             const int k = 3 * (t + m * T) + q;
             const float2 a = y(k), b = cconj(y(H - k));
             const float2 A = cadd(a, b);
-            const float2 B = cmul(csub(a, b), cconj(wm(p.tw_m, k)));
+            const float2 wk = kK5TwTable ? wm(p.tw_m, k) : cmul(bk, w32(m));
+            const float2 B = cmul(csub(a, b), cconj(wk));
             v[m] = make_float2(A.x - B.y, A.y + B.x);  // A + iB
         }
         if constexpr (kK5Tma) __syncthreads();  // Y reads done before the exchange reuses the bytes
@@ -1524,14 +1552,19 @@ __global__ void __launch_bounds__(XOutGeom<N>::THREADS) k_xlat_out(Params p) {
     auto tr_of = [&](int qq) { return kK5QMajor ? qq * ROWS + rl : 3 * rl + qq; };
     const auto e0 = G::lay(smem, tr_of(0)), e1 = G::lay(smem, tr_of(1)), e2 = G::lay(smem, tr_of(2));
     const float2 w31 = w3(1), w32 = w3(2);
+    // W_M^{2 n0} = W_M^{2t} W_48^m and W_M^{4 n0} = W_M^{4t} W_48^{2m} (n0 = t + m T)
+    const float2 b2 = kK5TwTable ? make_float2(1.f, 0.f) : wm(p.tw_m, 2 * t);
+    const float2 b4 = kK5TwTable ? make_float2(1.f, 0.f) : wm(p.tw_m, 4 * t);
 #pragma unroll
     for (int j = 0; j < 6; ++j) {
         const int m = q + 3 * j;
         if (m < 16) {
             const int n0 = t + m * T;
             const float2 x0 = e0.get(n0);
-            const float2 x1 = cmul(cconj(wm(p.tw_m, 2 * n0)), e1.get(n0));
-            const float2 x2 = cmul(cconj(wm(p.tw_m, 4 * n0)), e2.get(n0));
+            const float2 v2 = kK5TwTable ? wm(p.tw_m, 2 * n0) : cmul(b2, w48(m));
+            const float2 v4 = kK5TwTable ? wm(p.tw_m, 4 * n0) : cmul(b4, w48(2 * m));
+            const float2 x1 = cmul(cconj(v2), e1.get(n0));
+            const float2 x2 = cmul(cconj(v4), e2.get(n0));
             const float2 z0 = cadd(x0, cadd(x1, x2));                        // s = 0
             const float2 z2 = cadd(x0, cadd(cmul(w31, x1), cmul(w32, x2)));  // s = 2: W_3^{-2q} = W_3^{q}
             emit(2 * n0, z0.x * scale);                   // pos 2n0, 2n0+1 -> kx = pos
