@@ -42,7 +42,7 @@ struct Lane {
     float* gt = nullptr;
     float2* zbuf = nullptr;
     float* mag = nullptr;
-    float4* fgt = nullptr;
+    float2* fgt = nullptr;  // [chunk][2 planes][3np/4 + 1][np]
     Partial* part = nullptr;
     RotState* rot = nullptr;
     double* prof = nullptr;
@@ -338,7 +338,7 @@ fscan_status alloc_lane(fscan_ctx* ctx, Lane& l, int chunk) {
     CK(cudaMalloc(&l.zbuf, std::max(n * n, np * (size_t)ypitch((int)np)) * sizeof(float2) * chunk));
     // mag: the (|F|,|G|) tiles, later the np x np surface
     CK(cudaMalloc(&l.mag, std::max((size_t)ctx->mag_plane * 2, npp) * sizeof(float) * chunk));
-    CK(cudaMalloc(&l.fgt, (3 * np / 4 + 1) * np * sizeof(float4) * chunk));
+    CK(cudaMalloc(&l.fgt, 2 * (3 * np / 4 + 1) * np * sizeof(float2) * chunk));
     CK(cudaMalloc(&l.part, sizeof(Partial) * nparts * chunk));
     CK(cudaMalloc(&l.rot, sizeof(RotState) * chunk));
     CK(cudaMalloc(&l.prof, sizeof(double) * 2 * std::max(1, ctx->cfg.n_theta) * chunk));

@@ -719,6 +719,20 @@ __constant__ float kW32re[16] = {1.0f, 0.9807852506637573f, 0.9238795042037964f,
 __constant__ float kW32im[16] = {0.0f, -0.19509032368659973f, -0.3826834261417389f, -0.5555702447891235f, -0.7071067690849304f, -0.8314695954322815f, -0.9238795042037964f, -0.9807852506637573f, -1.0f, -0.9807852506637573f, -0.9238795042037964f, -0.8314695954322815f, -0.7071067690849304f, -0.5555702447891235f, -0.3826834261417389f, -0.19509032368659973f};
 __device__ __forceinline__ float2 w32(int k) { return make_float2(kW32re[k], kW32im[k]); }  // k < 16
 
+// Row spectra handed from K3 to K4, transposed: per pair an F plane then a G
+// plane, each [3N/4 + 1 bins][N rows] float2 (the column transforms of K4 read
+// one plane per pass: 8 bytes per element instead of a float4 (F, G) of which
+// each pass used half — K4 is bound by its L1 wavefronts: K4 7.8 -> 7.3 ms at
+// C4). N = 1024 keeps the interleaved [bins][rows] float4 (F, G): its K4 loads
+// each (F, G) site once for all three q groups (XColGeom::FOLD1), where the
+// planes measured 1.5% slower.
+template <int N>
+constexpr bool kFgtPlanes = N < 1024;
+template <int N>
+__device__ __forceinline__ float2* fgt_plane(const Params& p, int pair, int plane) {
+    return p.fgt + (2 * (size_t)pair + plane) * (size_t)(3 * N / 4 + 1) * N;
+}
+
 // W_M^e for 0 <= e < M (every caller passes a reduced exponent)
 __device__ __forceinline__ float2 wm(const float2* __restrict__ tw_m, int e) { return __ldg(tw_m + e); }
 
@@ -961,10 +975,22 @@ __global__ void __launch_bounds__(kXThreads, 3) k_xlat_rows(Params p) {
         const float dr = z1.x - z2.x, di = z1.y + z2.y;
         return make_float4(0.5f * (z1.x + z2.x), 0.5f * (z1.y - z2.y), 0.5f * di, -0.5f * dr);
     };
-    float4* dst = p.fgt + (size_t)pair * (H + 1) * N + y0 + ol;
-    for (int k = kk; k <= K / 2; k += KSTEP) dst[(size_t)(3 * k) * N] = sep(e0.get(k), e0.get((K - k) & (K - 1)));
-    for (int k = kk; 3 * k + 1 <= H; k += KSTEP) dst[(size_t)(3 * k + 1) * N] = sep(e1.get(k), e2.get(K - 1 - k));
-    for (int k = kk; 3 * k + 2 <= H; k += KSTEP) dst[(size_t)(3 * k + 2) * N] = sep(e2.get(k), e1.get(K - 1 - k));
+    // F and G planes of the pair (fgt_plane): each store a 64-byte run of the
+    // CTA's rows of one bin
+    float2* dF = fgt_plane<N>(p, pair, 0) + y0 + ol;
+    float2* dG = fgt_plane<N>(p, pair, 1) + y0 + ol;
+    float4* d4 = reinterpret_cast<float4*>(p.fgt) + (size_t)pair * (H + 1) * N + y0 + ol;
+    auto put = [&](int kb, float4 v) {
+        if constexpr (kFgtPlanes<N>) {
+            dF[(size_t)kb * N] = make_float2(v.x, v.y);
+            dG[(size_t)kb * N] = make_float2(v.z, v.w);
+        } else {
+            d4[(size_t)kb * N] = v;
+        }
+    };
+    for (int k = kk; k <= K / 2; k += KSTEP) put(3 * k, sep(e0.get(k), e0.get((K - k) & (K - 1))));
+    for (int k = kk; 3 * k + 1 <= H; k += KSTEP) put(3 * k + 1, sep(e1.get(k), e2.get(K - 1 - k)));
+    for (int k = kk; 3 * k + 2 <= H; k += KSTEP) put(3 * k + 2, sep(e2.get(k), e1.get(K - 1 - k)));
 }
 
 // ---------------------------------------------------------------- K4
@@ -977,11 +1003,6 @@ __global__ void __launch_bounds__(kXThreads, 3) k_xlat_rows(Params p) {
 // stored by surface row i = half - ky (the flip of matcher.cpp:171-182)
 // through a shared-memory tile (a k'-major output written straight from the
 // registers measured slower: K4 grows to 120 registers and K5's loads scatter).
-#ifdef FSCAN_K4_TMA
-constexpr bool kK4Tma = true;  // A/B: the block's fgt columns by one TMA bulk copy (measured slower)
-#else
-constexpr bool kK4Tma = false;
-#endif
 
 #ifdef FSCAN_K4_TABLES
 constexpr bool kK4W48 = false;
@@ -1042,17 +1063,10 @@ struct XColGeom {
     // instructions for the same wavefronts (MIO-throttle bound at N = 1024).
     using G = std::conditional_t<(N >= FSCAN_K4_F2_MIN), fscan_fft::Geom<N / 2, THREADS>,
                                  fscan_fft::GeomSoA<N / 2, THREADS>>;
-    // kK4Tma (below N = 1024; off by default): the CTA's COLS columns of fgt (one
-    // contiguous COLS x N float4 block) arrive by one TMA bulk copy into an input
-    // area that buffer B aliases once both folds have read it. Measured C4 -0.7%
-    // and C2 -2.5% (K4 9.4 -> 9.7 ms): unlike K5, whose one load phase it
-    // shortens, here every warp then waits for the whole block before its first
-    // fold instead of for its own loads, and the larger CTA (61 KB) costs C2's
-    // N = 256 kernel its fourth CTA per SM.
-    static constexpr bool TMA = kK4Tma && N <= 512;
-    static constexpr size_t IN_FLOATS = (size_t)4 * COLS * N;
-    static constexpr size_t B_FLOATS = (TMA && IN_FLOATS > (size_t)G::FLOATS) ? IN_FLOATS : (size_t)G::FLOATS;
-    static constexpr size_t FFT_FLOATS = (size_t)G::FLOATS + B_FLOATS;
+    // (round 2 measured a TMA bulk copy of the CTA's fgt columns into an input
+    // area aliased by buffer B: C4 -0.7%, C2 -2.5% — every warp then waits for
+    // the whole block before its first fold; removed)
+    static constexpr size_t FFT_FLOATS = (size_t)2 * G::FLOATS;
     static constexpr size_t WORK_FLOATS = FFT_FLOATS;
     // twiddle tables staged behind the work area: W_K (K entries) and, below
     // N = 1024, W_M (3K; at 1024 it would push the CTA past half an SM's smem)
@@ -1076,9 +1090,10 @@ struct XColGeom {
     // parked in shared memory (N = 1024: C5 +3%); below, every q group loads and
     // folds its own elements (the shared fold measured 1% slower at N = 512)
     static constexpr bool FOLD1 = N >= 1024;
+    static_assert(FOLD1 == !kFgtPlanes<N>, "K3 writes the layout this kernel reads");
     // merged-twiddle path (xlat_cols_merged, two-stage K-point transforms):
     // the exchange buffers + the [16][kQS] table W_M^{a j}
-    static constexpr bool MERGE = kK4Merge && !FOLD1 && !TMA && N == 512;
+    static constexpr bool MERGE = kK4Merge && !FOLD1 && N == 512;
     static constexpr size_t SMEM_MERGE = (FFT_FLOATS + 2 * 16 * fscan_fft::kQS) * sizeof(float);
 };
 
@@ -1124,18 +1139,8 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
     const int kq = kp <= H ? kp : H;  // the last block may hold fewer columns
     const auto bufA = G::lay(smem, tr);
     const auto bufB = G::lay(smem + G::FLOATS, tr);
-    const float4* src = p.fgt + ((size_t)pair * (H + 1) + kq) * N;
-    __shared__ uint64_t mbar;
-    if constexpr (X::TMA) pdl_enter();  // (otherwise after the constant tables' loads below)
-    if constexpr (X::TMA) {  // the block's columns: one bulk copy, read by both folds
-        const int ncols_in = min(COLS, H + 1 - (int)blockIdx.x * COLS);
-        if (threadIdx.x == 0) {
-            mbar_init(&mbar, 1);
-            bulk_load(smem + G::FLOATS, p.fgt + ((size_t)pair * (H + 1) + blockIdx.x * COLS) * N,
-                      (unsigned)(ncols_in * N * sizeof(float4)), &mbar);
-        }
-        src = reinterpret_cast<const float4*>(smem + G::FLOATS) + (size_t)min(c, ncols_in - 1) * N;
-    }
+    const float2* srcF = fgt_plane<N>(p, pair, 0) + (size_t)kq * N;
+    const float2* srcG = fgt_plane<N>(p, pair, 1) + (size_t)kq * N;
     // stage the twiddle tables in shared memory (latency: the FFT stages and
     // input/combine twiddles read them ~90 times per thread)
     float2* stw_rk = reinterpret_cast<float2*>(smem + X::WORK_FLOATS);
@@ -1143,7 +1148,7 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
     float2* stw_m_s = stw_k + X::TW_LIN;
     // PF: every table load issued up front into registers and stored after the
     // first fold (a load -> store loop waits out one L2 round trip per trip)
-    constexpr bool PF = !X::SMEM_WM && !X::TMA;
+    constexpr bool PF = !X::SMEM_WM;
     constexpr int TE = 240 + X::TW_LIN, TPT = PF ? (TE + X::THREADS - 1) / X::THREADS : 1;
     [[maybe_unused]] float2 tv[TPT];
     if constexpr (PF) {
@@ -1186,11 +1191,11 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
         if constexpr (kK4W48 && !X::FOLD1) return cmul(bq, w48(q * m));
         else return wq(n0, q);
     };
-    if constexpr (!X::TMA) pdl_enter();
+    pdl_enter();
     // LATE: the F fold reads no staged table, so its global loads are issued
     // before the barrier that publishes the twiddle tables (the table and input
     // load latencies overlap instead of following one another)
-    constexpr bool LATE = kK4LateSync && !X::FOLD1 && !X::TMA && !X::SMEM_WM;
+    constexpr bool LATE = kK4LateSync && !X::FOLD1 && !X::SMEM_WM;
     if constexpr (!LATE && !X::FOLD1) {
         tw_store();
         __syncthreads();
@@ -1216,7 +1221,8 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
             if (SITES % X::THREADS == 0 || e < SITES) {
                 const int cc = e / K, n0 = e % K;
                 const int kc = min((int)blockIdx.x * COLS + cc, H);
-                const float4* s4 = p.fgt + ((size_t)pair * (H + 1) + kc) * N;
+                static_assert(!kFgtPlanes<N>, "FOLD1 reads the interleaved (F, G) layout");
+                const float4* s4 = reinterpret_cast<const float4*>(p.fgt) + ((size_t)pair * (H + 1) + kc) * N;
                 v0[it] = s4[n0];
                 v1[it] = s4[n0 + K];
             }
@@ -1244,12 +1250,10 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
         for (int m = 0; m < 16; ++m) a[m] = bufA.get(t + m * T);
         __syncwarp();  // every input read before the transform's exchange writes
     } else {
-        if constexpr (X::TMA) mbar_wait(&mbar, 0);  // (the barrier above published the init)
 #pragma unroll
         for (int m = 0; m < 16; ++m) {
             const int n0 = t + m * T;
-            const float4 u0 = src[n0], u1 = src[n0 + K];
-            const float2 s = cadd(make_float2(u0.x, u0.y), cmul(w3q, make_float2(u1.x, u1.y)));
+            const float2 s = cadd(srcF[n0], cmul(w3q, srcF[n0 + K]));
             a[m] = q ? cmul(wq_m(m, n0), s) : s;
         }
         if constexpr (LATE) {
@@ -1268,11 +1272,9 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
 #pragma unroll
         for (int m = 0; m < 16; ++m) {
             const int n0 = t + m * T;
-            const float4 u0 = src[n0], u1 = src[n0 + K];
-            const float2 s = cadd(make_float2(u0.z, u0.w), cmul(w3q, make_float2(u1.z, u1.w)));
+            const float2 s = cadd(srcG[n0], cmul(w3q, srcG[n0 + K]));
             a[m] = q ? cmul(wq_m(m, n0), s) : s;
         }
-        if constexpr (X::TMA) __syncthreads();  // every fold read of the input area before buffer B reuses it
     }
     fft_regs<K, -1, true>(a, t, bufB, twk);
 #pragma unroll
@@ -1350,7 +1352,8 @@ __device__ __forceinline__ void xlat_cols_merged(const Params& p) {
     const int kq = kp <= H ? kp : H;  // the last block may hold fewer columns
     const auto bufA = G::lay(smem, tr);
     const auto bufB = G::lay(smem + G::FLOATS, tr);
-    const float4* src = p.fgt + ((size_t)pair * (H + 1) + kq) * N;
+    const float2* srcF = fgt_plane<N>(p, pair, 0) + (size_t)kq * N;
+    const float2* srcG = fgt_plane<N>(p, pair, 1) + (size_t)kq * N;
     float2* tab = reinterpret_cast<float2*>(smem + X::FFT_FLOATS);  // [16][QS]
     // the table's global loads are all issued first and stored to shared memory
     // only after the first fold (a load -> store loop waited out one L2 round
@@ -1378,8 +1381,7 @@ __device__ __forceinline__ void xlat_cols_merged(const Params& p) {
 #pragma unroll
     for (int m = 0; m < 16; ++m) {
         const int n0 = t + m * T;
-        const float4 u0 = src[n0], u1 = src[n0 + K];
-        a[m] = fold(make_float2(u0.x, u0.y), make_float2(u1.x, u1.y), m);
+        a[m] = fold(srcF[n0], srcF[n0 + K], m);
     }
 #pragma unroll
     for (int k = 0; k < TPT; ++k) {
@@ -1393,8 +1395,7 @@ __device__ __forceinline__ void xlat_cols_merged(const Params& p) {
 #pragma unroll
     for (int m = 0; m < 16; ++m) {
         const int n0 = t + m * T;
-        const float4 u0 = src[n0], u1 = src[n0 + K];
-        a[m] = fold(make_float2(u0.z, u0.w), make_float2(u1.z, u1.w), m);
+        a[m] = fold(srcG[n0], srcG[n0 + K], m);
     }
     fft_regs<K, -1, true>(a, t, bufB, fscan_fft::SmemTwQF{fq});
 #pragma unroll

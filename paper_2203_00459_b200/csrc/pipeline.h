@@ -69,7 +69,7 @@ struct Params {
     float* gt;     // masked g
     float2* zbuf;  // K1a->K1b spectra [batch][N][N]; reused as K4->K5 rows [batch][N][3N/4+1]
     float* mag;    // (|F|,|G|) band-passed half planes, tiled [batch][N/16][N][8] float2; reused as surface
-    float4* fgt;   // row spectra of f, g_rot (length 3N/2), transposed [batch][3N/4+1][N] (F, G)
+    float2* fgt;   // row spectra of f, g_rot (length 3N/2), transposed [batch][F, G plane][3N/4+1][N]
     float* surf;   // translation surface [batch][N][N]
     Partial* part; // K5 per-block argmax [batch][N / rows_per_block]
     RotState* rot; // [batch]
