@@ -388,10 +388,37 @@ __device__ __forceinline__ void exchange_sync() {
     }
 }
 
+// W_16^x (SIGN -1) or its conjugate, x a compile-time value after unrolling
+template <int SIGN>
+__device__ __forceinline__ float2 w16c(int x) {
+    constexpr float c1 = 0.92387953251128674f, s1 = 0.38268343236508977f, r = 0.70710678118654752f;
+    constexpr float cs[16] = {1.f, c1, r, s1, 0.f, -s1, -r, -c1, -1.f, -c1, -r, -s1, 0.f, s1, r, c1};
+    const float c = cs[x & 15], sn = cs[(x + 12) & 15];  // sin(2 pi x / 16) = cos(2 pi (x - 4) / 16)
+    return SIGN < 0 ? make_float2(c, -sn) : make_float2(c, sn);
+}
+
+#ifdef FSCAN_NO_POWJ
+constexpr bool kPowJ = false;  // A/B: last-stage twiddles read from the table per butterfly
+#else
+constexpr bool kPowJ = true;
+#endif
+
 template <int N, int R, int Ns, bool LAST, int SIGN, bool WARP, typename L, typename TW>
 __device__ __forceinline__ void stage(float2 (&v)[16], int t, const L& lay, const TW& tw) {
     constexpr int T = N / 16;
     constexpr int NB = 16 / R;
+    // POWJ: the last stage of a three-stage transform (span N / R > 16): butterfly
+    // j of thread t has k = t + j T, so its twiddles W_N^{r (t + j T)} are the
+    // thread's R - 1 table reads W_N^{r t} times the constants W_16^{r j}
+    // (instead of (R - 1) NB scattered table reads: L1 wavefronts bound these
+    // kernels, and the FMA pipe has room)
+    constexpr bool POWJ = kPowJ && LAST && Ns > 16 && NB > 1 && (kTwPow<TW> || kTwRK<TW>);
+    [[maybe_unused]] float2 tb[R];
+    if constexpr (POWJ) {
+        static_assert(Ns * R == N, "last stage");
+#pragma unroll
+        for (int r = 1; r < R; ++r) tb[r] = twiddle<SIGN>(tw, r * t);
+    }
 #pragma unroll
     for (int j = 0; j < NB; ++j) {
         float2 u[R];
@@ -401,7 +428,10 @@ __device__ __forceinline__ void stage(float2 (&v)[16], int t, const L& lay, cons
         const int k = b & (Ns - 1);
         if constexpr (Ns > 1) {
             constexpr int q = N / (Ns * R);  // W_{Ns R}^x = tw[x * q]
-            if constexpr (std::is_same_v<TW, SmemTwQF>) {
+            if constexpr (POWJ) {
+#pragma unroll
+                for (int r = 1; r < R; ++r) u[r] = cmul(u[r], j == 0 ? tb[r] : cmul(tb[r], w16c<SIGN>(r * j)));
+            } else if constexpr (std::is_same_v<TW, SmemTwQF>) {
                 static_assert(Ns == 16 && LAST, "merged twiddles: two-stage transforms only");
 #pragma unroll
                 for (int r = 1; r < R; ++r) u[r] = cmul(u[r], tw.f[r * kQS + 3 * k]);
