@@ -752,6 +752,19 @@ constexpr bool kK3TwTable = true;  // A/B: fold twiddles read from the W_M table
 #else
 constexpr bool kK3TwTable = false;
 #endif
+#ifdef FSCAN_K3_STASH
+constexpr bool kK3FoldGather = false;  // A/B: gather into a z stash, fold per group from it (rounds 1-2)
+#else
+constexpr bool kK3FoldGather = true;
+#endif
+#ifndef FSCAN_K3_FIG_MAXN
+#define FSCAN_K3_FIG_MAXN 4096
+#endif
+#ifdef FSCAN_K3_FIG_STAGE
+constexpr bool kK3FigNoStage = false;  // A/B: FIG with the f~ rows staged by TMA (C5 -2%: 71 KB CTAs)
+#else
+constexpr bool kK3FigNoStage = true;
+#endif
 #ifdef FSCAN_K3_STASH_SOA
 constexpr bool kK3StashSoA = true;  // A/B: split re / im stash (rounds 1-2)
 #else
@@ -773,8 +786,13 @@ struct XRowGeom {
     static constexpr size_t STASH = (size_t)2 * ROWS * SP;
     // + the CTA's ROWS rows of f~ (dense, one TMA bulk copy) behind the stash
     // (texture-gather instantiation only)
-    static constexpr size_t FT_OFF = STASH;
-    static constexpr size_t STAGE = kK3FtTma ? STASH + (size_t)ROWS * N : STASH;
+    // FIG (gather + fold, default): no stash; the f~ stage sits behind the
+    // exchange buffers the gather writes
+    static constexpr bool FIG = kK3FoldGather && N <= FSCAN_K3_FIG_MAXN;
+    // f~ staged by TMA (the texture-gather instantiation), unless FIG without it
+    static constexpr bool FT_STAGE = kK3FtTma && !(FIG && kK3FigNoStage);
+    static constexpr size_t FT_OFF = FIG ? (size_t)G::FLOATS : STASH;
+    static constexpr size_t STAGE = FT_OFF + (FT_STAGE ? (size_t)ROWS * N : 0);
     static constexpr size_t WORK = STAGE > (size_t)G::FLOATS ? STAGE : (size_t)G::FLOATS;
     // + the span-16 stage's [r][k] twiddle table (K >= 256): 15 shared loads
     // per thread instead of 4 global loads and 11 products (C4 +0.4%; the same
@@ -836,7 +854,7 @@ __global__ void __launch_bounds__(kXThreads, 3) k_xlat_rows(Params p) {
     const float* ft = p.ft + (size_t)src * N * N;
     // TEX (the lane's own workspace): the block's ROWS rows of f~ by one TMA bulk
     // copy into a dense stage; the gather reads them from there
-    constexpr bool FT_TMA = TEX && kK3FtTma;
+    constexpr bool FT_TMA = TEX && X::FT_STAGE;
     __shared__ uint64_t ft_bar;
     const float* fst = smem + X::FT_OFF;
     if constexpr (FT_TMA) {
@@ -853,72 +871,122 @@ __global__ void __launch_bounds__(kXThreads, 3) k_xlat_rows(Params p) {
     // rotate_bilinear(g~, -theta); -theta == 0.0 returns g~ itself, which st = 0,
     // ct = 1 reproduce exactly (integer source coordinates, zero fractions)
     const float stf = rs.identity ? 0.0f : (float)rs.st, ctf = rs.identity ? 1.0f : (float)rs.ct;
-    // gather: ROWS rows x N cells over all threads, consecutive threads on
-    // consecutive x; U cells per thread per round with every load issued
-    // before any use (memory-level parallelism for the L2/DRAM latency)
-    constexpr int CELLS = ROWS * N;
+    // one cell (x, yl) of the de-rotated scan: its f~ value (unless staged by
+    // TMA) and the four bilinear taps of g~, every load issued before any use
+    auto fetch = [&](int x, int yl, bool in_range, float& fv, float (&tap)[4], float& fr, float& fc) {
+        const int y = y0 + yl;
+        const bool live = in_range && (!EMB || (x < nvalid && y < nvalid));
+        // src_row = c + st*u + ct*v, src_col = c + ct*u - st*v (imageops.cpp:70-73)
+        // in fp32 FMAs: <= 5e-5 cell coordinate error, i.e. <= 5e-5 relative per
+        // bilinear sample (far inside the 1e-4 surface gate)
+        const float uu = (float)x - c0f32, vv = (float)y - c0f32;  // exact half-integers
+        const float sr = fmaf(stf, uu, fmaf(ctf, vv, c0f32));
+        const float sc = fmaf(ctf, uu, fmaf(-stf, vv, c0f32));
+        const float r0f = floorf(sr), cf = floorf(sc);
+        fr = sr - r0f;
+        fc = sc - cf;
+        // taps outside the grid are 0 (sample_bilinear, imageops.cpp:10-26)
+        const int r0 = (int)r0f, cc0 = (int)cf;
+        const bool r0in = live && (unsigned)r0 < (unsigned)N, r1in = live && (unsigned)(r0 + 1) < (unsigned)N;
+        const bool c0in = (unsigned)cc0 < (unsigned)N, c1in = (unsigned)(cc0 + 1) < (unsigned)N;
+        if constexpr (!FT_TMA) fv = live ? ft[y * N + x] : 0.f;
+        if constexpr (TEX) {
+            // texel (c, row) at coordinate (c + 1.0, row + 1.0): the gather's
+            // footprint starts at floor(coord - 0.5) = (cc0, r0); component
+            // order (c0, r1), (c1, r1), (c1, r0), (c0, r0)
+            const float4 g4 = tex2Dgather<float4>((cudaTextureObject_t)p.gtex, cf + 1.0f,
+                                                 (float)(pair * N + r0) + 1.0f, 0);
+            tap[0] = r0in ? g4.w : 0.f;
+            tap[1] = r0in ? g4.z : 0.f;
+            tap[2] = r1in ? g4.x : 0.f;
+            tap[3] = r1in ? g4.y : 0.f;
+        } else {
+            const float* gp = gt + (r0 * N + cc0);  // 32-bit offset, one address per cell
+            tap[0] = (r0in && c0in) ? gp[0] : 0.f;
+            tap[1] = (r0in && c1in) ? gp[1] : 0.f;
+            tap[2] = (r1in && c0in) ? gp[N] : 0.f;
+            tap[3] = (r1in && c1in) ? gp[N + 1] : 0.f;
+        }
+    };
     constexpr int U = FSCAN_K3_U;
+    if constexpr (X::FIG) {
+        // gather + fold: a thread takes the cells x and x + K of a row (a fold
+        // site), forms the three group inputs W_M^{q x} (z[x] + W_3^q z[x+K])
+        // and stores them straight into the groups' exchange buffers — no stash
+        // of z and no per-group re-read of it
+        constexpr int SITES = ROWS * K, US = U / 2;
 #pragma unroll 1
-    for (int e0 = threadIdx.x; e0 < CELLS; e0 += U * kXThreads) {
-        float fv[U], tap[U][4], frs[U], fcs[U];
+        for (int e0 = threadIdx.x; e0 < SITES; e0 += US * kXThreads) {
+            float fv[US][2], tap[US][2][4], frs[US][2], fcs[US][2];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int e = e0 + u * kXThreads;
-            const int yl = e / N, x = e % N;
-            const int y = y0 + yl;
-            const bool live = e < CELLS && (!EMB || (x < nvalid && y < nvalid));
-            // src_row = c + st*u + ct*v, src_col = c + ct*u - st*v (imageops.cpp:70-73)
-            // in fp32 FMAs: <= 5e-5 cell coordinate error, i.e. <= 5e-5 relative per
-            // bilinear sample (far inside the 1e-4 surface gate)
-            const float uu = (float)x - c0f32, vv = (float)y - c0f32;  // exact half-integers
-            const float sr = fmaf(stf, uu, fmaf(ctf, vv, c0f32));
-            const float sc = fmaf(ctf, uu, fmaf(-stf, vv, c0f32));
-            const float r0f = floorf(sr), cf = floorf(sc);
-            frs[u] = sr - r0f;
-            fcs[u] = sc - cf;
-            // taps outside the grid are 0 (sample_bilinear, imageops.cpp:10-26)
-            const int r0 = (int)r0f, cc0 = (int)cf;
-            const bool r0in = live && (unsigned)r0 < (unsigned)N, r1in = live && (unsigned)(r0 + 1) < (unsigned)N;
-            const bool c0in = (unsigned)cc0 < (unsigned)N, c1in = (unsigned)(cc0 + 1) < (unsigned)N;
-            if constexpr (!FT_TMA) fv[u] = live ? ft[y * N + x] : 0.f;
-            if constexpr (TEX) {
-                // texel (c, row) at coordinate (c + 1.0, row + 1.0): the gather's
-                // footprint starts at floor(coord - 0.5) = (cc0, r0); component
-                // order (c0, r1), (c1, r1), (c1, r0), (c0, r0)
-                const float4 g4 = tex2Dgather<float4>((cudaTextureObject_t)p.gtex, cf + 1.0f,
-                                                     (float)(pair * N + r0) + 1.0f, 0);
-                tap[u][0] = r0in ? g4.w : 0.f;
-                tap[u][1] = r0in ? g4.z : 0.f;
-                tap[u][2] = r1in ? g4.x : 0.f;
-                tap[u][3] = r1in ? g4.y : 0.f;
-            } else {
-                const float* gp = gt + (r0 * N + cc0);  // 32-bit offset, one address per cell
-                tap[u][0] = (r0in && c0in) ? gp[0] : 0.f;
-                tap[u][1] = (r0in && c1in) ? gp[1] : 0.f;
-                tap[u][2] = (r1in && c0in) ? gp[N] : 0.f;
-                tap[u][3] = (r1in && c1in) ? gp[N + 1] : 0.f;
+            for (int u = 0; u < US; ++u) {
+                const int e = e0 + u * kXThreads;
+                const int yl = e / K, x = e % K;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) fetch(x + h * K, yl, e < SITES, fv[u][h], tap[u][h], frs[u][h], fcs[u][h]);
+            }
+            if constexpr (FT_TMA) {
+                if (e0 == threadIdx.x) mbar_wait(&ft_bar, 0);  // first round: after its texture fetches are issued
+#pragma unroll
+                for (int u = 0; u < US; ++u) {
+                    const int e = e0 + u * kXThreads;
+                    const int yl = e / K, x = e % K;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) fv[u][h] = e < SITES ? fst[yl * N + x + h * K] : 0.f;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < US; ++u) {
+                const int e = e0 + u * kXThreads;
+                if (e < SITES) {
+                    const int yl = e / K, x = e % K;
+                    const float2 z0 = make_float2(fv[u][0], bilerp(frs[u][0], fcs[u][0], tap[u][0][0], tap[u][0][1],
+                                                                   tap[u][0][2], tap[u][0][3]));
+                    const float2 z1 = make_float2(fv[u][1], bilerp(frs[u][1], fcs[u][1], tap[u][1][0], tap[u][1][1],
+                                                                   tap[u][1][2], tap[u][1][3]));
+                    // z0 + W_3^q z1 for q = 0, 1, 2 (a radix-3 butterfly with one zero input)
+                    const float2 tt = make_float2(fmaf(-0.5f, z1.x, z0.x), fmaf(-0.5f, z1.y, z0.y));
+                    const float2 ss = make_float2(kS3 * z1.x, kS3 * z1.y);
+                    G::lay(xbase, 3 * yl).put(x, cadd(z0, z1));
+                    G::lay(xbase, 3 * yl + 1).put(x, cmul(wm(p.tw_m, x), make_float2(tt.x + ss.y, tt.y - ss.x)));
+                    G::lay(xbase, 3 * yl + 2).put(x, cmul(wm(p.tw_m, 2 * x), make_float2(tt.x - ss.y, tt.y + ss.x)));
+                }
             }
         }
-        if constexpr (FT_TMA) {
-            if (e0 == threadIdx.x) mbar_wait(&ft_bar, 0);  // first round: after its texture fetches are issued
+    } else {
+        // gather: ROWS rows x N cells over all threads, consecutive threads on
+        // consecutive x; U cells per thread per round with every load issued
+        // before any use (memory-level parallelism for the L2/DRAM latency)
+        constexpr int CELLS = ROWS * N;
+#pragma unroll 1
+        for (int e0 = threadIdx.x; e0 < CELLS; e0 += U * kXThreads) {
+            float fv[U], tap[U][4], frs[U], fcs[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int e = e0 + u * kXThreads;
-                fv[u] = e < CELLS ? fst[e] : 0.f;  // dense [ROWS][N]: e = yl * N + x
+                fetch(e % N, e / N, e < CELLS, fv[u], tap[u], frs[u], fcs[u]);
             }
-        }
+            if constexpr (FT_TMA) {
+                if (e0 == threadIdx.x) mbar_wait(&ft_bar, 0);  // first round: after its texture fetches are issued
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int e = e0 + u * kXThreads;
-            if (e < CELLS) {
-                const int yl = e / N, x = e % N;
-                const float gi = bilerp(frs[u], fcs[u], tap[u][0], tap[u][1], tap[u][2], tap[u][3]);
-                if constexpr (kK3StashSoA) {
-                    const int a = yl * SP + x + (x >> 5);
-                    st_re[a] = fv[u];
-                    st_im[a] = gi;
-                } else {
-                    st2[yl * SP + x] = make_float2(fv[u], gi);
+                for (int u = 0; u < U; ++u) {
+                    const int e = e0 + u * kXThreads;
+                    fv[u] = e < CELLS ? fst[e] : 0.f;  // dense [ROWS][N]: e = yl * N + x
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int e = e0 + u * kXThreads;
+                if (e < CELLS) {
+                    const int yl = e / N, x = e % N;
+                    const float gi = bilerp(frs[u], fcs[u], tap[u][0], tap[u][1], tap[u][2], tap[u][3]);
+                    if constexpr (kK3StashSoA) {
+                        const int a = yl * SP + x + (x >> 5);
+                        st_re[a] = fv[u];
+                        st_im[a] = gi;
+                    } else {
+                        st2[yl * SP + x] = make_float2(fv[u], gi);
+                    }
                 }
             }
         }
@@ -930,31 +998,37 @@ __global__ void __launch_bounds__(kXThreads, 3) k_xlat_rows(Params p) {
     G::map(threadIdx.x, tr, t);
     const int yl = tr / 3, q = tr % 3;
     {
-        const float2 w3q = w3(q);
-        // W_M^{q n0}, n0 = t + m T (M = 48 T): the thread's base W_M^{q t} times
-        // W_48^{q m} from the constant bank (a scattered table read per element
-        // cost an L1 wavefront per 16 bytes)
-        const float2 bq = kK3TwTable ? make_float2(1.f, 0.f) : wm(p.tw_m, q * t);
         float2 v[16];
+        if constexpr (X::FIG) {
 #pragma unroll
-        for (int m = 0; m < 16; ++m) {
-            const int n0 = t + m * T, n1 = n0 + K;
-            float2 z0, z1;
-            if constexpr (kK3StashSoA) {
-                const int a0 = yl * SP + n0 + (n0 >> 5), a1 = yl * SP + n1 + (n1 >> 5);
-                z0 = make_float2(st_re[a0], st_im[a0]);
-                z1 = make_float2(st_re[a1], st_im[a1]);
-            } else {
-                z0 = st2[yl * SP + n0];
-                z1 = st2[yl * SP + n1];
+            for (int m = 0; m < 16; ++m) v[m] = G::lay(xbase, tr).get(t + m * T);
+            __syncwarp();  // every input read before the transform's exchange writes
+        } else {
+            const float2 w3q = w3(q);
+            // W_M^{q n0}, n0 = t + m T (M = 48 T): the thread's base W_M^{q t} times
+            // W_48^{q m} from the constant bank (a scattered table read per element
+            // cost an L1 wavefront per 16 bytes)
+            const float2 bq = kK3TwTable ? make_float2(1.f, 0.f) : wm(p.tw_m, q * t);
+#pragma unroll
+            for (int m = 0; m < 16; ++m) {
+                const int n0 = t + m * T, n1 = n0 + K;
+                float2 z0, z1;
+                if constexpr (kK3StashSoA) {
+                    const int a0 = yl * SP + n0 + (n0 >> 5), a1 = yl * SP + n1 + (n1 >> 5);
+                    z0 = make_float2(st_re[a0], st_im[a0]);
+                    z1 = make_float2(st_re[a1], st_im[a1]);
+                } else {
+                    z0 = st2[yl * SP + n0];
+                    z1 = st2[yl * SP + n1];
+                }
+                const float2 s = cadd(z0, cmul(w3q, z1));
+                if constexpr (kK3TwTable)
+                    v[m] = q ? cmul(wm(p.tw_m, n0 * q), s) : s;
+                else
+                    v[m] = cmul(cmul(bq, w48(q * m)), s);
             }
-            const float2 s = cadd(z0, cmul(w3q, z1));
-            if constexpr (kK3TwTable)
-                v[m] = q ? cmul(wm(p.tw_m, n0 * q), s) : s;
-            else
-                v[m] = cmul(cmul(bq, w48(q * m)), s);
+            __syncthreads();  // every stash read done before the exchange buffers are written
         }
-        __syncthreads();  // every stash read done before the exchange buffers are written
         const auto b = G::lay(xbase, tr);
         if constexpr (X::RK)
             fft_regs<K, -1, true>(v, t, b, fscan_fft::SmemTwRK{srk, p.tw_k});  // T <= 32: within a warp
