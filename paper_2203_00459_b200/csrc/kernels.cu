@@ -129,6 +129,28 @@ __device__ __forceinline__ const float2* tile_at(const float2* m, int n, int r, 
     return m + ((size_t)(u / kTileW) * n + r) * kTileW + (u % kTileW);
 }
 
+// K1a -> K1b spectrum columns in K1b's column blocks: per pair, NB = zcols / U
+// direct blocks (columns b U + c) then NB mirror blocks (columns (N - b U - c)
+// mod N), each [N rows][U] float2 — exactly the 2U columns one K1b CTA
+// transforms, contiguous, so the CTA fetches them with two bulk copies instead
+// of 16 scattered 64-byte row pieces per thread (U = k1b_u<N>())
+#ifdef FSCAN_K1B_ROWMAJOR
+constexpr bool kK1bBlocks = false;  // A/B: row-major spectrum, per-thread column loads (rounds 1-2)
+#else
+constexpr bool kK1bBlocks = true;
+#endif
+template <int N>
+__host__ __device__ constexpr int k1b_u() {
+    return N >= 1024 ? 4 : 8;
+}
+// float2 offset of column slot c of direct (mirror = 0) or mirror (1) block b, row y
+template <int N>
+__device__ __forceinline__ size_t k1b_at(int pair, int zcols, int mirror, int w, int y) {
+    constexpr int U = k1b_u<N>();
+    const int blk = mirror * (zcols / U) + w / U;
+    return (size_t)pair * N * N + ((size_t)blk * N + y) * U + (w % U);
+}
+
 // ---------------------------------------------------------------- K1a
 // rows of f~ = f*mf and g~ = g*mg: write the masked scans (translation stage
 // input), window by the separable Hann w[r]*w[c], FFT the packed row
@@ -197,7 +219,13 @@ __global__ void FSCAN_K1A_BOUNDS k_rot_rows(Params p) {
 #pragma unroll
     for (int m = 0; m < 16; ++m) {
         const int x = t + m * T;
-        if (x < p.zcols || x > N - p.zcols) p.zbuf[base + x] = v[m];  // columns K1b reads
+        if constexpr (kK1bBlocks) {
+            // the columns K1b reads, in its column blocks (k1b_at)
+            if (x < p.zcols) p.zbuf[k1b_at<N>(pair, p.zcols, 0, x, y)] = v[m];
+            if (x == 0 || x > N - p.zcols) p.zbuf[k1b_at<N>(pair, p.zcols, 1, (N - x) & (N - 1), y)] = v[m];
+        } else if (x < p.zcols || x > N - p.zcols) {
+            p.zbuf[base + x] = v[m];  // columns K1b reads
+        }
     }
     if (p.chain) {  // flags per scan of the sequence
         if (badf) atomicOr(p.flags + 2 * pair, badf);
@@ -216,8 +244,12 @@ __global__ void FSCAN_K1A_BOUNDS k_rot_rows(Params p) {
 // (N = 1024 at 4 columns: 512 threads instead of 1024; C5 +0.4%; N = 512 at
 // 4 columns measured 0.8% slower than 8)
 template <int N>
-__host__ __device__ constexpr int k1b_u() {
-    return N >= 1024 ? 4 : 8;
+__host__ __device__ constexpr size_t k1b_smem_floats() {
+    // exchange buffer, or (kK1bBlocks) the two staged blocks with the mirror block
+    // 8 float2 further on (its half-warp reads then miss the direct block's banks)
+    constexpr size_t ex = (size_t)part_floats<N, 2 * k1b_u<N>()>();
+    constexpr size_t st = (size_t)2 * (2 * (size_t)N * k1b_u<N>() + 8);
+    return kK1bBlocks && st > ex ? st : ex;
 }
 
 template <int N>
@@ -230,13 +262,32 @@ __global__ void __launch_bounds__(N / 16 * 2 * k1b_u<N>()) k_rot_cols(Params p) 
     const int pair = blockIdx.y;
     const int u0 = blockIdx.x * U;
     const int c = threadIdx.x % CW, t = threadIdx.x / CW;
-    const int col = c < U ? (u0 + c) : ((N - (u0 + c - U)) & (N - 1));
+    [[maybe_unused]] const int col = c < U ? (u0 + c) : ((N - (u0 + c - U)) & (N - 1));
     float2* sbuf = reinterpret_cast<float2*>(smem);
     const Lay<CW> lay{sbuf, c};
-    const float2* z = p.zbuf + (size_t)pair * N * N;
     float2 v[16];
+    if constexpr (kK1bBlocks) {
+        // the CTA's direct and mirror column blocks by two bulk copies into the
+        // exchange buffer's bytes (read into registers before the first exchange)
+        constexpr unsigned BYTES = (unsigned)(N * U * sizeof(float2));
+        constexpr int BOFF = N * U + 8;
+        __shared__ uint64_t bar;
+        if (threadIdx.x == 0) {
+            mbar_init(&bar, 2);
+            bulk_load(sbuf, p.zbuf + k1b_at<N>(pair, p.zcols, 0, u0, 0), BYTES, &bar);
+            bulk_load(sbuf + BOFF, p.zbuf + k1b_at<N>(pair, p.zcols, 1, u0, 0), BYTES, &bar);
+        }
+        __syncthreads();  // publishes the barrier's initialisation
+        mbar_wait(&bar, 0);
+        const float2* sb = sbuf + (c < U ? c : BOFF + c - U);
 #pragma unroll
-    for (int m = 0; m < 16; ++m) v[m] = z[(size_t)(t + m * T) * N + col];
+        for (int m = 0; m < 16; ++m) v[m] = sb[(t + m * T) * U];
+        __syncthreads();  // every staged value read before the exchange reuses the bytes
+    } else {
+        const float2* z = p.zbuf + (size_t)pair * N * N;
+#pragma unroll
+        for (int m = 0; m < 16; ++m) v[m] = z[(size_t)(t + m * T) * N + col];
+    }
     fft_regs<N, -1>(v, t, lay, p.tw_n);
 #pragma unroll
     for (int m = 0; m < 16; ++m) lay.put(t + m * T, v[m]);
@@ -1948,7 +1999,7 @@ cudaError_t rot_rows(const Params& p, cudaStream_t s) {
 template <int N>
 cudaError_t rot_cols(const Params& p, cudaStream_t s) {
     constexpr int U = k1b_u<N>();
-    const size_t sm = (size_t)part_floats<N, 2 * U>() * sizeof(float);
+    const size_t sm = k1b_smem_floats<N>() * sizeof(float);
     cudaError_t e = set_smem(k_rot_cols<N>, sm);
     if (e != cudaSuccess) return e;
     return launch_k(k_rot_cols<N>, dim3(p.zcols / U, p.batch), dim3(N / 16 * 2 * U), sm, s, p, p);
