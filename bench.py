@@ -202,8 +202,15 @@ def ncu_issue(kernel: str, n: int) -> dict | None:
         if d.get("n_xy", 512) != n or kernel not in d or "issue_pct" not in d[kernel]:
             return None
         k = d[kernel]
-        return {"issue_active_frac": round(k["issue_pct"] / 100, 3), "dram_frac": round(k["dram_pct"] / 100, 3),
-                "warps_active_frac": round(k["warps_active_pct"] / 100, 3), "source": d.get("source", NCU_TRAFFIC)}
+        out = {"issue_active_frac": round(k["issue_pct"] / 100, 3), "dram_frac": round(k["dram_pct"] / 100, 3),
+               "warps_active_frac": round(k["warps_active_pct"] / 100, 3)}
+        # the translation kernels are bound by the L1 data pipe (shared-memory
+        # exchanges + loads) before the FMA pipe or DRAM
+        for key, name in (("l1_lsu_pct", "l1_lsu_wavefront_frac"), ("fma_pct", "fma_pipe_frac")):
+            if key in k:
+                out[name] = round(k[key] / 100, 3)
+        out["source"] = d.get("source", NCU_TRAFFIC)
+        return out
     except Exception:
         return None
 
@@ -492,8 +499,8 @@ def run_ours(args):
                 "alg_bytes_per_launch": alg, "pairs_per_launch": round(pairs_per_launch, 2),
                 "avg_launch_ms": dom_ms / dom_launches,
                 "kernel_share": round(dom_ms / sum(v[0] for v in kt.values()), 3),
-                # the dominant kernel is FFT-issue-bound, not DRAM-bound: its ncu issue
-                # utilisation says how close it runs to its own ceiling
+                # the dominant kernel is bound by its L1 data pipe and issue slots, not
+                # by DRAM: its ncu utilisations say how close it runs to those ceilings
                 "ncu": ncu_issue(dom, cfg.n_xy)}
     bpair = pair_bytes(cfg.n_xy, cfg.n_theta, cfg.pad_angle, masks=mf is not None,
                        s_in=(8.0 * spec.n_az * spec.n_range) if polar else None)

@@ -1,8 +1,8 @@
 """profiles/ncu_traffic.json from an ncu --set full capture of one C4 step:
 DRAM bytes (read + write) per launch and per pair for every pipeline kernel.
 Pairs per launch come from k_finalize's grid (one CTA per pair).
-Also records each kernel's issue-slot, warps-active and DRAM utilisation (what
-bench.py's roofline.ncu quotes).
+Also records each kernel's issue-slot, warps-active, DRAM, L1 (LSU data-pipe
+wavefronts) and FMA-pipe utilisation (what bench.py's roofline.ncu quotes).
 usage: python tools/ncu_traffic.py REP SOURCE_NOTE [PAIRS_PER_LAUNCH] > profiles/ncu_traffic.json"""
 import csv
 import io
@@ -35,7 +35,9 @@ for r in rows[2:]:
             k = k[: -len(suffix)]
     pc = {m: col(r, c) for m, c in (("issue_pct", "smsp__issue_active.avg.pct_of_peak_sustained_active"),
                                      ("warps_active_pct", "sm__warps_active.avg.pct_of_peak_sustained_active"),
-                                     ("dram_pct", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"))}
+                                     ("dram_pct", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
+                                     ("l1_lsu_pct", "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed"),
+                                     ("fma_pct", "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"))}
     recs.append((k, col(r, "dram__bytes_read.sum") + col(r, "dram__bytes_write.sum"),
                  col(r, "gpu__time_duration.sum"), col(r, "launch__grid_size"), pc))
 if len(sys.argv) > 3:
