@@ -1274,7 +1274,13 @@ fscan_status fscan_match_batch_host(fscan_ctx* ctx, const float* f, const float*
         p.theta_surf = tsurf ? l.tsurf : nullptr;
         p.xy_surf = xsurf ? l.xsurf : nullptr;
         fscan_status r = run_chunk(ctx, l, p, Stages::Full, &ctx->launches_last);
-        if (r != FSCAN_OK) return r;
+        if (r != FSCAN_OK) {
+            // nothing queued may still read the caller's host buffers after the return
+            cudaStreamSynchronize(ctx->h2d);
+            for (Lane& q : LaneRange{ctx}) cudaStreamSynchronize(q.stream);
+            for (auto& h : ctx->hslot) h.pending = false;
+            return r;
+        }
         CK(cudaMemcpyAsync(ctx->hres + off, l.res, sizeof(fscan_pair_result) * cnt, cudaMemcpyDeviceToHost, s));
         if (tsurf)
             CK(cudaMemcpyAsync(tsurf + (size_t)off * nt, l.tsurf, sizeof(double) * nt * cnt,

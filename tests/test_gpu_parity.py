@@ -1056,3 +1056,43 @@ def test_reference_written_fscn_files_to_trajectory(fb, orc, dev, tmp_path):
         acc = fb.compose(acc, fb.inverse(fb.Pose2D(r.theta, r.tx, r.ty)))
         assert abs(poses[k + 1].theta - acc.theta) <= THETA_TOL
         assert abs(poses[k + 1].tx - acc.tx) <= 3 * PX_TOL * delta and abs(poses[k + 1].ty - acc.ty) <= 3 * PX_TOL * delta
+
+
+def test_host_staging_ring_wraps_and_regrows(fb, dev):
+    """fscan_match_batch_host stages chunks through a 4-slot ring on its own copy
+    stream (slots released by events): many more chunks than slots, masked and
+    unmasked, a regrown chunk and the surfaces path all give the device API's
+    bytes."""
+    cfg, delta, _ = fb.baseline_config(2)
+    f, g, mf, mg, _ = fb.synth_pairs_host(fb.synth_spec(2), 3, 11)
+    F, G, MF, MG = to_dev(dev, f, g, mf, mg)
+    m = fb.Matcher(cfg, max_batch=11, chunk=1)
+    for masks in ((mf, mg), (None, None)):
+        dm = (MF, MG) if masks[0] is not None else (None, None)
+        ref = fb.decode_results(m.match_device(F, G, *dm, delta=delta))
+        torch.cuda.synchronize()
+        for chunk in (1, 3, 11):  # 11 chunks over 4 slots and 3 lanes; regrown slots
+            m.set_chunk(chunk)
+            host = m.match_host(f, g, *masks, delta=delta)
+            assert host.tobytes() == ref.tobytes(), (chunk, masks[0] is None)
+        res, ts, xs = m.match_host(f, g, *masks, delta=delta, surfaces=True)
+        assert res.tobytes() == ref.tobytes() and np.isfinite(ts).all() and np.isfinite(xs).all()
+
+
+def test_programmatic_dependent_launch_is_result_neutral(fb, dev, monkeypatch):
+    """FSCAN_PDL (read at context creation): the pipeline kernels launched with or
+    without programmatic stream serialisation, directly and as a graph replay,
+    give identical bytes."""
+    cfg, delta, _ = fb.baseline_config(2)
+    f, g, mf, mg, _ = fb.synth_pairs_host(fb.synth_spec(2), 50, 9)
+    F, G, MF, MG = to_dev(dev, f, g, mf, mg)
+    outs = []
+    for mode in ("0", "2"):
+        monkeypatch.setenv("FSCAN_PDL", mode)
+        m = fb.Matcher(cfg, max_batch=9, chunk=2)
+        outs.append(m.match_device(F, G, MF, MG, delta=delta).clone())
+        m.set_graphs(True)
+        for _ in range(2):
+            outs.append(m.match_device(F, G, MF, MG, delta=delta).clone())
+        torch.cuda.synchronize()
+    assert all(torch.equal(o, outs[0]) for o in outs)
