@@ -25,7 +25,7 @@ constexpr double kPi = 3.141592653589793;  // std::numbers::pi (geometry.hpp:11)
 #define FSCAN_PDL_DEFAULT 1
 #endif
 constexpr int kPdlDefault = FSCAN_PDL_DEFAULT;
-constexpr int kPdlChunk = 64;
+constexpr int kPdlLatencyChunk = 4;
 constexpr int kHostSlots = 4;              // fscan_match_batch_host input staging ring
 constexpr int kMaxLanes = 8;               // concurrent chunk pipelines (FSCAN_LANES, default 3)
 #ifdef FSCAN_NO_TEX_GATHER
@@ -73,10 +73,11 @@ struct fscan_ctx {
     int rot_col_blocks = 0;  // K1b column blocks (8 columns each) the polar taps read
     int phase = 0;           // opt-in phase correlation in the translation stage
     // programmatic dependent launch of the pipeline kernels (kernels.cu
-    // pdl_enter): 0 off, 1 for chunks of at most kPdlChunk pairs, 2 always
-    // (FSCAN_PDL overrides). Default 1: one-pair latency 65.6 -> 61.5 us, C5
-    // (63-pair chunks) +1.3%; at C4's 126-pair chunks neutral to -0.3% (the
-    // early CTAs of the next kernel hold SM slots the other lanes could use)
+    // pdl_enter): 0 off, 1 for latency-sized chunks (<= kPdlLatencyChunk pairs)
+    // and grid side >= 1024, 2 always (FSCAN_PDL overrides). Measured with
+    // PDL on: C1 (one pair) +2.7%, C5 (63 pairs of 1024^2) +1.0%, but C2 (three
+    // lanes of 22 pairs of 256^2) -4.5% and C4 -0.3%: the next kernel's early
+    // CTAs hold SM slots the other lanes' kernels could use
     int pdl_mode = kPdlDefault;
     // grid geometry: np = n for powers of two; otherwise the
     // rotation stage runs Bluestein DFTs of length bs_L at n and the
@@ -406,7 +407,7 @@ Params base_params(fscan_ctx* ctx, Lane& l, int batch, double delta) {
     p.n = ctx->n;
     p.np = ctx->np;
     p.embed = ctx->np != ctx->n;
-    p.pdl = ctx->pdl_mode == 2 || (ctx->pdl_mode == 1 && batch <= kPdlChunk);
+    p.pdl = ctx->pdl_mode == 2 || (ctx->pdl_mode == 1 && (batch <= kPdlLatencyChunk || ctx->np >= 1024));
     p.c0 = (float)((ctx->n - 1) / 2.0);
     p.win_off = (ctx->np / 2 - 1) - (ctx->n - 1) / 2;
     p.nw = ctx->nw;
