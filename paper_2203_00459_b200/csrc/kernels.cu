@@ -405,6 +405,13 @@ __device__ __forceinline__ void gather_sums(const Params& p, const float2* m, in
 #ifndef FSCAN_K2A_PB
 #define FSCAN_K2A_PB 2
 #endif
+// (K2a alone 2.69 -> 2.37 ms; the three-lane pipeline already hid that latency:
+// C4 / C5 unchanged)
+#ifdef FSCAN_K2A_NO_PREFETCH
+constexpr bool kK2aPrefetch = false;
+#else
+constexpr bool kK2aPrefetch = true;
+#endif
 template <int PB>
 __global__ void __launch_bounds__(kGatherThreads) k_rot_gather_multi(Params p) {
     pdl_enter();
@@ -421,12 +428,24 @@ __global__ void __launch_bounds__(kGatherThreads) k_rot_gather_multi(Params p) {
     for (int b = 0; b < PB; ++b) af[b] = ag[b] = 0.0;
     const int np = min(PB, p.batch - pair0);
     constexpr int U = PB >= 4 ? 1 : 4 / PB;
-    for (int j0 = rsub; j0 < n_live; j0 += 4 * U) {
-        PolarTap e[U];
+    auto taps_at = [&](int j0, PolarTap (&e)[U]) {
 #pragma unroll
         for (int q = 0; q < U; ++q) {
             const int j = j0 + 4 * q;
             e[q] = (live && j < n_live) ? col[(size_t)j * nt] : PolarTap{0, 0.f, 0.f, 0.f};  // flags 0: 0
+        }
+    };
+    // kK2aPrefetch: the next step's tap entries are loaded before this step's
+    // gathers, so the two dependent loads of a sample (entry, then the taps it
+    // addresses) overlap across steps
+    PolarTap e[U];
+    if constexpr (kK2aPrefetch) taps_at(rsub, e);
+    for (int j0 = rsub; j0 < n_live; j0 += 4 * U) {
+        PolarTap en[U];
+        if constexpr (kK2aPrefetch) {
+            taps_at(j0 + 4 * U, en);
+        } else {
+            taps_at(j0, e);
         }
         float2 tv[PB][U][4];
 #pragma unroll
@@ -449,6 +468,10 @@ __global__ void __launch_bounds__(kGatherThreads) k_rot_gather_multi(Params p) {
                 af[b] += (double)bilerp(e[q].fr, e[q].fc, tv[b][q][0].x, tv[b][q][1].x, tv[b][q][2].x, tv[b][q][3].x);
                 ag[b] += (double)bilerp(e[q].fr, e[q].fc, tv[b][q][0].y, tv[b][q][1].y, tv[b][q][2].y, tv[b][q][3].y);
             }
+        if constexpr (kK2aPrefetch) {
+#pragma unroll
+            for (int q = 0; q < U; ++q) e[q] = en[q];
+        }
     }
 #pragma unroll
     for (int b = 0; b < PB; ++b) {
