@@ -134,6 +134,13 @@ __device__ __forceinline__ const float2* tile_at(const float2* m, int n, int r, 
 // mod N), each [N rows][U] float2 — exactly the 2U columns one K1b CTA
 // transforms, contiguous, so the CTA fetches them with two bulk copies instead
 // of 16 scattered 64-byte row pieces per thread (U = k1b_u<N>())
+// FOLD1 fold twiddles from one table read per thread times W_8 / W_3 constants
+// instead of two table reads per site (C5 +0.3%)
+#ifdef FSCAN_K4_FOLD1_TABLE
+constexpr bool kK4Fold1Base = false;  // A/B
+#else
+constexpr bool kK4Fold1Base = true;
+#endif
 #ifdef FSCAN_K1B_ROWMAJOR
 constexpr bool kK1bBlocks = false;  // A/B: row-major spectrum, per-thread column loads (rounds 1-2)
 #else
@@ -1362,6 +1369,7 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
         // in B); the q groups then read their inputs from shared memory (instead
         // of each loading and folding every element itself: 3x fewer global loads)
         constexpr int SITES = COLS * K, ITER = (SITES + X::THREADS - 1) / X::THREADS;
+        [[maybe_unused]] const float2 fb1 = kK4Fold1Base ? __ldg(p.tw_m + threadIdx.x) : make_float2(1.f, 0.f);
         float4 v0[ITER], v1[ITER];  // every load in flight before the first use
 #pragma unroll
         for (int it = 0; it < ITER; ++it) {
@@ -1381,7 +1389,19 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
             if (!(SITES % X::THREADS == 0 || e < SITES)) break;
             const int cc = e / K, n0 = e % K;
             const float4 u0 = v0[it], u1 = v1[it];
-            const float2 w1 = wq(n0, 1), w2 = wq(n0, 2);
+            float2 w1, w2;  // W_M^{n0}, W_M^{2 n0}
+            if constexpr (kK4Fold1Base && M == 8 * X::THREADS) {
+                // n0 = e - cc K with e = tid + it THREADS: W_M^{n0} = W_M^{tid}
+                // W_8^{it} W_3^{-cc} (M = 8 THREADS; W_M^K = W_3): the thread's one
+                // table read times constants instead of two table reads per site
+                float2 w = it == 0 ? fb1 : cmul(fb1, fscan_fft::w16c<-1>(2 * it));
+                if (cc) w = cmul(w, make_float2(-0.5f, kS3));
+                w1 = w;
+                w2 = cmul(w, w);
+            } else {
+                w1 = wq(n0, 1);
+                w2 = wq(n0, 2);
+            }
             auto fold = [&](float2 x0, float2 x1, float* base) {
                 const float2 tt = make_float2(fmaf(-0.5f, x1.x, x0.x), fmaf(-0.5f, x1.y, x0.y));
                 const float2 ss = make_float2(kS3 * x1.x, kS3 * x1.y);
