@@ -518,7 +518,10 @@ fscan_status launch(fscan_ctx* ctx, Lane& l, int kid, L&& fn, int* launches) {
         b = ctx->ev_pool[ctx->ev_used++];
         CK(cudaEventRecord(a, l.stream));
     }
-    CK(fn());
+    if (cudaError_t e = fn(); e != cudaSuccess) {  // name the kernel (KernelId) in the error
+        const std::string what = "kernel " + std::to_string(kid);
+        return cuda_fail(ctx, e, what.c_str());
+    }
     if (ctx->profiling) {
         CK(cudaEventRecord(b, l.stream));
         ctx->prof.push_back({kid, {a, b}});
