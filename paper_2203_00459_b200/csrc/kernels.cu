@@ -1687,11 +1687,20 @@ __global__ void __launch_bounds__(XOutGeom<N>::THREADS) k_xlat_out(Params p) {
         // times W_32^m, a compile-time constant-bank address (kK5TwTable: one
         // scattered W_M table read per element, ~40% of K5's L1 wavefronts)
         const float2 bk = kK5TwTable ? make_float2(1.f, 0.f) : wm(p.tw_m, 3 * t + q);
+        // the bins k0 + 3 T m (and H - k0 - 3 T m) of this thread keep the row
+        // permutation of k0 whenever 3 T is a multiple of y_swz's bit period (N >= 256):
+        // one base address per direction, compile-time offsets 3 T m RB
+        constexpr int SWB = ROWS >= 16 ? 0 : (ROWS == 8 ? 1 : 2);
+        constexpr bool HOIST = (3 * T) % (4 << SWB) == 0;
+        const int k0 = 3 * t + q;
+        const float2* yf = yblk + k0 * ROWS + (rl ^ y_swz(ROWS, k0));
+        const float2* yb = yblk + (H - k0) * ROWS + (rl ^ y_swz(ROWS, H - k0));
         float2 v[16];
 #pragma unroll
         for (int m = 0; m < 16; ++m) {
             const int k = 3 * (t + m * T) + q;
-            const float2 a = y(k), b = cconj(y(H - k));
+            const float2 a = HOIST ? yf[3 * T * m * ROWS] : y(k);
+            const float2 b = cconj(HOIST ? yb[-3 * T * m * ROWS] : y(H - k));
             const float2 A = cadd(a, b);
             const float2 wk = kK5TwTable ? wm(p.tw_m, k) : cmul(bk, w32(m));
             const float2 B = cmul(csub(a, b), cconj(wk));
