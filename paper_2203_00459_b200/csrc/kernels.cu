@@ -1265,6 +1265,26 @@ __global__ void __launch_bounds__(XColGeom<N>::THREADS, MINB) k_xlat_cols_mb(Par
     xlat_cols_body<N>(p);
 }
 
+// K4's two stores of combine slot j (m = q + 3 j, n0 = t + m T) go to rows
+// half - n0 and half - n0 + K of the Y layout. When RB divides T, a row step of
+// 3 T keeps the row's place inside its block, so both sequences are a base
+// address minus compile-time multiples of 3 T / RB block strides.
+template <int N>
+struct YStores {
+    static constexpr int RB = y_rows(N);
+    float2* d0;
+    float2* d1;
+    __device__ __forceinline__ YStores(float2* dst, int t, int q, int T, int kp) {
+        const int i0 = N / 2 - 1 - (t + q * T);
+        d0 = dst + y_at<N>(i0, kp);
+        d1 = dst + y_at<N>(i0 + N / 2, kp);
+    }
+    template <int T>
+    __device__ __forceinline__ static constexpr int step(int j) {
+        return -(3 * j * T / RB) * (3 * N / 4 + 1) * RB;
+    }
+};
+
 template <int N>
 __device__ __forceinline__ void xlat_cols_merged(const Params& p);
 
@@ -1469,6 +1489,7 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
     // transform hold 16 consecutive rows of one bin, whole RB-row runs
     float2* dst = p.zbuf + (size_t)pair * N * (H + 1);
     const bool store = kp <= H;  // the last block's clamped duplicates store nothing
+    [[maybe_unused]] const YStores<N> ys(dst, t, q, T, kp);
 #pragma unroll
     for (int j = 0; j < 6; ++j) {
         const int m = q + 3 * j;
@@ -1486,8 +1507,14 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
             const float2 x1 = cmul(cconj(v1), e1.get(n0));
             const float2 x2 = cmul(cconj(v2), e2.get(n0));
             if (store) {
-                dst[y_at<N>(half - n0, kp)] = cadd(x0, cadd(x1, x2));
-                dst[y_at<N>(half - (n0 - K), kp)] = cadd(x0, cadd(cmul(w31, x1), cmul(w32, x2)));
+                const float2 o0 = cadd(x0, cadd(x1, x2)), o1 = cadd(x0, cadd(cmul(w31, x1), cmul(w32, x2)));
+                if constexpr (T % YStores<N>::RB == 0) {
+                    ys.d0[YStores<N>::template step<T>(j)] = o0;
+                    ys.d1[YStores<N>::template step<T>(j)] = o1;
+                } else {
+                    dst[y_at<N>(half - n0, kp)] = o0;
+                    dst[y_at<N>(half - (n0 - K), kp)] = o1;
+                }
             }
         }
     }
@@ -1585,6 +1612,7 @@ __device__ __forceinline__ void xlat_cols_merged(const Params& p) {
                e2 = G::lay(smem + G::FLOATS, 3 * c + 2);
     float2* dst = p.zbuf + (size_t)pair * N * (H + 1);
     const bool store = kp <= H;
+    [[maybe_unused]] const YStores<N> ys(dst, t, q, T, kp);
 #pragma unroll
     for (int j = 0; j < 6; ++j) {
         const int m = q + 3 * j;
@@ -1593,9 +1621,16 @@ __device__ __forceinline__ void xlat_cols_merged(const Params& p) {
             const float2 x0 = e0.get(n0), x1 = e1.get(n0), x2 = e2.get(n0);
             const float2 sa = cadd(x1, x2), df = csub(x1, x2);
             if (store) {
-                dst[y_at<N>(half - n0, kp)] = cadd(x0, sa);
-                dst[y_at<N>(half - (n0 - K), kp)] = make_float2(fmaf(kS3, df.y, fmaf(-0.5f, sa.x, x0.x)),
-                                                                fmaf(-kS3, df.x, fmaf(-0.5f, sa.y, x0.y)));
+                const float2 o0 = cadd(x0, sa);
+                const float2 o1 = make_float2(fmaf(kS3, df.y, fmaf(-0.5f, sa.x, x0.x)),
+                                              fmaf(-kS3, df.x, fmaf(-0.5f, sa.y, x0.y)));
+                if constexpr (T % YStores<N>::RB == 0) {
+                    ys.d0[YStores<N>::template step<T>(j)] = o0;
+                    ys.d1[YStores<N>::template step<T>(j)] = o1;
+                } else {
+                    dst[y_at<N>(half - n0, kp)] = o0;
+                    dst[y_at<N>(half - (n0 - K), kp)] = o1;
+                }
             }
         }
     }
