@@ -1168,7 +1168,6 @@ __global__ void __launch_bounds__(kXThreads, 3) k_xlat_rows(Params p) {
         for (int k = kk; 3 * k + 2 <= H; k += KSTEP) put(3 * k + 2, sep(e2.get(k), e1.get(K - 1 - k)));
     }
 }
-}
 
 // ---------------------------------------------------------------- K4
 // Column k' of the row spectra. Group q: F_q = FFT_K(W_M^{nq}(F[n] + W_3^q F[n+K]))
