@@ -223,10 +223,24 @@ __global__ void FSCAN_K1A_BOUNDS k_rot_rows(Params p) {
         v[m] = make_float2(fv * w, gv * w);
     }
     fft_regs<N, -1, (G::T <= 32)>(v, t, lay, p.tw_n);  // a row per warp (or two warps at N = 1024)
+    constexpr int UB = k1b_u<N>();
+    // HOIST: with U dividing T, column x = t + m T sits in direct block t / U + m T / U
+    // and its mirror N - x in mirror block (N - t) / U - m T / U, both at a fixed
+    // slot: one base address each, compile-time offsets (x = 0's mirror, column
+    // 0 itself, is stored separately)
+    constexpr bool HOIST = kK1bBlocks && T % UB == 0;
+    [[maybe_unused]] float2* zd = p.zbuf + k1b_at<N>(pair, p.zcols, 0, t, y);
+    [[maybe_unused]] float2* zm = p.zbuf + k1b_at<N>(pair, p.zcols, 1, N - t, y);  // (t = 0: one block past, m >= 1 only)
+    if constexpr (HOIST)
+        if (t == 0) p.zbuf[k1b_at<N>(pair, p.zcols, 1, 0, y)] = v[0];
 #pragma unroll
     for (int m = 0; m < 16; ++m) {
         const int x = t + m * T;
-        if constexpr (kK1bBlocks) {
+        if constexpr (HOIST) {
+            constexpr int STEP = (T / UB) * N * UB;
+            if (x < p.zcols) zd[m * STEP] = v[m];
+            if (x > N - p.zcols) zm[-m * STEP] = v[m];
+        } else if constexpr (kK1bBlocks) {
             // the columns K1b reads, in its column blocks (k1b_at)
             if (x < p.zcols) p.zbuf[k1b_at<N>(pair, p.zcols, 0, x, y)] = v[m];
             if (x == 0 || x > N - p.zcols) p.zbuf[k1b_at<N>(pair, p.zcols, 1, (N - x) & (N - 1), y)] = v[m];
