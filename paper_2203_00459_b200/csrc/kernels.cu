@@ -2022,9 +2022,12 @@ __global__ void k_polar_to_cart(const float* polar0, const float* polar1, int n_
     const int pair = blockIdx.y;
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= n * n) return;
-    const float* polar = (blockIdx.z ? polar1 : polar0) + (size_t)pair * n_az * n_range;
-    float* out = blockIdx.z ? out1 : out0;
-    out[(size_t)pair * n * n + idx] = (float)fscan_k0::polar_sample(polar, n_range, tab[idx]);
+    // both sweeps of the pair from one read of the cell's tap (geometry shared)
+    const fscan_k0::PolarTap tp = tab[idx];
+    const size_t po = (size_t)pair * n_az * n_range, oo = (size_t)pair * n * n + idx;
+    const float v0 = (float)fscan_k0::polar_sample(polar0 + po, n_range, tp);
+    if (polar1) out1[oo] = (float)fscan_k0::polar_sample(polar1 + po, n_range, tp);
+    out0[oo] = v0;
 }
 
 // Brute-force correlative search (oracle.cpp:21-67): per (pair, candidate)
@@ -2295,7 +2298,7 @@ cudaError_t launch_polar_to_cart(const float* d_polar0, const float* d_polar1, i
         if (e != cudaSuccess) return e;
         tab = own;
     }
-    k_polar_to_cart<<<dim3((unsigned)((total + 255) / 256), batch, d_polar1 ? 2 : 1), 256, 0, stream>>>(
+    k_polar_to_cart<<<dim3((unsigned)((total + 255) / 256), batch), 256, 0, stream>>>(
         d_polar0, d_polar1, n_az, n_range, n, static_cast<const fscan_k0::PolarTap*>(tab), d_out0, d_out1);
     cudaError_t e = cudaGetLastError();
     if (own) cudaFreeAsync(own, stream);
