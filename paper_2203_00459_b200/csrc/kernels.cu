@@ -141,6 +141,11 @@ constexpr bool kK4Fold1Base = false;  // A/B
 #else
 constexpr bool kK4Fold1Base = true;
 #endif
+#ifdef FSCAN_K1A_FLAG_CMP
+constexpr bool kK1aFlagAcc = false;  // A/B: per-element compares for the input flags
+#else
+constexpr bool kK1aFlagAcc = true;
+#endif
 #ifdef FSCAN_K1B_ROWMAJOR
 constexpr bool kK1bBlocks = false;  // A/B: row-major spectrum, per-thread column loads (rounds 1-2)
 #else
@@ -203,24 +208,58 @@ __global__ void FSCAN_K1A_BOUNDS k_rot_rows(Params p) {
     const float hy = p.hann[y];
     int badf = 0, badg = 0;  // bit0 non-finite, bit1 mask outside [0, 1]
     float2 v[16];
-#pragma unroll
-    for (int m = 0; m < 16; ++m) {
-        const int x = t + m * T;
-        float fv = __ldg(fp + x);
-        float gv = __ldg(gp + x);
-        if (mfp) {
-            const float a = __ldg(mfp + x), b = __ldg(mgp + x);
-            if (!(a >= 0.0f && a <= 1.0f)) badf |= 2;
-            if (!(b >= 0.0f && b <= 1.0f)) badg |= 2;
-            fv *= a;
-            gv *= b;
-        }
-        if (!isfinite(fv)) badf |= 1;
-        if (!isfinite(gv)) badg |= 1;
+    auto finish = [&](int m, int x, float fv, float gv) {
         ftp[x] = fv;
         gtp[x] = gv;
         const float w = hy * __ldg(p.hann + x);
         v[m] = make_float2(fv * w, gv * w);
+    };
+    if constexpr (kK1aFlagAcc) {
+        // flags as running values instead of per-element compares: fma(x, 0, c)
+        // turns NaN for any non-finite x (inf * 0 = NaN) and stays 0 otherwise;
+        // the masks' range as a running min / max (fminf / fmaxf skip NaN, which
+        // the fma check then catches) — the same tests as !isfinite(f * m) and
+        // !(m >= 0 && m <= 1), per scan
+        float cf = 0.f, cg = 0.f, ca = 0.f, cb = 0.f, alo = 0.f, ahi = 1.f, blo = 0.f, bhi = 1.f;
+        if (mfp) {
+#pragma unroll
+            for (int m = 0; m < 16; ++m) {
+                const int x = t + m * T;
+                const float a = __ldg(mfp + x), b = __ldg(mgp + x);
+                const float fv = __ldg(fp + x) * a, gv = __ldg(gp + x) * b;
+                alo = fminf(alo, a), ahi = fmaxf(ahi, a), blo = fminf(blo, b), bhi = fmaxf(bhi, b);
+                ca = fmaf(a, 0.f, ca), cb = fmaf(b, 0.f, cb);
+                cf = fmaf(fv, 0.f, cf), cg = fmaf(gv, 0.f, cg);
+                finish(m, x, fv, gv);
+            }
+        } else {
+#pragma unroll
+            for (int m = 0; m < 16; ++m) {
+                const int x = t + m * T;
+                const float fv = __ldg(fp + x), gv = __ldg(gp + x);
+                cf = fmaf(fv, 0.f, cf), cg = fmaf(gv, 0.f, cg);
+                finish(m, x, fv, gv);
+            }
+        }
+        badf = (cf != cf ? 1 : 0) | ((alo < 0.f || ahi > 1.f || ca != ca) ? 2 : 0);
+        badg = (cg != cg ? 1 : 0) | ((blo < 0.f || bhi > 1.f || cb != cb) ? 2 : 0);
+    } else {
+#pragma unroll
+        for (int m = 0; m < 16; ++m) {
+            const int x = t + m * T;
+            float fv = __ldg(fp + x);
+            float gv = __ldg(gp + x);
+            if (mfp) {
+                const float a = __ldg(mfp + x), b = __ldg(mgp + x);
+                if (!(a >= 0.0f && a <= 1.0f)) badf |= 2;
+                if (!(b >= 0.0f && b <= 1.0f)) badg |= 2;
+                fv *= a;
+                gv *= b;
+            }
+            if (!isfinite(fv)) badf |= 1;
+            if (!isfinite(gv)) badg |= 1;
+            finish(m, x, fv, gv);
+        }
     }
     fft_regs<N, -1, (G::T <= 32)>(v, t, lay, p.tw_n);  // a row per warp (or two warps at N = 1024)
     constexpr int UB = k1b_u<N>();
