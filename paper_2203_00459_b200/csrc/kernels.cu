@@ -462,6 +462,13 @@ __device__ __forceinline__ void gather_sums(const Params& p, const float2* m, in
 // PB pairs per CTA (independent pairs only): every tap-table entry is loaded once
 // for PB magnitude planes (the table read is a third of K2a's load bytes), and a
 // thread keeps PB x U taps in flight
+// radius phases per azimuth in k_rot_gather_multi, by grid side (a property of
+// the configuration, so results never depend on the batch split): 8 for N <= 256
+// (C1 +10%, C2 +1.2%: shorter per-thread radial loops), 4 above (C4: 8 phases
+// measured -1.3%, 16 -4%, the samples of a load then spread along the rays)
+#ifndef FSCAN_K2A_RP_SMALL
+#define FSCAN_K2A_RP_SMALL 8
+#endif
 #ifndef FSCAN_K2A_PB
 #define FSCAN_K2A_PB 2
 #endif
@@ -472,14 +479,15 @@ constexpr bool kK2aPrefetch = false;
 #else
 constexpr bool kK2aPrefetch = true;
 #endif
-template <int PB>
+template <int PB, int RP>
 __global__ void __launch_bounds__(kGatherThreads) k_rot_gather_multi(Params p) {
     pdl_enter();
     const int pair0 = blockIdx.y * PB;
     const int nt = p.n_theta, n = p.n, n_live = p.n_live;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int i = blockIdx.x * (kGatherThreads / 4) + warp * 8 + (lane >> 2);
-    const int rsub = lane & 3;
+    // RP radius phases per azimuth (lane = RP * azimuth + phase; k2a_rp)
+    const int i = blockIdx.x * (kGatherThreads / RP) + warp * (32 / RP) + lane / RP;
+    const int rsub = lane % RP;
     const bool live = i < nt;
     const float2* m0 = reinterpret_cast<const float2*>(p.mag) + (size_t)pair0 * p.mag_plane;
     const PolarTap* col = p.taps + (live ? i : 0);
@@ -491,7 +499,7 @@ __global__ void __launch_bounds__(kGatherThreads) k_rot_gather_multi(Params p) {
     auto taps_at = [&](int j0, PolarTap (&e)[U]) {
 #pragma unroll
         for (int q = 0; q < U; ++q) {
-            const int j = j0 + 4 * q;
+            const int j = j0 + RP * q;
             e[q] = (live && j < n_live) ? col[(size_t)j * nt] : PolarTap{0, 0.f, 0.f, 0.f};  // flags 0: 0
         }
     };
@@ -500,10 +508,10 @@ __global__ void __launch_bounds__(kGatherThreads) k_rot_gather_multi(Params p) {
     // addresses) overlap across steps
     PolarTap e[U];
     if constexpr (kK2aPrefetch) taps_at(rsub, e);
-    for (int j0 = rsub; j0 < n_live; j0 += 4 * U) {
+    for (int j0 = rsub; j0 < n_live; j0 += RP * U) {
         PolarTap en[U];
         if constexpr (kK2aPrefetch) {
-            taps_at(j0 + 4 * U, en);
+            taps_at(j0 + RP * U, en);
         } else {
             taps_at(j0, e);
         }
@@ -535,12 +543,13 @@ __global__ void __launch_bounds__(kGatherThreads) k_rot_gather_multi(Params p) {
     }
 #pragma unroll
     for (int b = 0; b < PB; ++b) {
-        // the four radius phases of an azimuth, summed in a fixed order
+        // the RP radius phases of an azimuth, summed in a fixed order
         double a = af[b], g = ag[b];
-        a += __shfl_xor_sync(0xffffffffu, a, 1);
-        g += __shfl_xor_sync(0xffffffffu, g, 1);
-        a += __shfl_xor_sync(0xffffffffu, a, 2);
-        g += __shfl_xor_sync(0xffffffffu, g, 2);
+#pragma unroll
+        for (int o = 1; o < RP; o <<= 1) {
+            a += __shfl_xor_sync(0xffffffffu, a, o);
+            g += __shfl_xor_sync(0xffffffffu, g, o);
+        }
         if (live && rsub == 0 && b < np) {
             double* prof = p.prof + (size_t)(pair0 + b) * 2 * nt;
             prof[i] = a;
@@ -2237,9 +2246,13 @@ cudaError_t launch_rot_gather(const Params& p, cudaStream_t s) {
     if (p.n_theta == 1) return cudaSuccess;
     if (FSCAN_K2A_PB > 1 && !p.chain) {
         constexpr int PB = FSCAN_K2A_PB > 1 ? FSCAN_K2A_PB : 2;
-        return launch_k(k_rot_gather_multi<PB>,
-                        dim3((p.n_theta + kGatherThreads / 4 - 1) / (kGatherThreads / 4), (p.batch + PB - 1) / PB),
-                        dim3(kGatherThreads), 0, s, p, p);
+        auto go = [&](auto kernel, int rp) {
+            const int az = kGatherThreads / rp;  // azimuths per CTA
+            return launch_k(kernel, dim3((p.n_theta + az - 1) / az, (p.batch + PB - 1) / PB), dim3(kGatherThreads),
+                            0, s, p, p);
+        };
+        if (p.n <= 256) return go(k_rot_gather_multi<PB, FSCAN_K2A_RP_SMALL>, FSCAN_K2A_RP_SMALL);
+        return go(k_rot_gather_multi<PB, 4>, 4);
     }
     return launch_k(k_rot_gather, dim3((p.n_theta + kGatherThreads / 4 - 1) / (kGatherThreads / 4), p.batch),
                     dim3(kGatherThreads), 0, s, p, p);
