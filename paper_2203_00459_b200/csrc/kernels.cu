@@ -1257,6 +1257,9 @@ constexpr bool kK4W48Fold1 = true;  // A/B: W_48 combine twiddles at N = 1024 to
 #else
 constexpr bool kK4W48Fold1 = false;
 #endif
+#ifndef FSCAN_K4_COLS512
+#define FSCAN_K4_COLS512 4  // K4 columns per CTA at N = 512
+#endif
 #ifndef FSCAN_K4_F2_MIN
 #define FSCAN_K4_F2_MIN 64
 #endif
@@ -1289,7 +1292,7 @@ struct XColGeom {
     // shorter CTAs interleaving better with the other lane's kernels)
     // (N = 1024 at 2 columns: 192-thread CTAs, three per SM at 96 registers;
     // C5 +8% over 4 columns in 384 threads at 80 registers)
-    static constexpr int COLS = (T >= 32) ? 2 : ((T >= 16) ? 4 : ((T >= 4) ? 8 : 16));
+    static constexpr int COLS = (T >= 32) ? 2 : ((T >= 16) ? FSCAN_K4_COLS512 : ((T >= 4) ? 8 : 16));
     static constexpr int THREADS = 3 * COLS * T;
     // (outputs are stored from registers into the blocked Y layout, y_at; round
     // 1-2 staged them in an [N][COLS + 1] shared tile copied out row-major,
