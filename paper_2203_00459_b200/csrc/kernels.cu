@@ -146,6 +146,9 @@ constexpr bool kK1aFlagAcc = false;  // A/B: per-element compares for the input 
 #else
 constexpr bool kK1aFlagAcc = true;
 #endif
+#ifndef FSCAN_K1B_U512
+#define FSCAN_K1B_U512 8  // K1b output columns per CTA at N = 512
+#endif
 #ifdef FSCAN_K1B_ROWMAJOR
 constexpr bool kK1bBlocks = false;  // A/B: row-major spectrum, per-thread column loads (rounds 1-2)
 #else
@@ -153,7 +156,7 @@ constexpr bool kK1bBlocks = true;
 #endif
 template <int N>
 __host__ __device__ constexpr int k1b_u() {
-    return N >= 1024 ? 4 : 8;
+    return N >= 1024 ? 4 : (N == 512 ? FSCAN_K1B_U512 : 8);
 }
 // float2 offset of column slot c of direct (mirror = 0) or mirror (1) block b, row y
 template <int N>
