@@ -362,14 +362,34 @@ constexpr bool kTwRK = std::is_same_v<TW, SmemTwRK>;
 //    over the last-stage butterfly k, which joins its input twiddles:
 //    W_K^{-r k} W_M^{-k q} = conj(F[k][3r + q]) (r = 0 included).
 constexpr int kQS = 49;  // odd row stride: the inverse's column reads F[k][.] spread over banks
-struct SmemTwQF {
+// S: the table's row stride; G: the table read through L1 from global memory
+// (__ldg) instead of a shared-memory copy
+template <int S, bool G>
+struct TwQF {
     const float2* f;
+    __device__ __forceinline__ float2 at(int i) const { return G ? __ldg(f + i) : f[i]; }
 };
-struct SmemTwQI {
+template <int S, bool G>
+struct TwQI {
     const float2* f;
+    __device__ __forceinline__ float2 at(int i) const { return G ? __ldg(f + i) : f[i]; }
+};
+using SmemTwQF = TwQF<kQS, false>;
+using SmemTwQI = TwQI<kQS, false>;
+template <typename TW>
+struct TwQInfo {
+    static constexpr int kind = 0, S = 0;
+};
+template <int S_, bool G>
+struct TwQInfo<TwQF<S_, G>> {
+    static constexpr int kind = 1, S = S_;
+};
+template <int S_, bool G>
+struct TwQInfo<TwQI<S_, G>> {
+    static constexpr int kind = 2, S = S_;
 };
 template <typename TW>
-constexpr bool kTwQ = std::is_same_v<TW, SmemTwQF> || std::is_same_v<TW, SmemTwQI>;
+constexpr bool kTwQ = TwQInfo<TW>::kind != 0;
 
 // Radix-16 twiddles as powers of one table read (global tables) or all read
 // from the table (shared-memory tables).
@@ -431,14 +451,16 @@ __device__ __forceinline__ void stage(float2 (&v)[16], int t, const L& lay, cons
             if constexpr (POWJ) {
 #pragma unroll
                 for (int r = 1; r < R; ++r) u[r] = cmul(u[r], j == 0 ? tb[r] : cmul(tb[r], w16c<SIGN>(r * j)));
-            } else if constexpr (std::is_same_v<TW, SmemTwQF>) {
+            } else if constexpr (TwQInfo<TW>::kind == 1) {
                 static_assert(Ns == 16 && LAST, "merged twiddles: two-stage transforms only");
+                constexpr int S = TwQInfo<TW>::S;
 #pragma unroll
-                for (int r = 1; r < R; ++r) u[r] = cmul(u[r], tw.f[r * kQS + 3 * k]);
-            } else if constexpr (std::is_same_v<TW, SmemTwQI>) {
+                for (int r = 1; r < R; ++r) u[r] = cmul(u[r], tw.at(r * S + 3 * k));
+            } else if constexpr (TwQInfo<TW>::kind == 2) {
                 static_assert(Ns == 16 && LAST, "merged twiddles: two-stage transforms only");
+                constexpr int S = TwQInfo<TW>::S;
 #pragma unroll
-                for (int r = 0; r < R; ++r) u[r] = cmul(u[r], cconj(tw.f[k * kQS + 3 * r]));
+                for (int r = 0; r < R; ++r) u[r] = cmul(u[r], cconj(tw.at(k * S + 3 * r)));
             } else if constexpr (Ns == 16 && kTwRK<TW>) {
                 // W_{16 R}^{r k} = W_256^{(16/R) r k}
 #pragma unroll

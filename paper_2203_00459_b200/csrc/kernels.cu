@@ -1260,6 +1260,11 @@ constexpr bool kK4W48Fold1 = true;  // A/B: W_48 combine twiddles at N = 1024 to
 #else
 constexpr bool kK4W48Fold1 = false;
 #endif
+#ifdef FSCAN_K4_TAB_GLOBAL
+constexpr bool kK4TabGlobal = true;  // A/B: merged twiddle table read through L1 instead of staged
+#else
+constexpr bool kK4TabGlobal = false;
+#endif
 #ifndef FSCAN_K4_COLS512
 #define FSCAN_K4_COLS512 4  // K4 columns per CTA at N = 512
 #endif
@@ -1624,7 +1629,7 @@ __device__ __forceinline__ void xlat_cols_merged(const Params& p) {
     using G = typename X::G;
     constexpr int T = G::T, COLS = X::COLS;
     constexpr int R = K / 16, NB = 16 / R;  // last-stage radix and butterflies per thread
-    constexpr int QS = fscan_fft::kQS;
+    [[maybe_unused]] constexpr int QS = fscan_fft::kQS;
     constexpr int half = N / 2 - 1;
     static_assert(K >= 32 && K <= 256 && R * 16 == K, "two-stage K-point transforms");
     extern __shared__ __align__(128) float smem[];
@@ -1642,17 +1647,23 @@ __device__ __forceinline__ void xlat_cols_merged(const Params& p) {
     // the table's global loads are all issued first and stored to shared memory
     // only after the first fold (a load -> store loop waited out one L2 round
     // trip per iteration: ~15% of K4's warp samples)
-    constexpr int TE = 16 * 48, TPT = (TE + X::THREADS - 1) / X::THREADS;
-    float2 tv[TPT];
+    // (kK4TabGlobal: the stages read the table through L1 from global memory —
+    // no per-CTA staging, its loads or its barrier)
+    constexpr int TE = 16 * 48, TPT = kK4TabGlobal ? 1 : (TE + X::THREADS - 1) / X::THREADS;
+    [[maybe_unused]] float2 tv[TPT];
+    if constexpr (!kK4TabGlobal) {
 #pragma unroll
-    for (int k = 0; k < TPT; ++k) {
-        const int i = threadIdx.x + k * X::THREADS;
-        if (TE % X::THREADS == 0 || i < TE) tv[k] = __ldg(p.tw_k4 + i);
+        for (int k = 0; k < TPT; ++k) {
+            const int i = threadIdx.x + k * X::THREADS;
+            if (TE % X::THREADS == 0 || i < TE) tv[k] = __ldg(p.tw_k4 + i);
+        }
     }
     pdl_enter();
     // W_3^q = (c1, wi): s = x0 + W_3^q x1 in four FMAs
     const float c1 = q ? -0.5f : 1.0f, wi = q == 0 ? 0.0f : (q == 1 ? -kS3 : kS3);
-    const float2* fq = tab + q;  // F[.][3k + q]
+    const float2* fq = kK4TabGlobal ? p.tw_k4 + q : tab + q;  // F[.][3k + q]
+    using TQF = std::conditional_t<kK4TabGlobal, fscan_fft::TwQF<48, true>, fscan_fft::SmemTwQF>;
+    using TQI = std::conditional_t<kK4TabGlobal, fscan_fft::TwQI<48, true>, fscan_fft::SmemTwQI>;
     // W_M^{m T q} = W_48^{m q} and W_M^{16 r' q} = W_48^{(16 / R) r' q} from the
     // constant-bank table (one address per half-warp)
     auto win = [&](int m) { return w48(m * q); };
@@ -1667,13 +1678,15 @@ __device__ __forceinline__ void xlat_cols_merged(const Params& p) {
         const int n0 = t + m * T;
         a[m] = fold(srcF[n0], srcF[n0 + K], m);
     }
+    if constexpr (!kK4TabGlobal) {
 #pragma unroll
-    for (int k = 0; k < TPT; ++k) {
-        const int i = threadIdx.x + k * X::THREADS;
-        if (TE % X::THREADS == 0 || i < TE) tab[(i / 48) * QS + i % 48] = tv[k];
+        for (int k = 0; k < TPT; ++k) {
+            const int i = threadIdx.x + k * X::THREADS;
+            if (TE % X::THREADS == 0 || i < TE) tab[(i / 48) * QS + i % 48] = tv[k];
+        }
+        __syncthreads();  // the table (the fold reads none of it)
     }
-    __syncthreads();  // the table (the fold reads none of it)
-    fft_regs<K, -1, true>(a, t, bufA, fscan_fft::SmemTwQF{fq});
+    fft_regs<K, -1, true>(a, t, bufA, TQF{fq});
 #pragma unroll
     for (int m = 0; m < 16; ++m) bufA.put(t + m * T, a[m]);  // park F_q (own slots)
 #pragma unroll
@@ -1681,7 +1694,7 @@ __device__ __forceinline__ void xlat_cols_merged(const Params& p) {
         const int n0 = t + m * T;
         a[m] = fold(srcG[n0], srcG[n0 + K], m);
     }
-    fft_regs<K, -1, true>(a, t, bufB, fscan_fft::SmemTwQF{fq});
+    fft_regs<K, -1, true>(a, t, bufB, TQF{fq});
 #pragma unroll
     for (int m = 0; m < 16; ++m) a[m] = cmul(cconj(bufA.get(t + m * T)), a[m]);  // conj(F) G
     if (p.phase) {  // opt-in phase correlation: X / |X| (0 where X = 0), SURVEY a21
@@ -1692,7 +1705,7 @@ __device__ __forceinline__ void xlat_cols_merged(const Params& p) {
             a[m] = make_float2(a[m].x * inv, a[m].y * inv);
         }
     }
-    fft_regs<K, +1, true>(a, t, bufB, fscan_fft::SmemTwQI{fq});
+    fft_regs<K, +1, true>(a, t, bufB, TQI{fq});
 #pragma unroll
     for (int m = 0; m < 16; ++m) bufB.put(t + m * T, cmul(a[m], cconj(wout(m / NB))));
     __syncthreads();
