@@ -847,7 +847,16 @@ fscan_status fscan_ctx_create(int device, const fscan_config* cfg_in, int max_ba
     ctx->alloc_chunk = chunk;
     CK(cudaEventCreateWithFlags(&ctx->start_ev, cudaEventDisableTiming));
     for (Lane& l : LaneRange{ctx}) {
-        CK(cudaStreamCreateWithFlags(&l.stream, cudaStreamNonBlocking));
+        if (const char* e = std::getenv("FSCAN_LANE_PRIO"); e && std::atoi(e)) {
+            // A/B: graded lane priorities (lane 0 highest), so one lane's kernels
+            // are scheduled ahead and the lanes stay phase-shifted
+            int lo = 0, hi = 0;
+            CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            const int li = (int)(&l - ctx->lanes_);
+            CK(cudaStreamCreateWithPriority(&l.stream, cudaStreamNonBlocking, std::min(lo, hi + li)));
+        } else {
+            CK(cudaStreamCreateWithFlags(&l.stream, cudaStreamNonBlocking));
+        }
         CK(cudaEventCreateWithFlags(&l.done, cudaEventDisableTiming));
         fscan_status a = alloc_lane(ctx, l, chunk);
         if (a != FSCAN_OK) return a;
