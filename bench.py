@@ -112,7 +112,10 @@ def kernel_alg_bytes(name: str, n: int, wcols: int, masks: bool = True) -> float
         "rot_polar": 0.0,                                 # profiles only (fp64 correlation)
         "xlat_rows": 8 * nn + 16 * n * h1,                # f~,g~ in; row spectra (F,G; M/2+1 bins) out
         "xlat_cols": 16 * n * h1 + 8 * n * h1,            # row spectra in; Y (N lags x M/2+1) out
-        "xlat_out": 8 * n * h1 + 4 * nn,                  # Y in; surface out
+        # Y in; surface out, except in the two-pass form (N >= 512 without requested
+        # surfaces: block maxima, then xlat_win recomputes the soft-argmax window rows)
+        "xlat_out": 8 * n * h1 + (0 if n >= 512 else 4 * nn),
+        "xlat_win": 0.0,                                  # a few Y row blocks per pair (< 8% of xlat_out)
         "finalize": 0.0, "theta_in": 0.0, "mag_unpack": 0.0, "bf_items": 0.0, "bf_final": 0.0,
         "polar_to_cart": 2 * (4 * POLAR_Q + 4 * nn),      # both raw sweeps in, both grids out
     }[name]

@@ -338,7 +338,8 @@ class Matcher:
         return lib().fscan_ctx_rot_columns(self._h)
 
     KERNELS = ("rot_rows", "rot_cols", "rot_polar", "theta_in", "xlat_rows", "xlat_cols", "xlat_out",
-               "finalize", "rot_gather", "polar_to_cart", "mag_unpack", "bf_items", "bf_final")
+               "finalize", "rot_gather", "polar_to_cart", "mag_unpack", "bf_items", "bf_final",
+               "xlat_win")
 
     def set_phase_correlation(self, on: bool):
         """Opt-in phase correlation in the translation stage (fscan_cuda.h)."""

@@ -461,7 +461,7 @@ enum class Stages { Full, Rotation, Translation, Magnitude };
 // Kernel ids for per-kernel profiling (fscan_ctx_kernel_times).
 enum KernelId { kRotRows = 0, kRotCols, kRotPolar, kThetaIn, kXlatRows, kXlatCols, kXlatOut, kFinalize,
                 kRotGather, kPolarToCart,
-                kMagUnpack, kBfItems, kBfFinal, kNumKernels };
+                kMagUnpack, kBfItems, kBfFinal, kXlatWin, kNumKernels };
 
 struct ProfEvent {
     int kid;
@@ -499,6 +499,7 @@ fscan_status run_chunk(fscan_ctx* ctx, Lane& l, Params p, Stages what, int* laun
         FSCAN_LAUNCH(kXlatRows, launch_xlat_rows);
         FSCAN_LAUNCH(kXlatCols, launch_xlat_cols);
         FSCAN_LAUNCH(kXlatOut, launch_xlat_out);
+        if (xlat_win_pass(p)) FSCAN_LAUNCH(kXlatWin, launch_xlat_win);
         FSCAN_LAUNCH(kFinalize, launch_finalize);
     }
 #undef FSCAN_LAUNCH
@@ -1200,6 +1201,7 @@ fscan_status fscan_odometry_batch(fscan_ctx* ctx, const float* d_scans, const fl
         FSCAN_LAUNCH(kXlatRows, launch_xlat_rows, p);
         FSCAN_LAUNCH(kXlatCols, launch_xlat_cols, p);
         FSCAN_LAUNCH(kXlatOut, launch_xlat_out, p);
+        if (xlat_win_pass(p)) FSCAN_LAUNCH(kXlatWin, launch_xlat_win, p);
         FSCAN_LAUNCH(kFinalize, launch_finalize, p);
 #undef FSCAN_LAUNCH
         return FSCAN_OK;

@@ -26,6 +26,12 @@
 #include "polar.h"
 
 
+#ifndef FSCAN_K5_TWO_PASS
+#define FSCAN_K5_TWO_PASS 1  // K5 block maxima only + soft-argmax window rows recomputed (k_xlat_out modes)
+#endif
+#ifndef FSCAN_K5_TWO_PASS_MIN_N
+#define FSCAN_K5_TWO_PASS_MIN_N 512
+#endif
 #ifndef FSCAN_K3_U
 #define FSCAN_K3_U 4  // K3 gather: cells per thread with their loads in flight together
 #endif
@@ -1784,7 +1790,23 @@ struct XOutGeom {
 // EMB: only the lag window [win_off, win_off + p.n)^2 of the embedded surface
 // competes for the argmax, and the surface stays in the workspace (K6 copies
 // the window out).
-template <int N, bool EMB>
+// MODE (kOutFull / kOutMax / kOutWin): the full surface (rows stored unless
+// p.skip_surface), or the two-pass throughput form — kOutMax keeps only the
+// block maxima (no surface store: 4N^2 bytes and ~20 STG per thread less),
+// then kOutWin recomputes just the row blocks the soft-argmax window of the
+// pair's peak touches (grid.x = window blocks, the peak reduced from the
+// kOutMax partials exactly as K6 reduces them) and stores those rows; the
+// values are the same instructions on the same inputs, so bit-identical.
+constexpr int kOutFull = 0, kOutMax = 1, kOutWin = 2;
+
+__device__ __forceinline__ void better(float& bv, int& bi, float v, int i) {
+    if (v > bv || (v == bv && i < bi)) {
+        bv = v;
+        bi = i;
+    }
+}
+
+template <int N, bool EMB, int MODE = kOutFull>
 __global__ void __launch_bounds__(XOutGeom<N>::THREADS) k_xlat_out(Params p) {
     pdl_enter();
     constexpr int K = N / 2, M = 3 * K, H = M / 2;
@@ -1798,19 +1820,47 @@ __global__ void __launch_bounds__(XOutGeom<N>::THREADS) k_xlat_out(Params p) {
     __shared__ float red_v[NW];
     __shared__ int red_i[NW];
     const int pair = blockIdx.y;
+    int blk = blockIdx.x;
+    __shared__ int win_blk, win_r0, win_r1, win_c0, win_c1;  // kOutWin: the peak's window
+    if constexpr (MODE == kOutWin) {
+        // the pair's peak from the kOutMax block maxima (K6's reduction), then
+        // this CTA's block among those rows [pr - w, pr + w] touches
+        if (threadIdx.x < 32) {
+            constexpr int NP = N / ROWS;
+            const Partial* pp = p.part + (size_t)pair * NP;
+            float bv = -INFINITY;
+            int bi = 0x7fffffff;
+            for (int b = threadIdx.x; b < NP; b += 32) better(bv, bi, pp[b].val, pp[b].idx);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1)
+                better(bv, bi, __shfl_xor_sync(0xffffffffu, bv, o), __shfl_xor_sync(0xffffffffu, bi, o));
+            if (threadIdx.x == 0) {
+                const int pk = bi == 0x7fffffff ? 0 : bi, pr = pk / N, pc = pk % N;
+                win_r0 = max(0, pr - p.window);
+                win_r1 = min(N - 1, pr + p.window);
+                win_c0 = max(0, pc - p.window);
+                win_c1 = min(N - 1, pc + p.window);
+                const int b0 = win_r0 / ROWS, b1 = win_r1 / ROWS;
+                win_blk = b0 + (int)blockIdx.x <= b1 ? b0 + (int)blockIdx.x : -1;
+            }
+        }
+        __syncthreads();
+        blk = win_blk;
+        if (blk < 0) return;
+    }
     int tr, t;
     G::map(threadIdx.x, tr, t);
     // q-major transform order (kK5QMajor): the transforms of a half-warp are one
     // q group of adjacent rows; with the row permutation of the Y blocks their
     // stride-3 bin reads fall on distinct bank pairs (y_swz)
     const int rl = kK5QMajor ? tr % ROWS : tr / 3, q = kK5QMajor ? tr / ROWS : tr % 3;
-    const int i = blockIdx.x * ROWS + rl;
+    const int i = blk * ROWS + rl;
     const auto buf = G::lay(smem, tr);
     {
         // kK5Tma: the block by one bulk copy (the per-thread global loads of the
         // stride-3 pattern left every warp waiting on its own loads; a per-thread
         // cp.async staging measured slower than those loads)
-        const float2* yblk = p.zbuf + ((size_t)pair * N + blockIdx.x * ROWS) * (H + 1);
+        const float2* yblk = p.zbuf + ((size_t)pair * N + blk * ROWS) * (H + 1);
         if constexpr (kK5Tma) {
             __shared__ uint64_t mbar;
             if (threadIdx.x == 0) mbar_init(&mbar, 1);
@@ -1852,11 +1902,17 @@ __global__ void __launch_bounds__(XOutGeom<N>::THREADS) k_xlat_out(Params p) {
     const float scale = 1.0f / ((float)M * (float)M);
     float* srow = ((p.xy_surf && !EMB) ? p.xy_surf : p.surf) + ((size_t)pair * N + i) * N;
     const bool row_in = !EMB || (i >= p.win_off && i < p.win_off + p.n);
+    bool win_row = false;
+    if constexpr (MODE == kOutWin) win_row = i >= win_r0 && i <= win_r1;
     float best_v = -INFINITY;
     int best_i = 0x7fffffff;
     auto emit = [&](int kx, float val) {
         const int j = kx + half;
-        if (!p.skip_surface) srow[j] = val;
+        if constexpr (MODE == kOutWin) {  // only the window cells K6 reads
+            if (win_row && j >= win_c0 && j <= win_c1) srow[j] = val;
+            return;
+        }
+        if (MODE == kOutFull && !p.skip_surface) srow[j] = val;
         const int li = i * N + j;
         if (EMB && !(row_in && j >= p.win_off && j < p.win_off + p.n)) return;
         if (val > best_v || (val == best_v && li < best_i)) {
@@ -1892,28 +1948,30 @@ __global__ void __launch_bounds__(XOutGeom<N>::THREADS) k_xlat_out(Params p) {
             }
         }
     }
+    if constexpr (MODE != kOutWin) {  // block maximum -> p.part
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const float ov = __shfl_xor_sync(0xffffffffu, best_v, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, best_i, o);
-        if (ov > best_v || (ov == best_v && oi < best_i)) {
-            best_v = ov;
-            best_i = oi;
-        }
-    }
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (lane == 0) {
-        red_v[warp] = best_v;
-        red_i[warp] = best_i;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int w = 1; w < NW; ++w)
-            if (red_v[w] > best_v || (red_v[w] == best_v && red_i[w] < best_i)) {
-                best_v = red_v[w];
-                best_i = red_i[w];
+        for (int o = 16; o > 0; o >>= 1) {
+            const float ov = __shfl_xor_sync(0xffffffffu, best_v, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, best_i, o);
+            if (ov > best_v || (ov == best_v && oi < best_i)) {
+                best_v = ov;
+                best_i = oi;
             }
-        p.part[(size_t)pair * gridDim.x + blockIdx.x] = Partial{best_v, best_i};
+        }
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        if (lane == 0) {
+            red_v[warp] = best_v;
+            red_i[warp] = best_i;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int w = 1; w < NW; ++w)
+                if (red_v[w] > best_v || (red_v[w] == best_v && red_i[w] < best_i)) {
+                    best_v = red_v[w];
+                    best_i = red_i[w];
+                }
+            p.part[(size_t)pair * gridDim.x + blk] = Partial{best_v, best_i};
+        }
     }
 }
 
@@ -2231,6 +2289,9 @@ cudaError_t xlat_cols(const Params& p, cudaStream_t s) {
 }
 
 template <int N>
+cudaError_t xlat_win(const Params& p, cudaStream_t s);
+
+template <int N>
 cudaError_t xlat_out(const Params& p, cudaStream_t s) {
     using X = XOutGeom<N>;
     const dim3 grid(N / X::ROWS, p.batch);
@@ -2239,10 +2300,29 @@ cudaError_t xlat_out(const Params& p, cudaStream_t s) {
         if (e != cudaSuccess) return e;
         return launch_k(kernel, grid, dim3(X::THREADS), X::SMEM, s, p, p);
     };
-    return p.embed ? go(k_xlat_out<N, true>) : go(k_xlat_out<N, false>);
+    if (p.embed) return go(k_xlat_out<N, true>);
+    return xlat_win_pass(p) ? go(k_xlat_out<N, false, kOutMax>) : go(k_xlat_out<N, false>);
+}
+
+template <int N>
+cudaError_t xlat_win(const Params& p, cudaStream_t s) {
+    using X = XOutGeom<N>;
+    constexpr int NB = N / X::ROWS;
+    // row blocks a window of 2w + 1 rows can touch
+    const int nb = std::min(NB, (2 * p.window + X::ROWS - 1) / X::ROWS + 1);
+    cudaError_t e = set_smem(k_xlat_out<N, false, kOutWin>, X::SMEM);
+    if (e != cudaSuccess) return e;
+    return launch_k(k_xlat_out<N, false, kOutWin>, dim3(nb, p.batch), dim3(X::THREADS), X::SMEM, s, p, p);
 }
 
 }  // namespace
+
+// Two-pass K5 (kOutMax + kOutWin) whenever no caller reads the full surface:
+// not for embedded grids (K6 copies their lag window out of it), requested
+// xy surfaces or the exhaustive search (block maxima only)
+bool xlat_win_pass(const Params& p) {
+    return FSCAN_K5_TWO_PASS && p.np >= FSCAN_K5_TWO_PASS_MIN_N && !p.embed && !p.xy_surf && !p.skip_surface;
+}
 
 int rows_per_block_out(int n) {
     switch (n) {
@@ -2260,6 +2340,7 @@ cudaError_t launch_rot_cols(const Params& p, cudaStream_t s) { FSCAN_DISPATCH_N(
 cudaError_t launch_xlat_rows(const Params& p, cudaStream_t s) { FSCAN_DISPATCH_N(p.np, xlat_rows) }
 cudaError_t launch_xlat_cols(const Params& p, cudaStream_t s) { FSCAN_DISPATCH_N(p.np, xlat_cols) }
 cudaError_t launch_xlat_out(const Params& p, cudaStream_t s) { FSCAN_DISPATCH_N(p.np, xlat_out) }
+cudaError_t launch_xlat_win(const Params& p, cudaStream_t s) { FSCAN_DISPATCH_N(p.np, xlat_win) }
 
 cudaError_t launch_rot_gather(const Params& p, cudaStream_t s) {
     if (p.n_theta == 1) return cudaSuccess;

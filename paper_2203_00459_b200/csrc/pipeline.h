@@ -145,6 +145,8 @@ cudaError_t launch_theta_in(const Params& p, cudaStream_t s);        // stage AP
 cudaError_t launch_xlat_rows(const Params& p, cudaStream_t s);       // K3
 cudaError_t launch_xlat_cols(const Params& p, cudaStream_t s);       // K4
 cudaError_t launch_xlat_out(const Params& p, cudaStream_t s);        // K5
+cudaError_t launch_xlat_win(const Params& p, cudaStream_t s);        // K5 window rows (two-pass form)
+bool xlat_win_pass(const Params& p);  // K5 runs as block maxima + window rows
 cudaError_t launch_finalize(const Params& p, cudaStream_t s);        // K6
 cudaError_t launch_mag_unpack(const Params& p, cudaStream_t s);      // stage API helper
 cudaError_t launch_bf_items(const Params& p, cudaStream_t s);        // brute force: item argmax

@@ -1096,3 +1096,32 @@ def test_programmatic_dependent_launch_is_result_neutral(fb, dev, monkeypatch):
             outs.append(m.match_device(F, G, MF, MG, delta=delta).clone())
         torch.cuda.synchronize()
     assert all(torch.equal(o, outs[0]) for o in outs)
+
+
+@pytest.mark.parametrize("n", [512, 1024])
+def test_two_pass_out_equals_full_surface(fb, dev, n):
+    """K5's two-pass throughput form (block maxima only, then the soft-argmax
+    window rows recomputed; taken at N >= 512 when no xy surface is requested)
+    against the full-surface path: byte-identical result rows, with peaks on the
+    lag-window borders (clipped windows) and windows from 3 rows to wider than
+    the grid, normalised and not."""
+    spec = fb.synth_spec(1, n=n, delta=0.5)
+    f, _, _, _, _ = fb.synth_pairs_host(spec, 11, 1)
+    h = n // 2
+    shifts = [(0, 0), (h - 1, 3), (-h + 1, -5), (7, h - 2), (-3, -h + 2), (h - 1, -h + 2), (h - 8, h - 8)]
+    ff = np.repeat(f, len(shifts), axis=0)
+    gg = np.stack([np.roll(f[0], s, axis=(0, 1)) for s in shifts])
+    F, G = to_dev(dev, ff, gg)
+    b = len(shifts)
+    for w, norm in ((1, True), (2, False), (16, True), (40, False), (3 * n, True)):
+        cfg = fb.MatchConfig.for_grid(n, 0.5, 90, softargmax_window=w, normalize_scores=norm)
+        m = fb.Matcher(cfg, max_batch=b)
+        xs = torch.zeros((b, n, n), dtype=torch.float32, device=dev)
+        full = fb.decode_results(m.match_device(F, G, delta=0.5, xy_surface=xs))
+        two = fb.decode_results(m.match_device(F, G, delta=0.5))
+        torch.cuda.synchronize()
+        assert full.tobytes() == two.tobytes(), (w, norm)
+        th = torch.zeros(b, dtype=torch.float64, device=dev)
+        t_full = m.estimate_translation(F, G, th, delta=0.5, xy_surface=xs).cpu().numpy()
+        t_two = m.estimate_translation(F, G, th, delta=0.5).cpu().numpy()
+        assert t_full.tobytes() == t_two.tobytes(), (w, norm)
