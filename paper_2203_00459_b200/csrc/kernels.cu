@@ -1280,6 +1280,12 @@ constexpr bool kK4TabGlobal = false;
 #ifndef FSCAN_K4_MINB512
 #define FSCAN_K4_MINB512 3
 #endif
+#ifndef FSCAN_K4_GSTAGE_BODY
+#define FSCAN_K4_GSTAGE_BODY 0
+#endif
+#ifndef FSCAN_K4_GSTAGE
+#define FSCAN_K4_GSTAGE 1  // merged K4 (N = 512): G columns prefetched by TMA during the F pass (C4 +1.0%)
+#endif
 #ifdef FSCAN_K4_EARLYSYNC
 constexpr bool kK4LateSync = false;  // A/B: the table barrier before the first fold's loads
 #else
@@ -1334,7 +1340,11 @@ struct XColGeom {
     // CTAs/SM, +10% C2), as the linear M-entry table at 512 (measured faster)
     static constexpr bool SPLIT_WM = N < 512;
     static constexpr size_t TW_FLOATS = (size_t)2 * (240 + TW_LIN + (SMEM_WM ? (SPLIT_WM ? 2 : 3) * (N / 2) : 0));
-    static constexpr size_t SMEM = (WORK_FLOATS + TW_FLOATS) * sizeof(float);
+    // FSCAN_K4_GSTAGE_BODY (A/B, plain path below N = 1024): the CTA's G columns by
+    // one TMA bulk copy into a stage behind the tables during the F pass
+    static constexpr bool GST_BODY = FSCAN_K4_GSTAGE_BODY && N < 512;
+    static constexpr size_t BODY_BASE = ((WORK_FLOATS + TW_FLOATS) * sizeof(float) + 127) / 128 * 128;
+    static constexpr size_t SMEM = GST_BODY ? BODY_BASE + (size_t)COLS * N * sizeof(float2) : (WORK_FLOATS + TW_FLOATS) * sizeof(float);
     // explicit residency targets where ptxas' own choice leaves the SM
     // register-bound (N = 256: 4 CTAs of 192 threads; N = 1024: 3 of 192)
     // (N = 512 without the staged W_M table: 54 KB of shared memory, three CTAs
@@ -1349,7 +1359,11 @@ struct XColGeom {
     // merged-twiddle path (xlat_cols_merged, two-stage K-point transforms):
     // the exchange buffers + the [16][kQS] table W_M^{a j}
     static constexpr bool MERGE = kK4Merge && !FOLD1 && N == 512;
-    static constexpr size_t SMEM_MERGE = (FFT_FLOATS + 2 * 16 * fscan_fft::kQS) * sizeof(float);
+    // FSCAN_K4_GSTAGE (A/B): the CTA's G columns (COLS x N float2, contiguous in
+    // the G plane) by one TMA bulk copy issued before the F pass, 1 = into their
+    // own stage behind the table, 2 = into buffer B (idle until G's transform)
+    static constexpr size_t MERGE_BASE = ((FFT_FLOATS + 2 * 16 * fscan_fft::kQS) * sizeof(float) + 127) / 128 * 128;
+    static constexpr size_t SMEM_MERGE = MERGE_BASE + (FSCAN_K4_GSTAGE == 1 ? (size_t)COLS * N * sizeof(float2) : 0);
 };
 
 template <int N>
@@ -1467,6 +1481,16 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
         else return wq(n0, q);
     };
     pdl_enter();
+    [[maybe_unused]] __shared__ uint64_t g_bar;
+    [[maybe_unused]] float2* gst = reinterpret_cast<float2*>(reinterpret_cast<char*>(smem) + X::BODY_BASE);
+    if constexpr (X::GST_BODY) {
+        if (threadIdx.x == 0) {
+            const int k0 = blockIdx.x * COLS;
+            const int nc = (H + 1 - k0) < COLS ? (H + 1 - k0) : COLS;
+            mbar_init(&g_bar, 1);
+            bulk_load(gst, fgt_plane<N>(p, pair, 1) + (size_t)k0 * N, (unsigned)(nc * N * sizeof(float2)), &g_bar);
+        }
+    }
     // LATE: the F fold reads no staged table, so its global loads are issued
     // before the barrier that publishes the twiddle tables (the table and input
     // load latencies overlap instead of following one another)
@@ -1557,10 +1581,16 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
         for (int m = 0; m < 16; ++m) a[m] = bufB.get(t + m * T);
         __syncwarp();
     } else {
+        const float2* gs = srcG;
+        if constexpr (X::GST_BODY) {
+            static_assert(!X::GST_BODY || (kK4LateSync && !X::SMEM_WM), "the table barrier publishes g_bar");
+            mbar_wait(&g_bar, 0);
+            gs = gst + (kq - blockIdx.x * COLS) * N;
+        }
 #pragma unroll
         for (int m = 0; m < 16; ++m) {
             const int n0 = t + m * T;
-            const float2 s = cadd(srcG[n0], cmul(w3q, srcG[n0 + K]));
+            const float2 s = cadd(gs[n0], cmul(w3q, gs[n0 + K]));
             a[m] = q ? cmul(wq_m(m, n0), s) : s;
         }
     }
@@ -1665,6 +1695,20 @@ __device__ __forceinline__ void xlat_cols_merged(const Params& p) {
         }
     }
     pdl_enter();
+    constexpr int GST = FSCAN_K4_GSTAGE;
+    [[maybe_unused]] __shared__ uint64_t g_bar;
+    [[maybe_unused]] float2* gst = reinterpret_cast<float2*>(
+        GST == 1 ? reinterpret_cast<char*>(smem) + X::MERGE_BASE : reinterpret_cast<char*>(smem + G::FLOATS));
+    if constexpr (GST != 0) {
+        static_assert(GST == 1 || G::FLOATS * sizeof(float) >= (size_t)COLS * N * sizeof(float2), "buffer B holds the G columns");
+        if (threadIdx.x == 0) {
+            const int k0 = blockIdx.x * COLS;
+            const int nc = (H + 1 - k0) < COLS ? (H + 1 - k0) : COLS;
+            mbar_init(&g_bar, 1);
+            bulk_load(gst, fgt_plane<N>(p, pair, 1) + (size_t)k0 * N,
+                      (unsigned)(nc * N * sizeof(float2)), &g_bar);
+        }
+    }
     // W_3^q = (c1, wi): s = x0 + W_3^q x1 in four FMAs
     const float c1 = q ? -0.5f : 1.0f, wi = q == 0 ? 0.0f : (q == 1 ? -kS3 : kS3);
     const float2* fq = kK4TabGlobal ? p.tw_k4 + q : tab + q;  // F[.][3k + q]
@@ -1695,10 +1739,22 @@ __device__ __forceinline__ void xlat_cols_merged(const Params& p) {
     fft_regs<K, -1, true>(a, t, bufA, TQF{fq});
 #pragma unroll
     for (int m = 0; m < 16; ++m) bufA.put(t + m * T, a[m]);  // park F_q (own slots)
+    if constexpr (GST != 0) {
+        static_assert(!kK4TabGlobal, "the table barrier publishes g_bar");
+        mbar_wait(&g_bar, 0);
+        const float2* gs = gst + (kq - blockIdx.x * COLS) * N;  // (the last block holds fewer columns)
 #pragma unroll
-    for (int m = 0; m < 16; ++m) {
-        const int n0 = t + m * T;
-        a[m] = fold(srcG[n0], srcG[n0 + K], m);
+        for (int m = 0; m < 16; ++m) {
+            const int n0 = t + m * T;
+            a[m] = fold(gs[n0], gs[n0 + K], m);
+        }
+        if constexpr (GST == 2) __syncthreads();  // every staged read before buffer B's exchange writes
+    } else {
+#pragma unroll
+        for (int m = 0; m < 16; ++m) {
+            const int n0 = t + m * T;
+            a[m] = fold(srcG[n0], srcG[n0 + K], m);
+        }
     }
     fft_regs<K, -1, true>(a, t, bufB, TQF{fq});
 #pragma unroll
