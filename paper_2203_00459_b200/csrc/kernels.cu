@@ -80,6 +80,9 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned b
                  ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
                  : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
@@ -1280,6 +1283,9 @@ constexpr bool kK4TabGlobal = false;
 #ifndef FSCAN_K4_MINB512
 #define FSCAN_K4_MINB512 3
 #endif
+#ifndef FSCAN_K4_BLOCKS
+#define FSCAN_K4_BLOCKS 1
+#endif
 #ifndef FSCAN_K4_GSTAGE_BODY
 #define FSCAN_K4_GSTAGE_BODY 0
 #endif
@@ -1362,6 +1368,9 @@ struct XColGeom {
     // FSCAN_K4_GSTAGE (A/B): the CTA's G columns (COLS x N float2, contiguous in
     // the G plane) by one TMA bulk copy issued before the F pass, 1 = into their
     // own stage behind the table, 2 = into buffer B (idle until G's transform)
+    // column blocks per pair, and per CTA on the merged path (FSCAN_K4_BLOCKS)
+    static constexpr int NBLOCKS = (3 * N / 4 + 1 + COLS - 1) / COLS;
+    static constexpr int NBLK = (kK4Merge && N == 512 && FSCAN_K4_GSTAGE == 1) ? FSCAN_K4_BLOCKS : 1;
     static constexpr size_t MERGE_BASE = ((FFT_FLOATS + 2 * 16 * fscan_fft::kQS) * sizeof(float) + 127) / 128 * 128;
     static constexpr size_t SMEM_MERGE = MERGE_BASE + (FSCAN_K4_GSTAGE == 1 ? (size_t)COLS * N * sizeof(float2) : 0);
 };
@@ -1673,12 +1682,18 @@ __device__ __forceinline__ void xlat_cols_merged(const Params& p) {
     int tr, t;
     G::map(threadIdx.x, tr, t);
     const int c = tr / 3, q = tr % 3;
-    const int kp = blockIdx.x * COLS + c;
-    const int kq = kp <= H ? kp : H;  // the last block may hold fewer columns
+    // NBLK consecutive column blocks per CTA (X::NBLK > 1 needs the G stage): the
+    // first block's F columns come by per-thread loads, every later block's by a
+    // bulk copy into the stage issued while the block before it is still in its
+    // product / inverse / combine phases; the stage alternates G(b), F(b+1),
+    // G(b+1), ... (`e_bar` counts the threads done reading it)
+    constexpr int GST = FSCAN_K4_GSTAGE;
+    constexpr int NBLK = X::NBLK;
+    static_assert(NBLK == 1 || GST == 1, "several blocks per CTA stream through the G stage");
+    const int b0 = blockIdx.x * NBLK;
+    const int nb = NBLK == 1 ? 1 : (X::NBLOCKS - b0 < NBLK ? X::NBLOCKS - b0 : NBLK);
     const auto bufA = G::lay(smem, tr);
     const auto bufB = G::lay(smem + G::FLOATS, tr);
-    const float2* srcF = fgt_plane<N>(p, pair, 0) + (size_t)kq * N;
-    const float2* srcG = fgt_plane<N>(p, pair, 1) + (size_t)kq * N;
     float2* tab = reinterpret_cast<float2*>(smem + X::FFT_FLOATS);  // [16][QS]
     // the table's global loads are all issued first and stored to shared memory
     // only after the first fold (a load -> store loop waited out one L2 round
@@ -1695,18 +1710,24 @@ __device__ __forceinline__ void xlat_cols_merged(const Params& p) {
         }
     }
     pdl_enter();
-    constexpr int GST = FSCAN_K4_GSTAGE;
-    [[maybe_unused]] __shared__ uint64_t g_bar;
+    [[maybe_unused]] __shared__ uint64_t g_bar, f_bar, e_bar;
     [[maybe_unused]] float2* gst = reinterpret_cast<float2*>(
         GST == 1 ? reinterpret_cast<char*>(smem) + X::MERGE_BASE : reinterpret_cast<char*>(smem + G::FLOATS));
+    // the stage <- the (up to) COLS columns of block `blk` of plane 0 (F) / 1 (G)
+    [[maybe_unused]] auto stage_block = [&](int plane, int blk, uint64_t* bar) {
+        const int k0 = blk * COLS;
+        const int nc = (H + 1 - k0) < COLS ? (H + 1 - k0) : COLS;
+        bulk_load(gst, fgt_plane<N>(p, pair, plane) + (size_t)k0 * N, (unsigned)(nc * N * sizeof(float2)), bar);
+    };
     if constexpr (GST != 0) {
         static_assert(GST == 1 || G::FLOATS * sizeof(float) >= (size_t)COLS * N * sizeof(float2), "buffer B holds the G columns");
         if (threadIdx.x == 0) {
-            const int k0 = blockIdx.x * COLS;
-            const int nc = (H + 1 - k0) < COLS ? (H + 1 - k0) : COLS;
             mbar_init(&g_bar, 1);
-            bulk_load(gst, fgt_plane<N>(p, pair, 1) + (size_t)k0 * N,
-                      (unsigned)(nc * N * sizeof(float2)), &g_bar);
+            if constexpr (NBLK > 1) {
+                mbar_init(&f_bar, 1);
+                mbar_init(&e_bar, X::THREADS);
+            }
+            stage_block(1, b0, &g_bar);
         }
     }
     // W_3^q = (c1, wi): s = x0 + W_3^q x1 in four FMAs
@@ -1722,78 +1743,114 @@ __device__ __forceinline__ void xlat_cols_merged(const Params& p) {
         const float2 sv = make_float2(fmaf(-wi, x1.y, fmaf(c1, x1.x, x0.x)), fmaf(wi, x1.x, fmaf(c1, x1.y, x0.y)));
         return cmul(sv, win(m));
     };
-    float2 a[16];
-#pragma unroll
-    for (int m = 0; m < 16; ++m) {
-        const int n0 = t + m * T;
-        a[m] = fold(srcF[n0], srcF[n0 + K], m);
-    }
-    if constexpr (!kK4TabGlobal) {
-#pragma unroll
-        for (int k = 0; k < TPT; ++k) {
-            const int i = threadIdx.x + k * X::THREADS;
-            if (TE % X::THREADS == 0 || i < TE) tab[(i / 48) * QS + i % 48] = tv[k];
-        }
-        __syncthreads();  // the table (the fold reads none of it)
-    }
-    fft_regs<K, -1, true>(a, t, bufA, TQF{fq});
-#pragma unroll
-    for (int m = 0; m < 16; ++m) bufA.put(t + m * T, a[m]);  // park F_q (own slots)
-    if constexpr (GST != 0) {
-        static_assert(!kK4TabGlobal, "the table barrier publishes g_bar");
-        mbar_wait(&g_bar, 0);
-        const float2* gs = gst + (kq - blockIdx.x * COLS) * N;  // (the last block holds fewer columns)
-#pragma unroll
-        for (int m = 0; m < 16; ++m) {
-            const int n0 = t + m * T;
-            a[m] = fold(gs[n0], gs[n0 + K], m);
-        }
-        if constexpr (GST == 2) __syncthreads();  // every staged read before buffer B's exchange writes
-    } else {
-#pragma unroll
-        for (int m = 0; m < 16; ++m) {
-            const int n0 = t + m * T;
-            a[m] = fold(srcG[n0], srcG[n0 + K], m);
-        }
-    }
-    fft_regs<K, -1, true>(a, t, bufB, TQF{fq});
-#pragma unroll
-    for (int m = 0; m < 16; ++m) a[m] = cmul(cconj(bufA.get(t + m * T)), a[m]);  // conj(F) G
-    if (p.phase) {  // opt-in phase correlation: X / |X| (0 where X = 0), SURVEY a21
-#pragma unroll
-        for (int m = 0; m < 16; ++m) {
-            const float mag = sqrtf(a[m].x * a[m].x + a[m].y * a[m].y);
-            const float inv = mag > 0.0f ? 1.0f / mag : 0.0f;
-            a[m] = make_float2(a[m].x * inv, a[m].y * inv);
-        }
-    }
-    fft_regs<K, +1, true>(a, t, bufB, TQI{fq});
-#pragma unroll
-    for (int m = 0; m < 16; ++m) bufB.put(t + m * T, cmul(a[m], cconj(wout(m / NB))));
-    __syncthreads();
-    // radix-3 combine of the pre-twiddled e_q; group q handles slots m = q, q+3, ...
-    const auto e0 = G::lay(smem + G::FLOATS, 3 * c), e1 = G::lay(smem + G::FLOATS, 3 * c + 1),
-               e2 = G::lay(smem + G::FLOATS, 3 * c + 2);
     float2* dst = p.zbuf + (size_t)pair * N * (H + 1);
-    const bool store = kp <= H;
-    [[maybe_unused]] const YStores<N> ys(dst, t, q, T, kp);
+    [[maybe_unused]] unsigned ephase = 0;
+#pragma unroll 1
+    for (int ib = 0; ib < nb; ++ib) {
+        const int blk = b0 + ib;
+        const int kp = blk * COLS + c;
+        const int kq = kp <= H ? kp : H;  // the last block may hold fewer columns
+        [[maybe_unused]] const float2* stg = gst + (kq - blk * COLS) * N;  // this thread's column in the stage
+        float2 a[16];
+        if (NBLK == 1 || ib == 0) {
+            const float2* srcF = fgt_plane<N>(p, pair, 0) + (size_t)kq * N;
 #pragma unroll
-    for (int j = 0; j < 6; ++j) {
-        const int m = q + 3 * j;
-        if (m < 16) {
-            const int n0 = t + m * T;
-            const float2 x0 = e0.get(n0), x1 = e1.get(n0), x2 = e2.get(n0);
-            const float2 sa = cadd(x1, x2), df = csub(x1, x2);
-            if (store) {
-                const float2 o0 = cadd(x0, sa);
-                const float2 o1 = make_float2(fmaf(kS3, df.y, fmaf(-0.5f, sa.x, x0.x)),
-                                              fmaf(-kS3, df.x, fmaf(-0.5f, sa.y, x0.y)));
-                if constexpr (T % YStores<N>::RB == 0) {
-                    ys.d0[YStores<N>::template step<T>(j)] = o0;
-                    ys.d1[YStores<N>::template step<T>(j)] = o1;
-                } else {
-                    dst[y_at<N>(half - n0, kp)] = o0;
-                    dst[y_at<N>(half - (n0 - K), kp)] = o1;
+            for (int m = 0; m < 16; ++m) {
+                const int n0 = t + m * T;
+                a[m] = fold(srcF[n0], srcF[n0 + K], m);
+            }
+            if constexpr (!kK4TabGlobal) {
+#pragma unroll
+                for (int k = 0; k < TPT; ++k) {
+                    const int i = threadIdx.x + k * X::THREADS;
+                    if (TE % X::THREADS == 0 || i < TE) tab[(i / 48) * QS + i % 48] = tv[k];
+                }
+                __syncthreads();  // the table (the fold reads none of it) and the mbarriers
+            }
+        } else {
+            mbar_wait(&f_bar, (ib - 1) & 1);
+#pragma unroll
+            for (int m = 0; m < 16; ++m) {
+                const int n0 = t + m * T;
+                a[m] = fold(stg[n0], stg[n0 + K], m);
+            }
+            mbar_arrive(&e_bar);
+            if (threadIdx.x == 0) {  // every thread has read F: the stage takes this block's G
+                mbar_wait(&e_bar, ephase);
+                stage_block(1, blk, &g_bar);
+            }
+            ephase ^= 1;
+        }
+        fft_regs<K, -1, true>(a, t, bufA, TQF{fq});
+#pragma unroll
+        for (int m = 0; m < 16; ++m) bufA.put(t + m * T, a[m]);  // park F_q (own slots)
+        if constexpr (GST != 0) {
+            static_assert(!kK4TabGlobal, "the table barrier publishes g_bar");
+            mbar_wait(&g_bar, ib & 1);
+#pragma unroll
+            for (int m = 0; m < 16; ++m) {
+                const int n0 = t + m * T;
+                a[m] = fold(stg[n0], stg[n0 + K], m);
+            }
+            if constexpr (GST == 2) __syncthreads();  // every staged read before buffer B's exchange writes
+            if constexpr (NBLK > 1) {
+                if (ib + 1 < nb) {
+                    mbar_arrive(&e_bar);
+                    if (threadIdx.x == 0) {  // every thread has read G: the stage takes the next block's F
+                        mbar_wait(&e_bar, ephase);
+                        stage_block(0, blk + 1, &f_bar);
+                    }
+                    ephase ^= 1;
+                }
+            }
+        } else {
+            const float2* srcG = fgt_plane<N>(p, pair, 1) + (size_t)kq * N;
+#pragma unroll
+            for (int m = 0; m < 16; ++m) {
+                const int n0 = t + m * T;
+                a[m] = fold(srcG[n0], srcG[n0 + K], m);
+            }
+        }
+        fft_regs<K, -1, true>(a, t, bufB, TQF{fq});
+#pragma unroll
+        for (int m = 0; m < 16; ++m) a[m] = cmul(cconj(bufA.get(t + m * T)), a[m]);  // conj(F) G
+        if (p.phase) {  // opt-in phase correlation: X / |X| (0 where X = 0), SURVEY a21
+#pragma unroll
+            for (int m = 0; m < 16; ++m) {
+                const float mag = sqrtf(a[m].x * a[m].x + a[m].y * a[m].y);
+                const float inv = mag > 0.0f ? 1.0f / mag : 0.0f;
+                a[m] = make_float2(a[m].x * inv, a[m].y * inv);
+            }
+        }
+        fft_regs<K, +1, true>(a, t, bufB, TQI{fq});
+#pragma unroll
+        for (int m = 0; m < 16; ++m) bufB.put(t + m * T, cmul(a[m], cconj(wout(m / NB))));
+        __syncthreads();
+        // radix-3 combine of the pre-twiddled e_q; group q handles slots m = q, q+3, ...
+        // (several blocks per CTA: the next block's first write to buffer B follows
+        // its wait on g_bar, i.e. every thread's arrival after this combine)
+        const auto e0 = G::lay(smem + G::FLOATS, 3 * c), e1 = G::lay(smem + G::FLOATS, 3 * c + 1),
+                   e2 = G::lay(smem + G::FLOATS, 3 * c + 2);
+        const bool store = kp <= H;
+        [[maybe_unused]] const YStores<N> ys(dst, t, q, T, kp);
+#pragma unroll
+        for (int j = 0; j < 6; ++j) {
+            const int m = q + 3 * j;
+            if (m < 16) {
+                const int n0 = t + m * T;
+                const float2 x0 = e0.get(n0), x1 = e1.get(n0), x2 = e2.get(n0);
+                const float2 sa = cadd(x1, x2), df = csub(x1, x2);
+                if (store) {
+                    const float2 o0 = cadd(x0, sa);
+                    const float2 o1 = make_float2(fmaf(kS3, df.y, fmaf(-0.5f, sa.x, x0.x)),
+                                                  fmaf(-kS3, df.x, fmaf(-0.5f, sa.y, x0.y)));
+                    if constexpr (T % YStores<N>::RB == 0) {
+                        ys.d0[YStores<N>::template step<T>(j)] = o0;
+                        ys.d1[YStores<N>::template step<T>(j)] = o1;
+                    } else {
+                        dst[y_at<N>(half - n0, kp)] = o0;
+                        dst[y_at<N>(half - (n0 - K), kp)] = o1;
+                    }
                 }
             }
         }
@@ -2331,7 +2388,7 @@ template <int N>
 cudaError_t xlat_cols(const Params& p, cudaStream_t s) {
     using X = XColGeom<N>;
     constexpr int H = 3 * N / 4;
-    const dim3 grid((H + 1 + X::COLS - 1) / X::COLS, p.batch);
+    const dim3 grid(X::MERGE ? (X::NBLOCKS + X::NBLK - 1) / X::NBLK : (H + 1 + X::COLS - 1) / X::COLS, p.batch);
     constexpr size_t SMEM = X::MERGE ? X::SMEM_MERGE : X::SMEM;
     auto go = [&](auto kernel) {
         cudaError_t e = set_smem(kernel, SMEM);
