@@ -486,6 +486,11 @@ __device__ __forceinline__ void gather_sums(const Params& p, const float2* m, in
 #endif
 // (K2a alone 2.69 -> 2.37 ms; the three-lane pipeline already hid that latency:
 // C4 / C5 unchanged)
+#ifdef FSCAN_K2A_TILE_AT
+constexpr bool kK2aOffsets = false;  // A/B: tile_at per tap
+#else
+constexpr bool kK2aOffsets = true;
+#endif
 #ifdef FSCAN_K2A_NO_PREFETCH
 constexpr bool kK2aPrefetch = false;
 #else
@@ -528,6 +533,34 @@ __global__ void __launch_bounds__(kGatherThreads) k_rot_gather_multi(Params p) {
             taps_at(j0, e);
         }
         float2 tv[PB][U][4];
+        if constexpr (kK2aOffsets) {
+            // the four tile offsets of an entry once for all PB planes, in 32-bit
+            // arithmetic: (r0, u) -> o, (r0, u+1) -> o + 1 or into the next tile
+            // column (+ 8 n - 7), row r0 + 1 -> + 8 (tile_at per tap was 36% of the
+            // kernel's instructions)
+            unsigned off[U][4];
+#pragma unroll
+            for (int q = 0; q < U; ++q) {
+                const unsigned r0 = e[q].packed & 0xFFF, u = (e[q].packed >> 12) & 0xFFF;
+                const unsigned o = ((u / kTileW) * (unsigned)n + r0) * kTileW + (u % kTileW);
+                const unsigned o1 = o + ((u % kTileW) == kTileW - 1 ? (unsigned)n * kTileW - (kTileW - 1) : 1u);
+                off[q][0] = o;
+                off[q][1] = o1;
+                off[q][2] = o + kTileW;
+                off[q][3] = o1 + kTileW;
+            }
+#pragma unroll
+            for (int b = 0; b < PB; ++b) {
+                const float2* m = m0 + (size_t)(b < np ? b : 0) * p.mag_plane;
+#pragma unroll
+                for (int q = 0; q < U; ++q) {
+                    const int fl = e[q].packed >> 24;
+#pragma unroll
+                    for (int tp = 0; tp < 4; ++tp)
+                        tv[b][q][tp] = ((fl >> tp) & 1) ? __ldg(m + off[q][tp]) : make_float2(0.f, 0.f);
+                }
+            }
+        } else {
 #pragma unroll
         for (int b = 0; b < PB; ++b) {
             const float2* m = m0 + (size_t)(b < np ? b : 0) * p.mag_plane;
@@ -540,6 +573,7 @@ __global__ void __launch_bounds__(kGatherThreads) k_rot_gather_multi(Params p) {
                     tv[b][q][tp] = on ? __ldg(tile_at(m, n, r0 + (tp >> 1), u + (tp & 1))) : make_float2(0.f, 0.f);
                 }
             }
+        }
         }
 #pragma unroll
         for (int b = 0; b < PB; ++b)
