@@ -28,8 +28,10 @@ def col(r, name):
 
 recs = []
 for r in rows[2:]:
-    k = r[hdr.index("Kernel Name")].split("(")[0].split("::")[-1]
-    k = k.split("<")[0].replace("k_", "", 1)
+    full = r[hdr.index("Kernel Name")].split("(")[0].split("::")[-1]
+    k = full.split("<")[0].replace("k_", "", 1)
+    if k == "xlat_out" and full.rstrip(">").replace(" ", "").endswith(",2"):
+        k = "xlat_win"  # the two-pass K5's window pass (MODE = kOutWin), bench.py's stage name
     for suffix in ("_mb", "_multi"):  # launch-bound / multi-pair instantiations report under the stage name
         if k.endswith(suffix):
             k = k[: -len(suffix)]

@@ -15,5 +15,5 @@ CMD="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-proxy --no-exha
 $CMD > $O/${T}_small.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_(rot_|xlat_|finalize)" -c 600 --csv --log-file $O/${T}_launches.csv $CMD > $O/${T}_ncu_list.log 2>&1
 echo "ncu list rc=$?"
-ncu --set full --clock-control none --import-source on -k regex:"rot_rows|rot_cols|rot_gather|rot_polar|xlat_rows|xlat_cols|xlat_out|finalize" -s 16 -c 8 -o $O/${T}_full $CMD > $O/${T}_ncu_full.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"rot_rows|rot_cols|rot_gather|rot_polar|xlat_rows|xlat_cols|xlat_out|finalize" -s 18 -c 9 -o $O/${T}_full $CMD > $O/${T}_ncu_full.log 2>&1
 echo "ncu full rc=$?"
