@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <math.h>
+#include <stdlib.h>
 #include <stdint.h>
 
 #include "fft.cuh"
@@ -941,6 +942,17 @@ constexpr bool kK3TwTable = true;  // A/B: fold twiddles read from the W_M table
 #else
 constexpr bool kK3TwTable = false;
 #endif
+__host__ __device__ constexpr int gcd_c(int a, int b) { return b == 0 ? a : gcd_c(b, a % b); }
+#ifdef FSCAN_K3_TW_LOAD2
+constexpr bool kK3TwSquare = false;  // A/B: W_M^{2x} by a second table read per fold site
+#else
+constexpr bool kK3TwSquare = true;
+#endif
+#ifdef FSCAN_K3_TW_REG
+constexpr bool kK3TwReg = true;  // A/B (K3 6.52 -> 6.72 ms at C4): a thread's <= 2 distinct W_M^x held in registers
+#else
+constexpr bool kK3TwReg = false;
+#endif
 #ifdef FSCAN_K3_STASH
 constexpr bool kK3FoldGather = false;  // A/B: gather into a z stash, fold per group from it (rounds 1-2)
 #else
@@ -1104,6 +1116,17 @@ __global__ void __launch_bounds__(kXThreads, 3) k_xlat_rows(Params p) {
         // and stores them straight into the groups' exchange buffers — no stash
         // of z and no per-group re-read of it
         constexpr int SITES = ROWS * K, US = U / 2;
+        // fold twiddles W_M^x: a thread's sites have x = (tid + u * kXThreads) mod K
+        // in every round when a round's stride is a multiple of K, i.e. TWP
+        // distinct x per thread: kK3TwReg (A/B, off) reads them once here
+        constexpr int XSTEP = kXThreads % K;
+        constexpr int TWP = XSTEP == 0 ? 1 : K / gcd_c(XSTEP, K);
+        constexpr bool TWREG = kK3TwReg && (US * kXThreads) % K == 0 && TWP <= 2 && TWP <= US;
+        [[maybe_unused]] float2 wreg[TWREG ? TWP : 1];
+        if constexpr (TWREG) {
+#pragma unroll
+            for (int j = 0; j < TWP; ++j) wreg[j] = wm(p.tw_m, (threadIdx.x + j * XSTEP) % K);
+        }
 #pragma unroll 1
         for (int e0 = threadIdx.x; e0 < SITES; e0 += US * kXThreads) {
             float fv[US][2], tap[US][2][4], frs[US][2], fcs[US][2];
@@ -1137,8 +1160,17 @@ __global__ void __launch_bounds__(kXThreads, 3) k_xlat_rows(Params p) {
                     const float2 tt = make_float2(fmaf(-0.5f, z1.x, z0.x), fmaf(-0.5f, z1.y, z0.y));
                     const float2 ss = make_float2(kS3 * z1.x, kS3 * z1.y);
                     G::lay(xbase, 3 * yl).put(x, cadd(z0, z1));
-                    G::lay(xbase, 3 * yl + 1).put(x, cmul(wm(p.tw_m, x), make_float2(tt.x + ss.y, tt.y - ss.x)));
-                    G::lay(xbase, 3 * yl + 2).put(x, cmul(wm(p.tw_m, 2 * x), make_float2(tt.x - ss.y, tt.y + ss.x)));
+                    float2 w1;
+                    if constexpr (TWREG)
+                        w1 = wreg[u % TWP];
+                    else
+                        w1 = wm(p.tw_m, x);
+                    // W_M^{2x} as a square (K3 6.73 -> 6.50 ms at C4, 7.66 -> 7.36 at C5:
+                    // the second table read was a stride-2 access); FSCAN_K3_TW_LOAD2
+                    // restores the read
+                    const float2 w2 = kK3TwSquare ? cmul(w1, w1) : wm(p.tw_m, 2 * x);
+                    G::lay(xbase, 3 * yl + 1).put(x, cmul(w1, make_float2(tt.x + ss.y, tt.y - ss.x)));
+                    G::lay(xbase, 3 * yl + 2).put(x, cmul(w2, make_float2(tt.x - ss.y, tt.y + ss.x)));
                 }
             }
         }
@@ -2350,8 +2382,28 @@ __global__ void k_bf_final(const Partial* items, const double* thetas, int nth, 
     out[pair] = o;
 }
 
+// A/B knob: FSCAN_CARVEOUT=<percent> asks for that shared-memory carveout
+// (cudaFuncAttributePreferredSharedMemoryCarveout) for the pipeline stages whose
+// bit is set in FSCAN_CARVEOUT_MASK (bit = Stage, default all); unset = the
+// driver's choice per kernel.
+enum Stage { kStRotRows, kStRotCols, kStRotGather, kStRotPolar, kStXRows, kStXCols, kStXOut, kStFin };
+inline int carveout_for(int stage) {
+    static const int pct = [] { const char* e = getenv("FSCAN_CARVEOUT"); return e ? atoi(e) : -1; }();
+    static const int mask = [] { const char* e = getenv("FSCAN_CARVEOUT_MASK"); return e ? (int)strtol(e, nullptr, 0) : 0xff; }();
+    return (pct >= 0 && ((mask >> stage) & 1)) ? pct : -1;
+}
 template <typename K>
-cudaError_t set_smem(K kernel, size_t bytes) {
+cudaError_t set_carveout(K kernel, int stage) {
+    const int pct = carveout_for(stage);
+    return pct < 0 ? cudaSuccess : cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+}
+
+template <typename K>
+cudaError_t set_smem(K kernel, size_t bytes, int stage = -1) {
+    if (stage >= 0) {
+        cudaError_t e = set_carveout(kernel, stage);
+        if (e != cudaSuccess) return e;
+    }
     if (bytes > 48 * 1024)
         return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     return cudaSuccess;
@@ -2388,7 +2440,7 @@ cudaError_t launch_k(void (*kernel)(KA...), dim3 grid, dim3 block, size_t smem, 
 template <int N>
 cudaError_t rot_rows(const Params& p, cudaStream_t s) {
     const size_t sm = (size_t)RowG<N>::FLOATS * sizeof(float);
-    cudaError_t e = set_smem(k_rot_rows<N>, sm);
+    cudaError_t e = set_smem(k_rot_rows<N>, sm, kStRotRows);
     if (e != cudaSuccess) return e;
     return launch_k(k_rot_rows<N>, dim3(N / RowG<N>::PER_CTA, p.batch), dim3(kRowThreads), sm, s, p, p);
 }
@@ -2397,7 +2449,7 @@ template <int N>
 cudaError_t rot_cols(const Params& p, cudaStream_t s) {
     constexpr int U = k1b_u<N>();
     const size_t sm = k1b_smem_floats<N>() * sizeof(float);
-    cudaError_t e = set_smem(k_rot_cols<N>, sm);
+    cudaError_t e = set_smem(k_rot_cols<N>, sm, kStRotCols);
     if (e != cudaSuccess) return e;
     return launch_k(k_rot_cols<N>, dim3(p.zcols / U, p.batch), dim3(N / 16 * 2 * U), sm, s, p, p);
 }
@@ -2407,7 +2459,7 @@ cudaError_t xlat_rows(const Params& p, cudaStream_t s) {
     using X = XRowGeom<N>;
     const dim3 grid(N / X::ROWS, p.batch);
     auto go = [&](auto kernel) {
-        cudaError_t e = set_smem(kernel, X::SMEM);
+        cudaError_t e = set_smem(kernel, X::SMEM, kStXRows);
         if (e != cudaSuccess) return e;
         return launch_k(kernel, grid, dim3(kXThreads), X::SMEM, s, p, p);
     };
@@ -2425,7 +2477,7 @@ cudaError_t xlat_cols(const Params& p, cudaStream_t s) {
     const dim3 grid(X::MERGE ? (X::NBLOCKS + X::NBLK - 1) / X::NBLK : (H + 1 + X::COLS - 1) / X::COLS, p.batch);
     constexpr size_t SMEM = X::MERGE ? X::SMEM_MERGE : X::SMEM;
     auto go = [&](auto kernel) {
-        cudaError_t e = set_smem(kernel, SMEM);
+        cudaError_t e = set_smem(kernel, SMEM, kStXCols);
         if (e != cudaSuccess) return e;
         return launch_k(kernel, grid, dim3(X::THREADS), SMEM, s, p, p);
     };
@@ -2443,7 +2495,7 @@ cudaError_t xlat_out(const Params& p, cudaStream_t s) {
     using X = XOutGeom<N>;
     const dim3 grid(N / X::ROWS, p.batch);
     auto go = [&](auto kernel) {
-        cudaError_t e = set_smem(kernel, X::SMEM);
+        cudaError_t e = set_smem(kernel, X::SMEM, kStXOut);
         if (e != cudaSuccess) return e;
         return launch_k(kernel, grid, dim3(X::THREADS), X::SMEM, s, p, p);
     };
@@ -2457,7 +2509,7 @@ cudaError_t xlat_win(const Params& p, cudaStream_t s) {
     constexpr int NB = N / X::ROWS;
     // row blocks a window of 2w + 1 rows can touch
     const int nb = std::min(NB, (2 * p.window + X::ROWS - 1) / X::ROWS + 1);
-    cudaError_t e = set_smem(k_xlat_out<N, false, kOutWin>, X::SMEM);
+    cudaError_t e = set_smem(k_xlat_out<N, false, kOutWin>, X::SMEM, kStXOut);
     if (e != cudaSuccess) return e;
     return launch_k(k_xlat_out<N, false, kOutWin>, dim3(nb, p.batch), dim3(X::THREADS), X::SMEM, s, p, p);
 }
@@ -2494,6 +2546,7 @@ cudaError_t launch_rot_gather(const Params& p, cudaStream_t s) {
     if (FSCAN_K2A_PB > 1 && !p.chain) {
         constexpr int PB = FSCAN_K2A_PB > 1 ? FSCAN_K2A_PB : 2;
         auto go = [&](auto kernel, int rp) {
+            if (cudaError_t e = set_carveout(kernel, kStRotGather); e != cudaSuccess) return e;
             const int az = kGatherThreads / rp;  // azimuths per CTA
             return launch_k(kernel, dim3((p.n_theta + az - 1) / az, (p.batch + PB - 1) / PB), dim3(kGatherThreads),
                             0, s, p, p);
@@ -2521,7 +2574,7 @@ cudaError_t launch_rot_polar(const Params& p, cudaStream_t s) {
         const int blocks = (p.n_theta + kLags - 1) / kLags, per = (blocks + S - 1) / S;
         const size_t sm = (size_t)(p.L + bx_len(p.L, p.n_theta) + (size_t)polar_parts(p.n_theta) * per * kLags) *
                           sizeof(double);
-        cudaError_t e = set_smem(k_rot_polar_part, sm);
+        cudaError_t e = set_smem(k_rot_polar_part, sm, kStRotPolar);
         if (e != cudaSuccess) return e;
         if ((e = launch_k(k_rot_polar_part, dim3(p.batch * S), dim3(kPolarThreads), sm, s, p, p, S)) != cudaSuccess)
             return e;
@@ -2532,7 +2585,7 @@ cudaError_t launch_rot_polar(const Params& p, cudaStream_t s) {
     const size_t sm = (size_t)(p.L + bx_len(p.L, p.n_theta) + p.n_theta * (1 + polar_parts(p.n_theta)) + 32) *
                           sizeof(double) +
                       32 * sizeof(int);
-    cudaError_t e = set_smem(k_rot_polar, sm);
+    cudaError_t e = set_smem(k_rot_polar, sm, kStRotPolar);
     if (e != cudaSuccess) return e;
     return launch_k(k_rot_polar, dim3(p.batch), dim3(kPolarThreads), sm, s, p, p);
 }
