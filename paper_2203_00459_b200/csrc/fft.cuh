@@ -364,10 +364,27 @@ constexpr bool kTwRK = std::is_same_v<TW, SmemTwRK>;
 constexpr int kQS = 49;  // odd row stride: the inverse's column reads F[k][.] spread over banks
 // S: the table's row stride; G: the table read through L1 from global memory
 // (__ldg) instead of a shared-memory copy
-template <int S, bool G>
+// W (forward only): the table is still being staged by the CTA when the
+// transform starts — `ready` is an mbarrier every thread arrives on after its
+// table stores, waited on (phase 0) just before the last stage's first read
+// (a split barrier: the first stage and its exchange run under the staging).
+__device__ __forceinline__ void wait_phase0(const uint64_t* bar) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "TWAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t"
+        "@!p bra TWAIT_%=;\n\t}" ::"r"(a)
+        : "memory");
+}
+template <int S, bool G, bool W = false>
 struct TwQF {
     const float2* f;
+    const uint64_t* ready = nullptr;
     __device__ __forceinline__ float2 at(int i) const { return G ? __ldg(f + i) : f[i]; }
+    __device__ __forceinline__ void wait() const {
+        if constexpr (W) wait_phase0(ready);
+    }
 };
 template <int S, bool G>
 struct TwQI {
@@ -380,8 +397,8 @@ template <typename TW>
 struct TwQInfo {
     static constexpr int kind = 0, S = 0;
 };
-template <int S_, bool G>
-struct TwQInfo<TwQF<S_, G>> {
+template <int S_, bool G, bool W>
+struct TwQInfo<TwQF<S_, G, W>> {
     static constexpr int kind = 1, S = S_;
 };
 template <int S_, bool G>
@@ -454,6 +471,7 @@ __device__ __forceinline__ void stage(float2 (&v)[16], int t, const L& lay, cons
             } else if constexpr (TwQInfo<TW>::kind == 1) {
                 static_assert(Ns == 16 && LAST, "merged twiddles: two-stage transforms only");
                 constexpr int S = TwQInfo<TW>::S;
+                if (j == 0) tw.wait();
 #pragma unroll
                 for (int r = 1; r < R; ++r) u[r] = cmul(u[r], tw.at(r * S + 3 * k));
             } else if constexpr (TwQInfo<TW>::kind == 2) {

@@ -1358,6 +1358,16 @@ constexpr bool kK4TabGlobal = false;
 #ifndef FSCAN_K4_GSTAGE
 #define FSCAN_K4_GSTAGE 1  // merged K4 (N = 512): G columns prefetched by TMA during the F pass (C4 +1.0%)
 #endif
+#ifdef FSCAN_K4_SPLIT_TAB
+constexpr bool kK4SplitTab = true;  // A/B: split table barrier (mbarrier arrive / wait before the last stage)
+#else
+constexpr bool kK4SplitTab = false;
+#endif
+#ifdef FSCAN_K4_PAIR_BAR
+constexpr bool kK4PairBar = true;  // A/B: per column pair named barrier before the combine
+#else
+constexpr bool kK4PairBar = false;
+#endif
 #ifdef FSCAN_K4_EARLYSYNC
 constexpr bool kK4LateSync = false;  // A/B: the table barrier before the first fold's loads
 #else
@@ -1776,7 +1786,7 @@ __device__ __forceinline__ void xlat_cols_merged(const Params& p) {
         }
     }
     pdl_enter();
-    [[maybe_unused]] __shared__ uint64_t g_bar, f_bar, e_bar;
+    [[maybe_unused]] __shared__ uint64_t g_bar, f_bar, e_bar, t_bar;
     [[maybe_unused]] float2* gst = reinterpret_cast<float2*>(
         GST == 1 ? reinterpret_cast<char*>(smem) + X::MERGE_BASE : reinterpret_cast<char*>(smem + G::FLOATS));
     // the stage <- the (up to) COLS columns of block `blk` of plane 0 (F) / 1 (G)
@@ -1785,16 +1795,23 @@ __device__ __forceinline__ void xlat_cols_merged(const Params& p) {
         const int nc = (H + 1 - k0) < COLS ? (H + 1 - k0) : COLS;
         bulk_load(gst, fgt_plane<N>(p, pair, plane) + (size_t)k0 * N, (unsigned)(nc * N * sizeof(float2)), bar);
     };
+    // kK4SplitTab: the table's barrier split into an arrive (after a thread's
+    // table stores) and a wait just before the first transform's last stage
+    // (fft.cuh TwQF<.., W>), so no warp waits out the slowest warp's F loads
+    // before its first FFT stage
+    constexpr bool SPLIT = kK4SplitTab && GST != 0 && !kK4TabGlobal;
     if constexpr (GST != 0) {
         static_assert(GST == 1 || G::FLOATS * sizeof(float) >= (size_t)COLS * N * sizeof(float2), "buffer B holds the G columns");
         if (threadIdx.x == 0) {
             mbar_init(&g_bar, 1);
+            if constexpr (SPLIT) mbar_init(&t_bar, X::THREADS);
             if constexpr (NBLK > 1) {
                 mbar_init(&f_bar, 1);
                 mbar_init(&e_bar, X::THREADS);
             }
             stage_block(1, b0, &g_bar);
         }
+        if constexpr (SPLIT) __syncthreads();  // publishes the mbarriers (no warp has a load in flight yet)
     }
     // W_3^q = (c1, wi): s = x0 + W_3^q x1 in four FMAs
     const float c1 = q ? -0.5f : 1.0f, wi = q == 0 ? 0.0f : (q == 1 ? -kS3 : kS3);
@@ -1831,7 +1848,10 @@ __device__ __forceinline__ void xlat_cols_merged(const Params& p) {
                     const int i = threadIdx.x + k * X::THREADS;
                     if (TE % X::THREADS == 0 || i < TE) tab[(i / 48) * QS + i % 48] = tv[k];
                 }
-                __syncthreads();  // the table (the fold reads none of it) and the mbarriers
+                if constexpr (SPLIT)
+                    mbar_arrive(&t_bar);
+                else
+                    __syncthreads();  // the table (the fold reads none of it) and the mbarriers
             }
         } else {
             mbar_wait(&f_bar, (ib - 1) & 1);
@@ -1847,7 +1867,10 @@ __device__ __forceinline__ void xlat_cols_merged(const Params& p) {
             }
             ephase ^= 1;
         }
-        fft_regs<K, -1, true>(a, t, bufA, TQF{fq});
+        if constexpr (SPLIT)
+            fft_regs<K, -1, true>(a, t, bufA, fscan_fft::TwQF<fscan_fft::kQS, false, true>{fq, &t_bar});
+        else
+            fft_regs<K, -1, true>(a, t, bufA, TQF{fq});
 #pragma unroll
         for (int m = 0; m < 16; ++m) bufA.put(t + m * T, a[m]);  // park F_q (own slots)
         if constexpr (GST != 0) {
@@ -1891,7 +1914,14 @@ __device__ __forceinline__ void xlat_cols_merged(const Params& p) {
         fft_regs<K, +1, true>(a, t, bufB, TQI{fq});
 #pragma unroll
         for (int m = 0; m < 16; ++m) bufB.put(t + m * T, cmul(a[m], cconj(wout(m / NB))));
-        __syncthreads();
+        // the combine of column c reads the three transforms 3c .. 3c + 2: with
+        // COLS = 4 and 16 threads per transform, columns (0, 1) live in warps 0-2
+        // and (2, 3) in warps 3-5, so a 96-thread named barrier per column pair
+        // is enough (kK4PairBar, A/B)
+        if constexpr (kK4PairBar && NBLK == 1 && COLS == 4 && T == 16 && X::THREADS == 192)
+            asm volatile("bar.sync %0, 96;" ::"r"(1 + (int)(threadIdx.x >= 96)) : "memory");
+        else
+            __syncthreads();
         // radix-3 combine of the pre-twiddled e_q; group q handles slots m = q, q+3, ...
         // (several blocks per CTA: the next block's first write to buffer B follows
         // its wait on g_bar, i.e. every thread's arrival after this combine)
