@@ -48,6 +48,7 @@ struct Lane {
     double* prof = nullptr;
     double* theta_ws = nullptr;
     int* flags = nullptr;
+    int* polar_cnt = nullptr;  // behind the flags (same allocation)
     cudaTextureObject_t gtex = 0;  // K3 texture over gt (pow2 grids whose chunk fits one 2-D texture)
     // host-API staging (the inputs go through fscan_ctx::hslot)
     float* cart = nullptr;  // K0 output (polar API): 2 grids x chunk
@@ -344,7 +345,9 @@ fscan_status alloc_lane(fscan_ctx* ctx, Lane& l, int chunk) {
     CK(cudaMalloc(&l.rot, sizeof(RotState) * chunk));
     CK(cudaMalloc(&l.prof, sizeof(double) * 2 * std::max(1, ctx->cfg.n_theta) * chunk));
     CK(cudaMalloc(&l.theta_ws, sizeof(double) * std::max(1, ctx->cfg.n_theta) * chunk));
-    CK(cudaMalloc(&l.flags, sizeof(int) * (chunk + 2)));  // chain mode: one per scan
+    CK(cudaMalloc(&l.flags, sizeof(int) * (2 * chunk + 2)));  // chain mode: one per scan; + K2b's per-pair counters
+    l.polar_cnt = l.flags + chunk + 2;
+    CK(cudaMemset(l.polar_cnt, 0, sizeof(int) * chunk));
     // K3 gathers g~ through a texture (tld4, zero border) when the chunk fits one
     // pitch-2D texture (rows = chunk * np)
     int max_h = 0;
@@ -430,6 +433,7 @@ Params base_params(fscan_ctx* ctx, Lane& l, int batch, double delta) {
     p.prof = l.prof;
     p.theta_ws = l.theta_ws;
     p.flags = l.flags;
+    p.polar_cnt = l.polar_cnt;
     p.tw_n = ctx->tw_n;
     p.tw_k = ctx->tw_k;
     p.tw_k2 = ctx->tw_k2;

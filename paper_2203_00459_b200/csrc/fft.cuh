@@ -30,6 +30,7 @@
 // the transform lives in one warp (fft_regs<..., WARP = true>), else the CTA.
 #pragma once
 
+#include <stdint.h>
 #include <cuda_runtime.h>
 
 #include <type_traits>

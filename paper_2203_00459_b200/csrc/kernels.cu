@@ -681,7 +681,7 @@ __device__ __forceinline__ void polar_profiles(const Params& p, int pair, double
 // (strict >, lowest index, matcher.cpp:47-53), windowed soft-argmax
 // (matcher.cpp:57-93), the pair's RotState and optional surface copy. Every
 // thread of the CTA calls it; red_v / red_i: 32 entries of scratch each.
-__device__ void polar_finish(const Params& p, int pair, const double* s, double* red_v, int* red_i) {
+__device__ void polar_finish(const Params& p, int pair, const double* s, double* red_v, int* red_i, double* wbuf) {
     const int nt = p.n_theta;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nwarps = blockDim.x / 32;
@@ -707,39 +707,51 @@ __device__ void polar_finish(const Params& p, int pair, const double* s, double*
         red_i[warp] = best_i;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (warp == 0) {
+        // every lane of warp 0 holds warp 0's maximum; each folds in the other
+        // warps' (same order, same result in every lane)
         for (int w = 1; w < nwarps; ++w)
             if (red_v[w] > best_v || (red_v[w] == best_v && red_i[w] < best_i)) {
                 best_v = red_v[w];
                 best_i = red_i[w];
             }
-        // soft_argmax over the n_theta x 1 surface (matcher.cpp:57-93)
+        // soft_argmax over the n_theta x 1 surface (matcher.cpp:57-93). The
+        // window's weights (an fp64 exp each: ~5 us of a one-pair call when one
+        // thread computed all 2w + 1) are spread over the warp's lanes into wbuf
+        // (>= min(2w + 1, n_theta) doubles); lane 0 then adds them up in the
+        // reference's order r0 .. r1, so the sums are those of a serial loop.
         const int pk = best_i == 0x7fffffff ? 0 : best_i;  // all-NaN surface: the first bin, as the reference's scan
         const int r0 = max(0, pk - p.window), r1 = min(nt - 1, pk + p.window);
         double scale = 1.0;
         if (p.normalize) {
-            double m = 0.0;
-            for (int r = r0; r <= r1; ++r) m = fmax(m, fabs(s[r]));
+            double m = 0.0;  // a maximum: the same value in any order
+            for (int r = r0 + lane; r <= r1; r += 32) m = fmax(m, fabs(s[r]));
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
             if (m > 0.0) scale = 1.0 / m;
         }
         const double top = s[pk] * scale;
-        double wsum = 0.0, rsum = 0.0;
-        for (int r = r0; r <= r1; ++r) {
-            const double w = exp(p.t_theta * (s[r] * scale - top));
-            wsum += w;
-            rsum += w * ((r - nt / 2) * p.delta_theta);
+        for (int r = r0 + lane; r <= r1; r += 32) wbuf[r - r0] = exp(p.t_theta * (s[r] * scale - top));
+        __syncwarp();
+        if (lane == 0) {
+            double wsum = 0.0, rsum = 0.0;
+            for (int r = r0; r <= r1; ++r) {
+                const double w = wbuf[r - r0];
+                wsum += w;
+                rsum += w * ((r - nt / 2) * p.delta_theta);
+            }
+            const double theta = rsum / wsum;
+            rs->theta = theta;
+            double sn, cs;
+            sincos(-theta, &sn, &cs);
+            rs->st = sn;
+            rs->ct = cs;
+            rs->identity = (-theta == 0.0);
+            rs->peak = s[pk];
+            rs->hard = (pk - nt / 2) * p.delta_theta;
+            rs->bin = pk;
+            if (p.theta_only) p.theta_only[pair] = theta;
         }
-        const double theta = rsum / wsum;
-        rs->theta = theta;
-        double sn, cs;
-        sincos(-theta, &sn, &cs);
-        rs->st = sn;
-        rs->ct = cs;
-        rs->identity = (-theta == 0.0);
-        rs->peak = s[pk];
-        rs->hard = (pk - nt / 2) * p.delta_theta;
-        rs->bin = pk;
-        if (p.theta_only) p.theta_only[pair] = theta;
     }
     if (p.theta_surf)
         for (int k = threadIdx.x; k < nt; k += blockDim.x) p.theta_surf[(size_t)pair * nt + k] = s[k];
@@ -804,21 +816,25 @@ __global__ void __launch_bounds__(kPolarThreads) k_rot_polar(Params p) {
         s[k] = acc * invC;
     }
     __syncthreads();
-    polar_finish(p, pair, s, red_v, red_i);
+    polar_finish(p, pair, s, red_v, red_i, part);  // the partial sums are dead: scratch for the window weights
 }
 
 // K2b split over S CTAs per pair (small batches: one CTA per pair would leave
 // the GPU nearly idle for ~25 us): CTA `part` of a pair owns a contiguous range
 // of lag blocks and writes their scores to theta_ws; k_rot_polar_fin then runs
 // the argmaxes per pair.
-__global__ void __launch_bounds__(kPolarThreads) k_rot_polar_part(Params p, int S) {
+// fuse: the pair's last CTA to finish (a counter in p.polar_cnt, reset by that
+// CTA) runs the argmaxes itself instead of a k_rot_polar_fin launch — one kernel
+// less on the critical path of a small batch.
+__global__ void __launch_bounds__(kPolarThreads) k_rot_polar_part(Params p, int S, int fuse) {
     pdl_enter();
     extern __shared__ double dsm[];
+    __shared__ int is_last;
     const int pair = blockIdx.x / S, part_id = blockIdx.x % S;
     const int nt = p.n_theta, L = p.L;
     const int blocks = (nt + kLags - 1) / kLags, per = (blocks + S - 1) / S;
     const int b0 = part_id * per, nb = min(blocks, b0 + per) - b0;
-    if (nb <= 0) return;
+    if (nb <= 0) return;  // (not counted: the pair's active CTAs are those with lag blocks)
     // the fused kernel's q partition and summation order: bit-identical scores
     // whatever the batch size (results do not depend on batching)
     const int np = polar_parts(nt);
@@ -847,6 +863,26 @@ __global__ void __launch_bounds__(kPolarThreads) k_rot_polar_part(Params p, int 
             p.theta_ws[(size_t)pair * nt + k] = acc * invC;
         }
     }
+    if (!fuse) return;
+    __threadfence();  // this thread's scores before the CTA's count
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int active = (blocks + per - 1) / per;
+        is_last = atomicAdd(p.polar_cnt + pair, 1) == active - 1;
+        if (is_last) p.polar_cnt[pair] = 0;  // ready for the next launch on this lane
+    }
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    // the profiles and partial sums are dead: the scores, reduction scratch and
+    // window weights take their place (the launch sizes the buffer for both)
+    double* s = dsm;
+    double* red_v = s + nt;
+    int* red_i = (int*)(red_v + 32);
+    double* wbuf = red_v + 32 + 16;
+    for (int k = threadIdx.x; k < nt; k += kPolarThreads) s[k] = __ldcg(p.theta_ws + (size_t)pair * nt + k);
+    __syncthreads();
+    polar_finish(p, pair, s, red_v, red_i, wbuf);
 }
 
 __global__ void __launch_bounds__(kPolarThreads) k_rot_polar_fin(Params p) {
@@ -856,9 +892,10 @@ __global__ void __launch_bounds__(kPolarThreads) k_rot_polar_fin(Params p) {
     double* s = dsm;
     double* red_v = s + nt;
     int* red_i = (int*)(red_v + 32);
+    double* wbuf = red_v + 32 + 16;  // behind the 32 ints: n_theta doubles for the window weights
     for (int k = threadIdx.x; k < nt; k += kPolarThreads) s[k] = p.theta_ws[(size_t)pair * nt + k];
     __syncthreads();
-    polar_finish(p, pair, s, red_v, red_i);
+    polar_finish(p, pair, s, red_v, red_i, wbuf);
 }
 
 __global__ void k_theta_in(Params p) {
@@ -2229,8 +2266,24 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(Params p, int nparts) 
     __shared__ double sh3[3 * (kFinThreads / 32)];
     __shared__ float pk_v;
     __shared__ int pk_i;
+    __shared__ double pre_sn, pre_cs, pre_th;
     const int pair = blockIdx.x;
     const int n = p.np;
+    if (threadIdx.x == 32) {
+        // the rotation's sine / cosine and normalised angle, computed by warp 1
+        // while warp 0 reduces the block maxima (off thread 0's serial tail)
+        const double theta = p.rot[pair].theta;
+        double sn, cs;
+        sincos(theta, &sn, &cs);  // rotate_vec (geometry.cpp:31-35)
+        const double two_pi = 6.283185307179586;
+        const double pi = 3.141592653589793;
+        double th = fmod(theta, two_pi);  // normalize_angle (geometry.cpp:9-14)
+        if (th <= -pi) th += two_pi;
+        if (th > pi) th -= two_pi;
+        pre_sn = sn;
+        pre_cs = cs;
+        pre_th = th;
+    }
     if (threadIdx.x < 32) {
         // the K5 block maxima reduced by warp 0: the largest value, the lowest
         // linear index among equal values (an order-independent maximum, so the
@@ -2294,8 +2347,7 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(Params p, int nparts) 
     if (threadIdx.x == 0) {
         const RotState rs = p.rot[pair];
         const double ty_ = rsum / ws, tx_ = csum / ws;
-        double sn, cs;
-        sincos(rs.theta, &sn, &cs);  // rotate_vec (geometry.cpp:31-35)
+        const double sn = pre_sn, cs = pre_cs;  // published by block_sum3's barriers
         const double tx = cs * tx_ - sn * ty_;
         const double ty = sn * tx_ + cs * ty_;
         if (p.txy_only) {
@@ -2303,13 +2355,8 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(Params p, int nparts) 
             p.txy_only[2 * pair + 1] = ty;
         }
         if (p.out) {
-            const double two_pi = 6.283185307179586;
-            const double pi = 3.141592653589793;
-            double th = fmod(rs.theta, two_pi);  // normalize_angle (geometry.cpp:9-14)
-            if (th <= -pi) th += two_pi;
-            if (th > pi) th -= two_pi;
             fscan_pair_result o;
-            o.theta = th;
+            o.theta = pre_th;
             o.tx = tx;
             o.ty = ty;
             o.theta_hard = rs.hard;
@@ -2589,6 +2636,9 @@ cudaError_t launch_rot_gather(const Params& p, cudaStream_t s) {
 }
 
 // CTAs per pair for K2b: one when the batch fills the GPU, else up to 16
+#ifndef FSCAN_K2B_FUSE_FIN
+#define FSCAN_K2B_FUSE_FIN 1  // split K2b: the pair's last CTA runs the argmaxes (no k_rot_polar_fin launch)
+#endif
 #ifndef FSCAN_K2B_BIG_SPLIT
 #define FSCAN_K2B_BIG_SPLIT 1  // CTAs per pair for batches that fill the GPU
 #endif
@@ -2602,13 +2652,18 @@ cudaError_t launch_rot_polar(const Params& p, cudaStream_t s) {
     const int S = polar_split(p.batch, p.n_theta);
     if (S > 1) {
         const int blocks = (p.n_theta + kLags - 1) / kLags, per = (blocks + S - 1) / S;
-        const size_t sm = (size_t)(p.L + bx_len(p.L, p.n_theta) + (size_t)polar_parts(p.n_theta) * per * kLags) *
-                          sizeof(double);
+        const size_t fm0 = (size_t)(2 * p.n_theta + 32) * sizeof(double) + 32 * sizeof(int);  // polar_finish
+        const int fuse = FSCAN_K2B_FUSE_FIN && p.polar_cnt != nullptr;
+        const size_t sm = std::max((size_t)(p.L + bx_len(p.L, p.n_theta) +
+                                            (size_t)polar_parts(p.n_theta) * per * kLags) * sizeof(double),
+                                   fuse ? fm0 : (size_t)0);
         cudaError_t e = set_smem(k_rot_polar_part, sm, kStRotPolar);
         if (e != cudaSuccess) return e;
-        if ((e = launch_k(k_rot_polar_part, dim3(p.batch * S), dim3(kPolarThreads), sm, s, p, p, S)) != cudaSuccess)
+        if ((e = launch_k(k_rot_polar_part, dim3(p.batch * S), dim3(kPolarThreads), sm, s, p, p, S, fuse)) !=
+                cudaSuccess ||
+            fuse)
             return e;
-        const size_t fm = (size_t)(p.n_theta + 32) * sizeof(double) + 32 * sizeof(int);
+        const size_t fm = (size_t)(2 * p.n_theta + 32) * sizeof(double) + 32 * sizeof(int);
         if ((e = set_smem(k_rot_polar_fin, fm)) != cudaSuccess) return e;
         return launch_k(k_rot_polar_fin, dim3(p.batch), dim3(kPolarThreads), fm, s, p, p);
     }

@@ -75,6 +75,7 @@ struct Params {
     RotState* rot; // [batch]
     double* prof;  // K2a radial-sum profiles [batch][2][n_theta]
     double* theta_ws;  // K2b split over several CTAs per pair (small batches): scores [batch][n_theta]
+    int* polar_cnt;    // split K2b: finished CTAs per pair [batch], zero between launches (nullptr: separate fin kernel)
     int* flags;    // [batch] (chain mode: [n_scans]) bit0 non-finite, bit1 mask out of [0,1]
     // tables
     const float2* tw_n;   // exp(-2 pi i k / N), k < N
