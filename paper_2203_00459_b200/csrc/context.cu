@@ -70,6 +70,7 @@ struct fscan_ctx {
     int max_batch = 0;
     int chunk = 0;       // pairs per pipeline chunk
     int alloc_chunk = 0; // workspace capacity (pairs)
+    int wide_chunk = 0;  // the ~2 GiB-per-lane chunk of this grid size, whatever max_batch (exhaustive search)
     int n_live = 0;
     int rot_col_blocks = 0;  // K1b column blocks (8 columns each) the polar taps read
     int phase = 0;           // opt-in phase correlation in the translation stage
@@ -840,14 +841,19 @@ fscan_status fscan_ctx_create(int device, const fscan_config* cfg_in, int max_ba
     // a batch smaller than the lanes' chunks is spread over all lanes (C2, 64
     // pairs: +7% over one 64-pair chunk); tiny contexts keep whole-batch chunks
     // (the exhaustive search runs pair x candidate items through them)
+    int wide = chunk;
     if (max_batch >= 16 * ctx->nlanes) chunk = std::min(chunk, (max_batch + ctx->nlanes - 1) / ctx->nlanes);
     if (const char* e = std::getenv("FSCAN_CHUNK")) chunk = std::max(1, std::atoi(e));
     chunk = std::min(chunk, max_batch);
     if (ctx->np == ctx->n && !kNoTexGather) {  // keep the chunk inside one K3 gather texture
         int max_h = 0;
         CK(cudaDeviceGetAttribute(&max_h, cudaDevAttrMaxTexture2DLinearHeight, device));
-        if (max_h >= ctx->np) chunk = std::min(chunk, max_h / ctx->np);
+        if (max_h >= ctx->np) {
+            chunk = std::min(chunk, max_h / ctx->np);
+            wide = std::min(wide, max_h / ctx->np);
+        }
     }
+    ctx->wide_chunk = wide;
     ctx->chunk = chunk;
     ctx->alloc_chunk = chunk;
     CK(cudaEventCreateWithFlags(&ctx->start_ev, cudaEventDisableTiming));
@@ -918,29 +924,36 @@ int fscan_ctx_launches_last(const fscan_ctx* ctx) { return ctx ? ctx->launches_l
 
 int fscan_ctx_rot_columns(const fscan_ctx* ctx) { return ctx ? 8 * ctx->rot_col_blocks : 0; }
 
+// Lane workspace for at least `pairs` pairs per chunk (the caller holds ctx->mu
+// and has dropped the cached graphs, which bake in the workspace pointers).
+static fscan_status grow_lanes(fscan_ctx* ctx, int pairs) {
+    if (pairs <= ctx->alloc_chunk) return FSCAN_OK;
+    cudaSetDevice(ctx->device);
+    // a graph replay on a user stream may still be using the workspace
+    if (ctx->graph_launched) cudaEventSynchronize(ctx->graph_ev);
+    for (Lane& l : LaneRange{ctx}) {
+        cudaStreamSynchronize(l.stream);
+        const bool had_host = l.res != nullptr;
+        free_lane(l);
+        fscan_status a = alloc_lane(ctx, l, pairs);
+        if (a != FSCAN_OK) return a;
+        if (had_host) {
+            a = alloc_host_staging(ctx, l, pairs);
+            if (a != FSCAN_OK) return a;
+        }
+    }
+    ctx->alloc_chunk = pairs;
+    return FSCAN_OK;
+}
+
 fscan_status fscan_ctx_set_chunk(fscan_ctx* ctx, int pairs) {
     if (!ctx || pairs < 0) return FSCAN_ERR_INVALID_ARGUMENT;
     std::lock_guard<std::mutex> g(ctx->mu);
     if (pairs == 0) pairs = ctx->alloc_chunk;
     // cached graphs bake in the chunking and the lane workspace pointers
     if (pairs != ctx->chunk || pairs > ctx->alloc_chunk) drop_graphs(ctx);
-    if (pairs > ctx->alloc_chunk) {
-        cudaSetDevice(ctx->device);
-        // a graph replay on a user stream may still be using the workspace
-        if (ctx->graph_launched) cudaEventSynchronize(ctx->graph_ev);
-        for (Lane& l : LaneRange{ctx}) {
-            cudaStreamSynchronize(l.stream);
-            const bool had_host = l.res != nullptr;
-            free_lane(l);
-            fscan_status a = alloc_lane(ctx, l, pairs);
-            if (a != FSCAN_OK) return a;
-            if (had_host) {
-                a = alloc_host_staging(ctx, l, pairs);
-                if (a != FSCAN_OK) return a;
-            }
-        }
-        ctx->alloc_chunk = pairs;
-    }
+    fscan_status a = grow_lanes(ctx, pairs);
+    if (a != FSCAN_OK) return a;
     ctx->chunk = pairs;
     return FSCAN_OK;
 }
@@ -1109,6 +1122,23 @@ fscan_status fscan_brute_force_batch(fscan_ctx* ctx, const float* d_f, const flo
         d_f = ef;
         d_g = ef + npp * batch;
     }
+    // (pair, candidate) items, not pairs, flow through the lanes: a context made
+    // for a few pairs gets lanes wide enough for the items to fill the GPU (with
+    // max_batch-sized chunks every 5-kernel chunk of a 4-pair search was launch
+    // bound: 720 chunks of 4 items at C4's 720 candidates)
+    const int saved_chunk = ctx->chunk;
+    {
+        const int want = std::min(ctx->wide_chunk, (items + ctx->nlanes - 1) / ctx->nlanes);
+        if (want > ctx->alloc_chunk) {
+            drop_graphs(ctx);
+            fscan_status a = grow_lanes(ctx, want);
+            if (a != FSCAN_OK) {
+                cudaFree(ef);
+                return a;
+            }
+        }
+        ctx->chunk = std::max(ctx->chunk, std::min(want, ctx->alloc_chunk));
+    }
     st = drive(ctx, items, user, [&](Lane& l, int off, int cnt) {
         Params p = base_params(ctx, l, cnt, delta);
         // brute_force_match scores the scans as given; only K3 reads ft / gt here
@@ -1132,6 +1162,7 @@ fscan_status fscan_brute_force_batch(fscan_ctx* ctx, const float* d_f, const flo
 #undef FSCAN_LAUNCH
         return FSCAN_OK;
     });
+    ctx->chunk = saved_chunk;
     if (st != FSCAN_OK) {
         cudaFree(ef);
         return st;
