@@ -2398,17 +2398,37 @@ __global__ void k_polar_taps(int n_az, double res, int n, double delta, fscan_k0
     tab[idx] = fscan_k0::polar_tap(n_az, res, n, delta, idx / n, idx % n);
 }
 
-__global__ void k_polar_to_cart(const float* polar0, const float* polar1, int n_az, int n_range, int n,
+// PP pairs per thread: the cell's 32-byte tap is read once for all of them (at
+// one pair per thread the table's L2 reads, 8 MB per pair at N = 512, were K0's
+// largest traffic) and their 8 PP gathers are in flight together. Measured at C3:
+// PP = 1 / 2 / 4 / 8 -> 110.9k / 115.1k / 113.3k / 111.5k pairs/s.
+#ifndef FSCAN_K0_PP
+#define FSCAN_K0_PP 2
+#endif
+template <int PP>
+__global__ void k_polar_to_cart(const float* polar0, const float* polar1, int batch, int n_az, int n_range, int n,
                                 const fscan_k0::PolarTap* __restrict__ tab, float* out0, float* out1) {
-    const int pair = blockIdx.y;
+    const int pair0 = blockIdx.y * PP;
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= n * n) return;
-    // both sweeps of the pair from one read of the cell's tap (geometry shared)
+    // both sweeps of every pair from one read of the cell's tap (geometry shared)
     const fscan_k0::PolarTap tp = tab[idx];
-    const size_t po = (size_t)pair * n_az * n_range, oo = (size_t)pair * n * n + idx;
-    const float v0 = (float)fscan_k0::polar_sample(polar0 + po, n_range, tp);
-    if (polar1) out1[oo] = (float)fscan_k0::polar_sample(polar1 + po, n_range, tp);
-    out0[oo] = v0;
+    float v0[PP], v1[PP];
+#pragma unroll
+    for (int j = 0; j < PP; ++j) {
+        const int pair = pair0 + j < batch ? pair0 + j : batch - 1;  // tail: recompute the last pair (not stored)
+        const size_t po = (size_t)pair * n_az * n_range;
+        v0[j] = (float)fscan_k0::polar_sample(polar0 + po, n_range, tp);
+        v1[j] = polar1 ? (float)fscan_k0::polar_sample(polar1 + po, n_range, tp) : 0.0f;
+    }
+#pragma unroll
+    for (int j = 0; j < PP; ++j) {
+        if (pair0 + j < batch) {
+            const size_t oo = (size_t)(pair0 + j) * n * n + idx;
+            out0[oo] = v0[j];
+            if (polar1) out1[oo] = v1[j];
+        }
+    }
 }
 
 // Brute-force correlative search (oracle.cpp:21-67): per (pair, candidate)
@@ -2735,8 +2755,9 @@ cudaError_t launch_polar_to_cart(const float* d_polar0, const float* d_polar1, i
         if (e != cudaSuccess) return e;
         tab = own;
     }
-    k_polar_to_cart<<<dim3((unsigned)((total + 255) / 256), batch), 256, 0, stream>>>(
-        d_polar0, d_polar1, n_az, n_range, n, static_cast<const fscan_k0::PolarTap*>(tab), d_out0, d_out1);
+    constexpr int PP = FSCAN_K0_PP;
+    k_polar_to_cart<PP><<<dim3((unsigned)((total + 255) / 256), (batch + PP - 1) / PP), 256, 0, stream>>>(
+        d_polar0, d_polar1, batch, n_az, n_range, n, static_cast<const fscan_k0::PolarTap*>(tab), d_out0, d_out1);
     cudaError_t e = cudaGetLastError();
     if (own) cudaFreeAsync(own, stream);
     return e;
