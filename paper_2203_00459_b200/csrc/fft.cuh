@@ -37,8 +37,44 @@
 
 namespace fscan_fft {
 
+// Packed fp32 (sm_100a FADD2 / FMUL2 / FFMA2 on aligned register pairs, PTX
+// add / mul / fma.rn.f32x2): a complex add or subtract is ONE instruction and a
+// complex product two plus a negation, each component rounded exactly as its
+// scalar form (add.rn / mul.rn / fma.rn) — same bits, half the issue slots.
+// The translation kernels are bound by issue slots and the L1 data pipe with
+// the FMA pipe half idle (tools/microbench/f32x2_probe.cu: a packed
+// instruction delivers the scalar forms' fp32 rate per SM from one issue slot
+// instead of two). Measured (C4 / C5, interleaved): packed add / subtract
+// K4 6.79 -> 6.59 ms / 8.39 -> 7.88 ms, K3 6.49 -> 6.40 ms, C4 +1.2%, C5 +1.2%;
+// the packed product as well: K4 6.8 -> 8.0 ms at N = 512 (its constant-bank
+// twiddles turn into LDC + MOV pairs: packed operands cannot name a constant,
+// and K4 runs at 4.5 warps per scheduler, too few to hide them), C4 -4.5%.
+// So: packed add / subtract on (FSCAN_NO_F32X2_ADD), packed product off
+// (FSCAN_F32X2_MUL).
+#ifdef FSCAN_NO_F32X2_ADD
+constexpr bool kF32x2Add = false;  // A/B: scalar complex add / subtract
+#else
+constexpr bool kF32x2Add = true;
+#endif
+#ifdef FSCAN_F32X2_MUL
+constexpr bool kF32x2Mul = true;
+#else
+constexpr bool kF32x2Mul = false;
+#endif
+
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
-    return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+    if constexpr (kF32x2Mul) {
+        // (a.x b.x + rn(-a.y b.y), a.x b.y + rn(a.y b.x)): the scalar form's roundings
+        float2 r;
+        asm("{ .reg .b64 ax, ay, bb, bs, t, rr;\n\t"
+            " mov.b64 ax, {%2, %2};\n\t mov.b64 ay, {%3, %3};\n\t mov.b64 bb, {%4, %5};\n\t mov.b64 bs, {%6, %4};\n\t"
+            " mul.rn.f32x2 t, ay, bs;\n\t fma.rn.f32x2 rr, ax, bb, t;\n\t mov.b64 {%0, %1}, rr; }"
+            : "=f"(r.x), "=f"(r.y)
+            : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(-b.y));
+        return r;
+    } else {
+        return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+    }
 }
 // sqrt.approx.f32 (one MUFU op, ~1 ulp): the IEEE-rounded sqrtf costs ~10
 // instructions and a slow-path branch; magnitudes feeding the polar gather need
@@ -48,8 +84,32 @@ __device__ __forceinline__ float sqrt_fast(float x) {
     asm("sqrt.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
-__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+template <bool PK = kF32x2Add>
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) {
+    if constexpr (PK) {
+        float2 r;
+        asm("{ .reg .b64 ra, rb, rr;\n\t mov.b64 ra, {%2, %3};\n\t mov.b64 rb, {%4, %5};\n\t"
+            " add.rn.f32x2 rr, ra, rb;\n\t mov.b64 {%0, %1}, rr; }"
+            : "=f"(r.x), "=f"(r.y)
+            : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+        return r;
+    } else {
+        return make_float2(a.x + b.x, a.y + b.y);
+    }
+}
+template <bool PK = kF32x2Add>
+__device__ __forceinline__ float2 csub(float2 a, float2 b) {
+    if constexpr (PK) {
+        float2 r;
+        asm("{ .reg .b64 ra, rb, rr;\n\t mov.b64 ra, {%2, %3};\n\t mov.b64 rb, {%4, %5};\n\t"
+            " sub.rn.f32x2 rr, ra, rb;\n\t mov.b64 {%0, %1}, rr; }"
+            : "=f"(r.x), "=f"(r.y)
+            : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+        return r;
+    } else {
+        return make_float2(a.x - b.x, a.y - b.y);
+    }
+}
 __device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
 // a * (-i) for SIGN=-1, a * (+i) for SIGN=+1
 template <int SIGN>
@@ -57,53 +117,53 @@ __device__ __forceinline__ float2 mul_mi(float2 a) {
     return SIGN < 0 ? make_float2(a.y, -a.x) : make_float2(-a.y, a.x);
 }
 
-template <int SIGN>
+template <int SIGN, bool PK = kF32x2Add>
 __device__ __forceinline__ void dft2(float2& a, float2& b) {
     const float2 t = a;
-    a = cadd(t, b);
-    b = csub(t, b);
+    a = cadd<PK>(t, b);
+    b = csub<PK>(t, b);
 }
 
 // 4-point DFT in place, natural order out.
-template <int SIGN>
+template <int SIGN, bool PK = kF32x2Add>
 __device__ __forceinline__ void dft4(float2& x0, float2& x1, float2& x2, float2& x3) {
-    const float2 a = cadd(x0, x2), b = csub(x0, x2);
-    const float2 c = cadd(x1, x3), d = mul_mi<SIGN>(csub(x1, x3));
-    x0 = cadd(a, c);
-    x2 = csub(a, c);
-    x1 = cadd(b, d);
-    x3 = csub(b, d);
+    const float2 a = cadd<PK>(x0, x2), b = csub<PK>(x0, x2);
+    const float2 c = cadd<PK>(x1, x3), d = mul_mi<SIGN>(csub<PK>(x1, x3));
+    x0 = cadd<PK>(a, c);
+    x2 = csub<PK>(a, c);
+    x1 = cadd<PK>(b, d);
+    x3 = csub<PK>(b, d);
 }
 
 // 8-point DFT as radix-2 x radix-4 (DIT over n = 2*n1 + n2).
-template <int SIGN>
+template <int SIGN, bool PK = kF32x2Add>
 __device__ __forceinline__ void dft8(float2* x) {
     constexpr float r = 0.70710678118654752f;
     float2 e0 = x[0], e1 = x[2], e2 = x[4], e3 = x[6];
     float2 o0 = x[1], o1 = x[3], o2 = x[5], o3 = x[7];
-    dft4<SIGN>(e0, e1, e2, e3);
-    dft4<SIGN>(o0, o1, o2, o3);
+    dft4<SIGN, PK>(e0, e1, e2, e3);
+    dft4<SIGN, PK>(o0, o1, o2, o3);
     o1 = SIGN < 0 ? make_float2(r * (o1.x + o1.y), r * (o1.y - o1.x)) : make_float2(r * (o1.x - o1.y), r * (o1.y + o1.x));
     o2 = mul_mi<SIGN>(o2);
     o3 = SIGN < 0 ? make_float2(r * (o3.y - o3.x), -r * (o3.x + o3.y)) : make_float2(-r * (o3.x + o3.y), r * (o3.x - o3.y));
-    x[0] = cadd(e0, o0);
-    x[4] = csub(e0, o0);
-    x[1] = cadd(e1, o1);
-    x[5] = csub(e1, o1);
-    x[2] = cadd(e2, o2);
-    x[6] = csub(e2, o2);
-    x[3] = cadd(e3, o3);
-    x[7] = csub(e3, o3);
+    x[0] = cadd<PK>(e0, o0);
+    x[4] = csub<PK>(e0, o0);
+    x[1] = cadd<PK>(e1, o1);
+    x[5] = csub<PK>(e1, o1);
+    x[2] = cadd<PK>(e2, o2);
+    x[6] = csub<PK>(e2, o2);
+    x[3] = cadd<PK>(e3, o3);
+    x[7] = csub<PK>(e3, o3);
 }
 
 // 16-point DFT as 4x4: X[k1 + 4*k2] = sum_n2 W4^(n2 k2) W16^(n2 k1) sum_n1 x[4 n1 + n2] W4^(n1 k1)
-template <int SIGN>
+template <int SIGN, bool PK = kF32x2Add>
 __device__ __forceinline__ void dft16(float2* x) {
     constexpr float c1 = 0.92387953251128674f;  // cos(pi/8)
     constexpr float s1 = 0.38268343236508977f;  // sin(pi/8)
     constexpr float r = 0.70710678118654752f;
 #pragma unroll
-    for (int n2 = 0; n2 < 4; ++n2) dft4<SIGN>(x[n2], x[4 + n2], x[8 + n2], x[12 + n2]);
+    for (int n2 = 0; n2 < 4; ++n2) dft4<SIGN, PK>(x[n2], x[4 + n2], x[8 + n2], x[12 + n2]);
     // x[4*k1 + n2] holds a[n2][k1]; apply W16^(n2*k1) = cos + i*SIGN*sin
     const float sg = (float)SIGN;
     const float2 w1 = make_float2(c1, sg * s1), w2 = make_float2(r, sg * r), w3 = make_float2(s1, sg * c1);
@@ -121,7 +181,7 @@ __device__ __forceinline__ void dft16(float2* x) {
 #pragma unroll
     for (int k1 = 0; k1 < 4; ++k1) {
         float2 a0 = x[4 * k1], a1 = x[4 * k1 + 1], a2 = x[4 * k1 + 2], a3 = x[4 * k1 + 3];
-        dft4<SIGN>(a0, a1, a2, a3);
+        dft4<SIGN, PK>(a0, a1, a2, a3);
         y[k1] = a0;
         y[k1 + 4] = a1;
         y[k1 + 8] = a2;
@@ -131,16 +191,16 @@ __device__ __forceinline__ void dft16(float2* x) {
     for (int i = 0; i < 16; ++i) x[i] = y[i];
 }
 
-template <int R, int SIGN>
+template <int R, int SIGN, bool PK = kF32x2Add>
 __device__ __forceinline__ void dft_r(float2* x) {
     if constexpr (R == 2) {
-        dft2<SIGN>(x[0], x[1]);
+        dft2<SIGN, PK>(x[0], x[1]);
     } else if constexpr (R == 4) {
-        dft4<SIGN>(x[0], x[1], x[2], x[3]);
+        dft4<SIGN, PK>(x[0], x[1], x[2], x[3]);
     } else if constexpr (R == 8) {
-        dft8<SIGN>(x);
+        dft8<SIGN, PK>(x);
     } else {
-        dft16<SIGN>(x);
+        dft16<SIGN, PK>(x);
     }
 }
 
@@ -441,7 +501,7 @@ constexpr bool kPowJ = false;  // A/B: last-stage twiddles read from the table p
 constexpr bool kPowJ = true;
 #endif
 
-template <int N, int R, int Ns, bool LAST, int SIGN, bool WARP, typename L, typename TW>
+template <int N, int R, int Ns, bool LAST, int SIGN, bool WARP, bool PK, typename L, typename TW>
 __device__ __forceinline__ void stage(float2 (&v)[16], int t, const L& lay, const TW& tw) {
     constexpr int T = N / 16;
     constexpr int NB = 16 / R;
@@ -511,7 +571,7 @@ __device__ __forceinline__ void stage(float2 (&v)[16], int t, const L& lay, cons
                 for (int r = 1; r < R; ++r) u[r] = cmul(u[r], twiddle<SIGN>(tw, r * k * q));
             }
         }
-        dft_r<R, SIGN>(u);
+        dft_r<R, SIGN, PK>(u);
         if constexpr (LAST) {
 #pragma unroll
             for (int r = 0; r < R; ++r) v[j + r * NB] = u[r];
@@ -533,19 +593,20 @@ __device__ __forceinline__ void stage(float2 (&v)[16], int t, const L& lay, cons
 // caller guarantees the transform's threads and exchange buffer live in one
 // warp (row layouts with T <= 32), so the exchanges need only __syncwarp;
 // otherwise every thread of the CTA must call fft_regs the same number of times.
-template <int N, int SIGN, bool WARP = false, typename L, typename TW>
+// PK: packed complex add / subtract in the butterflies (see cadd)
+template <int N, int SIGN, bool WARP = false, bool PK = kF32x2Add, typename L, typename TW>
 __device__ __forceinline__ void fft_regs(float2 (&v)[16], int t, const L& lay, const TW& tw) {
     static_assert(N >= 16 && (N & (N - 1)) == 0, "power-of-two length >= 16");
     static_assert(!WARP || N / 16 <= 32, "a warp-synchronous transform fits in one warp");
     if constexpr (N == 16) {
-        stage<N, 16, 1, true, SIGN, WARP>(v, t, lay, tw);
+        stage<N, 16, 1, true, SIGN, WARP, PK>(v, t, lay, tw);
     } else if constexpr (N <= 256) {
-        stage<N, 16, 1, false, SIGN, WARP>(v, t, lay, tw);
-        stage<N, N / 16, 16, true, SIGN, WARP>(v, t, lay, tw);
+        stage<N, 16, 1, false, SIGN, WARP, PK>(v, t, lay, tw);
+        stage<N, N / 16, 16, true, SIGN, WARP, PK>(v, t, lay, tw);
     } else {
-        stage<N, 16, 1, false, SIGN, WARP>(v, t, lay, tw);
-        stage<N, 16, 16, false, SIGN, WARP>(v, t, lay, tw);
-        stage<N, N / 256, 256, true, SIGN, WARP>(v, t, lay, tw);
+        stage<N, 16, 1, false, SIGN, WARP, PK>(v, t, lay, tw);
+        stage<N, 16, 16, false, SIGN, WARP, PK>(v, t, lay, tw);
+        stage<N, N / 256, 256, true, SIGN, WARP, PK>(v, t, lay, tw);
     }
 }
 

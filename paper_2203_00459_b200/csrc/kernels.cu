@@ -33,6 +33,19 @@
 #ifndef FSCAN_K5_TWO_PASS_MIN_N
 #define FSCAN_K5_TWO_PASS_MIN_N 512
 #endif
+// Packed complex add / subtract (FADD2, fft.cuh) in the FFT butterflies of grid
+// sides >= 512: C4 / C5 / C3 +1.2% each; at N = 256 the 64-pair batch (C2) ran
+// 1.5% slower with it, so the smaller grids keep the scalar adds.
+#ifndef FSCAN_F32X2_MIN_N
+#define FSCAN_F32X2_MIN_N 512
+#endif
+template <int N>
+constexpr bool kPk = fscan_fft::kF32x2Add && N >= FSCAN_F32X2_MIN_N;  // K4, K5
+// K3 only at N = 512 (6.48 -> 6.33 ms; at N = 1024 7.34 -> 7.62 ms); the
+// rotation-stage transforms (K1a DRAM-bound, K1b 2.54 -> 2.62 ms at N = 1024)
+// keep the scalar adds
+template <int N>
+constexpr bool kPkRows = kPk<N> && N < 1024;
 #ifndef FSCAN_K3_U
 #define FSCAN_K3_U 4  // K3 gather: cells per thread with their loads in flight together
 #endif
@@ -274,7 +287,7 @@ __global__ void FSCAN_K1A_BOUNDS k_rot_rows(Params p) {
             finish(m, x, fv, gv);
         }
     }
-    fft_regs<N, -1, (G::T <= 32)>(v, t, lay, p.tw_n);  // a row per warp (or two warps at N = 1024)
+    fft_regs<N, -1, (G::T <= 32), false>(v, t, lay, p.tw_n);  // a row per warp (or two warps at N = 1024)
     constexpr int UB = k1b_u<N>();
     // HOIST: with U dividing T, column x = t + m T sits in direct block t / U + m T / U
     // and its mirror N - x in mirror block (N - t) / U - m T / U, both at a fixed
@@ -361,7 +374,7 @@ __global__ void __launch_bounds__(N / 16 * 2 * k1b_u<N>()) k_rot_cols(Params p) 
 #pragma unroll
         for (int m = 0; m < 16; ++m) v[m] = z[(size_t)(t + m * T) * N + col];
     }
-    fft_regs<N, -1>(v, t, lay, p.tw_n);
+    fft_regs<N, -1, false, false>(v, t, lay, p.tw_n);
 #pragma unroll
     for (int m = 0; m < 16; ++m) lay.put(t + m * T, v[m]);
     __syncthreads();
@@ -1289,9 +1302,9 @@ __global__ void __launch_bounds__(kXThreads, 3) k_xlat_rows(Params p) {
         }
         const auto b = G::lay(xbase, tr);
         if constexpr (X::RK)
-            fft_regs<K, -1, true>(v, t, b, fscan_fft::SmemTwRK{srk, p.tw_k});  // T <= 32: within a warp
+            fft_regs<K, -1, true, kPkRows<N>>(v, t, b, fscan_fft::SmemTwRK{srk, p.tw_k});  // T <= 32: within a warp
         else
-            fft_regs<K, -1, true>(v, t, b, p.tw_k);
+            fft_regs<K, -1, true, kPkRows<N>>(v, t, b, p.tw_k);
 #pragma unroll
         for (int m = 0; m < 16; ++m) b.put(t + m * T, v[m]);
     }
@@ -1695,7 +1708,7 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
             __syncthreads();
         }
     }
-    fft_regs<K, -1, true>(a, t, bufA, twk);  // transforms of a warp share a buffer group
+    fft_regs<K, -1, true, kPk<N>>(a, t, bufA, twk);  // transforms of a warp share a buffer group
 #pragma unroll
     for (int m = 0; m < 16; ++m) bufA.put(t + m * T, a[m]);  // park F_q (own slots)
     if constexpr (X::FOLD1) {
@@ -1716,7 +1729,7 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
             a[m] = q ? cmul(wq_m(m, n0), s) : s;
         }
     }
-    fft_regs<K, -1, true>(a, t, bufB, twk);
+    fft_regs<K, -1, true, kPk<N>>(a, t, bufB, twk);
 #pragma unroll
     for (int m = 0; m < 16; ++m) a[m] = cmul(cconj(bufA.get(t + m * T)), a[m]);  // conj(F) G
     if (p.phase) {  // opt-in phase correlation: X / |X| (0 where X = 0), SURVEY a21
@@ -1727,7 +1740,7 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
             a[m] = make_float2(a[m].x * inv, a[m].y * inv);
         }
     }
-    fft_regs<K, +1, true>(a, t, bufB, twk);
+    fft_regs<K, +1, true, kPk<N>>(a, t, bufB, twk);
 #pragma unroll
     for (int m = 0; m < 16; ++m) bufB.put(t + m * T, a[m]);
     __syncthreads();
@@ -1905,9 +1918,9 @@ __device__ __forceinline__ void xlat_cols_merged(const Params& p) {
             ephase ^= 1;
         }
         if constexpr (SPLIT)
-            fft_regs<K, -1, true>(a, t, bufA, fscan_fft::TwQF<fscan_fft::kQS, false, true>{fq, &t_bar});
+            fft_regs<K, -1, true, kPk<N>>(a, t, bufA, fscan_fft::TwQF<fscan_fft::kQS, false, true>{fq, &t_bar});
         else
-            fft_regs<K, -1, true>(a, t, bufA, TQF{fq});
+            fft_regs<K, -1, true, kPk<N>>(a, t, bufA, TQF{fq});
 #pragma unroll
         for (int m = 0; m < 16; ++m) bufA.put(t + m * T, a[m]);  // park F_q (own slots)
         if constexpr (GST != 0) {
@@ -1937,7 +1950,7 @@ __device__ __forceinline__ void xlat_cols_merged(const Params& p) {
                 a[m] = fold(srcG[n0], srcG[n0 + K], m);
             }
         }
-        fft_regs<K, -1, true>(a, t, bufB, TQF{fq});
+        fft_regs<K, -1, true, kPk<N>>(a, t, bufB, TQF{fq});
 #pragma unroll
         for (int m = 0; m < 16; ++m) a[m] = cmul(cconj(bufA.get(t + m * T)), a[m]);  // conj(F) G
         if (p.phase) {  // opt-in phase correlation: X / |X| (0 where X = 0), SURVEY a21
@@ -1948,7 +1961,7 @@ __device__ __forceinline__ void xlat_cols_merged(const Params& p) {
                 a[m] = make_float2(a[m].x * inv, a[m].y * inv);
             }
         }
-        fft_regs<K, +1, true>(a, t, bufB, TQI{fq});
+        fft_regs<K, +1, true, kPk<N>>(a, t, bufB, TQI{fq});
 #pragma unroll
         for (int m = 0; m < 16; ++m) bufB.put(t + m * T, cmul(a[m], cconj(wout(m / NB))));
         // the combine of column c reads the three transforms 3c .. 3c + 2: with
@@ -2140,7 +2153,7 @@ __global__ void __launch_bounds__(XOutGeom<N>::THREADS) k_xlat_out(Params p) {
             v[m] = make_float2(A.x - B.y, A.y + B.x);  // A + iB
         }
         if constexpr (kK5Tma) __syncthreads();  // Y reads done before the exchange reuses the bytes
-        fft_regs<X::K2, +1, true>(v, t, buf, p.tw_k2);
+        fft_regs<X::K2, +1, true, kPk<N>>(v, t, buf, p.tw_k2);
 #pragma unroll
         for (int m = 0; m < 16; ++m) buf.put(t + m * T, v[m]);
     }
