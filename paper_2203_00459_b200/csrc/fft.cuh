@@ -62,8 +62,11 @@ constexpr bool kF32x2Mul = true;
 constexpr bool kF32x2Mul = false;
 #endif
 
+constexpr int kPkDefault = (kF32x2Add ? 1 : 0) | (kF32x2Mul ? 6 : 0);
+
+template <bool PK = kF32x2Mul>
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
-    if constexpr (kF32x2Mul) {
+    if constexpr (PK) {
         // (a.x b.x + rn(-a.y b.y), a.x b.y + rn(a.y b.x)): the scalar form's roundings
         float2 r;
         asm("{ .reg .b64 ax, ay, bb, bs, t, rr;\n\t"
@@ -117,26 +120,26 @@ __device__ __forceinline__ float2 mul_mi(float2 a) {
     return SIGN < 0 ? make_float2(a.y, -a.x) : make_float2(-a.y, a.x);
 }
 
-template <int SIGN, bool PK = kF32x2Add>
+template <int SIGN, int PK = kPkDefault>
 __device__ __forceinline__ void dft2(float2& a, float2& b) {
     const float2 t = a;
-    a = cadd<PK>(t, b);
-    b = csub<PK>(t, b);
+    a = cadd<(PK & 1) != 0>(t, b);
+    b = csub<(PK & 1) != 0>(t, b);
 }
 
 // 4-point DFT in place, natural order out.
-template <int SIGN, bool PK = kF32x2Add>
+template <int SIGN, int PK = kPkDefault>
 __device__ __forceinline__ void dft4(float2& x0, float2& x1, float2& x2, float2& x3) {
-    const float2 a = cadd<PK>(x0, x2), b = csub<PK>(x0, x2);
-    const float2 c = cadd<PK>(x1, x3), d = mul_mi<SIGN>(csub<PK>(x1, x3));
-    x0 = cadd<PK>(a, c);
-    x2 = csub<PK>(a, c);
-    x1 = cadd<PK>(b, d);
-    x3 = csub<PK>(b, d);
+    const float2 a = cadd<(PK & 1) != 0>(x0, x2), b = csub<(PK & 1) != 0>(x0, x2);
+    const float2 c = cadd<(PK & 1) != 0>(x1, x3), d = mul_mi<SIGN>(csub<(PK & 1) != 0>(x1, x3));
+    x0 = cadd<(PK & 1) != 0>(a, c);
+    x2 = csub<(PK & 1) != 0>(a, c);
+    x1 = cadd<(PK & 1) != 0>(b, d);
+    x3 = csub<(PK & 1) != 0>(b, d);
 }
 
 // 8-point DFT as radix-2 x radix-4 (DIT over n = 2*n1 + n2).
-template <int SIGN, bool PK = kF32x2Add>
+template <int SIGN, int PK = kPkDefault>
 __device__ __forceinline__ void dft8(float2* x) {
     constexpr float r = 0.70710678118654752f;
     float2 e0 = x[0], e1 = x[2], e2 = x[4], e3 = x[6];
@@ -146,18 +149,18 @@ __device__ __forceinline__ void dft8(float2* x) {
     o1 = SIGN < 0 ? make_float2(r * (o1.x + o1.y), r * (o1.y - o1.x)) : make_float2(r * (o1.x - o1.y), r * (o1.y + o1.x));
     o2 = mul_mi<SIGN>(o2);
     o3 = SIGN < 0 ? make_float2(r * (o3.y - o3.x), -r * (o3.x + o3.y)) : make_float2(-r * (o3.x + o3.y), r * (o3.x - o3.y));
-    x[0] = cadd<PK>(e0, o0);
-    x[4] = csub<PK>(e0, o0);
-    x[1] = cadd<PK>(e1, o1);
-    x[5] = csub<PK>(e1, o1);
-    x[2] = cadd<PK>(e2, o2);
-    x[6] = csub<PK>(e2, o2);
-    x[3] = cadd<PK>(e3, o3);
-    x[7] = csub<PK>(e3, o3);
+    x[0] = cadd<(PK & 1) != 0>(e0, o0);
+    x[4] = csub<(PK & 1) != 0>(e0, o0);
+    x[1] = cadd<(PK & 1) != 0>(e1, o1);
+    x[5] = csub<(PK & 1) != 0>(e1, o1);
+    x[2] = cadd<(PK & 1) != 0>(e2, o2);
+    x[6] = csub<(PK & 1) != 0>(e2, o2);
+    x[3] = cadd<(PK & 1) != 0>(e3, o3);
+    x[7] = csub<(PK & 1) != 0>(e3, o3);
 }
 
 // 16-point DFT as 4x4: X[k1 + 4*k2] = sum_n2 W4^(n2 k2) W16^(n2 k1) sum_n1 x[4 n1 + n2] W4^(n1 k1)
-template <int SIGN, bool PK = kF32x2Add>
+template <int SIGN, int PK = kPkDefault>
 __device__ __forceinline__ void dft16(float2* x) {
     constexpr float c1 = 0.92387953251128674f;  // cos(pi/8)
     constexpr float s1 = 0.38268343236508977f;  // sin(pi/8)
@@ -168,15 +171,15 @@ __device__ __forceinline__ void dft16(float2* x) {
     const float sg = (float)SIGN;
     const float2 w1 = make_float2(c1, sg * s1), w2 = make_float2(r, sg * r), w3 = make_float2(s1, sg * c1);
     const float2 w6 = make_float2(-r, sg * r), w9 = make_float2(-c1, -sg * s1);
-    x[4 * 1 + 1] = cmul(x[4 * 1 + 1], w1);
-    x[4 * 2 + 1] = cmul(x[4 * 2 + 1], w2);
-    x[4 * 3 + 1] = cmul(x[4 * 3 + 1], w3);
-    x[4 * 1 + 2] = cmul(x[4 * 1 + 2], w2);
+    x[4 * 1 + 1] = cmul<(PK & 4) != 0>(x[4 * 1 + 1], w1);
+    x[4 * 2 + 1] = cmul<(PK & 4) != 0>(x[4 * 2 + 1], w2);
+    x[4 * 3 + 1] = cmul<(PK & 4) != 0>(x[4 * 3 + 1], w3);
+    x[4 * 1 + 2] = cmul<(PK & 4) != 0>(x[4 * 1 + 2], w2);
     x[4 * 2 + 2] = mul_mi<SIGN>(x[4 * 2 + 2]);
-    x[4 * 3 + 2] = cmul(x[4 * 3 + 2], w6);
-    x[4 * 1 + 3] = cmul(x[4 * 1 + 3], w3);
-    x[4 * 2 + 3] = cmul(x[4 * 2 + 3], w6);
-    x[4 * 3 + 3] = cmul(x[4 * 3 + 3], w9);
+    x[4 * 3 + 2] = cmul<(PK & 4) != 0>(x[4 * 3 + 2], w6);
+    x[4 * 1 + 3] = cmul<(PK & 4) != 0>(x[4 * 1 + 3], w3);
+    x[4 * 2 + 3] = cmul<(PK & 4) != 0>(x[4 * 2 + 3], w6);
+    x[4 * 3 + 3] = cmul<(PK & 4) != 0>(x[4 * 3 + 3], w9);
     float2 y[16];
 #pragma unroll
     for (int k1 = 0; k1 < 4; ++k1) {
@@ -191,7 +194,7 @@ __device__ __forceinline__ void dft16(float2* x) {
     for (int i = 0; i < 16; ++i) x[i] = y[i];
 }
 
-template <int R, int SIGN, bool PK = kF32x2Add>
+template <int R, int SIGN, int PK = kPkDefault>
 __device__ __forceinline__ void dft_r(float2* x) {
     if constexpr (R == 2) {
         dft2<SIGN, PK>(x[0], x[1]);
@@ -501,7 +504,7 @@ constexpr bool kPowJ = false;  // A/B: last-stage twiddles read from the table p
 constexpr bool kPowJ = true;
 #endif
 
-template <int N, int R, int Ns, bool LAST, int SIGN, bool WARP, bool PK, typename L, typename TW>
+template <int N, int R, int Ns, bool LAST, int SIGN, bool WARP, int PK, typename L, typename TW>
 __device__ __forceinline__ void stage(float2 (&v)[16], int t, const L& lay, const TW& tw) {
     constexpr int T = N / 16;
     constexpr int NB = 16 / R;
@@ -528,24 +531,24 @@ __device__ __forceinline__ void stage(float2 (&v)[16], int t, const L& lay, cons
             constexpr int q = N / (Ns * R);  // W_{Ns R}^x = tw[x * q]
             if constexpr (POWJ) {
 #pragma unroll
-                for (int r = 1; r < R; ++r) u[r] = cmul(u[r], j == 0 ? tb[r] : cmul(tb[r], w16c<SIGN>(r * j)));
+                for (int r = 1; r < R; ++r) u[r] = cmul<(PK & 2) != 0>(u[r], j == 0 ? tb[r] : cmul<(PK & 2) != 0>(tb[r], w16c<SIGN>(r * j)));
             } else if constexpr (TwQInfo<TW>::kind == 1) {
                 static_assert(Ns == 16 && LAST, "merged twiddles: two-stage transforms only");
                 constexpr int S = TwQInfo<TW>::S;
                 if (j == 0) tw.wait();
 #pragma unroll
-                for (int r = 1; r < R; ++r) u[r] = cmul(u[r], tw.at(r * S + 3 * k));
+                for (int r = 1; r < R; ++r) u[r] = cmul<(PK & 2) != 0>(u[r], tw.at(r * S + 3 * k));
             } else if constexpr (TwQInfo<TW>::kind == 2) {
                 static_assert(Ns == 16 && LAST, "merged twiddles: two-stage transforms only");
                 constexpr int S = TwQInfo<TW>::S;
 #pragma unroll
-                for (int r = 0; r < R; ++r) u[r] = cmul(u[r], cconj(tw.at(k * S + 3 * r)));
+                for (int r = 0; r < R; ++r) u[r] = cmul<(PK & 2) != 0>(u[r], cconj(tw.at(k * S + 3 * r)));
             } else if constexpr (Ns == 16 && kTwRK<TW>) {
                 // W_{16 R}^{r k} = W_256^{(16/R) r k}
 #pragma unroll
                 for (int r = 1; r < R; ++r) {
                     const float2 w = tw.rk[((16 / R) * r - 1) * 16 + k];
-                    u[r] = cmul(u[r], SIGN < 0 ? w : make_float2(w.x, -w.y));
+                    u[r] = cmul<(PK & 2) != 0>(u[r], SIGN < 0 ? w : make_float2(w.x, -w.y));
                 }
             } else if constexpr (R == 16 && kTwPow<TW>) {
                 // the 15 powers w^r of w = W_{16 Ns}^k from four table reads (w, w^2,
@@ -558,17 +561,17 @@ __device__ __forceinline__ void stage(float2 (&v)[16], int t, const L& lay, cons
                 w[2] = twiddle<SIGN>(tw, 2 * k * q);
                 w[4] = twiddle<SIGN>(tw, 4 * k * q);
                 w[8] = twiddle<SIGN>(tw, 8 * k * q);
-                w[3] = cmul(w[1], w[2]);
-                w[5] = cmul(w[4], w[1]);
-                w[6] = cmul(w[4], w[2]);
-                w[7] = cmul(w[4], w[3]);
+                w[3] = cmul<(PK & 2) != 0>(w[1], w[2]);
+                w[5] = cmul<(PK & 2) != 0>(w[4], w[1]);
+                w[6] = cmul<(PK & 2) != 0>(w[4], w[2]);
+                w[7] = cmul<(PK & 2) != 0>(w[4], w[3]);
 #pragma unroll
-                for (int r = 9; r < 16; ++r) w[r] = cmul(w[8], w[r - 8]);
+                for (int r = 9; r < 16; ++r) w[r] = cmul<(PK & 2) != 0>(w[8], w[r - 8]);
 #pragma unroll
-                for (int r = 1; r < R; ++r) u[r] = cmul(u[r], w[r]);
+                for (int r = 1; r < R; ++r) u[r] = cmul<(PK & 2) != 0>(u[r], w[r]);
             } else {
 #pragma unroll
-                for (int r = 1; r < R; ++r) u[r] = cmul(u[r], twiddle<SIGN>(tw, r * k * q));
+                for (int r = 1; r < R; ++r) u[r] = cmul<(PK & 2) != 0>(u[r], twiddle<SIGN>(tw, r * k * q));
             }
         }
         dft_r<R, SIGN, PK>(u);
@@ -593,8 +596,10 @@ __device__ __forceinline__ void stage(float2 (&v)[16], int t, const L& lay, cons
 // caller guarantees the transform's threads and exchange buffer live in one
 // warp (row layouts with T <= 32), so the exchanges need only __syncwarp;
 // otherwise every thread of the CTA must call fft_regs the same number of times.
-// PK: packed complex add / subtract in the butterflies (see cadd)
-template <int N, int SIGN, bool WARP = false, bool PK = kF32x2Add, typename L, typename TW>
+// PK: packed fp32 (see cadd, cmul): bit 0 the butterflies' complex adds /
+// subtracts, bit 1 the stage twiddle products (operands in registers), bit 2
+// the radix-8 / 16 butterflies' products with compile-time constants
+template <int N, int SIGN, bool WARP = false, int PK = kPkDefault, typename L, typename TW>
 __device__ __forceinline__ void fft_regs(float2 (&v)[16], int t, const L& lay, const TW& tw) {
     static_assert(N >= 16 && (N & (N - 1)) == 0, "power-of-two length >= 16");
     static_assert(!WARP || N / 16 <= 32, "a warp-synchronous transform fits in one warp");

@@ -39,6 +39,15 @@
 #ifndef FSCAN_F32X2_MIN_N
 #define FSCAN_F32X2_MIN_N 512
 #endif
+#ifndef FSCAN_PK_K3
+#define FSCAN_PK_K3 1
+#endif
+#ifndef FSCAN_PK_K4
+#define FSCAN_PK_K4 1
+#endif
+#ifndef FSCAN_PK_K5
+#define FSCAN_PK_K5 1
+#endif
 template <int N>
 constexpr bool kPk = fscan_fft::kF32x2Add && N >= FSCAN_F32X2_MIN_N;  // K4, K5
 // K3 only at N = 512 (6.48 -> 6.33 ms; at N = 1024 7.34 -> 7.62 ms); the
@@ -1302,9 +1311,9 @@ __global__ void __launch_bounds__(kXThreads, 3) k_xlat_rows(Params p) {
         }
         const auto b = G::lay(xbase, tr);
         if constexpr (X::RK)
-            fft_regs<K, -1, true, kPkRows<N>>(v, t, b, fscan_fft::SmemTwRK{srk, p.tw_k});  // T <= 32: within a warp
+            fft_regs<K, -1, true, (kPkRows<N> ? FSCAN_PK_K3 : 0)>(v, t, b, fscan_fft::SmemTwRK{srk, p.tw_k});  // T <= 32: within a warp
         else
-            fft_regs<K, -1, true, kPkRows<N>>(v, t, b, p.tw_k);
+            fft_regs<K, -1, true, (kPkRows<N> ? FSCAN_PK_K3 : 0)>(v, t, b, p.tw_k);
 #pragma unroll
         for (int m = 0; m < 16; ++m) b.put(t + m * T, v[m]);
     }
@@ -1708,7 +1717,7 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
             __syncthreads();
         }
     }
-    fft_regs<K, -1, true, kPk<N>>(a, t, bufA, twk);  // transforms of a warp share a buffer group
+    fft_regs<K, -1, true, (kPk<N> ? FSCAN_PK_K4 : 0)>(a, t, bufA, twk);  // transforms of a warp share a buffer group
 #pragma unroll
     for (int m = 0; m < 16; ++m) bufA.put(t + m * T, a[m]);  // park F_q (own slots)
     if constexpr (X::FOLD1) {
@@ -1729,7 +1738,7 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
             a[m] = q ? cmul(wq_m(m, n0), s) : s;
         }
     }
-    fft_regs<K, -1, true, kPk<N>>(a, t, bufB, twk);
+    fft_regs<K, -1, true, (kPk<N> ? FSCAN_PK_K4 : 0)>(a, t, bufB, twk);
 #pragma unroll
     for (int m = 0; m < 16; ++m) a[m] = cmul(cconj(bufA.get(t + m * T)), a[m]);  // conj(F) G
     if (p.phase) {  // opt-in phase correlation: X / |X| (0 where X = 0), SURVEY a21
@@ -1740,7 +1749,7 @@ __device__ __forceinline__ void xlat_cols_body(const Params& p) {
             a[m] = make_float2(a[m].x * inv, a[m].y * inv);
         }
     }
-    fft_regs<K, +1, true, kPk<N>>(a, t, bufB, twk);
+    fft_regs<K, +1, true, (kPk<N> ? FSCAN_PK_K4 : 0)>(a, t, bufB, twk);
 #pragma unroll
     for (int m = 0; m < 16; ++m) bufB.put(t + m * T, a[m]);
     __syncthreads();
@@ -1918,9 +1927,9 @@ __device__ __forceinline__ void xlat_cols_merged(const Params& p) {
             ephase ^= 1;
         }
         if constexpr (SPLIT)
-            fft_regs<K, -1, true, kPk<N>>(a, t, bufA, fscan_fft::TwQF<fscan_fft::kQS, false, true>{fq, &t_bar});
+            fft_regs<K, -1, true, (kPk<N> ? FSCAN_PK_K4 : 0)>(a, t, bufA, fscan_fft::TwQF<fscan_fft::kQS, false, true>{fq, &t_bar});
         else
-            fft_regs<K, -1, true, kPk<N>>(a, t, bufA, TQF{fq});
+            fft_regs<K, -1, true, (kPk<N> ? FSCAN_PK_K4 : 0)>(a, t, bufA, TQF{fq});
 #pragma unroll
         for (int m = 0; m < 16; ++m) bufA.put(t + m * T, a[m]);  // park F_q (own slots)
         if constexpr (GST != 0) {
@@ -1950,7 +1959,7 @@ __device__ __forceinline__ void xlat_cols_merged(const Params& p) {
                 a[m] = fold(srcG[n0], srcG[n0 + K], m);
             }
         }
-        fft_regs<K, -1, true, kPk<N>>(a, t, bufB, TQF{fq});
+        fft_regs<K, -1, true, (kPk<N> ? FSCAN_PK_K4 : 0)>(a, t, bufB, TQF{fq});
 #pragma unroll
         for (int m = 0; m < 16; ++m) a[m] = cmul(cconj(bufA.get(t + m * T)), a[m]);  // conj(F) G
         if (p.phase) {  // opt-in phase correlation: X / |X| (0 where X = 0), SURVEY a21
@@ -1961,7 +1970,7 @@ __device__ __forceinline__ void xlat_cols_merged(const Params& p) {
                 a[m] = make_float2(a[m].x * inv, a[m].y * inv);
             }
         }
-        fft_regs<K, +1, true, kPk<N>>(a, t, bufB, TQI{fq});
+        fft_regs<K, +1, true, (kPk<N> ? FSCAN_PK_K4 : 0)>(a, t, bufB, TQI{fq});
 #pragma unroll
         for (int m = 0; m < 16; ++m) bufB.put(t + m * T, cmul(a[m], cconj(wout(m / NB))));
         // the combine of column c reads the three transforms 3c .. 3c + 2: with
@@ -2153,7 +2162,7 @@ __global__ void __launch_bounds__(XOutGeom<N>::THREADS) k_xlat_out(Params p) {
             v[m] = make_float2(A.x - B.y, A.y + B.x);  // A + iB
         }
         if constexpr (kK5Tma) __syncthreads();  // Y reads done before the exchange reuses the bytes
-        fft_regs<X::K2, +1, true, kPk<N>>(v, t, buf, p.tw_k2);
+        fft_regs<X::K2, +1, true, (kPk<N> ? FSCAN_PK_K5 : 0)>(v, t, buf, p.tw_k2);
 #pragma unroll
         for (int m = 0; m < 16; ++m) buf.put(t + m * T, v[m]);
     }
