@@ -498,6 +498,11 @@ __device__ __forceinline__ float2 w16c(int x) {
     return SIGN < 0 ? make_float2(c, -sn) : make_float2(c, sn);
 }
 
+#ifdef FSCAN_TWQ_POW
+constexpr bool kTwQPow = true;  // A/B: merged forward twiddles as powers of four table reads
+#else
+constexpr bool kTwQPow = false;
+#endif
 #ifdef FSCAN_NO_POWJ
 constexpr bool kPowJ = false;  // A/B: last-stage twiddles read from the table per butterfly
 #else
@@ -536,8 +541,27 @@ __device__ __forceinline__ void stage(float2 (&v)[16], int t, const L& lay, cons
                 static_assert(Ns == 16 && LAST, "merged twiddles: two-stage transforms only");
                 constexpr int S = TwQInfo<TW>::S;
                 if (j == 0) tw.wait();
+                if constexpr (kTwQPow && R == 16) {
+                    // A/B: F[r][3k + q] = w^r, w = F[1][3k + q]: rows 1, 2, 4, 8 read,
+                    // the other 11 powers by products (11 fewer 64-bit shared reads
+                    // per transform on the L1 data pipe K4 is bound by)
+                    float2 w[16];
+                    w[1] = tw.at(1 * S + 3 * k);
+                    w[2] = tw.at(2 * S + 3 * k);
+                    w[4] = tw.at(4 * S + 3 * k);
+                    w[8] = tw.at(8 * S + 3 * k);
+                    w[3] = cmul(w[1], w[2]);
+                    w[5] = cmul(w[4], w[1]);
+                    w[6] = cmul(w[4], w[2]);
+                    w[7] = cmul(w[4], w[3]);
 #pragma unroll
-                for (int r = 1; r < R; ++r) u[r] = cmul<(PK & 2) != 0>(u[r], tw.at(r * S + 3 * k));
+                    for (int r = 9; r < 16; ++r) w[r] = cmul(w[8], w[r - 8]);
+#pragma unroll
+                    for (int r = 1; r < R; ++r) u[r] = cmul<(PK & 2) != 0>(u[r], w[r]);
+                } else {
+#pragma unroll
+                    for (int r = 1; r < R; ++r) u[r] = cmul<(PK & 2) != 0>(u[r], tw.at(r * S + 3 * k));
+                }
             } else if constexpr (TwQInfo<TW>::kind == 2) {
                 static_assert(Ns == 16 && LAST, "merged twiddles: two-stage transforms only");
                 constexpr int S = TwQInfo<TW>::S;
