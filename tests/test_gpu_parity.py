@@ -926,6 +926,41 @@ def test_set_chunk_drops_cached_graphs(fb, dev):
     assert m.graph_stats()[0] == caps + 3  # every new chunking was captured afresh
 
 
+def test_brute_force_grows_lanes_and_keeps_the_matcher_intact(fb, orc, dev):
+    """fscan_brute_force_batch widens the lanes of a context made for a few pairs
+    (its (pair, candidate) items fill them): the graph captured before it must be
+    dropped, matches after it give the same bytes (graph replay and host API), and
+    the search itself equals a chunk-5 search (chunks straddling pairs and lanes)."""
+    cfg, delta, _ = fb.baseline_config(2)
+    f, g, mf, mg, _ = fb.synth_pairs_host(fb.synth_spec(2), 0, 2)
+    F, G, MF, MG = to_dev(dev, f, g, mf, mg)
+    m = fb.Matcher(cfg, max_batch=2)
+    direct = m.match_device(F, G, MF, MG, delta=delta).clone()
+    torch.cuda.synchronize()
+    m.set_graphs(True)
+    out = torch.zeros_like(direct)
+    m.match_device(F, G, MF, MG, delta=delta, out=out)
+    torch.cuda.synchronize()
+    assert torch.equal(out, direct)
+    caps = m.graph_stats()[0]
+    thetas = (np.arange(60) - 30) * cfg.delta_theta  # 120 items: far more than the 2-pair lanes held
+    wide = fb.decode_bf_results(m.brute_force(F, G, thetas, delta=delta))
+    torch.cuda.synchronize()
+    out.zero_()
+    m.match_device(F, G, MF, MG, delta=delta, out=out)  # re-captured on the new workspace
+    torch.cuda.synchronize()
+    assert torch.equal(out, direct)
+    assert m.graph_stats()[0] == caps + 1
+    host = m.match_host(f, g, mf, mg, delta=delta)
+    assert host.tobytes() == fb.decode_results(direct).tobytes()
+    m2 = fb.Matcher(cfg, max_batch=2, chunk=5)
+    narrow = fb.decode_bf_results(m2.brute_force(F, G, thetas, delta=delta))
+    assert wide.tobytes() == narrow.tobytes()
+    o = orc.brute_force(f[0].astype(np.float64), g[0].astype(np.float64), thetas, delta)
+    bf_compare(wide[0], o, 256, [])
+    assert wide[0]["status"] == fb.OK and wide[1]["status"] == fb.OK
+
+
 def test_host_call_after_graph_replay_on_side_stream(fb, dev):
     """fscan_match_batch_host must wait for a graph replay still
     running on a user stream before reusing the lane workspace."""
