@@ -174,7 +174,10 @@ typedef struct fscan_bf_result {
 
 /* batch pairs (device, N x N each), n_thetas candidates from a HOST array,
  * results to device d_out[batch]. Asynchronous on `stream`. Cost: one
- * translation stage per (pair, candidate). */
+ * translation stage per (pair, candidate). The (pair, candidate) items run
+ * through the context's chunk pipelines: a context created for fewer pairs
+ * than fill them has its workspace grown once (up to ~2 GiB per pipeline, or
+ * batch * n_thetas / pipelines items), which drops the cached CUDA graphs. */
 fscan_status fscan_brute_force_batch(fscan_ctx* ctx, const float* d_f, const float* d_g, int batch,
                                      const double* thetas, int n_thetas, double delta,
                                      fscan_bf_result* d_out, void* stream);
