@@ -2074,8 +2074,13 @@ __device__ __forceinline__ void better(float& bv, int& bi, float v, int i) {
     }
 }
 
+#ifdef FSCAN_K5_MINB
+#define FSCAN_K5_BOUNDS __launch_bounds__(XOutGeom<N>::THREADS, FSCAN_K5_MINB)
+#else
+#define FSCAN_K5_BOUNDS __launch_bounds__(XOutGeom<N>::THREADS)
+#endif
 template <int N, bool EMB, int MODE = kOutFull>
-__global__ void __launch_bounds__(XOutGeom<N>::THREADS) k_xlat_out(Params p) {
+__global__ void FSCAN_K5_BOUNDS k_xlat_out(Params p) {
     pdl_enter();
     constexpr int K = N / 2, M = 3 * K, H = M / 2;
     using X = XOutGeom<N>;
